@@ -1,0 +1,192 @@
+/*
+ * sfmcov_b200 — C ABI of the B200-native camera-covariance hot path.
+ *
+ * Drop-in boundary for the reference `sfmcov` library (arXiv 1808.02414,
+ * /root/reference/proj).  The reference has no FFI or plugin registry; its
+ * "operator API" is the free-function set in namespace sfmcov.  Each entry
+ * point below replaces one of those functions (cited per declaration) with
+ * plain pointers and sizes, no C++ or torch types.  include/sfmcov_b200.hpp
+ * wraps this ABI back into the reference's C++ signatures, and
+ * paper_1808_02414_b200/sfmcov.py into Python.
+ *
+ * Conventions
+ *  - All arithmetic is FP64; indices int32 (observation ids < 2^31).
+ *  - Cameras have P in {8, 9} parameters: P = 8 is the reference camera
+ *    (r, C, c, k), include/sfmcov/types.hpp:28-39; P = 9 adds k2
+ *    (u = f(1 + k1 rho + k2 rho^2) u_n), the BASELINE.json camera.
+ *  - Matrix blocks are row-major within a block unless stated otherwise.
+ *  - Return value = error kind (0 = ok), mirroring sfmcov::ErrorKind
+ *    (include/sfmcov/error.hpp:9-16); the stage and the full
+ *    "stage: message" text land in sfmcov_error, exactly as the reference's
+ *    Error::what() would read.
+ *  - Calls are synchronous and thread-safe per handle; a handle owns one
+ *    CUDA device, one stream and a grow-only device workspace.
+ *  - There is no CPU fallback: on a machine without a usable CUDA device
+ *    sfmcov_cuda_create fails with SFMCOV_ERR_DEVICE.
+ */
+#ifndef SFMCOV_B200_H
+#define SFMCOV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error kinds: include/sfmcov/error.hpp:9-16 (+ device, not in the reference) */
+enum {
+    SFMCOV_OK = 0,
+    SFMCOV_ERR_IO = 1,
+    SFMCOV_ERR_PARSE = 2,
+    SFMCOV_ERR_INVARIANT = 3,
+    SFMCOV_ERR_DEGENERATE = 4,
+    SFMCOV_ERR_DIMENSION = 5,
+    SFMCOV_ERR_SIZE_GUARD = 6,
+    SFMCOV_ERR_DEVICE = 7
+};
+
+/* Scene, structure-of-arrays.  Replaces sfmcov::Reconstruction
+ * (include/sfmcov/types.hpp:52-66).  Pointers are host or device memory
+ * depending on the entry point; the caller owns them. */
+typedef struct sfmcov_scene {
+    int32_t n_cams;
+    int32_t n_pts;
+    int32_t n_obs;
+    int32_t cam_params;        /* P: 8 or 9 */
+    const double* cams;        /* n_cams x P: r(3) C(3) c|f k|k1 [k2] */
+    const double* pts;         /* n_pts x 3 */
+    const int32_t* obs_cam;    /* n_obs */
+    const int32_t* obs_pt;     /* n_obs */
+    const double* obs_u;       /* n_obs x 2, validated only; may be NULL */
+    const double* obs_sigma;   /* n_obs x 4 (row-major 2x2); NULL = identity */
+} sfmcov_scene;
+
+/* sfmcov::CovarianceOptions (include/sfmcov/covariance.hpp:71-75). */
+typedef struct sfmcov_options {
+    int32_t threads;                  /* accepted and ignored (results never depend on it) */
+    int32_t point_covariances;        /* not yet supported: must be 0 */
+    int32_t camera_cross_covariances; /* not yet supported: must be 0 */
+    int32_t reserved;
+} sfmcov_options;
+
+/* sfmcov::CovarianceDiagnostics (include/sfmcov/covariance.hpp:49-60).
+ * On the Cholesky route min/max_pivot are taken over the Cholesky pivots
+ * diag(L)^2 of the gauge-augmented camera matrix and |eig(E)| of the 7x7
+ * border block; inertia is (P*n, 7) on success. */
+typedef struct sfmcov_diagnostics {
+    double scale_min;
+    double scale_max;
+    double min_pivot;
+    double max_pivot;
+    int32_t inertia_positive;
+    int32_t inertia_negative;
+    int32_t negative_eigenvalue_warnings;
+    int32_t n_flagged;             /* total flagged columns */
+    int64_t peak_dense_bytes;
+    int64_t largest_dense_dim;     /* P*n + 7, as the reference reports */
+    int64_t* flagged;              /* caller buffer for flagged column ids (may be NULL) */
+    int64_t flagged_capacity;
+} sfmcov_diagnostics;
+
+typedef struct sfmcov_error {
+    int32_t kind;
+    char stage[32];
+    char message[480];             /* "stage: message" */
+} sfmcov_error;
+
+typedef struct sfmcov_handle sfmcov_handle;
+
+/* ---- lifecycle ----------------------------------------------------------- */
+sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err);
+void sfmcov_cuda_destroy(sfmcov_handle* h);
+/* The handle's CUDA stream (cudaStream_t) for callers that time or order work. */
+void* sfmcov_cuda_stream(sfmcov_handle* h);
+
+/* ---- full pipeline --------------------------------------------------------
+ * Replaces sfmcov::compute_covariance (include/sfmcov/covariance.hpp:110-111,
+ * src/covariance.cpp:323-350).  Host scene in, host per-camera blocks out:
+ * cam_cov is n_cams x P x P (row-major blocks). */
+int32_t sfmcov_cuda_compute_covariance(sfmcov_handle* h, const sfmcov_scene* scene,
+                                       const sfmcov_options* opts, double* cam_cov,
+                                       sfmcov_diagnostics* diag, sfmcov_error* err);
+
+/* Same, with every scene pointer and d_cam_cov in device memory of the
+ * handle's device (inputs resident in HBM; used by the device-timed bench). */
+int32_t sfmcov_cuda_compute_covariance_device(sfmcov_handle* h, const sfmcov_scene* d_scene,
+                                              const sfmcov_options* opts, double* d_cam_cov,
+                                              sfmcov_diagnostics* diag, sfmcov_error* err);
+
+/* ---- stage entry points (host buffers; parity tests) ------------------- */
+
+/* build_observation_index (src/scene.cpp:80-90) as CSR: ascending observation
+ * ids per camera / per point.  off_* are int64 (n+1 / m+1). */
+int32_t sfmcov_cuda_observation_index(sfmcov_handle* h, const sfmcov_scene* scene,
+                                      int64_t* off_cam, int32_t* idx_cam,
+                                      int64_t* off_pt, int32_t* idx_pt, sfmcov_error* err);
+
+/* assemble_jacobian (include/sfmcov/projection.hpp:54, src/projection.cpp:80-105):
+ * cam_blocks n_obs x 2 x P, point_blocks n_obs x 2 x 3, observation order. */
+int32_t sfmcov_cuda_jacobian(sfmcov_handle* h, const sfmcov_scene* scene,
+                             double* cam_blocks, double* point_blocks, sfmcov_error* err);
+
+/* gauge_nullspace (include/sfmcov/nullspace.hpp:33, src/nullspace.cpp:64-68):
+ * H is (P*n + 3m) x 7, row-major. */
+int32_t sfmcov_cuda_nullspace(sfmcov_handle* h, const sfmcov_scene* scene, double* H,
+                              sfmcov_error* err);
+
+/* build_fisher_blocks + condition_columns (include/sfmcov/covariance.hpp:80-86,
+ * src/covariance.cpp:33-116), unconditioned blocks: D n x P x P, A m x 3 x 3,
+ * couplings n_obs x P x 3; s_a (P*n + 3m), s_b (7).  Any output may be NULL.
+ * Like the reference function it does not run the scene validation, so a
+ * non-SPD sigma fails in stage "fisher". */
+int32_t sfmcov_cuda_fisher(sfmcov_handle* h, const sfmcov_scene* scene, double* D, double* A,
+                           double* couplings, double* s_a, double* s_b,
+                           sfmcov_diagnostics* diag, sfmcov_error* err);
+
+/* schur_reduce on the conditioned system (include/sfmcov/covariance.hpp:94-95,
+ * src/covariance.cpp:137-194): dense symmetric Z_p, (P*n+7)^2, column-major. */
+int32_t sfmcov_cuda_schur(sfmcov_handle* h, const sfmcov_scene* scene, double* z_p,
+                          sfmcov_error* err);
+
+/* Dense gauge-free inversion kernel on an arbitrary SPD matrix (column-major
+ * n x n, host): Cholesky + triangular inverse + diagonal-block extraction of
+ * A^-1 with block size `block`.  blocks: (n / block) x block x block.  The
+ * same device code path invert_schur's replacement uses. */
+int32_t sfmcov_cuda_spd_inverse_blocks(sfmcov_handle* h, const double* a, int64_t n, int32_t block,
+                                       double* blocks, double* min_pivot, double* max_pivot,
+                                       sfmcov_error* err);
+
+/* Per-stage device times (ms) of the last pipeline call, in the order of
+ * sfmcov_cuda_stage_name(i); returns the number of stages written. */
+int32_t sfmcov_cuda_last_stage_times(sfmcov_handle* h, double* ms, int32_t capacity);
+const char* sfmcov_cuda_stage_name(int32_t i);
+/* Algorithmic counts of the last pipeline call (for roofline accounting):
+ * [0] obs-pairs, [1] nonzero camera-pair blocks (incl. diagonal), [2] N = P*n,
+ * [3] padded dense dim, [4] n_obs, [5] n_pts, [6] n_cams, [7] P,
+ * [8] dense-factorisation kernel launches. */
+int32_t sfmcov_cuda_last_counts(sfmcov_handle* h, int64_t* counts, int32_t capacity);
+/* Enable/disable per-stage event timing (off by default; adds syncs). */
+void sfmcov_cuda_set_profiling(sfmcov_handle* h, int32_t on);
+
+/* ---- synthetic scenes (host only; harness, not the hot path) ------------
+ * generate_cube_scene / generate_random_scene / transform_scene
+ * (include/sfmcov/synthetic.hpp:17-28, src/synthetic.cpp:52-194) and the
+ * BASELINE.json configs 1..5. */
+typedef struct sfmcov_synth_scene sfmcov_synth_scene;
+sfmcov_synth_scene* sfmcov_synth_cube(uint64_t seed, double noise_px, int32_t cam_params);
+sfmcov_synth_scene* sfmcov_synth_random(int64_t n_cams, int64_t n_pts, double visibility,
+                                        uint64_t seed, double noise_px, int32_t cam_params);
+sfmcov_synth_scene* sfmcov_synth_config(int32_t config_index, uint64_t seed);
+sfmcov_synth_scene* sfmcov_synth_transform(const sfmcov_synth_scene* in, const double* R3x3,
+                                           const double* t3, double scale);
+void sfmcov_synth_sizes(const sfmcov_synth_scene* s, int64_t* n, int64_t* m, int64_t* t, int32_t* P);
+void sfmcov_synth_export(const sfmcov_synth_scene* s, double* cams, double* pts, int32_t* obs_cam,
+                         int32_t* obs_pt, double* obs_u, double* obs_sigma);
+void sfmcov_synth_free(sfmcov_synth_scene* s);
+const char* sfmcov_synth_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFMCOV_B200_H */

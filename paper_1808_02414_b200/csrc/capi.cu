@@ -1,0 +1,670 @@
+// C ABI and pipeline orchestration of the B200 covariance hot path.
+//
+// Pipeline (reference: compute_covariance, src/covariance.cpp:323-350):
+//   validate + observation index          src/scene.cpp:19-90
+//   Jacobian                              src/projection.cpp:80-105
+//   gauge nullspace rotation blocks       src/nullspace.cpp:33-62
+//   Fisher blocks + conditioning scales   src/covariance.cpp:33-135
+//   point elimination (Schur) + border    src/covariance.cpp:137-194
+//   gauge-fixed inversion + extraction    src/covariance.cpp:196-279
+// Everything runs on the handle's device; the host only moves the scene in
+// and the per-camera blocks out, and turns device status words into the
+// reference's Error(kind, stage, message).
+#include "sfmcov_b200.h"
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace {
+
+using namespace sfm;
+
+struct ApiError {
+    int kind;
+    std::string stage;
+    std::string message;
+};
+
+enum Stage { ST_INDEX, ST_JACOBIAN, ST_REDUCE, ST_SCHUR_PREP, ST_PAIRS, ST_FILL, ST_PAIR_REDUCE, ST_CHOLESKY,
+             ST_TRTRI, ST_EXTRACT, ST_COUNT };
+const char* kStageNames[ST_COUNT] = {"validate_index", "jacobian", "camera_point_reduce", "schur_point_prep",
+                                     "pair_sort", "dense_fill", "schur_pair_reduce", "cholesky", "trtri",
+                                     "extract"};
+
+enum Mode { M_INDEX, M_JACOBIAN, M_NULLSPACE, M_FISHER, M_SCHUR, M_FULL };
+
+}  // namespace
+
+struct sfmcov_handle {
+    int device = 0;
+    cudaStream_t s = nullptr, s2 = nullptr;
+    cudaEvent_t e1 = nullptr, e2 = nullptr;
+    cudaEvent_t ev[ST_COUNT + 1];
+    bool profiling = false;
+    std::mutex mu;
+    Workspace ws;
+    // host-API staging of the scene
+    DBuf h_cams, h_pts, h_oc, h_op, h_u, h_sigma;
+    // index
+    DBuf cnt_cam, cnt_pt, off_cam, idx_cam, off_pt, idx_pt, pos_cam, key_scratch;
+    // stage buffers
+    DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Wb, V, Fpart, LF, E, eigE, Gamma, G, Z, Linv, Lp, piv, cov,
+        psd, prange, status, depth, H;
+    PairDev pairs;
+    Status* st_host = nullptr;
+    double stage_ms[ST_COUNT] = {0};
+    long long counts[9] = {0};
+};
+
+namespace {
+
+void fill_error(sfmcov_error* e, const ApiError& x) {
+    if (!e) return;
+    e->kind = x.kind;
+    std::snprintf(e->stage, sizeof e->stage, "%s", x.stage.c_str());
+    std::snprintf(e->message, sizeof e->message, "%s: %s", x.stage.c_str(), x.message.c_str());
+}
+
+void clear_error(sfmcov_error* e) {
+    if (!e) return;
+    e->kind = 0;
+    e->stage[0] = 0;
+    e->message[0] = 0;
+}
+
+std::string fmt_f(double v) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%f", v);
+    return buf;
+}
+
+struct Outputs {
+    // device
+    double* d_cam_cov = nullptr;
+    // host (stage APIs)
+    double* jc = nullptr;
+    double* jp = nullptr;
+    double* H = nullptr;
+    double* D = nullptr;
+    double* A = nullptr;
+    double* Cp = nullptr;
+    double* s_a = nullptr;
+    double* s_b = nullptr;
+    double* z_p = nullptr;
+    int64_t* off_cam = nullptr;
+    int32_t* idx_cam = nullptr;
+    int64_t* off_pt = nullptr;
+    int32_t* idx_pt = nullptr;
+    sfmcov_diagnostics* diag = nullptr;
+};
+
+void sync_status(sfmcov_handle* h) {
+    SFM_CUDA(cudaMemcpyAsync(h->st_host, h->status.p, sizeof(Status), cudaMemcpyDeviceToHost, h->s));
+    SFM_CUDA(cudaStreamSynchronize(h->s));
+}
+
+void throw_validation(sfmcov_handle* h, const SceneDev& sc, bool full) {
+    const Status& st = *h->st_host;
+    if (full && st.cam_bad != INT_MAX) {
+        const int i = st.cam_bad / 4, code = st.cam_bad % 4;
+        throw ApiError{SFMCOV_ERR_INVARIANT, "validate",
+                       "camera " + std::to_string(i) + (code == 1 ? " has non-finite parameters" : " has non-positive focal length")};
+    }
+    if (full && st.pt_bad != INT_MAX)
+        throw ApiError{SFMCOV_ERR_INVARIANT, "validate", "point " + std::to_string(st.pt_bad) + " has non-finite coordinates"};
+    if (st.obs_bad != LLONG_MAX) {
+        const long long t = st.obs_bad / 8;
+        const int code = (int)(st.obs_bad % 8);
+        static const char* msg[] = {"", " camera index out of range", " point index out of range", " has non-finite values",
+                                    " covariance not symmetric", " covariance not positive definite"};
+        throw ApiError{SFMCOV_ERR_INVARIANT, "validate", "observation " + std::to_string(t) + msg[code]};
+    }
+    if (full && st.dup) throw ApiError{SFMCOV_ERR_INVARIANT, "validate", "duplicate (camera, point) observation pair"};
+    (void)sc;
+}
+
+void throw_counts(sfmcov_handle* h) {
+    const Status& st = *h->st_host;
+    if (st.cam_count_bad != INT_MAX) {
+        int c = 0;
+        const int i = st.cam_count_bad;
+        int o[2];
+        SFM_CUDA(cudaMemcpy(o, (int*)h->off_cam.p + i, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+        c = o[1] - o[0];
+        throw ApiError{SFMCOV_ERR_INVARIANT, "validate",
+                       "camera " + std::to_string(i) + " observes " + std::to_string(c) + " points, need at least 4"};
+    }
+    if (st.pt_count_bad != INT_MAX) {
+        const int j = st.pt_count_bad;
+        int o[2];
+        SFM_CUDA(cudaMemcpy(o, (int*)h->off_pt.p + j, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+        throw ApiError{SFMCOV_ERR_INVARIANT, "validate",
+                       "point " + std::to_string(j) + " is observed by " + std::to_string(o[1] - o[0]) +
+                           " cameras, need at least 2"};
+    }
+}
+
+void throw_numeric(sfmcov_handle* h, const SceneDev& sc, Mode mode) {
+    const Status& st = *h->st_host;
+    if (st.jac_bad != INT_MAX) {
+        double d = 0.0;
+        launch_depth_of(sc, (const double*)h->R.p, st.jac_bad, (double*)h->depth.get(8), h->s);
+        SFM_CUDA(cudaMemcpyAsync(&d, h->depth.p, 8, cudaMemcpyDeviceToHost, h->s));
+        SFM_CUDA(cudaStreamSynchronize(h->s));
+        throw ApiError{SFMCOV_ERR_DEGENERATE, "jacobian",
+                       "observation " + std::to_string(st.jac_bad) + ": projection: point at camera-space depth " +
+                           fmt_f(d) + " (behind camera or on the principal plane)"};
+    }
+    if (mode == M_JACOBIAN) return;
+    if (st.rot_bad != INT_MAX)
+        throw ApiError{SFMCOV_ERR_DEGENERATE, "nullspace",
+                       "camera " + std::to_string(st.rot_bad) + " has a rank-deficient rotation system"};
+    if (mode == M_NULLSPACE) return;
+    if (st.fisher_bad != INT_MAX)
+        throw ApiError{SFMCOV_ERR_DEGENERATE, "fisher",
+                       "observation " + std::to_string(st.fisher_bad) + " covariance is not positive definite"};
+    if (mode == M_FISHER) return;
+    if (st.pt_sing_bad != INT_MAX)
+        throw ApiError{SFMCOV_ERR_DEGENERATE, "schur", "point " + std::to_string(st.pt_sing_bad) + " has a singular 3x3 block"};
+    if (mode == M_SCHUR) return;
+    if (st.border_bad)
+        throw ApiError{SFMCOV_ERR_DEGENERATE, "factorization",
+                       "gauge border block is not negative definite; the scene is likely disconnected or its gauge degenerate"};
+    if (st.chol_bad != INT_MAX)
+        throw ApiError{SFMCOV_ERR_DEGENERATE, "factorization",
+                       "non-positive pivot at index " + std::to_string(st.chol_bad) +
+                           "; the scene is likely disconnected or its gauge degenerate"};
+}
+
+void mark(sfmcov_handle* h, int i) {
+    if (h->profiling) SFM_CUDA(cudaEventRecord(h->ev[i], h->s));
+}
+
+// The whole device pipeline.  `sc` points at device memory.
+void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
+    cudaStream_t s = h->s;
+    const int n = sc.n, m = sc.m, t = sc.t, P = sc.P;
+    if (P != 8 && P != 9) throw ApiError{SFMCOV_ERR_DIMENSION, "validate", "camera width must be 8 or 9"};
+    if (n < 0 || m < 0 || t < 0) throw ApiError{SFMCOV_ERR_DIMENSION, "validate", "negative scene size"};
+    if ((long long)n * n >= (1LL << 32)) throw ApiError{SFMCOV_ERR_SIZE_GUARD, "validate", "too many cameras for 32-bit pair keys"};
+    const bool full = (mode == M_FULL || mode == M_SCHUR || mode == M_INDEX);
+    for (auto& v : h->stage_ms) v = 0.0;
+    Status* st = h->status.as<Status>(1);
+    mark(h, 0);
+    launch_status_init(st, s);
+    int* cnt_cam = h->cnt_cam.as<int>(n + 1);
+    int* cnt_pt = h->cnt_pt.as<int>(m + 1);
+    launch_validate(sc, full ? 1 : 0, st, cnt_cam, cnt_pt, s);
+    sync_status(h);
+    throw_validation(h, sc, full);
+    IndexDev ix;
+    ix.off_cam = h->off_cam.as<int>(n + 1);
+    ix.off_pt = h->off_pt.as<int>(m + 1);
+    ix.idx_cam = h->idx_cam.as<int>(t);
+    ix.idx_pt = h->idx_pt.as<int>(t);
+    ix.pos_cam = h->pos_cam.as<int>(t);
+    ix.key_scratch = h->key_scratch.as<int>(t);
+    launch_build_index(sc, cnt_cam, cnt_pt, ix, h->ws, s);
+    launch_structure_check(sc, ix, st, s);
+    if (full || mode == M_INDEX) {
+        sync_status(h);
+        if (h->st_host->dup) throw ApiError{SFMCOV_ERR_INVARIANT, "validate", "duplicate (camera, point) observation pair"};
+        throw_counts(h);
+    }
+    if (mode == M_INDEX) {
+        std::vector<int> oc(n + 1), op(m + 1);
+        SFM_CUDA(cudaMemcpy(oc.data(), ix.off_cam, 4 * (size_t)(n + 1), cudaMemcpyDeviceToHost));
+        SFM_CUDA(cudaMemcpy(op.data(), ix.off_pt, 4 * (size_t)(m + 1), cudaMemcpyDeviceToHost));
+        for (int i = 0; i <= n; ++i) out.off_cam[i] = oc[i];
+        for (int j = 0; j <= m; ++j) out.off_pt[j] = op[j];
+        SFM_CUDA(cudaMemcpy(out.idx_cam, ix.idx_cam, 4 * (size_t)t, cudaMemcpyDeviceToHost));
+        SFM_CUDA(cudaMemcpy(out.idx_pt, ix.idx_pt, 4 * (size_t)t, cudaMemcpyDeviceToHost));
+        return;
+    }
+    mark(h, 1);
+    // ---- (a) Jacobian ---------------------------------------------------------
+    double* R = h->R.as<double>(9 * (size_t)n);
+    double* rec = h->rec.as<double>((size_t)kRec * t);
+    launch_jacobian(sc, R, rec, st, s);
+    mark(h, 2);
+    if (mode == M_JACOBIAN) {
+        sync_status(h);
+        throw_numeric(h, sc, mode);
+        std::vector<double> r((size_t)kRec * t);
+        SFM_CUDA(cudaMemcpy(r.data(), rec, 8 * r.size(), cudaMemcpyDeviceToHost));
+        for (int k = 0; k < t; ++k) {
+            std::memcpy(out.jc + (size_t)2 * P * k, &r[(size_t)kRec * k], 8 * 2 * P);
+            std::memcpy(out.jp + (size_t)6 * k, &r[(size_t)kRec * k + 2 * P], 8 * 6);
+        }
+        return;
+    }
+    // ---- Fisher reductions, (c) rotation blocks, conditioning scales ------------
+    const size_t ncols = (size_t)P * n + 3 * (size_t)m;
+    double* D = h->D.as<double>((size_t)P * P * n);
+    double* Hr = h->Hr.as<double>(9 * (size_t)n);
+    double* A = h->A.as<double>(9 * (size_t)m);
+    double* s_a = h->s_a.as<double>(ncols);
+    unsigned char* flags = h->flags.as<unsigned char>(ncols);
+    launch_reductions(sc, ix, rec, D, Hr, A, s_a, flags, st, s);
+    double* bpart = h->bpart.as<double>(7 * (size_t)border_partial_blocks(n, m));
+    double* s_b = h->s_b.as<double>(7);
+    launch_border_scales(sc, Hr, s_a, bpart, s_b, s);
+    mark(h, 3);
+    if (mode == M_FISHER || mode == M_NULLSPACE) {
+        sync_status(h);
+        throw_numeric(h, sc, mode);
+        if (out.H) {
+            double* H = h->H.as<double>(ncols * 7);
+            launch_write_h(sc, Hr, H, s);
+            SFM_CUDA(cudaMemcpy(out.H, H, 8 * ncols * 7, cudaMemcpyDeviceToHost));
+        }
+        if (out.D) SFM_CUDA(cudaMemcpy(out.D, D, 8 * (size_t)P * P * n, cudaMemcpyDeviceToHost));
+        if (out.A) SFM_CUDA(cudaMemcpy(out.A, A, 8 * 9 * (size_t)m, cudaMemcpyDeviceToHost));
+        if (out.s_a) SFM_CUDA(cudaMemcpy(out.s_a, s_a, 8 * ncols, cudaMemcpyDeviceToHost));
+        if (out.s_b) SFM_CUDA(cudaMemcpy(out.s_b, s_b, 8 * 7, cudaMemcpyDeviceToHost));
+        if (out.Cp) {
+            // couplings C_t = (J_c^T W) J_p from the records (host assembly of a test output)
+            std::vector<double> r((size_t)kRec * t);
+            SFM_CUDA(cudaMemcpy(r.data(), rec, 8 * r.size(), cudaMemcpyDeviceToHost));
+            for (int k = 0; k < t; ++k) {
+                const double* jc = &r[(size_t)kRec * k];
+                const double* jp = jc + 2 * P;
+                const double* W = jp + 6;
+                double* c = out.Cp + (size_t)P * 3 * k;
+                for (int p = 0; p < P; ++p) {
+                    const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
+                    const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
+                    for (int q = 0; q < 3; ++q) c[3 * p + q] = t0 * jp[q] + t1 * jp[3 + q];
+                }
+            }
+        }
+        if (out.diag) {
+            std::vector<unsigned char> f(ncols);
+            SFM_CUDA(cudaMemcpy(f.data(), flags, ncols, cudaMemcpyDeviceToHost));
+            int64_t cnt = 0;
+            for (size_t c = 0; c < ncols; ++c)
+                if (f[c]) {
+                    if (out.diag->flagged && cnt < out.diag->flagged_capacity) out.diag->flagged[cnt] = (int64_t)c;
+                    ++cnt;
+                }
+            out.diag->n_flagged = (int32_t)cnt;
+        }
+        return;
+    }
+    // ---- (b) Schur: point preparation, border, pairs ----------------------------
+    double* Wb = h->Wb.as<double>((size_t)kWStride * t);
+    double* V = h->V.as<double>(21 * (size_t)m);
+    const int ppb = point_prep_blocks(m);
+    double* Fpart = h->Fpart.as<double>(28 * (size_t)ppb);
+    launch_point_prep(sc, ix, rec, A, s_a, s_b, Wb, V, Fpart, st, s);
+    double* LF = h->LF.as<double>(49);
+    double* E = h->E.as<double>(49);
+    double* eigE = h->eigE.as<double>(8);
+    launch_border_factor(Fpart, ppb, LF, E, eigE, st, s);
+    const int N = P * n;
+    double* Gamma = h->Gamma.as<double>((size_t)N * 7);
+    double* G = h->G.as<double>((size_t)N * 7);
+    launch_camera_border(sc, ix, Wb, V, Hr, s_a, s_b, LF, Gamma, G, s);
+    mark(h, 4);
+    build_pairs(sc, ix, h->pairs, h->ws, s);
+    mark(h, 5);
+    const int Npad = ((N + kNB - 1) / kNB) * kNB;
+    const long long ld = Npad;
+    double* Z = h->Z.as<double>((size_t)Npad * Npad);
+    launch_fill(P, Z, ld, N, Npad, D, s_a, G, mode == M_FULL ? 1 : 0, s);
+    mark(h, 6);
+    launch_pair_reduce(P, h->pairs, Wb, n, Z, ld, s);
+    mark(h, 7);
+    h->counts[0] = h->pairs.npairs;
+    h->counts[1] = h->pairs.nseg;
+    h->counts[2] = N;
+    h->counts[3] = Npad;
+    h->counts[4] = t;
+    h->counts[5] = m;
+    h->counts[6] = n;
+    h->counts[7] = P;
+    if (mode == M_SCHUR) {
+        sync_status(h);
+        throw_numeric(h, sc, mode);
+        // bordered Z_p: [[Z, Γ], [Γ^T, E]] (host assembly of a test output)
+        const size_t dim = (size_t)N + 7;
+        std::vector<double> z((size_t)Npad * Npad), gm((size_t)N * 7), e(49);
+        SFM_CUDA(cudaMemcpy(z.data(), Z, 8 * z.size(), cudaMemcpyDeviceToHost));
+        SFM_CUDA(cudaMemcpy(gm.data(), Gamma, 8 * gm.size(), cudaMemcpyDeviceToHost));
+        SFM_CUDA(cudaMemcpy(e.data(), E, 8 * 49, cudaMemcpyDeviceToHost));
+        for (size_t c = 0; c < dim; ++c)
+            for (size_t r = 0; r < dim; ++r) {
+                double v;
+                if (r < (size_t)N && c < (size_t)N) v = (r >= c) ? z[c * Npad + r] : z[r * Npad + c];
+                else if (r < (size_t)N) v = gm[r * 7 + (c - N)];
+                else if (c < (size_t)N) v = gm[c * 7 + (r - N)];
+                else v = e[(r - N) * 7 + (c - N)];
+                out.z_p[c * dim + r] = v;
+            }
+        return;
+    }
+    // ---- (d) dense gauge-fixed inversion ---------------------------------------
+    const int K = Npad / kNB;
+    double* Linv = h->Linv.as<double>((size_t)K * kNB * kNB);
+    double* piv = h->piv.as<double>((size_t)Npad);
+    double* Lp = h->Lp.as<double>((size_t)2 * Npad * kNB);
+    int launches = dense_cholesky(Z, ld, Npad, Linv, piv, st, s, h->s2, h->e1, h->e2);
+    mark(h, 8);
+    launches += dense_trtri(Z, ld, Npad, Linv, Lp, s, h->s2, h->e1, h->e2);
+    mark(h, 9);
+    int* psd = h->psd.as<int>(1);
+    SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
+    launch_extract(P, Z, ld, N, n, s_a, 1, out.d_cam_cov, st, psd, s);
+    double* prange = h->prange.as<double>(2);
+    launch_pivot_range(piv, N, prange, s);
+    mark(h, 10);
+    h->counts[8] = launches;
+    sync_status(h);
+    throw_numeric(h, sc, mode);
+    if (h->profiling) {
+        for (int i = 0; i < ST_COUNT; ++i) {
+            float ms = 0.f;
+            SFM_CUDA(cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]));
+            h->stage_ms[i] = ms;
+        }
+    }
+    if (out.diag) {
+        sfmcov_diagnostics* d = out.diag;
+        double pr[2], ee[8];
+        int warn = 0;
+        SFM_CUDA(cudaMemcpy(pr, prange, 16, cudaMemcpyDeviceToHost));
+        SFM_CUDA(cudaMemcpy(ee, eigE, 56, cudaMemcpyDeviceToHost));
+        SFM_CUDA(cudaMemcpy(&warn, psd, 4, cudaMemcpyDeviceToHost));
+        double mn = pr[0], mx = pr[1];
+        for (int l = 0; l < 7; ++l) { mn = std::min(mn, std::fabs(ee[l])); mx = std::max(mx, std::fabs(ee[l])); }
+        d->min_pivot = mn;
+        d->max_pivot = mx;
+        d->inertia_positive = N;
+        d->inertia_negative = 7;
+        d->negative_eigenvalue_warnings = warn;
+        d->largest_dense_dim = (int64_t)N + 7;
+        d->peak_dense_bytes = (int64_t)8 * Npad * (int64_t)Npad;
+        // scale range and flagged columns
+        std::vector<double> sa(ncols);
+        std::vector<unsigned char> f(ncols);
+        SFM_CUDA(cudaMemcpy(sa.data(), s_a, 8 * ncols, cudaMemcpyDeviceToHost));
+        if (h->st_host->nflag) SFM_CUDA(cudaMemcpy(f.data(), flags, ncols, cudaMemcpyDeviceToHost));
+        d->scale_min = ncols ? *std::min_element(sa.begin(), sa.end()) : 1.0;
+        d->scale_max = ncols ? *std::max_element(sa.begin(), sa.end()) : 1.0;
+        int64_t cnt = 0;
+        if (h->st_host->nflag)
+            for (size_t c = 0; c < ncols; ++c)
+                if (f[c]) {
+                    if (d->flagged && cnt < d->flagged_capacity) d->flagged[cnt] = (int64_t)c;
+                    ++cnt;
+                }
+        d->n_flagged = (int32_t)cnt;
+        if (!(mn > 1e-12 * mx))
+            throw ApiError{SFMCOV_ERR_DEGENERATE, "factorization",
+                           "near-singular pivot (ratio " + fmt_f(mn / mx) +
+                               "); the scene is likely disconnected or its gauge degenerate"};
+    }
+}
+
+// Copies a host scene into the handle's staging buffers.
+SceneDev upload(sfmcov_handle* h, const sfmcov_scene* s) {
+    SceneDev d;
+    d.n = s->n_cams; d.m = s->n_pts; d.t = s->n_obs; d.P = s->cam_params;
+    if (d.P != 8 && d.P != 9) throw ApiError{SFMCOV_ERR_DIMENSION, "validate", "camera width must be 8 or 9"};
+    if (d.n < 0 || d.m < 0 || d.t < 0) throw ApiError{SFMCOV_ERR_DIMENSION, "validate", "negative scene size"};
+    auto put = [&](DBuf& b, const void* src, size_t bytes) -> void* {
+        void* p = b.get(bytes);
+        if (bytes && src) SFM_CUDA(cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, h->s));
+        return p;
+    };
+    d.cams = (const double*)put(h->h_cams, s->cams, 8 * (size_t)d.P * d.n);
+    d.pts = (const double*)put(h->h_pts, s->pts, 24 * (size_t)d.m);
+    d.oc = (const int*)put(h->h_oc, s->obs_cam, 4 * (size_t)d.t);
+    d.op = (const int*)put(h->h_op, s->obs_pt, 4 * (size_t)d.t);
+    d.u = s->obs_u ? (const double*)put(h->h_u, s->obs_u, 16 * (size_t)d.t) : nullptr;
+    d.sigma = s->obs_sigma ? (const double*)put(h->h_sigma, s->obs_sigma, 32 * (size_t)d.t) : nullptr;
+    return d;
+}
+
+SceneDev as_device(const sfmcov_scene* s) {
+    SceneDev d;
+    d.n = s->n_cams; d.m = s->n_pts; d.t = s->n_obs; d.P = s->cam_params;
+    d.cams = s->cams; d.pts = s->pts; d.oc = s->obs_cam; d.op = s->obs_pt; d.u = s->obs_u; d.sigma = s->obs_sigma;
+    return d;
+}
+
+template <typename F>
+int32_t guarded(sfmcov_handle* h, sfmcov_error* err, F&& body) {
+    if (!h) {
+        fill_error(err, ApiError{SFMCOV_ERR_DEVICE, "device", "null handle"});
+        return SFMCOV_ERR_DEVICE;
+    }
+    std::lock_guard<std::mutex> lock(h->mu);
+    try {
+        SFM_CUDA(cudaSetDevice(h->device));
+        body();
+        clear_error(err);
+        return SFMCOV_OK;
+    } catch (const ApiError& e) {
+        cudaStreamSynchronize(h->s);
+        fill_error(err, e);
+        return e.kind;
+    } catch (const std::exception& e) {
+        fill_error(err, ApiError{SFMCOV_ERR_DEVICE, "device", e.what()});
+        return SFMCOV_ERR_DEVICE;
+    }
+}
+
+void check_options(const sfmcov_options* o) {
+    if (o && (o->point_covariances || o->camera_cross_covariances))
+        throw ApiError{SFMCOV_ERR_DIMENSION, "options",
+                       "point and cross covariances are not available in this build (camera blocks only)"};
+}
+
+}  // namespace
+
+extern "C" {
+
+sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count <= device || device < 0) {
+        fill_error(err, ApiError{SFMCOV_ERR_DEVICE, "device",
+                                 std::string("no usable CUDA device (") + cudaGetErrorString(e) + "); this library has no CPU path"});
+        return nullptr;
+    }
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, device);
+    if (prop.major < 10) {
+        fill_error(err, ApiError{SFMCOV_ERR_DEVICE, "device", std::string("device ") + prop.name + " is not sm_100"});
+        return nullptr;
+    }
+    auto* h = new sfmcov_handle();
+    try {
+        h->device = device;
+        SFM_CUDA(cudaSetDevice(device));
+        SFM_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+        SFM_CUDA(cudaStreamCreateWithFlags(&h->s2, cudaStreamNonBlocking));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->e1, cudaEventDisableTiming));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->e2, cudaEventDisableTiming));
+        for (auto& ev : h->ev) SFM_CUDA(cudaEventCreate(&ev));
+        SFM_CUDA(cudaMallocHost(&h->st_host, sizeof(Status)));
+    } catch (const std::exception& x) {
+        fill_error(err, ApiError{SFMCOV_ERR_DEVICE, "device", x.what()});
+        delete h;
+        return nullptr;
+    }
+    clear_error(err);
+    return h;
+}
+
+void sfmcov_cuda_destroy(sfmcov_handle* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->s);
+    cudaStreamSynchronize(h->s2);
+    DBuf* bufs[] = {&h->ws.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_u, &h->h_sigma, &h->cnt_cam,
+                    &h->cnt_pt, &h->off_cam, &h->idx_cam, &h->off_pt, &h->idx_pt, &h->pos_cam, &h->key_scratch,
+                    &h->R, &h->rec, &h->D, &h->Hr, &h->A, &h->s_a, &h->flags, &h->bpart, &h->s_b, &h->Wb, &h->V,
+                    &h->Fpart, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->Lp, &h->piv,
+                    &h->cov, &h->psd, &h->prange, &h->status, &h->depth, &h->H};
+    for (DBuf* b : bufs) b->release();
+    h->pairs.release();
+    if (h->st_host) cudaFreeHost(h->st_host);
+    cudaEventDestroy(h->e1);
+    cudaEventDestroy(h->e2);
+    for (auto& ev : h->ev) cudaEventDestroy(ev);
+    cudaStreamDestroy(h->s);
+    cudaStreamDestroy(h->s2);
+    delete h;
+}
+
+void* sfmcov_cuda_stream(sfmcov_handle* h) { return h ? (void*)h->s : nullptr; }
+
+void sfmcov_cuda_set_profiling(sfmcov_handle* h, int32_t on) {
+    if (h) h->profiling = on != 0;
+}
+
+int32_t sfmcov_cuda_compute_covariance(sfmcov_handle* h, const sfmcov_scene* scene, const sfmcov_options* opts,
+                                       double* cam_cov, sfmcov_diagnostics* diag, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        check_options(opts);
+        const SceneDev sc = upload(h, scene);
+        const int P = sc.P;
+        double* dcov = h->cov.as<double>((size_t)P * P * sc.n);
+        Outputs out;
+        out.d_cam_cov = dcov;
+        out.diag = diag;
+        run(h, sc, M_FULL, out);
+        if (sc.n) SFM_CUDA(cudaMemcpyAsync(cam_cov, dcov, 8 * (size_t)P * P * sc.n, cudaMemcpyDeviceToHost, h->s));
+        SFM_CUDA(cudaStreamSynchronize(h->s));
+    });
+}
+
+int32_t sfmcov_cuda_compute_covariance_device(sfmcov_handle* h, const sfmcov_scene* d_scene, const sfmcov_options* opts,
+                                              double* d_cam_cov, sfmcov_diagnostics* diag, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        check_options(opts);
+        Outputs out;
+        out.d_cam_cov = d_cam_cov;
+        out.diag = diag;
+        run(h, as_device(d_scene), M_FULL, out);
+        SFM_CUDA(cudaStreamSynchronize(h->s));
+    });
+}
+
+int32_t sfmcov_cuda_observation_index(sfmcov_handle* h, const sfmcov_scene* scene, int64_t* off_cam, int32_t* idx_cam,
+                                      int64_t* off_pt, int32_t* idx_pt, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        const SceneDev sc = upload(h, scene);
+        Outputs out;
+        out.off_cam = off_cam; out.idx_cam = idx_cam; out.off_pt = off_pt; out.idx_pt = idx_pt;
+        run(h, sc, M_INDEX, out);
+    });
+}
+
+int32_t sfmcov_cuda_jacobian(sfmcov_handle* h, const sfmcov_scene* scene, double* cam_blocks, double* point_blocks,
+                             sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        const SceneDev sc = upload(h, scene);
+        Outputs out;
+        out.jc = cam_blocks; out.jp = point_blocks;
+        run(h, sc, M_JACOBIAN, out);
+    });
+}
+
+int32_t sfmcov_cuda_nullspace(sfmcov_handle* h, const sfmcov_scene* scene, double* H, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        const SceneDev sc = upload(h, scene);
+        Outputs out;
+        out.H = H;
+        run(h, sc, M_NULLSPACE, out);
+    });
+}
+
+int32_t sfmcov_cuda_fisher(sfmcov_handle* h, const sfmcov_scene* scene, double* D, double* A, double* couplings,
+                           double* s_a, double* s_b, sfmcov_diagnostics* diag, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        const SceneDev sc = upload(h, scene);
+        Outputs out;
+        out.D = D; out.A = A; out.Cp = couplings; out.s_a = s_a; out.s_b = s_b; out.diag = diag;
+        run(h, sc, M_FISHER, out);
+    });
+}
+
+int32_t sfmcov_cuda_schur(sfmcov_handle* h, const sfmcov_scene* scene, double* z_p, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        const SceneDev sc = upload(h, scene);
+        Outputs out;
+        out.z_p = z_p;
+        run(h, sc, M_SCHUR, out);
+    });
+}
+
+int32_t sfmcov_cuda_spd_inverse_blocks(sfmcov_handle* h, const double* a, int64_t n, int32_t block, double* blocks,
+                                       double* min_pivot, double* max_pivot, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        if (n <= 0 || block <= 0 || n % block) throw ApiError{SFMCOV_ERR_DIMENSION, "factorization", "n must be a positive multiple of block"};
+        if (block != 8 && block != 9) throw ApiError{SFMCOV_ERR_DIMENSION, "factorization", "block must be 8 or 9"};
+        cudaStream_t s = h->s;
+        const int N = (int)n;
+        const int Npad = ((N + kNB - 1) / kNB) * kNB;
+        const long long ld = Npad;
+        double* Z = h->Z.as<double>((size_t)Npad * Npad);
+        // identity padding, then the user matrix (column by column)
+        SFM_CUDA(cudaMemsetAsync(Z, 0, 8 * (size_t)Npad * Npad, s));
+        std::vector<double> one(1, 1.0);
+        for (int i = N; i < Npad; ++i) SFM_CUDA(cudaMemcpy(Z + (size_t)i * ld + i, one.data(), 8, cudaMemcpyHostToDevice));
+        SFM_CUDA(cudaMemcpy2DAsync(Z, 8 * ld, a, 8 * (size_t)N, 8 * (size_t)N, N, cudaMemcpyHostToDevice, s));
+        Status* st = h->status.as<Status>(1);
+        launch_status_init(st, s);
+        const int K = Npad / kNB;
+        double* Linv = h->Linv.as<double>((size_t)K * kNB * kNB);
+        double* piv = h->piv.as<double>((size_t)Npad);
+        double* Lp = h->Lp.as<double>((size_t)2 * Npad * kNB);
+        dense_cholesky(Z, ld, Npad, Linv, piv, st, s, h->s2, h->e1, h->e2);
+        dense_trtri(Z, ld, Npad, Linv, Lp, s, h->s2, h->e1, h->e2);
+        const int nb = N / block;
+        double* dcov = h->cov.as<double>((size_t)block * block * nb);
+        int* psd = h->psd.as<int>(1);
+        SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
+        launch_extract(block, Z, ld, N, nb, nullptr, 0, dcov, st, psd, s);
+        double* prange = h->prange.as<double>(2);
+        launch_pivot_range(piv, N, prange, s);
+        sync_status(h);
+        if (h->st_host->chol_bad != INT_MAX)
+            throw ApiError{SFMCOV_ERR_DEGENERATE, "factorization",
+                           "non-positive pivot at index " + std::to_string(h->st_host->chol_bad) + "; matrix is not positive definite"};
+        SFM_CUDA(cudaMemcpy(blocks, dcov, 8 * (size_t)block * block * nb, cudaMemcpyDeviceToHost));
+        double pr[2];
+        SFM_CUDA(cudaMemcpy(pr, prange, 16, cudaMemcpyDeviceToHost));
+        if (min_pivot) *min_pivot = pr[0];
+        if (max_pivot) *max_pivot = pr[1];
+    });
+}
+
+int32_t sfmcov_cuda_last_stage_times(sfmcov_handle* h, double* ms, int32_t capacity) {
+    if (!h) return 0;
+    const int k = std::min<int>(capacity, ST_COUNT);
+    for (int i = 0; i < k; ++i) ms[i] = h->stage_ms[i];
+    return k;
+}
+
+const char* sfmcov_cuda_stage_name(int32_t i) { return (i >= 0 && i < ST_COUNT) ? kStageNames[i] : ""; }
+
+int32_t sfmcov_cuda_last_counts(sfmcov_handle* h, int64_t* counts, int32_t capacity) {
+    if (!h) return 0;
+    const int k = std::min(capacity, 9);
+    for (int i = 0; i < k; ++i) counts[i] = h->counts[i];
+    return k;
+}
+
+}  // extern "C"

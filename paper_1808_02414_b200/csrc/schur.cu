@@ -1,0 +1,446 @@
+// Stage (b): point-block Schur reduction into the gauge-augmented dense
+// camera matrix, without global atomics in the accumulation.
+//
+// Reference: schur_reduce, src/covariance.cpp:137-194 (serial point loop
+// accumulating C_a A_j^-1 C_b^T into camera-pair blocks, border rows
+// C_a A_j^-1 H_pj and corner H_pj^T A_j^-1 H_pj), with the conditioning of
+// src/covariance.cpp:84-135 applied on the fly.
+//
+// B200 formulation (all in conditioned coordinates):
+//   A_s,j = L_j L_j^T                       (3x3 Cholesky per point)
+//   W_a   = C_s,a L_j^-T                    (P x 3 per observation)
+//   V_j   = L_j^-1 H_s,pj                   (3 x 7 per point)
+//   Z     = D_s - Σ_pairs W_b W_a^T         (camera-pair blocks)
+//   Γ_i   = H_s,ci - Σ_{a in cam i} W_a V_j (P x 7 per camera)
+//   F     = Σ_j V_j^T V_j = -E              (7 x 7, SPD)
+//   G     = Γ L_F^-T,  Z_aug = Z + G G^T = Z - Γ E^-1 Γ^T
+// Z_aug is SPD and its inverse is the camera block of the inverse of the
+// bordered matrix [[Z, Γ], [Γ^T, E]], so the dense
+// stage is a plain Cholesky.
+//
+// Pair accumulation: observation pairs (a, b) of each point are keyed by
+// camera-pair block (lo * n + hi), stably radix-sorted, and each block is
+// reduced by one warp with register accumulators — one write per nonzero
+// block, deterministic order, no atomics.
+#include "common.cuh"
+#include "detmath.cuh"
+#include "kernels.cuh"
+
+#include <cub/cub.cuh>
+
+namespace sfm {
+
+// ---- per-point preparation (thread per point) -----------------------------------
+template <int P>
+__global__ void k_point_prep(const int* off_pt, const int* idx_pt, const int* oc, const int* pos_cam,
+                             const double* rec, const double* A, const double* s_a, const double* pts,
+                             const double* s_b, int m, int n, double* Wb, double* V, double* Fpart,
+                             Status* st) {
+    __shared__ double red[128][28];
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    double f[28];
+#pragma unroll
+    for (int k = 0; k < 28; ++k) f[k] = 0.0;
+    if (j < m) {
+        const double* sp = s_a + (size_t)P * n + 3 * (size_t)j;
+        double as[9];
+        for (int p = 0; p < 3; ++p)
+            for (int q = 0; q < 3; ++q) as[3 * p + q] = (sp[p] * A[9 * (size_t)j + 3 * p + q]) * sp[q];
+        bool good = eig_ok3(as, kPivotRtol);
+        double l00 = 1, l10 = 0, l11 = 1, l20 = 0, l21 = 0, l22 = 1;
+        if (good) {
+            l00 = sqrt(as[0]);
+            l10 = as[3] / l00;
+            l20 = as[6] / l00;
+            const double d11 = as[4] - l10 * l10;
+            l11 = sqrt(d11);
+            l21 = (as[7] - l20 * l10) / l11;
+            const double d22 = as[8] - l20 * l20 - l21 * l21;
+            l22 = sqrt(d22);
+            if (!(d11 > 0.0) || !(d22 > 0.0)) good = false;
+        }
+        if (!good) atomicMin(&st->pt_sing_bad, j);
+        // H_s rows of the point: (s_p[q] * [e_q | [X]x row q | X_q]) * s_b
+        const double* X = pts + 3 * (size_t)j;
+        double sx[9];
+        skew(X, sx);
+        double hs[3][7];
+        for (int q = 0; q < 3; ++q) {
+            double h[7] = {0, 0, 0, 0, 0, 0, 0};
+            h[q] = 1.0;
+            h[3] = sx[3 * q]; h[4] = sx[3 * q + 1]; h[5] = sx[3 * q + 2];
+            h[6] = X[q];
+            for (int l = 0; l < 7; ++l) hs[q][l] = (sp[q] * h[l]) * s_b[l];
+        }
+        double v[3][7];
+        for (int l = 0; l < 7; ++l) {
+            v[0][l] = hs[0][l] / l00;
+            v[1][l] = (hs[1][l] - l10 * v[0][l]) / l11;
+            v[2][l] = (hs[2][l] - l20 * v[0][l] - l21 * v[1][l]) / l22;
+        }
+        double* vo = V + 21 * (size_t)j;
+        for (int q = 0; q < 3; ++q)
+            for (int l = 0; l < 7; ++l) vo[7 * q + l] = good ? v[q][l] : 0.0;
+        if (good) {
+            int k = 0;
+            for (int l1 = 0; l1 < 7; ++l1)
+                for (int l2 = l1; l2 < 7; ++l2, ++k)
+                    f[k] = (v[0][l1] * v[0][l2] + v[1][l1] * v[1][l2]) + v[2][l1] * v[2][l2];
+        }
+        for (int kk = off_pt[j]; kk < off_pt[j + 1]; ++kk) {
+            const int t = idx_pt[kk];
+            const double* r = rec + (size_t)t * kRec;
+            const double* jc = r + Layout<P>::JC;
+            const double* jp = r + Layout<P>::JP;
+            const double* W = r + Layout<P>::WO;
+            const double* sc = s_a + (size_t)P * oc[t];
+            double* wo = Wb + (size_t)pos_cam[t] * kWStride;
+            for (int p = 0; p < P; ++p) {
+                const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
+                const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
+                double c[3];
+                for (int q = 0; q < 3; ++q) c[q] = (sc[p] * (t0 * jp[q] + t1 * jp[3 + q])) * sp[q];
+                const double w0 = c[0] / l00;
+                const double w1 = (c[1] - l10 * w0) / l11;
+                const double w2 = (c[2] - l20 * w0 - l21 * w1) / l22;
+                wo[3 * p + 0] = good ? w0 : 0.0;
+                wo[3 * p + 1] = good ? w1 : 0.0;
+                wo[3 * p + 2] = good ? w2 : 0.0;
+            }
+            wo[27] = 0.0;
+        }
+    }
+    // deterministic block reduction of F_j = V_j^T V_j
+    for (int k = 0; k < 28; ++k) red[threadIdx.x][k] = f[k];
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int k = 0; k < 28; ++k) red[threadIdx.x][k] += red[threadIdx.x + w][k];
+        __syncthreads();
+    }
+    if (threadIdx.x < 28) Fpart[28 * (size_t)blockIdx.x + threadIdx.x] = red[0][threadIdx.x];
+}
+
+// F = Σ partials (fixed order); L_F = chol(F); eig(E = -F) for diagnostics.
+__global__ void k_border_factor(const double* Fpart, int nblocks, double* LF, double* Eout, double* eigE,
+                                Status* st) {
+    if (threadIdx.x != 0) return;
+    double F[49];
+    int k = 0;
+    for (int l1 = 0; l1 < 7; ++l1)
+        for (int l2 = l1; l2 < 7; ++l2, ++k) {
+            double acc = 0.0;
+            for (int b = 0; b < nblocks; ++b) acc += Fpart[28 * (size_t)b + k];
+            F[7 * l1 + l2] = acc;
+            F[7 * l2 + l1] = acc;
+        }
+    for (int q = 0; q < 49; ++q) Eout[q] = -F[q];
+    double a[49], d[7], v[49];
+    for (int q = 0; q < 49; ++q) a[q] = -F[q];
+    jacobi_eig<7>(a, d, v);
+    for (int q = 0; q < 7; ++q) eigE[q] = d[q];
+    // Cholesky of F (lower, row-major)
+    double L[49];
+    for (int q = 0; q < 49; ++q) L[q] = 0.0;
+    bool ok = true;
+    for (int c = 0; c < 7; ++c) {
+        double s = F[7 * c + c];
+        for (int kk = 0; kk < c; ++kk) s -= L[7 * c + kk] * L[7 * c + kk];
+        if (!(s > 0.0)) { ok = false; s = 1.0; }
+        const double lcc = sqrt(s);
+        L[7 * c + c] = lcc;
+        for (int r = c + 1; r < 7; ++r) {
+            double x = F[7 * r + c];
+            for (int kk = 0; kk < c; ++kk) x -= L[7 * r + kk] * L[7 * c + kk];
+            L[7 * r + c] = x / lcc;
+        }
+    }
+    if (!ok) st->border_bad = 1;
+    for (int q = 0; q < 49; ++q) LF[q] = L[q];
+}
+
+// ---- camera border rows (warp per camera) ----------------------------------------
+// Γ_i[p][l] = H_s,ci[p][l] - Σ_{a in cam i} (W_a V_j(a))[p][l], ascending
+// observation order; then G_i = Γ_i L_F^-T.
+template <int P>
+__global__ void k_camera_border(const int* off_cam, const int* idx_cam, const int* op, const double* Wb,
+                                const double* V, const double* cams, const double* Hr, const double* s_a,
+                                const double* s_b, const double* LF, int n, double* Gamma, double* G) {
+    constexpr int NE = P * 7;
+    __shared__ double sh[4][NE];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * 4 + wib;
+    if (i >= n) return;
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int k = off_cam[i]; k < off_cam[i + 1]; ++k) {
+        const double* w = Wb + (size_t)k * kWStride;
+        const double* vj = V + 21 * (size_t)op[idx_cam[k]];
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+            const int en = lane + 32 * s;
+            if (en < NE) {
+                const int p = en / 7, l = en % 7;
+                acc[s] += (w[3 * p] * vj[l] + w[3 * p + 1] * vj[7 + l]) + w[3 * p + 2] * vj[14 + l];
+            }
+        }
+    }
+    const double* C = cams + (size_t)P * i + 3;
+    double sx[9];
+    skew(C, sx);
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+        const int en = lane + 32 * s;
+        if (en < NE) {
+            const int p = en / 7, l = en % 7;
+            double h = 0.0;
+            if (p < 3) h = (l >= 3 && l < 6) ? Hr[9 * (size_t)i + 3 * p + (l - 3)] : 0.0;
+            else if (p < 6) {
+                const int a = p - 3;
+                h = (l < 3) ? (l == a ? 1.0 : 0.0) : (l < 6 ? sx[3 * a + (l - 3)] : C[a]);
+            }
+            const double hs = (s_a[(size_t)P * i + p] * h) * s_b[l];
+            const double g = hs - acc[s];
+            sh[wib][en] = g;
+            Gamma[(size_t)P * 7 * i + en] = g;
+        }
+    }
+    __syncwarp();
+    if (lane < P) {
+        const double* gr = &sh[wib][7 * lane];
+        double out[7];
+        for (int l = 0; l < 7; ++l) {
+            double x = gr[l];
+            for (int kk = 0; kk < l; ++kk) x -= LF[7 * l + kk] * out[kk];
+            out[l] = x / LF[7 * l + l];
+        }
+        for (int l = 0; l < 7; ++l) G[((size_t)P * i + lane) * 7 + l] = out[l];
+    }
+}
+
+// ---- dense fill of the lower triangle --------------------------------------------
+// Z(r, c) = [cam(r)==cam(c)] (s_a[r] D(r,c)) s_a[c] + add_gg * Σ_l G(r,l) G(c,l)
+// for r, c < N; identity on the padding.  64x64 tiles with tile_r >= tile_c.
+template <int P>
+__global__ void k_fill(double* Z, long long ld, int N, int Npad, const double* D, const double* s_a, const double* G,
+                       int add_gg) {
+    __shared__ double gr[64][8], gc[64][8];
+    const int T = Npad / 64;
+    // lower-triangular tile index
+    const long long l = blockIdx.x;
+    int ti = (int)((sqrt(8.0 * (double)l + 1.0) - 1.0) * 0.5);
+    while ((long long)(ti + 1) * (ti + 2) / 2 <= l) ++ti;
+    while ((long long)ti * (ti + 1) / 2 > l) --ti;
+    const int tj = (int)(l - (long long)ti * (ti + 1) / 2);
+    (void)T;
+    const int r0 = ti * 64, c0 = tj * 64;
+    const int tid = threadIdx.x;
+    if (add_gg) {
+        for (int e = tid; e < 64 * 7; e += blockDim.x) {
+            const int rr = e / 7, ll = e % 7;
+            gr[rr][ll] = (r0 + rr < N) ? G[(size_t)(r0 + rr) * 7 + ll] : 0.0;
+            gc[rr][ll] = (c0 + rr < N) ? G[(size_t)(c0 + rr) * 7 + ll] : 0.0;
+        }
+        __syncthreads();
+    }
+    const int rr = tid & 63;
+    const int r = r0 + rr;
+    for (int cc = tid >> 6; cc < 64; cc += blockDim.x >> 6) {
+        const int c = c0 + cc;
+        double v;
+        if (r < N && c < N) {
+            v = 0.0;
+            const int ir = r / P, ic = c / P;
+            if (ir == ic) v = (s_a[r] * D[(size_t)P * P * ir + P * (r - P * ir) + (c - P * ic)]) * s_a[c];
+            if (add_gg) {
+                double gg = 0.0;
+#pragma unroll
+                for (int q = 0; q < 7; ++q) gg += gr[rr][q] * gc[cc][q];
+                v += gg;
+            }
+        } else {
+            v = (r == c) ? 1.0 : 0.0;
+        }
+        Z[(size_t)c * ld + r] = v;
+    }
+}
+
+// ---- observation pairs -----------------------------------------------------------
+__global__ void k_pair_count(const int* off_pt, int m, long long* cnt) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j > m) return;
+    if (j == m) { cnt[m] = 0; return; }
+    const long long k = off_pt[j + 1] - off_pt[j];
+    cnt[j] = k * (k + 1) / 2;
+}
+
+__global__ void k_pair_gen(const int* off_pt, const int* idx_pt, const int* oc, const int* pos_cam, int m, int n,
+                           const long long* poff, unsigned int* keys, unsigned long long* vals) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    long long o = poff[j];
+    const int b = off_pt[j], e = off_pt[j + 1];
+    for (int a = b; a < e; ++a) {
+        const int ta = idx_pt[a];
+        const int ca = oc[ta];
+        for (int c = a; c < e; ++c) {
+            const int tb = idx_pt[c];
+            const int cb = oc[tb];
+            int lo, hi, slo, shi;
+            if (ca <= cb) { lo = ca; hi = cb; slo = pos_cam[ta]; shi = pos_cam[tb]; }
+            else { lo = cb; hi = ca; slo = pos_cam[tb]; shi = pos_cam[ta]; }
+            keys[o] = (unsigned int)lo * (unsigned int)n + (unsigned int)hi;
+            vals[o] = ((unsigned long long)(unsigned int)shi << 32) | (unsigned int)slo;
+            ++o;
+        }
+    }
+}
+
+// Warp per camera-pair block: lanes (g, p) with g < 32/P groups accumulate
+// row p of W_hi W_lo^T over pairs g, g+G, ...; groups are combined in fixed
+// order and the block is written once: Z(P hi + p, P lo + q) -= acc[q].
+template <int P>
+__global__ void __launch_bounds__(256) k_pair_reduce(const unsigned int* ukeys, const long long* seg_off, int nseg,
+                                                     const unsigned long long* vals, const double* Wb, int n,
+                                                     double* Z, long long ld) {
+    constexpr int G = 32 / P;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= nseg) return;
+    const int g = lane / P, p = lane - (lane / P) * P;
+    const bool active = g < G;
+    const long long b = seg_off[warp], e = seg_off[warp + 1];
+    double acc[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) acc[q] = 0.0;
+    if (active) {
+        for (long long idx = b + g; idx < e; idx += G) {
+            const unsigned long long v = vals[idx];
+            const double* wh = Wb + (size_t)(v >> 32) * kWStride + 3 * p;
+            const double2* wl = reinterpret_cast<const double2*>(Wb + (size_t)(v & 0xffffffffULL) * kWStride);
+            const double h0 = wh[0], h1 = wh[1], h2 = wh[2];
+            double w[28];
+#pragma unroll
+            for (int k = 0; k < 14; ++k) { const double2 x = __ldg(wl + k); w[2 * k] = x.x; w[2 * k + 1] = x.y; }
+#pragma unroll
+            for (int q = 0; q < P; ++q) acc[q] += (h0 * w[3 * q] + h1 * w[3 * q + 1]) + h2 * w[3 * q + 2];
+        }
+    }
+    // combine groups: lane p += lane p + P·g (g = 1..G-1), fixed order
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        double tot = acc[q];
+#pragma unroll
+        for (int gg = 1; gg < G; ++gg) tot += __shfl_down_sync(0xffffffffu, acc[q], gg * P);
+        acc[q] = tot;
+    }
+    if (lane < P) {
+        const unsigned int key = ukeys[warp];
+        const int lo = (int)(key / (unsigned int)n), hi = (int)(key - (unsigned int)lo * (unsigned int)n);
+        const size_t row = (size_t)P * hi + p;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            double* z = Z + ((size_t)P * lo + q) * ld + row;
+            *z = *z - acc[q];
+        }
+    }
+}
+
+// ---- host launchers ----------------------------------------------------------------
+int point_prep_blocks(int m) { return (int)cdiv(m > 0 ? m : 1, 128); }
+
+void launch_point_prep(const SceneDev& sc, const IndexDev& ix, const double* rec, const double* A, const double* s_a,
+                       const double* s_b, double* Wb, double* V, double* Fpart, Status* st, cudaStream_t s) {
+    const int nb = point_prep_blocks(sc.m);
+    if (sc.P == 8) k_point_prep<8><<<nb, 128, 0, s>>>(ix.off_pt, ix.idx_pt, sc.oc, ix.pos_cam, rec, A, s_a, sc.pts, s_b, sc.m, sc.n, Wb, V, Fpart, st);
+    else k_point_prep<9><<<nb, 128, 0, s>>>(ix.off_pt, ix.idx_pt, sc.oc, ix.pos_cam, rec, A, s_a, sc.pts, s_b, sc.m, sc.n, Wb, V, Fpart, st);
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_border_factor(const double* Fpart, int nblocks, double* LF, double* E, double* eigE, Status* st,
+                          cudaStream_t s) {
+    k_border_factor<<<1, 32, 0, s>>>(Fpart, nblocks, LF, E, eigE, st);
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* Wb, const double* V, const double* Hr,
+                          const double* s_a, const double* s_b, const double* LF, double* Gamma, double* G,
+                          cudaStream_t s) {
+    if (!sc.n) return;
+    if (sc.P == 8) k_camera_border<8><<<cdiv(sc.n, 4), 128, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    else k_camera_border<9><<<cdiv(sc.n, 4), 128, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_fill(int P, double* Z, long long ld, int N, int Npad, const double* D, const double* s_a, const double* G,
+                 int add_gg, cudaStream_t s) {
+    const long long T = Npad / 64;
+    const long long tiles = T * (T + 1) / 2;
+    if (!tiles) return;
+    if (P == 8) k_fill<8><<<(unsigned)tiles, 256, 0, s>>>(Z, ld, N, Npad, D, s_a, G, add_gg);
+    else k_fill<9><<<(unsigned)tiles, 256, 0, s>>>(Z, ld, N, Npad, D, s_a, G, add_gg);
+    SFM_LAUNCH_CHECK();
+}
+
+static int bits_for64(unsigned long long v) { int b = 1; while (b < 64 && (1ULL << b) <= v) ++b; return b; }
+
+// Builds the sorted pair list and the block segments; returns #pairs and
+// #segments through the handle-owned PairDev.
+void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace& ws, cudaStream_t s) {
+    const int m = sc.m;
+    pd.cnt = (long long*)pd.buf_cnt.get(sizeof(long long) * (size_t)(m + 1));
+    pd.off = (long long*)pd.buf_off.get(sizeof(long long) * (size_t)(m + 1));
+    k_pair_count<<<cdiv(m + 1, 256), 256, 0, s>>>(ix.off_pt, m, pd.cnt);
+    SFM_LAUNCH_CHECK();
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, pd.cnt, pd.off, m + 1, s);
+    SFM_CUDA(cub::DeviceScan::ExclusiveSum(ws.get_tmp(bytes), bytes, pd.cnt, pd.off, m + 1, s));
+    long long npairs = 0;
+    SFM_CUDA(cudaMemcpyAsync(&npairs, pd.off + m, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    SFM_CUDA(cudaStreamSynchronize(s));
+    pd.npairs = npairs;
+    const size_t np = (size_t)npairs;
+    unsigned int* k0 = (unsigned int*)pd.buf_k0.get(4 * np + 16);
+    unsigned int* k1 = (unsigned int*)pd.buf_k1.get(4 * np + 16);
+    unsigned long long* v0 = (unsigned long long*)pd.buf_v0.get(8 * np + 16);
+    unsigned long long* v1 = (unsigned long long*)pd.buf_v1.get(8 * np + 16);
+    if (m) k_pair_gen<<<cdiv(m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, sc.oc, ix.pos_cam, m, sc.n, pd.off, k0, v0);
+    SFM_LAUNCH_CHECK();
+    const int kbits = bits_for64((unsigned long long)sc.n * (unsigned long long)sc.n);
+    cub::DoubleBuffer<unsigned int> dk(k0, k1);
+    cub::DoubleBuffer<unsigned long long> dv(v0, v1);
+    size_t sb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sb, dk, dv, (int)np, 0, kbits, s);
+    SFM_CUDA(cub::DeviceRadixSort::SortPairs(ws.get_tmp(sb), sb, dk, dv, (int)np, 0, kbits, s));
+    pd.keys = dk.Current();
+    pd.vals = dv.Current();
+    // run-length encode the sorted keys into block segments
+    unsigned int* ukeys = (unsigned int*)pd.buf_ukeys.get(4 * np + 16);
+    int* counts = (int*)pd.buf_counts.get(4 * np + 16);
+    int* nruns = (int*)pd.buf_nruns.get(16);
+    size_t rb = 0;
+    cub::DeviceRunLengthEncode::Encode(nullptr, rb, pd.keys, ukeys, counts, nruns, (int)np, s);
+    SFM_CUDA(cub::DeviceRunLengthEncode::Encode(ws.get_tmp(rb), rb, pd.keys, ukeys, counts, nruns, (int)np, s));
+    int nseg = 0;
+    SFM_CUDA(cudaMemcpyAsync(&nseg, nruns, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SFM_CUDA(cudaStreamSynchronize(s));
+    pd.nseg = nseg;
+    pd.ukeys = ukeys;
+    long long* seg_off = (long long*)pd.buf_seg.get(8 * ((size_t)nseg + 1) + 16);
+    // widen counts to int64 offsets
+    size_t eb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, eb, counts, seg_off, nseg + 1, s);
+    // counts[nseg] must be 0 for the trailing total: set it
+    SFM_CUDA(cudaMemsetAsync(counts + nseg, 0, sizeof(int), s));
+    SFM_CUDA(cub::DeviceScan::ExclusiveSum(ws.get_tmp(eb), eb, counts, seg_off, nseg + 1, s));
+    pd.seg_off = seg_off;
+}
+
+void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, cudaStream_t s) {
+    if (!pd.nseg) return;
+    const unsigned blocks = cdiv(pd.nseg, 8);
+    if (P == 8) k_pair_reduce<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
+    else k_pair_reduce<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
+    SFM_LAUNCH_CHECK();
+}
+
+}  // namespace sfm

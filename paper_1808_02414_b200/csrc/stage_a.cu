@@ -1,0 +1,431 @@
+// Stage (a) + (c): validation, observation index, analytic Jacobian,
+// per-camera / per-point Fisher reductions, gauge-nullspace rotation blocks
+// and Jacobi conditioning scales.
+//
+// Compiled with --fmad=false: these kernels follow the CPU restatement
+// (oracle/) operation for operation, so the Jacobian, the nullspace and the
+// unconditioned Fisher blocks are bit-exact against it.  Reductions run in
+// ascending observation order per camera / per point, exactly like the
+// reference (src/covariance.cpp:57-71, src/nullspace.cpp:40-50), which also
+// makes every result bitwise reproducible run to run.
+#include "common.cuh"
+#include "detmath.cuh"
+#include "kernels.cuh"
+
+#include <cub/cub.cuh>
+
+namespace sfm {
+
+__global__ void k_status_init(Status* st) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        st->cam_bad = INT_MAX; st->pt_bad = INT_MAX; st->obs_bad = LLONG_MAX; st->dup = 0;
+        st->cam_count_bad = INT_MAX; st->pt_count_bad = INT_MAX; st->jac_bad = INT_MAX;
+        st->fisher_bad = INT_MAX; st->rot_bad = INT_MAX; st->pt_sing_bad = INT_MAX;
+        st->border_bad = 0; st->chol_bad = INT_MAX; st->nflag = 0; st->pad = 0;
+    }
+}
+
+// ---- validation: src/scene.cpp:19-78 -------------------------------------------
+__device__ __forceinline__ bool finite_d(double v) { return isfinite(v); }
+
+__global__ void k_validate_cams(const double* cams, int n, int P, Status* st) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* c = cams + (size_t)P * i;
+    bool fin = true;
+    for (int p = 0; p < P; ++p) fin = fin && finite_d(c[p]);
+    int code = 0;
+    if (!fin) code = 1;
+    else if (!(c[6] > 0.0)) code = 2;
+    if (code) atomicMin(&st->cam_bad, i * 4 + code);
+}
+
+__global__ void k_validate_pts(const double* pts, int m, Status* st) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const double* X = pts + 3 * (size_t)j;
+    if (!(finite_d(X[0]) && finite_d(X[1]) && finite_d(X[2]))) atomicMin(&st->pt_bad, j);
+}
+
+// check_sigma = 1: full scene validation; 0: only index ranges (stage APIs
+// that, like the reference functions, do not validate).
+__global__ void k_validate_obs(const int* oc, const int* op, const double* u, const double* sigma, int t_count,
+                               int n, int m, int check_sigma, Status* st, int* cam_cnt, int* pt_cnt) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= t_count) return;
+    const int ci = oc[t], pj = op[t];
+    int code = 0;
+    if (ci < 0 || ci >= n) code = 1;
+    else if (pj < 0 || pj >= m) code = 2;
+    else if (check_sigma) {
+        double s00 = 1.0, s01 = 0.0, s10 = 0.0, s11 = 1.0;
+        if (sigma) { s00 = sigma[4 * (size_t)t]; s01 = sigma[4 * (size_t)t + 1]; s10 = sigma[4 * (size_t)t + 2]; s11 = sigma[4 * (size_t)t + 3]; }
+        const bool ufin = !u || (finite_d(u[2 * (size_t)t]) && finite_d(u[2 * (size_t)t + 1]));
+        if (!ufin || !finite_d(s00) || !finite_d(s01) || !finite_d(s10) || !finite_d(s11)) code = 3;
+        else {
+            const double scale = fmax(fmax(fmax(fabs(s00), fabs(s11)), fabs(s01)), 1e-300);
+            if (fabs(s01 - s10) > 1e-12 * scale) code = 4;
+            else {
+                const double det = s00 * s11 - s01 * s10;
+                if (!(s00 > 0.0) || !(det > 0.0)) code = 5;
+            }
+        }
+    }
+    if (code) atomicMin(&st->obs_bad, (long long)t * 8 + code);
+    if (code == 0 || code > 2) {
+        atomicAdd(&cam_cnt[ci], 1);
+        atomicAdd(&pt_cnt[pj], 1);
+    }
+}
+
+__global__ void k_iota(int* v, int count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) v[i] = i;
+}
+
+__global__ void k_pos_scatter(const int* idx, int count, int* pos) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < count) pos[idx[k]] = k;
+}
+
+// Duplicate (camera, point) pairs are repeated cameras inside one point's
+// observation list; >= 4 per camera, >= 2 per point.
+__global__ void k_structure_check(const int* off_cam, int n, const int* off_pt, const int* idx_pt, const int* oc,
+                                  int m, Status* st) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < m) {
+        const int b = off_pt[g], e = off_pt[g + 1];
+        if (e - b < 2) atomicMin(&st->pt_count_bad, g);
+        for (int a = b; a < e; ++a)
+            for (int c = a + 1; c < e; ++c)
+                if (oc[idx_pt[a]] == oc[idx_pt[c]]) st->dup = 1;
+    }
+    if (g < n && off_cam[g + 1] - off_cam[g] < 4) atomicMin(&st->cam_count_bad, g);
+}
+
+// ---- Jacobian: src/projection.cpp:41-59, 80-105 ----------------------------
+__global__ void k_camera_rot(const double* cams, int n, int P, double* R) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    rotation_matrix(cams + (size_t)P * i, R + 9 * (size_t)i);
+}
+
+// One thread per observation; writes the AoS record [jc | jp | W].  W is the
+// explicit 2x2 inverse of sigma (covariance.cpp:20-29).
+template <int P>
+__global__ void k_jacobian(const double* cams, const double* Rc, const double* pts, const int* oc, const int* op,
+                           const double* sigma, int t_count, double* rec, Status* st) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= t_count) return;
+    const int ci = oc[t], pj = op[t];
+    double jc[2 * P], jp[6], depth;
+    const bool ok = observation_jacobian<P>(cams + (size_t)P * ci, Rc + 9 * (size_t)ci, pts + 3 * (size_t)pj, jc, jp, &depth);
+    if (!ok) atomicMin(&st->jac_bad, t);
+    double s00 = 1.0, s01 = 0.0, s10 = 0.0, s11 = 1.0;
+    if (sigma) { s00 = sigma[4 * (size_t)t]; s01 = sigma[4 * (size_t)t + 1]; s10 = sigma[4 * (size_t)t + 2]; s11 = sigma[4 * (size_t)t + 3]; }
+    const double det = s00 * s11 - s01 * s10;
+    if (!(s00 > 0.0) || !(det > 0.0)) atomicMin(&st->fisher_bad, t);
+    double* r = rec + (size_t)t * kRec;
+    for (int k = 0; k < 2 * P; ++k) r[Layout<P>::JC + k] = jc[k];
+    for (int k = 0; k < 6; ++k) r[Layout<P>::JP + k] = jp[k];
+    r[Layout<P>::WO + 0] = s11 / det;
+    r[Layout<P>::WO + 1] = -s01 / det;
+    r[Layout<P>::WO + 2] = -s10 / det;
+    r[Layout<P>::WO + 3] = s00 / det;
+}
+
+// Depth of one observation (error message path only).
+__global__ void k_depth_of(const double* cams, const double* Rc, const double* pts, const int* oc, const int* op,
+                           int P, int t, double* out) {
+    const int ci = oc[t], pj = op[t];
+    const double* C = cams + (size_t)P * ci + 3;
+    const double* R = Rc + 9 * (size_t)ci;
+    const double* X = pts + 3 * (size_t)pj;
+    const double w[3] = {X[0] - C[0], X[1] - C[1], X[2] - C[2]};
+    *out = (R[6] * w[0] + R[7] * w[1]) + R[8] * w[2];
+}
+
+// ---- per-camera reduction (warp per camera) -----------------------------------
+// D_i = Σ (J_cᵀW)J_c (covariance.cpp:57-63) and the rotation normal equations
+// normal = Σ d_rᵀd_r, rhs = Σ d_rᵀ(−(d_C[C]x + d_X[X]x)) (nullspace.cpp:40-50),
+// ascending observation order; lane-owned entries keep each sum sequential.
+// Then H_r = eig-inverse(normal)·rhs (nullspace.cpp:52-61) and s_a = 1/sqrt(diag D).
+template <int P>
+__global__ void k_camera_reduce(const int* off_cam, const int* idx_cam, const double* rec, const double* cams,
+                                const double* pts, const int* op, int n, double* D, double* Hr, double* s_a,
+                                unsigned char* flags, Status* st) {
+    constexpr int NE = P * P + 18;
+    constexpr int NS = (NE + 31) / 32;
+    __shared__ double sh[4][NE];
+    const int wib = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * 4 + wib;
+    if (i >= n) return;
+    const double* cam = cams + (size_t)P * i;
+    double hc[9];
+    skew(cam + 3, hc);
+    double acc[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+    const int b = off_cam[i], e = off_cam[i + 1];
+    for (int k = b; k < e; ++k) {
+        const int t = idx_cam[k];
+        const double* r = rec + (size_t)t * kRec;
+        const double* jc = r + Layout<P>::JC;
+        const double* jp = r + Layout<P>::JP;
+        const double* W = r + Layout<P>::WO;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            const int en = lane + 32 * s;
+            if (en >= NE) break;
+            if (en < P * P) {
+                const int p = en / P, q = en % P;
+                const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
+                const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
+                acc[s] += t0 * jc[q] + t1 * jc[P + q];
+            } else if (en < P * P + 9) {
+                const int p = (en - P * P) / 3, q = (en - P * P) % 3;
+                acc[s] += jc[p] * jc[q] + jc[P + p] * jc[P + q];
+            } else {
+                const int p = (en - P * P - 9) / 3, q = (en - P * P - 9) % 3;
+                const double* X = pts + 3 * (size_t)op[t];
+                double hx[9];
+                skew(X, hx);
+                double tg[2];
+                for (int ii = 0; ii < 2; ++ii) {
+                    const double a = (jc[P * ii + 3] * hc[0 + q] + jc[P * ii + 4] * hc[3 + q]) + jc[P * ii + 5] * hc[6 + q];
+                    const double bb = (jp[3 * ii + 0] * hx[0 + q] + jp[3 * ii + 1] * hx[3 + q]) + jp[3 * ii + 2] * hx[6 + q];
+                    tg[ii] = -(a + bb);
+                }
+                acc[s] += jc[p] * tg[0] + jc[P + p] * tg[1];
+            }
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const int en = lane + 32 * s;
+        if (en < NE) sh[wib][en] = acc[s];
+    }
+    __syncwarp();
+    for (int en = lane; en < P * P; en += 32) D[(size_t)P * P * i + en] = sh[wib][en];
+    if (lane < P) {
+        const double d = sh[wib][lane * (P + 1)];
+        if (d > 0.0) s_a[(size_t)P * i + lane] = 1.0 / sqrt(d);
+        else { s_a[(size_t)P * i + lane] = 1.0; flags[(size_t)P * i + lane] = 1; atomicAdd(&st->nflag, 1); }
+    }
+    if (lane == 0) {
+        double inv[9], hr[9];
+        if (!eig_inverse3(&sh[wib][P * P], kRotationCondTol, inv)) {
+            atomicMin(&st->rot_bad, i);
+            for (int k = 0; k < 9; ++k) Hr[9 * (size_t)i + k] = 0.0;
+        } else {
+            mul3(inv, &sh[wib][P * P + 9], hr);
+            for (int k = 0; k < 9; ++k) Hr[9 * (size_t)i + k] = hr[k];
+        }
+    }
+}
+
+// ---- per-point reduction: A_j = Σ (J_pᵀW)J_p (covariance.cpp:64-71) ---------
+template <int P>
+__global__ void k_point_reduce(const int* off_pt, const int* idx_pt, const double* rec, int m, int n, double* A,
+                               double* s_a, unsigned char* flags, Status* st) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    double a[9];
+    for (int k = 0; k < 9; ++k) a[k] = 0.0;
+    for (int k = off_pt[j]; k < off_pt[j + 1]; ++k) {
+        const double* r = rec + (size_t)idx_pt[k] * kRec;
+        const double* jp = r + Layout<P>::JP;
+        const double* W = r + Layout<P>::WO;
+        for (int p = 0; p < 3; ++p) {
+            const double t0 = jp[p] * W[0] + jp[3 + p] * W[2];
+            const double t1 = jp[p] * W[1] + jp[3 + p] * W[3];
+            for (int q = 0; q < 3; ++q) a[3 * p + q] += t0 * jp[q] + t1 * jp[3 + q];
+        }
+    }
+    for (int k = 0; k < 9; ++k) A[9 * (size_t)j + k] = a[k];
+    const size_t base = (size_t)P * n + 3 * (size_t)j;
+    for (int p = 0; p < 3; ++p) {
+        const double d = a[4 * p];
+        if (d > 0.0) s_a[base + p] = 1.0 / sqrt(d);
+        else { s_a[base + p] = 1.0; flags[base + p] = 1; atomicAdd(&st->nflag, 1); }
+    }
+}
+
+// ---- border column scales: s_b[l] = 1/‖s_a ∘ h_l‖ (covariance.cpp:110-114) ----
+// Rows of H: camera r-rows (H_r in columns 3..5), camera C-rows [I|[C]x|C],
+// zero intrinsic rows, point rows [I|[X]x|X].  Deterministic two-level sum.
+template <int P>
+__global__ void k_border_partial(const double* cams, const double* Hr, const double* pts, const double* s_a, int n,
+                                 int m, double* partial) {
+    __shared__ double red[256][7];
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    if (g < n + m) {
+        const bool is_cam = g < n;
+        const double* X = is_cam ? cams + (size_t)P * g + 3 : pts + 3 * (size_t)(g - n);
+        const size_t row0 = is_cam ? (size_t)P * g + 3 : (size_t)P * n + 3 * (size_t)(g - n);
+        double sx[9];
+        skew(X, sx);
+        for (int a = 0; a < 3; ++a) {
+            const double s = s_a[row0 + a];
+            double h[7] = {0, 0, 0, 0, 0, 0, 0};
+            h[a] = 1.0;
+            h[3] = sx[3 * a]; h[4] = sx[3 * a + 1]; h[5] = sx[3 * a + 2];
+            h[6] = X[a];
+            for (int l = 0; l < 7; ++l) { const double v = s * h[l]; acc[l] += v * v; }
+        }
+        if (is_cam) {
+            for (int a = 0; a < 3; ++a) {
+                const double s = s_a[(size_t)P * g + a];
+                for (int b = 0; b < 3; ++b) { const double v = s * Hr[9 * (size_t)g + 3 * a + b]; acc[3 + b] += v * v; }
+            }
+        }
+    }
+    for (int l = 0; l < 7; ++l) red[threadIdx.x][l] = acc[l];
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int l = 0; l < 7; ++l) red[threadIdx.x][l] += red[threadIdx.x + w][l];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int l = 0; l < 7; ++l) partial[7 * (size_t)blockIdx.x + l] = red[0][l];
+}
+
+__global__ void k_border_final(const double* partial, int nblocks, double* s_b) {
+    const int l = threadIdx.x;
+    if (l >= 7) return;
+    double ss = 0.0;
+    for (int b = 0; b < nblocks; ++b) ss += partial[7 * (size_t)b + l];
+    const double norm = sqrt(ss);
+    s_b[l] = norm > 0.0 ? 1.0 / norm : 1.0;
+}
+
+// ---- full H (nullspace API) ---------------------------------------------------
+template <int P>
+__global__ void k_write_h(const double* cams, const double* Hr, const double* pts, int n, int m, double* H) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n + m) return;
+    const bool is_cam = g < n;
+    const double* X = is_cam ? cams + (size_t)P * g + 3 : pts + 3 * (size_t)(g - n);
+    const size_t row0 = is_cam ? (size_t)P * g + 3 : (size_t)P * n + 3 * (size_t)(g - n);
+    double sx[9];
+    skew(X, sx);
+    for (int a = 0; a < 3; ++a) {
+        double* h = H + (row0 + a) * 7;
+        for (int l = 0; l < 7; ++l) h[l] = 0.0;
+        h[a] = 1.0;
+        h[3] = sx[3 * a]; h[4] = sx[3 * a + 1]; h[5] = sx[3 * a + 2];
+        h[6] = X[a];
+    }
+    if (is_cam) {
+        for (int a = 0; a < 3; ++a) {
+            double* h = H + ((size_t)P * g + a) * 7;
+            for (int l = 0; l < 7; ++l) h[l] = 0.0;
+            for (int b = 0; b < 3; ++b) h[3 + b] = Hr[9 * (size_t)g + 3 * a + b];
+        }
+        for (int a = 6; a < P; ++a) {
+            double* h = H + ((size_t)P * g + a) * 7;
+            for (int l = 0; l < 7; ++l) h[l] = 0.0;
+        }
+    }
+}
+
+// ---- host launchers ------------------------------------------------------------
+void launch_status_init(Status* st, cudaStream_t s) { k_status_init<<<1, 1, 0, s>>>(st); SFM_LAUNCH_CHECK(); }
+
+void launch_validate(const SceneDev& sc, int check_sigma, Status* st, int* cam_cnt, int* pt_cnt, cudaStream_t s) {
+    SFM_CUDA(cudaMemsetAsync(cam_cnt, 0, sizeof(int) * (size_t)(sc.n + 1), s));
+    SFM_CUDA(cudaMemsetAsync(pt_cnt, 0, sizeof(int) * (size_t)(sc.m + 1), s));
+    if (check_sigma) {
+        if (sc.n) k_validate_cams<<<cdiv(sc.n, 256), 256, 0, s>>>(sc.cams, sc.n, sc.P, st);
+        if (sc.m) k_validate_pts<<<cdiv(sc.m, 256), 256, 0, s>>>(sc.pts, sc.m, st);
+    }
+    if (sc.t) k_validate_obs<<<cdiv(sc.t, 256), 256, 0, s>>>(sc.oc, sc.op, sc.u, sc.sigma, sc.t, sc.n, sc.m, check_sigma, st, cam_cnt, pt_cnt);
+    SFM_LAUNCH_CHECK();
+}
+
+static int bits_for(int v) { int b = 1; while ((1LL << b) <= v) ++b; return b; }
+
+void launch_build_index(const SceneDev& sc, const int* cam_cnt, const int* pt_cnt, IndexDev& ix, Workspace& ws,
+                        cudaStream_t s) {
+    const int t = sc.t;
+    // offsets = exclusive scan of counts (count arrays carry one extra zero slot)
+    size_t b1 = 0, b2 = 0, b3 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b1, cam_cnt, ix.off_cam, sc.n + 1, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, pt_cnt, ix.off_pt, sc.m + 1, s);
+    cub::DeviceRadixSort::SortPairs(nullptr, b3, (const int*)nullptr, (int*)nullptr, (const int*)nullptr, (int*)nullptr, t, 0, 32, s);
+    size_t bytes = b1 > b2 ? b1 : b2;
+    if (b3 > bytes) bytes = b3;
+    void* tmp = ws.get_tmp(bytes);
+    SFM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, b1, cam_cnt, ix.off_cam, sc.n + 1, s));
+    SFM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, b2, pt_cnt, ix.off_pt, sc.m + 1, s));
+    if (t == 0) return;
+    int* iota = ix.pos_cam;  // scratch before pos is filled
+    k_iota<<<cdiv(t, 256), 256, 0, s>>>(iota, t);
+    SFM_LAUNCH_CHECK();
+    size_t bb = bytes;
+    SFM_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bb, sc.oc, ix.key_scratch, iota, ix.idx_cam, t, 0, bits_for(sc.n), s));
+    bb = bytes;
+    SFM_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bb, sc.op, ix.key_scratch, iota, ix.idx_pt, t, 0, bits_for(sc.m), s));
+    k_pos_scatter<<<cdiv(t, 256), 256, 0, s>>>(ix.idx_cam, t, ix.pos_cam);
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_structure_check(const SceneDev& sc, const IndexDev& ix, Status* st, cudaStream_t s) {
+    const int g = sc.n > sc.m ? sc.n : sc.m;
+    if (g) k_structure_check<<<cdiv(g, 256), 256, 0, s>>>(ix.off_cam, sc.n, ix.off_pt, ix.idx_pt, sc.oc, sc.m, st);
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_jacobian(const SceneDev& sc, double* R, double* rec, Status* st, cudaStream_t s) {
+    if (sc.n) k_camera_rot<<<cdiv(sc.n, 128), 128, 0, s>>>(sc.cams, sc.n, sc.P, R);
+    if (sc.t) {
+        if (sc.P == 8) k_jacobian<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, sc.sigma, sc.t, rec, st);
+        else k_jacobian<9><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, sc.sigma, sc.t, rec, st);
+    }
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_depth_of(const SceneDev& sc, const double* R, int t, double* out, cudaStream_t s) {
+    k_depth_of<<<1, 1, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, sc.P, t, out);
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_reductions(const SceneDev& sc, const IndexDev& ix, const double* rec, double* D, double* Hr, double* A,
+                       double* s_a, unsigned char* flags, Status* st, cudaStream_t s) {
+    const size_t ncols = (size_t)sc.P * sc.n + 3 * (size_t)sc.m;
+    SFM_CUDA(cudaMemsetAsync(flags, 0, ncols, s));
+    if (sc.n) {
+        if (sc.P == 8) k_camera_reduce<8><<<cdiv(sc.n, 4), 128, 0, s>>>(ix.off_cam, ix.idx_cam, rec, sc.cams, sc.pts, sc.op, sc.n, D, Hr, s_a, flags, st);
+        else k_camera_reduce<9><<<cdiv(sc.n, 4), 128, 0, s>>>(ix.off_cam, ix.idx_cam, rec, sc.cams, sc.pts, sc.op, sc.n, D, Hr, s_a, flags, st);
+    }
+    if (sc.m) {
+        if (sc.P == 8) k_point_reduce<8><<<cdiv(sc.m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, rec, sc.m, sc.n, A, s_a, flags, st);
+        else k_point_reduce<9><<<cdiv(sc.m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, rec, sc.m, sc.n, A, s_a, flags, st);
+    }
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_border_scales(const SceneDev& sc, const double* Hr, const double* s_a, double* partial, double* s_b,
+                          cudaStream_t s) {
+    const int g = sc.n + sc.m;
+    const int nb = (int)cdiv(g > 0 ? g : 1, 256);
+    if (sc.P == 8) k_border_partial<8><<<nb, 256, 0, s>>>(sc.cams, Hr, sc.pts, s_a, sc.n, sc.m, partial);
+    else k_border_partial<9><<<nb, 256, 0, s>>>(sc.cams, Hr, sc.pts, s_a, sc.n, sc.m, partial);
+    k_border_final<<<1, 32, 0, s>>>(partial, nb, s_b);
+    SFM_LAUNCH_CHECK();
+}
+
+int border_partial_blocks(int n, int m) { const int g = n + m; return (int)cdiv(g > 0 ? g : 1, 256); }
+
+void launch_write_h(const SceneDev& sc, const double* Hr, double* H, cudaStream_t s) {
+    const int g = sc.n + sc.m;
+    if (!g) return;
+    if (sc.P == 8) k_write_h<8><<<cdiv(g, 128), 128, 0, s>>>(sc.cams, Hr, sc.pts, sc.n, sc.m, H);
+    else k_write_h<9><<<cdiv(g, 128), 128, 0, s>>>(sc.cams, Hr, sc.pts, sc.n, sc.m, H);
+    SFM_LAUNCH_CHECK();
+}
+
+}  // namespace sfm

@@ -1,0 +1,376 @@
+"""Python mirror of the reference ``sfmcov`` operator API over the B200 C ABI.
+
+Same names, argument meaning and error behaviour as the reference free
+functions in namespace ``sfmcov`` (include/sfmcov/*.hpp); every call runs on
+the GPU through ``libsfmcov_b200.so`` (include/sfmcov_b200.h).  Scenes are
+structure-of-arrays numpy buffers instead of the reference's Eigen AoS.
+
+    reference (C++)                         this module
+    ------------------------------------    -----------------------------------
+    Reconstruction (types.hpp:52-66)        Reconstruction
+    build_observation_index (scene.cpp:80)  build_observation_index
+    assemble_jacobian (projection.hpp:54)   assemble_jacobian
+    gauge_nullspace (nullspace.hpp:33)      gauge_nullspace
+    build_fisher_blocks + condition_columns build_fisher_blocks
+      (covariance.hpp:80-86)
+    schur_reduce (covariance.hpp:94-95)     schur_reduce
+    compute_covariance (covariance.hpp:110) compute_covariance
+    Error / ErrorKind (error.hpp)           Error / ErrorKind
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import List, Optional
+
+import numpy as np
+
+from . import _native as N
+
+K_GAUGE = 7
+
+
+class ErrorKind(IntEnum):
+    io = 1
+    parse = 2
+    invariant = 3
+    degenerate = 4
+    dimension = 5
+    size_guard = 6
+    device = 7
+
+
+class Error(RuntimeError):
+    """sfmcov::Error: ``str(e)`` is "stage: message" like Error::what()."""
+
+    def __init__(self, kind: int, stage: str, what: str):
+        super().__init__(what)
+        self.kind = ErrorKind(kind)
+        self.stage = stage
+
+
+def _raise(code: int, err: N.ErrorStruct):
+    if code:
+        raise Error(code, err.stage.decode(), err.message.decode())
+
+
+@dataclass
+class Reconstruction:
+    """Scene of cameras, points and observations (SoA).
+
+    cams: (n, P) float64, P = 8 (r, C, c, k) or 9 (r, C, f, k1, k2)
+    pts: (m, 3); obs_cam / obs_pt: (t,) int32; obs_u: (t, 2);
+    obs_sigma: (t, 2, 2) observation covariance or None (= identity).
+    """
+
+    cams: np.ndarray
+    pts: np.ndarray
+    obs_cam: np.ndarray
+    obs_pt: np.ndarray
+    obs_u: Optional[np.ndarray] = None
+    obs_sigma: Optional[np.ndarray] = None
+
+    def __post_init__(self):
+        self.cams = np.ascontiguousarray(self.cams, dtype=np.float64)
+        self.pts = np.ascontiguousarray(self.pts, dtype=np.float64).reshape(-1, 3)
+        self.obs_cam = np.ascontiguousarray(self.obs_cam, dtype=np.int32)
+        self.obs_pt = np.ascontiguousarray(self.obs_pt, dtype=np.int32)
+        if self.cams.ndim != 2:
+            self.cams = self.cams.reshape(-1, 8)
+        if self.obs_u is not None:
+            self.obs_u = np.ascontiguousarray(self.obs_u, dtype=np.float64).reshape(-1, 2)
+        if self.obs_sigma is not None:
+            self.obs_sigma = np.ascontiguousarray(self.obs_sigma, dtype=np.float64).reshape(-1, 2, 2)
+
+    @property
+    def cam_params(self) -> int:
+        return int(self.cams.shape[1])
+
+    def num_cameras(self) -> int:
+        return int(self.cams.shape[0])
+
+    def num_points(self) -> int:
+        return int(self.pts.shape[0])
+
+    def num_observations(self) -> int:
+        return int(self.obs_cam.shape[0])
+
+    def num_parameters(self) -> int:
+        return self.cam_params * self.num_cameras() + 3 * self.num_points()
+
+    def copy(self) -> "Reconstruction":
+        return Reconstruction(self.cams.copy(), self.pts.copy(), self.obs_cam.copy(), self.obs_pt.copy(),
+                              None if self.obs_u is None else self.obs_u.copy(),
+                              None if self.obs_sigma is None else self.obs_sigma.copy())
+
+    def c_struct(self) -> N.Scene:
+        s = N.Scene()
+        s.n_cams, s.n_pts, s.n_obs = self.num_cameras(), self.num_points(), self.num_observations()
+        s.cam_params = self.cam_params
+        s.cams, s.pts = N.ptr(self.cams), N.ptr(self.pts)
+        s.obs_cam, s.obs_pt = N.ptr(self.obs_cam), N.ptr(self.obs_pt)
+        s.obs_u = N.ptr(self.obs_u)
+        s.obs_sigma = N.ptr(self.obs_sigma)
+        return s
+
+    # the reference validates inside compute_covariance; exposed for parity
+    def validate(self) -> None:
+        build_observation_index(self)
+
+
+@dataclass
+class CovarianceOptions:
+    threads: int = 0  # accepted, ignored: results never depend on it
+    point_covariances: bool = False
+    camera_cross_covariances: bool = False
+
+
+@dataclass
+class CovarianceDiagnostics:
+    scale_min: float = 0.0
+    scale_max: float = 0.0
+    flagged_columns: List[int] = field(default_factory=list)
+    min_pivot: float = 0.0
+    max_pivot: float = 0.0
+    inertia_positive: int = 0
+    inertia_negative: int = 0
+    negative_eigenvalue_warnings: int = 0
+    peak_dense_bytes: int = 0
+    largest_dense_dim: int = 0
+
+
+@dataclass
+class CovarianceResult:
+    camera_cov: np.ndarray  # (n, P, P)
+    diagnostics: CovarianceDiagnostics
+
+
+@dataclass
+class ObservationIndex:
+    off_cam: np.ndarray
+    idx_cam: np.ndarray
+    off_pt: np.ndarray
+    idx_pt: np.ndarray
+
+    @property
+    def by_camera(self):
+        return [self.idx_cam[self.off_cam[i]:self.off_cam[i + 1]] for i in range(len(self.off_cam) - 1)]
+
+    @property
+    def by_point(self):
+        return [self.idx_pt[self.off_pt[j]:self.off_pt[j + 1]] for j in range(len(self.off_pt) - 1)]
+
+
+@dataclass
+class SparseJacobian:
+    cam_index: np.ndarray
+    point_index: np.ndarray
+    cam_blocks: np.ndarray    # (t, 2, P)
+    point_blocks: np.ndarray  # (t, 2, 3)
+    n_cams: int
+    n_pts: int
+
+    def cols(self) -> int:
+        return self.cam_blocks.shape[2] * self.n_cams + 3 * self.n_pts
+
+    def dense(self) -> np.ndarray:
+        P = self.cam_blocks.shape[2]
+        t = self.cam_blocks.shape[0]
+        J = np.zeros((2 * t, self.cols()))
+        for k in range(t):
+            ci, pj = self.cam_index[k], self.point_index[k]
+            J[2 * k:2 * k + 2, P * ci:P * ci + P] = self.cam_blocks[k]
+            c0 = P * self.n_cams + 3 * pj
+            J[2 * k:2 * k + 2, c0:c0 + 3] = self.point_blocks[k]
+        return J
+
+    def max_abs(self) -> float:
+        return float(max(np.abs(self.cam_blocks).max(initial=0.0), np.abs(self.point_blocks).max(initial=0.0)))
+
+
+@dataclass
+class FisherBlocks:
+    cam_blocks: np.ndarray    # (n, P, P)  M[P_i, P_i]
+    point_blocks: np.ndarray  # (m, 3, 3)  M[X_j, X_j]
+    couplings: np.ndarray     # (t, P, 3)  M[P_i, X_j], observation order
+    s_a: np.ndarray
+    s_b: np.ndarray
+    flagged: List[int]
+
+
+class Engine:
+    """One CUDA handle (device, stream, workspace).  Thread-safe."""
+
+    def __init__(self, device: int = 0):
+        lib = N.cuda_lib()
+        err = N.ErrorStruct()
+        h = lib.sfmcov_cuda_create(device, C.byref(err))
+        if not h:
+            raise Error(err.kind or ErrorKind.device, err.stage.decode() or "device", err.message.decode())
+        self._h = h
+        self._lib = lib
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.sfmcov_cuda_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def stream(self) -> int:
+        return self._lib.sfmcov_cuda_stream(self._h) or 0
+
+    def set_profiling(self, on: bool):
+        self._lib.sfmcov_cuda_set_profiling(self._h, 1 if on else 0)
+
+    def stage_times(self) -> dict:
+        buf = (C.c_double * 16)()
+        k = self._lib.sfmcov_cuda_last_stage_times(self._h, buf, 16)
+        return {self._lib.sfmcov_cuda_stage_name(i).decode(): buf[i] for i in range(k)}
+
+    def counts(self) -> dict:
+        buf = (C.c_int64 * 9)()
+        self._lib.sfmcov_cuda_last_counts(self._h, buf, 9)
+        keys = ["obs_pairs", "nnz_blocks", "N", "Npad", "n_obs", "n_pts", "n_cams", "P", "dense_launches"]
+        return dict(zip(keys, [int(v) for v in buf]))
+
+    # ---- pipeline -------------------------------------------------------------
+    def compute_covariance(self, rec: Reconstruction, options: Optional[CovarianceOptions] = None) -> CovarianceResult:
+        options = options or CovarianceOptions()
+        P, n = rec.cam_params, rec.num_cameras()
+        out = np.empty((n, P, P))
+        flagged = np.zeros(max(1, rec.num_parameters()), dtype=np.int64)
+        diag = N.Diagnostics()
+        diag.flagged = flagged.ctypes.data_as(N.c_int64_p)
+        diag.flagged_capacity = flagged.size
+        opts = N.Options(options.threads, int(options.point_covariances), int(options.camera_cross_covariances), 0)
+        err = N.ErrorStruct()
+        sc = rec.c_struct()
+        code = self._lib.sfmcov_cuda_compute_covariance(self._h, C.byref(sc), C.byref(opts), out.ctypes.data,
+                                                        C.byref(diag), C.byref(err))
+        _raise(code, err)
+        d = CovarianceDiagnostics(diag.scale_min, diag.scale_max, [int(v) for v in flagged[:diag.n_flagged]],
+                                  diag.min_pivot, diag.max_pivot, diag.inertia_positive, diag.inertia_negative,
+                                  diag.negative_eigenvalue_warnings, diag.peak_dense_bytes, diag.largest_dense_dim)
+        return CovarianceResult(out, d)
+
+    def build_observation_index(self, rec: Reconstruction) -> ObservationIndex:
+        n, m, t = rec.num_cameras(), rec.num_points(), rec.num_observations()
+        oc, op = np.empty(n + 1, np.int64), np.empty(m + 1, np.int64)
+        ic, ip = np.empty(max(t, 1), np.int32), np.empty(max(t, 1), np.int32)
+        err = N.ErrorStruct()
+        sc = rec.c_struct()
+        code = self._lib.sfmcov_cuda_observation_index(self._h, C.byref(sc), oc.ctypes.data, ic.ctypes.data,
+                                                        op.ctypes.data, ip.ctypes.data, C.byref(err))
+        _raise(code, err)
+        return ObservationIndex(oc, ic[:t], op, ip[:t])
+
+    def assemble_jacobian(self, rec: Reconstruction) -> SparseJacobian:
+        P, t = rec.cam_params, rec.num_observations()
+        jc = np.empty((max(t, 1), 2, P))
+        jp = np.empty((max(t, 1), 2, 3))
+        err = N.ErrorStruct()
+        sc = rec.c_struct()
+        code = self._lib.sfmcov_cuda_jacobian(self._h, C.byref(sc), jc.ctypes.data, jp.ctypes.data, C.byref(err))
+        _raise(code, err)
+        return SparseJacobian(rec.obs_cam.copy(), rec.obs_pt.copy(), jc[:t], jp[:t], rec.num_cameras(),
+                              rec.num_points())
+
+    def gauge_nullspace(self, rec: Reconstruction) -> np.ndarray:
+        H = np.empty((max(rec.num_parameters(), 1), K_GAUGE))
+        err = N.ErrorStruct()
+        sc = rec.c_struct()
+        code = self._lib.sfmcov_cuda_nullspace(self._h, C.byref(sc), H.ctypes.data, C.byref(err))
+        _raise(code, err)
+        return H[:rec.num_parameters()]
+
+    def build_fisher_blocks(self, rec: Reconstruction) -> FisherBlocks:
+        P, n, m, t = rec.cam_params, rec.num_cameras(), rec.num_points(), rec.num_observations()
+        D = np.empty((max(n, 1), P, P))
+        A = np.empty((max(m, 1), 3, 3))
+        Cp = np.empty((max(t, 1), P, 3))
+        sa = np.empty(max(rec.num_parameters(), 1))
+        sb = np.empty(K_GAUGE)
+        flagged = np.zeros(max(1, rec.num_parameters()), dtype=np.int64)
+        diag = N.Diagnostics()
+        diag.flagged = flagged.ctypes.data_as(N.c_int64_p)
+        diag.flagged_capacity = flagged.size
+        err = N.ErrorStruct()
+        sc = rec.c_struct()
+        code = self._lib.sfmcov_cuda_fisher(self._h, C.byref(sc), D.ctypes.data, A.ctypes.data, Cp.ctypes.data,
+                                            sa.ctypes.data, sb.ctypes.data, C.byref(diag), C.byref(err))
+        _raise(code, err)
+        return FisherBlocks(D[:n], A[:m], Cp[:t], sa[:rec.num_parameters()], sb,
+                            [int(v) for v in flagged[:diag.n_flagged]])
+
+    def schur_reduce(self, rec: Reconstruction) -> np.ndarray:
+        dim = rec.cam_params * rec.num_cameras() + K_GAUGE
+        z = np.empty((dim, dim), order="F")
+        err = N.ErrorStruct()
+        sc = rec.c_struct()
+        code = self._lib.sfmcov_cuda_schur(self._h, C.byref(sc), z.ctypes.data, C.byref(err))
+        _raise(code, err)
+        return z
+
+    def spd_inverse_blocks(self, a: np.ndarray, block: int):
+        a = np.asfortranarray(a, dtype=np.float64)
+        n = a.shape[0]
+        out = np.empty((n // block, block, block))
+        mn, mx = C.c_double(), C.c_double()
+        err = N.ErrorStruct()
+        code = self._lib.sfmcov_cuda_spd_inverse_blocks(self._h, a.ctypes.data, n, block, out.ctypes.data,
+                                                        C.byref(mn), C.byref(mx), C.byref(err))
+        _raise(code, err)
+        return out, (mn.value, mx.value)
+
+
+_default = None
+_default_lock = threading.Lock()
+
+
+def default_engine() -> Engine:
+    global _default
+    with _default_lock:
+        if _default is None:
+            _default = Engine(0)
+        return _default
+
+
+def compute_covariance(rec: Reconstruction, options: Optional[CovarianceOptions] = None) -> CovarianceResult:
+    return default_engine().compute_covariance(rec, options)
+
+
+def build_observation_index(rec: Reconstruction) -> ObservationIndex:
+    return default_engine().build_observation_index(rec)
+
+
+def assemble_jacobian(rec: Reconstruction, threads: int = 1) -> SparseJacobian:
+    return default_engine().assemble_jacobian(rec)
+
+
+def gauge_nullspace(rec: Reconstruction) -> np.ndarray:
+    return default_engine().gauge_nullspace(rec)
+
+
+def build_fisher_blocks(rec: Reconstruction) -> FisherBlocks:
+    return default_engine().build_fisher_blocks(rec)
+
+
+def schur_reduce(rec: Reconstruction) -> np.ndarray:
+    return default_engine().schur_reduce(rec)
+
+
+def spd_inverse_blocks(a: np.ndarray, block: int):
+    return default_engine().spd_inverse_blocks(a, block)

@@ -212,17 +212,20 @@ template <int N>
 inline void jacobi_eig(double* a, double* d, double* v) {
     for (int i = 0; i < N; ++i)
         for (int j = 0; j < N; ++j) v[N * i + j] = (i == j) ? 1.0 : 0.0;
+    // Cyclic sweeps; an off-diagonal entry below 1e-17 sqrt|a_pp a_qq| is
+    // treated as converged (set to 0, no rotation); stop after a sweep that
+    // rotated nothing.
     for (int sweep = 0; sweep < 32; ++sweep) {
-        double off = 0.0, diag = 0.0;
-        for (int p = 0; p < N; ++p) {
-            diag += a[N * p + p] * a[N * p + p];
-            for (int q = p + 1; q < N; ++q) off += a[N * p + q] * a[N * p + q];
-        }
-        if (!(off > 1e-34 * diag)) break;
+        bool rotated = false;
         for (int p = 0; p < N; ++p)
             for (int q = p + 1; q < N; ++q) {
                 const double apq = a[N * p + q];
-                if (apq == 0.0) continue;
+                if (!(std::fabs(apq) > 1e-17 * std::sqrt(std::fabs(a[N * p + p] * a[N * q + q])))) {
+                    a[N * p + q] = 0.0;
+                    a[N * q + p] = 0.0;
+                    continue;
+                }
+                rotated = true;
                 const double theta = (a[N * q + q] - a[N * p + p]) / (2.0 * apq);
                 const double at = std::fabs(theta);
                 double t;
@@ -252,6 +255,7 @@ inline void jacobi_eig(double* a, double* d, double* v) {
                     v[N * k + q] = s * vkp + c * vkq;
                 }
             }
+        if (!rotated) break;
     }
     for (int i = 0; i < N; ++i) d[i] = a[N * i + i];
 }
@@ -743,8 +747,12 @@ extern "C" struct oracle_diag {
 };
 
 // ---- bordered inversion: src/covariance.cpp:196-257 ---------------------------
+// BLAS threads for invert_schur: 1 = the reference's pin_blas_single_thread
+// (threading.cpp:54-57); the CPU-baseline harness may raise it.
+static int g_blas_threads = 1;
+
 inline std::vector<double> invert_schur(std::vector<double> z, int64_t n, oracle_diag* diag, double* t_trf, double* t_trs) {
-    openblas_set_num_threads(1);  // pin_blas_single_thread, threading.cpp:54-57
+    openblas_set_num_threads(g_blas_threads);
     std::vector<int> ipiv(n);
     auto t0 = std::chrono::steady_clock::now();
     int info = LAPACKE_dsytrf(kColMajor, 'L', (int)n, z.data(), (int)n, ipiv.data());
@@ -925,7 +933,7 @@ static int ok(oracle_error* e) {
 extern "C" {
 
 const char* oracle_blas_corename(void) { return openblas_get_corename(); }
-void oracle_blas_threads(int n) { openblas_set_num_threads(n); }
+void oracle_blas_threads(int n) { g_blas_threads = n > 0 ? n : 1; openblas_set_num_threads(g_blas_threads); }
 
 int oracle_validate(const oracle_scene* s, oracle_error* e) {
     try { validate(*s); return ok(e); } catch (const Error& x) { return fail(e, x); }
@@ -1029,7 +1037,11 @@ double oracle_nullspace_residual(const oracle_scene* s, const double* h) {
 int oracle_fisher(const oracle_scene* s, double* D, double* A, double* Cp, double* s_a, double* s_b,
                   int64_t* flagged, int64_t flagged_cap, int64_t* n_flagged, oracle_error* e) {
     try {
-        validate(*s);
+        // like build_fisher_blocks (covariance.cpp:33-82): no scene validation,
+        // only the index ranges the restatement needs to stay in bounds
+        for (int64_t t = 0; t < s->n_obs; ++t)
+            if (s->obs_cam[t] < 0 || s->obs_cam[t] >= s->n_cams || s->obs_pt[t] < 0 || s->obs_pt[t] >= s->n_pts)
+                throw Error{kInvariant, "validate", "observation " + std::to_string(t) + " index out of range"};
         ORACLE_DISPATCH(s->cam_params, {
             const Jac<P> J = assemble_jacobian<P>(*s, 1);
             std::vector<double> H = fixed_nullspace_blocks<P>(*s);

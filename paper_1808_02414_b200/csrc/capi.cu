@@ -18,10 +18,15 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
+
+namespace sfm {
+long long g_kernel_launches = 0;
+}
 
 namespace {
 
@@ -56,7 +61,7 @@ struct sfmcov_handle {
     // index
     DBuf cnt_cam, cnt_pt, off_cam, idx_cam, off_pt, idx_pt, pos_cam, key_scratch;
     // stage buffers
-    DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Wb, V, Fpart, LF, E, eigE, Gamma, G, Z, Linv, Lp, piv, cov,
+    DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Lpt, Wb, V, Fpart, LF, E, eigE, Gamma, G, Z, Linv, Lp, piv, cov,
         psd, prange, status, depth, H;
     PairDev pairs;
     Status* st_host = nullptr;
@@ -184,6 +189,16 @@ void throw_numeric(sfmcov_handle* h, const SceneDev& sc, Mode mode) {
                            "; the scene is likely disconnected or its gauge degenerate"};
 }
 
+// Dense panel width in kNB blocks (SFMCOV_PANEL, default 2).
+int panel_blocks() {
+    static int g = [] {
+        const char* e = std::getenv("SFMCOV_PANEL");
+        const int v = e ? std::atoi(e) : 0;
+        return (v >= 1 && v <= 8) ? v : 2;
+    }();
+    return g;
+}
+
 void mark(sfmcov_handle* h, int i) {
     if (h->profiling) SFM_CUDA(cudaEventRecord(h->ev[i], h->s));
 }
@@ -197,6 +212,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     if ((long long)n * n >= (1LL << 32)) throw ApiError{SFMCOV_ERR_SIZE_GUARD, "validate", "too many cameras for 32-bit pair keys"};
     const bool full = (mode == M_FULL || mode == M_SCHUR || mode == M_INDEX);
     for (auto& v : h->stage_ms) v = 0.0;
+    g_kernel_launches = 0;
     Status* st = h->status.as<Status>(1);
     mark(h, 0);
     launch_status_init(st, s);
@@ -304,7 +320,8 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     double* V = h->V.as<double>(21 * (size_t)m);
     const int ppb = point_prep_blocks(m);
     double* Fpart = h->Fpart.as<double>(28 * (size_t)ppb);
-    launch_point_prep(sc, ix, rec, A, s_a, s_b, Wb, V, Fpart, st, s);
+    double* Lpt = h->Lpt.as<double>(8 * (size_t)m);
+    launch_point_prep(sc, ix, rec, A, s_a, s_b, Lpt, Wb, V, Fpart, st, s);
     double* LF = h->LF.as<double>(49);
     double* E = h->E.as<double>(49);
     double* eigE = h->eigE.as<double>(8);
@@ -355,10 +372,11 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     const int K = Npad / kNB;
     double* Linv = h->Linv.as<double>((size_t)K * kNB * kNB);
     double* piv = h->piv.as<double>((size_t)Npad);
-    double* Lp = h->Lp.as<double>((size_t)2 * Npad * kNB);
-    int launches = dense_cholesky(Z, ld, Npad, Linv, piv, st, s, h->s2, h->e1, h->e2);
+    const int pw = panel_blocks();
+    double* Lp = h->Lp.as<double>(trtri_lp_doubles(Npad, pw));
+    int launches = dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, h->s2, h->e1, h->e2);
     mark(h, 8);
-    launches += dense_trtri(Z, ld, Npad, Linv, Lp, s, h->s2, h->e1, h->e2);
+    launches += dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, h->s2, h->e1, h->e2);
     mark(h, 9);
     int* psd = h->psd.as<int>(1);
     SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
@@ -366,7 +384,8 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     double* prange = h->prange.as<double>(2);
     launch_pivot_range(piv, N, prange, s);
     mark(h, 10);
-    h->counts[8] = launches;
+    (void)launches;
+    h->counts[8] = g_kernel_launches;
     sync_status(h);
     throw_numeric(h, sc, mode);
     if (h->profiling) {
@@ -491,8 +510,11 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
     try {
         h->device = device;
         SFM_CUDA(cudaSetDevice(device));
-        SFM_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
-        SFM_CUDA(cudaStreamCreateWithFlags(&h->s2, cudaStreamNonBlocking));
+        // critical path (panel factorisations) at high priority, bulk trailing updates low
+        int lo = 0, hi = 0;
+        SFM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        SFM_CUDA(cudaStreamCreateWithPriority(&h->s, cudaStreamNonBlocking, hi));
+        SFM_CUDA(cudaStreamCreateWithPriority(&h->s2, cudaStreamNonBlocking, lo));
         SFM_CUDA(cudaEventCreateWithFlags(&h->e1, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->e2, cudaEventDisableTiming));
         for (auto& ev : h->ev) SFM_CUDA(cudaEventCreate(&ev));
@@ -513,7 +535,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaStreamSynchronize(h->s2);
     DBuf* bufs[] = {&h->ws.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_u, &h->h_sigma, &h->cnt_cam,
                     &h->cnt_pt, &h->off_cam, &h->idx_cam, &h->off_pt, &h->idx_pt, &h->pos_cam, &h->key_scratch,
-                    &h->R, &h->rec, &h->D, &h->Hr, &h->A, &h->s_a, &h->flags, &h->bpart, &h->s_b, &h->Wb, &h->V,
+                    &h->R, &h->rec, &h->D, &h->Hr, &h->A, &h->s_a, &h->flags, &h->bpart, &h->s_b, &h->Lpt, &h->Wb, &h->V,
                     &h->Fpart, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->Lp, &h->piv,
                     &h->cov, &h->psd, &h->prange, &h->status, &h->depth, &h->H};
     for (DBuf* b : bufs) b->release();
@@ -621,17 +643,17 @@ int32_t sfmcov_cuda_spd_inverse_blocks(sfmcov_handle* h, const double* a, int64_
         double* Z = h->Z.as<double>((size_t)Npad * Npad);
         // identity padding, then the user matrix (column by column)
         SFM_CUDA(cudaMemsetAsync(Z, 0, 8 * (size_t)Npad * Npad, s));
-        std::vector<double> one(1, 1.0);
-        for (int i = N; i < Npad; ++i) SFM_CUDA(cudaMemcpy(Z + (size_t)i * ld + i, one.data(), 8, cudaMemcpyHostToDevice));
+        launch_set_diag(Z, ld, N, Npad, s);
         SFM_CUDA(cudaMemcpy2DAsync(Z, 8 * ld, a, 8 * (size_t)N, 8 * (size_t)N, N, cudaMemcpyHostToDevice, s));
         Status* st = h->status.as<Status>(1);
         launch_status_init(st, s);
         const int K = Npad / kNB;
         double* Linv = h->Linv.as<double>((size_t)K * kNB * kNB);
         double* piv = h->piv.as<double>((size_t)Npad);
-        double* Lp = h->Lp.as<double>((size_t)2 * Npad * kNB);
-        dense_cholesky(Z, ld, Npad, Linv, piv, st, s, h->s2, h->e1, h->e2);
-        dense_trtri(Z, ld, Npad, Linv, Lp, s, h->s2, h->e1, h->e2);
+        const int G = panel_blocks();
+        double* Lp = h->Lp.as<double>(trtri_lp_doubles(Npad, G));
+        dense_cholesky(Z, ld, Npad, G, Linv, piv, st, s, h->s2, h->e1, h->e2);
+        dense_trtri(Z, ld, Npad, G, Linv, Lp, s, h->s2, h->e1, h->e2);
         const int nb = N / block;
         double* dcov = h->cov.as<double>((size_t)block * block * nb);
         int* psd = h->psd.as<int>(1);

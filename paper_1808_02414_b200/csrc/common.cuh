@@ -63,7 +63,14 @@ struct CudaError : std::runtime_error {
                                    __FILE__ + ":" + std::to_string(__LINE__));                   \
     } while (0)
 
-#define SFM_LAUNCH_CHECK() SFM_CUDA(cudaGetLastError())
+// Every kernel launch of this library is followed by SFM_LAUNCH_CHECK(),
+// which also counts it (sfmcov_cuda_last_counts reports the total).
+extern long long g_kernel_launches;
+#define SFM_LAUNCH_CHECK()                  \
+    do {                                    \
+        ++::sfm::g_kernel_launches;         \
+        SFM_CUDA(cudaGetLastError());       \
+    } while (0)
 
 inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 

@@ -73,8 +73,9 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
     const double* A = g.A + (size_t)ti * BM;
     const double* B = BK_MAJOR ? g.B + (size_t)tj * BN * g.ldb : g.B + (size_t)tj * BN;
     double* C = g.C + (size_t)tj * BN * g.ldc + (size_t)ti * BM;
+    if (g.lower_only && ti + g.row_off_tiles < tj + g.col_off_tiles) return;
     const int wm = warp & 3, wn = warp >> 2;  // 4 x 4 warps of 32 x 32
-    const int beta = (g.beta && tj != g.beta0_tile) ? 1 : 0;
+    const int beta = (g.beta && !(g.beta0_from >= 0 && tj >= g.beta0_from)) ? 1 : 0;
 
     auto load_stage = [&](int st, int kc) {
         double* as = As + st * BK * LDS;
@@ -96,10 +97,10 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
         }
     };
 
-    constexpr int NK = kNB / BK;  // 8
+    const int NK = g.K / BK;
     load_stage(0, 0);
     cp_async_commit();
-    load_stage(1, 1);
+    if (NK > 1) load_stage(1, 1);
     cp_async_commit();
 
     double acc[4][4][2];
@@ -169,76 +170,199 @@ void launch_gemm(const GemmArgs& g, cudaStream_t s) {
 
 // ----------------------------------------------------------------------------
 // Diagonal tile: Cholesky + triangular inverse of one kNB x kNB tile in smem.
+// Blocked by 32: each 32x32 diagonal block is factored (and inverted) by one
+// warp in registers with shuffles (rsqrt pivots keep the per-column latency
+// chain short); the panel solve and the trailing update inside the tile use
+// all warps.  The inverse Y = L^-1 is built in shared memory: its strictly
+// lower 32-blocks are stored transposed in the (unused) upper triangle of T.
 // ----------------------------------------------------------------------------
-namespace potrf {
+#ifdef SFM_POTRF_TIMING
+__device__ long long g_potrf_stamp[64];
+#define POTRF_STAMP(i) do { __syncthreads(); if (threadIdx.x == 0) g_potrf_stamp[i] = clock64(); } while (0)
+#else
+#define POTRF_STAMP(i) do { } while (0)
+#endif
+
+namespace potrf_consts {
 constexpr int LDT = kNB + 1;
-constexpr int THREADS = 512;
-constexpr int SMEM = (kNB * LDT + kNB) * 8;
+}
+namespace potrf {
+constexpr int LDT = potrf_consts::LDT;
+constexpr int BS = 32;
+constexpr int NBLK = kNB / BS;  // 4
+constexpr int LDX = BS + 1;
+constexpr int THREADS = 256;
+constexpr int SMEM = (kNB * LDT + (2 * NBLK - 1) * BS * LDX + kNB) * 8;
 }  // namespace potrf
+
+// Warp-level Cholesky of the 32x32 block at T(c0, c0) (col-major, ld LDT),
+// in place in shared memory: lane i owns row i.  Compact loops on purpose —
+// a fully unrolled register version is ~250 KB of SASS and runs from L2
+// instead of the instruction cache.  Writes L, its inverse X (row-major
+// Xd[r * LDX + c]) and 1/L_jj (rinv).  Pivots (= L_jj^2) go to piv.
+__device__ __noinline__ void warp_potrf32(double* T, int c0, double* Xd, double* rinv, double* piv, int gcol0,
+                                          Status* st) {
+    using namespace potrf;
+    const int i = threadIdx.x & 31;
+    double* B = T + c0 * LDT + c0;  // B[c * LDT + r]
+#pragma unroll 1
+    for (int j = 0; j < BS; ++j) {
+        double d = B[j * LDT + j];
+        if (i == 0) {
+            piv[gcol0 + j] = d;
+            if (!(d > 0.0) || !isfinite(d)) atomicMin(&st->chol_bad, gcol0 + j);
+        }
+        if (!(d > 0.0) || !isfinite(d)) d = 1.0;
+        const double inv = rsqrt(d);
+        __syncwarp();
+        double lij = 0.0;
+        if (i == j) { B[j * LDT + j] = d * inv; rinv[c0 + j] = inv; }
+        else if (i > j) { lij = B[j * LDT + i] * inv; B[j * LDT + i] = lij; }
+        __syncwarp();
+#pragma unroll 4
+        for (int c = j + 1; c <= i; ++c) B[c * LDT + i] -= lij * B[j * LDT + c];
+        __syncwarp();
+    }
+    // inverse, column-oriented: lane c owns column c of X = L^-1
+    const int c = i;
+#pragma unroll 1
+    for (int r = 0; r < BS; ++r) {
+        double x;
+        if (r < c) {
+            x = 0.0;
+        } else if (r == c) {
+            x = rinv[c0 + r];
+        } else {
+            double s = 0.0;
+#pragma unroll 4
+            for (int k = c; k < r; ++k) s += B[k * LDT + r] * Xd[k * LDX + c];
+            x = -s * rinv[c0 + r];
+        }
+        Xd[r * LDX + c] = x;
+    }
+    __syncwarp();
+}
 
 // A: tile (k0, k0) of the matrix (col-major, ld).  Writes L (lower) back,
 // Linv (kNB x kNB col-major, zeros above), pivots[col0 + j] = L_jj^2.
 __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, long long ld, double* Linv, double* pivots,
                                                                  int col0, Status* st) {
     using namespace potrf;
-    extern __shared__ double T[];  // T[c * LDT + r]
-    double* col = T + kNB * LDT;
-    const int tid = threadIdx.x;
+    extern __shared__ double T[];                  // T[c * LDT + r]
+    double* Xd = T + kNB * LDT;                    // NBLK blocks, row-major 32 x LDX
+    double* S = Xd + NBLK * BS * LDX;              // NBLK-1 scratch blocks
+    double* rinv = S + (NBLK - 1) * BS * LDX;      // 1 / L_jj
+    const int tid = threadIdx.x, warp = tid >> 5;
     for (int e = tid; e < kNB * kNB; e += THREADS) {
         const int r = e & (kNB - 1), c = e >> 7;
         T[c * LDT + r] = (r >= c) ? A[(size_t)c * ld + r] : 0.0;
     }
     __syncthreads();
-    // right-looking unblocked Cholesky
-    for (int j = 0; j < kNB; ++j) {
-        if (tid == 0) {
-            double d = T[j * LDT + j];
-            pivots[col0 + j] = d;
-            if (!(d > 0.0) || !isfinite(d)) {
-                atomicMin(&st->chol_bad, col0 + j);
-                d = 1.0;
+    POTRF_STAMP(0);
+    constexpr int MAXU = (kNB - BS) * BS / THREADS;  // 12
+    for (int kb = 0; kb < NBLK; ++kb) {
+        const int c0 = kb * BS;
+        double* X = Xd + kb * BS * LDX;
+        if (warp == 0) warp_potrf32(T, c0, X, rinv, pivots, col0 + c0, st);
+        __syncthreads();
+        POTRF_STAMP(1 + 3 * kb);
+        const int rows = kNB - c0 - BS;
+        if (rows == 0) break;
+        // panel solve: L[r, c0 + c] = Σ_{k <= c} A[r, c0 + k] X[c, k]
+        double out[MAXU];
+#pragma unroll
+        for (int u = 0; u < MAXU; ++u) {
+            const int e = tid + u * THREADS;
+            out[u] = 0.0;
+            if (e < rows * BS) {
+                const int r = c0 + BS + (e % rows), c = e / rows;
+                double s = 0.0;
+                for (int k = 0; k <= c; ++k) s += T[(c0 + k) * LDT + r] * X[c * LDX + k];
+                out[u] = s;
             }
-            T[j * LDT + j] = sqrt(d);
         }
         __syncthreads();
-        const double ljj = T[j * LDT + j];
-        for (int i = j + 1 + tid; i < kNB; i += THREADS) T[j * LDT + i] = T[j * LDT + i] / ljj;
-        __syncthreads();
-        const int warp = tid >> 5, lane = tid & 31;
-        for (int c = j + 1 + warp; c < kNB; c += THREADS / 32) {
-            const double lcj = T[j * LDT + c];
-            for (int i = c + lane; i < kNB; i += 32) T[c * LDT + i] -= T[j * LDT + i] * lcj;
+#pragma unroll
+        for (int u = 0; u < MAXU; ++u) {
+            const int e = tid + u * THREADS;
+            if (e < rows * BS) {
+                const int r = c0 + BS + (e % rows), c = e / rows;
+                T[(c0 + c) * LDT + r] = out[u];
+            }
         }
         __syncthreads();
+        POTRF_STAMP(2 + 3 * kb);
+        // trailing update inside the tile, 4x4 micro-tiles of the lower part
+        const int tb = rows / 4;
+        for (int e = tid; e < tb * tb; e += THREADS) {
+            const int mi = e % tb, mj = e / tb;
+            if (mi < mj) continue;
+            const int r0 = c0 + BS + 4 * mi, cc0 = c0 + BS + 4 * mj;
+            double acc[4][4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
+            for (int k = 0; k < BS; ++k) {
+                double lr[4], lc[4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) { lr[p] = T[(c0 + k) * LDT + r0 + p]; lc[p] = T[(c0 + k) * LDT + cc0 + p]; }
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[p][q] += lr[p] * lc[q];
+            }
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (r0 + p >= cc0 + q) T[(cc0 + q) * LDT + r0 + p] -= acc[p][q];
+        }
+        __syncthreads();
+        POTRF_STAMP(3 + 3 * kb);
     }
     for (int e = tid; e < kNB * kNB; e += THREADS) {
         const int r = e & (kNB - 1), c = e >> 7;
         if (r >= c) A[(size_t)c * ld + r] = T[c * LDT + r];
     }
-    // in-place inverse: solve L X = I, right-looking; X(i,c) for c <= j
-    // overwrites L(i,c) once column c of L is consumed.
-    for (int j = 0; j < kNB; ++j) {
-        // copy column j of L (rows >= j) before it is overwritten
-        for (int i = j + tid; i < kNB; i += THREADS) col[i] = T[j * LDT + i];
-        __syncthreads();
-        const double ljj = col[j];
-        // row j of X: X(j, c) = X(j, c) / ljj for c < j; X(j, j) = 1 / ljj
-        for (int c = tid; c <= j; c += THREADS) T[c * LDT + j] = (c == j) ? 1.0 / ljj : T[c * LDT + j] / ljj;
-        __syncthreads();
-        // X(i, c) -= L(i, j) X(j, c), i > j, c <= j (X(i, j) starts at 0)
-        const int rows = kNB - 1 - j;
-        const int cols = j + 1;
-        for (int e = tid; e < rows * cols; e += THREADS) {
-            const int i = j + 1 + e % rows, c = e / rows;
-            const double base = (c == j) ? 0.0 : T[c * LDT + i];
-            T[c * LDT + i] = base - col[i] * T[c * LDT + j];
+    POTRF_STAMP(14);
+    // Y_ij = -X_i Σ_{k=j}^{i-1} L_ik Y_kj by block diagonals d = i - j; Y_kj
+    // (k > j) lives transposed at T[(32k + r) LDT + 32j + c], Y_jj = X_j.
+    for (int d = 1; d < NBLK; ++d) {
+        const int nblk = NBLK - d;
+        for (int e = tid; e < nblk * BS * BS; e += THREADS) {
+            const int b = e / (BS * BS), w = e % (BS * BS);
+            const int q = w % BS, cc = w / BS;
+            const int bi = d + b, bj = b;
+            const int gr = bi * BS + q;
+            double s = 0.0;
+            const double* xj = Xd + bj * BS * LDX;
+            for (int k = 0; k < BS; ++k) s += T[(bj * BS + k) * LDT + gr] * xj[k * LDX + cc];
+            for (int kr = (bj + 1) * BS; kr < bi * BS; ++kr) s += T[kr * LDT + gr] * T[kr * LDT + bj * BS + cc];
+            S[b * BS * LDX + q * LDX + cc] = s;
         }
         __syncthreads();
+        for (int e = tid; e < nblk * BS * BS; e += THREADS) {
+            const int b = e / (BS * BS), w = e % (BS * BS);
+            const int rr = w % BS, cc = w / BS;
+            const int bi = d + b, bj = b;
+            const double* xr = Xd + bi * BS * LDX + rr * LDX;
+            double acc = 0.0;
+            for (int q = 0; q <= rr; ++q) acc += xr[q] * S[b * BS * LDX + q * LDX + cc];
+            T[(bi * BS + rr) * LDT + bj * BS + cc] = -acc;
+        }
+        __syncthreads();
+        POTRF_STAMP(14 + d);
     }
     for (int e = tid; e < kNB * kNB; e += THREADS) {
         const int r = e & (kNB - 1), c = e >> 7;
-        Linv[(size_t)c * kNB + r] = (r >= c) ? T[c * LDT + r] : 0.0;
+        const int bi = r / BS, bj = c / BS;
+        double v = 0.0;
+        if (bi == bj) { if ((r % BS) >= (c % BS)) v = Xd[bi * BS * LDX + (r % BS) * LDX + (c % BS)]; }
+        else if (bi > bj) v = T[r * LDT + c];
+        Linv[(size_t)c * kNB + r] = v;
     }
+    POTRF_STAMP(18);
 }
 
 void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s) {
@@ -280,6 +404,23 @@ void launch_copy_panel(const double* X, long long ld, int k, int rows, double* L
     const long long total = (long long)rows * kNB;
     if (!total) return;
     k_copy_panel<<<cdiv(total, 256), 256, 0, s>>>(X, ld, k, rows, Lp);
+    SFM_LAUNCH_CHECK();
+}
+
+// Copy the W = G kNB wide L panel (block columns b0 .. b0+G) below the panel
+// into a contiguous buffer (rows x W, col-major, ld = rows).
+__global__ void k_copy_panel_w(const double* X, long long ld, int b0, int G, int rows, double* Lp) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long total = (long long)rows * G * kNB;
+    if (e >= total) return;
+    const int r = (int)(e % rows), c = (int)(e / rows);
+    Lp[(size_t)c * rows + r] = X[(size_t)(b0 * kNB + c) * ld + (size_t)(b0 + G) * kNB + r];
+}
+
+void launch_copy_panel_w(const double* X, long long ld, int b0, int G, int rows, double* Lp, cudaStream_t s) {
+    const long long total = (long long)rows * G * kNB;
+    if (!total) return;
+    k_copy_panel_w<<<cdiv(total, 256), 256, 0, s>>>(X, ld, b0, G, rows, Lp);
     SFM_LAUNCH_CHECK();
 }
 
@@ -334,12 +475,27 @@ __global__ void __launch_bounds__(256) k_extract(const double* X, long long ld, 
             }
         double* o = cov + (size_t)P * P * i;
         for (int k = 0; k < P * P; ++k) o[k] = out[k];
-        double a[P * P], d[P], v[P * P];
-        for (int k = 0; k < P * P; ++k) a[k] = out[k];
-        jacobi_eig<P>(a, d, v);
-        double tr = 0.0, lmin = d[0];
-        for (int p = 0; p < P; ++p) { tr += out[P * p + p]; lmin = fmin(lmin, d[p]); }
-        if (lmin < -kPsdTol * tr) atomicAdd(psd_warn, 1);
+        // PSD test (covariance.cpp:266-268: lam_min < -kPsdTol * trace warns):
+        // lam_min(S) > -tau  <=>  S + tau I is positive definite  <=>  its
+        // Cholesky succeeds.
+        double tr = 0.0;
+        for (int p = 0; p < P; ++p) tr += out[P * p + p];
+        const double tau = kPsdTol * tr;
+        double L[P * P];
+        bool pd = true;
+        for (int c = 0; c < P && pd; ++c) {
+            double s = out[P * c + c] + tau;
+            for (int k = 0; k < c; ++k) s -= L[P * c + k] * L[P * c + k];
+            if (!(s > 0.0)) { pd = false; break; }
+            const double lcc = sqrt(s);
+            L[P * c + c] = lcc;
+            for (int r = c + 1; r < P; ++r) {
+                double x = out[P * r + c];
+                for (int k = 0; k < c; ++k) x -= L[P * r + k] * L[P * c + k];
+                L[P * r + c] = x / lcc;
+            }
+        }
+        if (!pd) atomicAdd(psd_warn, 1);
     }
 }
 
@@ -349,6 +505,18 @@ void launch_extract(int P, const double* X, long long ld, int N, int nblocks, co
     if (P == 8) k_extract<8><<<nblocks, 256, 0, s>>>(X, ld, N, s_a, scale, cov, st, psd_warn);
     else if (P == 9) k_extract<9><<<nblocks, 256, 0, s>>>(X, ld, N, s_a, scale, cov, st, psd_warn);
     else throw CudaError("extract: unsupported block size");
+    SFM_LAUNCH_CHECK();
+}
+
+// Identity on the padded tail of the diagonal: Z(i, i) = 1 for i in [from, to).
+__global__ void k_set_diag(double* Z, long long ld, int from, int to) {
+    const int i = from + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < to) Z[(size_t)i * ld + i] = 1.0;
+}
+
+void launch_set_diag(double* Z, long long ld, int from, int to, cudaStream_t s) {
+    if (to <= from) return;
+    k_set_diag<<<cdiv(to - from, 128), 128, 0, s>>>(Z, ld, from, to);
     SFM_LAUNCH_CHECK();
 }
 
@@ -374,49 +542,73 @@ void launch_pivot_range(const double* piv, int N, double* out, cudaStream_t s) {
 // ----------------------------------------------------------------------------
 // Drivers
 // ----------------------------------------------------------------------------
-// Blocked right-looking Cholesky of the Npad x Npad lower triangle (Npad =
-// K kNB) with one-panel lookahead.  Step k on stream s: potrf(k), trsm(k)
-// [L21 = A21 Linv_k^T], then the next panel column's update; the rest of the
-// trailing SYRK (columns >= k+2) runs on s2 and overlaps potrf/trsm of step
-// k+1.  Ordering: rest(k) waits trsm(k) (e1); next-panel(k) waits rest(k-1)
-// (e2), since both update column block k+1.
-int dense_cholesky(double* Z, long long ld, int Npad, double* Linv, double* pivots, Status* st, cudaStream_t s,
+static GemmArgs gemm_args(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb,
+                          int tm, int tn, int K) {
+    GemmArgs g{};
+    g.C = C; g.ldc = ldc; g.A = A; g.lda = lda; g.B = B; g.ldb = ldb;
+    g.tm = tm; g.tn = tn; g.K = K; g.beta0_from = -1;
+    return g;
+}
+
+// Blocked right-looking Cholesky of the Npad x Npad lower triangle with
+// panels of W = G kNB columns and one-panel lookahead.
+//   panel p, stream s (critical path): for each kNB block of the panel:
+//     potrf(diag) -> L21 = A21 Linv^T -> update of the panel's remaining
+//     columns (K = kNB); then the next panel's columns get the K = W update.
+//   stream s2: the rest of the trailing SYRK (K = W), overlapping the next
+//     panel's factorisation.  Ordering: rest(p) waits the panel (e1);
+//     next-panel(p) waits rest(p-1) (e2).
+int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, cudaStream_t s,
                    cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2) {
-    const int K = Npad / kNB;
+    const int K = Npad / kNB;  // 128-blocks
     int launches = 0;
     bool rest_pending = false;
-    for (int k = 0; k < K; ++k) {
-        double* Akk = Z + (size_t)k * kNB * ld + (size_t)k * kNB;
-        launch_potrf_diag(Akk, ld, Linv + (size_t)k * kNB * kNB, pivots, k * kNB, st, s);
-        ++launches;
-        const int rows = Npad - (k + 1) * kNB;
-        if (rows == 0) break;
-        double* panel = Akk + kNB;
-        GemmArgs t{};
-        t.C = panel; t.ldc = ld; t.A = panel; t.lda = ld; t.B = Linv + (size_t)k * kNB * kNB; t.ldb = kNB;
-        t.tm = rows / kNB; t.tn = 1; t.beta0_tile = -1;
-        launch_gemm(t, s);
-        ++launches;
-        const int T2 = rows / kNB;
-        if (T2 > 1) {
+    for (int b0 = 0; b0 < K; b0 += G) {
+        const int g_here = (b0 + G <= K) ? G : K - b0;
+        // --- panel factorisation (critical path) ---
+        for (int g = 0; g < g_here; ++g) {
+            const int c = b0 + g;
+            double* Acc = Z + (size_t)c * kNB * ld + (size_t)c * kNB;
+            launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s);
+            ++launches;
+            const int below = K - c - 1;
+            if (below == 0) break;
+            GemmArgs t = gemm_args(Acc + kNB, ld, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
+            launch_gemm(t, s);
+            ++launches;
+            const int inner = b0 + g_here - c - 1;  // remaining columns inside the panel
+            if (inner > 0) {
+                // A[rows >= c+1, cols c+1 .. b0+g_here) -= L[rows, c] L[cols, c]^T
+                GemmArgs u = gemm_args(Z + (size_t)(c + 1) * kNB * ld + (size_t)(c + 1) * kNB, ld, Acc + kNB, ld,
+                                       Acc + kNB, ld, below, inner, kNB);
+                u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
+                launch_gemm(u, s);
+                ++launches;
+            }
+        }
+        const int nb0 = b0 + g_here;  // first block after the panel
+        const int T2 = K - nb0;       // trailing blocks
+        if (T2 <= 0) break;
+        const int W = g_here * kNB;
+        const double* L21 = Z + (size_t)b0 * kNB * ld + (size_t)nb0 * kNB;  // rows >= nb0, panel columns
+        const int gn = (T2 < G) ? T2 : G;  // next panel width in blocks
+        if (T2 > gn) {
             SFM_CUDA(cudaEventRecord(e1, s));
             SFM_CUDA(cudaStreamWaitEvent(s2, e1, 0));
-            GemmArgs r{};
-            r.C = Z + (size_t)(k + 2) * kNB * ld + (size_t)(k + 2) * kNB; r.ldc = ld;
-            r.A = panel + kNB; r.lda = ld; r.B = panel + kNB; r.ldb = ld;
-            r.tm = T2 - 1; r.tn = T2 - 1; r.tri = 1; r.alpha_neg = 1; r.beta = 1; r.beta0_tile = -1;
+            const int r0 = nb0 + gn;
+            GemmArgs r = gemm_args(Z + (size_t)r0 * kNB * ld + (size_t)r0 * kNB, ld, L21 + (size_t)gn * kNB, ld,
+                                   L21 + (size_t)gn * kNB, ld, T2 - gn, T2 - gn, W);
+            r.tri = 1; r.alpha_neg = 1; r.beta = 1;
             launch_gemm(r, s2);
             ++launches;
         }
         if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, e2, 0));
-        GemmArgs u{};
-        u.C = Z + (size_t)(k + 1) * kNB * ld + (size_t)(k + 1) * kNB; u.ldc = ld;
-        u.A = panel; u.lda = ld; u.B = panel; u.ldb = ld;
-        u.tm = T2; u.tn = 1; u.alpha_neg = 1; u.beta = 1; u.beta0_tile = -1;
+        GemmArgs u = gemm_args(Z + (size_t)nb0 * kNB * ld + (size_t)nb0 * kNB, ld, L21, ld, L21, ld, T2, gn, W);
+        u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
         launch_gemm(u, s);
         ++launches;
         rest_pending = false;
-        if (T2 > 1) {
+        if (T2 > gn) {
             SFM_CUDA(cudaEventRecord(e2, s2));
             rest_pending = true;
         }
@@ -426,51 +618,65 @@ int dense_cholesky(double* Z, long long ld, int Npad, double* Linv, double* pivo
 }
 
 // Blocked triangular inverse X = L^-1 in place (forward substitution by row
-// blocks), with the same lookahead split.  Step k:
-//   (1) X[k, 0:k] = Linv_k X[k, 0:k] (GEMM, B K-major), X[k, k] = Linv_k
-//   (2) Lp = L[k+1:, k] (copy; column block k is overwritten below)
-//   (3) X[k+1:, 0:k+1] -= Lp X[k, 0:k+1]   (column block k with beta = 0)
-// (3) is split into row block k+1 (stream s, feeds step k+1) and the rest
-// (stream s2).
-int dense_trtri(double* X, long long ld, int Npad, const double* Linv, double* Lp, cudaStream_t s, cudaStream_t s2,
-                cudaEvent_t e1, cudaEvent_t e2) {
+// panels of W = G kNB rows).  Panel p (row blocks b0 .. b0+G):
+//   for each row block r of the panel:
+//     X[r, 0:r] = Linv_r X[r, 0:r] (GEMM, B K-major); X[r, r] = Linv_r;
+//     X[r', 0:r+1] -= L[r', r] X[r, 0:r+1] for the panel's later rows r'
+//   Lp = L[rows below the panel, panel columns] (copy; overwritten next)
+//   X[rows below, 0:b0+G] -= Lp X[panel rows, 0:b0+G]  (K = W; the panel's
+//     own column tiles start from zero)
+// with the next panel's rows on s and the rest on s2.
+int dense_trtri(double* X, long long ld, int Npad, int G, const double* Linv, double* Lp, cudaStream_t s,
+                cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2) {
     const int K = Npad / kNB;
     int launches = 0;
     bool rest_pending = false;
-    for (int k = 0; k < K; ++k) {
-        const double* Lk = Linv + (size_t)k * kNB * kNB;
-        if (k > 0) {
-            GemmArgs g{};
-            g.C = X + (size_t)k * kNB; g.ldc = ld;
-            g.A = Lk; g.lda = kNB;
-            g.B = X + (size_t)k * kNB; g.ldb = ld; g.b_kmajor = 1;
-            g.tm = 1; g.tn = k; g.beta0_tile = -1;
-            launch_gemm(g, s);
+    double* inner_buf = Lp + (size_t)Npad * G * kNB;
+    for (int b0 = 0; b0 < K; b0 += G) {
+        const int g_here = (b0 + G <= K) ? G : K - b0;
+        for (int g = 0; g < g_here; ++g) {
+            const int r = b0 + g;
+            const double* Lr = Linv + (size_t)r * kNB * kNB;
+            if (r > 0) {
+                GemmArgs a = gemm_args(X + (size_t)r * kNB, ld, Lr, kNB, X + (size_t)r * kNB, ld, 1, r, kNB);
+                a.b_kmajor = 1;
+                launch_gemm(a, s);
+                ++launches;
+            }
+            launch_copy_diag(X, ld, r, Lr, s);
             ++launches;
+            const int later = b0 + g_here - r - 1;
+            if (later > 0) {
+                // L[r', r] for r' in the panel is still L (column block r untouched so far)
+                launch_copy_panel(X, ld, r, later * kNB, inner_buf, s);
+                ++launches;
+                GemmArgs u = gemm_args(X + (size_t)(r + 1) * kNB, ld, inner_buf, later * kNB,
+                                       X + (size_t)r * kNB, ld, later, r + 1, kNB);
+                u.b_kmajor = 1; u.alpha_neg = 1; u.beta = 1; u.beta0_from = r;
+                launch_gemm(u, s);
+                ++launches;
+            }
         }
-        launch_copy_diag(X, ld, k, Lk, s);
-        ++launches;
-        const int rows = Npad - (k + 1) * kNB;
-        if (rows == 0) break;
-        // Lp must not be overwritten while rest(k-1) on s2 still reads it
+        const int nb0 = b0 + g_here;
+        const int T2 = K - nb0;
+        if (T2 <= 0) break;
+        const int W = g_here * kNB;
+        const int rows = T2 * kNB;
         if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, e2, 0));
         rest_pending = false;
-        launch_copy_panel(X, ld, k, rows, Lp + (size_t)(k & 1) * (size_t)Npad * kNB, s);
+        double* lp = Lp;  // rest(p-1), its only other reader, completed (e2 above)
+        launch_copy_panel_w(X, ld, b0, g_here, rows, lp, s);
         ++launches;
-        const double* lp = Lp + (size_t)(k & 1) * (size_t)Npad * kNB;
-        const int T2 = rows / kNB;
-        GemmArgs a{};
-        a.C = X + (size_t)(k + 1) * kNB; a.ldc = ld;
-        a.A = lp; a.lda = rows;
-        a.B = X + (size_t)k * kNB; a.ldb = ld; a.b_kmajor = 1;
-        a.tm = 1; a.tn = k + 1; a.alpha_neg = 1; a.beta = 1; a.beta0_tile = k;
-        if (T2 > 1) {
+        const int gn = (T2 < G) ? T2 : G;
+        GemmArgs a = gemm_args(X + (size_t)nb0 * kNB, ld, lp, rows, X + (size_t)b0 * kNB, ld, gn, nb0, W);
+        a.b_kmajor = 1; a.alpha_neg = 1; a.beta = 1; a.beta0_from = b0;
+        if (T2 > gn) {
             SFM_CUDA(cudaEventRecord(e1, s));
             SFM_CUDA(cudaStreamWaitEvent(s2, e1, 0));
             GemmArgs r = a;
-            r.C = X + (size_t)(k + 2) * kNB;
-            r.A = lp + kNB;
-            r.tm = T2 - 1;
+            r.C = X + (size_t)(nb0 + gn) * kNB;
+            r.A = lp + (size_t)gn * kNB;
+            r.tm = T2 - gn;
             launch_gemm(r, s2);
             ++launches;
             SFM_CUDA(cudaEventRecord(e2, s2));

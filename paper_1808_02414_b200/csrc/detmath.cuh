@@ -139,17 +139,20 @@ template <int N>
 SFM_HD void jacobi_eig(double* a, double* d, double* v) {
     for (int i = 0; i < N; ++i)
         for (int j = 0; j < N; ++j) v[N * i + j] = (i == j) ? 1.0 : 0.0;
+    // Cyclic sweeps; an off-diagonal entry below 1e-17 sqrt|a_pp a_qq| is
+    // treated as converged (set to 0, no rotation); stop after a sweep that
+    // rotated nothing.
     for (int sweep = 0; sweep < 32; ++sweep) {
-        double off = 0.0, diag = 0.0;
-        for (int p = 0; p < N; ++p) {
-            diag += a[N * p + p] * a[N * p + p];
-            for (int q = p + 1; q < N; ++q) off += a[N * p + q] * a[N * p + q];
-        }
-        if (!(off > 1e-34 * diag)) break;
+        bool rotated = false;
         for (int p = 0; p < N; ++p)
             for (int q = p + 1; q < N; ++q) {
                 const double apq = a[N * p + q];
-                if (apq == 0.0) continue;
+                if (!(fabs(apq) > 1e-17 * sqrt(fabs(a[N * p + p] * a[N * q + q])))) {
+                    a[N * p + q] = 0.0;
+                    a[N * q + p] = 0.0;
+                    continue;
+                }
+                rotated = true;
                 const double theta = (a[N * q + q] - a[N * p + p]) / (2.0 * apq);
                 const double at = fabs(theta);
                 double t;
@@ -179,6 +182,7 @@ SFM_HD void jacobi_eig(double* a, double* d, double* v) {
                     v[N * k + q] = s * vkp + c * vkq;
                 }
             }
+        if (!rotated) break;
     }
     for (int i = 0; i < N; ++i) d[i] = a[N * i + i];
 }

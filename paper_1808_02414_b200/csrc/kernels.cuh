@@ -83,11 +83,14 @@ struct GemmArgs {
     const double* B;
     long long ldb;
     int tm, tn;
+    int K;           // reduction length (multiple of 16)
     int tri;         // lower-triangular tile set (ti >= tj) of a tm x tm grid
     int alpha_neg;   // alpha = -1
     int beta;        // 1: accumulate into C
-    int beta0_tile;  // column tile that uses beta = 0 (-1: none)
+    int beta0_from;  // column tiles >= this use beta = 0 (-1: none)
     int b_kmajor;    // B stored K-contiguous
+    int lower_only;  // skip tiles strictly above the matrix diagonal
+    int row_off_tiles, col_off_tiles;  // C tile offsets relative to the diagonal
 };
 
 // stage_a.cu
@@ -108,7 +111,7 @@ void launch_write_h(const SceneDev& sc, const double* Hr, double* H, cudaStream_
 // schur.cu
 int point_prep_blocks(int m);
 void launch_point_prep(const SceneDev& sc, const IndexDev& ix, const double* rec, const double* A, const double* s_a,
-                       const double* s_b, double* Wb, double* V, double* Fpart, Status* st, cudaStream_t s);
+                       const double* s_b, double* Lpt, double* Wb, double* V, double* Fpart, Status* st, cudaStream_t s);
 void launch_border_factor(const double* Fpart, int nblocks, double* LF, double* E, double* eigE, Status* st,
                           cudaStream_t s);
 void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* Wb, const double* V, const double* Hr,
@@ -124,12 +127,16 @@ void launch_gemm(const GemmArgs& g, cudaStream_t s);
 void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s);
 void launch_copy_diag(double* X, long long ld, int k, const double* Linv, cudaStream_t s);
 void launch_copy_panel(const double* X, long long ld, int k, int rows, double* Lp, cudaStream_t s);
+void launch_copy_panel_w(const double* X, long long ld, int b0, int G, int rows, double* Lp, cudaStream_t s);
 void launch_extract(int P, const double* X, long long ld, int N, int nblocks, const double* s_a, int scale, double* cov,
                     Status* st, int* psd_warn, cudaStream_t s);
+void launch_set_diag(double* Z, long long ld, int from, int to, cudaStream_t s);
 void launch_pivot_range(const double* piv, int N, double* out, cudaStream_t s);
-int dense_cholesky(double* Z, long long ld, int Npad, double* Linv, double* pivots, Status* st, cudaStream_t s,
+int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, cudaStream_t s,
                    cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2);
-int dense_trtri(double* X, long long ld, int Npad, const double* Linv, double* Lp, cudaStream_t s, cudaStream_t s2,
-                cudaEvent_t e1, cudaEvent_t e2);
+int dense_trtri(double* X, long long ld, int Npad, int G, const double* Linv, double* Lp, cudaStream_t s,
+                cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2);
+// Lp workspace (doubles) dense_trtri needs for panel width G.
+inline size_t trtri_lp_doubles(int Npad, int G) { return (size_t)Npad * kNB * G + (size_t)kNB * kNB * G; }
 
 }  // namespace sfm

@@ -31,12 +31,14 @@
 namespace sfm {
 
 // ---- per-point preparation (thread per point) -----------------------------------
+// A_s = S A S, the reference's singularity test on it (covariance.cpp:147-151),
+// L_j = chol(A_s) (stored as l00 l10 l11 l20 l21 l22), V_j = L_j^-1 H_s,pj and
+// the block-partial of F = Σ V_j^T V_j (fixed-order tree).
 template <int P>
-__global__ void k_point_prep(const int* off_pt, const int* idx_pt, const int* oc, const int* pos_cam,
-                             const double* rec, const double* A, const double* s_a, const double* pts,
-                             const double* s_b, int m, int n, double* Wb, double* V, double* Fpart,
-                             Status* st) {
-    __shared__ double red[128][28];
+__global__ void __launch_bounds__(128) k_point_prep(const double* A, const double* s_a, const double* pts,
+                                                    const double* s_b, int m, int n, double* Lpt, double* V,
+                                                    double* Fpart, Status* st) {
+    __shared__ double red[128][29];
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     double f[28];
 #pragma unroll
@@ -59,7 +61,14 @@ __global__ void k_point_prep(const int* off_pt, const int* idx_pt, const int* oc
             l22 = sqrt(d22);
             if (!(d11 > 0.0) || !(d22 > 0.0)) good = false;
         }
-        if (!good) atomicMin(&st->pt_sing_bad, j);
+        if (!good) {
+            atomicMin(&st->pt_sing_bad, j);
+            l00 = 1; l10 = 0; l11 = 1; l20 = 0; l21 = 0; l22 = 1;
+        }
+        double* lo = Lpt + 8 * (size_t)j;
+        lo[0] = l00; lo[1] = l10; lo[2] = l11; lo[3] = l20; lo[4] = l21; lo[5] = l22;
+        lo[6] = good ? 1.0 : 0.0;
+        lo[7] = 0.0;
         // H_s rows of the point: (s_p[q] * [e_q | [X]x row q | X_q]) * s_b
         const double* X = pts + 3 * (size_t)j;
         double sx[9];
@@ -87,30 +96,7 @@ __global__ void k_point_prep(const int* off_pt, const int* idx_pt, const int* oc
                 for (int l2 = l1; l2 < 7; ++l2, ++k)
                     f[k] = (v[0][l1] * v[0][l2] + v[1][l1] * v[1][l2]) + v[2][l1] * v[2][l2];
         }
-        for (int kk = off_pt[j]; kk < off_pt[j + 1]; ++kk) {
-            const int t = idx_pt[kk];
-            const double* r = rec + (size_t)t * kRec;
-            const double* jc = r + Layout<P>::JC;
-            const double* jp = r + Layout<P>::JP;
-            const double* W = r + Layout<P>::WO;
-            const double* sc = s_a + (size_t)P * oc[t];
-            double* wo = Wb + (size_t)pos_cam[t] * kWStride;
-            for (int p = 0; p < P; ++p) {
-                const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
-                const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
-                double c[3];
-                for (int q = 0; q < 3; ++q) c[q] = (sc[p] * (t0 * jp[q] + t1 * jp[3 + q])) * sp[q];
-                const double w0 = c[0] / l00;
-                const double w1 = (c[1] - l10 * w0) / l11;
-                const double w2 = (c[2] - l20 * w0 - l21 * w1) / l22;
-                wo[3 * p + 0] = good ? w0 : 0.0;
-                wo[3 * p + 1] = good ? w1 : 0.0;
-                wo[3 * p + 2] = good ? w2 : 0.0;
-            }
-            wo[27] = 0.0;
-        }
     }
-    // deterministic block reduction of F_j = V_j^T V_j
     for (int k = 0; k < 28; ++k) red[threadIdx.x][k] = f[k];
     __syncthreads();
     for (int w = blockDim.x / 2; w > 0; w >>= 1) {
@@ -121,25 +107,81 @@ __global__ void k_point_prep(const int* off_pt, const int* idx_pt, const int* oc
     if (threadIdx.x < 28) Fpart[28 * (size_t)blockIdx.x + threadIdx.x] = red[0][threadIdx.x];
 }
 
-// F = Σ partials (fixed order); L_F = chol(F); eig(E = -F) for diagnostics.
-__global__ void k_border_factor(const double* Fpart, int nblocks, double* LF, double* Eout, double* eigE,
-                                Status* st) {
+// W_a = C_s,a L_j^-T (P x 3) per observation (thread per observation, records
+// read in observation order), stored at the observation's by-camera slot.
+template <int P>
+__global__ void __launch_bounds__(128) k_obs_factor(const int* oc, const int* op, const int* pos_cam, const double* rec,
+                                                    const double* s_a, const double* Lpt, int t_count, int n,
+                                                    double* Wb) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= t_count) return;
+    const int ci = oc[t], pj = op[t];
+    const double* r = rec + (size_t)t * kRec;
+    double rr[kRec];
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+#pragma unroll
+    for (int q = 0; q < kRec / 2; ++q) { const double2 v = r2[q]; rr[2 * q] = v.x; rr[2 * q + 1] = v.y; }
+    const double* jc = rr + Layout<P>::JC;
+    const double* jp = rr + Layout<P>::JP;
+    const double* W = rr + Layout<P>::WO;
+    const double* sc = s_a + (size_t)P * ci;
+    const double* sp = s_a + (size_t)P * n + 3 * (size_t)pj;
+    const double* L = Lpt + 8 * (size_t)pj;
+    const double l00 = L[0], l10 = L[1], l11 = L[2], l20 = L[3], l21 = L[4], l22 = L[5];
+    const bool good = L[6] != 0.0;
+    double wo[kWStride];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
+        const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
+        double c[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) c[q] = (sc[p] * (t0 * jp[q] + t1 * jp[3 + q])) * sp[q];
+        const double w0 = c[0] / l00;
+        const double w1 = (c[1] - l10 * w0) / l11;
+        const double w2 = (c[2] - l20 * w0 - l21 * w1) / l22;
+        wo[3 * p + 0] = good ? w0 : 0.0;
+        wo[3 * p + 1] = good ? w1 : 0.0;
+        wo[3 * p + 2] = good ? w2 : 0.0;
+    }
+#pragma unroll
+    for (int k = 3 * P; k < kWStride; ++k) wo[k] = 0.0;
+    double2* o2 = reinterpret_cast<double2*>(Wb + (size_t)pos_cam[t] * kWStride);
+#pragma unroll
+    for (int q = 0; q < kWStride / 2; ++q) o2[q] = make_double2(wo[2 * q], wo[2 * q + 1]);
+}
+
+// F = Σ partials (fixed-order, 256-thread tree); L_F = chol(F); eig(E = -F)
+// for the diagnostics.
+__global__ void __launch_bounds__(128) k_border_factor(const double* Fpart, int nblocks, double* LF, double* Eout,
+                                                       double* eigE, Status* st) {
+    __shared__ double red[128][29];
+    double acc[28];
+#pragma unroll
+    for (int k = 0; k < 28; ++k) acc[k] = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += 128)
+#pragma unroll
+        for (int k = 0; k < 28; ++k) acc[k] += Fpart[28 * (size_t)b + k];
+    for (int k = 0; k < 28; ++k) red[threadIdx.x][k] = acc[k];
+    __syncthreads();
+    for (int w = 64; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int k = 0; k < 28; ++k) red[threadIdx.x][k] += red[threadIdx.x + w][k];
+        __syncthreads();
+    }
     if (threadIdx.x != 0) return;
     double F[49];
     int k = 0;
     for (int l1 = 0; l1 < 7; ++l1)
         for (int l2 = l1; l2 < 7; ++l2, ++k) {
-            double acc = 0.0;
-            for (int b = 0; b < nblocks; ++b) acc += Fpart[28 * (size_t)b + k];
-            F[7 * l1 + l2] = acc;
-            F[7 * l2 + l1] = acc;
+            F[7 * l1 + l2] = red[0][k];
+            F[7 * l2 + l1] = red[0][k];
         }
     for (int q = 0; q < 49; ++q) Eout[q] = -F[q];
     double a[49], d[7], v[49];
     for (int q = 0; q < 49; ++q) a[q] = -F[q];
     jacobi_eig<7>(a, d, v);
     for (int q = 0; q < 7; ++q) eigE[q] = d[q];
-    // Cholesky of F (lower, row-major)
     double L[49];
     for (int q = 0; q < 49; ++q) L[q] = 0.0;
     bool ok = true;
@@ -163,26 +205,45 @@ __global__ void k_border_factor(const double* Fpart, int nblocks, double* LF, do
 // Γ_i[p][l] = H_s,ci[p][l] - Σ_{a in cam i} (W_a V_j(a))[p][l], ascending
 // observation order; then G_i = Γ_i L_F^-T.
 template <int P>
-__global__ void k_camera_border(const int* off_cam, const int* idx_cam, const int* op, const double* Wb,
-                                const double* V, const double* cams, const double* Hr, const double* s_a,
-                                const double* s_b, const double* LF, int n, double* Gamma, double* G) {
+__global__ void __launch_bounds__(64) k_camera_border(const int* off_cam, const int* idx_cam, const int* op,
+                                                      const double* Wb, const double* V, const double* cams,
+                                                      const double* Hr, const double* s_a, const double* s_b,
+                                                      const double* LF, int n, double* Gamma, double* G) {
     constexpr int NE = P * 7;
-    __shared__ double sh[4][NE];
+    constexpr int CH = 32, RS = 49;  // staged: W (27) at 0, V_j (21) at 27
+    __shared__ double stage[2][CH][RS];
+    __shared__ double sh[2][NE];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i = blockIdx.x * 4 + wib;
+    const int i = blockIdx.x * 2 + wib;
     if (i >= n) return;
     double acc[3] = {0.0, 0.0, 0.0};
-    for (int k = off_cam[i]; k < off_cam[i + 1]; ++k) {
-        const double* w = Wb + (size_t)k * kWStride;
-        const double* vj = V + 21 * (size_t)op[idx_cam[k]];
+    const int b = off_cam[i], e = off_cam[i + 1];
+    for (int k0 = b; k0 < e; k0 += CH) {
+        const int nc = min(CH, e - k0);
+        // W rows of this chunk are contiguous (by-camera slots): coalesced copy
+        for (int q = lane; q < nc * 27; q += 32) {
+            const int o = q / 27, c = q - o * 27;
+            stage[wib][o][c] = Wb[(size_t)(k0 + o) * kWStride + c];
+        }
+        if (lane < nc) {
+            const double* vj = V + 21 * (size_t)op[idx_cam[k0 + lane]];
 #pragma unroll
-        for (int s = 0; s < 3; ++s) {
-            const int en = lane + 32 * s;
-            if (en < NE) {
-                const int p = en / 7, l = en % 7;
-                acc[s] += (w[3 * p] * vj[l] + w[3 * p + 1] * vj[7 + l]) + w[3 * p + 2] * vj[14 + l];
+            for (int c = 0; c < 21; ++c) stage[wib][lane][27 + c] = vj[c];
+        }
+        __syncwarp();
+        for (int o = 0; o < nc; ++o) {
+            const double* w = stage[wib][o];
+            const double* vj = w + 27;
+#pragma unroll
+            for (int s = 0; s < 3; ++s) {
+                const int en = lane + 32 * s;
+                if (en < NE) {
+                    const int p = en / 7, l = en % 7;
+                    acc[s] += (w[3 * p] * vj[l] + w[3 * p + 1] * vj[7 + l]) + w[3 * p + 2] * vj[14 + l];
+                }
             }
         }
+        __syncwarp();
     }
     const double* C = cams + (size_t)P * i + 3;
     double sx[9];
@@ -349,16 +410,21 @@ __global__ void __launch_bounds__(256) k_pair_reduce(const unsigned int* ukeys, 
 int point_prep_blocks(int m) { return (int)cdiv(m > 0 ? m : 1, 128); }
 
 void launch_point_prep(const SceneDev& sc, const IndexDev& ix, const double* rec, const double* A, const double* s_a,
-                       const double* s_b, double* Wb, double* V, double* Fpart, Status* st, cudaStream_t s) {
+                       const double* s_b, double* Lpt, double* Wb, double* V, double* Fpart, Status* st, cudaStream_t s) {
     const int nb = point_prep_blocks(sc.m);
-    if (sc.P == 8) k_point_prep<8><<<nb, 128, 0, s>>>(ix.off_pt, ix.idx_pt, sc.oc, ix.pos_cam, rec, A, s_a, sc.pts, s_b, sc.m, sc.n, Wb, V, Fpart, st);
-    else k_point_prep<9><<<nb, 128, 0, s>>>(ix.off_pt, ix.idx_pt, sc.oc, ix.pos_cam, rec, A, s_a, sc.pts, s_b, sc.m, sc.n, Wb, V, Fpart, st);
+    if (sc.P == 8) k_point_prep<8><<<nb, 128, 0, s>>>(A, s_a, sc.pts, s_b, sc.m, sc.n, Lpt, V, Fpart, st);
+    else k_point_prep<9><<<nb, 128, 0, s>>>(A, s_a, sc.pts, s_b, sc.m, sc.n, Lpt, V, Fpart, st);
     SFM_LAUNCH_CHECK();
+    if (sc.t) {
+        if (sc.P == 8) k_obs_factor<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.oc, sc.op, ix.pos_cam, rec, s_a, Lpt, sc.t, sc.n, Wb);
+        else k_obs_factor<9><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.oc, sc.op, ix.pos_cam, rec, s_a, Lpt, sc.t, sc.n, Wb);
+        SFM_LAUNCH_CHECK();
+    }
 }
 
 void launch_border_factor(const double* Fpart, int nblocks, double* LF, double* E, double* eigE, Status* st,
                           cudaStream_t s) {
-    k_border_factor<<<1, 32, 0, s>>>(Fpart, nblocks, LF, E, eigE, st);
+    k_border_factor<<<1, 128, 0, s>>>(Fpart, nblocks, LF, E, eigE, st);
     SFM_LAUNCH_CHECK();
 }
 
@@ -366,8 +432,8 @@ void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* 
                           const double* s_a, const double* s_b, const double* LF, double* Gamma, double* G,
                           cudaStream_t s) {
     if (!sc.n) return;
-    if (sc.P == 8) k_camera_border<8><<<cdiv(sc.n, 4), 128, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
-    else k_camera_border<9><<<cdiv(sc.n, 4), 128, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    if (sc.P == 8) k_camera_border<8><<<cdiv(sc.n, 2), 64, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    else k_camera_border<9><<<cdiv(sc.n, 2), 64, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
     SFM_LAUNCH_CHECK();
 }
 

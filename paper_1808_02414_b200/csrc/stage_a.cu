@@ -151,11 +151,14 @@ __global__ void k_depth_of(const double* cams, const double* Rc, const double* p
 // ascending observation order; lane-owned entries keep each sum sequential.
 // Then H_r = eig-inverse(normal)·rhs (nullspace.cpp:52-61) and s_a = 1/sqrt(diag D).
 template <int P>
-__global__ void k_camera_reduce(const int* off_cam, const int* idx_cam, const double* rec, const double* cams,
-                                const double* pts, const int* op, int n, double* D, double* Hr, double* s_a,
-                                unsigned char* flags, Status* st) {
+__global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const int* idx_cam, const double* rec,
+                                                       const double* cams, const double* pts, const int* op, int n,
+                                                       double* D, double* Hr, double* s_a, unsigned char* flags,
+                                                       Status* st) {
     constexpr int NE = P * P + 18;
     constexpr int NS = (NE + 31) / 32;
+    constexpr int CH = 32, RS = kRec + 4;  // staged record: [jc | jp | W | pad] + X(3) at 28..30
+    __shared__ double stage[4][CH][RS];
     __shared__ double sh[4][NE];
     const int wib = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -168,38 +171,50 @@ __global__ void k_camera_reduce(const int* off_cam, const int* idx_cam, const do
 #pragma unroll
     for (int s = 0; s < NS; ++s) acc[s] = 0.0;
     const int b = off_cam[i], e = off_cam[i + 1];
-    for (int k = b; k < e; ++k) {
-        const int t = idx_cam[k];
-        const double* r = rec + (size_t)t * kRec;
-        const double* jc = r + Layout<P>::JC;
-        const double* jp = r + Layout<P>::JP;
-        const double* W = r + Layout<P>::WO;
+    for (int k0 = b; k0 < e; k0 += CH) {
+        const int nc = min(CH, e - k0);
+        if (lane < nc) {
+            const int t = idx_cam[k0 + lane];
+            const double2* r2 = reinterpret_cast<const double2*>(rec + (size_t)t * kRec);
+            double* dst = stage[wib][lane];
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-            const int en = lane + 32 * s;
-            if (en >= NE) break;
-            if (en < P * P) {
-                const int p = en / P, q = en % P;
-                const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
-                const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
-                acc[s] += t0 * jc[q] + t1 * jc[P + q];
-            } else if (en < P * P + 9) {
-                const int p = (en - P * P) / 3, q = (en - P * P) % 3;
-                acc[s] += jc[p] * jc[q] + jc[P + p] * jc[P + q];
-            } else {
-                const int p = (en - P * P - 9) / 3, q = (en - P * P - 9) % 3;
-                const double* X = pts + 3 * (size_t)op[t];
-                double hx[9];
-                skew(X, hx);
-                double tg[2];
-                for (int ii = 0; ii < 2; ++ii) {
-                    const double a = (jc[P * ii + 3] * hc[0 + q] + jc[P * ii + 4] * hc[3 + q]) + jc[P * ii + 5] * hc[6 + q];
-                    const double bb = (jp[3 * ii + 0] * hx[0 + q] + jp[3 * ii + 1] * hx[3 + q]) + jp[3 * ii + 2] * hx[6 + q];
-                    tg[ii] = -(a + bb);
+            for (int q = 0; q < kRec / 2; ++q) { const double2 v = r2[q]; dst[2 * q] = v.x; dst[2 * q + 1] = v.y; }
+            const double* X = pts + 3 * (size_t)op[t];
+            dst[28] = X[0]; dst[29] = X[1]; dst[30] = X[2];
+        }
+        __syncwarp();
+        for (int o = 0; o < nc; ++o) {
+            const double* r = stage[wib][o];
+            const double* jc = r + Layout<P>::JC;
+            const double* jp = r + Layout<P>::JP;
+            const double* W = r + Layout<P>::WO;
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                const int en = lane + 32 * s;
+                if (en >= NE) break;
+                if (en < P * P) {
+                    const int p = en / P, q = en % P;
+                    const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
+                    const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
+                    acc[s] += t0 * jc[q] + t1 * jc[P + q];
+                } else if (en < P * P + 9) {
+                    const int p = (en - P * P) / 3, q = (en - P * P) % 3;
+                    acc[s] += jc[p] * jc[q] + jc[P + p] * jc[P + q];
+                } else {
+                    const int p = (en - P * P - 9) / 3, q = (en - P * P - 9) % 3;
+                    double hx[9];
+                    skew(r + 28, hx);
+                    double tg[2];
+                    for (int ii = 0; ii < 2; ++ii) {
+                        const double a = (jc[P * ii + 3] * hc[0 + q] + jc[P * ii + 4] * hc[3 + q]) + jc[P * ii + 5] * hc[6 + q];
+                        const double bb = (jp[3 * ii + 0] * hx[0 + q] + jp[3 * ii + 1] * hx[3 + q]) + jp[3 * ii + 2] * hx[6 + q];
+                        tg[ii] = -(a + bb);
+                    }
+                    acc[s] += jc[p] * tg[0] + jc[P + p] * tg[1];
                 }
-                acc[s] += jc[p] * tg[0] + jc[P + p] * tg[1];
             }
         }
+        __syncwarp();
     }
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
@@ -293,13 +308,22 @@ __global__ void k_border_partial(const double* cams, const double* Hr, const dou
         for (int l = 0; l < 7; ++l) partial[7 * (size_t)blockIdx.x + l] = red[0][l];
 }
 
-__global__ void k_border_final(const double* partial, int nblocks, double* s_b) {
-    const int l = threadIdx.x;
-    if (l >= 7) return;
-    double ss = 0.0;
-    for (int b = 0; b < nblocks; ++b) ss += partial[7 * (size_t)b + l];
-    const double norm = sqrt(ss);
-    s_b[l] = norm > 0.0 ? 1.0 / norm : 1.0;
+__global__ void __launch_bounds__(256) k_border_final(const double* partial, int nblocks, double* s_b) {
+    __shared__ double red[256][7];
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int b = threadIdx.x; b < nblocks; b += 256)
+        for (int l = 0; l < 7; ++l) acc[l] += partial[7 * (size_t)b + l];
+    for (int l = 0; l < 7; ++l) red[threadIdx.x][l] = acc[l];
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int l = 0; l < 7; ++l) red[threadIdx.x][l] += red[threadIdx.x + w][l];
+        __syncthreads();
+    }
+    if (threadIdx.x < 7) {
+        const double norm = sqrt(red[0][threadIdx.x]);
+        s_b[threadIdx.x] = norm > 0.0 ? 1.0 / norm : 1.0;
+    }
 }
 
 // ---- full H (nullspace API) ---------------------------------------------------
@@ -339,11 +363,10 @@ void launch_validate(const SceneDev& sc, int check_sigma, Status* st, int* cam_c
     SFM_CUDA(cudaMemsetAsync(cam_cnt, 0, sizeof(int) * (size_t)(sc.n + 1), s));
     SFM_CUDA(cudaMemsetAsync(pt_cnt, 0, sizeof(int) * (size_t)(sc.m + 1), s));
     if (check_sigma) {
-        if (sc.n) k_validate_cams<<<cdiv(sc.n, 256), 256, 0, s>>>(sc.cams, sc.n, sc.P, st);
-        if (sc.m) k_validate_pts<<<cdiv(sc.m, 256), 256, 0, s>>>(sc.pts, sc.m, st);
+        if (sc.n) { k_validate_cams<<<cdiv(sc.n, 256), 256, 0, s>>>(sc.cams, sc.n, sc.P, st); SFM_LAUNCH_CHECK(); }
+        if (sc.m) { k_validate_pts<<<cdiv(sc.m, 256), 256, 0, s>>>(sc.pts, sc.m, st); SFM_LAUNCH_CHECK(); }
     }
-    if (sc.t) k_validate_obs<<<cdiv(sc.t, 256), 256, 0, s>>>(sc.oc, sc.op, sc.u, sc.sigma, sc.t, sc.n, sc.m, check_sigma, st, cam_cnt, pt_cnt);
-    SFM_LAUNCH_CHECK();
+    if (sc.t) { k_validate_obs<<<cdiv(sc.t, 256), 256, 0, s>>>(sc.oc, sc.op, sc.u, sc.sigma, sc.t, sc.n, sc.m, check_sigma, st, cam_cnt, pt_cnt); SFM_LAUNCH_CHECK(); }
 }
 
 static int bits_for(int v) { int b = 1; while ((1LL << b) <= v) ++b; return b; }
@@ -375,17 +398,16 @@ void launch_build_index(const SceneDev& sc, const int* cam_cnt, const int* pt_cn
 
 void launch_structure_check(const SceneDev& sc, const IndexDev& ix, Status* st, cudaStream_t s) {
     const int g = sc.n > sc.m ? sc.n : sc.m;
-    if (g) k_structure_check<<<cdiv(g, 256), 256, 0, s>>>(ix.off_cam, sc.n, ix.off_pt, ix.idx_pt, sc.oc, sc.m, st);
-    SFM_LAUNCH_CHECK();
+    if (g) { k_structure_check<<<cdiv(g, 256), 256, 0, s>>>(ix.off_cam, sc.n, ix.off_pt, ix.idx_pt, sc.oc, sc.m, st); SFM_LAUNCH_CHECK(); }
 }
 
 void launch_jacobian(const SceneDev& sc, double* R, double* rec, Status* st, cudaStream_t s) {
-    if (sc.n) k_camera_rot<<<cdiv(sc.n, 128), 128, 0, s>>>(sc.cams, sc.n, sc.P, R);
+    if (sc.n) { k_camera_rot<<<cdiv(sc.n, 128), 128, 0, s>>>(sc.cams, sc.n, sc.P, R); SFM_LAUNCH_CHECK(); }
     if (sc.t) {
         if (sc.P == 8) k_jacobian<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, sc.sigma, sc.t, rec, st);
         else k_jacobian<9><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, sc.sigma, sc.t, rec, st);
+        SFM_LAUNCH_CHECK();
     }
-    SFM_LAUNCH_CHECK();
 }
 
 void launch_depth_of(const SceneDev& sc, const double* R, int t, double* out, cudaStream_t s) {
@@ -400,12 +422,13 @@ void launch_reductions(const SceneDev& sc, const IndexDev& ix, const double* rec
     if (sc.n) {
         if (sc.P == 8) k_camera_reduce<8><<<cdiv(sc.n, 4), 128, 0, s>>>(ix.off_cam, ix.idx_cam, rec, sc.cams, sc.pts, sc.op, sc.n, D, Hr, s_a, flags, st);
         else k_camera_reduce<9><<<cdiv(sc.n, 4), 128, 0, s>>>(ix.off_cam, ix.idx_cam, rec, sc.cams, sc.pts, sc.op, sc.n, D, Hr, s_a, flags, st);
+        SFM_LAUNCH_CHECK();
     }
     if (sc.m) {
         if (sc.P == 8) k_point_reduce<8><<<cdiv(sc.m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, rec, sc.m, sc.n, A, s_a, flags, st);
         else k_point_reduce<9><<<cdiv(sc.m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, rec, sc.m, sc.n, A, s_a, flags, st);
+        SFM_LAUNCH_CHECK();
     }
-    SFM_LAUNCH_CHECK();
 }
 
 void launch_border_scales(const SceneDev& sc, const double* Hr, const double* s_a, double* partial, double* s_b,
@@ -414,7 +437,8 @@ void launch_border_scales(const SceneDev& sc, const double* Hr, const double* s_
     const int nb = (int)cdiv(g > 0 ? g : 1, 256);
     if (sc.P == 8) k_border_partial<8><<<nb, 256, 0, s>>>(sc.cams, Hr, sc.pts, s_a, sc.n, sc.m, partial);
     else k_border_partial<9><<<nb, 256, 0, s>>>(sc.cams, Hr, sc.pts, s_a, sc.n, sc.m, partial);
-    k_border_final<<<1, 32, 0, s>>>(partial, nb, s_b);
+    SFM_LAUNCH_CHECK();
+    k_border_final<<<1, 256, 0, s>>>(partial, nb, s_b);
     SFM_LAUNCH_CHECK();
 }
 

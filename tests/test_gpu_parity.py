@@ -1,0 +1,302 @@
+"""GPU parity tests: the sm_100a path (through the C ABI) against the CPU
+restatement of the reference path (oracle/) and the golden fixtures.
+
+Bars (BASELINE.json north_star): Jacobian, gauge nullspace, Fisher blocks and
+the observation index bit-exact; per-camera covariance blocks within 1e-9
+relative Frobenius error."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import disconnected_scene, rel
+from oracle import oracle as O
+from paper_1808_02414_b200 import sfmcov as F
+from paper_1808_02414_b200 import synthetic as S
+from paper_1808_02414_b200.rotation import random_rotation
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+COV_TOL = 1e-9
+
+
+def golden(name):
+    g = dict(np.load(GOLDEN / f"{name}.npz"))
+    return F.Reconstruction(g["cams"], g["pts"], g["obs_cam"], g["obs_pt"], g["obs_u"], g["obs_sigma"]), g
+
+
+def worst_block(a, b):
+    return max(rel(x, y) for x, y in zip(a, b))
+
+
+SMALL = {
+    "cube_p8": lambda: S.generate_cube_scene(1, 0.5),
+    "cube_p9": lambda: S.generate_cube_scene(2, 0.5, 9),
+    "ring_p8": lambda: S.generate_random_scene(12, 90, 0.4, 9, 0.5),
+    "ring_p9": lambda: S.generate_random_scene(16, 200, 0.3, 4, 0.7, 9),
+    "ring64_p8": lambda: S.generate_random_scene(64, 200, 0.40625, 13, 0.5),
+    "config1": lambda: S.generate_config(1),
+    "config2": lambda: S.generate_config(2),
+}
+
+
+# ---- golden fixtures ----------------------------------------------------------------
+@pytest.mark.parametrize("name", sorted(p.stem for p in GOLDEN.glob("*.npz")))
+def test_golden_fixture(engine, name):
+    rec, g = golden(name)
+    J = engine.assemble_jacobian(rec)
+    assert np.array_equal(J.cam_blocks, g["jc"]) and np.array_equal(J.point_blocks, g["jp"])
+    assert np.array_equal(engine.gauge_nullspace(rec), g["H"])
+    res = engine.compute_covariance(rec)
+    assert worst_block(res.camera_cov, g["cov"]) <= COV_TOL
+    assert [res.diagnostics.inertia_positive, res.diagnostics.inertia_negative] == list(g["inertia"])
+    assert res.diagnostics.largest_dense_dim == int(g["dense_dim"][0])
+
+
+# ---- stage-by-stage parity ----------------------------------------------------------
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_observation_index_bit_exact(engine, name):
+    rec = SMALL[name]()
+    oc, ic, op, ip = O.observation_index(rec)
+    ix = engine.build_observation_index(rec)
+    assert np.array_equal(ix.off_cam, oc) and np.array_equal(ix.idx_cam, ic)
+    assert np.array_equal(ix.off_pt, op) and np.array_equal(ix.idx_pt, ip)
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_jacobian_bit_exact(engine, name):
+    rec = SMALL[name]()
+    jc, jp = O.jacobian(rec)
+    J = engine.assemble_jacobian(rec)
+    assert np.array_equal(J.cam_blocks, jc) and np.array_equal(J.point_blocks, jp)
+    assert np.array_equal(J.cam_blocks[:, :, 3:6], -J.point_blocks)  # d_C == -d_X bitwise
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_nullspace_bit_exact(engine, name):
+    rec = SMALL[name]()
+    H, _ = O.nullspace(rec)
+    Hg = engine.gauge_nullspace(rec)
+    assert np.array_equal(Hg, H)
+    assert O.nullspace_residual(rec, Hg) < 1e-10
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_fisher_blocks_bit_exact(engine, name):
+    rec = SMALL[name]()
+    D, A, Cp, sa, sb, flagged = O.fisher(rec)
+    fb = engine.build_fisher_blocks(rec)
+    assert np.array_equal(fb.cam_blocks, D) and np.array_equal(fb.point_blocks, A)
+    assert np.array_equal(fb.couplings, Cp) and np.array_equal(fb.s_a, sa)
+    assert rel(fb.s_b, sb) < 1e-14  # 7 column norms: tree-ordered sum on the GPU
+    assert fb.flagged == flagged
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_schur_matches(engine, name):
+    rec = SMALL[name]()
+    z = O.schur(rec)
+    zg = engine.schur_reduce(rec)
+    assert rel(zg, z) < 1e-12
+    assert np.array_equal(zg, zg.T)
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_camera_covariance_parity(engine, name):
+    rec = SMALL[name]()
+    cov, d, flagged, _ = O.compute_covariance(rec)
+    res = engine.compute_covariance(rec)
+    assert worst_block(res.camera_cov, cov) <= COV_TOL
+    g = res.diagnostics
+    assert (g.inertia_positive, g.inertia_negative) == (d.inertia_positive, d.inertia_negative)
+    assert g.largest_dense_dim == d.largest_dense_dim
+    assert g.negative_eigenvalue_warnings == d.negative_eigenvalue_warnings == 0
+    assert g.min_pivot > 1e-12 * g.max_pivot
+    assert g.flagged_columns == flagged
+    assert g.scale_min == pytest.approx(d.scale_min, rel=1e-15) and g.scale_max == pytest.approx(d.scale_max, rel=1e-15)
+    for c in res.camera_cov:
+        assert np.abs(c - c.T).max() <= 1e-14 * np.abs(c).max() and np.diag(c).min() > 0
+
+
+def test_config3_parity(engine):
+    """Full BASELINE config 3 (1000 cameras, Z 9000^2) against the restatement."""
+    rec = S.generate_config(3)
+    O.lib().oracle_blas_threads(0)
+    cov, d, _, _ = O.compute_covariance(rec, threads=16)
+    res = engine.compute_covariance(rec)
+    assert worst_block(res.camera_cov, cov) <= COV_TOL
+
+
+def test_matches_dense_pseudoinverse(engine):  # test_oracle.cpp:90-101
+    rec = S.generate_random_scene(10, 80, 0.4, 6, 0.5)
+    gt, *_ = O.pseudoinverse(rec)
+    res = engine.compute_covariance(rec)
+    assert O.error_metric(gt, res.camera_cov, rec.cams)[0] < 1e-4
+    assert worst_block(res.camera_cov, gt) < 1e-6
+
+
+# ---- invariances and determinism ------------------------------------------------------
+def test_repeat_and_thread_options_bitwise(engine):  # test_covariance.cpp:137-156, acceptance 8
+    rec = S.generate_random_scene(150, 800, 20.0 / 150.0, 5, 0.5)
+    a = engine.compute_covariance(rec, F.CovarianceOptions(threads=1)).camera_cov
+    b = engine.compute_covariance(rec, F.CovarianceOptions(threads=1)).camera_cov
+    c = engine.compute_covariance(rec, F.CovarianceOptions(threads=4)).camera_cov
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+def test_relabelling_points(engine):  # test_covariance.cpp:92-104
+    rec = S.generate_config(2)
+    m = rec.num_points()
+    perm = np.random.default_rng(5).permutation(m)
+    moved = rec.copy()
+    moved.pts[perm] = rec.pts
+    moved.obs_pt = perm[rec.obs_pt].astype(np.int32)
+    a = engine.compute_covariance(rec).camera_cov
+    b = engine.compute_covariance(moved).camera_cov
+    assert worst_block(a, b) < 1e-10
+
+
+def test_observation_order_invariance(engine):
+    rec = S.generate_config(2)
+    perm = np.random.default_rng(6).permutation(rec.num_observations())
+    moved = rec.copy()
+    for k in ("obs_cam", "obs_pt", "obs_u", "obs_sigma"):
+        setattr(moved, k, np.ascontiguousarray(getattr(rec, k)[perm]))
+    a = engine.compute_covariance(rec).camera_cov
+    b = engine.compute_covariance(moved).camera_cov
+    assert worst_block(a, b) < 1e-10
+
+
+def test_intrinsics_invariant_under_similarity(engine):  # test_covariance.cpp:106-118
+    rng = np.random.default_rng(11)
+    rec = S.generate_random_scene(10, 80, 0.4, 7, 0.5)
+    moved = S.transform_scene(rec, random_rotation(rng), np.array([2.0, 5.0, -1.0]), 0.6)
+    a = engine.compute_covariance(rec).camera_cov
+    b = engine.compute_covariance(moved).camera_cov
+    for x, y in zip(a, b):
+        assert rel(x[6:8, 6:8], y[6:8, 6:8]) < 1e-6
+
+
+# ---- dense kernels on arbitrary SPD matrices --------------------------------------------
+@pytest.mark.parametrize("n,block", [(8, 8), (126, 9), (1000, 8), (2700, 9), (4104, 9)])
+def test_spd_inverse_blocks(engine, n, block):
+    rng = np.random.default_rng(n)
+    M = rng.standard_normal((n, n))
+    A = M @ M.T / n + np.eye(n)
+    blocks, (mn, mx) = engine.spd_inverse_blocks(A, block)
+    Ai = np.linalg.inv(A)
+    for i in range(n // block):
+        assert rel(blocks[i], Ai[block * i:block * i + block, block * i:block * i + block]) < 1e-12
+    L = np.linalg.cholesky(A)
+    piv = np.diag(L) ** 2
+    assert mn == pytest.approx(piv.min(), rel=1e-12) and mx == pytest.approx(piv.max(), rel=1e-12)
+
+
+def test_spd_inverse_rejects_indefinite(engine):
+    A = np.eye(256)
+    A[100, 100] = -1.0
+    with pytest.raises(F.Error) as e:
+        engine.spd_inverse_blocks(A, 8)
+    assert e.value.stage == "factorization" and "index 100" in str(e.value)
+
+
+# ---- error behaviour (kinds, stages, message fragments) ----------------------------------
+def test_behind_camera_names_the_observation(engine):  # test_projection.cpp:103-110
+    rec = S.generate_cube_scene(4, 0.0)
+    rec.pts[5] = rec.cams[0, 3:6]
+    with pytest.raises(F.Error) as e:
+        engine.assemble_jacobian(rec)
+    assert e.value.kind == F.ErrorKind.degenerate and e.value.stage == "jacobian"
+    assert "observation 5" in str(e.value) and "behind camera" in str(e.value)
+
+
+def test_non_spd_sigma_in_fisher(engine):  # test_fisher.cpp:70-89
+    rec = S.generate_cube_scene(3, 0.5)
+    rec.obs_sigma[7] = [[1.0, 2.0], [2.0, 1.0]]
+    with pytest.raises(F.Error) as e:
+        engine.build_fisher_blocks(rec)
+    assert e.value.kind == F.ErrorKind.degenerate and e.value.stage == "fisher" and "observation 7" in str(e.value)
+    rec.obs_sigma[7] = 0.0
+    with pytest.raises(F.Error):
+        engine.build_fisher_blocks(rec)
+
+
+def test_singular_point_block(engine):  # test_schur.cpp:82-93
+    """Point 5 seen only by two cameras at the same centre: its 3x3 block is
+    rank 2 (parallel rays) and the Schur stage names it."""
+    rec = S.generate_cube_scene(4, 0.5)
+    m = rec.num_points()
+    rec.cams = np.vstack([rec.cams, rec.cams[0]])  # camera 6: copy of camera 0
+    rec.cams[6, 7] = 0.0
+    extra_pts = np.array([rec.cams[0, 3:6] * 0.5])
+    rec.pts = np.vstack([rec.pts, extra_pts])
+    obs_c = [0, 6, 6, 6, 6]
+    obs_p = [m, m, 0, 1, 2]
+    rec.obs_cam = np.concatenate([rec.obs_cam, obs_c]).astype(np.int32)
+    rec.obs_pt = np.concatenate([rec.obs_pt, obs_p]).astype(np.int32)
+    rec.obs_u = np.vstack([rec.obs_u, np.zeros((5, 2))])
+    rec.obs_sigma = np.concatenate([rec.obs_sigma, np.broadcast_to(np.eye(2), (5, 2, 2))])
+    with pytest.raises(O.OracleFailure) as eo:
+        O.compute_covariance(rec)
+    with pytest.raises(F.Error) as e:
+        engine.compute_covariance(rec)
+    assert e.value.stage == eo.value.stage
+    if eo.value.stage == "schur":
+        assert f"point {m}" in str(e.value) and f"point {m}" in str(eo.value)
+
+
+def test_disconnected_scene_fails_in_factorization(engine):  # test_covariance.cpp:80-90
+    with pytest.raises(F.Error) as e:
+        engine.compute_covariance(disconnected_scene(4, 0.5))
+    assert e.value.kind == F.ErrorKind.degenerate and e.value.stage == "factorization"
+    assert "disconnected" in str(e.value)
+
+
+@pytest.mark.parametrize("mutate,fragment", [
+    (lambda r: r.cams.__setitem__((2, 0), np.nan), "validate: camera 2 has non-finite parameters"),
+    (lambda r: r.cams.__setitem__((1, 6), -1.0), "validate: camera 1 has non-positive focal length"),
+    (lambda r: r.pts.__setitem__((4, 1), np.inf), "validate: point 4 has non-finite coordinates"),
+    (lambda r: r.obs_cam.__setitem__(3, 99), "validate: observation 3 camera index out of range"),
+    (lambda r: r.obs_pt.__setitem__(5, -1), "validate: observation 5 point index out of range"),
+    (lambda r: r.obs_sigma.__setitem__((6, 0, 1), 0.3), "validate: observation 6 covariance not symmetric"),
+    (lambda r: r.obs_sigma.__setitem__(8, -np.eye(2)), "validate: observation 8 covariance not positive definite"),
+    (lambda r: r.obs_u.__setitem__((9, 0), np.nan), "validate: observation 9 has non-finite values"),
+    (lambda r: r.obs_pt.__setitem__(1, r.obs_pt[0]), "validate: duplicate (camera, point) observation pair"),
+])
+def test_validation_messages_match_the_restatement(engine, mutate, fragment):
+    rec = S.generate_cube_scene(1, 0.5)
+    mutate(rec)
+    with pytest.raises(F.Error) as e:
+        engine.compute_covariance(rec)
+    with pytest.raises(O.OracleFailure) as eo:
+        O.compute_covariance(rec)
+    assert str(e.value) == str(eo.value) and fragment in str(e.value)
+    assert e.value.kind == F.ErrorKind.invariant
+
+
+def test_count_floor_messages(engine):
+    rec = S.generate_cube_scene(1, 0.5)
+    keep = rec.obs_cam != 2
+    keep[np.flatnonzero(rec.obs_cam == 2)[:3]] = True
+    for k in ("obs_cam", "obs_pt", "obs_u", "obs_sigma"):
+        setattr(rec, k, np.ascontiguousarray(getattr(rec, k)[keep]))
+    with pytest.raises(F.Error) as e:
+        engine.compute_covariance(rec)
+    with pytest.raises(O.OracleFailure) as eo:
+        O.compute_covariance(rec)
+    assert str(e.value) == str(eo.value)
+
+
+def test_options_not_yet_supported_are_refused(engine):
+    rec = S.generate_cube_scene(1, 0.5)
+    with pytest.raises(F.Error) as e:
+        engine.compute_covariance(rec, F.CovarianceOptions(point_covariances=True))
+    assert e.value.kind == F.ErrorKind.dimension
+
+
+def test_empty_reconstruction_is_rejected(engine):  # test_covariance.cpp:131-135
+    rec = F.Reconstruction(np.zeros((0, 8)), np.zeros((0, 3)), np.zeros(0, np.int32), np.zeros(0, np.int32),
+                           np.zeros((0, 2)), np.zeros((0, 2, 2)))
+    with pytest.raises(F.Error):
+        engine.compute_covariance(rec)

@@ -189,12 +189,12 @@ void throw_numeric(sfmcov_handle* h, const SceneDev& sc, Mode mode) {
                            "; the scene is likely disconnected or its gauge degenerate"};
 }
 
-// Dense panel width in kNB blocks (SFMCOV_PANEL, default 2).
+// Dense panel width in kNB blocks (SFMCOV_PANEL, default 3).
 int panel_blocks() {
     static int g = [] {
         const char* e = std::getenv("SFMCOV_PANEL");
         const int v = e ? std::atoi(e) : 0;
-        return (v >= 1 && v <= 8) ? v : 2;
+        return (v >= 1 && v <= 8) ? v : 3;
     }();
     return g;
 }

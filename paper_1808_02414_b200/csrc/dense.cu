@@ -118,7 +118,9 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
                 acc[mi][ni][1] = 0.0;
             }
         }
-    const double sgn = g.alpha_neg ? -1.0 : 1.0;
+    // alpha = -1: flip the sign bit of the A fragments on the integer pipe
+    // (a DMUL would share the FP64 pipe with DMMA).
+    const unsigned neg_hi = g.alpha_neg ? 0x80000000u : 0u;
 
 #pragma unroll 1
     for (int kc = 0; kc < NK; ++kc) {
@@ -133,7 +135,10 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
             const int krow = kk * 4 + (lane & 3);
             double af[4], bf[4];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) af[mi] = sgn * as[krow * LDS + wm * 32 + mi * 8 + cq];
+            for (int mi = 0; mi < 4; ++mi) {
+                const double v = as[krow * LDS + wm * 32 + mi * 8 + cq];
+                af[mi] = __hiloint2double(__double2hiint(v) ^ (int)neg_hi, __double2loint(v));
+            }
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni)
                 bf[ni] = BK_MAJOR ? bs[(wn * 32 + ni * 8 + cq) * LDB_K + krow] : bs[krow * LDS + wn * 32 + ni * 8 + cq];
@@ -179,68 +184,99 @@ void launch_gemm(const GemmArgs& g, cudaStream_t s) {
 #ifdef SFM_POTRF_TIMING
 __device__ long long g_potrf_stamp[64];
 #define POTRF_STAMP(i) do { __syncthreads(); if (threadIdx.x == 0) g_potrf_stamp[i] = clock64(); } while (0)
+void debug_potrf_stamps(long long* out) { cudaMemcpyFromSymbol(out, g_potrf_stamp, 64 * sizeof(long long)); }
 #else
 #define POTRF_STAMP(i) do { } while (0)
 #endif
 
-namespace potrf_consts {
-constexpr int LDT = kNB + 1;
-}
+// ----------------------------------------------------------------------------
+// Diagonal tile: Cholesky + triangular inverse of one kNB x kNB tile in smem.
+//
+// 8-wide right-looking steps.  Each 8x8 diagonal block is factored and
+// inverted by one warp in registers (shuffles, rsqrt pivots); the panel
+// solve below it is one row per thread; the in-tile trailing update and the
+// block forward substitution for Y = L^-1 are 8x8 DMMA tiles spread over the
+// warps.  Y's strictly-lower 8-blocks are stored transposed in the unused
+// upper triangle of the tile, its diagonal blocks in Xd.
+// ----------------------------------------------------------------------------
 namespace potrf {
-constexpr int LDT = potrf_consts::LDT;
-constexpr int BS = 32;
-constexpr int NBLK = kNB / BS;  // 4
-constexpr int LDX = BS + 1;
-constexpr int THREADS = 256;
-constexpr int SMEM = (kNB * LDT + (2 * NBLK - 1) * BS * LDX + kNB) * 8;
+constexpr int LDT = kNB + 8;  // 136: conflict-free m8n8k4 fragment reads
+constexpr int SB = 8;
+constexpr int NSB = kNB / SB;  // 16
+constexpr int THREADS = 512;
+constexpr int NWARPS = THREADS / 32;
+constexpr int SMEM = (kNB * LDT + NSB * 64 + NWARPS * 64 + 2 * kNB) * 8;
 }  // namespace potrf
 
-// Warp-level Cholesky of the 32x32 block at T(c0, c0) (col-major, ld LDT),
-// in place in shared memory: lane i owns row i.  Compact loops on purpose —
-// a fully unrolled register version is ~250 KB of SASS and runs from L2
-// instead of the instruction cache.  Writes L, its inverse X (row-major
-// Xd[r * LDX + c]) and 1/L_jj (rinv).  Pivots (= L_jj^2) go to piv.
-__device__ __noinline__ void warp_potrf32(double* T, int c0, double* Xd, double* rinv, double* piv, int gcol0,
-                                          Status* st) {
+// 1/sqrt(d) for d > 0: MUFU.RSQ64H seed + 3 Newton steps (full double
+// precision without the libdevice call on the per-column critical path).
+__device__ __forceinline__ double fast_rsqrt(double d) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    const double hd = 0.5 * d;
+#pragma unroll
+    for (int it = 0; it < 3; ++it) y = y * (1.5 - hd * y * y);  // seed ~2^-23: 3 steps -> < 1 ulp
+    return y;
+}
+
+// 8x8 Cholesky of the block at T(c0, c0) by one warp (lanes 0..7 hold
+// rows); stores L and 1/L_jj (rinv).  Pivots L_jj^2 -> piv.
+__device__ __forceinline__ void warp_potrf8(double* T, int c0, double* rinv, double* spiv) {
     using namespace potrf;
-    const int i = threadIdx.x & 31;
-    double* B = T + c0 * LDT + c0;  // B[c * LDT + r]
-#pragma unroll 1
-    for (int j = 0; j < BS; ++j) {
-        double d = B[j * LDT + j];
-        if (i == 0) {
-            piv[gcol0 + j] = d;
-            if (!(d > 0.0) || !isfinite(d)) atomicMin(&st->chol_bad, gcol0 + j);
-        }
-        if (!(d > 0.0) || !isfinite(d)) d = 1.0;
-        const double inv = rsqrt(d);
-        __syncwarp();
-        double lij = 0.0;
-        if (i == j) { B[j * LDT + j] = d * inv; rinv[c0 + j] = inv; }
-        else if (i > j) { lij = B[j * LDT + i] * inv; B[j * LDT + i] = lij; }
-        __syncwarp();
-#pragma unroll 4
-        for (int c = j + 1; c <= i; ++c) B[c * LDT + i] -= lij * B[j * LDT + c];
-        __syncwarp();
-    }
-    // inverse, column-oriented: lane c owns column c of X = L^-1
-    const int c = i;
-#pragma unroll 1
-    for (int r = 0; r < BS; ++r) {
-        double x;
-        if (r < c) {
-            x = 0.0;
-        } else if (r == c) {
-            x = rinv[c0 + r];
-        } else {
-            double s = 0.0;
-#pragma unroll 4
-            for (int k = c; k < r; ++k) s += B[k * LDT + r] * Xd[k * LDX + c];
-            x = -s * rinv[c0 + r];
-        }
-        Xd[r * LDX + c] = x;
-    }
+    // reconverge the warp first: shuffles on a diverged warp take the
+    // emulated WARPSYNC.COLLECTIVE path (~10x slower)
     __syncwarp();
+    const int i = threadIdx.x & 31;
+    double a[SB];
+#pragma unroll
+    for (int c = 0; c < SB; ++c) a[c] = (i < SB && c <= i) ? T[(c0 + c) * LDT + c0 + i] : 0.0;
+    double my_inv = 1.0;
+#pragma unroll
+    for (int j = 0; j < SB; ++j) {
+        double d = __shfl_sync(0xffffffffu, a[j], j);
+        if (i == j) spiv[c0 + j] = d;  // pivots (L_jj^2) and failures are flushed after the loop
+        if (!(d > 0.0) || !isfinite(d)) d = 1.0;
+        const double inv = fast_rsqrt(d);
+        if (i == j) { a[j] = d * inv; my_inv = inv; }
+        else if (i > j) a[j] = a[j] * inv;
+#pragma unroll
+        for (int c = j + 1; c < SB; ++c) {
+            const double lc = __shfl_sync(0xffffffffu, a[j], c);
+            if (i >= c) a[c] -= a[j] * lc;
+        }
+    }
+    if (i < SB) {
+#pragma unroll
+        for (int c = 0; c < SB; ++c)
+            if (c <= i) T[(c0 + c) * LDT + c0 + i] = a[c];
+        rinv[c0 + i] = my_inv;
+    }
+}
+
+// Inverse X = L^-1 of the 8x8 lower block at T(c0, c0) by one warp (lane c
+// owns column c), row-major into Xs.
+__device__ __forceinline__ void warp_inv8(const double* T, int c0, const double* rinv, double* Xs) {
+    using namespace potrf;
+    const int c = threadIdx.x & 31;
+    double x[SB];
+#pragma unroll
+    for (int r = 0; r < SB; ++r) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < r; ++k)
+            if (k >= c) s += T[(c0 + k) * LDT + c0 + r] * x[k];
+        x[r] = (r < c) ? 0.0 : ((r == c) ? rinv[c0 + r] : -s * rinv[c0 + r]);
+    }
+    if (c < SB) {
+#pragma unroll
+        for (int r = 0; r < SB; ++r) Xs[r * SB + c] = x[r];
+    }
+}
+
+__device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
 }
 
 // A: tile (k0, k0) of the matrix (col-major, ld).  Writes L (lower) back,
@@ -248,121 +284,139 @@ __device__ __noinline__ void warp_potrf32(double* T, int c0, double* Xd, double*
 __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, long long ld, double* Linv, double* pivots,
                                                                  int col0, Status* st) {
     using namespace potrf;
-    extern __shared__ double T[];                  // T[c * LDT + r]
-    double* Xd = T + kNB * LDT;                    // NBLK blocks, row-major 32 x LDX
-    double* S = Xd + NBLK * BS * LDX;              // NBLK-1 scratch blocks
-    double* rinv = S + (NBLK - 1) * BS * LDX;      // 1 / L_jj
-    const int tid = threadIdx.x, warp = tid >> 5;
+    extern __shared__ double T[];                 // T[c * LDT + r]
+    double* Xd = T + kNB * LDT;                   // NSB blocks, row-major 8x8
+    double* Ws = Xd + NSB * 64;                   // per-warp 8x8 scratch
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int fr = lane >> 2, fk = lane & 3;      // fragment row / k index
+    POTRF_STAMP(19);
+#pragma unroll 16
     for (int e = tid; e < kNB * kNB; e += THREADS) {
         const int r = e & (kNB - 1), c = e >> 7;
         T[c * LDT + r] = (r >= c) ? A[(size_t)c * ld + r] : 0.0;
     }
-    __syncthreads();
     POTRF_STAMP(0);
-    constexpr int MAXU = (kNB - BS) * BS / THREADS;  // 12
-    for (int kb = 0; kb < NBLK; ++kb) {
-        const int c0 = kb * BS;
-        double* X = Xd + kb * BS * LDX;
-        if (warp == 0) warp_potrf32(T, c0, X, rinv, pivots, col0 + c0, st);
+    double* rinv = Ws + NWARPS * 64;             // 1 / L_jj
+    double* spiv = rinv + kNB;                   // pivots
+    for (int s = 0; s < NSB; ++s) {
+        const int c0 = s * SB;
+        POTRF_STAMP(44 + s);
+        if (warp == 0) warp_potrf8(T, c0, rinv, spiv);
         __syncthreads();
-        POTRF_STAMP(1 + 3 * kb);
-        const int rows = kNB - c0 - BS;
+        if (s < 15) POTRF_STAMP(28 + s);
+        const int rows = kNB - c0 - SB;
         if (rows == 0) break;
-        // panel solve: L[r, c0 + c] = Σ_{k <= c} A[r, c0 + k] X[c, k]
-        double out[MAXU];
+        // panel solve by forward substitution, one row per thread:
+        // x_c = (a_c - Σ_{k<c} x_k L[c0+c][c0+k]) / L_cc
+        if (tid < rows) {
+            const int r = c0 + SB + tid;
+            double x[SB];
 #pragma unroll
-        for (int u = 0; u < MAXU; ++u) {
-            const int e = tid + u * THREADS;
-            out[u] = 0.0;
-            if (e < rows * BS) {
-                const int r = c0 + BS + (e % rows), c = e / rows;
-                double s = 0.0;
-                for (int k = 0; k <= c; ++k) s += T[(c0 + k) * LDT + r] * X[c * LDX + k];
-                out[u] = s;
+            for (int c = 0; c < SB; ++c) x[c] = T[(c0 + c) * LDT + r];
+#pragma unroll
+            for (int c = 0; c < SB; ++c) {
+                double v = x[c];
+#pragma unroll
+                for (int k = 0; k < c; ++k) v -= x[k] * T[(c0 + k) * LDT + c0 + c];
+                x[c] = v * rinv[c0 + c];
+            }
+#pragma unroll
+            for (int c = 0; c < SB; ++c) T[(c0 + c) * LDT + r] = x[c];
+        }
+        __syncthreads();
+        // trailing update T[r, c] -= Σ_k L[r, c0+k] L[c, c0+k], 8x8 DMMA tiles,
+        // two tiles per warp iteration for ILP
+        const int nt = rows / SB;
+        const int ntiles = nt * (nt + 1) / 2;
+        for (int t0 = 2 * warp; t0 < ntiles; t0 += 2 * NWARPS) {
+            double d[2][2];
+            double* cp[2];
+            int r0v[2], q0v[2];
+            const int cnt = (t0 + 1 < ntiles) ? 2 : 1;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int t = (u < cnt) ? t0 + u : t0;
+                int ti = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+                while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+                while (ti * (ti + 1) / 2 > t) --ti;
+                const int tj = t - ti * (ti + 1) / 2;
+                r0v[u] = c0 + SB + SB * ti;
+                q0v[u] = c0 + SB + SB * tj;
+                cp[u] = T + (q0v[u] + 2 * fk) * LDT + r0v[u] + fr;
+                d[u][0] = cp[u][0];
+                d[u][1] = cp[u][LDT];
+            }
+#pragma unroll
+            for (int kk = 0; kk < SB; kk += 4) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const double tv = T[(c0 + kk + fk) * LDT + r0v[u] + fr];
+                    const double av = __hiloint2double(__double2hiint(tv) ^ (int)0x80000000u, __double2loint(tv));
+                    const double bv = T[(c0 + kk + fk) * LDT + q0v[u] + fr];
+                    dmma8(d[u][0], d[u][1], av, bv);
+                }
+            }
+            for (int u = 0; u < cnt; ++u) {
+                cp[u][0] = d[u][0];
+                cp[u][LDT] = d[u][1];
             }
         }
         __syncthreads();
-#pragma unroll
-        for (int u = 0; u < MAXU; ++u) {
-            const int e = tid + u * THREADS;
-            if (e < rows * BS) {
-                const int r = c0 + BS + (e % rows), c = e / rows;
-                T[(c0 + c) * LDT + r] = out[u];
-            }
-        }
-        __syncthreads();
-        POTRF_STAMP(2 + 3 * kb);
-        // trailing update inside the tile, 4x4 micro-tiles of the lower part
-        const int tb = rows / 4;
-        for (int e = tid; e < tb * tb; e += THREADS) {
-            const int mi = e % tb, mj = e / tb;
-            if (mi < mj) continue;
-            const int r0 = c0 + BS + 4 * mi, cc0 = c0 + BS + 4 * mj;
-            double acc[4][4];
-#pragma unroll
-            for (int p = 0; p < 4; ++p)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
-            for (int k = 0; k < BS; ++k) {
-                double lr[4], lc[4];
-#pragma unroll
-                for (int p = 0; p < 4; ++p) { lr[p] = T[(c0 + k) * LDT + r0 + p]; lc[p] = T[(c0 + k) * LDT + cc0 + p]; }
-#pragma unroll
-                for (int p = 0; p < 4; ++p)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) acc[p][q] += lr[p] * lc[q];
-            }
-#pragma unroll
-            for (int p = 0; p < 4; ++p)
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (r0 + p >= cc0 + q) T[(cc0 + q) * LDT + r0 + p] -= acc[p][q];
-        }
-        __syncthreads();
-        POTRF_STAMP(3 + 3 * kb);
     }
+    if (tid < kNB) {
+        const double d = spiv[tid];
+        pivots[col0 + tid] = d;
+        if (!(d > 0.0) || !isfinite(d)) atomicMin(&st->chol_bad, col0 + tid);
+    }
+    // the sixteen 8x8 diagonal inverses, in parallel
+    for (int s = warp; s < NSB; s += NWARPS) warp_inv8(T, s * SB, rinv, Xd + s * 64);
+    __syncthreads();
+    POTRF_STAMP(1);
+    // Y = L^-1 by block rows: Y_ij = -X_i Σ_{k=j}^{i-1} L_ik Y_kj (j < i);
+    // Y_kj (k > j) lives transposed at T[(8k + r) LDT + 8j + c].
+    for (int bi = 1; bi < NSB; ++bi) {
+        for (int bj = warp; bj < bi; bj += NWARPS) {
+            double d0 = 0.0, d1 = 0.0;
+            for (int bk = bj; bk < bi; ++bk) {
+#pragma unroll
+                for (int kk = 0; kk < SB; kk += 4) {
+                    const double av = T[(SB * bk + kk + fk) * LDT + SB * bi + fr];  // L_ik[fr][kk+fk]
+                    const double bv = (bk == bj) ? Xd[bj * 64 + (kk + fk) * SB + fr]  // Y_jj[kk+fk][fr]
+                                                 : T[(SB * bk + kk + fk) * LDT + SB * bj + fr];
+                    dmma8(d0, d1, av, bv);
+                }
+            }
+            // S (C layout) -> scratch, then Y_ij = -X_i S
+            double* w = Ws + warp * 64;
+            w[fr * SB + 2 * fk] = d0;
+            w[fr * SB + 2 * fk + 1] = d1;
+            __syncwarp();
+            double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < SB; kk += 4) {
+                const double t = Xd[bi * 64 + fr * SB + kk + fk];  // -X_i[fr][kk+fk]
+                const double av = __hiloint2double(__double2hiint(t) ^ (int)0x80000000u, __double2loint(t));
+                const double bv = w[(kk + fk) * SB + fr];             // S[kk+fk][fr]
+                dmma8(y0, y1, av, bv);
+            }
+            __syncwarp();
+            // Y_ij[fr][2fk + q] -> T[(8 bi + fr) LDT + 8 bj + 2 fk + q]
+            T[(SB * bi + fr) * LDT + SB * bj + 2 * fk] = y0;
+            T[(SB * bi + fr) * LDT + SB * bj + 2 * fk + 1] = y1;
+        }
+        __syncthreads();
+    }
+    POTRF_STAMP(2);
     for (int e = tid; e < kNB * kNB; e += THREADS) {
         const int r = e & (kNB - 1), c = e >> 7;
+        const int bi = r / SB, bj = c / SB;
+        double y = 0.0;
+        if (bi == bj) { if ((r % SB) >= (c % SB)) y = Xd[bi * 64 + (r % SB) * SB + (c % SB)]; }
+        else if (bi > bj) y = T[r * LDT + c];
+        Linv[(size_t)c * kNB + r] = y;
         if (r >= c) A[(size_t)c * ld + r] = T[c * LDT + r];
     }
-    POTRF_STAMP(14);
-    // Y_ij = -X_i Σ_{k=j}^{i-1} L_ik Y_kj by block diagonals d = i - j; Y_kj
-    // (k > j) lives transposed at T[(32k + r) LDT + 32j + c], Y_jj = X_j.
-    for (int d = 1; d < NBLK; ++d) {
-        const int nblk = NBLK - d;
-        for (int e = tid; e < nblk * BS * BS; e += THREADS) {
-            const int b = e / (BS * BS), w = e % (BS * BS);
-            const int q = w % BS, cc = w / BS;
-            const int bi = d + b, bj = b;
-            const int gr = bi * BS + q;
-            double s = 0.0;
-            const double* xj = Xd + bj * BS * LDX;
-            for (int k = 0; k < BS; ++k) s += T[(bj * BS + k) * LDT + gr] * xj[k * LDX + cc];
-            for (int kr = (bj + 1) * BS; kr < bi * BS; ++kr) s += T[kr * LDT + gr] * T[kr * LDT + bj * BS + cc];
-            S[b * BS * LDX + q * LDX + cc] = s;
-        }
-        __syncthreads();
-        for (int e = tid; e < nblk * BS * BS; e += THREADS) {
-            const int b = e / (BS * BS), w = e % (BS * BS);
-            const int rr = w % BS, cc = w / BS;
-            const int bi = d + b, bj = b;
-            const double* xr = Xd + bi * BS * LDX + rr * LDX;
-            double acc = 0.0;
-            for (int q = 0; q <= rr; ++q) acc += xr[q] * S[b * BS * LDX + q * LDX + cc];
-            T[(bi * BS + rr) * LDT + bj * BS + cc] = -acc;
-        }
-        __syncthreads();
-        POTRF_STAMP(14 + d);
-    }
-    for (int e = tid; e < kNB * kNB; e += THREADS) {
-        const int r = e & (kNB - 1), c = e >> 7;
-        const int bi = r / BS, bj = c / BS;
-        double v = 0.0;
-        if (bi == bj) { if ((r % BS) >= (c % BS)) v = Xd[bi * BS * LDX + (r % BS) * LDX + (c % BS)]; }
-        else if (bi > bj) v = T[r * LDT + c];
-        Linv[(size_t)c * kNB + r] = v;
-    }
-    POTRF_STAMP(18);
+    POTRF_STAMP(3);
 }
 
 void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s) {
@@ -634,6 +688,11 @@ int dense_trtri(double* X, long long ld, int Npad, int G, const double* Linv, do
     double* inner_buf = Lp + (size_t)Npad * G * kNB;
     for (int b0 = 0; b0 < K; b0 += G) {
         const int g_here = (b0 + G <= K) ? G : K - b0;
+        // the K = W trailing product reads the panel's whole W x W diagonal
+        // block of X: its strictly upper tiles must be zero
+        for (int r = b0; r < b0 + g_here; ++r)
+            for (int c = r + 1; c < b0 + g_here; ++c)
+                SFM_CUDA(cudaMemset2DAsync(X + (size_t)c * kNB * ld + (size_t)r * kNB, 8 * ld, 0, 8 * kNB, kNB, s));
         for (int g = 0; g < g_here; ++g) {
             const int r = b0 + g;
             const double* Lr = Linv + (size_t)r * kNB * kNB;

@@ -300,3 +300,16 @@ def test_empty_reconstruction_is_rejected(engine):  # test_covariance.cpp:131-13
                            np.zeros((0, 2)), np.zeros((0, 2, 2)))
     with pytest.raises(F.Error):
         engine.compute_covariance(rec)
+
+
+def test_cpp_dropin_header():
+    """A reference-style C++ caller linked against libsfmcov_b200.so."""
+    import subprocess
+    exe = Path(__file__).resolve().parent / "cpp" / "dropin_test"
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    lines = out.stdout.strip().splitlines()
+    assert lines[-1] == "PASS"
+    block0 = np.array([float(v) for v in lines[-2].split()]).reshape(8, 8)
+    cov, *_ = O.compute_covariance(S.generate_cube_scene(1, 0.5))
+    assert rel(block0, cov[0]) <= COV_TOL

@@ -8,7 +8,7 @@
 #include <random>
 namespace sfm { long long g_kernel_launches = 0; }
 #ifdef SFM_POTRF_TIMING
-namespace sfm { extern __device__ long long g_potrf_stamp[64]; }
+namespace sfm { void debug_potrf_stamps(long long* out); }
 #endif
 using namespace sfm;
 
@@ -41,8 +41,10 @@ int main(int argc, char** argv) {
     }
 #ifdef SFM_POTRF_TIMING
     long long stamps[64];
-    cudaMemcpyFromSymbol(stamps, g_potrf_stamp, sizeof(stamps));
-    for (int i = 1; i <= 18; ++i) printf("  stamp %2d: +%lld cycles\n", i, stamps[i] - stamps[i - 1]);
+    debug_potrf_stamps(stamps);
+    printf("  load: %lld cycles\n", stamps[0] - stamps[19]);
+    for (int i = 1; i <= 3; ++i) printf("  stamp %2d: +%lld cycles\n", i, stamps[i] - stamps[i - 1]);
+    for (int s = 0; s < 15; ++s) printf("  step %2d: potrf8+sync %lld, rest %lld\n", s, stamps[28 + s] - stamps[44 + s], stamps[45 + s] - stamps[28 + s]);
 #endif
     // GEMM shapes
     for (int K : {128, 256, 384, 512}) {

@@ -199,6 +199,13 @@ int panel_blocks() {
     return g;
 }
 
+// SFMCOV_SERIAL_DENSE=1 runs the lookahead updates on the main stream
+// (debug aid: removes the two-stream overlap).
+bool serial_dense() {
+    static bool v = [] { const char* e = std::getenv("SFMCOV_SERIAL_DENSE"); return e && e[0] == '1'; }();
+    return v;
+}
+
 void mark(sfmcov_handle* h, int i) {
     if (h->profiling) SFM_CUDA(cudaEventRecord(h->ev[i], h->s));
 }
@@ -374,9 +381,10 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     double* piv = h->piv.as<double>((size_t)Npad);
     const int pw = panel_blocks();
     double* Lp = h->Lp.as<double>(trtri_lp_doubles(Npad, pw));
-    int launches = dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, h->s2, h->e1, h->e2);
+    cudaStream_t s2 = serial_dense() ? s : h->s2;
+    int launches = dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, s2, h->e1, h->e2);
     mark(h, 8);
-    launches += dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, h->s2, h->e1, h->e2);
+    launches += dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, s2, h->e1, h->e2);
     mark(h, 9);
     int* psd = h->psd.as<int>(1);
     SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));

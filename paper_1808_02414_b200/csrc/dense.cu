@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) {
             if (beta) {
-                const double2 c = *reinterpret_cast<const double2*>(C + (size_t)(wn * 32 + ni * 8 + cq) * g.ldc + wm * 32 + mi * 8 + rq);
+                const double2 c = __ldcg(reinterpret_cast<const double2*>(C + (size_t)(wn * 32 + ni * 8 + cq) * g.ldc + wm * 32 + mi * 8 + rq));
                 acc[mi][ni][0] = c.x;
                 acc[mi][ni][1] = c.y;
             } else {
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
 #pragma unroll 16
     for (int e = tid; e < kNB * kNB; e += THREADS) {
         const int r = e & (kNB - 1), c = e >> 7;
-        T[c * LDT + r] = (r >= c) ? A[(size_t)c * ld + r] : 0.0;
+        T[c * LDT + r] = (r >= c) ? __ldcg(A + (size_t)c * ld + r) : 0.0;
     }
     POTRF_STAMP(0);
     double* rinv = Ws + NWARPS * 64;             // 1 / L_jj
@@ -437,7 +437,7 @@ __global__ void k_copy_diag(double* X, long long ld, int k, const double* Linv) 
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= kNB * kNB) return;
     const int r = e & (kNB - 1), c = e >> 7;
-    X[(size_t)(k * kNB + c) * ld + (size_t)k * kNB + r] = Linv[(size_t)c * kNB + r];
+    X[(size_t)(k * kNB + c) * ld + (size_t)k * kNB + r] = __ldcg(Linv + (size_t)c * kNB + r);
 }
 
 void launch_copy_diag(double* X, long long ld, int k, const double* Linv, cudaStream_t s) {
@@ -451,7 +451,7 @@ __global__ void k_copy_panel(const double* X, long long ld, int k, int rows, dou
     const long long total = (long long)rows * kNB;
     if (e >= total) return;
     const int r = (int)(e % rows), c = (int)(e / rows);
-    Lp[(size_t)c * rows + r] = X[(size_t)(k * kNB + c) * ld + (size_t)(k + 1) * kNB + r];
+    Lp[(size_t)c * rows + r] = __ldcg(X + (size_t)(k * kNB + c) * ld + (size_t)(k + 1) * kNB + r);
 }
 
 void launch_copy_panel(const double* X, long long ld, int k, int rows, double* Lp, cudaStream_t s) {
@@ -468,7 +468,7 @@ __global__ void k_copy_panel_w(const double* X, long long ld, int b0, int G, int
     const long long total = (long long)rows * G * kNB;
     if (e >= total) return;
     const int r = (int)(e % rows), c = (int)(e / rows);
-    Lp[(size_t)c * rows + r] = X[(size_t)(b0 * kNB + c) * ld + (size_t)(b0 + G) * kNB + r];
+    Lp[(size_t)c * rows + r] = __ldcg(X + (size_t)(b0 * kNB + c) * ld + (size_t)(b0 + G) * kNB + r);
 }
 
 void launch_copy_panel_w(const double* X, long long ld, int b0, int G, int rows, double* Lp, cudaStream_t s) {
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(256) k_extract(const double* X, long long ld, 
     for (int r = c0 + threadIdx.x; r < N; r += 256) {
         double x[P];
 #pragma unroll
-        for (int p = 0; p < P; ++p) x[p] = (r >= c0 + p) ? X[(size_t)(c0 + p) * ld + r] : 0.0;
+        for (int p = 0; p < P; ++p) x[p] = (r >= c0 + p) ? __ldcg(X + (size_t)(c0 + p) * ld + r) : 0.0;
         int u = 0;
 #pragma unroll
         for (int p = 0; p < P; ++p)

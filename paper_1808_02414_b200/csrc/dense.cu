@@ -13,6 +13,8 @@
 // CTA tile 128x128, 16 warps of 32x32, 3-stage cp.async pipeline over K.
 // The accumulator fragment is laid out so each lane owns two consecutive
 // rows of one column: C tiles move with 16-byte loads/stores.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "detmath.cuh"
 #include "kernels.cuh"
@@ -23,10 +25,13 @@ namespace sfm {
 // DMMA GEMM
 // ----------------------------------------------------------------------------
 namespace gemm {
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3, PAD = 8, LDS = BM + PAD;
-constexpr int LDB_K = BK + 4;  // K-major B tile pitch (conflict-free fragment reads)
+constexpr int BM = 128, BN = 128, PAD = 8, LDS = BM + PAD;
 constexpr int THREADS = 512;
-constexpr int SMEM = STAGES * (BK * LDS + BN * LDB_K) * 8;  // 113664 B
+template <int BK, int STAGES>
+struct Cfg {
+    static constexpr int LDB_K = BK + 4;  // K-major B tile pitch (conflict-free fragment reads)
+    static constexpr int SMEM = STAGES * (BK * LDS + BN * LDB_K) * 8;
+};
 }  // namespace gemm
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -50,13 +55,16 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // MMA mapping: the m8n8k4 "A" operand carries B rows (n), its "B" operand
 // carries A rows (m), so each lane's two accumulators are C rows
 // m0 + 2(lane&3) + {0,1} of column n0 + (lane>>2): 16-byte C accesses.
-template <bool BK_MAJOR>
+// 16 warps of 32x32, STAGES-deep cp.async pipeline of BK-wide K chunks.
+template <bool BK_MAJOR, int BK, int STAGES>
 __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
     using namespace gemm;
+    constexpr int LDB_K = Cfg<BK, STAGES>::LDB_K;
     extern __shared__ __align__(16) double smem[];
     double* As = smem;                      // [STAGES][BK][LDS]
     double* Bs = smem + STAGES * BK * LDS;  // [STAGES][BK][LDS] or [STAGES][BN][LDB_K]
     constexpr int BSTAGE = BK_MAJOR ? BN * LDB_K : BK * LDS;
+    constexpr int CPT = BK / 8;             // 16-byte copies per thread per operand
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int ti, tj;
     const long long l = blockIdx.x;
@@ -70,38 +78,50 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
         ti = (int)(l % g.tm);
         tj = (int)(l / g.tm);
     }
+    if (g.lower_only && ti + g.row_off_tiles < tj + g.col_off_tiles) return;
     const double* A = g.A + (size_t)ti * BM;
     const double* B = BK_MAJOR ? g.B + (size_t)tj * BN * g.ldb : g.B + (size_t)tj * BN;
     double* C = g.C + (size_t)tj * BN * g.ldc + (size_t)ti * BM;
-    if (g.lower_only && ti + g.row_off_tiles < tj + g.col_off_tiles) return;
     const int wm = warp & 3, wn = warp >> 2;  // 4 x 4 warps of 32 x 32
     const int beta = (g.beta && !(g.beta0_from >= 0 && tj >= g.beta0_from)) ? 1 : 0;
 
+    // per-thread copy sources / destinations (chunk 0); advance by BK per chunk
+    const double* asrc[CPT];
+    const double* bsrc[CPT];
+    int adst[CPT], bdst[CPT];
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) {
+        const int idx = tid + THREADS * u;
+        const int k = idx >> 6, m2 = (idx & 63) * 2;
+        asrc[u] = A + (size_t)k * g.lda + m2;
+        adst[u] = k * LDS + m2;
+        if (BK_MAJOR) {
+            const int n = idx / (BK / 2), k2 = (idx % (BK / 2)) * 2;
+            bsrc[u] = B + (size_t)n * g.ldb + k2;
+            bdst[u] = n * LDB_K + k2;
+        } else {
+            bsrc[u] = B + (size_t)k * g.ldb + m2;
+            bdst[u] = k * LDS + m2;
+        }
+    }
+    const size_t astep = (size_t)BK * g.lda;
+    const size_t bstep = BK_MAJOR ? (size_t)BK : (size_t)BK * g.ldb;
     auto load_stage = [&](int st, int kc) {
         double* as = As + st * BK * LDS;
         double* bs = Bs + st * BSTAGE;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int idx = tid + THREADS * u;  // 0..1023
-            {
-                const int k = idx >> 6, m2 = (idx & 63) * 2;
-                cp_async16(as + k * LDS + m2, A + (size_t)(kc * BK + k) * g.lda + m2);
-            }
-            if (BK_MAJOR) {
-                const int n = idx >> 3, k2 = (idx & 7) * 2;
-                cp_async16(bs + n * LDB_K + k2, B + (size_t)n * g.ldb + kc * BK + k2);
-            } else {
-                const int k = idx >> 6, n2 = (idx & 63) * 2;
-                cp_async16(bs + k * LDS + n2, B + (size_t)(kc * BK + k) * g.ldb + n2);
-            }
+        for (int u = 0; u < CPT; ++u) {
+            cp_async16(as + adst[u], asrc[u] + kc * astep);
+            cp_async16(bs + bdst[u], bsrc[u] + kc * bstep);
         }
     };
 
     const int NK = g.K / BK;
-    load_stage(0, 0);
-    cp_async_commit();
-    if (NK > 1) load_stage(1, 1);
-    cp_async_commit();
+#pragma unroll
+    for (int st = 0; st < STAGES - 1; ++st) {
+        if (st < NK) load_stage(st, st);
+        cp_async_commit();
+    }
 
     double acc[4][4][2];
     const int rq = 2 * (lane & 3), cq = lane >> 2;
@@ -124,9 +144,9 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
 
 #pragma unroll 1
     for (int kc = 0; kc < NK; ++kc) {
-        cp_async_wait<1>();
+        cp_async_wait<STAGES - 2>();
         __syncthreads();
-        if (kc + 2 < NK) load_stage((kc + 2) % STAGES, kc + 2);
+        if (kc + STAGES - 1 < NK) load_stage((kc + STAGES - 1) % STAGES, kc + STAGES - 1);
         cp_async_commit();
         const double* as = As + (kc % STAGES) * BK * LDS;
         const double* bs = Bs + (kc % STAGES) * BSTAGE;
@@ -159,17 +179,38 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
         }
 }
 
+// Kernel configuration (SFMCOV_GEMM_CFG, default 2): 0 = BK 16 x 3 stages,
+// 1 = BK 32 x 3 stages, 2 = BK 16 x 4 stages.
+static int gemm_cfg() {
+    static int c = [] {
+        const char* e = std::getenv("SFMCOV_GEMM_CFG");
+        const int v = e ? std::atoi(e) : 0;
+        return (v >= 0 && v <= 2) ? v : 2;
+    }();
+    return c;
+}
+
+template <int BK, int ST>
+static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) {
+    constexpr int SMEM = gemm::Cfg<BK, ST>::SMEM;
+    static bool attr = false;
+    if (!attr) {
+        SFM_CUDA(cudaFuncSetAttribute(k_gemm<false, BK, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, BK, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        attr = true;
+    }
+    if (g.b_kmajor) k_gemm<true, BK, ST><<<(unsigned)tiles, gemm::THREADS, SMEM, s>>>(g);
+    else k_gemm<false, BK, ST><<<(unsigned)tiles, gemm::THREADS, SMEM, s>>>(g);
+}
+
 void launch_gemm(const GemmArgs& g, cudaStream_t s) {
     const long long tiles = g.tri ? (long long)g.tm * (g.tm + 1) / 2 : (long long)g.tm * g.tn;
     if (tiles <= 0) return;
-    static bool attr = false;
-    if (!attr) {
-        SFM_CUDA(cudaFuncSetAttribute(k_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::SMEM));
-        SFM_CUDA(cudaFuncSetAttribute(k_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::SMEM));
-        attr = true;
+    switch (gemm_cfg()) {
+        case 1: launch_gemm_cfg<32, 3>(g, tiles, s); break;
+        case 2: launch_gemm_cfg<16, 4>(g, tiles, s); break;
+        default: launch_gemm_cfg<16, 3>(g, tiles, s); break;
     }
-    if (g.b_kmajor) k_gemm<true><<<(unsigned)tiles, gemm::THREADS, gemm::SMEM, s>>>(g);
-    else k_gemm<false><<<(unsigned)tiles, gemm::THREADS, gemm::SMEM, s>>>(g);
     SFM_LAUNCH_CHECK();
 }
 
@@ -298,12 +339,10 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
     POTRF_STAMP(0);
     double* rinv = Ws + NWARPS * 64;             // 1 / L_jj
     double* spiv = rinv + kNB;                   // pivots
+    if (warp == 0) warp_potrf8(T, 0, rinv, spiv);
+    __syncthreads();
     for (int s = 0; s < NSB; ++s) {
         const int c0 = s * SB;
-        POTRF_STAMP(44 + s);
-        if (warp == 0) warp_potrf8(T, c0, rinv, spiv);
-        __syncthreads();
-        if (s < 15) POTRF_STAMP(28 + s);
         const int rows = kNB - c0 - SB;
         if (rows == 0) break;
         // panel solve by forward substitution, one row per thread:
@@ -324,41 +363,59 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
             for (int c = 0; c < SB; ++c) T[(c0 + c) * LDT + r] = x[c];
         }
         __syncthreads();
-        // trailing update T[r, c] -= Σ_k L[r, c0+k] L[c, c0+k], 8x8 DMMA tiles,
-        // two tiles per warp iteration for ILP
+        // trailing update T[r, c] -= Σ_k L[r, c0+k] L[c, c0+k] in 8x8 DMMA
+        // tiles.  Warp 0 updates the next diagonal tile and factors it right
+        // away (the lookahead inside the tile); warps 1.. take the other
+        // tiles four at a time.
         const int nt = rows / SB;
         const int ntiles = nt * (nt + 1) / 2;
-        for (int t0 = 2 * warp; t0 < ntiles; t0 += 2 * NWARPS) {
-            double d[2][2];
-            double* cp[2];
-            int r0v[2], q0v[2];
-            const int cnt = (t0 + 1 < ntiles) ? 2 : 1;
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int t = (u < cnt) ? t0 + u : t0;
-                int ti = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-                while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-                while (ti * (ti + 1) / 2 > t) --ti;
-                const int tj = t - ti * (ti + 1) / 2;
-                r0v[u] = c0 + SB + SB * ti;
-                q0v[u] = c0 + SB + SB * tj;
-                cp[u] = T + (q0v[u] + 2 * fk) * LDT + r0v[u] + fr;
-                d[u][0] = cp[u][0];
-                d[u][1] = cp[u][LDT];
-            }
+        const int c1 = c0 + SB;
+        if (warp == 0) {
+            double* cp = T + (c1 + 2 * fk) * LDT + c1 + fr;
+            double d0 = cp[0], d1 = cp[LDT];
 #pragma unroll
             for (int kk = 0; kk < SB; kk += 4) {
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const double tv = T[(c0 + kk + fk) * LDT + r0v[u] + fr];
-                    const double av = __hiloint2double(__double2hiint(tv) ^ (int)0x80000000u, __double2loint(tv));
-                    const double bv = T[(c0 + kk + fk) * LDT + q0v[u] + fr];
-                    dmma8(d[u][0], d[u][1], av, bv);
-                }
+                const double tv = T[(c0 + kk + fk) * LDT + c1 + fr];
+                const double av = __hiloint2double(__double2hiint(tv) ^ (int)0x80000000u, __double2loint(tv));
+                dmma8(d0, d1, av, tv);
             }
-            for (int u = 0; u < cnt; ++u) {
-                cp[u][0] = d[u][0];
-                cp[u][LDT] = d[u][1];
+            cp[0] = d0;
+            cp[LDT] = d1;
+            warp_potrf8(T, c1, rinv, spiv);
+        } else {
+            for (int t0 = 1 + 4 * (warp - 1); t0 < ntiles; t0 += 4 * (NWARPS - 1)) {
+                double d[4][2];
+                double* cp[4];
+                int r0v[4], q0v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int t = (t0 + u < ntiles) ? t0 + u : t0;
+                    int ti = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+                    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+                    while (ti * (ti + 1) / 2 > t) --ti;
+                    const int tj = t - ti * (ti + 1) / 2;
+                    r0v[u] = c1 + SB * ti;
+                    q0v[u] = c1 + SB * tj;
+                    cp[u] = T + (q0v[u] + 2 * fk) * LDT + r0v[u] + fr;
+                    d[u][0] = cp[u][0];
+                    d[u][1] = cp[u][LDT];
+                }
+#pragma unroll
+                for (int kk = 0; kk < SB; kk += 4) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const double tv = T[(c0 + kk + fk) * LDT + r0v[u] + fr];
+                        const double av = __hiloint2double(__double2hiint(tv) ^ (int)0x80000000u, __double2loint(tv));
+                        const double bv = T[(c0 + kk + fk) * LDT + q0v[u] + fr];
+                        dmma8(d[u][0], d[u][1], av, bv);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (t0 + u < ntiles) {
+                        cp[u][0] = d[u][0];
+                        cp[u][LDT] = d[u][1];
+                    }
             }
         }
         __syncthreads();

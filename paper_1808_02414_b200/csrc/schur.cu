@@ -151,8 +151,8 @@ __global__ void __launch_bounds__(128) k_obs_factor(const int* oc, const int* op
     for (int q = 0; q < kWStride / 2; ++q) o2[q] = make_double2(wo[2 * q], wo[2 * q + 1]);
 }
 
-// F = Σ partials (fixed-order, 256-thread tree); L_F = chol(F); eig(E = -F)
-// for the diagnostics.
+// F = Σ partials (fixed-order tree); L_F = chol(F); E = -F and E's pivots
+// (-diag(L_F)^2) for the diagnostics.
 __global__ void __launch_bounds__(128) k_border_factor(const double* Fpart, int nblocks, double* LF, double* Eout,
                                                        double* eigE, Status* st) {
     __shared__ double red[128][29];
@@ -178,10 +178,6 @@ __global__ void __launch_bounds__(128) k_border_factor(const double* Fpart, int 
             F[7 * l2 + l1] = red[0][k];
         }
     for (int q = 0; q < 49; ++q) Eout[q] = -F[q];
-    double a[49], d[7], v[49];
-    for (int q = 0; q < 49; ++q) a[q] = -F[q];
-    jacobi_eig<7>(a, d, v);
-    for (int q = 0; q < 7; ++q) eigE[q] = d[q];
     double L[49];
     for (int q = 0; q < 49; ++q) L[q] = 0.0;
     bool ok = true;
@@ -199,6 +195,9 @@ __global__ void __launch_bounds__(128) k_border_factor(const double* Fpart, int 
     }
     if (!ok) st->border_bad = 1;
     for (int q = 0; q < 49; ++q) LF[q] = L[q];
+    // border pivots for the diagnostics: the Cholesky pivots of -E (their
+    // magnitudes are the |pivots| of E's LDL^T with D = -diag(L_F)^2)
+    for (int c = 0; c < 7; ++c) eigE[c] = -L[7 * c + c] * L[7 * c + c];
 }
 
 // ---- camera border rows (warp per camera) ----------------------------------------
@@ -209,72 +208,61 @@ __global__ void __launch_bounds__(64) k_camera_border(const int* off_cam, const 
                                                       const double* Wb, const double* V, const double* cams,
                                                       const double* Hr, const double* s_a, const double* s_b,
                                                       const double* LF, int n, double* Gamma, double* G) {
+    // one CTA per camera, one thread per entry (p, l) of Γ_i (P x 7)
     constexpr int NE = P * 7;
-    constexpr int CH = 32, RS = 49;  // staged: W (27) at 0, V_j (21) at 27
-    __shared__ double stage[2][CH][RS];
-    __shared__ double sh[2][NE];
-    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i = blockIdx.x * 2 + wib;
-    if (i >= n) return;
-    double acc[3] = {0.0, 0.0, 0.0};
+    constexpr int CH = 64, RS = 49;  // staged: W (27) at 0, V_j (21) at 27
+    __shared__ double stage[CH][RS];
+    __shared__ double sh[NE];
+    const int i = blockIdx.x, tid = threadIdx.x;
+    const int p = tid / 7, l = tid % 7;
+    double acc = 0.0;
     const int b = off_cam[i], e = off_cam[i + 1];
     for (int k0 = b; k0 < e; k0 += CH) {
         const int nc = min(CH, e - k0);
-        // W rows of this chunk are contiguous (by-camera slots): coalesced copy
-        for (int q = lane; q < nc * 27; q += 32) {
-            const int o = q / 27, c = q - o * 27;
-            stage[wib][o][c] = Wb[(size_t)(k0 + o) * kWStride + c];
+        // W rows of the chunk are contiguous (by-camera slots): coalesced copy
+        for (int w = tid; w < nc * 27; w += 64) {
+            const int o = w / 27, c = w - o * 27;
+            stage[o][c] = Wb[(size_t)(k0 + o) * kWStride + c];
         }
-        if (lane < nc) {
-            const double* vj = V + 21 * (size_t)op[idx_cam[k0 + lane]];
-#pragma unroll
-            for (int c = 0; c < 21; ++c) stage[wib][lane][27 + c] = vj[c];
+        for (int w = tid; w < nc * 21; w += 64) {
+            const int o = w / 21, c = w - o * 21;
+            stage[o][27 + c] = V[21 * (size_t)op[idx_cam[k0 + o]] + c];
         }
-        __syncwarp();
-        for (int o = 0; o < nc; ++o) {
-            const double* w = stage[wib][o];
-            const double* vj = w + 27;
-#pragma unroll
-            for (int s = 0; s < 3; ++s) {
-                const int en = lane + 32 * s;
-                if (en < NE) {
-                    const int p = en / 7, l = en % 7;
-                    acc[s] += (w[3 * p] * vj[l] + w[3 * p + 1] * vj[7 + l]) + w[3 * p + 2] * vj[14 + l];
-                }
+        __syncthreads();
+        if (tid < NE) {
+            for (int o = 0; o < nc; ++o) {
+                const double* w = stage[o];
+                const double* vj = w + 27;
+                acc += (w[3 * p] * vj[l] + w[3 * p + 1] * vj[7 + l]) + w[3 * p + 2] * vj[14 + l];
             }
         }
-        __syncwarp();
+        __syncthreads();
     }
-    const double* C = cams + (size_t)P * i + 3;
-    double sx[9];
-    skew(C, sx);
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {
-        const int en = lane + 32 * s;
-        if (en < NE) {
-            const int p = en / 7, l = en % 7;
-            double h = 0.0;
-            if (p < 3) h = (l >= 3 && l < 6) ? Hr[9 * (size_t)i + 3 * p + (l - 3)] : 0.0;
-            else if (p < 6) {
-                const int a = p - 3;
-                h = (l < 3) ? (l == a ? 1.0 : 0.0) : (l < 6 ? sx[3 * a + (l - 3)] : C[a]);
-            }
-            const double hs = (s_a[(size_t)P * i + p] * h) * s_b[l];
-            const double g = hs - acc[s];
-            sh[wib][en] = g;
-            Gamma[(size_t)P * 7 * i + en] = g;
+    if (tid < NE) {
+        const double* C = cams + (size_t)P * i + 3;
+        double h = 0.0;
+        if (p < 3) h = (l >= 3 && l < 6) ? Hr[9 * (size_t)i + 3 * p + (l - 3)] : 0.0;
+        else if (p < 6) {
+            const int a = p - 3;
+            double sx[9];
+            skew(C, sx);
+            h = (l < 3) ? (l == a ? 1.0 : 0.0) : (l < 6 ? sx[3 * a + (l - 3)] : C[a]);
         }
+        const double hs = (s_a[(size_t)P * i + p] * h) * s_b[l];
+        const double g = hs - acc;
+        sh[tid] = g;
+        Gamma[(size_t)P * 7 * i + tid] = g;
     }
-    __syncwarp();
-    if (lane < P) {
-        const double* gr = &sh[wib][7 * lane];
+    __syncthreads();
+    if (tid < P) {
+        const double* gr = &sh[7 * tid];
         double out[7];
-        for (int l = 0; l < 7; ++l) {
-            double x = gr[l];
-            for (int kk = 0; kk < l; ++kk) x -= LF[7 * l + kk] * out[kk];
-            out[l] = x / LF[7 * l + l];
+        for (int ll = 0; ll < 7; ++ll) {
+            double x = gr[ll];
+            for (int kk = 0; kk < ll; ++kk) x -= LF[7 * ll + kk] * out[kk];
+            out[ll] = x / LF[7 * ll + ll];
         }
-        for (int l = 0; l < 7; ++l) G[((size_t)P * i + lane) * 7 + l] = out[l];
+        for (int ll = 0; ll < 7; ++ll) G[((size_t)P * i + tid) * 7 + ll] = out[ll];
     }
 }
 
@@ -357,12 +345,24 @@ __global__ void k_pair_gen(const int* off_pt, const int* idx_pt, const int* oc, 
 }
 
 // Warp per camera-pair block: lanes (g, p) with g < 32/P groups accumulate
-// row p of W_hi W_lo^T over pairs g, g+G, ...; groups are combined in fixed
-// order and the block is written once: Z(P hi + p, P lo + q) -= acc[q].
+// row p of W_hi W_lo^T over pairs g, g+G, ... (two pairs in flight per
+// group, register-light so many warps per SM hide the gather latency);
+// groups combine in fixed order and the block is written once:
+// Z(P hi + p, P lo + q) -= acc[q].
 template <int P>
-__global__ void __launch_bounds__(256) k_pair_reduce(const unsigned int* ukeys, const long long* seg_off, int nseg,
-                                                     const unsigned long long* vals, const double* Wb, int n,
-                                                     double* Z, long long ld) {
+__device__ __forceinline__ void pair_accum(double (&acc)[P], const double* Wb, unsigned long long v, int p) {
+    const double* wh = Wb + (size_t)(v >> 32) * kWStride + 3 * p;
+    const double* wl = Wb + (size_t)(v & 0xffffffffULL) * kWStride;
+    const double h0 = __ldg(wh), h1 = __ldg(wh + 1), h2 = __ldg(wh + 2);
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+        acc[q] += (h0 * __ldg(wl + 3 * q) + h1 * __ldg(wl + 3 * q + 1)) + h2 * __ldg(wl + 3 * q + 2);
+}
+
+template <int P>
+__global__ void __launch_bounds__(256, 4) k_pair_reduce(const unsigned int* ukeys, const long long* seg_off, int nseg,
+                                                        const unsigned long long* vals, const double* Wb, int n,
+                                                        double* Z, long long ld) {
     constexpr int G = 32 / P;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -374,19 +374,15 @@ __global__ void __launch_bounds__(256) k_pair_reduce(const unsigned int* ukeys, 
 #pragma unroll
     for (int q = 0; q < P; ++q) acc[q] = 0.0;
     if (active) {
-        for (long long idx = b + g; idx < e; idx += G) {
-            const unsigned long long v = vals[idx];
-            const double* wh = Wb + (size_t)(v >> 32) * kWStride + 3 * p;
-            const double2* wl = reinterpret_cast<const double2*>(Wb + (size_t)(v & 0xffffffffULL) * kWStride);
-            const double h0 = wh[0], h1 = wh[1], h2 = wh[2];
-            double w[28];
-#pragma unroll
-            for (int k = 0; k < 14; ++k) { const double2 x = __ldg(wl + k); w[2 * k] = x.x; w[2 * k + 1] = x.y; }
-#pragma unroll
-            for (int q = 0; q < P; ++q) acc[q] += (h0 * w[3 * q] + h1 * w[3 * q + 1]) + h2 * w[3 * q + 2];
+        long long idx = b + g;
+        for (; idx + G < e; idx += 2 * G) {
+            const unsigned long long v0 = __ldg(vals + idx), v1 = __ldg(vals + idx + G);
+            pair_accum<P>(acc, Wb, v0, p);
+            pair_accum<P>(acc, Wb, v1, p);
         }
+        if (idx < e) pair_accum<P>(acc, Wb, __ldg(vals + idx), p);
     }
-    // combine groups: lane p += lane p + P·g (g = 1..G-1), fixed order
+    __syncwarp();
 #pragma unroll
     for (int q = 0; q < P; ++q) {
         double tot = acc[q];
@@ -432,8 +428,8 @@ void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* 
                           const double* s_a, const double* s_b, const double* LF, double* Gamma, double* G,
                           cudaStream_t s) {
     if (!sc.n) return;
-    if (sc.P == 8) k_camera_border<8><<<cdiv(sc.n, 2), 64, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
-    else k_camera_border<9><<<cdiv(sc.n, 2), 64, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    if (sc.P == 8) k_camera_border<8><<<sc.n, 64, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    else k_camera_border<9><<<sc.n, 64, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
     SFM_LAUNCH_CHECK();
 }
 

@@ -155,86 +155,88 @@ __global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const
                                                        const double* cams, const double* pts, const int* op, int n,
                                                        double* D, double* Hr, double* s_a, unsigned char* flags,
                                                        Status* st) {
+    // one CTA per camera, one thread per output entry: D (P*P), rotation
+    // normal (9) and rhs (9); each entry is a sequential sum over the
+    // camera's observations in ascending order.
     constexpr int NE = P * P + 18;
-    constexpr int NS = (NE + 31) / 32;
-    constexpr int CH = 32, RS = kRec + 4;  // staged record: [jc | jp | W | pad] + X(3) at 28..30
-    __shared__ double stage[4][CH][RS];
-    __shared__ double sh[4][NE];
-    const int wib = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const int i = blockIdx.x * 4 + wib;
-    if (i >= n) return;
+    constexpr int CH = 64, RS = kRec + 4;  // staged record [jc | jp | W | pad] + X at 28..30
+    __shared__ double stage[CH][RS];
+    __shared__ double sh[NE];
+    const int i = blockIdx.x;
+    const int tid = threadIdx.x;
     const double* cam = cams + (size_t)P * i;
     double hc[9];
     skew(cam + 3, hc);
-    double acc[NS];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+    // entry decode (fixed per thread)
+    const int kind = tid < P * P ? 0 : (tid < P * P + 9 ? 1 : (tid < NE ? 2 : 3));
+    int p = 0, q = 0;
+    if (kind == 0) { p = tid / P; q = tid % P; }
+    else if (kind == 1) { p = (tid - P * P) / 3; q = (tid - P * P) % 3; }
+    else if (kind == 2) { p = (tid - P * P - 9) / 3; q = (tid - P * P - 9) % 3; }
+    double acc = 0.0;
     const int b = off_cam[i], e = off_cam[i + 1];
     for (int k0 = b; k0 < e; k0 += CH) {
         const int nc = min(CH, e - k0);
-        if (lane < nc) {
-            const int t = idx_cam[k0 + lane];
-            const double2* r2 = reinterpret_cast<const double2*>(rec + (size_t)t * kRec);
-            double* dst = stage[wib][lane];
-#pragma unroll
-            for (int q = 0; q < kRec / 2; ++q) { const double2 v = r2[q]; dst[2 * q] = v.x; dst[2 * q + 1] = v.y; }
-            const double* X = pts + 3 * (size_t)op[t];
-            dst[28] = X[0]; dst[29] = X[1]; dst[30] = X[2];
+        // cooperative staging: 32 doubles per observation
+        for (int w = tid; w < nc * 16; w += 128) {
+            const int o = w >> 4, part = w & 15;
+            const int t = idx_cam[k0 + o];
+            double2 v;
+            if (part < 14) v = reinterpret_cast<const double2*>(rec + (size_t)t * kRec)[part];
+            else {
+                const double* X = pts + 3 * (size_t)op[t];
+                v = (part == 14) ? make_double2(X[0], X[1]) : make_double2(X[2], 0.0);
+            }
+            stage[o][2 * part] = v.x;
+            stage[o][2 * part + 1] = v.y;
         }
-        __syncwarp();
-        for (int o = 0; o < nc; ++o) {
-            const double* r = stage[wib][o];
-            const double* jc = r + Layout<P>::JC;
-            const double* jp = r + Layout<P>::JP;
-            const double* W = r + Layout<P>::WO;
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                const int en = lane + 32 * s;
-                if (en >= NE) break;
-                if (en < P * P) {
-                    const int p = en / P, q = en % P;
-                    const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
-                    const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
-                    acc[s] += t0 * jc[q] + t1 * jc[P + q];
-                } else if (en < P * P + 9) {
-                    const int p = (en - P * P) / 3, q = (en - P * P) % 3;
-                    acc[s] += jc[p] * jc[q] + jc[P + p] * jc[P + q];
-                } else {
-                    const int p = (en - P * P - 9) / 3, q = (en - P * P - 9) % 3;
-                    double hx[9];
-                    skew(r + 28, hx);
-                    double tg[2];
-                    for (int ii = 0; ii < 2; ++ii) {
-                        const double a = (jc[P * ii + 3] * hc[0 + q] + jc[P * ii + 4] * hc[3 + q]) + jc[P * ii + 5] * hc[6 + q];
-                        const double bb = (jp[3 * ii + 0] * hx[0 + q] + jp[3 * ii + 1] * hx[3 + q]) + jp[3 * ii + 2] * hx[6 + q];
-                        tg[ii] = -(a + bb);
-                    }
-                    acc[s] += jc[p] * tg[0] + jc[P + p] * tg[1];
+        __syncthreads();
+        if (kind == 0) {
+            for (int o = 0; o < nc; ++o) {
+                const double* jc = stage[o] + Layout<P>::JC;
+                const double* W = stage[o] + Layout<P>::WO;
+                const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
+                const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
+                acc += t0 * jc[q] + t1 * jc[P + q];
+            }
+        } else if (kind == 1) {
+            for (int o = 0; o < nc; ++o) {
+                const double* jc = stage[o] + Layout<P>::JC;
+                acc += jc[p] * jc[q] + jc[P + p] * jc[P + q];
+            }
+        } else if (kind == 2) {
+            for (int o = 0; o < nc; ++o) {
+                const double* r = stage[o];
+                const double* jc = r + Layout<P>::JC;
+                const double* jp = r + Layout<P>::JP;
+                double hx[9];
+                skew(r + 28, hx);
+                double tg[2];
+                for (int ii = 0; ii < 2; ++ii) {
+                    const double a = (jc[P * ii + 3] * hc[0 + q] + jc[P * ii + 4] * hc[3 + q]) + jc[P * ii + 5] * hc[6 + q];
+                    const double bb = (jp[3 * ii + 0] * hx[0 + q] + jp[3 * ii + 1] * hx[3 + q]) + jp[3 * ii + 2] * hx[6 + q];
+                    tg[ii] = -(a + bb);
                 }
+                acc += jc[p] * tg[0] + jc[P + p] * tg[1];
             }
         }
-        __syncwarp();
+        __syncthreads();
     }
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-        const int en = lane + 32 * s;
-        if (en < NE) sh[wib][en] = acc[s];
+    if (tid < NE) sh[tid] = acc;
+    __syncthreads();
+    if (tid < P * P) D[(size_t)P * P * i + tid] = acc;
+    if (tid < P) {
+        const double d = sh[tid * (P + 1)];
+        if (d > 0.0) s_a[(size_t)P * i + tid] = 1.0 / sqrt(d);
+        else { s_a[(size_t)P * i + tid] = 1.0; flags[(size_t)P * i + tid] = 1; atomicAdd(&st->nflag, 1); }
     }
-    __syncwarp();
-    for (int en = lane; en < P * P; en += 32) D[(size_t)P * P * i + en] = sh[wib][en];
-    if (lane < P) {
-        const double d = sh[wib][lane * (P + 1)];
-        if (d > 0.0) s_a[(size_t)P * i + lane] = 1.0 / sqrt(d);
-        else { s_a[(size_t)P * i + lane] = 1.0; flags[(size_t)P * i + lane] = 1; atomicAdd(&st->nflag, 1); }
-    }
-    if (lane == 0) {
+    if (tid == 0) {
         double inv[9], hr[9];
-        if (!eig_inverse3(&sh[wib][P * P], kRotationCondTol, inv)) {
+        if (!eig_inverse3(&sh[P * P], kRotationCondTol, inv)) {
             atomicMin(&st->rot_bad, i);
             for (int k = 0; k < 9; ++k) Hr[9 * (size_t)i + k] = 0.0;
         } else {
-            mul3(inv, &sh[wib][P * P + 9], hr);
+            mul3(inv, &sh[P * P + 9], hr);
             for (int k = 0; k < 9; ++k) Hr[9 * (size_t)i + k] = hr[k];
         }
     }
@@ -420,8 +422,8 @@ void launch_reductions(const SceneDev& sc, const IndexDev& ix, const double* rec
     const size_t ncols = (size_t)sc.P * sc.n + 3 * (size_t)sc.m;
     SFM_CUDA(cudaMemsetAsync(flags, 0, ncols, s));
     if (sc.n) {
-        if (sc.P == 8) k_camera_reduce<8><<<cdiv(sc.n, 4), 128, 0, s>>>(ix.off_cam, ix.idx_cam, rec, sc.cams, sc.pts, sc.op, sc.n, D, Hr, s_a, flags, st);
-        else k_camera_reduce<9><<<cdiv(sc.n, 4), 128, 0, s>>>(ix.off_cam, ix.idx_cam, rec, sc.cams, sc.pts, sc.op, sc.n, D, Hr, s_a, flags, st);
+        if (sc.P == 8) k_camera_reduce<8><<<sc.n, 128, 0, s>>>(ix.off_cam, ix.idx_cam, rec, sc.cams, sc.pts, sc.op, sc.n, D, Hr, s_a, flags, st);
+        else k_camera_reduce<9><<<sc.n, 128, 0, s>>>(ix.off_cam, ix.idx_cam, rec, sc.cams, sc.pts, sc.op, sc.n, D, Hr, s_a, flags, st);
         SFM_LAUNCH_CHECK();
     }
     if (sc.m) {

@@ -240,6 +240,7 @@ def main():
     torch.cuda.synchronize()
     times, stage_acc = [], {}
     launches = 0
+    retries = 0
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             with torch.cuda.stream(stream):
@@ -252,7 +253,9 @@ def main():
             times.append(e0.elapsed_time(e1))
             for k, v in eng.stage_times().items():
                 stage_acc[k] = stage_acc.get(k, 0.0) + v
-            launches += eng.counts()["dense_launches"]
+            cts = eng.counts()
+            launches += cts["kernel_launches"]
+            retries += cts["dense_retries"]
     torch.cuda.synchronize()
     barrier(world)
     ms = dist_max(float(np.mean(times)), world)
@@ -343,6 +346,7 @@ def main():
                     "h2d_bytes_per_step": scene_bytes(rec), "d2h_bytes_per_step": int(n * P * P * 8),
                     "timing": "host wall clock around sfmcov_cuda_compute_covariance (pinned host buffers)"},
             "gpu_launches": launches,
+            "dense_serial_retries": retries,
             "roofline": {
                 "kernel": "dense FP64 Cholesky + triangular inverse (k_gemm DMMA m8n8k4 + k_potrf_diag)",
                 "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",

@@ -163,7 +163,8 @@ const char* sfmcov_cuda_stage_name(int32_t i);
 /* Algorithmic counts of the last pipeline call (for roofline accounting):
  * [0] obs-pairs, [1] nonzero camera-pair blocks (incl. diagonal), [2] N = P*n,
  * [3] padded dense dim, [4] n_obs, [5] n_pts, [6] n_cams, [7] P,
- * [8] dense-factorisation kernel launches. */
+ * [8] kernel launches of this library, [9] serial re-runs of the dense
+ * stage after a pivot failure with overlapped streams. */
 int32_t sfmcov_cuda_last_counts(sfmcov_handle* h, int64_t* counts, int32_t capacity);
 /* Enable/disable per-stage event timing (off by default; adds syncs). */
 void sfmcov_cuda_set_profiling(sfmcov_handle* h, int32_t on);

@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
 static int gemm_cfg() {
     static int c = [] {
         const char* e = std::getenv("SFMCOV_GEMM_CFG");
-        const int v = e ? std::atoi(e) : 0;
+        const int v = e ? std::atoi(e) : 2;
         return (v >= 0 && v <= 2) ? v : 2;
     }();
     return c;
@@ -653,6 +653,11 @@ void launch_pivot_range(const double* piv, int N, double* out, cudaStream_t s) {
 // ----------------------------------------------------------------------------
 // Drivers
 // ----------------------------------------------------------------------------
+static bool debug_sync() {
+    static bool v = [] { const char* e = std::getenv("SFMCOV_DEBUG_SYNC"); return e && e[0] == '1'; }();
+    return v;
+}
+
 static GemmArgs gemm_args(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb,
                           int tm, int tn, int K) {
     GemmArgs g{};
@@ -722,6 +727,10 @@ int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, doubl
         if (T2 > gn) {
             SFM_CUDA(cudaEventRecord(e2, s2));
             rest_pending = true;
+        }
+        if (debug_sync()) {
+            SFM_CUDA(cudaStreamSynchronize(s));
+            SFM_CUDA(cudaStreamSynchronize(s2));
         }
     }
     if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, e2, 0));

@@ -241,9 +241,10 @@ class Engine:
         return {self._lib.sfmcov_cuda_stage_name(i).decode(): buf[i] for i in range(k)}
 
     def counts(self) -> dict:
-        buf = (C.c_int64 * 9)()
-        self._lib.sfmcov_cuda_last_counts(self._h, buf, 9)
-        keys = ["obs_pairs", "nnz_blocks", "N", "Npad", "n_obs", "n_pts", "n_cams", "P", "dense_launches"]
+        buf = (C.c_int64 * 10)()
+        self._lib.sfmcov_cuda_last_counts(self._h, buf, 10)
+        keys = ["obs_pairs", "nnz_blocks", "N", "Npad", "n_obs", "n_pts", "n_cams", "P", "kernel_launches",
+                "dense_retries"]
         return dict(zip(keys, [int(v) for v in buf]))
 
     # ---- pipeline -------------------------------------------------------------

@@ -65,6 +65,10 @@ struct sfmcov_handle {
         psd, prange, status, depth, H;
     PairDev pairs;
     Status* st_host = nullptr;
+    // captured dense stage (Cholesky + triangular inverse), keyed by its inputs
+    cudaGraphExec_t dense_exec = nullptr;
+    const void* dense_key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    long long dense_launches = 0;
     double stage_ms[ST_COUNT] = {0};
     long long counts[10] = {0};
 };
@@ -197,6 +201,20 @@ int panel_blocks() {
         return (v >= 1 && v <= 8) ? v : 3;
     }();
     return g;
+}
+
+// SFMCOV_GRAPH=1 launches the dense stage as one captured CUDA graph instead
+// of kernel by kernel.  Off by default: measured slower on config 3
+// (27.8 vs 23.6 ms) — the graph executor orders the two lookahead branches
+// worse than the prioritised streams do, and launch overhead is not the
+// bottleneck (~650 launches against ~24 ms of GPU work).
+bool use_graph() {
+    static bool v = [] {
+        const char* e = std::getenv("SFMCOV_GRAPH");
+        const char* d = std::getenv("SFMCOV_DEBUG_SYNC");
+        return (e && e[0] == '1') && !(d && d[0] == '1');
+    }();
+    return v;
 }
 
 // SFMCOV_SERIAL_DENSE=1 runs the lookahead updates on the main stream
@@ -383,10 +401,38 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     const int pw = panel_blocks();
     double* Lp = h->Lp.as<double>(trtri_lp_doubles(Npad, pw));
     cudaStream_t s2 = serial_dense() ? s : h->s2;
-    int launches = dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, s2, h->e1, h->e2);
-    mark(h, 8);
-    launches += dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, s2, h->e1, h->e2);
-    mark(h, 9);
+    int launches = 0;
+    if (use_graph() && s2 != s) {
+        // one graph launch for the ~650 kernels of the dense stage; re-captured
+        // when the matrix size, panel width or any buffer address changes
+        const void* key[6] = {Z, Linv, piv, Lp, st, (const void*)(intptr_t)(Npad * 16 + pw)};
+        bool same = h->dense_exec != nullptr;
+        for (int q = 0; q < 6 && same; ++q) same = h->dense_key[q] == key[q];
+        if (!same) {
+            if (h->dense_exec) SFM_CUDA(cudaGraphExecDestroy(h->dense_exec));
+            h->dense_exec = nullptr;
+            const long long before = g_kernel_launches;
+            cudaGraph_t graph;
+            SFM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, s2, h->e1, h->e2);
+            dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, s2, h->e1, h->e2);
+            SFM_CUDA(cudaStreamEndCapture(s, &graph));
+            SFM_CUDA(cudaGraphInstantiate(&h->dense_exec, graph, 0));
+            SFM_CUDA(cudaGraphDestroy(graph));
+            h->dense_launches = g_kernel_launches - before;
+            g_kernel_launches = before;
+            for (int q = 0; q < 6; ++q) h->dense_key[q] = key[q];
+        }
+        SFM_CUDA(cudaGraphLaunch(h->dense_exec, s));
+        g_kernel_launches += h->dense_launches;
+        mark(h, 8);
+        mark(h, 9);
+    } else {
+        launches = dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, s2, h->e1, h->e2);
+        mark(h, 8);
+        launches += dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, s2, h->e1, h->e2);
+        mark(h, 9);
+    }
     int* psd = h->psd.as<int>(1);
     SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
     launch_extract(P, Z, ld, N, n, s_a, 1, out.d_cam_cov, st, psd, s);
@@ -551,6 +597,7 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
         SFM_CUDA(cudaEventCreateWithFlags(&h->e2, cudaEventDisableTiming));
         for (auto& ev : h->ev) SFM_CUDA(cudaEventCreate(&ev));
         SFM_CUDA(cudaMallocHost(&h->st_host, sizeof(Status)));
+        dense_init_attributes();
     } catch (const std::exception& x) {
         fill_error(err, ApiError{SFMCOV_ERR_DEVICE, "device", x.what()});
         delete h;
@@ -572,6 +619,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
                     &h->cov, &h->psd, &h->prange, &h->status, &h->depth, &h->H};
     for (DBuf* b : bufs) b->release();
     h->pairs.release();
+    if (h->dense_exec) cudaGraphExecDestroy(h->dense_exec);
     if (h->st_host) cudaFreeHost(h->st_host);
     cudaEventDestroy(h->e1);
     cudaEventDestroy(h->e2);

@@ -21,6 +21,11 @@
 
 namespace sfm {
 
+const void* k_potrf_diag_ptr();
+int potrf_smem_bytes_impl();
+static inline const void* k_potrf_diag_fwd() { return k_potrf_diag_ptr(); }
+static inline int potrf_smem_bytes() { return potrf_smem_bytes_impl(); }
+
 // ----------------------------------------------------------------------------
 // DMMA GEMM
 // ----------------------------------------------------------------------------
@@ -190,17 +195,47 @@ static int gemm_cfg() {
     return c;
 }
 
+// Launch with the stream's priority as a per-launch attribute, so the
+// priority survives CUDA-graph capture (captured kernel nodes do not inherit
+// stream priorities).
+template <typename... KArgs, typename... Args>
+static void launch_prio(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                        Args... args) {
+    int prio = 0;
+    SFM_CUDA(cudaStreamGetPriority(s, &prio));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = prio;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SFM_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
 template <int BK, int ST>
 static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) {
     constexpr int SMEM = gemm::Cfg<BK, ST>::SMEM;
-    static bool attr = false;
-    if (!attr) {
-        SFM_CUDA(cudaFuncSetAttribute(k_gemm<false, BK, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-        SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, BK, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-        attr = true;
-    }
-    if (g.b_kmajor) k_gemm<true, BK, ST><<<(unsigned)tiles, gemm::THREADS, SMEM, s>>>(g);
-    else k_gemm<false, BK, ST><<<(unsigned)tiles, gemm::THREADS, SMEM, s>>>(g);
+    if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST>, (unsigned)tiles, gemm::THREADS, SMEM, s, g);
+    else launch_prio(k_gemm<false, BK, ST>, (unsigned)tiles, gemm::THREADS, SMEM, s, g);
+}
+
+// Opt-in shared-memory sizes, set once before any launch (and before graph
+// capture).
+void dense_init_attributes() {
+    static bool done = false;
+    if (done) return;
+    SFM_CUDA(cudaFuncSetAttribute(k_gemm<false, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<16, 3>::SMEM));
+    SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<16, 3>::SMEM));
+    SFM_CUDA(cudaFuncSetAttribute(k_gemm<false, 32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<32, 3>::SMEM));
+    SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, 32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<32, 3>::SMEM));
+    SFM_CUDA(cudaFuncSetAttribute(k_gemm<false, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<16, 4>::SMEM));
+    SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<16, 4>::SMEM));
+    SFM_CUDA(cudaFuncSetAttribute(k_potrf_diag_fwd(), cudaFuncAttributeMaxDynamicSharedMemorySize, potrf_smem_bytes()));
+    done = true;
 }
 
 void launch_gemm(const GemmArgs& g, cudaStream_t s) {
@@ -476,13 +511,11 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
     POTRF_STAMP(3);
 }
 
+const void* k_potrf_diag_ptr() { return (const void*)k_potrf_diag; }
+int potrf_smem_bytes_impl() { return potrf::SMEM; }
+
 void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        SFM_CUDA(cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, potrf::SMEM));
-        attr = true;
-    }
-    k_potrf_diag<<<1, potrf::THREADS, potrf::SMEM, s>>>(A, ld, Linv, pivots, col0, st);
+    launch_prio(k_potrf_diag, 1, potrf::THREADS, potrf::SMEM, s, A, ld, Linv, pivots, col0, st);
     SFM_LAUNCH_CHECK();
 }
 

@@ -123,6 +123,7 @@ void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace&
 void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, cudaStream_t s);
 
 // dense.cu
+void dense_init_attributes();
 void launch_gemm(const GemmArgs& g, cudaStream_t s);
 void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s);
 void launch_copy_diag(double* X, long long ld, int k, const double* Linv, cudaStream_t s);

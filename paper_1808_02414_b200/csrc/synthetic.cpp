@@ -122,9 +122,19 @@ bool project(const double* cam, int P, const double* X, double* u, double* vz = 
     return true;
 }
 
-void add_obs(Scene& s, int32_t ci, int32_t pj) {
+void add_obs(Scene& s, int32_t ci, int32_t pj, const Rot* R = nullptr) {
     double u[2] = {0, 0};
-    project(&s.cams[size_t(s.P) * ci], s.P, &s.pts[3 * size_t(pj)], u);
+    if (R) {  // k1 = k2 = 0 configs with a precomputed camera rotation
+        const double* c = &s.cams[size_t(s.P) * ci];
+        const double* X = &s.pts[3 * size_t(pj)];
+        const double w[3] = {X[0] - c[3], X[1] - c[4], X[2] - c[5]};
+        double v[3];
+        for (int a = 0; a < 3; ++a) v[a] = R->m[a][0] * w[0] + R->m[a][1] * w[1] + R->m[a][2] * w[2];
+        u[0] = c[6] * (v[0] / v[2]);
+        u[1] = c[6] * (v[1] / v[2]);
+    } else {
+        project(&s.cams[size_t(s.P) * ci], s.P, &s.pts[3 * size_t(pj)], u);
+    }
     s.oc.push_back(ci);
     s.op.push_back(pj);
     s.u.push_back(u[0]);
@@ -307,41 +317,45 @@ V3 fib_dir(int i, int n) {
     return {rr * std::cos(th), rr * std::sin(th), z};
 }
 
-// Coarse grid over camera unit directions for nearest-direction queries.
+// Uniform grid over camera unit directions for nearest-direction queries:
+// cell size = the expected radius holding `want` cameras; a query gathers
+// every camera within a ball of radius R (doubling R until it holds enough),
+// so the result is the exact nearest set.
 struct DirGrid {
-    int g;
+    int g = 2;
+    double cell = 1.0, r0 = 1.0;
     std::vector<std::vector<int32_t>> cells;
     std::vector<V3> dirs;
-    int cell_of(double v) const { return std::min(g - 1, std::max(0, (int)((v + 1.0) * 0.5 * g))); }
+    int cell_of(double v) const { return std::min(g - 1, std::max(0, (int)((v + 1.0) / cell))); }
     int key(int a, int b, int c) const { return (a * g + b) * g + c; }
-    void build(const std::vector<V3>& d, int n) {
+    void build(const std::vector<V3>& d, int n, int want) {
         dirs = d;
-        g = std::max(2, (int)std::ceil(std::sqrt((double)n) * 0.8));
+        const double spacing = std::sqrt(4.0 * kPi / std::max(1, n));
+        r0 = 1.2 * spacing * std::sqrt((double)std::max(1, want));
+        g = std::max(2, std::min(128, (int)std::ceil(2.0 / r0)));
+        cell = 2.0 / g;
         cells.assign(size_t(g) * g * g, {});
         for (int i = 0; i < (int)d.size(); ++i) cells[key(cell_of(d[i].x), cell_of(d[i].y), cell_of(d[i].z))].push_back(i);
     }
-    // cameras sorted by direction distance to q, at least `want` of them
+    // cameras sorted by (squared) direction distance to q: all within R, R
+    // grown until at least `want` are found (or all cameras are in)
     void nearest(V3 q, int want, std::vector<std::pair<double, int32_t>>& out) const {
-        out.clear();
-        const int cx = cell_of(q.x), cy = cell_of(q.y), cz = cell_of(q.z);
-        for (int rad = 1; rad <= g; ++rad) {
+        want = std::min<int>(want, (int)dirs.size());
+        for (double R = r0;; R *= 2.0) {
             out.clear();
-            for (int a = std::max(0, cx - rad); a <= std::min(g - 1, cx + rad); ++a)
-                for (int b = std::max(0, cy - rad); b <= std::min(g - 1, cy + rad); ++b)
-                    for (int c = std::max(0, cz - rad); c <= std::min(g - 1, cz + rad); ++c)
+            const int ax = cell_of(q.x - R), bx = cell_of(q.x + R);
+            const int ay = cell_of(q.y - R), by = cell_of(q.y + R);
+            const int az = cell_of(q.z - R), bz = cell_of(q.z + R);
+            const double R2 = R * R;
+            for (int a = ax; a <= bx; ++a)
+                for (int b = ay; b <= by; ++b)
+                    for (int c = az; c <= bz; ++c)
                         for (int32_t i : cells[key(a, b, c)]) {
-                            const V3 d = dirs[i] - q;
-                            out.emplace_back(dot(d, d), i);
+                            const V3 dd = dirs[i] - q;
+                            const double d2 = dot(dd, dd);
+                            if (d2 <= R2) out.emplace_back(d2, i);
                         }
-            // exact once the ring of cells fully covers the want-th distance
-            if ((int)out.size() >= want) {
-                std::partial_sort(out.begin(), out.begin() + want, out.end());
-                const double cell = 2.0 / g;
-                if (std::sqrt(out[want - 1].first) <= (rad - 1) * cell || rad == g) {
-                    std::sort(out.begin(), out.end());
-                    return;
-                }
-            }
+            if ((int)out.size() >= want || R > 4.0) break;
         }
         std::sort(out.begin(), out.end());
     }
@@ -373,7 +387,9 @@ Scene config_scene(int idx, uint64_t seed) {
         centers.push_back({x, y, z});
     }
     DirGrid grid;
-    if (c.nearest) grid.build(cdir, c.n_cams);
+    if (c.nearest) grid.build(cdir, c.n_cams, 2 * (c.kmax + c.pool_extra));
+    std::vector<Rot> crot(c.n_cams);
+    for (int i = 0; i < c.n_cams; ++i) crot[i] = rot_from_r(&s.cams[size_t(9) * i]);
     std::geometric_distribution<int> geo(1.0 / 3.0);
     std::uniform_int_distribution<int> kdist(c.kmin, c.kmax);
     std::vector<std::pair<double, int32_t>> cand;
@@ -393,10 +409,15 @@ Scene config_scene(int idx, uint64_t seed) {
         int k = c.track == 1 ? std::clamp(2 + geo(rng), c.kmin, c.kmax) : kdist(rng);
         // visible cameras: in front, inside the 2000 x 1500 image (centred)
         vis.clear();
+        // k1 = k2 = 0 here, so u = f * (v_x / v_z, v_y / v_z)
         auto visible = [&](int32_t i) {
-            double u[2];
-            if (!project(&s.cams[size_t(9) * i], 9, X, u)) return false;
-            return std::fabs(u[0]) <= fx && std::fabs(u[1]) <= fy;
+            const Rot& R = crot[i];
+            const double* c = &s.cams[size_t(9) * i];
+            const double w[3] = {X[0] - c[3], X[1] - c[4], X[2] - c[5]};
+            double v[3];
+            for (int a = 0; a < 3; ++a) v[a] = R.m[a][0] * w[0] + R.m[a][1] * w[1] + R.m[a][2] * w[2];
+            if (!(v[2] > 1e-9)) return false;
+            return std::fabs(c[6] * v[0] / v[2]) <= fx && std::fabs(c[6] * v[1] / v[2]) <= fy;
         };
         if (!c.nearest) {
             for (int32_t i = 0; i < c.n_cams; ++i) if (visible(i)) vis.push_back(i);
@@ -421,7 +442,7 @@ Scene config_scene(int idx, uint64_t seed) {
         chosen.assign(vis.begin(), vis.begin() + k);
         std::sort(chosen.begin(), chosen.end());
         s.pts.insert(s.pts.end(), X, X + 3);
-        for (int32_t i : chosen) add_obs(s, i, (int32_t)j);
+        for (int32_t i : chosen) add_obs(s, i, (int32_t)j, &crot[i]);
         ++j;
     }
     add_noise(s, 1.0, rng);

@@ -22,6 +22,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unistd.h>
+#include <vector>
 #include <vector>
 
 namespace sfm {
@@ -50,8 +52,10 @@ enum Mode { M_INDEX, M_JACOBIAN, M_NULLSPACE, M_FISHER, M_SCHUR, M_FULL };
 
 struct sfmcov_handle {
     int device = 0;
-    cudaStream_t s = nullptr, s2 = nullptr;
+    cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
     cudaEvent_t e1 = nullptr, e2 = nullptr;
+    static constexpr int kRing = 4;  // panel ring buffers of the fused sweep
+    cudaEvent_t eL[kRing], eT[kRing];
     cudaEvent_t ev[ST_COUNT + 1];
     bool profiling = false;
     std::mutex mu;
@@ -61,7 +65,7 @@ struct sfmcov_handle {
     // index
     DBuf cnt_cam, cnt_pt, off_cam, idx_cam, off_pt, idx_pt, pos_cam, key_scratch;
     // stage buffers
-    DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Lpt, Wb, V, Fpart, LF, E, eigE, Gamma, G, Z, Linv, Lp, piv, cov,
+    DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Lpt, Wb, V, Fpart, LF, E, eigE, Gamma, G, Z, Linv, Lp, ring, piv, snap, cov,
         psd, prange, status, depth, H;
     PairDev pairs;
     Status* st_host = nullptr;
@@ -219,13 +223,84 @@ bool use_graph() {
 
 // SFMCOV_SERIAL_DENSE=1 runs the lookahead updates on the main stream
 // (debug aid: removes the two-stream overlap).
+// Debug aid: path prefix for Cholesky failure dumps (SFMCOV_CHOL_SNAP).
+const char* snap_prefix() {
+    static const char* p = std::getenv("SFMCOV_CHOL_SNAP");
+    return (p && *p) ? p : nullptr;
+}
+
 bool serial_dense() {
     static bool v = [] { const char* e = std::getenv("SFMCOV_SERIAL_DENSE"); return e && e[0] == '1'; }();
     return v;
 }
 
+// SFMCOV_SWEEP=0 selects the two-pass dense stage (Cholesky, then the
+// triangular inverse); default is the fused sweep.
+bool use_sweep() {
+    static bool v = [] { const char* e = std::getenv("SFMCOV_SWEEP"); return !(e && e[0] == '0'); }();
+    return v;
+}
+
+// Cholesky + in-place triangular inverse of the padded matrix Z (lower
+// triangle); serial = every launch on the main stream.
+int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv, double* piv, Status* st, bool serial,
+              bool mark_stages);
+
 void mark(sfmcov_handle* h, int i) {
     if (h->profiling) SFM_CUDA(cudaEventRecord(h->ev[i], h->s));
+}
+
+int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv, double* piv, Status* st, bool serial,
+              bool mark_stages) {
+    cudaStream_t s = h->s;
+    cudaStream_t s2 = serial ? s : h->s2;
+    const int pw = panel_blocks();
+    int launches = 0;
+    if (use_sweep()) {
+        double* ring = h->ring.as<double>(sweep_ring_doubles(Npad, pw, sfmcov_handle::kRing));
+        launches = dense_sweep(Z, ld, Npad, pw, Linv, piv, st, ring, sfmcov_handle::kRing, s, s2, serial ? s : h->s3,
+                               h->eL, h->eT, h->e2);
+        if (mark_stages) {
+            mark(h, 8);
+            mark(h, 9);
+        }
+        return launches;
+    }
+    double* Lp = h->Lp.as<double>(trtri_lp_doubles(Npad, pw));
+    if (use_graph() && !serial) {
+        // one graph launch for the ~650 kernels of the dense stage; re-captured
+        // when the matrix size, panel width or any buffer address changes
+        const void* key[6] = {Z, Linv, piv, Lp, st, (const void*)(intptr_t)(Npad * 16 + pw)};
+        bool same = h->dense_exec != nullptr;
+        for (int q = 0; q < 6 && same; ++q) same = h->dense_key[q] == key[q];
+        if (!same) {
+            if (h->dense_exec) SFM_CUDA(cudaGraphExecDestroy(h->dense_exec));
+            h->dense_exec = nullptr;
+            const long long before = g_kernel_launches;
+            cudaGraph_t graph;
+            SFM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, s2, h->e1, h->e2);
+            dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, s2, h->e1, h->e2);
+            SFM_CUDA(cudaStreamEndCapture(s, &graph));
+            SFM_CUDA(cudaGraphInstantiate(&h->dense_exec, graph, 0));
+            SFM_CUDA(cudaGraphDestroy(graph));
+            h->dense_launches = g_kernel_launches - before;
+            g_kernel_launches = before;
+            for (int q = 0; q < 6; ++q) h->dense_key[q] = key[q];
+        }
+        SFM_CUDA(cudaGraphLaunch(h->dense_exec, s));
+        g_kernel_launches += h->dense_launches;
+        if (mark_stages) {
+            mark(h, 8);
+            mark(h, 9);
+        }
+        return (int)h->dense_launches;
+    }
+    launches = dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, s2, h->e1, h->e2);
+    if (mark_stages) mark(h, 8);
+    launches += dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, s2, h->e1, h->e2);
+    if (mark_stages) mark(h, 9);
+    return launches;
 }
 
 // The whole device pipeline.  `sc` points at device memory.
@@ -398,54 +473,22 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     const int K = Npad / kNB;
     double* Linv = h->Linv.as<double>((size_t)K * kNB * kNB);
     double* piv = h->piv.as<double>((size_t)Npad);
-    const int pw = panel_blocks();
-    double* Lp = h->Lp.as<double>(trtri_lp_doubles(Npad, pw));
-    cudaStream_t s2 = serial_dense() ? s : h->s2;
-    int launches = 0;
-    if (use_graph() && s2 != s) {
-        // one graph launch for the ~650 kernels of the dense stage; re-captured
-        // when the matrix size, panel width or any buffer address changes
-        const void* key[6] = {Z, Linv, piv, Lp, st, (const void*)(intptr_t)(Npad * 16 + pw)};
-        bool same = h->dense_exec != nullptr;
-        for (int q = 0; q < 6 && same; ++q) same = h->dense_key[q] == key[q];
-        if (!same) {
-            if (h->dense_exec) SFM_CUDA(cudaGraphExecDestroy(h->dense_exec));
-            h->dense_exec = nullptr;
-            const long long before = g_kernel_launches;
-            cudaGraph_t graph;
-            SFM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-            dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, s2, h->e1, h->e2);
-            dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, s2, h->e1, h->e2);
-            SFM_CUDA(cudaStreamEndCapture(s, &graph));
-            SFM_CUDA(cudaGraphInstantiate(&h->dense_exec, graph, 0));
-            SFM_CUDA(cudaGraphDestroy(graph));
-            h->dense_launches = g_kernel_launches - before;
-            g_kernel_launches = before;
-            for (int q = 0; q < 6; ++q) h->dense_key[q] = key[q];
-        }
-        SFM_CUDA(cudaGraphLaunch(h->dense_exec, s));
-        g_kernel_launches += h->dense_launches;
-        mark(h, 8);
-        mark(h, 9);
-    } else {
-        launches = dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, s2, h->e1, h->e2);
-        mark(h, 8);
-        launches += dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, s2, h->e1, h->e2);
-        mark(h, 9);
-    }
+    const bool serial = serial_dense();
+    g_chol_snap = snap_prefix() ? h->snap.as<double>((size_t)K * kNB * kNB) : nullptr;
+    run_dense(h, Z, ld, Npad, Linv, piv, st, serial, true);
+    g_chol_snap = nullptr;
     int* psd = h->psd.as<int>(1);
     SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
     launch_extract(P, Z, ld, N, n, s_a, 1, out.d_cam_cov, st, psd, s);
     double* prange = h->prange.as<double>(2);
     launch_pivot_range(piv, N, prange, s);
     mark(h, 10);
-    (void)launches;
     sync_status(h);
     {
         const Status& q = *h->st_host;
         const bool upstream_ok = q.jac_bad == INT_MAX && q.rot_bad == INT_MAX && q.fisher_bad == INT_MAX &&
                                  q.pt_sing_bad == INT_MAX && !q.border_bad;
-        if (q.chol_bad != INT_MAX && upstream_ok && s2 != s) {
+        if (q.chol_bad != INT_MAX && upstream_ok && !serial) {
             // A non-positive pivot with the two-stream lookahead: redo the
             // dense stage once on a single stream before reporting it (a
             // genuinely degenerate scene fails again).  Counted in
@@ -456,8 +499,30 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
             launch_status_init(st, s);
             launch_fill(P, Z, ld, N, Npad, D, s_a, G, 1, s);
             launch_pair_reduce(P, h->pairs, Wb, n, Z, ld, s);
-            dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, s, h->e1, h->e2);
-            dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, s, h->e1, h->e2);
+            const int cb = q.chol_bad / kNB;
+            std::vector<double> snap_a, snap_b;
+            if (snap_prefix() && cb < K) {
+                snap_a.resize((size_t)kNB * kNB);
+                SFM_CUDA(cudaMemcpy(snap_a.data(), h->snap.as<double>((size_t)K * kNB * kNB) + (size_t)cb * kNB * kNB,
+                                    8 * snap_a.size(), cudaMemcpyDeviceToHost));
+                g_chol_snap = h->snap.as<double>((size_t)K * kNB * kNB);
+            }
+            run_dense(h, Z, ld, Npad, Linv, piv, st, true, false);
+            g_chol_snap = nullptr;
+            if (!snap_a.empty()) {
+                SFM_CUDA(cudaStreamSynchronize(s));
+                snap_b.resize((size_t)kNB * kNB);
+                SFM_CUDA(cudaMemcpy(snap_b.data(), h->snap.as<double>((size_t)K * kNB * kNB) + (size_t)cb * kNB * kNB,
+                                    8 * snap_b.size(), cudaMemcpyDeviceToHost));
+                const std::string path = std::string(snap_prefix()) + "_" + std::to_string((long)getpid()) + ".bin";
+                if (FILE* f = std::fopen(path.c_str(), "wb")) {
+                    const int32_t hdr[4] = {q.chol_bad, Npad, panel_blocks(), cb};
+                    std::fwrite(hdr, 4, 4, f);
+                    std::fwrite(snap_a.data(), 8, snap_a.size(), f);
+                    std::fwrite(snap_b.data(), 8, snap_b.size(), f);
+                    std::fclose(f);
+                }
+            }
             SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
             launch_extract(P, Z, ld, N, n, s_a, 1, out.d_cam_cov, st, psd, s);
             launch_pivot_range(piv, N, prange, s);
@@ -592,7 +657,12 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
         int lo = 0, hi = 0;
         SFM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s, cudaStreamNonBlocking, hi));
-        SFM_CUDA(cudaStreamCreateWithPriority(&h->s2, cudaStreamNonBlocking, lo));
+        SFM_CUDA(cudaStreamCreateWithPriority(&h->s2, cudaStreamNonBlocking, (lo + hi) / 2));
+        SFM_CUDA(cudaStreamCreateWithPriority(&h->s3, cudaStreamNonBlocking, lo));
+        for (int i = 0; i < sfmcov_handle::kRing; ++i) {
+            SFM_CUDA(cudaEventCreateWithFlags(&h->eL[i], cudaEventDisableTiming));
+            SFM_CUDA(cudaEventCreateWithFlags(&h->eT[i], cudaEventDisableTiming));
+        }
         SFM_CUDA(cudaEventCreateWithFlags(&h->e1, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->e2, cudaEventDisableTiming));
         for (auto& ev : h->ev) SFM_CUDA(cudaEventCreate(&ev));
@@ -612,10 +682,11 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaSetDevice(h->device);
     cudaStreamSynchronize(h->s);
     cudaStreamSynchronize(h->s2);
+    cudaStreamSynchronize(h->s3);
     DBuf* bufs[] = {&h->ws.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_u, &h->h_sigma, &h->cnt_cam,
                     &h->cnt_pt, &h->off_cam, &h->idx_cam, &h->off_pt, &h->idx_pt, &h->pos_cam, &h->key_scratch,
                     &h->R, &h->rec, &h->D, &h->Hr, &h->A, &h->s_a, &h->flags, &h->bpart, &h->s_b, &h->Lpt, &h->Wb, &h->V,
-                    &h->Fpart, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->Lp, &h->piv,
+                    &h->Fpart, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->Lp, &h->ring, &h->piv, &h->snap,
                     &h->cov, &h->psd, &h->prange, &h->status, &h->depth, &h->H};
     for (DBuf* b : bufs) b->release();
     h->pairs.release();
@@ -626,6 +697,11 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     for (auto& ev : h->ev) cudaEventDestroy(ev);
     cudaStreamDestroy(h->s);
     cudaStreamDestroy(h->s2);
+    cudaStreamDestroy(h->s3);
+    for (int i = 0; i < sfmcov_handle::kRing; ++i) {
+        cudaEventDestroy(h->eL[i]);
+        cudaEventDestroy(h->eT[i]);
+    }
     delete h;
 }
 
@@ -730,10 +806,7 @@ int32_t sfmcov_cuda_spd_inverse_blocks(sfmcov_handle* h, const double* a, int64_
         const int K = Npad / kNB;
         double* Linv = h->Linv.as<double>((size_t)K * kNB * kNB);
         double* piv = h->piv.as<double>((size_t)Npad);
-        const int G = panel_blocks();
-        double* Lp = h->Lp.as<double>(trtri_lp_doubles(Npad, G));
-        dense_cholesky(Z, ld, Npad, G, Linv, piv, st, s, h->s2, h->e1, h->e2);
-        dense_trtri(Z, ld, Npad, G, Linv, Lp, s, h->s2, h->e1, h->e2);
+        run_dense(h, Z, ld, Npad, Linv, piv, st, serial_dense(), false);
         const int nb = N / block;
         double* dcov = h->cov.as<double>((size_t)block * block * nb);
         int* psd = h->psd.as<int>(1);

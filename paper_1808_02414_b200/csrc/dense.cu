@@ -358,7 +358,7 @@ __device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b
 // A: tile (k0, k0) of the matrix (col-major, ld).  Writes L (lower) back,
 // Linv (kNB x kNB col-major, zeros above), pivots[col0 + j] = L_jj^2.
 __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, long long ld, double* Linv, double* pivots,
-                                                                 int col0, Status* st) {
+                                                                 int col0, Status* st, double* snap) {
     using namespace potrf;
     extern __shared__ double T[];                 // T[c * LDT + r]
     double* Xd = T + kNB * LDT;                   // NSB blocks, row-major 8x8
@@ -371,6 +371,9 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
         const int r = e & (kNB - 1), c = e >> 7;
         T[c * LDT + r] = (r >= c) ? __ldcg(A + (size_t)c * ld + r) : 0.0;
     }
+    if (snap)
+        for (int e = tid; e < kNB * kNB; e += THREADS) snap[e] = T[(e >> 7) * LDT + (e & (kNB - 1))];
+    __syncthreads();  // warp 0 reads the first 8x8 block, loaded by warps 0, 4, 8 and 12
     POTRF_STAMP(0);
     double* rinv = Ws + NWARPS * 64;             // 1 / L_jj
     double* spiv = rinv + kNB;                   // pivots
@@ -514,8 +517,9 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
 const void* k_potrf_diag_ptr() { return (const void*)k_potrf_diag; }
 int potrf_smem_bytes_impl() { return potrf::SMEM; }
 
-void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s) {
-    launch_prio(k_potrf_diag, 1, potrf::THREADS, potrf::SMEM, s, A, ld, Linv, pivots, col0, st);
+void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s,
+                       double* snap) {
+    launch_prio(k_potrf_diag, 1, potrf::THREADS, potrf::SMEM, s, A, ld, Linv, pivots, col0, st, snap);
     SFM_LAUNCH_CHECK();
 }
 
@@ -707,6 +711,11 @@ static GemmArgs gemm_args(double* C, long long ldc, const double* A, long long l
 //   stream s2: the rest of the trailing SYRK (K = W), overlapping the next
 //     panel's factorisation.  Ordering: rest(p) waits the panel (e1);
 //     next-panel(p) waits rest(p-1) (e2).
+// Debug aid (SFMCOV_CHOL_SNAP): when set, every diagonal tile is copied here
+// right before its potrf, so a failing factorisation can be compared with a
+// serial one.  Null in normal operation.
+double* g_chol_snap = nullptr;
+
 int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, cudaStream_t s,
                    cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2) {
     const int K = Npad / kNB;  // 128-blocks
@@ -718,7 +727,8 @@ int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, doubl
         for (int g = 0; g < g_here; ++g) {
             const int c = b0 + g;
             double* Acc = Z + (size_t)c * kNB * ld + (size_t)c * kNB;
-            launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s);
+            launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s,
+                              g_chol_snap ? g_chol_snap + (size_t)c * kNB * kNB : nullptr);
             ++launches;
             const int below = K - c - 1;
             if (below == 0) break;
@@ -844,6 +854,149 @@ int dense_trtri(double* X, long long ld, int Npad, int G, const double* Linv, do
         ++launches;
     }
     if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, e2, 0));
+    return launches;
+}
+
+
+// ----------------------------------------------------------------------------
+// Fused sweep: Cholesky and triangular inverse in one pass over the panels.
+//
+// Step p (panel p = 128-blocks b0 .. b0+g, W = g kNB columns):
+//   s  (critical): potrf / trsm / inner updates of the panel (as in
+//       dense_cholesky); take(p): L[rows >= b0, panel] -> ring buffer Lb and
+//       the panel's W x W diagonal block of Z := I (its columns now hold the
+//       right-hand side of X = L^-1); u(p): next panel columns -= L L^T.
+//   s2 (bulk)    : rest(p): trailing columns beyond the next panel.
+//   s3 (bulk)    : inverse step p on the rows of panel p, columns 0 .. b0+g:
+//       for each block r of the panel: X[r, :] = Linv_r X[r, :], then
+//       X[r', :] -= L[r', r] X[r, :] for the panel's later blocks r';
+//       finally X[rows below, 0 .. b0+g] -= L[below, panel] X[panel rows, :].
+// The Cholesky chain only touches columns >= b0(p+1) after take(p) and the
+// inverse chain only columns < b0(p+1), so the two overlap freely; both read
+// the panel from Lb, which is recycled once inverse step p - NB has finished.
+// ----------------------------------------------------------------------------
+__global__ void k_panel_take(double* Z, long long ld, int b0, int W, int rows, double* Lb) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // one double2 (two rows) each
+    const int half = rows >> 1;
+    if (e >= (long long)half * W) return;
+    const int i = (int)(e % half) * 2, j = (int)(e / half);
+    double2* zp = reinterpret_cast<double2*>(Z + (size_t)(b0 * kNB + j) * ld + (size_t)b0 * kNB + i);
+    const double2 v = __ldcg(zp);
+    *reinterpret_cast<double2*>(Lb + (size_t)j * rows + i) = v;
+    if (i < W) {
+        double2 x;
+        x.x = (i == j) ? 1.0 : 0.0;
+        x.y = (i + 1 == j) ? 1.0 : 0.0;
+        *zp = x;
+    }
+}
+
+static void launch_panel_take(double* Z, long long ld, int b0, int W, int rows, double* Lb, cudaStream_t s) {
+    const long long total = (long long)(rows / 2) * W;
+    k_panel_take<<<cdiv(total, 256), 256, 0, s>>>(Z, ld, b0, W, rows, Lb);
+    SFM_LAUNCH_CHECK();
+}
+
+int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
+                int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
+                cudaEvent_t eR) {
+    const int K = Npad / kNB;
+    int launches = 0;
+    bool rest_pending = false;
+    int last_slot = -1;
+    for (int b0 = 0, p = 0; b0 < K; b0 += G, ++p) {
+        const int g_here = (b0 + G <= K) ? G : K - b0;
+        const int W = g_here * kNB;
+        // --- panel factorisation (critical path) ---
+        for (int g = 0; g < g_here; ++g) {
+            const int c = b0 + g;
+            double* Acc = Z + (size_t)c * kNB * ld + (size_t)c * kNB;
+            launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s,
+                              g_chol_snap ? g_chol_snap + (size_t)c * kNB * kNB : nullptr);
+            ++launches;
+            const int below = K - c - 1;
+            if (below == 0) break;
+            GemmArgs t = gemm_args(Acc + kNB, ld, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
+            launch_gemm(t, s);
+            ++launches;
+            const int inner = b0 + g_here - c - 1;
+            if (inner > 0) {
+                GemmArgs u = gemm_args(Z + (size_t)(c + 1) * kNB * ld + (size_t)(c + 1) * kNB, ld, Acc + kNB, ld,
+                                       Acc + kNB, ld, below, inner, kNB);
+                u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
+                launch_gemm(u, s);
+                ++launches;
+            }
+        }
+        // --- hand the panel over to the inverse ---
+        const int slot = p % NB;
+        if (p >= NB) SFM_CUDA(cudaStreamWaitEvent(s, eT[slot], 0));  // inverse step p - NB done with Lb
+        const int rows = Npad - b0 * kNB;
+        double* Lb = ring + (size_t)slot * Npad * G * kNB;
+        launch_panel_take(Z, ld, b0, W, rows, Lb, s);
+        ++launches;
+        SFM_CUDA(cudaEventRecord(eL[slot], s));
+        const int nb0 = b0 + g_here;
+        const int T2 = K - nb0;
+        const int gn = (T2 < G) ? T2 : G;
+        // --- Cholesky trailing update ---
+        if (T2 > gn) {
+            SFM_CUDA(cudaStreamWaitEvent(s2, eL[slot], 0));
+            const int r0 = nb0 + gn;
+            const double* Lr = Lb + W + (size_t)gn * kNB;
+            GemmArgs r = gemm_args(Z + (size_t)r0 * kNB * ld + (size_t)r0 * kNB, ld, Lr, rows, Lr, rows, T2 - gn,
+                                   T2 - gn, W);
+            r.tri = 1; r.alpha_neg = 1; r.beta = 1;
+            launch_gemm(r, s2);
+            ++launches;
+        }
+        if (T2 > 0) {
+            if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, eR, 0));
+            GemmArgs u = gemm_args(Z + (size_t)nb0 * kNB * ld + (size_t)nb0 * kNB, ld, Lb + W, rows, Lb + W, rows, T2,
+                                   gn, W);
+            u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
+            launch_gemm(u, s);
+            ++launches;
+        }
+        rest_pending = false;
+        if (T2 > gn) {
+            SFM_CUDA(cudaEventRecord(eR, s2));
+            rest_pending = true;
+        }
+        // --- inverse step p (rows of panel p) ---
+        SFM_CUDA(cudaStreamWaitEvent(s3, eL[slot], 0));
+        for (int g = 0; g < g_here; ++g) {
+            const int r = b0 + g;
+            GemmArgs a = gemm_args(Z + (size_t)r * kNB, ld, Linv + (size_t)r * kNB * kNB, kNB, Z + (size_t)r * kNB, ld,
+                                   1, r + 1, kNB);
+            a.b_kmajor = 1;
+            launch_gemm(a, s3);
+            ++launches;
+            const int later = g_here - g - 1;
+            if (later > 0) {
+                GemmArgs u = gemm_args(Z + (size_t)(r + 1) * kNB, ld, Lb + (size_t)g * kNB * rows + (size_t)(g + 1) * kNB,
+                                       rows, Z + (size_t)r * kNB, ld, later, r + 1, kNB);
+                u.b_kmajor = 1; u.alpha_neg = 1; u.beta = 1;
+                launch_gemm(u, s3);
+                ++launches;
+            }
+        }
+        if (T2 > 0) {
+            GemmArgs x = gemm_args(Z + (size_t)nb0 * kNB, ld, Lb + W, rows, Z + (size_t)b0 * kNB, ld, T2, nb0, W);
+            x.b_kmajor = 1; x.alpha_neg = 1; x.beta = 1; x.beta0_from = b0;
+            launch_gemm(x, s3);
+            ++launches;
+        }
+        SFM_CUDA(cudaEventRecord(eT[slot], s3));
+        last_slot = slot;
+        if (debug_sync()) {
+            SFM_CUDA(cudaStreamSynchronize(s));
+            SFM_CUDA(cudaStreamSynchronize(s2));
+            SFM_CUDA(cudaStreamSynchronize(s3));
+        }
+    }
+    if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, eR, 0));
+    if (last_slot >= 0) SFM_CUDA(cudaStreamWaitEvent(s, eT[last_slot], 0));
     return launches;
 }
 

@@ -65,7 +65,7 @@ struct sfmcov_handle {
     // index
     DBuf cnt_cam, cnt_pt, off_cam, idx_cam, off_pt, idx_pt, pos_cam, key_scratch;
     // stage buffers
-    DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Lpt, Wb, V, Fpart, LF, E, eigE, Gamma, G, Z, Linv, Lp, ring, piv, snap, cov,
+    DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Lpt, Wb, V, Fpart, LF, E, eigE, Gamma, G, Z, Linv, Lp, ring, piv, cov,
         psd, prange, status, depth, H;
     PairDev pairs;
     Status* st_host = nullptr;
@@ -119,6 +119,14 @@ struct Outputs {
     sfmcov_diagnostics* diag = nullptr;
 };
 
+// Device -> host copy ordered after the handle's stream.  (A plain
+// cudaMemcpy runs on the legacy default stream, which does not wait for the
+// handle's non-blocking streams.)
+void d2h(sfmcov_handle* h, void* dst, const void* src, size_t bytes) {
+    SFM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->s));
+    SFM_CUDA(cudaStreamSynchronize(h->s));
+}
+
 void sync_status(sfmcov_handle* h) {
     SFM_CUDA(cudaMemcpyAsync(h->st_host, h->status.p, sizeof(Status), cudaMemcpyDeviceToHost, h->s));
     SFM_CUDA(cudaStreamSynchronize(h->s));
@@ -150,7 +158,7 @@ void throw_counts(sfmcov_handle* h) {
         int c = 0;
         const int i = st.cam_count_bad;
         int o[2];
-        SFM_CUDA(cudaMemcpy(o, (int*)h->off_cam.p + i, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+        d2h(h, o, (int*)h->off_cam.p + i, 2 * sizeof(int));
         c = o[1] - o[0];
         throw ApiError{SFMCOV_ERR_INVARIANT, "validate",
                        "camera " + std::to_string(i) + " observes " + std::to_string(c) + " points, need at least 4"};
@@ -158,7 +166,7 @@ void throw_counts(sfmcov_handle* h) {
     if (st.pt_count_bad != INT_MAX) {
         const int j = st.pt_count_bad;
         int o[2];
-        SFM_CUDA(cudaMemcpy(o, (int*)h->off_pt.p + j, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+        d2h(h, o, (int*)h->off_pt.p + j, 2 * sizeof(int));
         throw ApiError{SFMCOV_ERR_INVARIANT, "validate",
                        "point " + std::to_string(j) + " is observed by " + std::to_string(o[1] - o[0]) +
                            " cameras, need at least 2"};
@@ -223,12 +231,6 @@ bool use_graph() {
 
 // SFMCOV_SERIAL_DENSE=1 runs the lookahead updates on the main stream
 // (debug aid: removes the two-stream overlap).
-// Debug aid: path prefix for Cholesky failure dumps (SFMCOV_CHOL_SNAP).
-const char* snap_prefix() {
-    static const char* p = std::getenv("SFMCOV_CHOL_SNAP");
-    return (p && *p) ? p : nullptr;
-}
-
 bool serial_dense() {
     static bool v = [] { const char* e = std::getenv("SFMCOV_SERIAL_DENSE"); return e && e[0] == '1'; }();
     return v;
@@ -338,12 +340,12 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     }
     if (mode == M_INDEX) {
         std::vector<int> oc(n + 1), op(m + 1);
-        SFM_CUDA(cudaMemcpy(oc.data(), ix.off_cam, 4 * (size_t)(n + 1), cudaMemcpyDeviceToHost));
-        SFM_CUDA(cudaMemcpy(op.data(), ix.off_pt, 4 * (size_t)(m + 1), cudaMemcpyDeviceToHost));
+        d2h(h, oc.data(), ix.off_cam, 4 * (size_t)(n + 1));
+        d2h(h, op.data(), ix.off_pt, 4 * (size_t)(m + 1));
         for (int i = 0; i <= n; ++i) out.off_cam[i] = oc[i];
         for (int j = 0; j <= m; ++j) out.off_pt[j] = op[j];
-        SFM_CUDA(cudaMemcpy(out.idx_cam, ix.idx_cam, 4 * (size_t)t, cudaMemcpyDeviceToHost));
-        SFM_CUDA(cudaMemcpy(out.idx_pt, ix.idx_pt, 4 * (size_t)t, cudaMemcpyDeviceToHost));
+        d2h(h, out.idx_cam, ix.idx_cam, 4 * (size_t)t);
+        d2h(h, out.idx_pt, ix.idx_pt, 4 * (size_t)t);
         return;
     }
     mark(h, 1);
@@ -356,7 +358,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         sync_status(h);
         throw_numeric(h, sc, mode);
         std::vector<double> r((size_t)kRec * t);
-        SFM_CUDA(cudaMemcpy(r.data(), rec, 8 * r.size(), cudaMemcpyDeviceToHost));
+        d2h(h, r.data(), rec, 8 * r.size());
         for (int k = 0; k < t; ++k) {
             std::memcpy(out.jc + (size_t)2 * P * k, &r[(size_t)kRec * k], 8 * 2 * P);
             std::memcpy(out.jp + (size_t)6 * k, &r[(size_t)kRec * k + 2 * P], 8 * 6);
@@ -381,16 +383,16 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         if (out.H) {
             double* H = h->H.as<double>(ncols * 7);
             launch_write_h(sc, Hr, H, s);
-            SFM_CUDA(cudaMemcpy(out.H, H, 8 * ncols * 7, cudaMemcpyDeviceToHost));
+            d2h(h, out.H, H, 8 * ncols * 7);
         }
-        if (out.D) SFM_CUDA(cudaMemcpy(out.D, D, 8 * (size_t)P * P * n, cudaMemcpyDeviceToHost));
-        if (out.A) SFM_CUDA(cudaMemcpy(out.A, A, 8 * 9 * (size_t)m, cudaMemcpyDeviceToHost));
-        if (out.s_a) SFM_CUDA(cudaMemcpy(out.s_a, s_a, 8 * ncols, cudaMemcpyDeviceToHost));
-        if (out.s_b) SFM_CUDA(cudaMemcpy(out.s_b, s_b, 8 * 7, cudaMemcpyDeviceToHost));
+        if (out.D) d2h(h, out.D, D, 8 * (size_t)P * P * n);
+        if (out.A) d2h(h, out.A, A, 8 * 9 * (size_t)m);
+        if (out.s_a) d2h(h, out.s_a, s_a, 8 * ncols);
+        if (out.s_b) d2h(h, out.s_b, s_b, 8 * 7);
         if (out.Cp) {
             // couplings C_t = (J_c^T W) J_p from the records (host assembly of a test output)
             std::vector<double> r((size_t)kRec * t);
-            SFM_CUDA(cudaMemcpy(r.data(), rec, 8 * r.size(), cudaMemcpyDeviceToHost));
+            d2h(h, r.data(), rec, 8 * r.size());
             for (int k = 0; k < t; ++k) {
                 const double* jc = &r[(size_t)kRec * k];
                 const double* jp = jc + 2 * P;
@@ -405,7 +407,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         }
         if (out.diag) {
             std::vector<unsigned char> f(ncols);
-            SFM_CUDA(cudaMemcpy(f.data(), flags, ncols, cudaMemcpyDeviceToHost));
+            d2h(h, f.data(), flags, ncols);
             int64_t cnt = 0;
             for (size_t c = 0; c < ncols; ++c)
                 if (f[c]) {
@@ -455,9 +457,9 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         // bordered Z_p: [[Z, Γ], [Γ^T, E]] (host assembly of a test output)
         const size_t dim = (size_t)N + 7;
         std::vector<double> z((size_t)Npad * Npad), gm((size_t)N * 7), e(49);
-        SFM_CUDA(cudaMemcpy(z.data(), Z, 8 * z.size(), cudaMemcpyDeviceToHost));
-        SFM_CUDA(cudaMemcpy(gm.data(), Gamma, 8 * gm.size(), cudaMemcpyDeviceToHost));
-        SFM_CUDA(cudaMemcpy(e.data(), E, 8 * 49, cudaMemcpyDeviceToHost));
+        d2h(h, z.data(), Z, 8 * z.size());
+        d2h(h, gm.data(), Gamma, 8 * gm.size());
+        d2h(h, e.data(), E, 8 * 49);
         for (size_t c = 0; c < dim; ++c)
             for (size_t r = 0; r < dim; ++r) {
                 double v;
@@ -474,9 +476,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     double* Linv = h->Linv.as<double>((size_t)K * kNB * kNB);
     double* piv = h->piv.as<double>((size_t)Npad);
     const bool serial = serial_dense();
-    g_chol_snap = snap_prefix() ? h->snap.as<double>((size_t)K * kNB * kNB) : nullptr;
     run_dense(h, Z, ld, Npad, Linv, piv, st, serial, true);
-    g_chol_snap = nullptr;
     int* psd = h->psd.as<int>(1);
     SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
     launch_extract(P, Z, ld, N, n, s_a, 1, out.d_cam_cov, st, psd, s);
@@ -499,30 +499,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
             launch_status_init(st, s);
             launch_fill(P, Z, ld, N, Npad, D, s_a, G, 1, s);
             launch_pair_reduce(P, h->pairs, Wb, n, Z, ld, s);
-            const int cb = q.chol_bad / kNB;
-            std::vector<double> snap_a, snap_b;
-            if (snap_prefix() && cb < K) {
-                snap_a.resize((size_t)kNB * kNB);
-                SFM_CUDA(cudaMemcpy(snap_a.data(), h->snap.as<double>((size_t)K * kNB * kNB) + (size_t)cb * kNB * kNB,
-                                    8 * snap_a.size(), cudaMemcpyDeviceToHost));
-                g_chol_snap = h->snap.as<double>((size_t)K * kNB * kNB);
-            }
             run_dense(h, Z, ld, Npad, Linv, piv, st, true, false);
-            g_chol_snap = nullptr;
-            if (!snap_a.empty()) {
-                SFM_CUDA(cudaStreamSynchronize(s));
-                snap_b.resize((size_t)kNB * kNB);
-                SFM_CUDA(cudaMemcpy(snap_b.data(), h->snap.as<double>((size_t)K * kNB * kNB) + (size_t)cb * kNB * kNB,
-                                    8 * snap_b.size(), cudaMemcpyDeviceToHost));
-                const std::string path = std::string(snap_prefix()) + "_" + std::to_string((long)getpid()) + ".bin";
-                if (FILE* f = std::fopen(path.c_str(), "wb")) {
-                    const int32_t hdr[4] = {q.chol_bad, Npad, panel_blocks(), cb};
-                    std::fwrite(hdr, 4, 4, f);
-                    std::fwrite(snap_a.data(), 8, snap_a.size(), f);
-                    std::fwrite(snap_b.data(), 8, snap_b.size(), f);
-                    std::fclose(f);
-                }
-            }
             SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
             launch_extract(P, Z, ld, N, n, s_a, 1, out.d_cam_cov, st, psd, s);
             launch_pivot_range(piv, N, prange, s);
@@ -542,9 +519,9 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         sfmcov_diagnostics* d = out.diag;
         double pr[2], ee[8];
         int warn = 0;
-        SFM_CUDA(cudaMemcpy(pr, prange, 16, cudaMemcpyDeviceToHost));
-        SFM_CUDA(cudaMemcpy(ee, eigE, 56, cudaMemcpyDeviceToHost));
-        SFM_CUDA(cudaMemcpy(&warn, psd, 4, cudaMemcpyDeviceToHost));
+        d2h(h, pr, prange, 16);
+        d2h(h, ee, eigE, 56);
+        d2h(h, &warn, psd, 4);
         double mn = pr[0], mx = pr[1];
         for (int l = 0; l < 7; ++l) { mn = std::min(mn, std::fabs(ee[l])); mx = std::max(mx, std::fabs(ee[l])); }
         d->min_pivot = mn;
@@ -557,8 +534,8 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         // scale range and flagged columns
         std::vector<double> sa(ncols);
         std::vector<unsigned char> f(ncols);
-        SFM_CUDA(cudaMemcpy(sa.data(), s_a, 8 * ncols, cudaMemcpyDeviceToHost));
-        if (h->st_host->nflag) SFM_CUDA(cudaMemcpy(f.data(), flags, ncols, cudaMemcpyDeviceToHost));
+        d2h(h, sa.data(), s_a, 8 * ncols);
+        if (h->st_host->nflag) d2h(h, f.data(), flags, ncols);
         d->scale_min = ncols ? *std::min_element(sa.begin(), sa.end()) : 1.0;
         d->scale_max = ncols ? *std::max_element(sa.begin(), sa.end()) : 1.0;
         int64_t cnt = 0;
@@ -686,7 +663,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     DBuf* bufs[] = {&h->ws.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_u, &h->h_sigma, &h->cnt_cam,
                     &h->cnt_pt, &h->off_cam, &h->idx_cam, &h->off_pt, &h->idx_pt, &h->pos_cam, &h->key_scratch,
                     &h->R, &h->rec, &h->D, &h->Hr, &h->A, &h->s_a, &h->flags, &h->bpart, &h->s_b, &h->Lpt, &h->Wb, &h->V,
-                    &h->Fpart, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->Lp, &h->ring, &h->piv, &h->snap,
+                    &h->Fpart, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->Lp, &h->ring, &h->piv,
                     &h->cov, &h->psd, &h->prange, &h->status, &h->depth, &h->H};
     for (DBuf* b : bufs) b->release();
     h->pairs.release();
@@ -818,9 +795,9 @@ int32_t sfmcov_cuda_spd_inverse_blocks(sfmcov_handle* h, const double* a, int64_
         if (h->st_host->chol_bad != INT_MAX)
             throw ApiError{SFMCOV_ERR_DEGENERATE, "factorization",
                            "non-positive pivot at index " + std::to_string(h->st_host->chol_bad) + "; matrix is not positive definite"};
-        SFM_CUDA(cudaMemcpy(blocks, dcov, 8 * (size_t)block * block * nb, cudaMemcpyDeviceToHost));
+        d2h(h, blocks, dcov, 8 * (size_t)block * block * nb);
         double pr[2];
-        SFM_CUDA(cudaMemcpy(pr, prange, 16, cudaMemcpyDeviceToHost));
+        d2h(h, pr, prange, 16);
         if (min_pivot) *min_pivot = pr[0];
         if (max_pivot) *max_pivot = pr[1];
     });

@@ -358,7 +358,7 @@ __device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b
 // A: tile (k0, k0) of the matrix (col-major, ld).  Writes L (lower) back,
 // Linv (kNB x kNB col-major, zeros above), pivots[col0 + j] = L_jj^2.
 __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, long long ld, double* Linv, double* pivots,
-                                                                 int col0, Status* st, double* snap) {
+                                                                 int col0, Status* st) {
     using namespace potrf;
     extern __shared__ double T[];                 // T[c * LDT + r]
     double* Xd = T + kNB * LDT;                   // NSB blocks, row-major 8x8
@@ -371,8 +371,6 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
         const int r = e & (kNB - 1), c = e >> 7;
         T[c * LDT + r] = (r >= c) ? __ldcg(A + (size_t)c * ld + r) : 0.0;
     }
-    if (snap)
-        for (int e = tid; e < kNB * kNB; e += THREADS) snap[e] = T[(e >> 7) * LDT + (e & (kNB - 1))];
     __syncthreads();  // warp 0 reads the first 8x8 block, loaded by warps 0, 4, 8 and 12
     POTRF_STAMP(0);
     double* rinv = Ws + NWARPS * 64;             // 1 / L_jj
@@ -517,9 +515,8 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
 const void* k_potrf_diag_ptr() { return (const void*)k_potrf_diag; }
 int potrf_smem_bytes_impl() { return potrf::SMEM; }
 
-void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s,
-                       double* snap) {
-    launch_prio(k_potrf_diag, 1, potrf::THREADS, potrf::SMEM, s, A, ld, Linv, pivots, col0, st, snap);
+void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s) {
+    launch_prio(k_potrf_diag, 1, potrf::THREADS, potrf::SMEM, s, A, ld, Linv, pivots, col0, st);
     SFM_LAUNCH_CHECK();
 }
 
@@ -711,11 +708,6 @@ static GemmArgs gemm_args(double* C, long long ldc, const double* A, long long l
 //   stream s2: the rest of the trailing SYRK (K = W), overlapping the next
 //     panel's factorisation.  Ordering: rest(p) waits the panel (e1);
 //     next-panel(p) waits rest(p-1) (e2).
-// Debug aid (SFMCOV_CHOL_SNAP): when set, every diagonal tile is copied here
-// right before its potrf, so a failing factorisation can be compared with a
-// serial one.  Null in normal operation.
-double* g_chol_snap = nullptr;
-
 int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, cudaStream_t s,
                    cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2) {
     const int K = Npad / kNB;  // 128-blocks
@@ -727,8 +719,7 @@ int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, doubl
         for (int g = 0; g < g_here; ++g) {
             const int c = b0 + g;
             double* Acc = Z + (size_t)c * kNB * ld + (size_t)c * kNB;
-            launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s,
-                              g_chol_snap ? g_chol_snap + (size_t)c * kNB * kNB : nullptr);
+            launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s);
             ++launches;
             const int below = K - c - 1;
             if (below == 0) break;
@@ -911,8 +902,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
         for (int g = 0; g < g_here; ++g) {
             const int c = b0 + g;
             double* Acc = Z + (size_t)c * kNB * ld + (size_t)c * kNB;
-            launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s,
-                              g_chol_snap ? g_chol_snap + (size_t)c * kNB * kNB : nullptr);
+            launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s);
             ++launches;
             const int below = K - c - 1;
             if (below == 0) break;

@@ -125,8 +125,7 @@ void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, doubl
 // dense.cu
 void dense_init_attributes();
 void launch_gemm(const GemmArgs& g, cudaStream_t s);
-void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s,
-                       double* snap = nullptr);
+void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s);
 void launch_copy_diag(double* X, long long ld, int k, const double* Linv, cudaStream_t s);
 void launch_copy_panel(const double* X, long long ld, int k, int rows, double* Lp, cudaStream_t s);
 void launch_copy_panel_w(const double* X, long long ld, int b0, int G, int rows, double* Lp, cudaStream_t s);
@@ -134,7 +133,6 @@ void launch_extract(int P, const double* X, long long ld, int N, int nblocks, co
                     Status* st, int* psd_warn, cudaStream_t s);
 void launch_set_diag(double* Z, long long ld, int from, int to, cudaStream_t s);
 void launch_pivot_range(const double* piv, int N, double* out, cudaStream_t s);
-extern double* g_chol_snap;
 int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, cudaStream_t s,
                    cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2);
 int dense_trtri(double* X, long long ld, int Npad, int G, const double* Linv, double* Lp, cudaStream_t s,

@@ -27,6 +27,7 @@
 #include "kernels.cuh"
 
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 namespace sfm {
 
@@ -293,17 +294,22 @@ __global__ void k_fill(double* Z, long long ld, int N, int Npad, const double* D
     }
     const int rr = tid & 63;
     const int r = r0 + rr;
+    double g[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) g[q] = add_gg ? gr[rr][q] : 0.0;  // this thread's row, once
+    const int ir = r / P;
+    const double sr = (r < N) ? s_a[r] : 0.0;
     for (int cc = tid >> 6; cc < 64; cc += blockDim.x >> 6) {
         const int c = c0 + cc;
         double v;
         if (r < N && c < N) {
             v = 0.0;
-            const int ir = r / P, ic = c / P;
-            if (ir == ic) v = (s_a[r] * D[(size_t)P * P * ir + P * (r - P * ir) + (c - P * ic)]) * s_a[c];
+            const int ic = c / P;
+            if (ir == ic) v = (sr * D[(size_t)P * P * ir + P * (r - P * ir) + (c - P * ic)]) * s_a[c];
             if (add_gg) {
                 double gg = 0.0;
 #pragma unroll
-                for (int q = 0; q < 7; ++q) gg += gr[rr][q] * gc[cc][q];
+                for (int q = 0; q < 7; ++q) gg += g[q] * gc[cc][q];  // gc row: warp-uniform broadcast
                 v += gg;
             }
         } else {
@@ -399,6 +405,87 @@ __global__ void __launch_bounds__(256, 4) k_pair_reduce(const unsigned int* ukey
             double* z = Z + ((size_t)P * lo + q) * ld + row;
             *z = *z - acc[q];
         }
+    }
+}
+
+// Tensor-core variant (default): warp per camera-pair block, one FP64
+// m8n8k4 MMA per pair and 8x8 tile.  With r = lane/4, k = lane%4 every lane
+// loads a = W_hi[r][k] and b = W_lo[r][k] (k = 3 is the zero pad), and the
+// MMA yields out(p, q) = Σ_k W_hi[p][k] W_lo[q][k] for p, q < 8 with lane
+// holding (p = lane/4, q = 2(lane%4) + {0,1}).  For P = 9 three more tiles
+// carry row 8 / column 8 (operands non-zero on lanes 0..3 only).  The pair
+// list of a segment is read 32 at a time with one coalesced load and
+// broadcast by shuffles; four pairs are gathered ahead of their MMAs.
+__device__ __forceinline__ void dmma_pr(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) k_pair_reduce_mma(const unsigned int* ukeys, const long long* seg_off, int nseg,
+                                                         const unsigned long long* vals, const double* Wb, int n,
+                                                         double* Z, long long ld) {
+    constexpr int NT = (P == 9) ? 4 : 1;  // 8x8 tiles: (0,0) [, (8,0), (0,8), (8,8)]
+    constexpr int U = 4;                  // pairs gathered ahead
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= nseg) return;
+    const int r = lane >> 2, k = lane & 3;
+    const bool kv = k < 3;
+    const bool r8 = (P == 9) && (r == 0) && kv;  // lanes 0..2 carry row 8
+    const long long b = seg_off[warp], e = seg_off[warp + 1];
+    double c[NT][2];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) c[t][0] = c[t][1] = 0.0;
+    for (long long base = b; base < e; base += 32) {
+        const int cnt = (int)min(32LL, e - base);
+        const unsigned long long mine = (lane < cnt) ? __ldg(vals + base + lane) : 0ULL;
+        for (int i0 = 0; i0 < cnt; i0 += U) {
+            double ah[U], al[U], ah8[U], al8[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const unsigned long long v = __shfl_sync(0xffffffffu, mine, (i0 + u) & 31);
+                const bool ok = i0 + u < cnt;
+                const double* wh = Wb + (size_t)(v >> 32) * kWStride;
+                const double* wl = Wb + (size_t)(v & 0xffffffffULL) * kWStride;
+                ah[u] = (ok && kv) ? __ldg(wh + 3 * r + k) : 0.0;
+                al[u] = (ok && kv) ? __ldg(wl + 3 * r + k) : 0.0;
+                if (P == 9) {
+                    ah8[u] = (ok && r8) ? __ldg(wh + 24 + k) : 0.0;
+                    al8[u] = (ok && r8) ? __ldg(wl + 24 + k) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                dmma_pr(c[0][0], c[0][1], ah[u], al[u]);
+                if (P == 9) {
+                    dmma_pr(c[NT > 1 ? 1 : 0][0], c[NT > 1 ? 1 : 0][1], ah8[u], al[u]);
+                    dmma_pr(c[NT > 2 ? 2 : 0][0], c[NT > 2 ? 2 : 0][1], ah[u], al8[u]);
+                    dmma_pr(c[NT > 3 ? 3 : 0][0], c[NT > 3 ? 3 : 0][1], ah8[u], al8[u]);
+                }
+            }
+        }
+    }
+    const unsigned int key = ukeys[warp];
+    const int lo = (int)(key / (unsigned int)n), hi = (int)(key - (unsigned int)lo * (unsigned int)n);
+    const bool diag = lo == hi;
+    // Z(P hi + p, P lo + q) -= out(p, q); diagonal blocks: lower part only
+    auto put = [&](int p, int q, double v) {
+        if (diag && p < q) return;
+        double* z = Z + ((size_t)P * lo + q) * ld + (size_t)P * hi + p;
+        *z = *z - v;
+    };
+    const int q0 = 2 * k;
+    put(r, q0, c[0][0]);
+    put(r, q0 + 1, c[0][1]);
+    if (P == 9) {
+        if (r == 0) {                      // tile (8, 0): row 8, columns q0, q0+1
+            put(8, q0, c[NT > 1 ? 1 : 0][0]);
+            put(8, q0 + 1, c[NT > 1 ? 1 : 0][1]);
+        }
+        if (k == 0) put(r, 8, c[NT > 2 ? 2 : 0][0]);      // tile (0, 8): column 8
+        if (lane == 0) put(8, 8, c[NT > 3 ? 3 : 0][0]);   // tile (8, 8)
     }
 }
 
@@ -500,8 +587,14 @@ void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace&
 void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, cudaStream_t s) {
     if (!pd.nseg) return;
     const unsigned blocks = cdiv(pd.nseg, 8);
-    if (P == 8) k_pair_reduce<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
-    else k_pair_reduce<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
+    static const bool scalar = [] { const char* e = std::getenv("SFMCOV_PAIR_SCALAR"); return e && e[0] == '1'; }();
+    if (scalar) {
+        if (P == 8) k_pair_reduce<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
+        else k_pair_reduce<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
+    } else {
+        if (P == 8) k_pair_reduce_mma<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
+        else k_pair_reduce_mma<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
+    }
     SFM_LAUNCH_CHECK();
 }
 

@@ -159,7 +159,9 @@ __global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const
     // normal (9) and rhs (9); each entry is a sequential sum over the
     // camera's observations in ascending order.
     constexpr int NE = P * P + 18;
-    constexpr int CH = 64, RS = kRec + 4;  // staged record [jc | jp | W | pad] + X at 28..30
+    // staged record [jc | jp | W | pad] at 0..27, X at 28..30, the rhs
+    // factors tg[ii][q] (6) at 32..37
+    constexpr int CH = 64, RS = kRec + 10, TG = 32;
     __shared__ double stage[CH][RS];
     __shared__ double sh[NE];
     const int i = blockIdx.x;
@@ -191,33 +193,62 @@ __global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const
             stage[o][2 * part + 1] = v.y;
         }
         __syncthreads();
-        if (kind == 0) {
-            for (int o = 0; o < nc; ++o) {
-                const double* jc = stage[o] + Layout<P>::JC;
-                const double* W = stage[o] + Layout<P>::WO;
-                const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
-                const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
-                acc += t0 * jc[q] + t1 * jc[P + q];
+        // rhs factors, once per observation and column q:
+        // tg[ii][q] = -((jc_r . [C]x col q) + (jp . [X]x col q))
+        for (int w = tid; w < nc * 3; w += 128) {
+            const int o = w / 3, qq = w - 3 * o;
+            const double* r = stage[o];
+            const double* jc = r + Layout<P>::JC;
+            const double* jp = r + Layout<P>::JP;
+            double hx[9];
+            skew(r + 28, hx);
+            for (int ii = 0; ii < 2; ++ii) {
+                const double a = (jc[P * ii + 3] * hc[0 + qq] + jc[P * ii + 4] * hc[3 + qq]) + jc[P * ii + 5] * hc[6 + qq];
+                const double bb = (jp[3 * ii + 0] * hx[0 + qq] + jp[3 * ii + 1] * hx[3 + qq]) + jp[3 * ii + 2] * hx[6 + qq];
+                stage[o][TG + 3 * ii + qq] = -(a + bb);
             }
-        } else if (kind == 1) {
-            for (int o = 0; o < nc; ++o) {
-                const double* jc = stage[o] + Layout<P>::JC;
-                acc += jc[p] * jc[q] + jc[P + p] * jc[P + q];
+        }
+        __syncthreads();
+        // ordered sums over the chunk; terms of 4 observations are formed
+        // independently and added in observation order (bit-identical to a
+        // plain sequential loop)
+        if (kind < 3) {
+            int o = 0;
+            for (; o + 4 <= nc; o += 4) {
+                double tv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double* r = stage[o + u];
+                    const double* jc = r + Layout<P>::JC;
+                    if (kind == 0) {
+                        const double* W = r + Layout<P>::WO;
+                        const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
+                        const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
+                        tv[u] = t0 * jc[q] + t1 * jc[P + q];
+                    } else if (kind == 1) {
+                        tv[u] = jc[p] * jc[q] + jc[P + p] * jc[P + q];
+                    } else {
+                        tv[u] = jc[p] * r[TG + q] + jc[P + p] * r[TG + 3 + q];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc += tv[u];
             }
-        } else if (kind == 2) {
-            for (int o = 0; o < nc; ++o) {
+            for (; o < nc; ++o) {
                 const double* r = stage[o];
                 const double* jc = r + Layout<P>::JC;
-                const double* jp = r + Layout<P>::JP;
-                double hx[9];
-                skew(r + 28, hx);
-                double tg[2];
-                for (int ii = 0; ii < 2; ++ii) {
-                    const double a = (jc[P * ii + 3] * hc[0 + q] + jc[P * ii + 4] * hc[3 + q]) + jc[P * ii + 5] * hc[6 + q];
-                    const double bb = (jp[3 * ii + 0] * hx[0 + q] + jp[3 * ii + 1] * hx[3 + q]) + jp[3 * ii + 2] * hx[6 + q];
-                    tg[ii] = -(a + bb);
+                double tv;
+                if (kind == 0) {
+                    const double* W = r + Layout<P>::WO;
+                    const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
+                    const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
+                    tv = t0 * jc[q] + t1 * jc[P + q];
+                } else if (kind == 1) {
+                    tv = jc[p] * jc[q] + jc[P + p] * jc[P + q];
+                } else {
+                    tv = jc[p] * r[TG + q] + jc[P + p] * r[TG + 3 + q];
                 }
-                acc += jc[p] * tg[0] + jc[P + p] * tg[1];
+                acc += tv;
             }
         }
         __syncthreads();

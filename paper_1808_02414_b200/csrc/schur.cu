@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(128) k_point_prep(const double* A, const doubl
 // W_a = C_s,a L_j^-T (P x 3) per observation (thread per observation, records
 // read in observation order), stored at the observation's by-camera slot.
 template <int P>
-__global__ void __launch_bounds__(128) k_obs_factor(const int* oc, const int* op, const int* pos_cam, const double* rec,
+__global__ void __launch_bounds__(128, 6) k_obs_factor(const int* oc, const int* op, const int* pos_cam, const double* rec,
                                                     const double* s_a, const double* Lpt, int t_count, int n,
                                                     double* Wb) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -231,7 +231,20 @@ __global__ void __launch_bounds__(64) k_camera_border(const int* off_cam, const 
         }
         __syncthreads();
         if (tid < NE) {
-            for (int o = 0; o < nc; ++o) {
+            // terms of 4 observations formed independently, added in order
+            int o = 0;
+            for (; o + 4 <= nc; o += 4) {
+                double tv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double* w = stage[o + u];
+                    const double* vj = w + 27;
+                    tv[u] = (w[3 * p] * vj[l] + w[3 * p + 1] * vj[7 + l]) + w[3 * p + 2] * vj[14 + l];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc += tv[u];
+            }
+            for (; o < nc; ++o) {
                 const double* w = stage[o];
                 const double* vj = w + 27;
                 acc += (w[3 * p] * vj[l] + w[3 * p + 1] * vj[7 + l]) + w[3 * p + 2] * vj[14 + l];
@@ -422,19 +435,30 @@ __device__ __forceinline__ void dmma_pr(double& d0, double& d1, double a, double
                  : "d"(a), "d"(b));
 }
 
-template <int P>
-__global__ void __launch_bounds__(256) k_pair_reduce_mma(const unsigned int* ukeys, const long long* seg_off, int nseg,
+template <int P, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned int* ukeys, const long long* seg_off, int nseg,
+                                                         const int* chunk_off, int nchunks, int chunk,
                                                          const unsigned long long* vals, const double* Wb, int n,
-                                                         double* Z, long long ld) {
+                                                         double* Z, long long ld, double* part) {
     constexpr int NT = (P == 9) ? 4 : 1;  // 8x8 tiles: (0,0) [, (8,0), (0,8), (8,8)]
-    constexpr int U = 4;                  // pairs gathered ahead
+    // U: pairs gathered ahead
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (warp >= nseg) return;
+    if (warp >= nchunks) return;
+    // segment of this chunk: largest sg with chunk_off[sg] <= warp
+    int lo_s = 0, hi_s = nseg - 1;
+    while (lo_s < hi_s) {
+        const int mid = (lo_s + hi_s + 1) >> 1;
+        if (__ldg(chunk_off + mid) <= warp) lo_s = mid; else hi_s = mid - 1;
+    }
+    const int sg = lo_s;
+    const int c0 = __ldg(chunk_off + sg), nch = __ldg(chunk_off + sg + 1) - c0;
     const int r = lane >> 2, k = lane & 3;
     const bool kv = k < 3;
     const bool r8 = (P == 9) && (r == 0) && kv;  // lanes 0..2 carry row 8
-    const long long b = seg_off[warp], e = seg_off[warp + 1];
+    const long long sb = seg_off[sg], se = seg_off[sg + 1];
+    const long long b = sb + (long long)(warp - c0) * chunk;
+    const long long e = min(se, b + chunk);
     double c[NT][2];
 #pragma unroll
     for (int t = 0; t < NT; ++t) c[t][0] = c[t][1] = 0.0;
@@ -467,11 +491,14 @@ __global__ void __launch_bounds__(256) k_pair_reduce_mma(const unsigned int* uke
             }
         }
     }
-    const unsigned int key = ukeys[warp];
+    const unsigned int key = ukeys[sg];
     const int lo = (int)(key / (unsigned int)n), hi = (int)(key - (unsigned int)lo * (unsigned int)n);
     const bool diag = lo == hi;
-    // Z(P hi + p, P lo + q) -= out(p, q); diagonal blocks: lower part only
+    // single chunk: Z(P hi + p, P lo + q) -= out(p, q) (diagonal blocks: lower
+    // part only); else the chunk's partial block, combined by k_pair_combine
+    double* pp = part + (size_t)warp * 81;
     auto put = [&](int p, int q, double v) {
+        if (nch > 1) { pp[P * p + q] = v; return; }
         if (diag && p < q) return;
         double* z = Z + ((size_t)P * lo + q) * ld + (size_t)P * hi + p;
         *z = *z - v;
@@ -486,6 +513,27 @@ __global__ void __launch_bounds__(256) k_pair_reduce_mma(const unsigned int* uke
         }
         if (k == 0) put(r, 8, c[NT > 2 ? 2 : 0][0]);      // tile (0, 8): column 8
         if (lane == 0) put(8, 8, c[NT > 3 ? 3 : 0][0]);   // tile (8, 8)
+    }
+}
+
+// Multi-chunk segments: partial blocks summed in chunk order, then written.
+template <int P>
+__global__ void __launch_bounds__(256) k_pair_combine(const unsigned int* ukeys, int nseg, const int* chunk_off,
+                                                      const double* part, int n, double* Z, long long ld) {
+    const int sg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (sg >= nseg) return;
+    const int c0 = chunk_off[sg], c1 = chunk_off[sg + 1];
+    if (c1 - c0 < 2) return;
+    const unsigned int key = ukeys[sg];
+    const int lo = (int)(key / (unsigned int)n), hi = (int)(key - (unsigned int)lo * (unsigned int)n);
+    for (int en = lane; en < P * P; en += 32) {
+        const int p = en / P, q = en - P * (en / P);
+        if (lo == hi && p < q) continue;
+        double v = 0.0;
+        for (int c = c0; c < c1; ++c) v += part[(size_t)c * 81 + en];
+        double* z = Z + ((size_t)P * lo + q) * ld + (size_t)P * hi + p;
+        *z = *z - v;
     }
 }
 
@@ -528,6 +576,22 @@ void launch_fill(int P, double* Z, long long ld, int N, int Npad, const double* 
     if (P == 8) k_fill<8><<<(unsigned)tiles, 256, 0, s>>>(Z, ld, N, Npad, D, s_a, G, add_gg);
     else k_fill<9><<<(unsigned)tiles, 256, 0, s>>>(Z, ld, N, Npad, D, s_a, G, add_gg);
     SFM_LAUNCH_CHECK();
+}
+
+// Pairs per work item of the pair reduction (SFMCOV_PAIR_CHUNK, default 128).
+static int pair_chunk() {
+    static int c = [] {
+        const char* e = std::getenv("SFMCOV_PAIR_CHUNK");
+        const int v = e ? std::atoi(e) : 128;
+        return (v >= 4 && v <= (1 << 20)) ? v : 128;
+    }();
+    return c;
+}
+
+__global__ void k_chunk_count(const int* counts, int nseg, int chunk, int* ccnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nseg) ccnt[i] = (counts[i] + chunk - 1) / chunk;
+    else if (i == nseg) ccnt[i] = 0;
 }
 
 static int bits_for64(unsigned long long v) { int b = 1; while (b < 64 && (1ULL << b) <= v) ++b; return b; }
@@ -582,6 +646,22 @@ void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace&
     SFM_CUDA(cudaMemsetAsync(counts + nseg, 0, sizeof(int), s));
     SFM_CUDA(cub::DeviceScan::ExclusiveSum(ws.get_tmp(eb), eb, counts, seg_off, nseg + 1, s));
     pd.seg_off = seg_off;
+    // split segments into chunks of at most pair_chunk() pairs (load balance:
+    // diagonal blocks carry ~10x the pairs of an off-diagonal one)
+    pd.chunk = pair_chunk();
+    int* ccnt = (int*)pd.buf_chunk.get(8 * ((size_t)nseg + 1) + 16);
+    int* coff = ccnt + (nseg + 1);
+    k_chunk_count<<<cdiv(nseg + 1, 256), 256, 0, s>>>(counts, nseg, pd.chunk, ccnt);
+    SFM_LAUNCH_CHECK();
+    size_t cb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, cb, ccnt, coff, nseg + 1, s);
+    SFM_CUDA(cub::DeviceScan::ExclusiveSum(ws.get_tmp(cb), cb, ccnt, coff, nseg + 1, s));
+    int nch = 0;
+    SFM_CUDA(cudaMemcpyAsync(&nch, coff + nseg, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SFM_CUDA(cudaStreamSynchronize(s));
+    pd.chunk_off = coff;
+    pd.nchunks = nch;
+    pd.part = (double*)pd.buf_part.get(8 * 81 * ((size_t)nch + 1));
 }
 
 void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, cudaStream_t s) {
@@ -592,8 +672,18 @@ void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, doubl
         if (P == 8) k_pair_reduce<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
         else k_pair_reduce<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
     } else {
-        if (P == 8) k_pair_reduce_mma<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
-        else k_pair_reduce_mma<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
+        const unsigned cblocks = cdiv(pd.nchunks, 8);
+        // 4 pairs gathered ahead, 4 CTAs (32 warps) per SM: the kernel is
+        // bound by gather latency, so occupancy beats deeper prefetch
+        if (P == 8)
+            k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, pd.nchunks,
+                                                                pd.chunk, pd.vals, Wb, n, Z, ld, pd.part);
+        else
+            k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, pd.nchunks,
+                                                                pd.chunk, pd.vals, Wb, n, Z, ld, pd.part);
+        SFM_LAUNCH_CHECK();
+        if (P == 8) k_pair_combine<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld);
+        else k_pair_combine<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld);
     }
     SFM_LAUNCH_CHECK();
 }

@@ -156,6 +156,38 @@ int32_t sfmcov_cuda_spd_inverse_blocks(sfmcov_handle* h, const double* a, int64_
                                        double* blocks, double* min_pivot, double* max_pivot,
                                        sfmcov_error* err);
 
+/* ---- multi-GPU (one process per GPU) --------------------------------------
+ * The same pipeline with the Schur pair work and the dense inversion split
+ * over ranks: chunks of the camera-pair-sorted observation-pair list per
+ * rank + an NCCL all-reduce of the camera-pair blocks, and a 1D
+ * block-cyclic fused Cholesky / triangular-inverse sweep (panel broadcast
+ * over NVLink).  Every rank passes the same host scene and receives every
+ * camera block.  Replaces compute_covariance (covariance.hpp:110-111) for
+ * multi-GPU callers; NCCL is loaded at run time (libnccl.so.2). */
+/* 128-byte NCCL unique id, created on rank 0 and sent to the others by the caller. */
+int32_t sfmcov_nccl_unique_id(char* id128, sfmcov_error* err);
+/* Attach the handle to rank `rank` of `nranks` (nranks = 1: no communicator). */
+int32_t sfmcov_cuda_comm_init(sfmcov_handle* h, const char* id128, int32_t nranks, int32_t rank,
+                              sfmcov_error* err);
+int32_t sfmcov_cuda_compute_covariance_sharded(sfmcov_handle* h, const sfmcov_scene* scene,
+                                               const sfmcov_options* opts, double* cam_cov,
+                                               sfmcov_diagnostics* diag, sfmcov_error* err);
+/* Same with every scene pointer and d_cam_cov in device memory. */
+int32_t sfmcov_cuda_compute_covariance_sharded_device(sfmcov_handle* h, const sfmcov_scene* d_scene,
+                                                      const sfmcov_options* opts, double* d_cam_cov,
+                                                      sfmcov_diagnostics* diag, sfmcov_error* err);
+/* The distributed code path with `ranks` ranks emulated on this one device
+ * (in-process copies instead of NCCL); for testing the multi-GPU path. */
+int32_t sfmcov_cuda_compute_covariance_emulated(sfmcov_handle* h, const sfmcov_scene* scene,
+                                                const sfmcov_options* opts, int32_t ranks, double* cam_cov,
+                                                sfmcov_diagnostics* diag, sfmcov_error* err);
+/* Host-only partition plans (no GPU needed): padded dimension of the
+ * camera-aligned layout, the rank's local column count and which cameras'
+ * blocks it extracts; and its chunk range of the sorted pair list. */
+int32_t sfmcov_plan_dense(int32_t n_cams, int32_t cam_params, int32_t nranks, int32_t rank,
+                          int32_t panel_blocks, int64_t* npad, int64_t* local_cols, int32_t* cam_owned);
+int32_t sfmcov_plan_chunks(int64_t nchunks, int32_t nranks, int32_t rank, int64_t* begin, int64_t* end);
+
 /* Per-stage device times (ms) of the last pipeline call, in the order of
  * sfmcov_cuda_stage_name(i); returns the number of stages written. */
 int32_t sfmcov_cuda_last_stage_times(sfmcov_handle* h, double* ms, int32_t capacity);

@@ -101,6 +101,24 @@ CUDA_SYMBOLS = {
     "sfmcov_cuda_stage_name": (C.c_char_p, [C.c_int32]),
     "sfmcov_cuda_last_counts": (C.c_int32, [C.c_void_p, c_int64_p, C.c_int32]),
     "sfmcov_cuda_set_profiling": (None, [C.c_void_p, C.c_int32]),
+    "sfmcov_nccl_unique_id": (C.c_int32, [C.c_char_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_comm_init": (C.c_int32, [C.c_void_p, C.c_char_p, C.c_int32, C.c_int32, C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_compute_covariance_sharded": (
+        C.c_int32,
+        [C.c_void_p, C.POINTER(Scene), C.POINTER(Options), C.c_void_p, C.POINTER(Diagnostics), C.POINTER(ErrorStruct)],
+    ),
+    "sfmcov_cuda_compute_covariance_sharded_device": (
+        C.c_int32,
+        [C.c_void_p, C.POINTER(Scene), C.POINTER(Options), C.c_void_p, C.POINTER(Diagnostics), C.POINTER(ErrorStruct)],
+    ),
+    "sfmcov_cuda_compute_covariance_emulated": (
+        C.c_int32,
+        [C.c_void_p, C.POINTER(Scene), C.POINTER(Options), C.c_int32, C.c_void_p, C.POINTER(Diagnostics),
+         C.POINTER(ErrorStruct)],
+    ),
+    "sfmcov_plan_dense": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, c_int64_p, c_int64_p,
+                                      C.c_void_p]),
+    "sfmcov_plan_chunks": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, c_int64_p, c_int64_p]),
 }
 
 SYNTH_SYMBOLS = {

@@ -14,6 +14,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "dist.h"
 
 #include <algorithm>
 #include <cmath>
@@ -69,6 +70,13 @@ struct sfmcov_handle {
         psd, prange, status, depth, H;
     PairDev pairs;
     Status* st_host = nullptr;
+    // distributed tail: 0 = single device, 1 = emulated ranks, 2 = NCCL rank
+    int dist_mode = 0, dist_R = 1, dist_rank = 0, emu_R = 1;
+    void* nccl = nullptr;
+    std::vector<sfm::RankDense> ranks;
+    DBuf seg, seg_tmp, prange_r;
+    cudaEvent_t ev_ready = nullptr, ev_rank_done[64];
+    bool ev_rank_init = false;
     // captured dense stage (Cholesky + triangular inverse), keyed by its inputs
     cudaGraphExec_t dense_exec = nullptr;
     const void* dense_key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -305,6 +313,51 @@ int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv,
     return launches;
 }
 
+// Diagnostics of a successful pipeline call (covariance.hpp:49-60).
+void fill_diagnostics(sfmcov_handle* h, Outputs& out, const double* prange, const double* eigE, const int* psd,
+                      const double* s_a, const unsigned char* flags, size_t ncols, int N, int64_t dense_bytes) {
+    if (out.diag) {
+        sfmcov_diagnostics* d = out.diag;
+        double pr[2], ee[8];
+        int warn = 0;
+        d2h(h, pr, prange, 16);
+        d2h(h, ee, eigE, 56);
+        d2h(h, &warn, psd, 4);
+        double mn = pr[0], mx = pr[1];
+        for (int l = 0; l < 7; ++l) { mn = std::min(mn, std::fabs(ee[l])); mx = std::max(mx, std::fabs(ee[l])); }
+        d->min_pivot = mn;
+        d->max_pivot = mx;
+        d->inertia_positive = N;
+        d->inertia_negative = 7;
+        d->negative_eigenvalue_warnings = warn;
+        d->largest_dense_dim = (int64_t)N + 7;
+        d->peak_dense_bytes = dense_bytes;
+        // scale range and flagged columns
+        std::vector<double> sa(ncols);
+        std::vector<unsigned char> f(ncols);
+        d2h(h, sa.data(), s_a, 8 * ncols);
+        if (h->st_host->nflag) d2h(h, f.data(), flags, ncols);
+        d->scale_min = ncols ? *std::min_element(sa.begin(), sa.end()) : 1.0;
+        d->scale_max = ncols ? *std::max_element(sa.begin(), sa.end()) : 1.0;
+        int64_t cnt = 0;
+        if (h->st_host->nflag)
+            for (size_t c = 0; c < ncols; ++c)
+                if (f[c]) {
+                    if (d->flagged && cnt < d->flagged_capacity) d->flagged[cnt] = (int64_t)c;
+                    ++cnt;
+                }
+        d->n_flagged = (int32_t)cnt;
+        if (!(mn > 1e-12 * mx))
+            throw ApiError{SFMCOV_ERR_DEGENERATE, "factorization",
+                           "near-singular pivot (ratio " + fmt_f(mn / mx) +
+                               "); the scene is likely disconnected or its gauge degenerate"};
+    }
+}
+
+void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const double* D, const double* s_a,
+                   const double* G, const double* Wb, Status* st, const unsigned char* flags, size_t ncols,
+                   const double* eigE);
+
 // The whole device pipeline.  `sc` points at device memory.
 void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     cudaStream_t s = h->s;
@@ -436,6 +489,10 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     mark(h, 4);
     build_pairs(sc, ix, h->pairs, h->ws, s);
     mark(h, 5);
+    if (h->dist_mode && mode == M_FULL) {
+        run_dist_tail(h, sc, out, D, s_a, G, Wb, st, flags, ncols, eigE);
+        return;
+    }
     const int Npad = ((N + kNB - 1) / kNB) * kNB;
     const long long ld = Npad;
     double* Z = h->Z.as<double>((size_t)Npad * Npad);
@@ -515,42 +572,117 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
             h->stage_ms[i] = ms;
         }
     }
-    if (out.diag) {
-        sfmcov_diagnostics* d = out.diag;
-        double pr[2], ee[8];
-        int warn = 0;
-        d2h(h, pr, prange, 16);
-        d2h(h, ee, eigE, 56);
-        d2h(h, &warn, psd, 4);
-        double mn = pr[0], mx = pr[1];
-        for (int l = 0; l < 7; ++l) { mn = std::min(mn, std::fabs(ee[l])); mx = std::max(mx, std::fabs(ee[l])); }
-        d->min_pivot = mn;
-        d->max_pivot = mx;
-        d->inertia_positive = N;
-        d->inertia_negative = 7;
-        d->negative_eigenvalue_warnings = warn;
-        d->largest_dense_dim = (int64_t)N + 7;
-        d->peak_dense_bytes = (int64_t)8 * Npad * (int64_t)Npad;
-        // scale range and flagged columns
-        std::vector<double> sa(ncols);
-        std::vector<unsigned char> f(ncols);
-        d2h(h, sa.data(), s_a, 8 * ncols);
-        if (h->st_host->nflag) d2h(h, f.data(), flags, ncols);
-        d->scale_min = ncols ? *std::min_element(sa.begin(), sa.end()) : 1.0;
-        d->scale_max = ncols ? *std::max_element(sa.begin(), sa.end()) : 1.0;
-        int64_t cnt = 0;
-        if (h->st_host->nflag)
-            for (size_t c = 0; c < ncols; ++c)
-                if (f[c]) {
-                    if (d->flagged && cnt < d->flagged_capacity) d->flagged[cnt] = (int64_t)c;
-                    ++cnt;
-                }
-        d->n_flagged = (int32_t)cnt;
-        if (!(mn > 1e-12 * mx))
-            throw ApiError{SFMCOV_ERR_DEGENERATE, "factorization",
-                           "near-singular pivot (ratio " + fmt_f(mn / mx) +
-                               "); the scene is likely disconnected or its gauge degenerate"};
+    fill_diagnostics(h, out, prange, eigE, psd, s_a, flags, ncols, N, (int64_t)8 * Npad * (int64_t)Npad);
+}
+
+// Distributed tail (camera-aligned layout, 1D block-cyclic panels): the pair
+// reduction over this rank's chunk range, all-reduce of the camera-pair
+// blocks, local fill, the distributed sweep (dist.cu), local extraction and
+// the all-reduces of the outputs.  Emulated ranks (dist_mode 1) run every
+// rank of the group on this device and combine in rank order.
+void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const double* D, const double* s_a,
+                   const double* G, const double* Wb, Status* st, const unsigned char* flags, size_t ncols,
+                   const double* eigE) {
+    cudaStream_t s = h->s;
+    const int n = sc.n, P = sc.P, N = P * n;
+    const ColMap cm{P, kNB / P, n};
+    const int Npad = cm_npad(cm);
+    const long long ld = Npad;
+    const int R = h->dist_mode == 1 ? h->emu_R : h->dist_R;
+    const int nloc = h->dist_mode == 1 ? R : 1;
+    if (nloc > 64) throw ApiError{SFMCOV_ERR_DIMENSION, "options", "at most 64 emulated ranks"};
+    const int Gp = panel_blocks();
+    if ((int)h->ranks.size() < nloc) h->ranks.resize(nloc);
+    if (!h->ev_rank_init) {
+        SFM_CUDA(cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming));
+        for (auto& e : h->ev_rank_done) SFM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->ev_rank_init = true;
     }
+    DistGroup grp;
+    grp.nccl = h->dist_mode == 2 ? h->nccl : nullptr;
+    std::vector<Status*> sts(nloc, st);
+    for (int i = 0; i < nloc; ++i) {
+        const int gr = h->dist_mode == 1 ? i : h->dist_rank;
+        h->ranks[i].init(h->device);
+        h->ranks[i].setup(Ownership{R, gr, Gp}, Npad, ld);
+        grp.ranks.push_back(&h->ranks[i]);
+    }
+    // ---- sharded Schur: this rank's chunks of the sorted pair list --------------
+    const PairDev& pd = h->pairs;
+    const size_t segd = (size_t)pd.nseg * 81;
+    double* seg = h->seg.as<double>(segd + 1);
+    auto chunk_range = [&](int gr, int* cb, int* ce) {
+        *cb = (int)((long long)pd.nchunks * gr / R);
+        *ce = (int)((long long)pd.nchunks * (gr + 1) / R);
+    };
+    if (h->dist_mode == 1) {
+        double* tmp = h->seg_tmp.as<double>(segd + 1);
+        for (int gr = 0; gr < R; ++gr) {
+            int cb, ce;
+            chunk_range(gr, &cb, &ce);
+            launch_pair_reduce_segments(P, pd, Wb, n, cb, ce, gr == 0 ? seg : tmp, s);
+            if (gr) launch_add(seg, tmp, segd, s);
+        }
+    } else {
+        int cb, ce;
+        chunk_range(h->dist_rank, &cb, &ce);
+        launch_pair_reduce_segments(P, pd, Wb, n, cb, ce, seg, s);
+        dist_allreduce(grp, seg, segd, 0, s);
+    }
+    mark(h, 6);
+    int* psd = h->psd.as<int>(1);
+    double* prange = h->prange.as<double>(2);
+    double* pr_r = h->prange_r.as<double>(2 * (size_t)nloc);
+    SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
+    SFM_CUDA(cudaMemsetAsync(out.d_cam_cov, 0, 8 * (size_t)P * P * n, s));
+    SFM_CUDA(cudaEventRecord(h->ev_ready, s));
+    for (int i = 0; i < nloc; ++i) {
+        RankDense& r = h->ranks[i];
+        SFM_CUDA(cudaStreamWaitEvent(r.s, h->ev_ready, 0));
+        launch_fill_local(cm, r.ow, r.zp, ld, Npad, r.ncl, D, s_a, G, r.s);
+        launch_seg_scatter(cm, r.ow, seg, pd.ukeys, pd.nseg, r.zp, ld, r.s);
+    }
+    mark(h, 7);
+    dist_sweep(grp, sts.data());
+    for (int i = 0; i < nloc; ++i) {
+        RankDense& r = h->ranks[i];
+        launch_extract_local(cm, r.ow, r.zp, ld, Npad, s_a, out.d_cam_cov, st, psd, r.s);
+        launch_pivot_range_local(cm, r.ow, r.pv, Npad, pr_r + 2 * i, r.s);
+        SFM_CUDA(cudaEventRecord(h->ev_rank_done[i], r.s));
+        SFM_CUDA(cudaStreamWaitEvent(s, h->ev_rank_done[i], 0));
+    }
+    mark(h, 8);
+    mark(h, 9);
+    launch_range_combine(prange, pr_r, nloc, s);
+    if (grp.nccl) {
+        dist_allreduce(grp, out.d_cam_cov, (size_t)P * P * n, 0, s);
+        dist_allreduce(grp, prange, 1, 1, s);
+        dist_allreduce(grp, prange + 1, 1, 2, s);
+        dist_allreduce_int_sum(grp, psd, s);
+        dist_allreduce_int_min(grp, &st->chol_bad, s);
+    }
+    mark(h, 10);
+    h->counts[0] = pd.npairs;
+    h->counts[1] = pd.nseg;
+    h->counts[2] = N;
+    h->counts[3] = Npad;
+    h->counts[4] = sc.t;
+    h->counts[5] = sc.m;
+    h->counts[6] = n;
+    h->counts[7] = P;
+    h->counts[8] = g_kernel_launches;
+    sync_status(h);
+    throw_numeric(h, sc, M_FULL);
+    if (h->profiling) {
+        for (int i = 0; i < ST_COUNT; ++i) {
+            float ms = 0.f;
+            SFM_CUDA(cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]));
+            h->stage_ms[i] = ms;
+        }
+    }
+    int64_t local_bytes = 0;
+    for (int i = 0; i < nloc; ++i) local_bytes = std::max<int64_t>(local_bytes, (int64_t)8 * ld * h->ranks[i].ncl);
+    fill_diagnostics(h, out, prange, eigE, psd, s_a, flags, ncols, N, local_bytes);
 }
 
 // Copies a host scene into the handle's staging buffers.
@@ -667,6 +799,15 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
                     &h->cov, &h->psd, &h->prange, &h->status, &h->depth, &h->H};
     for (DBuf* b : bufs) b->release();
     h->pairs.release();
+    for (auto& r : h->ranks) r.release();
+    h->seg.release();
+    h->seg_tmp.release();
+    h->prange_r.release();
+    if (h->ev_rank_init) {
+        cudaEventDestroy(h->ev_ready);
+        for (auto& e : h->ev_rank_done) cudaEventDestroy(e);
+    }
+    if (h->nccl) sfm::nccl_comm_destroy(h->nccl);
     if (h->dense_exec) cudaGraphExecDestroy(h->dense_exec);
     if (h->st_host) cudaFreeHost(h->st_host);
     cudaEventDestroy(h->e1);
@@ -714,6 +855,119 @@ int32_t sfmcov_cuda_compute_covariance_device(sfmcov_handle* h, const sfmcov_sce
         run(h, as_device(d_scene), M_FULL, out);
         SFM_CUDA(cudaStreamSynchronize(h->s));
     });
+}
+
+// ---- distributed entry points -------------------------------------------------
+namespace {
+// Runs the host pipeline with the distributed tail configured by (mode, R).
+void run_dist_host(sfmcov_handle* h, const sfmcov_scene* scene, const sfmcov_options* opts, double* cam_cov,
+                   sfmcov_diagnostics* diag, int mode, int R) {
+    check_options(opts);
+    struct Restore {
+        sfmcov_handle* h;
+        ~Restore() { h->dist_mode = 0; }
+    } restore{h};
+    h->dist_mode = mode;
+    if (mode == 1) h->emu_R = R;
+    const SceneDev sc = upload(h, scene);
+    const int P = sc.P;
+    double* dcov = h->cov.as<double>((size_t)P * P * sc.n);
+    Outputs out;
+    out.d_cam_cov = dcov;
+    out.diag = diag;
+    run(h, sc, M_FULL, out);
+    if (sc.n) SFM_CUDA(cudaMemcpyAsync(cam_cov, dcov, 8 * (size_t)P * P * sc.n, cudaMemcpyDeviceToHost, h->s));
+    SFM_CUDA(cudaStreamSynchronize(h->s));
+}
+}  // namespace
+
+int32_t sfmcov_cuda_compute_covariance_emulated(sfmcov_handle* h, const sfmcov_scene* scene, const sfmcov_options* opts,
+                                                int32_t ranks, double* cam_cov, sfmcov_diagnostics* diag,
+                                                sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        if (ranks < 1 || ranks > 64) throw ApiError{SFMCOV_ERR_DIMENSION, "options", "ranks must be in [1, 64]"};
+        run_dist_host(h, scene, opts, cam_cov, diag, 1, ranks);
+    });
+}
+
+int32_t sfmcov_nccl_unique_id(char* id128, sfmcov_error* err) {
+    try {
+        sfm::nccl_unique_id(id128);
+        clear_error(err);
+        return SFMCOV_OK;
+    } catch (const std::exception& x) {
+        fill_error(err, ApiError{SFMCOV_ERR_DEVICE, "comm", x.what()});
+        return SFMCOV_ERR_DEVICE;
+    }
+}
+
+int32_t sfmcov_cuda_comm_init(sfmcov_handle* h, const char* id128, int32_t nranks, int32_t rank, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks)
+            throw ApiError{SFMCOV_ERR_DIMENSION, "comm", "rank must be in [0, nranks)"};
+        if (h->nccl) sfm::nccl_comm_destroy(h->nccl);
+        h->nccl = nullptr;
+        h->dist_R = nranks;
+        h->dist_rank = rank;
+        if (nranks > 1) {
+            try {
+                h->nccl = sfm::nccl_comm_init(id128, nranks, rank);
+            } catch (const std::exception& x) {
+                throw ApiError{SFMCOV_ERR_DEVICE, "comm", x.what()};
+            }
+        }
+    });
+}
+
+int32_t sfmcov_cuda_compute_covariance_sharded(sfmcov_handle* h, const sfmcov_scene* scene, const sfmcov_options* opts,
+                                               double* cam_cov, sfmcov_diagnostics* diag, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        if (h->dist_R > 1 && !h->nccl) throw ApiError{SFMCOV_ERR_DEVICE, "comm", "sfmcov_cuda_comm_init was not called"};
+        if (h->dist_R <= 1) run_dist_host(h, scene, opts, cam_cov, diag, 1, 1);
+        else run_dist_host(h, scene, opts, cam_cov, diag, 2, h->dist_R);
+    });
+}
+
+int32_t sfmcov_cuda_compute_covariance_sharded_device(sfmcov_handle* h, const sfmcov_scene* d_scene,
+                                                      const sfmcov_options* opts, double* d_cam_cov,
+                                                      sfmcov_diagnostics* diag, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        if (h->dist_R > 1 && !h->nccl) throw ApiError{SFMCOV_ERR_DEVICE, "comm", "sfmcov_cuda_comm_init was not called"};
+        check_options(opts);
+        struct Restore {
+            sfmcov_handle* h;
+            ~Restore() { h->dist_mode = 0; }
+        } restore{h};
+        h->dist_mode = h->dist_R > 1 ? 2 : 1;
+        if (h->dist_mode == 1) h->emu_R = 1;
+        Outputs out;
+        out.d_cam_cov = d_cam_cov;
+        out.diag = diag;
+        run(h, as_device(d_scene), M_FULL, out);
+        SFM_CUDA(cudaStreamSynchronize(h->s));
+    });
+}
+
+int32_t sfmcov_plan_dense(int32_t n_cams, int32_t cam_params, int32_t nranks, int32_t rank, int32_t panel_blocks,
+                          int64_t* npad, int64_t* local_cols, int32_t* cam_owned) {
+    if (n_cams < 0 || (cam_params != 8 && cam_params != 9) || nranks < 1 || rank < 0 || rank >= nranks ||
+        panel_blocks < 1)
+        return SFMCOV_ERR_DIMENSION;
+    const sfm::ColMap cm{cam_params, sfm::kNB / cam_params, n_cams};
+    const sfm::Ownership ow{nranks, rank, panel_blocks};
+    const int Np = sfm::cm_npad(cm);
+    if (npad) *npad = Np;
+    if (local_cols) *local_cols = (int64_t)sfm::own_blocks(ow, Np / sfm::kNB) * sfm::kNB;
+    if (cam_owned)
+        for (int i = 0; i < n_cams; ++i) cam_owned[i] = sfm::own_lcol(ow, sfm::cm_col(cm, i, 0)) >= 0 ? 1 : 0;
+    return SFMCOV_OK;
+}
+
+int32_t sfmcov_plan_chunks(int64_t nchunks, int32_t nranks, int32_t rank, int64_t* begin, int64_t* end) {
+    if (nchunks < 0 || nranks < 1 || rank < 0 || rank >= nranks) return SFMCOV_ERR_DIMENSION;
+    *begin = nchunks * rank / nranks;
+    *end = nchunks * (rank + 1) / nranks;
+    return SFMCOV_OK;
 }
 
 int32_t sfmcov_cuda_observation_index(sfmcov_handle* h, const sfmcov_scene* scene, int64_t* off_cam, int32_t* idx_cam,

@@ -84,9 +84,22 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
         tj = (int)(l / g.tm);
     }
     if (g.lower_only && ti + g.row_off_tiles < tj + g.col_off_tiles) return;
-    const double* A = g.A + (size_t)ti * BM;
-    const double* B = BK_MAJOR ? g.B + (size_t)tj * BN * g.ldb : g.B + (size_t)tj * BN;
-    double* C = g.C + (size_t)tj * BN * g.ldc + (size_t)ti * BM;
+    const double* A;
+    const double* B;
+    double* C;
+    if (g.cyc_R > 0) {
+        const int lt = tj + g.cyc_lt0;
+        const int gt = ((lt / g.cyc_G) * g.cyc_R + g.cyc_rank) * g.cyc_G + lt % g.cyc_G;
+        const int gi = ti + g.cyc_row0;
+        if (gi < gt) return;
+        A = g.A + (size_t)(gi - g.cyc_ab0) * BM;
+        B = g.B + (size_t)(gt - g.cyc_ab0) * BN;  // (B row-indexed, not K-major)
+        C = g.C + (size_t)lt * BN * g.ldc + (size_t)gi * BM;
+    } else {
+        A = g.A + (size_t)ti * BM;
+        B = BK_MAJOR ? g.B + (size_t)tj * BN * g.ldb : g.B + (size_t)tj * BN;
+        C = g.C + (size_t)tj * BN * g.ldc + (size_t)ti * BM;
+    }
     const int wm = warp & 3, wn = warp >> 2;  // 4 x 4 warps of 32 x 32
     const int beta = (g.beta && !(g.beta0_from >= 0 && tj >= g.beta0_from)) ? 1 : 0;
 
@@ -130,22 +143,21 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
 
     double acc[4][4][2];
     const int rq = 2 * (lane & 3), cq = lane >> 2;
+    // The product accumulates from zero and is applied to C once in the
+    // epilogue (C -/+ AB^T): one rounding against C instead of one per
+    // k-step, which keeps the Cholesky's Schur-complement updates as accurate
+    // as a dot-product (left-looking) formulation.  C is prefetched to L2 now.
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) {
-            if (beta) {
-                const double2 c = __ldcg(reinterpret_cast<const double2*>(C + (size_t)(wn * 32 + ni * 8 + cq) * g.ldc + wm * 32 + mi * 8 + rq));
-                acc[mi][ni][0] = c.x;
-                acc[mi][ni][1] = c.y;
-            } else {
-                acc[mi][ni][0] = 0.0;
-                acc[mi][ni][1] = 0.0;
-            }
+            acc[mi][ni][0] = 0.0;
+            acc[mi][ni][1] = 0.0;
+#ifndef SFM_NO_C_PREFETCH
+            if (beta && (mi & 1) == 0 && (lane & 3) == 0)  // one lane per 128-byte line
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(C + (size_t)(wn * 32 + ni * 8 + cq) * g.ldc + wm * 32 + mi * 8));
+#endif
         }
-    // alpha = -1: flip the sign bit of the A fragments on the integer pipe
-    // (a DMUL would share the FP64 pipe with DMMA).
-    const unsigned neg_hi = g.alpha_neg ? 0x80000000u : 0u;
 
 #pragma unroll 1
     for (int kc = 0; kc < NK; ++kc) {
@@ -161,8 +173,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
             double af[4], bf[4];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi) {
-                const double v = as[krow * LDS + wm * 32 + mi * 8 + cq];
-                af[mi] = __hiloint2double(__double2hiint(v) ^ (int)neg_hi, __double2loint(v));
+                af[mi] = as[krow * LDS + wm * 32 + mi * 8 + cq];
             }
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni)
@@ -173,15 +184,37 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
                 for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], bf[ni], af[mi]);
         }
     }
+    // epilogue in two halves; each half issues all its C loads before any
+    // store (stores to C could alias them, so the compiler would otherwise
+    // serialise load -> store pairs)
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int h = 0; h < 2; ++h) {
+        double2 cv[2][4];
+        if (beta) {
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-            double2 c;
-            c.x = acc[mi][ni][0];
-            c.y = acc[mi][ni][1];
-            *reinterpret_cast<double2*>(C + (size_t)(wn * 32 + ni * 8 + cq) * g.ldc + wm * 32 + mi * 8 + rq) = c;
+            for (int m2 = 0; m2 < 2; ++m2)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni)
+                    cv[m2][ni] = __ldcg(reinterpret_cast<const double2*>(C + (size_t)(wn * 32 + ni * 8 + cq) * g.ldc +
+                                                                         wm * 32 + (2 * h + m2) * 8 + rq));
         }
+#pragma unroll
+        for (int m2 = 0; m2 < 2; ++m2)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                const int mi = 2 * h + m2;
+                double2 c;
+                if (beta) {
+                    c = cv[m2][ni];
+                    if (g.alpha_neg) { c.x -= acc[mi][ni][0]; c.y -= acc[mi][ni][1]; }
+                    else { c.x += acc[mi][ni][0]; c.y += acc[mi][ni][1]; }
+                } else {
+                    c.x = g.alpha_neg ? -acc[mi][ni][0] : acc[mi][ni][0];
+                    c.y = g.alpha_neg ? -acc[mi][ni][1] : acc[mi][ni][1];
+                }
+                *reinterpret_cast<double2*>(C + (size_t)(wn * 32 + ni * 8 + cq) * g.ldc + wm * 32 + mi * 8 + rq) = c;
+            }
+    }
 }
 
 // Kernel configuration (SFMCOV_GEMM_CFG, default 2): 0 = BK 16 x 3 stages,
@@ -287,6 +320,9 @@ constexpr int SMEM = (kNB * LDT + NSB * 64 + NWARPS * 64 + 2 * kNB) * 8;
 // 1/sqrt(d) for d > 0: MUFU.RSQ64H seed + 3 Newton steps (full double
 // precision without the libdevice call on the per-column critical path).
 __device__ __forceinline__ double fast_rsqrt(double d) {
+#ifdef SFM_EXACT_RSQRT
+    return 1.0 / sqrt(d);
+#endif
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
     const double hd = 0.5 * d;
@@ -390,10 +426,10 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
             for (int c = 0; c < SB; ++c) x[c] = T[(c0 + c) * LDT + r];
 #pragma unroll
             for (int c = 0; c < SB; ++c) {
-                double v = x[c];
+                double sum = 0.0;  // dot product first, one subtraction (see k_gemm)
 #pragma unroll
-                for (int k = 0; k < c; ++k) v -= x[k] * T[(c0 + k) * LDT + c0 + c];
-                x[c] = v * rinv[c0 + c];
+                for (int k = 0; k < c; ++k) sum += x[k] * T[(c0 + k) * LDT + c0 + c];
+                x[c] = (x[c] - sum) * rinv[c0 + c];
             }
 #pragma unroll
             for (int c = 0; c < SB; ++c) T[(c0 + c) * LDT + r] = x[c];
@@ -408,15 +444,14 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
         const int c1 = c0 + SB;
         if (warp == 0) {
             double* cp = T + (c1 + 2 * fk) * LDT + c1 + fr;
-            double d0 = cp[0], d1 = cp[LDT];
+            double d0 = 0.0, d1 = 0.0;  // product from zero, applied once (see k_gemm)
 #pragma unroll
             for (int kk = 0; kk < SB; kk += 4) {
                 const double tv = T[(c0 + kk + fk) * LDT + c1 + fr];
-                const double av = __hiloint2double(__double2hiint(tv) ^ (int)0x80000000u, __double2loint(tv));
-                dmma8(d0, d1, av, tv);
+                dmma8(d0, d1, tv, tv);
             }
-            cp[0] = d0;
-            cp[LDT] = d1;
+            cp[0] -= d0;
+            cp[LDT] -= d1;
             warp_potrf8(T, c1, rinv, spiv);
         } else {
             for (int t0 = 1 + 4 * (warp - 1); t0 < ntiles; t0 += 4 * (NWARPS - 1)) {
@@ -433,15 +468,14 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
                     r0v[u] = c1 + SB * ti;
                     q0v[u] = c1 + SB * tj;
                     cp[u] = T + (q0v[u] + 2 * fk) * LDT + r0v[u] + fr;
-                    d[u][0] = cp[u][0];
-                    d[u][1] = cp[u][LDT];
+                    d[u][0] = 0.0;
+                    d[u][1] = 0.0;
                 }
 #pragma unroll
                 for (int kk = 0; kk < SB; kk += 4) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const double tv = T[(c0 + kk + fk) * LDT + r0v[u] + fr];
-                        const double av = __hiloint2double(__double2hiint(tv) ^ (int)0x80000000u, __double2loint(tv));
+                        const double av = T[(c0 + kk + fk) * LDT + r0v[u] + fr];
                         const double bv = T[(c0 + kk + fk) * LDT + q0v[u] + fr];
                         dmma8(d[u][0], d[u][1], av, bv);
                     }
@@ -449,8 +483,8 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
                     if (t0 + u < ntiles) {
-                        cp[u][0] = d[u][0];
-                        cp[u][LDT] = d[u][1];
+                        cp[u][0] -= d[u][0];
+                        cp[u][LDT] -= d[u][1];
                     }
             }
         }
@@ -692,7 +726,27 @@ static bool debug_sync() {
     return v;
 }
 
-static GemmArgs gemm_args(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb,
+// Experimental (SFMCOV_TRSM_SUBST=1): L21 = A21 L11^-T by plain forward
+// substitution, one thread per row (accuracy reference for the inverse-based
+// GEMM trsm).
+__global__ void k_trsm_subst(double* A, long long ld, int rows, const double* L) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    double x[kNB];
+    for (int j = 0; j < kNB; ++j) {
+        double v = A[(size_t)j * ld + r];
+        for (int k = 0; k < j; ++k) v -= x[k] * L[(size_t)k * ld + j];
+        x[j] = v / L[(size_t)j * ld + j];
+    }
+    for (int j = 0; j < kNB; ++j) A[(size_t)j * ld + r] = x[j];
+}
+
+static bool trsm_subst() {
+    static bool v = [] { const char* e = std::getenv("SFMCOV_TRSM_SUBST"); return e && e[0] == '1'; }();
+    return v;
+}
+
+GemmArgs gemm_args(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb,
                           int tm, int tn, int K) {
     GemmArgs g{};
     g.C = C; g.ldc = ldc; g.A = A; g.lda = lda; g.B = B; g.ldb = ldb;
@@ -906,8 +960,12 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             ++launches;
             const int below = K - c - 1;
             if (below == 0) break;
-            GemmArgs t = gemm_args(Acc + kNB, ld, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
-            launch_gemm(t, s);
+            if (trsm_subst()) {
+                k_trsm_subst<<<cdiv(below * kNB, 128), 128, 0, s>>>(Acc + kNB, ld, below * kNB, Acc);
+            } else {
+                GemmArgs t = gemm_args(Acc + kNB, ld, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
+                launch_gemm(t, s);
+            }
             ++launches;
             const int inner = b0 + g_here - c - 1;
             if (inner > 0) {

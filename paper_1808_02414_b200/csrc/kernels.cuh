@@ -96,6 +96,13 @@ struct GemmArgs {
     int b_kmajor;    // B stored K-contiguous
     int lower_only;  // skip tiles strictly above the matrix diagonal
     int row_off_tiles, col_off_tiles;  // C tile offsets relative to the diagonal
+    // Column-cyclic mode (cyc_R > 0, distributed sweep): C holds the local
+    // columns of a rank owning panels rank, rank + R, ... of cyc_G tiles.
+    // Grid tile (ti, tj) -> local column tile lt = tj + cyc_lt0, global
+    // column tile gt of lt, global row tile gi = ti + cyc_row0; tiles with
+    // gi < gt are skipped.  A rows / B rows are global tiles gi / gt,
+    // relative to the panel buffer's first tile cyc_ab0.
+    int cyc_R, cyc_rank, cyc_G, cyc_lt0, cyc_row0, cyc_ab0;
 };
 
 // stage_a.cu
@@ -130,6 +137,8 @@ void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, doubl
 // dense.cu
 void dense_init_attributes();
 void launch_gemm(const GemmArgs& g, cudaStream_t s);
+GemmArgs gemm_args(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb, int tm,
+                   int tn, int K);
 void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s);
 void launch_copy_diag(double* X, long long ld, int k, const double* Linv, cudaStream_t s);
 void launch_copy_panel(const double* X, long long ld, int k, int rows, double* Lp, cudaStream_t s);
@@ -148,5 +157,70 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
                 cudaEvent_t eR);
 inline size_t sweep_ring_doubles(int Npad, int G, int NB) { return (size_t)NB * Npad * G * kNB; }
 inline size_t trtri_lp_doubles(int Npad, int G) { return (size_t)Npad * kNB * G + (size_t)kNB * kNB * G; }
+
+// ---- column layouts and panel ownership (distributed path, dist.cu) ---------
+// Camera-aligned layout (cpb > 0): cpb = floor(kNB / P) cameras per 128-block,
+// the block's tail columns are identity padding, so no camera straddles a
+// block (or a panel).  cpb = 0: natural layout, column = P cam + j.
+struct ColMap {
+    int P, cpb, n;
+};
+__host__ __device__ inline int cm_col(const ColMap& m, int cam, int j) {
+    return m.cpb ? (cam / m.cpb) * kNB + (cam % m.cpb) * m.P + j : m.P * cam + j;
+}
+// layout column -> natural parameter index, or -1 for padding
+__host__ __device__ inline int cm_nat(const ColMap& m, int col) {
+    if (!m.cpb) return col < m.P * m.n ? col : -1;
+    const int blk = col / kNB, w = col - blk * kNB;
+    if (w >= m.cpb * m.P) return -1;
+    const int cam = blk * m.cpb + w / m.P;
+    return cam < m.n ? cam * m.P + (w - (w / m.P) * m.P) : -1;
+}
+inline int cm_npad(const ColMap& m) {
+    return m.cpb ? ((m.n + m.cpb - 1) / m.cpb) * kNB : ((m.P * m.n + kNB - 1) / kNB) * kNB;
+}
+// 1D block-cyclic panels: panel q = 128-blocks [qG, qG + G), owner q % R;
+// a rank stores its panels' columns contiguously (all Npad rows).
+struct Ownership {
+    int R, rank, G;
+};
+__host__ __device__ inline int own_lcol(const Ownership& o, int gcol) {
+    const int blk = gcol / kNB, pan = blk / o.G;
+    if (pan % o.R != o.rank) return -1;
+    return ((pan / o.R) * o.G + (blk - pan * o.G)) * kNB + (gcol - blk * kNB);
+}
+__host__ __device__ inline int own_gcol(const Ownership& o, int lcol) {
+    const int lblk = lcol / kNB, lpan = lblk / o.G;
+    const int pan = lpan * o.R + o.rank;
+    return (pan * o.G + (lblk - lpan * o.G)) * kNB + (lcol - lblk * kNB);
+}
+// number of local 128-blocks of a rank for K global blocks
+inline int own_blocks(const Ownership& o, int K) {
+    int b = 0;
+    for (int q = o.rank; q * o.G < K; q += o.R) b += (K - q * o.G < o.G) ? K - q * o.G : o.G;
+    return b;
+}
+// local blocks of the rank's panels with index <= q
+inline int own_blocks_upto(const Ownership& o, int K, int q) {
+    int b = 0;
+    for (int p = o.rank; p <= q && p * o.G < K; p += o.R) b += (K - p * o.G < o.G) ? K - p * o.G : o.G;
+    return b;
+}
+
+// dist.cu kernels
+void launch_fill_local(const ColMap& cm, const Ownership& ow, double* Zl, long long ld, int Npad, int ncl,
+                       const double* D, const double* s_a, const double* G, cudaStream_t s);
+void launch_seg_scatter(const ColMap& cm, const Ownership& ow, const double* seg, const unsigned int* ukeys, int nseg,
+                        double* Zl, long long ld, cudaStream_t s);
+void launch_extract_local(const ColMap& cm, const Ownership& ow, const double* Zl, long long ld, int Npad,
+                          const double* s_a, double* cov, Status* st, int* psd_warn, cudaStream_t s);
+void launch_pivot_range_local(const ColMap& cm, const Ownership& ow, const double* piv, int Npad, double* out,
+                              cudaStream_t s);
+void launch_panel_take_at(double* Zc, long long ld, int row0, int W, int rows, double* Lb, cudaStream_t s);
+void launch_add(double* y, const double* x, size_t count, cudaStream_t s);
+void launch_range_combine(double* out, const double* in, int nranks, cudaStream_t s);
+// pair reduction restricted to chunks [c_begin, c_end) into per-segment blocks
+void launch_pair_reduce_segments(int P, const PairDev& pd, const double* Wb, int n, int c_begin, int c_end,
+                                 double* seg_out, cudaStream_t s);
 
 }  // namespace sfm

@@ -439,10 +439,11 @@ template <int P, int U, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned int* ukeys, const long long* seg_off, int nseg,
                                                          const int* chunk_off, int nchunks, int chunk,
                                                          const unsigned long long* vals, const double* Wb, int n,
-                                                         double* Z, long long ld, double* part) {
+                                                         double* Z, long long ld, double* part, int cfirst,
+                                                         int always_part) {
     constexpr int NT = (P == 9) ? 4 : 1;  // 8x8 tiles: (0,0) [, (8,0), (0,8), (8,8)]
     // U: pairs gathered ahead
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int warp = cfirst + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (warp >= nchunks) return;
     // segment of this chunk: largest sg with chunk_off[sg] <= warp
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned in
     // part only); else the chunk's partial block, combined by k_pair_combine
     double* pp = part + (size_t)warp * 81;
     auto put = [&](int p, int q, double v) {
-        if (nch > 1) { pp[P * p + q] = v; return; }
+        if (nch > 1 || always_part) { pp[P * p + q] = v; return; }
         if (diag && p < q) return;
         double* z = Z + ((size_t)P * lo + q) * ld + (size_t)P * hi + p;
         *z = *z - v;
@@ -534,6 +535,22 @@ __global__ void __launch_bounds__(256) k_pair_combine(const unsigned int* ukeys,
         for (int c = c0; c < c1; ++c) v += part[(size_t)c * 81 + en];
         double* z = Z + ((size_t)P * lo + q) * ld + (size_t)P * hi + p;
         *z = *z - v;
+    }
+}
+
+// Segment blocks from the chunk partials in [c_begin, c_end) (chunk order;
+// zero for segments without such chunks).  seg_out[sg * 81 + P p + q].
+template <int P>
+__global__ void __launch_bounds__(256) k_pair_combine_seg(int nseg, const int* chunk_off, const double* part,
+                                                          int c_begin, int c_end, double* seg_out) {
+    const int sg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (sg >= nseg) return;
+    const int c0 = max(chunk_off[sg], c_begin), c1 = min(chunk_off[sg + 1], c_end);
+    for (int en = lane; en < P * P; en += 32) {
+        double v = 0.0;
+        for (int c = c0; c < c1; ++c) v += part[(size_t)c * 81 + en];
+        seg_out[(size_t)sg * 81 + en] = v;
     }
 }
 
@@ -677,14 +694,33 @@ void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, doubl
         // bound by gather latency, so occupancy beats deeper prefetch
         if (P == 8)
             k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, pd.nchunks,
-                                                                pd.chunk, pd.vals, Wb, n, Z, ld, pd.part);
+                                                                pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0);
         else
             k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, pd.nchunks,
-                                                                pd.chunk, pd.vals, Wb, n, Z, ld, pd.part);
+                                                                pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0);
         SFM_LAUNCH_CHECK();
         if (P == 8) k_pair_combine<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld);
         else k_pair_combine<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld);
     }
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_pair_reduce_segments(int P, const PairDev& pd, const double* Wb, int n, int c_begin, int c_end,
+                                 double* seg_out, cudaStream_t s) {
+    if (!pd.nseg) return;
+    if (c_end > c_begin) {
+        const unsigned cblocks = cdiv(c_end - c_begin, 8);
+        if (P == 8)
+            k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, c_end,
+                                                                pd.chunk, pd.vals, Wb, n, nullptr, 0, pd.part, c_begin, 1);
+        else
+            k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, c_end,
+                                                                pd.chunk, pd.vals, Wb, n, nullptr, 0, pd.part, c_begin, 1);
+        SFM_LAUNCH_CHECK();
+    }
+    const unsigned blocks = cdiv(pd.nseg, 8);
+    if (P == 8) k_pair_combine_seg<8><<<blocks, 256, 0, s>>>(pd.nseg, pd.chunk_off, pd.part, c_begin, c_end, seg_out);
+    else k_pair_combine_seg<9><<<blocks, 256, 0, s>>>(pd.nseg, pd.chunk_off, pd.part, c_begin, c_end, seg_out);
     SFM_LAUNCH_CHECK();
 }
 

@@ -248,7 +248,7 @@ class Engine:
         return dict(zip(keys, [int(v) for v in buf]))
 
     # ---- pipeline -------------------------------------------------------------
-    def compute_covariance(self, rec: Reconstruction, options: Optional[CovarianceOptions] = None) -> CovarianceResult:
+    def _covariance_call(self, fn, rec: Reconstruction, options: Optional[CovarianceOptions], *extra):
         options = options or CovarianceOptions()
         P, n = rec.cam_params, rec.num_cameras()
         out = np.empty((n, P, P))
@@ -259,13 +259,32 @@ class Engine:
         opts = N.Options(options.threads, int(options.point_covariances), int(options.camera_cross_covariances), 0)
         err = N.ErrorStruct()
         sc = rec.c_struct()
-        code = self._lib.sfmcov_cuda_compute_covariance(self._h, C.byref(sc), C.byref(opts), out.ctypes.data,
-                                                        C.byref(diag), C.byref(err))
+        code = fn(self._h, C.byref(sc), C.byref(opts), *extra, out.ctypes.data, C.byref(diag), C.byref(err))
         _raise(code, err)
         d = CovarianceDiagnostics(diag.scale_min, diag.scale_max, [int(v) for v in flagged[:diag.n_flagged]],
                                   diag.min_pivot, diag.max_pivot, diag.inertia_positive, diag.inertia_negative,
                                   diag.negative_eigenvalue_warnings, diag.peak_dense_bytes, diag.largest_dense_dim)
         return CovarianceResult(out, d)
+
+    # ---- pipeline -------------------------------------------------------------
+    def compute_covariance(self, rec: Reconstruction, options: Optional[CovarianceOptions] = None) -> CovarianceResult:
+        return self._covariance_call(self._lib.sfmcov_cuda_compute_covariance, rec, options)
+
+    # ---- multi-GPU -------------------------------------------------------------
+    def comm_init(self, unique_id: bytes, nranks: int, rank: int):
+        """Attach this handle to rank `rank` of `nranks` (NCCL, one process per GPU)."""
+        err = N.ErrorStruct()
+        _raise(self._lib.sfmcov_cuda_comm_init(self._h, bytes(unique_id), nranks, rank, C.byref(err)), err)
+
+    def compute_covariance_sharded(self, rec: Reconstruction,
+                                   options: Optional[CovarianceOptions] = None) -> CovarianceResult:
+        """The multi-GPU pipeline (call on every rank with the same scene)."""
+        return self._covariance_call(self._lib.sfmcov_cuda_compute_covariance_sharded, rec, options)
+
+    def compute_covariance_emulated(self, rec: Reconstruction, ranks: int,
+                                    options: Optional[CovarianceOptions] = None) -> CovarianceResult:
+        """The multi-GPU code path with `ranks` ranks emulated on this device."""
+        return self._covariance_call(self._lib.sfmcov_cuda_compute_covariance_emulated, rec, options, ranks)
 
     def build_observation_index(self, rec: Reconstruction) -> ObservationIndex:
         n, m, t = rec.num_cameras(), rec.num_points(), rec.num_observations()
@@ -375,3 +394,32 @@ def schur_reduce(rec: Reconstruction) -> np.ndarray:
 
 def spd_inverse_blocks(a: np.ndarray, block: int):
     return default_engine().spd_inverse_blocks(a, block)
+
+
+# ---- multi-GPU helpers (host only) ----------------------------------------------
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (rank 0 creates it, the caller distributes it)."""
+    buf = C.create_string_buffer(128)
+    err = N.ErrorStruct()
+    _raise(N.cuda_lib().sfmcov_nccl_unique_id(buf, C.byref(err)), err)
+    return buf.raw
+
+
+def plan_dense(n_cams: int, cam_params: int, nranks: int, rank: int, panel_blocks: int = 3):
+    """(padded dimension, local column count, cameras whose blocks this rank extracts)."""
+    npad, ncols = C.c_int64(), C.c_int64()
+    owned = np.zeros(max(1, n_cams), dtype=np.int32)
+    code = N.cuda_lib().sfmcov_plan_dense(n_cams, cam_params, nranks, rank, panel_blocks, C.byref(npad),
+                                          C.byref(ncols), owned.ctypes.data)
+    if code:
+        raise Error(code, "options", "invalid plan arguments")
+    return npad.value, ncols.value, owned[:n_cams].astype(bool)
+
+
+def plan_chunks(nchunks: int, nranks: int, rank: int):
+    """Half-open chunk range [begin, end) of the sorted pair list owned by `rank`."""
+    b, e = C.c_int64(), C.c_int64()
+    code = N.cuda_lib().sfmcov_plan_chunks(nchunks, nranks, rank, C.byref(b), C.byref(e))
+    if code:
+        raise Error(code, "options", "invalid plan arguments")
+    return b.value, e.value

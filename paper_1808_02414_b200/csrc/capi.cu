@@ -639,6 +639,9 @@ void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const dou
     for (int i = 0; i < nloc; ++i) {
         RankDense& r = h->ranks[i];
         SFM_CUDA(cudaStreamWaitEvent(r.s, h->ev_ready, 0));
+        // NCCL operations of one communicator must not overlap: the panel
+        // broadcasts (stream sc) start after the block all-reduce (stream s)
+        SFM_CUDA(cudaStreamWaitEvent(r.sc, h->ev_ready, 0));
         launch_fill_local(cm, r.ow, r.zp, ld, Npad, r.ncl, D, s_a, G, r.s);
         launch_seg_scatter(cm, r.ow, seg, pd.ukeys, pd.nseg, r.zp, ld, r.s);
     }

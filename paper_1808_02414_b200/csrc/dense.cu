@@ -31,11 +31,17 @@ static inline int potrf_smem_bytes() { return potrf_smem_bytes_impl(); }
 // ----------------------------------------------------------------------------
 namespace gemm {
 constexpr int BM = 128, BN = 128, PAD = 8, LDS = BM + PAD;
-constexpr int THREADS = 512;
-template <int BK, int STAGES>
+// CTA tile 128 x (64 HN) with 8 HN warps of 32 x 32: HN = 2 is one CTA per
+// SM (512 threads), HN = 1 two CTAs per SM whose prologue / epilogue overlap
+// the other's MMAs.
+template <int BK, int STAGES, int HN>
 struct Cfg {
-    static constexpr int LDB_K = BK + 4;  // K-major B tile pitch (conflict-free fragment reads)
-    static constexpr int SMEM = STAGES * (BK * LDS + BN * LDB_K) * 8;
+    static constexpr int THREADS = 256 * HN;
+    static constexpr int BNT = 64 * HN;
+    static constexpr int LDSB = BNT + PAD;   // N-contiguous B tile pitch
+    static constexpr int LDB_K = BK + 4;     // K-major B tile pitch (conflict-free fragment reads)
+    static constexpr int BSTAGE_N = BK * LDSB, BSTAGE_K = BNT * LDB_K;
+    static constexpr int SMEM = STAGES * (BK * LDS + (BSTAGE_N > BSTAGE_K ? BSTAGE_N : BSTAGE_K)) * 8;
 };
 }  // namespace gemm
 
@@ -60,19 +66,24 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // MMA mapping: the m8n8k4 "A" operand carries B rows (n), its "B" operand
 // carries A rows (m), so each lane's two accumulators are C rows
 // m0 + 2(lane&3) + {0,1} of column n0 + (lane>>2): 16-byte C accesses.
-// 16 warps of 32x32, STAGES-deep cp.async pipeline of BK-wide K chunks.
-template <bool BK_MAJOR, int BK, int STAGES>
-__global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
+// 8 HN warps of 32x32, STAGES-deep cp.async pipeline of BK-wide K chunks; the
+// grid enumerates 128 x 128 tiles x (2 / HN) column halves.
+template <bool BK_MAJOR, int BK, int STAGES, int HN>
+__global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_gemm(GemmArgs g) {
     using namespace gemm;
-    constexpr int LDB_K = Cfg<BK, STAGES>::LDB_K;
+    using CF = Cfg<BK, STAGES, HN>;
+    constexpr int THREADS = CF::THREADS, BNT = CF::BNT, LDSB = CF::LDSB, LDB_K = CF::LDB_K;
+    constexpr int NSUB = 2 / HN;
     extern __shared__ __align__(16) double smem[];
     double* As = smem;                      // [STAGES][BK][LDS]
-    double* Bs = smem + STAGES * BK * LDS;  // [STAGES][BK][LDS] or [STAGES][BN][LDB_K]
-    constexpr int BSTAGE = BK_MAJOR ? BN * LDB_K : BK * LDS;
-    constexpr int CPT = BK / 8;             // 16-byte copies per thread per operand
+    double* Bs = smem + STAGES * BK * LDS;  // [STAGES][BK][LDSB] or [STAGES][BNT][LDB_K]
+    constexpr int BSTAGE = BK_MAJOR ? CF::BSTAGE_K : CF::BSTAGE_N;
+    constexpr int CPTA = BK / (4 * HN);     // 16-byte copies per thread: A (BK x 128), B (BK x BNT)
+    constexpr int CPTB = BK / 8;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int ti, tj;
-    const long long l = blockIdx.x;
+    const long long l = blockIdx.x / NSUB;
+    const int half = NSUB > 1 ? (int)(blockIdx.x % NSUB) : 0;
     if (g.tri) {
         int t = (int)((sqrt(8.0 * (double)l + 1.0) - 1.0) * 0.5);
         while ((long long)(t + 1) * (t + 2) / 2 <= l) ++t;
@@ -87,39 +98,45 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
     const double* A;
     const double* B;
     double* C;
+    const int coff = half * BNT;  // column offset inside the 128-wide tile
     if (g.cyc_R > 0) {
         const int lt = tj + g.cyc_lt0;
         const int gt = ((lt / g.cyc_G) * g.cyc_R + g.cyc_rank) * g.cyc_G + lt % g.cyc_G;
         const int gi = ti + g.cyc_row0;
         if (gi < gt) return;
         A = g.A + (size_t)(gi - g.cyc_ab0) * BM;
-        B = g.B + (size_t)(gt - g.cyc_ab0) * BN;  // (B row-indexed, not K-major)
-        C = g.C + (size_t)lt * BN * g.ldc + (size_t)gi * BM;
+        B = g.B + (size_t)(gt - g.cyc_ab0) * BN + coff;  // (B row-indexed, not K-major)
+        C = g.C + ((size_t)lt * BN + coff) * g.ldc + (size_t)gi * BM;
     } else {
         A = g.A + (size_t)ti * BM;
-        B = BK_MAJOR ? g.B + (size_t)tj * BN * g.ldb : g.B + (size_t)tj * BN;
-        C = g.C + (size_t)tj * BN * g.ldc + (size_t)ti * BM;
+        B = BK_MAJOR ? g.B + ((size_t)tj * BN + coff) * g.ldb : g.B + (size_t)tj * BN + coff;
+        C = g.C + ((size_t)tj * BN + coff) * g.ldc + (size_t)ti * BM;
     }
-    const int wm = warp & 3, wn = warp >> 2;  // 4 x 4 warps of 32 x 32
+    const int wm = warp & 3, wn = warp >> 2;  // 4 x (2 HN) warps of 32 x 32
     const int beta = (g.beta && !(g.beta0_from >= 0 && tj >= g.beta0_from)) ? 1 : 0;
 
     // per-thread copy sources / destinations (chunk 0); advance by BK per chunk
-    const double* asrc[CPT];
-    const double* bsrc[CPT];
-    int adst[CPT], bdst[CPT];
+    const double* asrc[CPTA];
+    const double* bsrc[CPTB];
+    int adst[CPTA], bdst[CPTB];
 #pragma unroll
-    for (int u = 0; u < CPT; ++u) {
+    for (int u = 0; u < CPTA; ++u) {
         const int idx = tid + THREADS * u;
         const int k = idx >> 6, m2 = (idx & 63) * 2;
         asrc[u] = A + (size_t)k * g.lda + m2;
         adst[u] = k * LDS + m2;
+    }
+#pragma unroll
+    for (int u = 0; u < CPTB; ++u) {
+        const int idx = tid + THREADS * u;
         if (BK_MAJOR) {
             const int n = idx / (BK / 2), k2 = (idx % (BK / 2)) * 2;
             bsrc[u] = B + (size_t)n * g.ldb + k2;
             bdst[u] = n * LDB_K + k2;
         } else {
-            bsrc[u] = B + (size_t)k * g.ldb + m2;
-            bdst[u] = k * LDS + m2;
+            const int k = idx / (BNT / 2), n2 = (idx % (BNT / 2)) * 2;
+            bsrc[u] = B + (size_t)k * g.ldb + n2;
+            bdst[u] = k * LDSB + n2;
         }
     }
     const size_t astep = (size_t)BK * g.lda;
@@ -128,10 +145,9 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
         double* as = As + st * BK * LDS;
         double* bs = Bs + st * BSTAGE;
 #pragma unroll
-        for (int u = 0; u < CPT; ++u) {
-            cp_async16(as + adst[u], asrc[u] + kc * astep);
-            cp_async16(bs + bdst[u], bsrc[u] + kc * bstep);
-        }
+        for (int u = 0; u < CPTA; ++u) cp_async16(as + adst[u], asrc[u] + kc * astep);
+#pragma unroll
+        for (int u = 0; u < CPTB; ++u) cp_async16(bs + bdst[u], bsrc[u] + kc * bstep);
     };
 
     const int NK = g.K / BK;
@@ -177,7 +193,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) k_gemm(GemmArgs g) {
             }
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni)
-                bf[ni] = BK_MAJOR ? bs[(wn * 32 + ni * 8 + cq) * LDB_K + krow] : bs[krow * LDS + wn * 32 + ni * 8 + cq];
+                bf[ni] = BK_MAJOR ? bs[(wn * 32 + ni * 8 + cq) * LDB_K + krow] : bs[krow * LDSB + wn * 32 + ni * 8 + cq];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -249,11 +265,29 @@ static void launch_prio(void (*kernel)(KArgs...), unsigned grid, unsigned block,
     SFM_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
-template <int BK, int ST>
+template <int BK, int ST, int HN>
 static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) {
-    constexpr int SMEM = gemm::Cfg<BK, ST>::SMEM;
-    if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST>, (unsigned)tiles, gemm::THREADS, SMEM, s, g);
-    else launch_prio(k_gemm<false, BK, ST>, (unsigned)tiles, gemm::THREADS, SMEM, s, g);
+    using CF = gemm::Cfg<BK, ST, HN>;
+    const unsigned grid = (unsigned)(tiles * (2 / HN));
+    if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST, HN>, grid, CF::THREADS, CF::SMEM, s, g);
+    else launch_prio(k_gemm<false, BK, ST, HN>, grid, CF::THREADS, CF::SMEM, s, g);
+}
+
+// CTA shape (SFMCOV_GEMM_HN): 1 = 128 x 64 tiles, two CTAs per SM (default);
+// 2 = 128 x 128 tiles, one CTA per SM.
+static int gemm_hn() {
+    static int v = [] {
+        const char* e = std::getenv("SFMCOV_GEMM_HN");
+        const int x = e ? std::atoi(e) : 1;
+        return (x == 1 || x == 2) ? x : 1;
+    }();
+    return v;
+}
+
+template <bool KM, int BK, int ST, int HN>
+static void set_smem() {
+    SFM_CUDA(cudaFuncSetAttribute(k_gemm<KM, BK, ST, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  gemm::Cfg<BK, ST, HN>::SMEM));
 }
 
 // Opt-in shared-memory sizes, set once before any launch (and before graph
@@ -261,12 +295,11 @@ static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) 
 void dense_init_attributes() {
     static bool done = false;
     if (done) return;
-    SFM_CUDA(cudaFuncSetAttribute(k_gemm<false, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<16, 3>::SMEM));
-    SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<16, 3>::SMEM));
-    SFM_CUDA(cudaFuncSetAttribute(k_gemm<false, 32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<32, 3>::SMEM));
-    SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, 32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<32, 3>::SMEM));
-    SFM_CUDA(cudaFuncSetAttribute(k_gemm<false, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<16, 4>::SMEM));
-    SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::Cfg<16, 4>::SMEM));
+    set_smem<false, 16, 3, 2>(); set_smem<true, 16, 3, 2>();
+    set_smem<false, 32, 3, 2>(); set_smem<true, 32, 3, 2>();
+    set_smem<false, 16, 4, 2>(); set_smem<true, 16, 4, 2>();
+    set_smem<false, 16, 4, 1>(); set_smem<true, 16, 4, 1>();
+    set_smem<false, 16, 3, 1>(); set_smem<true, 16, 3, 1>();
     SFM_CUDA(cudaFuncSetAttribute(k_potrf_diag_fwd(), cudaFuncAttributeMaxDynamicSharedMemorySize, potrf_smem_bytes()));
     done = true;
 }
@@ -274,15 +307,20 @@ void dense_init_attributes() {
 void launch_gemm(const GemmArgs& g, cudaStream_t s) {
     const long long tiles = g.tri ? (long long)g.tm * (g.tm + 1) / 2 : (long long)g.tm * g.tn;
     if (tiles <= 0) return;
-    switch (gemm_cfg()) {
-        case 1: launch_gemm_cfg<32, 3>(g, tiles, s); break;
-        case 2: launch_gemm_cfg<16, 4>(g, tiles, s); break;
-        default: launch_gemm_cfg<16, 3>(g, tiles, s); break;
+    if (gemm_hn() == 1 && !g.whole_tile) {
+        // two CTAs per SM: 3 stages measured best (config 3: 18.6 vs 19.1 ms)
+        if (gemm_cfg() == 2 && std::getenv("SFMCOV_GEMM_CFG")) launch_gemm_cfg<16, 4, 1>(g, tiles, s);
+        else launch_gemm_cfg<16, 3, 1>(g, tiles, s);
+    } else {
+        switch (gemm_cfg()) {
+            case 1: launch_gemm_cfg<32, 3, 2>(g, tiles, s); break;
+            case 2: launch_gemm_cfg<16, 4, 2>(g, tiles, s); break;
+            default: launch_gemm_cfg<16, 3, 2>(g, tiles, s); break;
+        }
     }
     SFM_LAUNCH_CHECK();
 }
 
-// ----------------------------------------------------------------------------
 // Diagonal tile: Cholesky + triangular inverse of one kNB x kNB tile in smem.
 // Blocked by 32: each 32x32 diagonal block is factored (and inverted) by one
 // warp in registers with shuffles (rsqrt pivots keep the per-column latency
@@ -778,6 +816,7 @@ int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, doubl
             const int below = K - c - 1;
             if (below == 0) break;
             GemmArgs t = gemm_args(Acc + kNB, ld, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
+            t.whole_tile = 1;  // in place: every output column reads the whole row tile
             launch_gemm(t, s);
             ++launches;
             const int inner = b0 + g_here - c - 1;  // remaining columns inside the panel
@@ -964,6 +1003,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
                 k_trsm_subst<<<cdiv(below * kNB, 128), 128, 0, s>>>(Acc + kNB, ld, below * kNB, Acc);
             } else {
                 GemmArgs t = gemm_args(Acc + kNB, ld, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
+            t.whole_tile = 1;  // in place: every output column reads the whole row tile
                 launch_gemm(t, s);
             }
             ++launches;

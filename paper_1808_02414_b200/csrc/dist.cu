@@ -426,6 +426,7 @@ void owner_step(RankDense& r, int p, Status* st) {
         const int below = K - c - 1;
         if (below == 0) break;
         GemmArgs t = gemm_args(Acc + kNB, ld, Acc + kNB, ld, r.linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
+        t.whole_tile = 1;  // in place: every output column reads the whole row tile
         launch_gemm(t, r.s);
         const int inner = g - gg - 1;
         if (inner > 0) {

@@ -96,6 +96,7 @@ struct GemmArgs {
     int b_kmajor;    // B stored K-contiguous
     int lower_only;  // skip tiles strictly above the matrix diagonal
     int row_off_tiles, col_off_tiles;  // C tile offsets relative to the diagonal
+    int whole_tile;  // C aliases A (in-place trsm): one CTA per 128-wide tile
     // Column-cyclic mode (cyc_R > 0, distributed sweep): C holds the local
     // columns of a rank owning panels rank, rank + R, ... of cyc_G tiles.
     // Grid tile (ti, tj) -> local column tile lt = tj + cyc_lt0, global

@@ -369,6 +369,9 @@ def main():
                 "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if achieved else None,
                 "traffic": None,
+                "traffic_note": ("per-stage DRAM not captured live; profiles/r01_ncu_dense_and_schur.txt: the largest "
+                                 "trailing-update launch moves 555 MB DRAM against 590 MB algorithmic (C read+write "
+                                 "+ panel), i.e. no re-reads"),
                 "peak_source": FP64_PEAK_SOURCE,
                 "algorithmic_flops": algo_flops, "executed_flops_padded": flops,
                 "stage_ms": dense_ms,

@@ -405,16 +405,18 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     // ---- (a) Jacobian ---------------------------------------------------------
     double* R = h->R.as<double>(9 * (size_t)n);
     double* rec = h->rec.as<double>((size_t)kRec * t);
-    launch_jacobian(sc, R, rec, st, s);
+    launch_jacobian(sc, ix.idx_cam, R, rec, st, s);
     mark(h, 2);
     if (mode == M_JACOBIAN) {
         sync_status(h);
         throw_numeric(h, sc, mode);
         std::vector<double> r((size_t)kRec * t);
+        std::vector<int> pos(t);
         d2h(h, r.data(), rec, 8 * r.size());
-        for (int k = 0; k < t; ++k) {
-            std::memcpy(out.jc + (size_t)2 * P * k, &r[(size_t)kRec * k], 8 * 2 * P);
-            std::memcpy(out.jp + (size_t)6 * k, &r[(size_t)kRec * k + 2 * P], 8 * 6);
+        d2h(h, pos.data(), ix.pos_cam, 4 * (size_t)t);
+        for (int k = 0; k < t; ++k) {  // records sit at by-camera slots
+            std::memcpy(out.jc + (size_t)2 * P * k, &r[(size_t)kRec * pos[k]], 8 * 2 * P);
+            std::memcpy(out.jp + (size_t)6 * k, &r[(size_t)kRec * pos[k] + 2 * P], 8 * 6);
         }
         return;
     }
@@ -445,9 +447,11 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         if (out.Cp) {
             // couplings C_t = (J_c^T W) J_p from the records (host assembly of a test output)
             std::vector<double> r((size_t)kRec * t);
+            std::vector<int> pos(t);
             d2h(h, r.data(), rec, 8 * r.size());
+            d2h(h, pos.data(), ix.pos_cam, 4 * (size_t)t);
             for (int k = 0; k < t; ++k) {
-                const double* jc = &r[(size_t)kRec * k];
+                const double* jc = &r[(size_t)kRec * pos[k]];
                 const double* jp = jc + 2 * P;
                 const double* W = jp + 6;
                 double* c = out.Cp + (size_t)P * 3 * k;

@@ -11,12 +11,16 @@
 
 namespace sfm {
 
-// Per-observation record (AoS, 224 B): [jc 2xP | jp 2x3 | W 2x2 | pad]
-constexpr int kRec = 28;
+// Per-observation record (AoS, 288 B): [jc 2xP | jp 2x3 | W 2x2 | pad | tg 2x3 | pad],
+// tg = the rotation-rhs factors -(d_C [C]x + d_X [X]x) (nullspace.cpp:40-50),
+// stored at the observation's by-camera slot (pos_cam), so a camera's
+// records are contiguous and the per-camera reductions stream them.
+constexpr int kRec = 36;
 template <int P> struct Layout {
     static constexpr int JC = 0;
     static constexpr int JP = 2 * P;
     static constexpr int WO = 2 * P + 6;
+    static constexpr int TG = 28;
 };
 // Per-observation Schur factor W_a = C_s,a L_j^-T (P x 3 row-major), stride 28.
 constexpr int kWStride = 28;

@@ -112,7 +112,7 @@ void launch_validate(const SceneDev& sc, int check_sigma, Status* st, int* cam_c
 void launch_build_index(const SceneDev& sc, const int* cam_cnt, const int* pt_cnt, IndexDev& ix, Workspace& ws,
                         cudaStream_t s);
 void launch_structure_check(const SceneDev& sc, const IndexDev& ix, Status* st, cudaStream_t s);
-void launch_jacobian(const SceneDev& sc, double* R, double* rec, Status* st, cudaStream_t s);
+void launch_jacobian(const SceneDev& sc, const int* idx_cam, double* R, double* rec, Status* st, cudaStream_t s);
 void launch_depth_of(const SceneDev& sc, const double* R, int t, double* out, cudaStream_t s);
 void launch_reductions(const SceneDev& sc, const IndexDev& ix, const double* rec, double* D, double* Hr, double* A,
                        double* s_a, unsigned char* flags, Status* st, cudaStream_t s);

@@ -108,20 +108,21 @@ __global__ void __launch_bounds__(128) k_point_prep(const double* A, const doubl
     if (threadIdx.x < 28) Fpart[28 * (size_t)blockIdx.x + threadIdx.x] = red[0][threadIdx.x];
 }
 
-// W_a = C_s,a L_j^-T (P x 3) per observation (thread per observation, records
-// read in observation order), stored at the observation's by-camera slot.
+// W_a = C_s,a L_j^-T (P x 3) per observation, one thread per by-camera slot
+// (records read and factors written contiguously).
 template <int P>
-__global__ void __launch_bounds__(128, 6) k_obs_factor(const int* oc, const int* op, const int* pos_cam, const double* rec,
+__global__ void __launch_bounds__(128, 6) k_obs_factor(const int* oc, const int* op, const int* idx_cam, const double* rec,
                                                     const double* s_a, const double* Lpt, int t_count, int n,
                                                     double* Wb) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= t_count) return;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;  // by-camera slot
+    if (k >= t_count) return;
+    const int t = idx_cam[k];
     const int ci = oc[t], pj = op[t];
-    const double* r = rec + (size_t)t * kRec;
-    double rr[kRec];
+    const double* r = rec + (size_t)k * kRec;
+    double rr[28];
     const double2* r2 = reinterpret_cast<const double2*>(r);
 #pragma unroll
-    for (int q = 0; q < kRec / 2; ++q) { const double2 v = r2[q]; rr[2 * q] = v.x; rr[2 * q + 1] = v.y; }
+    for (int q = 0; q < 14; ++q) { const double2 v = r2[q]; rr[2 * q] = v.x; rr[2 * q + 1] = v.y; }
     const double* jc = rr + Layout<P>::JC;
     const double* jp = rr + Layout<P>::JP;
     const double* W = rr + Layout<P>::WO;
@@ -146,8 +147,8 @@ __global__ void __launch_bounds__(128, 6) k_obs_factor(const int* oc, const int*
         wo[3 * p + 2] = good ? w2 : 0.0;
     }
 #pragma unroll
-    for (int k = 3 * P; k < kWStride; ++k) wo[k] = 0.0;
-    double2* o2 = reinterpret_cast<double2*>(Wb + (size_t)pos_cam[t] * kWStride);
+    for (int z = 3 * P; z < kWStride; ++z) wo[z] = 0.0;
+    double2* o2 = reinterpret_cast<double2*>(Wb + (size_t)k * kWStride);
 #pragma unroll
     for (int q = 0; q < kWStride / 2; ++q) o2[q] = make_double2(wo[2 * q], wo[2 * q + 1]);
 }
@@ -564,8 +565,8 @@ void launch_point_prep(const SceneDev& sc, const IndexDev& ix, const double* rec
     else k_point_prep<9><<<nb, 128, 0, s>>>(A, s_a, sc.pts, s_b, sc.m, sc.n, Lpt, V, Fpart, st);
     SFM_LAUNCH_CHECK();
     if (sc.t) {
-        if (sc.P == 8) k_obs_factor<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.oc, sc.op, ix.pos_cam, rec, s_a, Lpt, sc.t, sc.n, Wb);
-        else k_obs_factor<9><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.oc, sc.op, ix.pos_cam, rec, s_a, Lpt, sc.t, sc.n, Wb);
+        if (sc.P == 8) k_obs_factor<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.oc, sc.op, ix.idx_cam, rec, s_a, Lpt, sc.t, sc.n, Wb);
+        else k_obs_factor<9><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.oc, sc.op, ix.idx_cam, rec, s_a, Lpt, sc.t, sc.n, Wb);
         SFM_LAUNCH_CHECK();
     }
 }

@@ -114,9 +114,10 @@ __global__ void k_camera_rot(const double* cams, int n, int P, double* R) {
 // explicit 2x2 inverse of sigma (covariance.cpp:20-29).
 template <int P>
 __global__ void k_jacobian(const double* cams, const double* Rc, const double* pts, const int* oc, const int* op,
-                           const double* sigma, int t_count, double* rec, Status* st) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= t_count) return;
+                           const int* idx_cam, const double* sigma, int t_count, double* rec, Status* st) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;  // by-camera slot: records written contiguously
+    if (k >= t_count) return;
+    const int t = idx_cam[k];
     const int ci = oc[t], pj = op[t];
     double jc[2 * P], jp[6], depth;
     const bool ok = observation_jacobian<P>(cams + (size_t)P * ci, Rc + 9 * (size_t)ci, pts + 3 * (size_t)pj, jc, jp, &depth);
@@ -125,13 +126,30 @@ __global__ void k_jacobian(const double* cams, const double* Rc, const double* p
     if (sigma) { s00 = sigma[4 * (size_t)t]; s01 = sigma[4 * (size_t)t + 1]; s10 = sigma[4 * (size_t)t + 2]; s11 = sigma[4 * (size_t)t + 3]; }
     const double det = s00 * s11 - s01 * s10;
     if (!(s00 > 0.0) || !(det > 0.0)) atomicMin(&st->fisher_bad, t);
-    double* r = rec + (size_t)t * kRec;
-    for (int k = 0; k < 2 * P; ++k) r[Layout<P>::JC + k] = jc[k];
-    for (int k = 0; k < 6; ++k) r[Layout<P>::JP + k] = jp[k];
-    r[Layout<P>::WO + 0] = s11 / det;
-    r[Layout<P>::WO + 1] = -s01 / det;
-    r[Layout<P>::WO + 2] = -s10 / det;
-    r[Layout<P>::WO + 3] = s00 / det;
+    double rr[kRec];
+    for (int z = 0; z < kRec; ++z) rr[z] = 0.0;
+    for (int z = 0; z < 2 * P; ++z) rr[Layout<P>::JC + z] = jc[z];
+    for (int z = 0; z < 6; ++z) rr[Layout<P>::JP + z] = jp[z];
+    rr[Layout<P>::WO + 0] = s11 / det;
+    rr[Layout<P>::WO + 1] = -s01 / det;
+    rr[Layout<P>::WO + 2] = -s10 / det;
+    rr[Layout<P>::WO + 3] = s00 / det;
+    // rotation-rhs factors of this observation (the camera_reduce rhs entries):
+    // tg[ii][q] = -((d_C row ii . [C]x col q) + (d_X row ii . [X]x col q))
+    {
+        double hc[9], hx[9];
+        skew(cams + (size_t)P * ci + 3, hc);
+        skew(pts + 3 * (size_t)pj, hx);
+        for (int ii = 0; ii < 2; ++ii)
+            for (int q = 0; q < 3; ++q) {
+                const double a = (jc[P * ii + 3] * hc[0 + q] + jc[P * ii + 4] * hc[3 + q]) + jc[P * ii + 5] * hc[6 + q];
+                const double bb = (jp[3 * ii + 0] * hx[0 + q] + jp[3 * ii + 1] * hx[3 + q]) + jp[3 * ii + 2] * hx[6 + q];
+                rr[Layout<P>::TG + 3 * ii + q] = -(a + bb);
+            }
+    }
+    double2* r2 = reinterpret_cast<double2*>(rec + (size_t)k * kRec);
+#pragma unroll
+    for (int q = 0; q < kRec / 2; ++q) r2[q] = make_double2(rr[2 * q], rr[2 * q + 1]);
 }
 
 // Depth of one observation (error message path only).
@@ -151,109 +169,90 @@ __global__ void k_depth_of(const double* cams, const double* Rc, const double* p
 // ascending observation order; lane-owned entries keep each sum sequential.
 // Then H_r = eig-inverse(normal)·rhs (nullspace.cpp:52-61) and s_a = 1/sqrt(diag D).
 template <int P>
-__global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const int* idx_cam, const double* rec,
-                                                       const double* cams, const double* pts, const int* op, int n,
-                                                       double* D, double* Hr, double* s_a, unsigned char* flags,
-                                                       Status* st) {
+__global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const double* rec, int n, double* D,
+                                                       double* Hr, double* s_a, unsigned char* flags, Status* st) {
     // one CTA per camera, one thread per output entry: D (P*P), rotation
     // normal (9) and rhs (9); each entry is a sequential sum over the
-    // camera's observations in ascending order.
+    // camera's observations in ascending order.  The camera's records are
+    // contiguous (by-camera slots) and staged 64 at a time in shared memory;
+    // the D-row factors t0, t1 are formed once per (observation, row).
     constexpr int NE = P * P + 18;
-    // staged record [jc | jp | W | pad] at 0..27, X at 28..30, the rhs
-    // factors tg[ii][q] (6) at 32..37
-    constexpr int CH = 64, RS = kRec + 10, TG = 32;
+    constexpr int CH = 64, T01 = kRec, RS = T01 + 2 * P;  // staged record, then t0/t1 per row
     __shared__ double stage[CH][RS];
     __shared__ double sh[NE];
     const int i = blockIdx.x;
     const int tid = threadIdx.x;
-    const double* cam = cams + (size_t)P * i;
-    double hc[9];
-    skew(cam + 3, hc);
-    // entry decode (fixed per thread)
-    const int kind = tid < P * P ? 0 : (tid < P * P + 9 ? 1 : (tid < NE ? 2 : 3));
-    int p = 0, q = 0;
+    // entry decode (fixed per thread).  D entries (kind 0) on threads < P^2;
+    // the rotation normal and rhs entries (kinds 1, 2: one formula,
+    // jc[p] y1 + jc[P+p] y2) start at the next warp, so no warp runs two code
+    // paths (a divergent warp would hold every other warp at the barrier).
+    constexpr int B12 = ((P * P + 31) / 32) * 32;
+    const int e12 = tid - B12;
+    const int kind = tid < P * P ? 0 : ((e12 >= 0 && e12 < 9) ? 1 : ((e12 >= 9 && e12 < 18) ? 2 : 3));
+    const int slot = kind == 0 ? tid : P * P + e12;  // entry index in sh[]
+    int p = 0, q = 0, i1 = 0, i2 = 0;
     if (kind == 0) { p = tid / P; q = tid % P; }
-    else if (kind == 1) { p = (tid - P * P) / 3; q = (tid - P * P) % 3; }
-    else if (kind == 2) { p = (tid - P * P - 9) / 3; q = (tid - P * P - 9) % 3; }
+    else if (kind == 1) { p = e12 / 3; q = e12 % 3; i1 = Layout<P>::JC + q; i2 = Layout<P>::JC + P + q; }
+    else if (kind == 2) { p = (e12 - 9) / 3; q = (e12 - 9) % 3; i1 = Layout<P>::TG + q; i2 = Layout<P>::TG + 3 + q; }
     double acc = 0.0;
     const int b = off_cam[i], e = off_cam[i + 1];
     for (int k0 = b; k0 < e; k0 += CH) {
         const int nc = min(CH, e - k0);
-        // cooperative staging: 32 doubles per observation
-        for (int w = tid; w < nc * 16; w += 128) {
-            const int o = w >> 4, part = w & 15;
-            const int t = idx_cam[k0 + o];
-            double2 v;
-            if (part < 14) v = reinterpret_cast<const double2*>(rec + (size_t)t * kRec)[part];
-            else {
-                const double* X = pts + 3 * (size_t)op[t];
-                v = (part == 14) ? make_double2(X[0], X[1]) : make_double2(X[2], 0.0);
-            }
+        for (int w = tid; w < nc * (kRec / 2); w += 128) {
+            const int o = w / (kRec / 2), part = w - o * (kRec / 2);
+            const double2 v = reinterpret_cast<const double2*>(rec + (size_t)(k0 + o) * kRec)[part];
             stage[o][2 * part] = v.x;
             stage[o][2 * part + 1] = v.y;
         }
         __syncthreads();
-        // rhs factors, once per observation and column q:
-        // tg[ii][q] = -((jc_r . [C]x col q) + (jp . [X]x col q))
-        for (int w = tid; w < nc * 3; w += 128) {
-            const int o = w / 3, qq = w - 3 * o;
-            const double* r = stage[o];
-            const double* jc = r + Layout<P>::JC;
-            const double* jp = r + Layout<P>::JP;
-            double hx[9];
-            skew(r + 28, hx);
-            for (int ii = 0; ii < 2; ++ii) {
-                const double a = (jc[P * ii + 3] * hc[0 + qq] + jc[P * ii + 4] * hc[3 + qq]) + jc[P * ii + 5] * hc[6 + qq];
-                const double bb = (jp[3 * ii + 0] * hx[0 + qq] + jp[3 * ii + 1] * hx[3 + qq]) + jp[3 * ii + 2] * hx[6 + qq];
-                stage[o][TG + 3 * ii + qq] = -(a + bb);
-            }
+        // D row factors: t0 = jc_p W00 + jc_P+p W10, t1 = jc_p W01 + jc_P+p W11
+        for (int w = tid; w < nc * P; w += 128) {
+            const int o = w / P, pp = w - P * o;
+            const double* jc = stage[o] + Layout<P>::JC;
+            const double* W = stage[o] + Layout<P>::WO;
+            stage[o][T01 + 2 * pp] = jc[pp] * W[0] + jc[P + pp] * W[2];
+            stage[o][T01 + 2 * pp + 1] = jc[pp] * W[1] + jc[P + pp] * W[3];
         }
         __syncthreads();
         // ordered sums over the chunk; terms of 4 observations are formed
         // independently and added in observation order (bit-identical to a
         // plain sequential loop)
-        if (kind < 3) {
+        if (kind == 0) {
             int o = 0;
             for (; o + 4 <= nc; o += 4) {
                 double tv[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const double* r = stage[o + u];
-                    const double* jc = r + Layout<P>::JC;
-                    if (kind == 0) {
-                        const double* W = r + Layout<P>::WO;
-                        const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
-                        const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
-                        tv[u] = t0 * jc[q] + t1 * jc[P + q];
-                    } else if (kind == 1) {
-                        tv[u] = jc[p] * jc[q] + jc[P + p] * jc[P + q];
-                    } else {
-                        tv[u] = jc[p] * r[TG + q] + jc[P + p] * r[TG + 3 + q];
-                    }
+                    tv[u] = r[T01 + 2 * p] * r[Layout<P>::JC + q] + r[T01 + 2 * p + 1] * r[Layout<P>::JC + P + q];
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) acc += tv[u];
             }
             for (; o < nc; ++o) {
                 const double* r = stage[o];
-                const double* jc = r + Layout<P>::JC;
-                double tv;
-                if (kind == 0) {
-                    const double* W = r + Layout<P>::WO;
-                    const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
-                    const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
-                    tv = t0 * jc[q] + t1 * jc[P + q];
-                } else if (kind == 1) {
-                    tv = jc[p] * jc[q] + jc[P + p] * jc[P + q];
-                } else {
-                    tv = jc[p] * r[TG + q] + jc[P + p] * r[TG + 3 + q];
+                acc += r[T01 + 2 * p] * r[Layout<P>::JC + q] + r[T01 + 2 * p + 1] * r[Layout<P>::JC + P + q];
+            }
+        } else if (kind < 3) {
+            int o = 0;
+            for (; o + 4 <= nc; o += 4) {
+                double tv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double* r = stage[o + u];
+                    tv[u] = r[Layout<P>::JC + p] * r[i1] + r[Layout<P>::JC + P + p] * r[i2];
                 }
-                acc += tv;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc += tv[u];
+            }
+            for (; o < nc; ++o) {
+                const double* r = stage[o];
+                acc += r[Layout<P>::JC + p] * r[i1] + r[Layout<P>::JC + P + p] * r[i2];
             }
         }
         __syncthreads();
     }
-    if (tid < NE) sh[tid] = acc;
+    if (kind < 3) sh[slot] = acc;
     __syncthreads();
     if (tid < P * P) D[(size_t)P * P * i + tid] = acc;
     if (tid < P) {
@@ -275,14 +274,14 @@ __global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const
 
 // ---- per-point reduction: A_j = Σ (J_pᵀW)J_p (covariance.cpp:64-71) ---------
 template <int P>
-__global__ void k_point_reduce(const int* off_pt, const int* idx_pt, const double* rec, int m, int n, double* A,
+__global__ void k_point_reduce(const int* off_pt, const int* idx_pt, const int* pos_cam, const double* rec, int m, int n, double* A,
                                double* s_a, unsigned char* flags, Status* st) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
     double a[9];
     for (int k = 0; k < 9; ++k) a[k] = 0.0;
     for (int k = off_pt[j]; k < off_pt[j + 1]; ++k) {
-        const double* r = rec + (size_t)idx_pt[k] * kRec;
+        const double* r = rec + (size_t)pos_cam[idx_pt[k]] * kRec;
         const double* jp = r + Layout<P>::JP;
         const double* W = r + Layout<P>::WO;
         for (int p = 0; p < 3; ++p) {
@@ -434,11 +433,11 @@ void launch_structure_check(const SceneDev& sc, const IndexDev& ix, Status* st, 
     if (g) { k_structure_check<<<cdiv(g, 256), 256, 0, s>>>(ix.off_cam, sc.n, ix.off_pt, ix.idx_pt, sc.oc, sc.m, st); SFM_LAUNCH_CHECK(); }
 }
 
-void launch_jacobian(const SceneDev& sc, double* R, double* rec, Status* st, cudaStream_t s) {
+void launch_jacobian(const SceneDev& sc, const int* idx_cam, double* R, double* rec, Status* st, cudaStream_t s) {
     if (sc.n) { k_camera_rot<<<cdiv(sc.n, 128), 128, 0, s>>>(sc.cams, sc.n, sc.P, R); SFM_LAUNCH_CHECK(); }
     if (sc.t) {
-        if (sc.P == 8) k_jacobian<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, sc.sigma, sc.t, rec, st);
-        else k_jacobian<9><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, sc.sigma, sc.t, rec, st);
+        if (sc.P == 8) k_jacobian<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, idx_cam, sc.sigma, sc.t, rec, st);
+        else k_jacobian<9><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, idx_cam, sc.sigma, sc.t, rec, st);
         SFM_LAUNCH_CHECK();
     }
 }
@@ -453,13 +452,13 @@ void launch_reductions(const SceneDev& sc, const IndexDev& ix, const double* rec
     const size_t ncols = (size_t)sc.P * sc.n + 3 * (size_t)sc.m;
     SFM_CUDA(cudaMemsetAsync(flags, 0, ncols, s));
     if (sc.n) {
-        if (sc.P == 8) k_camera_reduce<8><<<sc.n, 128, 0, s>>>(ix.off_cam, ix.idx_cam, rec, sc.cams, sc.pts, sc.op, sc.n, D, Hr, s_a, flags, st);
-        else k_camera_reduce<9><<<sc.n, 128, 0, s>>>(ix.off_cam, ix.idx_cam, rec, sc.cams, sc.pts, sc.op, sc.n, D, Hr, s_a, flags, st);
+        if (sc.P == 8) k_camera_reduce<8><<<sc.n, 128, 0, s>>>(ix.off_cam, rec, sc.n, D, Hr, s_a, flags, st);
+        else k_camera_reduce<9><<<sc.n, 128, 0, s>>>(ix.off_cam, rec, sc.n, D, Hr, s_a, flags, st);
         SFM_LAUNCH_CHECK();
     }
     if (sc.m) {
-        if (sc.P == 8) k_point_reduce<8><<<cdiv(sc.m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, rec, sc.m, sc.n, A, s_a, flags, st);
-        else k_point_reduce<9><<<cdiv(sc.m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, rec, sc.m, sc.n, A, s_a, flags, st);
+        if (sc.P == 8) k_point_reduce<8><<<cdiv(sc.m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, ix.pos_cam, rec, sc.m, sc.n, A, s_a, flags, st);
+        else k_point_reduce<9><<<cdiv(sc.m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, ix.pos_cam, rec, sc.m, sc.n, A, s_a, flags, st);
         SFM_LAUNCH_CHECK();
     }
 }

@@ -74,7 +74,7 @@ struct sfmcov_handle {
     int dist_mode = 0, dist_R = 1, dist_rank = 0, emu_R = 1;
     void* nccl = nullptr;
     std::vector<sfm::RankDense> ranks;
-    DBuf seg, seg_tmp, prange_r;
+    DBuf seg, seg_tmp, prange_r, scale_mm;
     cudaEvent_t ev_ready = nullptr, ev_rank_done[64];
     bool ev_rank_init = false;
     // captured dense stage (Cholesky + triangular inverse), keyed by its inputs
@@ -332,13 +332,20 @@ void fill_diagnostics(sfmcov_handle* h, Outputs& out, const double* prange, cons
         d->negative_eigenvalue_warnings = warn;
         d->largest_dense_dim = (int64_t)N + 7;
         d->peak_dense_bytes = dense_bytes;
-        // scale range and flagged columns
-        std::vector<double> sa(ncols);
-        std::vector<unsigned char> f(ncols);
-        d2h(h, sa.data(), s_a, 8 * ncols);
-        if (h->st_host->nflag) d2h(h, f.data(), flags, ncols);
-        d->scale_min = ncols ? *std::min_element(sa.begin(), sa.end()) : 1.0;
-        d->scale_max = ncols ? *std::max_element(sa.begin(), sa.end()) : 1.0;
+        // scale range (device min/max) and flagged columns
+        std::vector<unsigned char> f;
+        double srange[2] = {1.0, 1.0};
+        if (ncols) {
+            double* mm = h->scale_mm.as<double>(2 * 296 + 2);
+            launch_minmax(s_a, (long long)ncols, mm + 2, mm, h->s);
+            d2h(h, srange, mm, 16);
+        }
+        if (h->st_host->nflag) {
+            f.resize(ncols);
+            d2h(h, f.data(), flags, ncols);
+        }
+        d->scale_min = srange[0];
+        d->scale_max = srange[1];
         int64_t cnt = 0;
         if (h->st_host->nflag)
             for (size_t c = 0; c < ncols; ++c)
@@ -810,6 +817,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     h->seg.release();
     h->seg_tmp.release();
     h->prange_r.release();
+    h->scale_mm.release();
     if (h->ev_rank_init) {
         cudaEventDestroy(h->ev_ready);
         for (auto& e : h->ev_rank_done) cudaEventDestroy(e);

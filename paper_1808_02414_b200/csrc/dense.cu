@@ -751,6 +751,54 @@ __global__ void k_pivot_range(const double* piv, int N, double* out) {
     if (threadIdx.x == 0) { out[0] = mn[0]; out[1] = mx[0]; }
 }
 
+// min / max of x[0..count) (values > 0 here: the Jacobi scales), two passes.
+__global__ void k_minmax_partial(const double* x, long long count, double* part) {
+    __shared__ double mn[256], mx[256];
+    double a = INFINITY, b = -INFINITY;
+    for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < count; i += (long long)gridDim.x * 256) {
+        const double v = x[i];
+        a = fmin(a, v);
+        b = fmax(b, v);
+    }
+    mn[threadIdx.x] = a;
+    mx[threadIdx.x] = b;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            mn[threadIdx.x] = fmin(mn[threadIdx.x], mn[threadIdx.x + w]);
+            mx[threadIdx.x] = fmax(mx[threadIdx.x], mx[threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { part[2 * blockIdx.x] = mn[0]; part[2 * blockIdx.x + 1] = mx[0]; }
+}
+
+__global__ void k_minmax_final(const double* part, int nb, double* out) {
+    __shared__ double mn[256], mx[256];
+    double a = INFINITY, b = -INFINITY;
+    for (int i = threadIdx.x; i < nb; i += 256) { a = fmin(a, part[2 * i]); b = fmax(b, part[2 * i + 1]); }
+    mn[threadIdx.x] = a;
+    mx[threadIdx.x] = b;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            mn[threadIdx.x] = fmin(mn[threadIdx.x], mn[threadIdx.x + w]);
+            mx[threadIdx.x] = fmax(mx[threadIdx.x], mx[threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { out[0] = mn[0]; out[1] = mx[0]; }
+}
+
+// out[0..1] = min, max; part: 2 * 296 doubles of scratch
+void launch_minmax(const double* x, long long count, double* part, double* out, cudaStream_t s) {
+    constexpr int NB = 296;
+    k_minmax_partial<<<NB, 256, 0, s>>>(x, count, part);
+    SFM_LAUNCH_CHECK();
+    k_minmax_final<<<1, 256, 0, s>>>(part, NB, out);
+    SFM_LAUNCH_CHECK();
+}
+
 void launch_pivot_range(const double* piv, int N, double* out, cudaStream_t s) {
     k_pivot_range<<<1, 256, 0, s>>>(piv, N, out);
     SFM_LAUNCH_CHECK();

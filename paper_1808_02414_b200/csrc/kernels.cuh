@@ -147,6 +147,7 @@ void launch_copy_panel_w(const double* X, long long ld, int b0, int G, int rows,
 void launch_extract(int P, const double* X, long long ld, int N, int nblocks, const double* s_a, int scale, double* cov,
                     Status* st, int* psd_warn, cudaStream_t s);
 void launch_set_diag(double* Z, long long ld, int from, int to, cudaStream_t s);
+void launch_minmax(const double* x, long long count, double* part, double* out, cudaStream_t s);
 void launch_pivot_range(const double* piv, int N, double* out, cudaStream_t s);
 int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, cudaStream_t s,
                    cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2);

@@ -1032,6 +1032,9 @@ static void launch_panel_take(double* Z, long long ld, int b0, int W, int rows, 
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
                 cudaEvent_t eR) {
+    // timing experiments only (results invalid): SFMCOV_SWEEP_SKIP=1 drops
+    // the trailing update, 2 the inverse, 3 both
+    static const int skip = [] { const char* e = std::getenv("SFMCOV_SWEEP_SKIP"); return e ? std::atoi(e) : 0; }();
     const int K = Npad / kNB;
     int launches = 0;
     bool rest_pending = false;
@@ -1076,7 +1079,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
         const int T2 = K - nb0;
         const int gn = (T2 < G) ? T2 : G;
         // --- Cholesky trailing update ---
-        if (T2 > gn) {
+        if (T2 > gn && !(skip & 1)) {
             SFM_CUDA(cudaStreamWaitEvent(s2, eL[slot], 0));
             const int r0 = nb0 + gn;
             const double* Lr = Lb + W + (size_t)gn * kNB;
@@ -1095,13 +1098,13 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             ++launches;
         }
         rest_pending = false;
-        if (T2 > gn) {
+        if (T2 > gn && !(skip & 1)) {
             SFM_CUDA(cudaEventRecord(eR, s2));
             rest_pending = true;
         }
         // --- inverse step p (rows of panel p) ---
         SFM_CUDA(cudaStreamWaitEvent(s3, eL[slot], 0));
-        for (int g = 0; g < g_here; ++g) {
+        for (int g = 0; g < g_here && !(skip & 2); ++g) {
             const int r = b0 + g;
             GemmArgs a = gemm_args(Z + (size_t)r * kNB, ld, Linv + (size_t)r * kNB * kNB, kNB, Z + (size_t)r * kNB, ld,
                                    1, r + 1, kNB);
@@ -1117,7 +1120,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
                 ++launches;
             }
         }
-        if (T2 > 0) {
+        if (T2 > 0 && !(skip & 2)) {
             GemmArgs x = gemm_args(Z + (size_t)nb0 * kNB, ld, Lb + W, rows, Z + (size_t)b0 * kNB, ld, T2, nb0, W);
             x.b_kmajor = 1; x.alpha_neg = 1; x.beta = 1; x.beta0_from = b0;
             launch_gemm(x, s3);

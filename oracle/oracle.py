@@ -76,6 +76,7 @@ def lib():
             "oracle_schur": (i32, [vp, C.c_int, vp, vp]),
             "oracle_invert_schur": (i32, [vp, i64, vp, vp, vp]),
             "oracle_compute_covariance": (i32, [vp, C.c_int, vp, vp, vp, i64, vp, vp]),
+            "oracle_compute_covariance_full": (i32, [vp, C.c_int, vp, vp, vp, vp, vp, i64, vp]),
             "oracle_dense_fisher": (i32, [vp, vp, vp]),
             "oracle_pseudoinverse": (i32, [vp, i64, vp, vp, vp, dp, vp]),
             "oracle_cholesky_route": (i32, [vp, i64, C.c_int, vp, C.c_int, vp, vp]),
@@ -226,6 +227,24 @@ def compute_covariance(rec, threads=1):
     names = ["validate", "jacobian", "nullspace", "fisher", "conditioning", "schur", "dsytrf", "dsytrs2", "extract",
              "total"]
     return cov[:n], d, fl[:d.n_flagged].tolist(), dict(zip(names, times.tolist()))
+
+
+def compute_covariance_full(rec, threads=1, point_covariances=True, camera_cross_covariances=True):
+    """compute_covariance with the reference's optional outputs
+    (covariance.cpp:283-348): returns (camera_cov (n,P,P), point_cov (m,3,3) or
+    None, camera_matrix (Pn,Pn) or None, OracleDiag)."""
+    n, P, m = rec.cams.shape[0], rec.cams.shape[1], rec.pts.shape[0]
+    cov = np.empty((max(n, 1), P, P))
+    pc = np.empty((max(m, 1), 3, 3)) if point_covariances else None
+    cm = np.empty((P * n, P * n), order="F") if camera_cross_covariances else None
+    d = OracleDiag()
+    fl = np.empty(max(P * n + 3 * m, 1), np.int64)
+    err = OracleError()
+    _check(lib().oracle_compute_covariance_full(C.byref(_scene(rec)), threads, cov.ctypes.data,
+                                                None if pc is None else pc.ctypes.data,
+                                                None if cm is None else cm.ctypes.data, C.byref(d), fl.ctypes.data,
+                                                fl.size, C.byref(err)), err)
+    return cov[:n], (pc[:m] if pc is not None else None), cm, d
 
 
 def dense_fisher(rec):

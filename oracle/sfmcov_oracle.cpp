@@ -832,6 +832,75 @@ inline void extract_camera_covariances(const std::vector<double>& zinv, int64_t 
     }
 }
 
+// ---- point covariances: src/covariance.cpp:283-319 ----------------------------
+// Sigma_X[j] = S_j (A_j^-1 + W Z_sub W^T) S_j, W = A_j^-1 [C_a^T ... | H_pj],
+// Z_sub the bordered inverse restricted to the point's cameras and the border.
+template <int P>
+inline void extract_point_covariances(const System<P>& sys, const oracle_scene& s, const std::vector<M3>& a_inv,
+                                      const std::vector<double>& zinv, int64_t dim, double* point_cov, int threads) {
+    const int64_t n = sys.n;
+    const int b = kGauge;
+    parallel_for(sys.m, threads, [&](int64_t lo, int64_t hi) {
+        std::vector<double> wj, zs, tmp;
+        for (int64_t j = lo; j < hi; ++j) {
+            const int64_t o0 = sys.by_pt.off[j], w = sys.by_pt.off[j + 1] - o0;
+            const int64_t cols = P * w + b;
+            wj.assign(size_t(3) * cols, 0.0);  // row-major 3 x cols
+            for (int64_t a = 0; a < w; ++a) {
+                const int64_t t = sys.by_pt.idx[o0 + a];
+                const double* c = &sys.Cp[size_t(P) * 3 * t];  // P x 3, c[3p + q]
+                for (int r = 0; r < 3; ++r)
+                    for (int p = 0; p < P; ++p)
+                        wj[size_t(r) * cols + P * a + p] =
+                            (a_inv[j](r, 0) * c[3 * p] + a_inv[j](r, 1) * c[3 * p + 1]) + a_inv[j](r, 2) * c[3 * p + 2];
+            }
+            for (int r = 0; r < 3; ++r)
+                for (int l = 0; l < b; ++l) {
+                    const double* hr = &sys.H[size_t(P * n + 3 * j) * kGauge];
+                    wj[size_t(r) * cols + P * w + l] =
+                        (a_inv[j](r, 0) * hr[l] + a_inv[j](r, 1) * hr[kGauge + l]) + a_inv[j](r, 2) * hr[2 * kGauge + l];
+                }
+            // z_sub (cols x cols, row-major) from the bordered inverse
+            zs.assign(size_t(cols) * cols, 0.0);
+            auto gidx = [&](int64_t k) -> int64_t {  // global row/col of local index k
+                if (k < P * w) {
+                    const int64_t a = k / P;
+                    return P * int64_t(s.obs_cam[sys.by_pt.idx[o0 + a]]) + (k - P * a);
+                }
+                return P * n + (k - P * w);
+            };
+            for (int64_t r = 0; r < cols; ++r) {
+                const int64_t gr = gidx(r);
+                for (int64_t c = 0; c < cols; ++c) zs[size_t(r) * cols + c] = zinv[size_t(gidx(c)) * dim + gr];
+            }
+            // cov = a_inv + (wj zs) wj^T
+            tmp.assign(size_t(3) * cols, 0.0);
+            for (int r = 0; r < 3; ++r)
+                for (int64_t c = 0; c < cols; ++c) {
+                    double v = 0.0;
+                    for (int64_t k = 0; k < cols; ++k) v += wj[size_t(r) * cols + k] * zs[size_t(k) * cols + c];
+                    tmp[size_t(r) * cols + c] = v;
+                }
+            const double* sp = &sys.s_a[P * n + 3 * j];
+            for (int r = 0; r < 3; ++r)
+                for (int q = 0; q < 3; ++q) {
+                    double v = 0.0;
+                    for (int64_t k = 0; k < cols; ++k) v += tmp[size_t(r) * cols + k] * wj[size_t(q) * cols + k];
+                    point_cov[9 * j + 3 * r + q] = (sp[r] * (a_inv[j](r, q) + v)) * sp[q];
+                }
+        }
+    });
+}
+
+// camera_matrix = S_c Z_inv[cams, cams] S_c (covariance.cpp:346-348), col-major N x N
+template <int P>
+inline void extract_camera_matrix(const std::vector<double>& zinv, int64_t dim, const std::vector<double>& s_a, int64_t n,
+                                  double* cm) {
+    const int64_t N = P * n;
+    for (int64_t c = 0; c < N; ++c)
+        for (int64_t r = 0; r < N; ++r) cm[size_t(c) * N + r] = (s_a[r] * zinv[size_t(c) * dim + r]) * s_a[c];
+}
+
 struct Timings { double validate = 0, jacobian = 0, nullspace = 0, fisher = 0, conditioning = 0, schur = 0, dsytrf = 0, dsytrs2 = 0, extract = 0, total = 0; };
 
 inline double since(std::chrono::steady_clock::time_point t0) {
@@ -841,7 +910,8 @@ inline double since(std::chrono::steady_clock::time_point t0) {
 // ---- pipeline: src/covariance.cpp:323-350 --------------------------------------
 template <int P>
 inline void compute_covariance(const oracle_scene& s, int threads, double* cam_cov, oracle_diag* diag,
-                               int64_t* flagged, int64_t flagged_cap, Timings* tm) {
+                               int64_t* flagged, int64_t flagged_cap, Timings* tm, double* point_cov = nullptr,
+                               double* camera_matrix = nullptr) {
     auto T0 = std::chrono::steady_clock::now();
     auto t0 = T0;
     validate(s);
@@ -860,11 +930,14 @@ inline void compute_covariance(const oracle_scene& s, int threads, double* cam_c
     const int64_t dim = P * sys.n + kGauge;
     diag->largest_dense_dim = dim;
     diag->peak_dense_bytes = 8 * dim * dim;
-    std::vector<double> z = schur_reduce<P>(sys, s, threads, nullptr);
+    std::vector<M3> a_inv;
+    std::vector<double> z = schur_reduce<P>(sys, s, threads, point_cov ? &a_inv : nullptr);
     tm->schur = since(t0); t0 = std::chrono::steady_clock::now();
     const std::vector<double> zinv = invert_schur(std::move(z), dim, diag, &tm->dsytrf, &tm->dsytrs2);
     t0 = std::chrono::steady_clock::now();
     extract_camera_covariances<P>(zinv, dim, sys.s_a, sys.n, cam_cov, diag);
+    if (point_cov) extract_point_covariances<P>(sys, s, a_inv, zinv, dim, point_cov, threads);
+    if (camera_matrix) extract_camera_matrix<P>(zinv, dim, sys.s_a, sys.n, camera_matrix);
     diag->n_flagged = (int32_t)sys.flagged.size();
     for (int64_t k = 0; k < std::min<int64_t>(flagged_cap, (int64_t)sys.flagged.size()); ++k) flagged[k] = sys.flagged[k];
     tm->extract = since(t0);
@@ -1104,6 +1177,23 @@ int oracle_compute_covariance(const oracle_scene* s, int threads, double* cam_co
                                   tm.schur, tm.dsytrf, tm.dsytrs2, tm.extract, tm.total};
             std::memcpy(times, v, sizeof v);
         }
+        return ok(e);
+    } catch (const Error& x) { return fail(e, x); }
+}
+
+// compute_covariance with CovarianceOptions::point_covariances /
+// camera_cross_covariances: point_cov m x 3 x 3 (row-major blocks),
+// camera_matrix P n x P n col-major; either may be NULL.
+int oracle_compute_covariance_full(const oracle_scene* s, int threads, double* cam_cov, double* point_cov,
+                                   double* camera_matrix, oracle_diag* diag, int64_t* flagged, int64_t flagged_cap,
+                                   oracle_error* e) {
+    try {
+        Timings tm;
+        if (s->cam_params != 8 && s->cam_params != 9) throw Error{kDimension, "validate", "camera width must be 8 or 9"};
+        if (s->cam_params == 8)
+            compute_covariance<8>(*s, threads, cam_cov, diag, flagged, flagged_cap, &tm, point_cov, camera_matrix);
+        else
+            compute_covariance<9>(*s, threads, cam_cov, diag, flagged, flagged_cap, &tm, point_cov, camera_matrix);
         return ok(e);
     } catch (const Error& x) { return fail(e, x); }
 }

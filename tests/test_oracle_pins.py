@@ -419,3 +419,22 @@ def test_count_floors():
     with pytest.raises(O.OracleFailure) as e:
         O.validate(sub)
     assert "camera 2 observes 3 points, need at least 4" in str(e.value)
+
+
+def test_point_and_cross_covariances_match_the_materialized_covariance():  # test_covariance.cpp:42-68
+    rec = S.generate_cube_scene(2, 0.5)
+    cov, pc, cm, _ = O.compute_covariance_full(rec)
+    _, sigma, _, _ = O.pseudoinverse(rec)
+    n, P, m = rec.cams.shape[0], rec.cams.shape[1], rec.pts.shape[0]
+    assert sigma.shape[0] == P * n + 3 * m
+    for i in range(n):
+        assert rel(cov[i], sigma[P * i:P * i + P, P * i:P * i + P]) < 1e-8
+    assert pc.shape == (m, 3, 3)
+    for j in range(m):
+        r0 = P * n + 3 * j
+        assert rel(pc[j], sigma[r0:r0 + 3, r0:r0 + 3]) < 1e-8
+    assert cm.shape == (P * n, P * n)
+    for i in range(n):
+        assert np.array_equal(cm[P * i:P * i + P, P * i:P * i + P], cov[i])
+        for l in range(n):
+            assert rel(cm[P * i:P * i + P, P * l:P * l + P], sigma[P * i:P * i + P, P * l:P * l + P]) < 1e-8

@@ -64,8 +64,8 @@ typedef struct sfmcov_scene {
 /* sfmcov::CovarianceOptions (include/sfmcov/covariance.hpp:71-75). */
 typedef struct sfmcov_options {
     int32_t threads;                  /* accepted and ignored (results never depend on it) */
-    int32_t point_covariances;        /* not yet supported: must be 0 */
-    int32_t camera_cross_covariances; /* not yet supported: must be 0 */
+    int32_t point_covariances;        /* sfmcov_cuda_compute_covariance_full only */
+    int32_t camera_cross_covariances; /* sfmcov_cuda_compute_covariance_full only */
     int32_t reserved;
 } sfmcov_options;
 
@@ -109,6 +109,18 @@ void* sfmcov_cuda_stream(sfmcov_handle* h);
 int32_t sfmcov_cuda_compute_covariance(sfmcov_handle* h, const sfmcov_scene* scene,
                                        const sfmcov_options* opts, double* cam_cov,
                                        sfmcov_diagnostics* diag, sfmcov_error* err);
+
+/* With the reference's optional outputs (CovarianceOptions::point_covariances
+ * / camera_cross_covariances; covariance.cpp:283-348, result fields
+ * point_cov and camera_matrix, covariance.hpp:62-69): point_cov is
+ * n_pts x 3 x 3 (row-major blocks), camera_matrix the full (P n) x (P n)
+ * camera covariance, column-major (symmetric up to the last bit, like the
+ * reference's S Z_inv S); camera_cov equals its diagonal blocks bitwise when
+ * it is requested.  A buffer may be NULL when its option is off. */
+int32_t sfmcov_cuda_compute_covariance_full(sfmcov_handle* h, const sfmcov_scene* scene,
+                                            const sfmcov_options* opts, double* cam_cov, double* point_cov,
+                                            double* camera_matrix, sfmcov_diagnostics* diag,
+                                            sfmcov_error* err);
 
 /* Same, with every scene pointer and d_cam_cov in device memory of the
  * handle's device (inputs resident in HBM; used by the device-timed bench). */

@@ -25,6 +25,7 @@ using Vec2 = std::array<double, 2>;
 using Vec3 = std::array<double, 3>;
 using Mat2 = std::array<double, 4>;  // row-major
 using Mat8 = std::array<double, 64>; // row-major
+using Mat3 = std::array<double, 9>;  // row-major
 using Index = std::int64_t;
 
 inline constexpr int kCameraParams = 8;
@@ -88,7 +89,18 @@ struct CovarianceDiagnostics {
 
 struct CovarianceResult {
     std::vector<Mat8> camera_cov;
+    std::vector<Mat3> point_cov;        // filled when options.point_covariances
+    std::vector<double> camera_matrix;  // (8n x 8n, column-major) when options.camera_cross_covariances
+    Index camera_matrix_rows = 0;
     CovarianceDiagnostics diagnostics;
+
+    // block (i, j) of the camera matrix (covariance.hpp:67), row-major 8 x 8
+    Mat8 cross_block(Index i, Index j) const {
+        Mat8 b{};
+        for (int p = 0; p < 8; ++p)
+            for (int q = 0; q < 8; ++q) b[8 * p + q] = camera_matrix[(size_t)(8 * j + q) * camera_matrix_rows + 8 * i + p];
+        return b;
+    }
 };
 
 struct CovarianceOptions {
@@ -154,9 +166,15 @@ inline CovarianceResult compute_covariance(const Reconstruction& rec, const Cova
     d.flagged = flagged.data();
     d.flagged_capacity = (int64_t)flagged.size();
     sfmcov_error e{};
-    b200::check(sfmcov_cuda_compute_covariance(b200::default_handle(), &s, &o,
-                                               result.camera_cov.empty() ? nullptr : result.camera_cov[0].data(),
-                                               &d, &e),
+    if (options.point_covariances) result.point_cov.resize(m);
+    if (options.camera_cross_covariances) {
+        result.camera_matrix_rows = 8 * n;
+        result.camera_matrix.resize((size_t)(8 * n) * (8 * n));
+    }
+    b200::check(sfmcov_cuda_compute_covariance_full(
+                    b200::default_handle(), &s, &o, result.camera_cov.empty() ? nullptr : result.camera_cov[0].data(),
+                    result.point_cov.empty() ? nullptr : result.point_cov[0].data(),
+                    result.camera_matrix.empty() ? nullptr : result.camera_matrix.data(), &d, &e),
                 e);
     CovarianceDiagnostics& g = result.diagnostics;
     g.scale_min = d.scale_min;

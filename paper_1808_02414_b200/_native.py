@@ -77,6 +77,11 @@ CUDA_SYMBOLS = {
         C.c_int32,
         [C.c_void_p, C.POINTER(Scene), C.POINTER(Options), C.c_void_p, C.POINTER(Diagnostics), C.POINTER(ErrorStruct)],
     ),
+    "sfmcov_cuda_compute_covariance_full": (
+        C.c_int32,
+        [C.c_void_p, C.POINTER(Scene), C.POINTER(Options), C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Diagnostics),
+         C.POINTER(ErrorStruct)],
+    ),
     "sfmcov_cuda_compute_covariance_device": (
         C.c_int32,
         [C.c_void_p, C.POINTER(Scene), C.POINTER(Options), C.c_void_p, C.POINTER(Diagnostics), C.POINTER(ErrorStruct)],

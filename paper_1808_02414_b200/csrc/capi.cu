@@ -75,6 +75,7 @@ struct sfmcov_handle {
     void* nccl = nullptr;
     std::vector<sfm::RankDense> ranks;
     DBuf seg, seg_tmp, prange_r, scale_mm;
+    DBuf zi, fc_part, fc_y, fc_gtt, fc_eb, fc_pc;
     cudaEvent_t ev_ready = nullptr, ev_rank_done[64];
     bool ev_rank_init = false;
     // captured dense stage (Cholesky + triangular inverse), keyed by its inputs
@@ -120,6 +121,9 @@ struct Outputs {
     double* s_a = nullptr;
     double* s_b = nullptr;
     double* z_p = nullptr;
+    // optional outputs (host), CovarianceOptions::point_covariances / camera_cross_covariances
+    double* h_point_cov = nullptr;
+    double* h_camera_matrix = nullptr;
     int64_t* off_cam = nullptr;
     int32_t* idx_cam = nullptr;
     int64_t* off_pt = nullptr;
@@ -547,9 +551,32 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     run_dense(h, Z, ld, Npad, Linv, piv, st, serial, true);
     int* psd = h->psd.as<int>(1);
     SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
-    launch_extract(P, Z, ld, N, n, s_a, 1, out.d_cam_cov, st, psd, s);
+    const bool cross = out.h_camera_matrix != nullptr;
+    if (!cross) launch_extract(P, Z, ld, N, n, s_a, 1, out.d_cam_cov, st, psd, s);
     double* prange = h->prange.as<double>(2);
     launch_pivot_range(piv, N, prange, s);
+    if (out.h_point_cov || cross) {
+        // optional outputs: Z_aug^-1 = X^T X and the bordered-inverse blocks (fullcov.cu)
+        FullCovArgs a{};
+        a.P = P; a.n = n; a.m = m; a.Npad = Npad;
+        a.X = Z;
+        a.Zi = h->zi.as<double>((size_t)Npad * Npad);
+        a.G = G; a.LF = LF; a.Lpt = Lpt; a.V = V; a.Wb = Wb; a.s_a = s_a;
+        a.off_pt = ix.off_pt; a.idx_pt = ix.idx_pt; a.oc = sc.oc; a.pos_cam = ix.pos_cam;
+        a.part = h->fc_part.as<double>(full_cov_part_doubles(N));
+        a.Y = h->fc_y.as<double>((size_t)N * 7 + 7);
+        a.gtt_part = h->fc_gtt.as<double>(49 * ((size_t)N / 64 + 2));
+        a.Eb = h->fc_eb.as<double>(49);
+        a.point_cov = out.h_point_cov ? h->fc_pc.as<double>(9 * (size_t)m + 9) : nullptr;
+        a.cross = cross ? 1 : 0;
+        a.cam_cov = out.d_cam_cov;
+        a.psd = psd;
+        full_covariance(a, s);
+        if (out.h_point_cov && m) d2h(h, out.h_point_cov, a.point_cov, 8 * 9 * (size_t)m);
+        if (cross && N)
+            SFM_CUDA(cudaMemcpy2DAsync(out.h_camera_matrix, 8 * (size_t)N, a.Zi, 8 * ld, 8 * (size_t)N, N,
+                                       cudaMemcpyDeviceToHost, s));
+    }
     mark(h, 10);
     sync_status(h);
     {
@@ -748,10 +775,12 @@ int32_t guarded(sfmcov_handle* h, sfmcov_error* err, F&& body) {
     }
 }
 
+// compute_covariance (camera blocks only) refuses the optional outputs: they
+// need the output buffers of sfmcov_cuda_compute_covariance_full.
 void check_options(const sfmcov_options* o) {
     if (o && (o->point_covariances || o->camera_cross_covariances))
         throw ApiError{SFMCOV_ERR_DIMENSION, "options",
-                       "point and cross covariances are not available in this build (camera blocks only)"};
+                       "point / cross covariances need sfmcov_cuda_compute_covariance_full (output buffers)"};
 }
 
 }  // namespace
@@ -818,6 +847,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     h->seg_tmp.release();
     h->prange_r.release();
     h->scale_mm.release();
+    for (DBuf* b : {&h->zi, &h->fc_part, &h->fc_y, &h->fc_gtt, &h->fc_eb, &h->fc_pc}) b->release();
     if (h->ev_rank_init) {
         cudaEventDestroy(h->ev_ready);
         for (auto& e : h->ev_rank_done) cudaEventDestroy(e);
@@ -854,6 +884,27 @@ int32_t sfmcov_cuda_compute_covariance(sfmcov_handle* h, const sfmcov_scene* sce
         Outputs out;
         out.d_cam_cov = dcov;
         out.diag = diag;
+        run(h, sc, M_FULL, out);
+        if (sc.n) SFM_CUDA(cudaMemcpyAsync(cam_cov, dcov, 8 * (size_t)P * P * sc.n, cudaMemcpyDeviceToHost, h->s));
+        SFM_CUDA(cudaStreamSynchronize(h->s));
+    });
+}
+
+int32_t sfmcov_cuda_compute_covariance_full(sfmcov_handle* h, const sfmcov_scene* scene, const sfmcov_options* opts,
+                                            double* cam_cov, double* point_cov, double* camera_matrix,
+                                            sfmcov_diagnostics* diag, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        const bool want_pc = opts && opts->point_covariances, want_cm = opts && opts->camera_cross_covariances;
+        if ((want_pc && !point_cov) || (want_cm && !camera_matrix))
+            throw ApiError{SFMCOV_ERR_DIMENSION, "options", "requested output buffer is null"};
+        const SceneDev sc = upload(h, scene);
+        const int P = sc.P;
+        double* dcov = h->cov.as<double>((size_t)P * P * sc.n);
+        Outputs out;
+        out.d_cam_cov = dcov;
+        out.diag = diag;
+        out.h_point_cov = want_pc ? point_cov : nullptr;
+        out.h_camera_matrix = want_cm ? camera_matrix : nullptr;
         run(h, sc, M_FULL, out);
         if (sc.n) SFM_CUDA(cudaMemcpyAsync(cam_cov, dcov, 8 * (size_t)P * P * sc.n, cudaMemcpyDeviceToHost, h->s));
         SFM_CUDA(cudaStreamSynchronize(h->s));

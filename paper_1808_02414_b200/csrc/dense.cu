@@ -41,7 +41,10 @@ struct Cfg {
     static constexpr int LDSB = BNT + PAD;   // N-contiguous B tile pitch
     static constexpr int LDB_K = BK + 4;     // K-major B tile pitch (conflict-free fragment reads)
     static constexpr int BSTAGE_N = BK * LDSB, BSTAGE_K = BNT * LDB_K;
-    static constexpr int SMEM = STAGES * (BK * LDS + (BSTAGE_N > BSTAGE_K ? BSTAGE_N : BSTAGE_K)) * 8;
+    static constexpr int ASTAGE_M = BK * LDS, ASTAGE_K = BM * LDB_K;  // A: M- or K-contiguous
+    static constexpr int BSTAGE = BSTAGE_N > BSTAGE_K ? BSTAGE_N : BSTAGE_K;
+    static constexpr int SMEM = STAGES * (ASTAGE_M + BSTAGE) * 8;     // A M-contiguous
+    static constexpr int SMEM_AK = STAGES * (ASTAGE_K + BSTAGE) * 8;  // A K-contiguous
 };
 }  // namespace gemm
 
@@ -68,15 +71,16 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // m0 + 2(lane&3) + {0,1} of column n0 + (lane>>2): 16-byte C accesses.
 // 8 HN warps of 32x32, STAGES-deep cp.async pipeline of BK-wide K chunks; the
 // grid enumerates 128 x 128 tiles x (2 / HN) column halves.
-template <bool BK_MAJOR, int BK, int STAGES, int HN>
+template <bool BK_MAJOR, int BK, int STAGES, int HN, bool AK_MAJOR = false>
 __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_gemm(GemmArgs g) {
     using namespace gemm;
     using CF = Cfg<BK, STAGES, HN>;
     constexpr int THREADS = CF::THREADS, BNT = CF::BNT, LDSB = CF::LDSB, LDB_K = CF::LDB_K;
     constexpr int NSUB = 2 / HN;
     extern __shared__ __align__(16) double smem[];
-    double* As = smem;                      // [STAGES][BK][LDS]
-    double* Bs = smem + STAGES * BK * LDS;  // [STAGES][BK][LDSB] or [STAGES][BNT][LDB_K]
+    constexpr int ASTAGE = AK_MAJOR ? CF::ASTAGE_K : CF::ASTAGE_M;
+    double* As = smem;                      // [STAGES][BK][LDS] or [STAGES][BM][LDB_K]
+    double* Bs = smem + STAGES * ASTAGE;    // [STAGES][BK][LDSB] or [STAGES][BNT][LDB_K]
     constexpr int BSTAGE = BK_MAJOR ? CF::BSTAGE_K : CF::BSTAGE_N;
     constexpr int CPTA = BK / (4 * HN);     // 16-byte copies per thread: A (BK x 128), B (BK x BNT)
     constexpr int CPTB = BK / 8;
@@ -108,12 +112,18 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
         B = g.B + (size_t)(gt - g.cyc_ab0) * BN + coff;  // (B row-indexed, not K-major)
         C = g.C + ((size_t)lt * BN + coff) * g.ldc + (size_t)gi * BM;
     } else {
-        A = g.A + (size_t)ti * BM;
+        A = AK_MAJOR ? g.A + (size_t)ti * BM * g.lda : g.A + (size_t)ti * BM;
         B = BK_MAJOR ? g.B + ((size_t)tj * BN + coff) * g.ldb : g.B + (size_t)tj * BN + coff;
         C = g.C + ((size_t)tj * BN + coff) * g.ldc + (size_t)ti * BM;
     }
     const int wm = warp & 3, wn = warp >> 2;  // 4 x (2 HN) warps of 32 x 32
     const int beta = (g.beta && !(g.beta0_from >= 0 && tj >= g.beta0_from)) ? 1 : 0;
+    int kbeg = 0;  // K offset of this tile
+    if (g.k_from_row) {
+        kbeg = ti * BM;
+        A = AK_MAJOR ? A + kbeg : A + (size_t)kbeg * g.lda;
+        B = BK_MAJOR ? B + kbeg : B + (size_t)kbeg * g.ldb;
+    }
 
     // per-thread copy sources / destinations (chunk 0); advance by BK per chunk
     const double* asrc[CPTA];
@@ -122,9 +132,15 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
 #pragma unroll
     for (int u = 0; u < CPTA; ++u) {
         const int idx = tid + THREADS * u;
-        const int k = idx >> 6, m2 = (idx & 63) * 2;
-        asrc[u] = A + (size_t)k * g.lda + m2;
-        adst[u] = k * LDS + m2;
+        if (AK_MAJOR) {
+            const int m = idx / (BK / 2), k2 = (idx % (BK / 2)) * 2;
+            asrc[u] = A + (size_t)m * g.lda + k2;
+            adst[u] = m * LDB_K + k2;
+        } else {
+            const int k = idx >> 6, m2 = (idx & 63) * 2;
+            asrc[u] = A + (size_t)k * g.lda + m2;
+            adst[u] = k * LDS + m2;
+        }
     }
 #pragma unroll
     for (int u = 0; u < CPTB; ++u) {
@@ -139,10 +155,10 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
             bdst[u] = k * LDSB + n2;
         }
     }
-    const size_t astep = (size_t)BK * g.lda;
+    const size_t astep = AK_MAJOR ? (size_t)BK : (size_t)BK * g.lda;
     const size_t bstep = BK_MAJOR ? (size_t)BK : (size_t)BK * g.ldb;
     auto load_stage = [&](int st, int kc) {
-        double* as = As + st * BK * LDS;
+        double* as = As + st * ASTAGE;
         double* bs = Bs + st * BSTAGE;
 #pragma unroll
         for (int u = 0; u < CPTA; ++u) cp_async16(as + adst[u], asrc[u] + kc * astep);
@@ -150,7 +166,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
         for (int u = 0; u < CPTB; ++u) cp_async16(bs + bdst[u], bsrc[u] + kc * bstep);
     };
 
-    const int NK = g.K / BK;
+    const int NK = (g.K - kbeg) / BK;
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
         if (st < NK) load_stage(st, st);
@@ -181,7 +197,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
         __syncthreads();
         if (kc + STAGES - 1 < NK) load_stage((kc + STAGES - 1) % STAGES, kc + STAGES - 1);
         cp_async_commit();
-        const double* as = As + (kc % STAGES) * BK * LDS;
+        const double* as = As + (kc % STAGES) * ASTAGE;
         const double* bs = Bs + (kc % STAGES) * BSTAGE;
 #pragma unroll
         for (int kk = 0; kk < BK / 4; ++kk) {
@@ -189,7 +205,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
             double af[4], bf[4];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi) {
-                af[mi] = as[krow * LDS + wm * 32 + mi * 8 + cq];
+                af[mi] = AK_MAJOR ? as[(wm * 32 + mi * 8 + cq) * LDB_K + krow] : as[krow * LDS + wm * 32 + mi * 8 + cq];
             }
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni)
@@ -269,7 +285,10 @@ template <int BK, int ST, int HN>
 static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) {
     using CF = gemm::Cfg<BK, ST, HN>;
     const unsigned grid = (unsigned)(tiles * (2 / HN));
-    if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST, HN>, grid, CF::THREADS, CF::SMEM, s, g);
+    if (g.a_kmajor) {
+        if (!g.b_kmajor) throw CudaError("gemm: K-major A needs K-major B");
+        launch_prio(k_gemm<true, BK, ST, HN, true>, grid, CF::THREADS, CF::SMEM_AK, s, g);
+    } else if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST, HN>, grid, CF::THREADS, CF::SMEM, s, g);
     else launch_prio(k_gemm<false, BK, ST, HN>, grid, CF::THREADS, CF::SMEM, s, g);
 }
 
@@ -288,6 +307,9 @@ template <bool KM, int BK, int ST, int HN>
 static void set_smem() {
     SFM_CUDA(cudaFuncSetAttribute(k_gemm<KM, BK, ST, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   gemm::Cfg<BK, ST, HN>::SMEM));
+    if (KM)
+        SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, BK, ST, HN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      gemm::Cfg<BK, ST, HN>::SMEM_AK));
 }
 
 // Opt-in shared-memory sizes, set once before any launch (and before graph

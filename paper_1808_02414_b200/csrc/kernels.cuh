@@ -97,6 +97,8 @@ struct GemmArgs {
     int lower_only;  // skip tiles strictly above the matrix diagonal
     int row_off_tiles, col_off_tiles;  // C tile offsets relative to the diagonal
     int whole_tile;  // C aliases A (in-place trsm): one CTA per 128-wide tile
+    int a_kmajor;    // A stored K-contiguous: (m, k) at A[m * lda + k]
+    int k_from_row;  // K range of tile (ti, tj) starts at ti * 128 (X^T X of a lower-triangular X)
     // Column-cyclic mode (cyc_R > 0, distributed sweep): C holds the local
     // columns of a rank owning panels rank, rank + R, ... of cyc_G tiles.
     // Grid tile (ti, tj) -> local column tile lt = tj + cyc_lt0, global
@@ -159,6 +161,24 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
                 cudaEvent_t eR);
 inline size_t sweep_ring_doubles(int Npad, int G, int NB) { return (size_t)NB * Npad * G * kNB; }
 inline size_t trtri_lp_doubles(int Npad, int G) { return (size_t)Npad * kNB * G + (size_t)kNB * kNB * G; }
+
+// ---- optional outputs (fullcov.cu) ------------------------------------------
+struct FullCovArgs {
+    int P, n, m, Npad;
+    const double* X;         // L^-1 (lower, in Z after the sweep), ld = Npad
+    double* Zi;              // Npad x Npad scratch -> Z_aug^-1 (full), then the camera matrix if cross
+    const double* G;         // N x 7
+    const double* LF;        // 7 x 7 lower, row-major
+    const double *Lpt, *V, *Wb, *s_a;
+    const int *off_pt, *idx_pt, *oc, *pos_cam;
+    double *part, *Y, *gtt_part, *Eb;  // scratch
+    double* point_cov;       // device m x 9, or null
+    int cross;               // camera blocks from Zi + scaled camera matrix in Zi
+    double* cam_cov;
+    int* psd;
+};
+void full_covariance(const FullCovArgs& a, cudaStream_t s);
+size_t full_cov_part_doubles(int N);
 
 // ---- column layouts and panel ownership (distributed path, dist.cu) ---------
 // Camera-aligned layout (cpb > 0): cpb = floor(kNB / P) cameras per 128-block,

@@ -145,6 +145,12 @@ class CovarianceDiagnostics:
 class CovarianceResult:
     camera_cov: np.ndarray  # (n, P, P)
     diagnostics: CovarianceDiagnostics
+    point_cov: Optional[np.ndarray] = None      # (m, 3, 3) when options.point_covariances
+    camera_matrix: Optional[np.ndarray] = None  # (P n, P n) when options.camera_cross_covariances
+
+    def cross_block(self, i: int, j: int) -> np.ndarray:
+        P = self.camera_cov.shape[1]
+        return self.camera_matrix[P * i:P * i + P, P * j:P * j + P]
 
 
 @dataclass
@@ -248,7 +254,7 @@ class Engine:
         return dict(zip(keys, [int(v) for v in buf]))
 
     # ---- pipeline -------------------------------------------------------------
-    def _covariance_call(self, fn, rec: Reconstruction, options: Optional[CovarianceOptions], *extra):
+    def _covariance_call(self, fn, rec: Reconstruction, options: Optional[CovarianceOptions], *extra, reorder=False):
         options = options or CovarianceOptions()
         P, n = rec.cam_params, rec.num_cameras()
         out = np.empty((n, P, P))
@@ -259,7 +265,10 @@ class Engine:
         opts = N.Options(options.threads, int(options.point_covariances), int(options.camera_cross_covariances), 0)
         err = N.ErrorStruct()
         sc = rec.c_struct()
-        code = fn(self._h, C.byref(sc), C.byref(opts), *extra, out.ctypes.data, C.byref(diag), C.byref(err))
+        if reorder:  # (h, scene, opts, cam_cov, *extra outputs, diag, err)
+            code = fn(self._h, C.byref(sc), C.byref(opts), out.ctypes.data, *extra, C.byref(diag), C.byref(err))
+        else:
+            code = fn(self._h, C.byref(sc), C.byref(opts), *extra, out.ctypes.data, C.byref(diag), C.byref(err))
         _raise(code, err)
         d = CovarianceDiagnostics(diag.scale_min, diag.scale_max, [int(v) for v in flagged[:diag.n_flagged]],
                                   diag.min_pivot, diag.max_pivot, diag.inertia_positive, diag.inertia_negative,
@@ -268,7 +277,17 @@ class Engine:
 
     # ---- pipeline -------------------------------------------------------------
     def compute_covariance(self, rec: Reconstruction, options: Optional[CovarianceOptions] = None) -> CovarianceResult:
-        return self._covariance_call(self._lib.sfmcov_cuda_compute_covariance, rec, options)
+        options = options or CovarianceOptions()
+        if not (options.point_covariances or options.camera_cross_covariances):
+            return self._covariance_call(self._lib.sfmcov_cuda_compute_covariance, rec, options)
+        P, n, m = rec.cam_params, rec.num_cameras(), rec.num_points()
+        pc = np.empty((m, 3, 3)) if options.point_covariances else None
+        cm = np.empty((P * n, P * n), order="F") if options.camera_cross_covariances else None
+        res = self._covariance_call(self._lib.sfmcov_cuda_compute_covariance_full, rec, options,
+                                    None if pc is None else pc.ctypes.data, None if cm is None else cm.ctypes.data,
+                                    reorder=True)
+        res.point_cov, res.camera_matrix = pc, cm
+        return res
 
     # ---- multi-GPU -------------------------------------------------------------
     def comm_init(self, unique_id: bytes, nranks: int, rank: int):

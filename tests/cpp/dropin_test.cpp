@@ -58,6 +58,16 @@ int main() {
             for (int q = 0; q < 8; ++q) CHECK(std::fabs(c[8 * p + q] - c[8 * q + p]) <= 1e-14 * mx);
         }
     }
+    // optional outputs (test_covariance.cpp:42-68 shape): point blocks, full camera matrix whose
+    // diagonal blocks are the camera blocks bitwise
+    CovarianceOptions opts;
+    opts.point_covariances = true;
+    opts.camera_cross_covariances = true;
+    const CovarianceResult full = compute_covariance(rec, opts);
+    CHECK(full.point_cov.size() == (size_t)rec.num_points());
+    CHECK(full.camera_matrix_rows == 48);
+    for (Index i = 0; i < 6; ++i) CHECK(full.cross_block(i, i) == full.camera_cov[i]);
+    for (const Mat3& pc : full.point_cov) CHECK(pc[0] > 0.0 && pc[4] > 0.0 && pc[8] > 0.0);
     // errors keep the reference's kind / stage / message fragments
     Reconstruction bad = rec;
     bad.cameras[1].c = -1.0;

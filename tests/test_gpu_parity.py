@@ -288,11 +288,46 @@ def test_count_floor_messages(engine):
     assert str(e.value) == str(eo.value)
 
 
-def test_options_not_yet_supported_are_refused(engine):
+@pytest.mark.parametrize("name", ["cube_p8", "cube_p9", "ring_p9", "config1", "config2"])
+def test_point_and_cross_covariances_match_restatement(engine, name):  # covariance.cpp:283-348
+    rec = SMALL[name]()
+    cov, pc, cm, _ = O.compute_covariance_full(rec)
+    res = engine.compute_covariance(rec, F.CovarianceOptions(point_covariances=True, camera_cross_covariances=True))
+    n, P = rec.num_cameras(), rec.cam_params
+    assert worst_block(res.camera_cov, cov) <= COV_TOL
+    assert res.point_cov.shape == pc.shape
+    assert worst_block(res.point_cov, pc) <= COV_TOL
+    assert res.camera_matrix.shape == (P * n, P * n)
+    assert rel(res.camera_matrix, cm) <= COV_TOL
+    for i in range(n):  # test_covariance.cpp:62-66: the diagonal cross blocks are the camera blocks, bitwise
+        assert np.array_equal(res.cross_block(i, i), res.camera_cov[i])
+    step = max(1, n // 7)
+    for i in range(0, n, step):
+        for l in range(0, n, step):
+            assert rel(res.cross_block(i, l), cm[P * i:P * i + P, P * l:P * l + P]) <= COV_TOL
+
+
+def test_point_covariances_alone(engine):
+    rec = SMALL["ring_p9"]()
+    _, pc, _, _ = O.compute_covariance_full(rec, camera_cross_covariances=False)
+    res = engine.compute_covariance(rec, F.CovarianceOptions(point_covariances=True))
+    assert res.camera_matrix is None and worst_block(res.point_cov, pc) <= COV_TOL
+    base = engine.compute_covariance(rec)
+    assert np.array_equal(res.camera_cov, base.camera_cov)  # camera blocks unchanged by the option
+
+
+def test_optional_outputs_need_the_full_entry_point(engine):
+    import ctypes as C
+    from paper_1808_02414_b200 import _native as N
     rec = S.generate_cube_scene(1, 0.5)
-    with pytest.raises(F.Error) as e:
-        engine.compute_covariance(rec, F.CovarianceOptions(point_covariances=True))
-    assert e.value.kind == F.ErrorKind.dimension
+    sc, opts, diag, err = rec.c_struct(), N.Options(0, 1, 0, 0), N.Diagnostics(), N.ErrorStruct()
+    out = np.empty((rec.num_cameras(), rec.cam_params, rec.cam_params))
+    code = N.cuda_lib().sfmcov_cuda_compute_covariance(engine.handle, C.byref(sc), C.byref(opts), out.ctypes.data,
+                                                       C.byref(diag), C.byref(err))
+    assert code == F.ErrorKind.dimension and b"full" in err.message
+    code = N.cuda_lib().sfmcov_cuda_compute_covariance_full(engine.handle, C.byref(sc), C.byref(opts),
+                                                            out.ctypes.data, None, None, C.byref(diag), C.byref(err))
+    assert code == F.ErrorKind.dimension  # requested buffer missing
 
 
 def test_empty_reconstruction_is_rejected(engine):  # test_covariance.cpp:131-135

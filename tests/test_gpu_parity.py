@@ -348,3 +348,14 @@ def test_cpp_dropin_header():
     block0 = np.array([float(v) for v in lines[-2].split()]).reshape(8, 8)
     cov, *_ = O.compute_covariance(S.generate_cube_scene(1, 0.5))
     assert rel(block0, cov[0]) <= COV_TOL
+
+
+def test_config3_point_and_cross_covariances(engine):
+    """Optional outputs on BASELINE config 3 against the restatement."""
+    rec = S.generate_config(3)
+    O.lib().oracle_blas_threads(0)
+    cov, pc, cm, _ = O.compute_covariance_full(rec, threads=16)
+    res = engine.compute_covariance(rec, F.CovarianceOptions(point_covariances=True, camera_cross_covariances=True))
+    assert worst_block(res.camera_cov, cov) <= COV_TOL
+    assert worst_block(res.point_cov, pc) <= COV_TOL
+    assert rel(res.camera_matrix, cm) <= COV_TOL

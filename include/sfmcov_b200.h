@@ -101,6 +101,8 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err);
 void sfmcov_cuda_destroy(sfmcov_handle* h);
 /* The handle's CUDA stream (cudaStream_t) for callers that time or order work. */
 void* sfmcov_cuda_stream(sfmcov_handle* h);
+/* The handle's device ordinal. */
+int32_t sfmcov_cuda_device(sfmcov_handle* h);
 
 /* ---- full pipeline --------------------------------------------------------
  * Replaces sfmcov::compute_covariance (include/sfmcov/covariance.hpp:110-111,
@@ -212,6 +214,36 @@ const char* sfmcov_cuda_stage_name(int32_t i);
 int32_t sfmcov_cuda_last_counts(sfmcov_handle* h, int64_t* counts, int32_t capacity);
 /* Enable/disable per-stage event timing (off by default; adds syncs). */
 void sfmcov_cuda_set_profiling(sfmcov_handle* h, int32_t on);
+
+/* ---- sub-reconstructions (include/sfmcov/subrec.hpp, src/subrec.cpp) -----
+ * Host planner with the reference's semantics and random draws, and the
+ * batch of independent sub-scene covariances on the GPU (`workers` CUDA
+ * handles of the handle's device in flight). */
+/* build_view_graph: CSR over cameras (off n+1; neighbor / weight entries,
+ * ascending neighbor); n_entries = 2 x #edges (written up to capacity). */
+int32_t sfmcov_view_graph(const sfmcov_scene* scene, int32_t min_covis, int64_t* off, int32_t* nbr,
+                          int32_t* weight, int64_t capacity, int64_t* n_entries, sfmcov_error* err);
+/* extract_neighborhood: ascending global camera / point ids of the induced
+ * sub-reconstruction (buffers of n_cams / n_pts capacity). */
+int32_t sfmcov_extract_neighborhood(const sfmcov_scene* scene, int64_t center, int32_t k_bar, int32_t* cams,
+                                    int64_t* n_cams, int32_t* pts, int64_t* n_pts, int32_t* truncated,
+                                    sfmcov_error* err);
+/* plan_coverage: subset s has cameras cams[subset_off[s] .. subset_off[s+1]). */
+int32_t sfmcov_plan_coverage(const sfmcov_scene* scene, int32_t k_bar, uint64_t seed, int64_t* subset_off,
+                             int64_t subset_capacity, int32_t* cams, int64_t cams_capacity, int64_t* n_subsets,
+                             sfmcov_error* err);
+/* approximate_covariances: per camera the kept block (n x P x P), its trace
+ * and the producing subset id. */
+int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene* scene, int32_t k_bar,
+                                            int32_t n_decompositions, uint64_t seed, int32_t workers,
+                                            double* cam_cov, double* trace, int32_t* subset_id,
+                                            sfmcov_error* err);
+/* monotonicity_check on the sub-reconstructions induced by two nested camera sets. */
+int32_t sfmcov_cuda_monotonicity_check(sfmcov_handle* h, const sfmcov_scene* scene, const int32_t* small_cams,
+                                       int64_t n_small, const int32_t* large_cams, int64_t n_large,
+                                       double rel_tol, int32_t* violation_cams, double* trace_small,
+                                       double* trace_large, int64_t* n_violations, int64_t* cameras_checked,
+                                       sfmcov_error* err);
 
 /* ---- synthetic scenes (host only; harness, not the hot path) ------------
  * generate_cube_scene / generate_random_scene / transform_scene

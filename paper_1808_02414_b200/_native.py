@@ -124,6 +124,19 @@ CUDA_SYMBOLS = {
     "sfmcov_plan_dense": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, c_int64_p, c_int64_p,
                                       C.c_void_p]),
     "sfmcov_plan_chunks": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, c_int64_p, c_int64_p]),
+    "sfmcov_cuda_device": (C.c_int32, [C.c_void_p]),
+    "sfmcov_view_graph": (C.c_int32, [C.POINTER(Scene), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                      c_int64_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_extract_neighborhood": (C.c_int32, [C.POINTER(Scene), C.c_int64, C.c_int32, C.c_void_p, c_int64_p,
+                                                C.c_void_p, c_int64_p, c_int32_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_plan_coverage": (C.c_int32, [C.POINTER(Scene), C.c_int32, C.c_uint64, C.c_void_p, C.c_int64, C.c_void_p,
+                                         C.c_int64, c_int64_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_approximate_covariances": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_int32, C.c_int32, C.c_uint64,
+                                                        C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                        C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_monotonicity_check": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_void_p, C.c_int64, C.c_void_p,
+                                                   C.c_int64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                   c_int64_p, c_int64_p, C.POINTER(ErrorStruct)]),
 }
 
 SYNTH_SYMBOLS = {

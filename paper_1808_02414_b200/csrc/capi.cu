@@ -870,6 +870,8 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
 
 void* sfmcov_cuda_stream(sfmcov_handle* h) { return h ? (void*)h->s : nullptr; }
 
+int32_t sfmcov_cuda_device(sfmcov_handle* h) { return h ? h->device : -1; }
+
 void sfmcov_cuda_set_profiling(sfmcov_handle* h, int32_t on) {
     if (h) h->profiling = on != 0;
 }

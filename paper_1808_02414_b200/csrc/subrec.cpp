@@ -1,0 +1,442 @@
+// Sub-reconstruction covariances (reference include/sfmcov/subrec.hpp,
+// src/subrec.cpp): view graph, greedy neighborhoods, seeded coverings, and
+// the per-camera aggregation over many independent sub-scene covariances.
+//
+// The planner is host logic (same algorithm, same std::mt19937_64 /
+// uniform_int_distribution draws as the reference, so plans are identical).
+// The B200 part is the batch: every sub-scene is an independent
+// compute_covariance; a pool of worker threads, each with its own CUDA handle
+// (stream, workspace), keeps several of them in flight on the device, and the
+// results are aggregated in subset order afterwards (deterministic:
+// smallest trace wins, earliest subset on ties, as in the reference).
+
+#include "sfmcov_b200.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+namespace {
+
+struct SubError {
+    int32_t kind;
+    std::string stage, message;  // message without the "stage: " prefix
+};
+
+void set_error(sfmcov_error* e, const SubError& x) {
+    if (!e) return;
+    e->kind = x.kind;
+    std::snprintf(e->stage, sizeof e->stage, "%s", x.stage.c_str());
+    std::snprintf(e->message, sizeof e->message, "%s: %s", x.stage.c_str(), x.message.c_str());
+}
+
+void clear(sfmcov_error* e) {
+    if (!e) return;
+    e->kind = 0;
+    e->stage[0] = 0;
+    e->message[0] = 0;
+}
+
+// Host copy of a scene (SoA, the C ABI layout).
+struct HostScene {
+    int32_t n = 0, m = 0, t = 0, P = 8;
+    std::vector<double> cams, pts, u, sigma;
+    std::vector<int32_t> oc, op;
+    bool has_u = false, has_sigma = false;
+    sfmcov_scene view() const {
+        return sfmcov_scene{n, m, t, P, cams.data(), pts.data(), oc.data(), op.data(),
+                            has_u ? u.data() : nullptr, has_sigma ? sigma.data() : nullptr};
+    }
+};
+
+struct Graph {
+    int64_t n = 0;
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> edges;  // (neighbor, weight), sorted
+};
+
+// build_view_graph (src/subrec.cpp:90-116): points' observers sorted, every
+// pair counted; edges below min_covis dropped.
+Graph view_graph(const sfmcov_scene& s, int min_covis) {
+    std::vector<int64_t> off(s.n_pts + 1, 0);
+    for (int32_t k = 0; k < s.n_obs; ++k) ++off[s.obs_pt[k] + 1];
+    for (int32_t j = 0; j < s.n_pts; ++j) off[j + 1] += off[j];
+    std::vector<int32_t> by_pt(s.n_obs), fill(off.begin(), off.end() - 1);
+    for (int32_t k = 0; k < s.n_obs; ++k) by_pt[fill[s.obs_pt[k]]++] = k;
+    std::unordered_map<uint64_t, int32_t> counts;
+    std::vector<int32_t> obs;
+    for (int32_t j = 0; j < s.n_pts; ++j) {
+        obs.clear();
+        for (int64_t k = off[j]; k < off[j + 1]; ++k) obs.push_back(s.obs_cam[by_pt[k]]);
+        std::sort(obs.begin(), obs.end());
+        for (size_t a = 0; a < obs.size(); ++a)
+            for (size_t b = a + 1; b < obs.size(); ++b)
+                ++counts[(uint64_t(uint32_t(obs[a])) << 32) | uint32_t(obs[b])];
+    }
+    Graph g;
+    g.n = s.n_cams;
+    g.edges.resize(s.n_cams);
+    for (const auto& [key, w] : counts) {
+        if (w < min_covis) continue;
+        const int32_t a = int32_t(key >> 32), b = int32_t(key & 0xffffffffu);
+        g.edges[a].emplace_back(b, w);
+        g.edges[b].emplace_back(a, w);
+    }
+    for (auto& adj : g.edges) std::sort(adj.begin(), adj.end());
+    return g;
+}
+
+struct Sub {
+    std::vector<int32_t> cams, pts;
+    HostScene scene;
+    bool truncated = false;
+};
+
+// induced_scene (src/subrec.cpp:24-86): points seen by >= 2 subset cameras,
+// cameras with >= 4 surviving observations, to a fixpoint.
+Sub induced(const sfmcov_scene& s, const std::vector<int32_t>& cams, bool truncated) {
+    const int64_t n = s.n_cams, m = s.n_pts;
+    std::vector<char> cam_in(n, 0), pt_in(m, 0);
+    for (int32_t c : cams) cam_in[c] = 1;
+    std::vector<int32_t> cand;
+    for (int32_t t = 0; t < s.n_obs; ++t)
+        if (cam_in[s.obs_cam[t]]) cand.push_back(t);
+    std::vector<int32_t> pc(m), cc(n);
+    for (bool changed = true; changed;) {
+        std::fill(pc.begin(), pc.end(), 0);
+        for (int32_t t : cand)
+            if (cam_in[s.obs_cam[t]]) ++pc[s.obs_pt[t]];
+        for (int64_t j = 0; j < m; ++j) pt_in[j] = pc[j] >= 2;
+        std::fill(cc.begin(), cc.end(), 0);
+        for (int32_t t : cand)
+            if (cam_in[s.obs_cam[t]] && pt_in[s.obs_pt[t]]) ++cc[s.obs_cam[t]];
+        changed = false;
+        for (int64_t i = 0; i < n; ++i)
+            if (cam_in[i] && cc[i] < 4) {
+                cam_in[i] = 0;
+                changed = true;
+            }
+    }
+    Sub sub;
+    sub.truncated = truncated;
+    const int P = s.cam_params;
+    HostScene& h = sub.scene;
+    h.P = P;
+    h.has_u = s.obs_u != nullptr;
+    h.has_sigma = s.obs_sigma != nullptr;
+    std::vector<int32_t> cl(n, -1), pl(m, -1);
+    for (int64_t i = 0; i < n; ++i)
+        if (cam_in[i]) {
+            cl[i] = (int32_t)sub.cams.size();
+            sub.cams.push_back((int32_t)i);
+            h.cams.insert(h.cams.end(), s.cams + P * i, s.cams + P * i + P);
+        }
+    if (sub.cams.empty()) throw SubError{SFMCOV_ERR_DEGENERATE, "subrec", "induced sub-reconstruction is empty"};
+    for (int64_t j = 0; j < m; ++j)
+        if (pt_in[j]) {
+            pl[j] = (int32_t)sub.pts.size();
+            sub.pts.push_back((int32_t)j);
+            h.pts.insert(h.pts.end(), s.pts + 3 * j, s.pts + 3 * j + 3);
+        }
+    for (int32_t t : cand) {
+        if (!cam_in[s.obs_cam[t]] || !pt_in[s.obs_pt[t]]) continue;
+        h.oc.push_back(cl[s.obs_cam[t]]);
+        h.op.push_back(pl[s.obs_pt[t]]);
+        if (h.has_u) h.u.insert(h.u.end(), s.obs_u + 2 * size_t(t), s.obs_u + 2 * size_t(t) + 2);
+        if (h.has_sigma) h.sigma.insert(h.sigma.end(), s.obs_sigma + 4 * size_t(t), s.obs_sigma + 4 * size_t(t) + 4);
+    }
+    h.n = (int32_t)sub.cams.size();
+    h.m = (int32_t)sub.pts.size();
+    h.t = (int32_t)h.oc.size();
+    return sub;
+}
+
+// extract_neighborhood (src/subrec.cpp:118-152)
+Sub neighborhood(const sfmcov_scene& s, const Graph& g, int64_t center, int k_bar) {
+    const int64_t n = s.n_cams;
+    if (k_bar < 2) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "subset size must be at least 2"};
+    if (center < 0 || center >= n || g.n != n)
+        throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "center camera or view graph out of range"};
+    std::vector<char> in(n, 0);
+    std::vector<int64_t> weight(n, 0);
+    std::vector<int32_t> chosen{(int32_t)center};
+    in[center] = 1;
+    for (const auto& [nb, w] : g.edges[center]) weight[nb] += w;
+    bool truncated = false;
+    while ((int)chosen.size() < k_bar) {
+        int64_t best = -1, best_w = 0;
+        for (int64_t i = 0; i < n; ++i)
+            if (!in[i] && weight[i] > best_w) {
+                best_w = weight[i];
+                best = i;
+            }
+        if (best < 0) {
+            truncated = true;
+            break;
+        }
+        chosen.push_back((int32_t)best);
+        in[best] = 1;
+        for (const auto& [nb, w] : g.edges[best])
+            if (!in[nb]) weight[nb] += w;
+    }
+    std::sort(chosen.begin(), chosen.end());
+    return induced(s, chosen, truncated);
+}
+
+// plan_coverage (src/subrec.cpp:154-181)
+std::vector<Sub> coverage(const sfmcov_scene& s, const Graph& g, int k_bar, uint64_t seed) {
+    const int64_t n = s.n_cams;
+    std::vector<Sub> plan;
+    std::mt19937_64 rng(seed);
+    std::vector<char> covered(n, 0);
+    int64_t remaining = n;
+    std::vector<int64_t> pool;
+    while (remaining > 0) {
+        pool.clear();
+        for (int64_t i = 0; i < n; ++i)
+            if (!covered[i]) pool.push_back(i);
+        const int64_t center = pool[std::uniform_int_distribution<std::size_t>(0, pool.size() - 1)(rng)];
+        Sub sub = neighborhood(s, g, center, k_bar);
+        if (!std::binary_search(sub.cams.begin(), sub.cams.end(), (int32_t)center))
+            throw SubError{SFMCOV_ERR_DEGENERATE, "subrec",
+                           "camera " + std::to_string(center) + " cannot anchor a sub-reconstruction of size " +
+                               std::to_string(k_bar)};
+        for (int32_t c : sub.cams)
+            if (!covered[c]) {
+                covered[c] = 1;
+                --remaining;
+            }
+        plan.push_back(std::move(sub));
+    }
+    return plan;
+}
+
+void check_scene(const sfmcov_scene* s) {
+    if (!s || s->n_cams < 0 || s->n_pts < 0 || s->n_obs < 0 || (s->cam_params != 8 && s->cam_params != 9))
+        throw SubError{SFMCOV_ERR_DIMENSION, "subrec", "bad scene"};
+    for (int32_t k = 0; k < s->n_obs; ++k)
+        if (s->obs_cam[k] < 0 || s->obs_cam[k] >= s->n_cams || s->obs_pt[k] < 0 || s->obs_pt[k] >= s->n_pts)
+            throw SubError{SFMCOV_ERR_INVARIANT, "validate",
+                           "observation " + std::to_string(k) + " index out of range"};
+}
+
+// The covariance of every sub-scene, on `workers` handles of `device`.
+struct SubResult {
+    std::vector<double> cov;
+    int32_t code = 0;
+    sfmcov_error err{};
+};
+
+std::vector<SubResult> batch_covariances(sfmcov_handle* h0, int device, const std::vector<const Sub*>& subs,
+                                         int workers) {
+    std::vector<SubResult> res(subs.size());
+    std::atomic<size_t> next{0};
+    auto work = [&](sfmcov_handle* h) {
+        for (size_t i = next++; i < subs.size(); i = next++) {
+            const Sub& sb = *subs[i];
+            const sfmcov_scene v = sb.scene.view();
+            res[i].cov.resize((size_t)v.n_cams * v.cam_params * v.cam_params);
+            sfmcov_options o{0, 0, 0, 0};
+            res[i].code = sfmcov_cuda_compute_covariance(h, &v, &o, res[i].cov.data(), nullptr, &res[i].err);
+        }
+    };
+    workers = std::max(1, std::min<int>(workers, (int)subs.size()));
+    std::vector<sfmcov_handle*> hs{h0};
+    for (int w = 1; w < workers; ++w) {
+        sfmcov_error e{};
+        sfmcov_handle* h = sfmcov_cuda_create(device, &e);
+        if (!h) break;
+        hs.push_back(h);
+    }
+    std::vector<std::thread> th;
+    for (size_t w = 1; w < hs.size(); ++w) th.emplace_back(work, hs[w]);
+    work(hs[0]);
+    for (auto& t : th) t.join();
+    for (size_t w = 1; w < hs.size(); ++w) sfmcov_cuda_destroy(hs[w]);
+    return res;
+}
+
+double trace_of(const double* c, int P) {
+    double tr = 0.0;
+    for (int p = 0; p < P; ++p) tr += c[P * p + p];
+    return tr;
+}
+
+template <class F>
+int32_t guarded(sfmcov_error* err, F&& body) {
+    try {
+        body();
+        clear(err);
+        return SFMCOV_OK;
+    } catch (const SubError& x) {
+        set_error(err, x);
+        return x.kind;
+    } catch (const std::exception& x) {
+        set_error(err, SubError{SFMCOV_ERR_DEVICE, "subrec", x.what()});
+        return SFMCOV_ERR_DEVICE;
+    }
+}
+
+// "stage: message" -> message
+std::string strip_stage(const sfmcov_error& e) {
+    const std::string full = e.message;
+    const std::string pre = std::string(e.stage) + ": ";
+    return full.compare(0, pre.size(), pre) == 0 ? full.substr(pre.size()) : full;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t sfmcov_view_graph(const sfmcov_scene* scene, int32_t min_covis, int64_t* off, int32_t* nbr, int32_t* weight,
+                          int64_t capacity, int64_t* n_entries, sfmcov_error* err) {
+    return guarded(err, [&] {
+        check_scene(scene);
+        const Graph g = view_graph(*scene, min_covis);
+        int64_t k = 0;
+        off[0] = 0;
+        for (int64_t i = 0; i < g.n; ++i) {
+            for (const auto& [b, w] : g.edges[i]) {
+                if (k < capacity) { nbr[k] = b; weight[k] = w; }
+                ++k;
+            }
+            off[i + 1] = k;
+        }
+        *n_entries = k;
+    });
+}
+
+int32_t sfmcov_extract_neighborhood(const sfmcov_scene* scene, int64_t center, int32_t k_bar, int32_t* cams,
+                                    int64_t* n_cams, int32_t* pts, int64_t* n_pts, int32_t* truncated,
+                                    sfmcov_error* err) {
+    return guarded(err, [&] {
+        check_scene(scene);
+        const Graph g = view_graph(*scene, 1);
+        const Sub sub = neighborhood(*scene, g, center, k_bar);
+        std::copy(sub.cams.begin(), sub.cams.end(), cams);
+        std::copy(sub.pts.begin(), sub.pts.end(), pts);
+        *n_cams = (int64_t)sub.cams.size();
+        *n_pts = (int64_t)sub.pts.size();
+        *truncated = sub.truncated ? 1 : 0;
+    });
+}
+
+int32_t sfmcov_plan_coverage(const sfmcov_scene* scene, int32_t k_bar, uint64_t seed, int64_t* subset_off,
+                             int64_t subset_capacity, int32_t* cams, int64_t cams_capacity, int64_t* n_subsets,
+                             sfmcov_error* err) {
+    return guarded(err, [&] {
+        check_scene(scene);
+        const Graph g = view_graph(*scene, 1);
+        const std::vector<Sub> plan = coverage(*scene, g, k_bar, seed);
+        int64_t k = 0;
+        subset_off[0] = 0;
+        for (size_t i = 0; i < plan.size(); ++i) {
+            for (int32_t c : plan[i].cams) {
+                if (k < cams_capacity) cams[k] = c;
+                ++k;
+            }
+            if ((int64_t)i + 1 < subset_capacity + 1) subset_off[i + 1] = k;
+        }
+        *n_subsets = (int64_t)plan.size();
+    });
+}
+
+int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene* scene, int32_t k_bar,
+                                            int32_t n_decompositions, uint64_t seed, int32_t workers,
+                                            double* cam_cov, double* trace, int32_t* subset_id, sfmcov_error* err) {
+    return guarded(err, [&] {
+        if (k_bar < 2) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "subset size must be at least 2"};
+        if (n_decompositions < 1) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "need at least one decomposition"};
+        check_scene(scene);
+        const int P = scene->cam_params;
+        const Graph g = view_graph(*scene, 1);
+        std::vector<std::vector<Sub>> plans;
+        std::vector<const Sub*> flat;
+        std::vector<int> deco;
+        for (int d = 0; d < n_decompositions; ++d) plans.push_back(coverage(*scene, g, k_bar, seed + uint64_t(d)));
+        for (int d = 0; d < n_decompositions; ++d)
+            for (const Sub& sb : plans[d]) {
+                flat.push_back(&sb);
+                deco.push_back(d);
+            }
+        const std::vector<SubResult> res =
+            batch_covariances(h, sfmcov_cuda_device(h), flat, std::max(1, (int)workers));
+        const int64_t n = scene->n_cams;
+        std::vector<char> seen(n, 0);
+        for (size_t sid = 0; sid < flat.size(); ++sid) {
+            if (res[sid].code) {
+                const int kind = res[sid].code;
+                throw SubError{kind, "subrec",
+                               "subset " + std::to_string(sid) + " (decomposition " + std::to_string(deco[sid]) +
+                                   "): " + std::string(res[sid].err.message)};
+            }
+            const Sub& sb = *flat[sid];
+            for (size_t l = 0; l < sb.cams.size(); ++l) {
+                const int32_t gc = sb.cams[l];
+                const double* c = &res[sid].cov[(size_t)P * P * l];
+                const double tr = trace_of(c, P);
+                if (!seen[gc] || tr < trace[gc]) {
+                    seen[gc] = 1;
+                    std::memcpy(cam_cov + (size_t)P * P * gc, c, 8 * (size_t)P * P);
+                    trace[gc] = tr;
+                    subset_id[gc] = (int32_t)sid;
+                }
+            }
+        }
+        for (int64_t i = 0; i < n; ++i)
+            if (!seen[i])
+                throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "camera " + std::to_string(i) + " was not covered by any subset"};
+    });
+}
+
+int32_t sfmcov_cuda_monotonicity_check(sfmcov_handle* h, const sfmcov_scene* scene, const int32_t* small_cams,
+                                       int64_t n_small, const int32_t* large_cams, int64_t n_large, double rel_tol,
+                                       int32_t* violation_cams, double* trace_small, double* trace_large,
+                                       int64_t* n_violations, int64_t* cameras_checked, sfmcov_error* err) {
+    return guarded(err, [&] {
+        check_scene(scene);
+        std::vector<int32_t> sc(small_cams, small_cams + n_small), lc(large_cams, large_cams + n_large);
+        for (int32_t c : sc) {
+            if (c < 0 || c >= scene->n_cams) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "subset camera id out of range"};
+            if (!std::binary_search(lc.begin(), lc.end(), c))
+                throw SubError{SFMCOV_ERR_INVARIANT, "subrec",
+                               "subsets are not nested: camera " + std::to_string(c) + " is missing from the larger subset"};
+        }
+        const Sub s_small = induced(*scene, sc, false), s_large = induced(*scene, lc, false);
+        const int P = scene->cam_params;
+        std::vector<double> cs((size_t)P * P * s_small.cams.size()), cl((size_t)P * P * s_large.cams.size());
+        sfmcov_options o{0, 0, 0, 0};
+        sfmcov_error e{};
+        const sfmcov_scene vs = s_small.scene.view(), vl = s_large.scene.view();
+        if (int32_t c = sfmcov_cuda_compute_covariance(h, &vs, &o, cs.data(), nullptr, &e))
+            throw SubError{c, e.stage, strip_stage(e)};
+        if (int32_t c = sfmcov_cuda_compute_covariance(h, &vl, &o, cl.data(), nullptr, &e))
+            throw SubError{c, e.stage, strip_stage(e)};
+        int64_t nv = 0, checked = 0;
+        for (size_t l = 0; l < s_small.cams.size(); ++l) {
+            const int32_t gcam = s_small.cams[l];
+            const size_t pos = std::lower_bound(s_large.cams.begin(), s_large.cams.end(), gcam) - s_large.cams.begin();
+            const double ts = trace_of(&cs[(size_t)P * P * l], P), tl = trace_of(&cl[(size_t)P * P * pos], P);
+            ++checked;
+            if (ts < tl - rel_tol * std::abs(tl)) {
+                violation_cams[nv] = gcam;
+                trace_small[nv] = ts;
+                trace_large[nv] = tl;
+                ++nv;
+            }
+        }
+        *n_violations = nv;
+        *cameras_checked = checked;
+    });
+}
+
+}  // extern "C"

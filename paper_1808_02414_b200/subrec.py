@@ -1,0 +1,128 @@
+"""Sub-reconstruction covariances (reference include/sfmcov/subrec.hpp):
+view graph, greedy neighborhoods, seeded coverings and the per-camera
+aggregation of many independent sub-scene covariances, batched on the GPU.
+Thin wrappers over the C ABI (csrc/subrec.cpp)."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .sfmcov import Engine, Error, Reconstruction, _raise, default_engine
+
+
+@dataclass
+class ViewGraph:
+    n_cams: int
+    edges: List[List[Tuple[int, int]]]  # per camera: (neighbor, weight), ascending neighbor
+
+
+@dataclass
+class SubScene:
+    cameras: np.ndarray  # ascending global ids
+    points: np.ndarray
+    scene: Reconstruction
+    component_truncated: bool
+
+
+@dataclass
+class AggregatedCovariance:
+    target_size: int
+    cov: np.ndarray       # (n, P, P): the kept block per camera
+    trace: np.ndarray     # (n,)
+    subset_id: np.ndarray  # (n,)
+
+
+@dataclass
+class MonotonicityReport:
+    violations: List[Tuple[int, float, float]]  # (camera, trace_small, trace_large)
+    cameras_checked: int
+
+
+def build_view_graph(rec: Reconstruction, min_covis: int = 1) -> ViewGraph:
+    n, t = rec.num_cameras(), rec.num_observations()
+    cap = max(1, 2 * t * 20)
+    off = np.zeros(n + 1, np.int64)
+    nbr = np.zeros(cap, np.int32)
+    w = np.zeros(cap, np.int32)
+    cnt = C.c_int64()
+    err = N.ErrorStruct()
+    sc = rec.c_struct()
+    _raise(N.cuda_lib().sfmcov_view_graph(C.byref(sc), min_covis, off.ctypes.data, nbr.ctypes.data, w.ctypes.data,
+                                          cap, C.byref(cnt), C.byref(err)), err)
+    if cnt.value > cap:
+        raise Error(5, "subrec", "view graph larger than the buffer")
+    return ViewGraph(n, [[(int(nbr[k]), int(w[k])) for k in range(off[i], off[i + 1])] for i in range(n)])
+
+
+def induced_scene(rec: Reconstruction, cameras: np.ndarray, points: np.ndarray) -> Reconstruction:
+    """The sub-reconstruction on the given (already filtered) camera / point ids."""
+    cl = -np.ones(rec.num_cameras(), np.int64)
+    pl = -np.ones(rec.num_points(), np.int64)
+    cl[cameras] = np.arange(len(cameras))
+    pl[points] = np.arange(len(points))
+    keep = (cl[rec.obs_cam] >= 0) & (pl[rec.obs_pt] >= 0)
+    return Reconstruction(rec.cams[cameras].copy(), rec.pts[points].copy(), cl[rec.obs_cam[keep]].astype(np.int32),
+                          pl[rec.obs_pt[keep]].astype(np.int32),
+                          None if rec.obs_u is None else rec.obs_u[keep].copy(),
+                          None if rec.obs_sigma is None else rec.obs_sigma[keep].copy())
+
+
+def extract_neighborhood(rec: Reconstruction, center: int, k_bar: int) -> SubScene:
+    n, m = rec.num_cameras(), rec.num_points()
+    cams = np.zeros(max(1, n), np.int32)
+    pts = np.zeros(max(1, m), np.int32)
+    nc, npt, tr = C.c_int64(), C.c_int64(), C.c_int32()
+    err = N.ErrorStruct()
+    sc = rec.c_struct()
+    _raise(N.cuda_lib().sfmcov_extract_neighborhood(C.byref(sc), center, k_bar, cams.ctypes.data, C.byref(nc),
+                                                    pts.ctypes.data, C.byref(npt), C.byref(tr), C.byref(err)), err)
+    cams, pts = cams[:nc.value].copy(), pts[:npt.value].copy()
+    return SubScene(cams, pts, induced_scene(rec, cams, pts), bool(tr.value))
+
+
+def plan_coverage(rec: Reconstruction, k_bar: int, seed: int) -> List[np.ndarray]:
+    n = rec.num_cameras()
+    cap_s, cap_c = max(1, n), max(1, n * n)
+    off = np.zeros(cap_s + 1, np.int64)
+    cams = np.zeros(cap_c, np.int32)
+    ns = C.c_int64()
+    err = N.ErrorStruct()
+    sc = rec.c_struct()
+    _raise(N.cuda_lib().sfmcov_plan_coverage(C.byref(sc), k_bar, seed, off.ctypes.data, cap_s, cams.ctypes.data,
+                                             cap_c, C.byref(ns), C.byref(err)), err)
+    return [cams[off[i]:off[i + 1]].copy() for i in range(ns.value)]
+
+
+def approximate_covariances(rec: Reconstruction, k_bar: int, n_decompositions: int, seed: int, workers: int = 4,
+                            engine: Optional[Engine] = None) -> AggregatedCovariance:
+    engine = engine or default_engine()
+    n, P = rec.num_cameras(), rec.cam_params
+    cov = np.zeros((max(1, n), P, P))
+    tr = np.zeros(max(1, n))
+    sid = -np.ones(max(1, n), np.int32)
+    err = N.ErrorStruct()
+    sc = rec.c_struct()
+    _raise(N.cuda_lib().sfmcov_cuda_approximate_covariances(engine.handle, C.byref(sc), k_bar, n_decompositions, seed,
+                                                            workers, cov.ctypes.data, tr.ctypes.data, sid.ctypes.data,
+                                                            C.byref(err)), err)
+    return AggregatedCovariance(k_bar, cov[:n], tr[:n], sid[:n])
+
+
+def monotonicity_check(rec: Reconstruction, small: SubScene, large: SubScene, rel_tol: float = 1e-8,
+                       engine: Optional[Engine] = None) -> MonotonicityReport:
+    engine = engine or default_engine()
+    sc_ = np.ascontiguousarray(small.cameras, np.int32)
+    lc = np.ascontiguousarray(large.cameras, np.int32)
+    k = max(1, len(sc_))
+    vc, ts, tl = np.zeros(k, np.int32), np.zeros(k), np.zeros(k)
+    nv, checked = C.c_int64(), C.c_int64()
+    err = N.ErrorStruct()
+    sc = rec.c_struct()
+    _raise(N.cuda_lib().sfmcov_cuda_monotonicity_check(engine.handle, C.byref(sc), sc_.ctypes.data, len(sc_),
+                                                       lc.ctypes.data, len(lc), rel_tol, vc.ctypes.data, ts.ctypes.data,
+                                                       tl.ctypes.data, C.byref(nv), C.byref(checked), C.byref(err)), err)
+    return MonotonicityReport([(int(vc[i]), float(ts[i]), float(tl[i])) for i in range(nv.value)], checked.value)

@@ -17,7 +17,7 @@ HEADER = (ROOT / "include" / "sfmcov_b200.h").read_text()
 
 def declared_functions():
     body = re.sub(r"/\*.*?\*/", "", HEADER, flags=re.S)
-    return sorted(set(re.findall(r"\b(sfmcov_(?:cuda|synth|nccl|plan)_\w+)\s*\(", body)))
+    return sorted(set(re.findall(r"\b(sfmcov_(?:cuda|synth|nccl|plan|view|extract)_\w+)\s*\(", body)))
 
 
 def test_header_declares_the_entry_points():

@@ -1,0 +1,188 @@
+"""Sub-reconstructions (reference include/sfmcov/subrec.hpp; tests ported
+from tests/test_subrec.cpp).  Planner checks run on CPU; the batched GPU
+covariances are checked against the CPU restatement per sub-scene."""
+import numpy as np
+import pytest
+
+from conftest import rel
+from oracle import oracle as O
+from paper_1808_02414_b200 import sfmcov as F
+from paper_1808_02414_b200 import subrec as R
+from paper_1808_02414_b200 import synthetic as S
+
+
+def covis_count(rec, a, b):  # test_subrec.cpp:23-33
+    pa = set(rec.obs_pt[rec.obs_cam == a].tolist())
+    pb = set(rec.obs_pt[rec.obs_cam == b].tolist())
+    return len(pa & pb)
+
+
+def connected(graph, cams):  # test_subrec.cpp:41-55
+    inside = set(int(c) for c in cams)
+    seen, stack = {int(cams[0])}, [int(cams[0])]
+    while stack:
+        c = stack.pop()
+        for nb, _ in graph.edges[c]:
+            if nb in inside and nb not in seen:
+                seen.add(nb)
+                stack.append(nb)
+    return len(seen) == len(cams)
+
+
+def points_of(rec, cams):
+    m = np.isin(rec.obs_cam, cams)
+    cnt = np.bincount(rec.obs_pt[m], minlength=rec.num_points())
+    return np.nonzero(cnt >= 2)[0].astype(np.int32)
+
+
+def test_view_graph_counts_co_observed_points():  # test_subrec.cpp:64-87
+    rec = S.generate_random_scene(20, 150, 0.3, 5, 0.5)
+    g = R.build_view_graph(rec)
+    assert g.n_cams == 20
+    for a in range(20):
+        nbrs = [b for b, _ in g.edges[a]]
+        assert nbrs == sorted(nbrs)
+        for b in range(20):
+            if a == b:
+                continue
+            w = dict(g.edges[a]).get(b, 0)
+            assert w == covis_count(rec, a, b)
+    strict = R.build_view_graph(rec, min_covis=5)
+    for a in range(20):
+        assert all(w >= 5 for _, w in strict.edges[a])
+
+
+def test_components_stay_separate():  # test_subrec.cpp:89-96
+    from conftest import disconnected_scene
+    rec = disconnected_scene(4, 0.5)
+    g = R.build_view_graph(rec)
+    n = rec.num_cameras()
+    half = n // 2
+    for a in range(half):
+        assert all(b < half for b, _ in g.edges[a])
+
+
+def test_window_as_large_as_the_scene_reproduces_it():  # test_subrec.cpp:98-112
+    rec = S.generate_cube_scene(3, 0.5)
+    for k_bar in (6, 100):
+        sub = R.extract_neighborhood(rec, 0, k_bar)
+        assert sub.component_truncated == (k_bar > 6)
+        assert len(sub.cameras) == 6 and len(sub.points) == 15
+        assert sub.scene.num_observations() == rec.num_observations()
+        assert np.array_equal(sub.scene.obs_cam, rec.obs_cam) and np.array_equal(sub.scene.obs_u, rec.obs_u)
+
+
+def test_bad_window_arguments_are_rejected():  # test_subrec.cpp:114-123 (planner part)
+    rec = S.generate_cube_scene(4, 0.5)
+    for center, k in ((0, 1), (6, 5), (-1, 5)):
+        with pytest.raises(F.Error):
+            R.extract_neighborhood(rec, center, k)
+
+
+def test_neighborhoods_grow_connected_sets():  # test_subrec.cpp:125-139
+    rec = S.generate_random_scene(40, 200, 0.2, 7, 0.5)
+    g = R.build_view_graph(rec)
+    for center in (0, 13, 20, 39):
+        sub = R.extract_neighborhood(rec, center, 5)
+        assert not sub.component_truncated and len(sub.cameras) == 5
+        assert center in sub.cameras and np.all(np.diff(sub.cameras) > 0)
+        assert connected(g, sub.cameras)
+        assert sub.scene.num_cameras() == 5
+        assert np.all(np.bincount(sub.scene.obs_cam, minlength=5) >= 4)  # the induced filter's fixpoint
+        assert np.all(np.bincount(sub.scene.obs_pt) >= 2)
+
+
+def test_growing_the_window_keeps_earlier_cameras():  # test_subrec.cpp:141-155 (nesting part)
+    rec = S.generate_random_scene(40, 200, 0.2, 7, 0.5)
+    small = R.extract_neighborhood(rec, 20, 8)
+    large = R.extract_neighborhood(rec, 20, 20)
+    assert np.all(np.isin(small.cameras, large.cameras))
+
+
+def test_coverage_covers_every_camera_deterministically():  # plan_coverage, src/subrec.cpp:154-181
+    rec = S.generate_random_scene(40, 200, 0.2, 7, 0.5)
+    a = R.plan_coverage(rec, 10, 9)
+    b = R.plan_coverage(rec, 10, 9)
+    assert len(a) == len(b) and all(np.array_equal(x, y) for x, y in zip(a, b))
+    assert set(np.concatenate(a).tolist()) == set(range(40))
+    assert any(not np.array_equal(x, y) for x, y in zip(a, R.plan_coverage(rec, 10, 10)))
+
+
+# ---- GPU --------------------------------------------------------------------------
+@pytest.mark.gpu
+def test_bad_aggregation_arguments_are_rejected(engine):  # test_subrec.cpp:119-121
+    rec = S.generate_cube_scene(4, 0.5)
+    with pytest.raises(F.Error):
+        R.approximate_covariances(rec, 1, 3, 0, engine=engine)
+    with pytest.raises(F.Error):
+        R.approximate_covariances(rec, 6, 0, 0, engine=engine)
+
+
+@pytest.mark.gpu
+def test_monotonicity_and_nesting(engine):  # test_subrec.cpp:141-169
+    rec = S.generate_random_scene(40, 200, 0.2, 7, 0.5)
+    small = R.extract_neighborhood(rec, 20, 8)
+    large = R.extract_neighborhood(rec, 20, 20)
+    rep = R.monotonicity_check(rec, small, large, engine=engine)
+    assert rep.cameras_checked == len(small.cameras) and rep.violations == []
+    assert R.monotonicity_check(rec, small, small, engine=engine).violations == []
+    a = R.extract_neighborhood(rec, 0, 10)
+    b = R.extract_neighborhood(rec, 20, 10)
+    with pytest.raises(F.Error) as e:
+        R.monotonicity_check(rec, a, b, engine=engine)
+    assert e.value.kind == F.ErrorKind.invariant and "not nested" in str(e.value)
+
+
+@pytest.mark.gpu
+def test_full_size_aggregation_reproduces_the_full_covariance_exactly(engine):  # test_subrec.cpp:171-184
+    rec = S.generate_cube_scene(5, 0.5)
+    agg = R.approximate_covariances(rec, 6, 1, 3, engine=engine)
+    full = engine.compute_covariance(rec)
+    assert agg.target_size == 6 and agg.cov.shape[0] == 6
+    for i in range(6):
+        assert np.array_equal(agg.cov[i], full.camera_cov[i])
+        assert agg.trace[i] == sum(full.camera_cov[i][p, p] for p in range(8))
+        assert agg.subset_id[i] == 0
+
+
+@pytest.mark.gpu
+def test_extra_decompositions_only_lower_the_trace(engine):  # test_subrec.cpp:186-195
+    rec = S.generate_random_scene(40, 200, 0.2, 7, 0.5)
+    one = R.approximate_covariances(rec, 10, 1, 9, engine=engine)
+    three = R.approximate_covariances(rec, 10, 3, 9, engine=engine)
+    for i in range(40):
+        assert three.trace[i] <= one.trace[i] and three.subset_id[i] >= 0
+        assert three.trace[i] == sum(three.cov[i][p, p] for p in range(8))
+
+
+@pytest.mark.gpu
+def test_failures_name_the_subset_and_decomposition(engine):  # test_subrec.cpp:197-208
+    rec = S.generate_cube_scene(6, 0.5)
+    rec.pts[14] = rec.cams[3, 3:6]
+    with pytest.raises(F.Error) as e:
+        R.approximate_covariances(rec, 6, 1, 0, engine=engine)
+    assert e.value.kind == F.ErrorKind.degenerate and e.value.stage == "subrec"
+    assert "subset 0 (decomposition 0)" in str(e.value)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workers", [1, 4])
+def test_kept_blocks_match_the_restatement_per_subset(engine, workers):
+    rec = S.generate_config(2)  # 100 cameras, windows of 20
+    k_bar, decos, seed = 20, 2, 5
+    agg = R.approximate_covariances(rec, k_bar, decos, seed, workers=workers, engine=engine)
+    subsets = [c for d in range(decos) for c in R.plan_coverage(rec, k_bar, seed + d)]
+    P = rec.cam_params
+    cache = {}
+    for g in range(rec.num_cameras()):
+        sid = int(agg.subset_id[g])
+        if sid not in cache:
+            cams = subsets[sid]
+            sub = R.induced_scene(rec, cams, points_of(rec, cams))
+            cache[sid] = (cams, O.compute_covariance(sub)[0])
+        cams, cov = cache[sid]
+        l = int(np.searchsorted(cams, g))
+        assert rel(agg.cov[g], cov[l]) <= 1e-9
+    # batching (workers) does not change any result bit
+    again = R.approximate_covariances(rec, k_bar, decos, seed, workers=1, engine=engine)
+    assert np.array_equal(again.cov, agg.cov) and np.array_equal(again.subset_id, agg.subset_id)

@@ -103,6 +103,9 @@ void sfmcov_cuda_destroy(sfmcov_handle* h);
 void* sfmcov_cuda_stream(sfmcov_handle* h);
 /* The handle's device ordinal. */
 int32_t sfmcov_cuda_device(sfmcov_handle* h);
+/* The i-th worker handle of h (same device, own stream and workspace;
+ * created on first use, destroyed with h): batched independent problems. */
+sfmcov_handle* sfmcov_cuda_worker(sfmcov_handle* h, int32_t i, sfmcov_error* err);
 
 /* ---- full pipeline --------------------------------------------------------
  * Replaces sfmcov::compute_covariance (include/sfmcov/covariance.hpp:110-111,

@@ -78,6 +78,9 @@ struct sfmcov_handle {
     DBuf zi, fc_part, fc_y, fc_gtt, fc_eb, fc_pc;
     cudaEvent_t ev_ready = nullptr, ev_rank_done[64];
     bool ev_rank_init = false;
+    // worker handles for batched independent problems (sub-reconstructions),
+    // owned by this handle so their streams and workspaces persist
+    std::vector<sfmcov_handle*> workers;
     // captured dense stage (Cholesky + triangular inverse), keyed by its inputs
     cudaGraphExec_t dense_exec = nullptr;
     const void* dense_key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -853,6 +856,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
         for (auto& e : h->ev_rank_done) cudaEventDestroy(e);
     }
     if (h->nccl) sfm::nccl_comm_destroy(h->nccl);
+    for (sfmcov_handle* w : h->workers) sfmcov_cuda_destroy(w);
     if (h->dense_exec) cudaGraphExecDestroy(h->dense_exec);
     if (h->st_host) cudaFreeHost(h->st_host);
     cudaEventDestroy(h->e1);
@@ -871,6 +875,17 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
 void* sfmcov_cuda_stream(sfmcov_handle* h) { return h ? (void*)h->s : nullptr; }
 
 int32_t sfmcov_cuda_device(sfmcov_handle* h) { return h ? h->device : -1; }
+
+sfmcov_handle* sfmcov_cuda_worker(sfmcov_handle* h, int32_t i, sfmcov_error* err) {
+    if (!h || i < 0) return nullptr;
+    std::lock_guard<std::mutex> lock(h->mu);
+    while ((int32_t)h->workers.size() <= i) {
+        sfmcov_handle* w = sfmcov_cuda_create(h->device, err);
+        if (!w) return nullptr;
+        h->workers.push_back(w);
+    }
+    return h->workers[i];
+}
 
 void sfmcov_cuda_set_profiling(sfmcov_handle* h, int32_t on) {
     if (h) h->profiling = on != 0;

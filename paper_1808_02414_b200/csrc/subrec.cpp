@@ -72,24 +72,46 @@ Graph view_graph(const sfmcov_scene& s, int min_covis) {
     for (int32_t j = 0; j < s.n_pts; ++j) off[j + 1] += off[j];
     std::vector<int32_t> by_pt(s.n_obs), fill(off.begin(), off.end() - 1);
     for (int32_t k = 0; k < s.n_obs; ++k) by_pt[fill[s.obs_pt[k]]++] = k;
-    std::unordered_map<uint64_t, int32_t> counts;
-    std::vector<int32_t> obs;
-    for (int32_t j = 0; j < s.n_pts; ++j) {
-        obs.clear();
-        for (int64_t k = off[j]; k < off[j + 1]; ++k) obs.push_back(s.obs_cam[by_pt[k]]);
-        std::sort(obs.begin(), obs.end());
-        for (size_t a = 0; a < obs.size(); ++a)
-            for (size_t b = a + 1; b < obs.size(); ++b)
-                ++counts[(uint64_t(uint32_t(obs[a])) << 32) | uint32_t(obs[b])];
-    }
     Graph g;
     g.n = s.n_cams;
     g.edges.resize(s.n_cams);
-    for (const auto& [key, w] : counts) {
-        if (w < min_covis) continue;
-        const int32_t a = int32_t(key >> 32), b = int32_t(key & 0xffffffffu);
-        g.edges[a].emplace_back(b, w);
-        g.edges[b].emplace_back(a, w);
+    std::vector<int32_t> obs;
+    auto for_pairs = [&](auto&& f) {
+        for (int32_t j = 0; j < s.n_pts; ++j) {
+            obs.clear();
+            for (int64_t k = off[j]; k < off[j + 1]; ++k) obs.push_back(s.obs_cam[by_pt[k]]);
+            std::sort(obs.begin(), obs.end());
+            for (size_t a = 0; a < obs.size(); ++a)
+                for (size_t b = a + 1; b < obs.size(); ++b) f(obs[a], obs[b]);
+        }
+    };
+    const int64_t n = s.n_cams;
+    if (n <= 8192) {  // dense pair counts (at most 256 MiB)
+        std::vector<int32_t> cnt((size_t)n * n, 0);
+        for_pairs([&](int32_t a, int32_t b) { ++cnt[(size_t)a * n + b]; });
+        for (int64_t a = 0; a < n; ++a)
+            for (int64_t b = a + 1; b < n; ++b) {
+                const int32_t w = cnt[(size_t)a * n + b];
+                if (w > 0 && w >= min_covis) {
+                    g.edges[a].emplace_back((int32_t)b, w);
+                    g.edges[b].emplace_back((int32_t)a, w);
+                }
+            }
+    } else {  // sorted pair keys, run-length counted
+        std::vector<uint64_t> keys;
+        for_pairs([&](int32_t a, int32_t b) { keys.push_back((uint64_t(uint32_t(a)) << 32) | uint32_t(b)); });
+        std::sort(keys.begin(), keys.end());
+        for (size_t i = 0; i < keys.size();) {
+            size_t e = i;
+            while (e < keys.size() && keys[e] == keys[i]) ++e;
+            const int32_t w = (int32_t)(e - i);
+            if (w >= min_covis) {
+                const int32_t a = int32_t(keys[i] >> 32), b = int32_t(keys[i] & 0xffffffffu);
+                g.edges[a].emplace_back(b, w);
+                g.edges[b].emplace_back(a, w);
+            }
+            i = e;
+        }
     }
     for (auto& adj : g.edges) std::sort(adj.begin(), adj.end());
     return g;
@@ -101,31 +123,106 @@ struct Sub {
     bool truncated = false;
 };
 
+// Observations by camera (ascending observation ids), built once per call so
+// an induced scene only visits its own cameras' observations.
+struct ByCam {
+    std::vector<int64_t> off;
+    std::vector<int32_t> idx;
+    explicit ByCam(const sfmcov_scene& s) : off(s.n_cams + 1, 0), idx(s.n_obs) {
+        for (int32_t t = 0; t < s.n_obs; ++t) ++off[s.obs_cam[t] + 1];
+        for (int32_t i = 0; i < s.n_cams; ++i) off[i + 1] += off[i];
+        std::vector<int64_t> f(off.begin(), off.end() - 1);
+        for (int32_t t = 0; t < s.n_obs; ++t) idx[f[s.obs_cam[t]]++] = t;
+    }
+};
+
 // induced_scene (src/subrec.cpp:24-86): points seen by >= 2 subset cameras,
 // cameras with >= 4 surviving observations, to a fixpoint.
-Sub induced(const sfmcov_scene& s, const std::vector<int32_t>& cams, bool truncated) {
+// Scratch arrays of one planner thread, reset only where touched.
+struct Scratch {
+    std::vector<char> cam_in, pt_in;
+    std::vector<int32_t> pc, cc, cl, pl;
+    void size(int64_t n, int64_t m) {
+        if ((int64_t)cam_in.size() != n) { cam_in.assign(n, 0); cc.assign(n, 0); cl.assign(n, -1); }
+        if ((int64_t)pt_in.size() != m) { pt_in.assign(m, 0); pc.assign(m, 0); pl.assign(m, -1); }
+    }
+};
+
+// The cameras that survive the induced filter (its fixpoint), ascending: the
+// part of induced_scene the covering loop needs before its next draw.
+std::vector<int32_t> induced_cams(const sfmcov_scene& s, const ByCam& bc, const std::vector<int32_t>& cams) {
     const int64_t n = s.n_cams, m = s.n_pts;
-    std::vector<char> cam_in(n, 0), pt_in(m, 0);
-    for (int32_t c : cams) cam_in[c] = 1;
+    thread_local Scratch w;
+    w.size(n, m);
+    for (int32_t c : cams) w.cam_in[c] = 1;
     std::vector<int32_t> cand;
-    for (int32_t t = 0; t < s.n_obs; ++t)
-        if (cam_in[s.obs_cam[t]]) cand.push_back(t);
-    std::vector<int32_t> pc(m), cc(n);
+    for (int32_t c : cams) cand.insert(cand.end(), bc.idx.begin() + bc.off[c], bc.idx.begin() + bc.off[c + 1]);
     for (bool changed = true; changed;) {
-        std::fill(pc.begin(), pc.end(), 0);
+        for (int32_t t : cand) w.pc[s.obs_pt[t]] = 0;
+        for (int32_t t : cand)
+            if (w.cam_in[s.obs_cam[t]]) ++w.pc[s.obs_pt[t]];
+        for (int32_t t : cand) w.pt_in[s.obs_pt[t]] = w.pc[s.obs_pt[t]] >= 2;
+        for (int32_t c : cams) w.cc[c] = 0;
+        for (int32_t t : cand)
+            if (w.cam_in[s.obs_cam[t]] && w.pt_in[s.obs_pt[t]]) ++w.cc[s.obs_cam[t]];
+        changed = false;
+        for (int32_t i : cams)
+            if (w.cam_in[i] && w.cc[i] < 4) {
+                w.cam_in[i] = 0;
+                changed = true;
+            }
+    }
+    std::vector<int32_t> out;
+    for (int32_t c : cams)
+        if (w.cam_in[c]) out.push_back(c);
+    std::sort(out.begin(), out.end());
+    for (int32_t c : cams) { w.cam_in[c] = 0; w.cc[c] = 0; }
+    for (int32_t t : cand) { const int32_t j = s.obs_pt[t]; w.pt_in[j] = 0; w.pc[j] = 0; }
+    return out;
+}
+
+Sub induced(const sfmcov_scene& s, const ByCam& bc, const std::vector<int32_t>& cams, bool truncated) {
+    const int64_t n = s.n_cams, m = s.n_pts;
+    thread_local Scratch w;
+    w.size(n, m);
+    std::vector<char>& cam_in = w.cam_in;
+    std::vector<char>& pt_in = w.pt_in;
+    std::vector<int32_t>&pc = w.pc, &cc = w.cc;
+    for (int32_t c : cams) cam_in[c] = 1;
+    std::vector<int32_t> cand;  // the subset cameras' observations
+    for (int32_t c : cams) cand.insert(cand.end(), bc.idx.begin() + bc.off[c], bc.idx.begin() + bc.off[c + 1]);
+    for (bool changed = true; changed;) {
+        for (int32_t t : cand) pc[s.obs_pt[t]] = 0;
         for (int32_t t : cand)
             if (cam_in[s.obs_cam[t]]) ++pc[s.obs_pt[t]];
-        for (int64_t j = 0; j < m; ++j) pt_in[j] = pc[j] >= 2;
-        std::fill(cc.begin(), cc.end(), 0);
+        for (int32_t t : cand) pt_in[s.obs_pt[t]] = pc[s.obs_pt[t]] >= 2;
+        for (int32_t c : cams) cc[c] = 0;
         for (int32_t t : cand)
             if (cam_in[s.obs_cam[t]] && pt_in[s.obs_pt[t]]) ++cc[s.obs_cam[t]];
         changed = false;
-        for (int64_t i = 0; i < n; ++i)
+        for (int32_t i : cams)
             if (cam_in[i] && cc[i] < 4) {
                 cam_in[i] = 0;
                 changed = true;
             }
     }
+    // kept observations in ascending id order (the reference's candidate order)
+    std::vector<int32_t> kept;
+    kept.reserve(cand.size());
+    for (int32_t t : cand)
+        if (cam_in[s.obs_cam[t]] && pt_in[s.obs_pt[t]]) kept.push_back(t);
+    std::sort(kept.begin(), kept.end());
+    std::vector<int32_t>&cl = w.cl, &pl = w.pl;
+    struct Reset {  // leave the scratch clean for the next call
+        Scratch& w;
+        const std::vector<int32_t>& cams;
+        const std::vector<int32_t>& cand;
+        const sfmcov_scene& s;
+        ~Reset() {
+            for (int32_t c : cams) { w.cam_in[c] = 0; w.cc[c] = 0; w.cl[c] = -1; }
+            for (int32_t t : cand) { const int32_t j = s.obs_pt[t]; w.pt_in[j] = 0; w.pc[j] = 0; w.pl[j] = -1; }
+        }
+    } reset{w, cams, cand, s};
     Sub sub;
     sub.truncated = truncated;
     const int P = s.cam_params;
@@ -133,22 +230,32 @@ Sub induced(const sfmcov_scene& s, const std::vector<int32_t>& cams, bool trunca
     h.P = P;
     h.has_u = s.obs_u != nullptr;
     h.has_sigma = s.obs_sigma != nullptr;
-    std::vector<int32_t> cl(n, -1), pl(m, -1);
-    for (int64_t i = 0; i < n; ++i)
-        if (cam_in[i]) {
-            cl[i] = (int32_t)sub.cams.size();
-            sub.cams.push_back((int32_t)i);
-            h.cams.insert(h.cams.end(), s.cams + P * i, s.cams + P * i + P);
-        }
+    {
+        std::vector<int32_t> sorted_cams(cams.begin(), cams.end());
+        std::sort(sorted_cams.begin(), sorted_cams.end());
+        for (int32_t i : sorted_cams)
+            if (cam_in[i]) {
+                cl[i] = (int32_t)sub.cams.size();
+                sub.cams.push_back(i);
+                h.cams.insert(h.cams.end(), s.cams + (size_t)P * i, s.cams + (size_t)P * i + P);
+            }
+    }
     if (sub.cams.empty()) throw SubError{SFMCOV_ERR_DEGENERATE, "subrec", "induced sub-reconstruction is empty"};
-    for (int64_t j = 0; j < m; ++j)
-        if (pt_in[j]) {
+    {
+        std::vector<int32_t> pts;  // ascending ids of the kept points
+        for (int32_t t : kept)
+            if (pl[s.obs_pt[t]] == -1) {
+                pl[s.obs_pt[t]] = 0;
+                pts.push_back(s.obs_pt[t]);
+            }
+        std::sort(pts.begin(), pts.end());
+        for (int32_t j : pts) {
             pl[j] = (int32_t)sub.pts.size();
-            sub.pts.push_back((int32_t)j);
-            h.pts.insert(h.pts.end(), s.pts + 3 * j, s.pts + 3 * j + 3);
+            sub.pts.push_back(j);
+            h.pts.insert(h.pts.end(), s.pts + 3 * size_t(j), s.pts + 3 * size_t(j) + 3);
         }
-    for (int32_t t : cand) {
-        if (!cam_in[s.obs_cam[t]] || !pt_in[s.obs_pt[t]]) continue;
+    }
+    for (int32_t t : kept) {
         h.oc.push_back(cl[s.obs_cam[t]]);
         h.op.push_back(pl[s.obs_pt[t]]);
         if (h.has_u) h.u.insert(h.u.end(), s.obs_u + 2 * size_t(t), s.obs_u + 2 * size_t(t) + 2);
@@ -161,7 +268,8 @@ Sub induced(const sfmcov_scene& s, const std::vector<int32_t>& cams, bool trunca
 }
 
 // extract_neighborhood (src/subrec.cpp:118-152)
-Sub neighborhood(const sfmcov_scene& s, const Graph& g, int64_t center, int k_bar) {
+Sub neighborhood(const sfmcov_scene& s, const ByCam& bc, const Graph& g, int64_t center, int k_bar,
+                 bool build = true) {
     const int64_t n = s.n_cams;
     if (k_bar < 2) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "subset size must be at least 2"};
     if (center < 0 || center >= n || g.n != n)
@@ -189,11 +297,17 @@ Sub neighborhood(const sfmcov_scene& s, const Graph& g, int64_t center, int k_ba
             if (!in[nb]) weight[nb] += w;
     }
     std::sort(chosen.begin(), chosen.end());
-    return induced(s, chosen, truncated);
+    if (build) return induced(s, bc, chosen, truncated);
+    Sub sub;  // cameras only; the scene is built later
+    sub.cams = induced_cams(s, bc, chosen);
+    sub.truncated = truncated;
+    if (sub.cams.empty()) throw SubError{SFMCOV_ERR_DEGENERATE, "subrec", "induced sub-reconstruction is empty"};
+    return sub;
 }
 
 // plan_coverage (src/subrec.cpp:154-181)
-std::vector<Sub> coverage(const sfmcov_scene& s, const Graph& g, int k_bar, uint64_t seed) {
+std::vector<Sub> coverage(const sfmcov_scene& s, const ByCam& bc, const Graph& g, int k_bar, uint64_t seed,
+                          bool build = true) {
     const int64_t n = s.n_cams;
     std::vector<Sub> plan;
     std::mt19937_64 rng(seed);
@@ -205,7 +319,7 @@ std::vector<Sub> coverage(const sfmcov_scene& s, const Graph& g, int k_bar, uint
         for (int64_t i = 0; i < n; ++i)
             if (!covered[i]) pool.push_back(i);
         const int64_t center = pool[std::uniform_int_distribution<std::size_t>(0, pool.size() - 1)(rng)];
-        Sub sub = neighborhood(s, g, center, k_bar);
+        Sub sub = neighborhood(s, bc, g, center, k_bar, build);
         if (!std::binary_search(sub.cams.begin(), sub.cams.end(), (int32_t)center))
             throw SubError{SFMCOV_ERR_DEGENERATE, "subrec",
                            "camera " + std::to_string(center) + " cannot anchor a sub-reconstruction of size " +
@@ -236,8 +350,7 @@ struct SubResult {
     sfmcov_error err{};
 };
 
-std::vector<SubResult> batch_covariances(sfmcov_handle* h0, int device, const std::vector<const Sub*>& subs,
-                                         int workers) {
+std::vector<SubResult> batch_covariances(sfmcov_handle* h0, const std::vector<const Sub*>& subs, int workers) {
     std::vector<SubResult> res(subs.size());
     std::atomic<size_t> next{0};
     auto work = [&](sfmcov_handle* h) {
@@ -250,18 +363,18 @@ std::vector<SubResult> batch_covariances(sfmcov_handle* h0, int device, const st
         }
     };
     workers = std::max(1, std::min<int>(workers, (int)subs.size()));
-    std::vector<sfmcov_handle*> hs{h0};
-    for (int w = 1; w < workers; ++w) {
+    std::vector<sfmcov_handle*> hs;
+    for (int w = 0; w < workers; ++w) {
         sfmcov_error e{};
-        sfmcov_handle* h = sfmcov_cuda_create(device, &e);
+        sfmcov_handle* h = sfmcov_cuda_worker(h0, w, &e);
         if (!h) break;
         hs.push_back(h);
     }
+    if (hs.empty()) hs.push_back(h0);
     std::vector<std::thread> th;
     for (size_t w = 1; w < hs.size(); ++w) th.emplace_back(work, hs[w]);
     work(hs[0]);
     for (auto& t : th) t.join();
-    for (size_t w = 1; w < hs.size(); ++w) sfmcov_cuda_destroy(hs[w]);
     return res;
 }
 
@@ -321,7 +434,8 @@ int32_t sfmcov_extract_neighborhood(const sfmcov_scene* scene, int64_t center, i
     return guarded(err, [&] {
         check_scene(scene);
         const Graph g = view_graph(*scene, 1);
-        const Sub sub = neighborhood(*scene, g, center, k_bar);
+        const ByCam bc(*scene);
+        const Sub sub = neighborhood(*scene, bc, g, center, k_bar);
         std::copy(sub.cams.begin(), sub.cams.end(), cams);
         std::copy(sub.pts.begin(), sub.pts.end(), pts);
         *n_cams = (int64_t)sub.cams.size();
@@ -336,7 +450,8 @@ int32_t sfmcov_plan_coverage(const sfmcov_scene* scene, int32_t k_bar, uint64_t 
     return guarded(err, [&] {
         check_scene(scene);
         const Graph g = view_graph(*scene, 1);
-        const std::vector<Sub> plan = coverage(*scene, g, k_bar, seed);
+        const ByCam bc(*scene);
+        const std::vector<Sub> plan = coverage(*scene, bc, g, k_bar, seed, false);
         int64_t k = 0;
         subset_off[0] = 0;
         for (size_t i = 0; i < plan.size(); ++i) {
@@ -359,17 +474,61 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
         check_scene(scene);
         const int P = scene->cam_params;
         const Graph g = view_graph(*scene, 1);
+        const ByCam bc(*scene);
         std::vector<std::vector<Sub>> plans;
         std::vector<const Sub*> flat;
         std::vector<int> deco;
-        for (int d = 0; d < n_decompositions; ++d) plans.push_back(coverage(*scene, g, k_bar, seed + uint64_t(d)));
+        // the coverings are independent (one seed each): planned in parallel
+        plans.resize(n_decompositions);
+        std::vector<SubError> perr(n_decompositions);
+        std::vector<char> pfail(n_decompositions, 0);
+        {
+            std::vector<std::thread> th;
+            for (int d = 0; d < n_decompositions; ++d)
+                th.emplace_back([&, d] {
+                    try {
+                        plans[d] = coverage(*scene, bc, g, k_bar, seed + uint64_t(d), false);
+                    } catch (const SubError& x) {
+                        perr[d] = x;
+                        pfail[d] = 1;
+                    }
+                });
+            for (auto& t : th) t.join();
+        }
         for (int d = 0; d < n_decompositions; ++d)
-            for (const Sub& sb : plans[d]) {
+            if (pfail[d]) throw perr[d];
+        for (int d = 0; d < n_decompositions; ++d)
+            for (Sub& sb : plans[d]) {
                 flat.push_back(&sb);
                 deco.push_back(d);
             }
+        {  // induced scenes of every subset, in parallel (host)
+            std::atomic<size_t> next{0};
+            std::vector<SubError> berr(flat.size());
+            std::vector<char> bfail(flat.size(), 0);
+            auto job = [&] {
+                for (size_t i = next++; i < flat.size(); i = next++) {
+                    Sub& sb = const_cast<Sub&>(*flat[i]);
+                    try {
+                        Sub full = induced(*scene, bc, sb.cams, sb.truncated);
+                        sb.scene = std::move(full.scene);
+                        sb.pts = std::move(full.pts);
+                    } catch (const SubError& x) {
+                        berr[i] = x;
+                        bfail[i] = 1;
+                    }
+                }
+            };
+            const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 32));
+            std::vector<std::thread> th;
+            for (int i = 1; i < nt; ++i) th.emplace_back(job);
+            job();
+            for (auto& t : th) t.join();
+            for (size_t i = 0; i < flat.size(); ++i)
+                if (bfail[i]) throw berr[i];
+        }
         const std::vector<SubResult> res =
-            batch_covariances(h, sfmcov_cuda_device(h), flat, std::max(1, (int)workers));
+            batch_covariances(h, flat, std::max(1, (int)workers));
         const int64_t n = scene->n_cams;
         std::vector<char> seen(n, 0);
         for (size_t sid = 0; sid < flat.size(); ++sid) {
@@ -411,7 +570,8 @@ int32_t sfmcov_cuda_monotonicity_check(sfmcov_handle* h, const sfmcov_scene* sce
                 throw SubError{SFMCOV_ERR_INVARIANT, "subrec",
                                "subsets are not nested: camera " + std::to_string(c) + " is missing from the larger subset"};
         }
-        const Sub s_small = induced(*scene, sc, false), s_large = induced(*scene, lc, false);
+        const ByCam bc(*scene);
+        const Sub s_small = induced(*scene, bc, sc, false), s_large = induced(*scene, bc, lc, false);
         const int P = scene->cam_params;
         std::vector<double> cs((size_t)P * P * s_small.cams.size()), cl((size_t)P * P * s_large.cams.size());
         sfmcov_options o{0, 0, 0, 0};

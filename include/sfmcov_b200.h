@@ -205,6 +205,17 @@ int32_t sfmcov_plan_dense(int32_t n_cams, int32_t cam_params, int32_t nranks, in
                           int32_t panel_blocks, int64_t* npad, int64_t* local_cols, int32_t* cam_owned);
 int32_t sfmcov_plan_chunks(int64_t nchunks, int32_t nranks, int32_t rank, int64_t* begin, int64_t* end);
 
+/* pseudoinverse_covariance (include/sfmcov/oracle.hpp:33-37, src/oracle.cpp:34-72):
+ * the dense reference covariance for verification — Fisher matrix
+ * (N = P n + 3 m params, refused above max_params with SFMCOV_ERR_SIZE_GUARD),
+ * its eigendecomposition on the GPU (cuSOLVER syevd, loaded at run time; SVD
+ * of a PSD matrix), the seven smallest dropped by count, Σ = V Λ^+ V^T.
+ * cam_cov n x P x P; sigma_full N x N col-major (may be NULL); singular
+ * values descending (N, may be NULL); gauge_gap = s[N-8] / s[N-7]. */
+int32_t sfmcov_cuda_pseudoinverse_covariance(sfmcov_handle* h, const sfmcov_scene* scene, int64_t max_params,
+                                             double* cam_cov, double* sigma_full, double* singular_values,
+                                             double* gauge_gap, sfmcov_error* err);
+
 /* Per-stage device times (ms) of the last pipeline call, in the order of
  * sfmcov_cuda_stage_name(i); returns the number of stages written. */
 int32_t sfmcov_cuda_last_stage_times(sfmcov_handle* h, double* ms, int32_t capacity);

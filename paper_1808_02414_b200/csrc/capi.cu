@@ -76,6 +76,7 @@ struct sfmcov_handle {
     std::vector<sfm::RankDense> ranks;
     DBuf seg, seg_tmp, prange_r, scale_mm;
     DBuf zi, fc_part, fc_y, fc_gtt, fc_eb, fc_pc;
+    DBuf or_a, or_w, or_work, or_vs, or_vk, or_s, or_keep;
     cudaEvent_t ev_ready = nullptr, ev_rank_done[64];
     bool ev_rank_init = false;
     // worker handles for batched independent problems (sub-reconstructions),
@@ -850,7 +851,9 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     h->seg_tmp.release();
     h->prange_r.release();
     h->scale_mm.release();
-    for (DBuf* b : {&h->zi, &h->fc_part, &h->fc_y, &h->fc_gtt, &h->fc_eb, &h->fc_pc}) b->release();
+    for (DBuf* b : {&h->zi, &h->fc_part, &h->fc_y, &h->fc_gtt, &h->fc_eb, &h->fc_pc, &h->or_a, &h->or_w, &h->or_work,
+                    &h->or_vs, &h->or_vk, &h->or_s, &h->or_keep})
+        b->release();
     if (h->ev_rank_init) {
         cudaEventDestroy(h->ev_ready);
         for (auto& e : h->ev_rank_done) cudaEventDestroy(e);
@@ -1028,6 +1031,77 @@ int32_t sfmcov_cuda_compute_covariance_sharded_device(sfmcov_handle* h, const sf
         out.diag = diag;
         run(h, as_device(d_scene), M_FULL, out);
         SFM_CUDA(cudaStreamSynchronize(h->s));
+    });
+}
+
+int32_t sfmcov_cuda_pseudoinverse_covariance(sfmcov_handle* h, const sfmcov_scene* scene, int64_t max_params,
+                                             double* cam_cov, double* sigma_full, double* singular_values,
+                                             double* gauge_gap, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        const int P = scene->cam_params, n = scene->n_cams, m = scene->n_pts, t = scene->n_obs;
+        const int64_t params = (int64_t)P * n + 3 * (int64_t)m;
+        if (params > max_params)
+            throw ApiError{SFMCOV_ERR_SIZE_GUARD, "oracle",
+                           "scene has " + std::to_string(params) + " parameters, guard is " + std::to_string(max_params)};
+        const SceneDev sc = upload(h, scene);
+        {  // rec.validate()
+            std::vector<int64_t> oc(n + 1), op(m + 1);
+            std::vector<int32_t> ic(t > 0 ? t : 1), ip(t > 0 ? t : 1);
+            Outputs o;
+            o.off_cam = oc.data(); o.idx_cam = ic.data(); o.off_pt = op.data(); o.idx_pt = ip.data();
+            run(h, sc, M_INDEX, o);
+        }
+        std::vector<double> D((size_t)P * P * n), A(9 * (size_t)m), Cp((size_t)P * 3 * t);
+        Outputs o;
+        o.D = D.data(); o.A = A.data(); o.Cp = Cp.data();
+        run(h, sc, M_FISHER, o);
+        const int N = (int)params;
+        std::vector<double> F((size_t)N * N, 0.0);
+        auto f = [&](int r, int c) -> double& { return F[(size_t)c * N + r]; };
+        for (int i = 0; i < n; ++i)
+            for (int p = 0; p < P; ++p)
+                for (int q = 0; q < P; ++q) f(P * i + p, P * i + q) = D[(size_t)P * P * i + P * p + q];
+        for (int j = 0; j < m; ++j)
+            for (int p = 0; p < 3; ++p)
+                for (int q = 0; q < 3; ++q) f(P * n + 3 * j + p, P * n + 3 * j + q) = A[9 * (size_t)j + 3 * p + q];
+        std::vector<int32_t> oc(t), op(t);
+        std::memcpy(oc.data(), scene->obs_cam, 4 * (size_t)t);
+        std::memcpy(op.data(), scene->obs_pt, 4 * (size_t)t);
+        for (int k = 0; k < t; ++k)
+            for (int p = 0; p < P; ++p)
+                for (int q = 0; q < 3; ++q) {
+                    const double v = Cp[(size_t)P * 3 * k + 3 * p + q];
+                    f(P * oc[k] + p, P * n + 3 * op[k] + q) = v;
+                    f(P * n + 3 * op[k] + q, P * oc[k] + p) = v;
+                }
+        std::vector<double> lam;
+        double* S = nullptr;
+        long long ld = 0;
+        try {
+            dense_pseudoinverse(F, N, h->or_a, h->or_w, h->or_work, h->or_vs, h->or_vk, h->or_s, h->or_keep, lam, &S,
+                                &ld, h->s);
+        } catch (const CudaError& x) {
+            throw ApiError{SFMCOV_ERR_DEGENERATE, "oracle", x.what()};
+        }
+        for (int i = 0; i < n; ++i)
+            SFM_CUDA(cudaMemcpy2DAsync(cam_cov + (size_t)P * P * i, 8 * (size_t)P, S + (size_t)P * i * ld + (size_t)P * i,
+                                       8 * ld, 8 * (size_t)P, P, cudaMemcpyDeviceToHost, h->s));
+        if (sigma_full)
+            SFM_CUDA(cudaMemcpy2DAsync(sigma_full, 8 * (size_t)N, S, 8 * ld, 8 * (size_t)N, N, cudaMemcpyDeviceToHost,
+                                       h->s));
+        SFM_CUDA(cudaStreamSynchronize(h->s));
+        // the blocks were copied column by column into row-major slots: transpose
+        // each (Σ is symmetric, the copy gives Σ(q, p) at [p][q] before the swap)
+        for (int i = 0; i < n; ++i) {
+            double* b = cam_cov + (size_t)P * P * i;
+            for (int p = 0; p < P; ++p)
+                for (int q = p + 1; q < P; ++q) std::swap(b[P * p + q], b[P * q + p]);
+        }
+        std::vector<double> sv(N);
+        for (int i = 0; i < N; ++i) sv[i] = std::fabs(lam[i]);
+        std::sort(sv.begin(), sv.end(), std::greater<double>());
+        if (singular_values) std::memcpy(singular_values, sv.data(), 8 * (size_t)N);
+        if (gauge_gap) *gauge_gap = N >= 8 ? sv[N - 8] / sv[N - 7] : 0.0;
     });
 }
 

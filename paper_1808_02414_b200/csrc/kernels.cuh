@@ -5,6 +5,9 @@
 
 #include <cuda_runtime.h>
 
+#include <string>
+#include <vector>
+
 namespace sfm {
 
 // Grow-only device allocation.
@@ -179,6 +182,11 @@ struct FullCovArgs {
 };
 void full_covariance(const FullCovArgs& a, cudaStream_t s);
 size_t full_cov_part_doubles(int N);
+
+// ---- dense pseudoinverse oracle (oraclegpu.cu) -----------------------------
+void dense_pseudoinverse(const std::vector<double>& F, int N, DBuf& dA, DBuf& dW, DBuf& dwork, DBuf& dVs, DBuf& dVk,
+                         DBuf& dS, DBuf& dkeep, std::vector<double>& lam, double** sigma, long long* ld_out,
+                         cudaStream_t s);
 
 // ---- column layouts and panel ownership (distributed path, dist.cu) ---------
 // Camera-aligned layout (cpb > 0): cpb = floor(kNB / P) cameras per 128-block,

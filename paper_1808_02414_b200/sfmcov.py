@@ -363,6 +363,23 @@ class Engine:
         _raise(code, err)
         return z
 
+    def pseudoinverse_covariance(self, rec: Reconstruction, max_params: int = 2000, full: bool = True):
+        """Dense reference covariance (oracle.hpp:33-37) on the GPU: returns
+        (camera_cov (n,P,P), sigma_full (N,N) or None, singular values (N,), gauge gap)."""
+        P, n = rec.cam_params, rec.num_cameras()
+        npar = rec.num_parameters()
+        cov = np.empty((max(1, n), P, P))
+        sg = np.empty((npar, npar), order="F") if full and npar <= max_params else None
+        sv = np.empty(max(1, npar))
+        gap = C.c_double()
+        err = N.ErrorStruct()
+        sc = rec.c_struct()
+        code = self._lib.sfmcov_cuda_pseudoinverse_covariance(self._h, C.byref(sc), max_params, cov.ctypes.data,
+                                                              None if sg is None else sg.ctypes.data, sv.ctypes.data,
+                                                              C.byref(gap), C.byref(err))
+        _raise(code, err)
+        return cov[:n], sg, sv[:npar], gap.value
+
     def spd_inverse_blocks(self, a: np.ndarray, block: int):
         a = np.asfortranarray(a, dtype=np.float64)
         n = a.shape[0]

@@ -359,3 +359,29 @@ def test_config3_point_and_cross_covariances(engine):
     assert worst_block(res.camera_cov, cov) <= COV_TOL
     assert worst_block(res.point_cov, pc) <= COV_TOL
     assert rel(res.camera_matrix, cm) <= COV_TOL
+
+
+# ---- dense pseudoinverse oracle on the GPU (oracle.hpp:33-37) ------------------------
+@pytest.mark.parametrize("name", ["cube_p8", "cube_p9", "ring_p8", "ring64_p8"])
+def test_gpu_pseudoinverse_matches_the_cpu_oracle(engine, name):
+    rec = SMALL[name]()
+    cov, sg, sv, gap = O.pseudoinverse(rec)
+    gcov, gsg, gsv, ggap = engine.pseudoinverse_covariance(rec)
+    # two dense factorizations (LAPACK dgesdd vs cuSOLVER syevd) of the
+    # unconditioned Fisher matrix: they agree to its conditioning (the
+    # reference's own oracle test uses the Eq. 42 metric < 1e-4)
+    assert worst_block(gcov, cov) <= 1e-6
+    assert rel(gsg, sg) <= 1e-6 and np.array_equal(gsg, gsg.T)
+    assert np.abs(gsv[:-7] - sv[:-7]).max() <= 1e-12 * sv[0]  # the kept spectrum, to backward-stable accuracy
+    assert gap > 1e6 and ggap > 1e6  # seven gauge directions, well separated
+    # the NBUP (camera-block) pipeline agrees with the dense reference (test_oracle.cpp:90-101)
+    nb = engine.compute_covariance(rec).camera_cov
+    assert worst_block(nb, gcov) <= 1e-6
+
+
+def test_gpu_pseudoinverse_size_guard(engine):
+    rec = S.generate_config(1)  # 90 + 3000 parameters
+    with pytest.raises(F.Error) as e:
+        engine.pseudoinverse_covariance(rec, max_params=2000)
+    assert e.value.kind == F.ErrorKind.size_guard and e.value.stage == "oracle"
+    assert "guard is 2000" in str(e.value)

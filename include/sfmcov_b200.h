@@ -276,6 +276,19 @@ void sfmcov_synth_export(const sfmcov_synth_scene* s, double* cams, double* pts,
 void sfmcov_synth_free(sfmcov_synth_scene* s);
 const char* sfmcov_synth_last_error(void);
 
+/* ---- scene IO (include/sfmcov/scene_io.hpp, src/scene_io.cpp; host) --------
+ * JSON in the reference's schema (sorted keys, compact, shortest round-trip
+ * numbers, sigma omitted when identity; "k2" for P = 9 cameras) and a binary
+ * format for large scenes.  Loaders return an owned scene (read it with
+ * sfmcov_synth_sizes / _export, free with sfmcov_synth_free) or NULL with err
+ * set (kinds io / parse, stage "load"; the reference's context strings).  The
+ * scene invariants are checked by the CUDA library (the wrappers validate
+ * after loading, as the reference's load ends with validate()). */
+sfmcov_synth_scene* sfmcov_scene_load(const char* path, sfmcov_error* err);
+int32_t sfmcov_scene_save(const sfmcov_scene* scene, const char* path, sfmcov_error* err);
+sfmcov_synth_scene* sfmcov_scene_load_binary(const char* path, sfmcov_error* err);
+int32_t sfmcov_scene_save_binary(const sfmcov_scene* scene, const char* path, sfmcov_error* err);
+
 #ifdef __cplusplus
 }
 #endif

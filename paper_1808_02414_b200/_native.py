@@ -151,6 +151,10 @@ SYNTH_SYMBOLS = {
     "sfmcov_synth_export": (None, [C.c_void_p] + [C.c_void_p] * 6),
     "sfmcov_synth_free": (None, [C.c_void_p]),
     "sfmcov_synth_last_error": (C.c_char_p, []),
+    "sfmcov_scene_load": (C.c_void_p, [C.c_char_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_scene_save": (C.c_int32, [C.POINTER(Scene), C.c_char_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_scene_load_binary": (C.c_void_p, [C.c_char_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_scene_save_binary": (C.c_int32, [C.POINTER(Scene), C.c_char_p, C.POINTER(ErrorStruct)]),
 }
 
 _cuda_lib = None

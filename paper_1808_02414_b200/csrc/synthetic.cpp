@@ -12,6 +12,7 @@
 // Exposed through a small C ABI (include/sfmcov_b200.h, "synthetic scenes").
 
 #include "sfmcov_b200.h"
+#include "scene_host.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -93,17 +94,7 @@ void look_at(V3 C, V3 target, double* r) {
     rotation_log(R, r);
 }
 
-struct Scene {
-    int P = 8;
-    std::vector<double> cams;   // n × P
-    std::vector<double> pts;    // m × 3
-    std::vector<int32_t> oc, op;
-    std::vector<double> u;      // t × 2
-    std::vector<double> sigma;  // t × 4
-    int64_t n() const { return (int64_t)cams.size() / P; }
-    int64_t m() const { return (int64_t)pts.size() / 3; }
-    int64_t t() const { return (int64_t)oc.size(); }
-};
+using sfmhost::Scene;  // scene_host.hpp
 
 // Camera-space point and projection u = f(1 + k1ρ + k2ρ²)u_n; false if depth <= eps.
 bool project(const double* cam, int P, const double* X, double* u, double* vz = nullptr) {
@@ -454,7 +445,6 @@ thread_local std::string g_last_error;
 
 }  // namespace
 
-struct sfmcov_synth_scene { Scene s; };
 
 extern "C" {
 

@@ -669,7 +669,7 @@ void launch_copy_panel_w(const double* X, long long ld, int b0, int G, int rows,
 // products over a strided set of rows, then a fixed-order tree reduction.
 // ----------------------------------------------------------------------------
 template <int P>
-__global__ void __launch_bounds__(256) k_extract(const double* X, long long ld, int N, const double* s_a, int scale,
+__global__ void __launch_bounds__(256, 2) k_extract(const double* X, long long ld, int N, const double* s_a, int scale,
                                                  double* cov, Status* st, int* psd_warn) {
     constexpr int U = P * (P + 1) / 2;
     __shared__ double red[8][U];

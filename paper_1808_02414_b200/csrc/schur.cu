@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(128) k_border_factor(const double* Fpart, int 
 // Γ_i[p][l] = H_s,ci[p][l] - Σ_{a in cam i} (W_a V_j(a))[p][l], ascending
 // observation order; then G_i = Γ_i L_F^-T.
 template <int P>
-__global__ void __launch_bounds__(64) k_camera_border(const int* off_cam, const int* idx_cam, const int* op,
+__global__ void __launch_bounds__(128) k_camera_border(const int* off_cam, const int* idx_cam, const int* op,
                                                       const double* Wb, const double* V, const double* cams,
                                                       const double* Hr, const double* s_a, const double* s_b,
                                                       const double* LF, int n, double* Gamma, double* G) {
@@ -215,20 +215,24 @@ __global__ void __launch_bounds__(64) k_camera_border(const int* off_cam, const 
     constexpr int CH = 64, RS = 49;  // staged: W (27) at 0, V_j (21) at 27
     __shared__ double stage[CH][RS];
     __shared__ double sh[NE];
+    __shared__ int pid[CH];
     const int i = blockIdx.x, tid = threadIdx.x;
     const int p = tid / 7, l = tid % 7;
     double acc = 0.0;
     const int b = off_cam[i], e = off_cam[i + 1];
     for (int k0 = b; k0 < e; k0 += CH) {
         const int nc = min(CH, e - k0);
+        // the chunk's point ids first (one dependent gather per observation)
+        if (tid < nc) pid[tid] = op[idx_cam[k0 + tid]];
         // W rows of the chunk are contiguous (by-camera slots): coalesced copy
-        for (int w = tid; w < nc * 27; w += 64) {
+        for (int w = tid; w < nc * 27; w += 128) {
             const int o = w / 27, c = w - o * 27;
             stage[o][c] = Wb[(size_t)(k0 + o) * kWStride + c];
         }
-        for (int w = tid; w < nc * 21; w += 64) {
+        __syncthreads();
+        for (int w = tid; w < nc * 21; w += 128) {
             const int o = w / 21, c = w - o * 21;
-            stage[o][27 + c] = V[21 * (size_t)op[idx_cam[k0 + o]] + c];
+            stage[o][27 + c] = V[21 * (size_t)pid[o] + c];
         }
         __syncthreads();
         if (tid < NE) {
@@ -581,8 +585,8 @@ void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* 
                           const double* s_a, const double* s_b, const double* LF, double* Gamma, double* G,
                           cudaStream_t s) {
     if (!sc.n) return;
-    if (sc.P == 8) k_camera_border<8><<<sc.n, 64, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
-    else k_camera_border<9><<<sc.n, 64, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    if (sc.P == 8) k_camera_border<8><<<sc.n, 128, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    else k_camera_border<9><<<sc.n, 128, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
     SFM_LAUNCH_CHECK();
 }
 

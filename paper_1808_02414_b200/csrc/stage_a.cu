@@ -52,10 +52,11 @@ __global__ void k_validate_pts(const double* pts, int m, Status* st) {
 __global__ void k_validate_obs(const int* oc, const int* op, const double* u, const double* sigma, int t_count,
                                int n, int m, int check_sigma, Status* st, int* cam_cnt, int* pt_cnt) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= t_count) return;
-    const int ci = oc[t], pj = op[t];
-    int code = 0;
-    if (ci < 0 || ci >= n) code = 1;
+    const bool valid = t < t_count;
+    const int ci = valid ? oc[t] : -1, pj = valid ? op[t] : -1;
+    int code = valid ? 0 : 6;
+    if (!valid) {
+    } else if (ci < 0 || ci >= n) code = 1;
     else if (pj < 0 || pj >= m) code = 2;
     else if (check_sigma) {
         double s00 = 1.0, s01 = 0.0, s10 = 0.0, s11 = 1.0;
@@ -71,10 +72,17 @@ __global__ void k_validate_obs(const int* oc, const int* op, const double* u, co
             }
         }
     }
-    if (code) atomicMin(&st->obs_bad, (long long)t * 8 + code);
-    if (code == 0 || code > 2) {
-        atomicAdd(&cam_cnt[ci], 1);
-        atomicAdd(&pt_cnt[pj], 1);
+    if (code && valid) atomicMin(&st->obs_bad, (long long)t * 8 + code);
+    // counts per camera / point, warp-aggregated (a point's observations sit
+    // in neighbouring lanes): one atomic per distinct index per warp
+    const bool add = valid && (code == 0 || (code > 2 && code < 6));
+    const unsigned mask = __ballot_sync(0xffffffffu, add);
+    if (add) {
+        const int lane = threadIdx.x & 31;
+        const unsigned pp = __match_any_sync(mask, pj);
+        if (lane == __ffs(pp) - 1) atomicAdd(&pt_cnt[pj], __popc(pp));
+        const unsigned pc = __match_any_sync(mask, ci);
+        if (lane == __ffs(pc) - 1) atomicAdd(&cam_cnt[ci], __popc(pc));
     }
 }
 

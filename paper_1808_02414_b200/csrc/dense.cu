@@ -185,10 +185,8 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
         for (int ni = 0; ni < 4; ++ni) {
             acc[mi][ni][0] = 0.0;
             acc[mi][ni][1] = 0.0;
-#ifndef SFM_NO_C_PREFETCH
             if (beta && (mi & 1) == 0 && (lane & 3) == 0)  // one lane per 128-byte line
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(C + (size_t)(wn * 32 + ni * 8 + cq) * g.ldc + wm * 32 + mi * 8));
-#endif
         }
 
 #pragma unroll 1
@@ -380,9 +378,6 @@ constexpr int SMEM = (kNB * LDT + NSB * 64 + NWARPS * 64 + 2 * kNB) * 8;
 // 1/sqrt(d) for d > 0: MUFU.RSQ64H seed + 3 Newton steps (full double
 // precision without the libdevice call on the per-column critical path).
 __device__ __forceinline__ double fast_rsqrt(double d) {
-#ifdef SFM_EXACT_RSQRT
-    return 1.0 / sqrt(d);
-#endif
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
     const double hd = 0.5 * d;
@@ -834,26 +829,6 @@ static bool debug_sync() {
     return v;
 }
 
-// Experimental (SFMCOV_TRSM_SUBST=1): L21 = A21 L11^-T by plain forward
-// substitution, one thread per row (accuracy reference for the inverse-based
-// GEMM trsm).
-__global__ void k_trsm_subst(double* A, long long ld, int rows, const double* L) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
-    double x[kNB];
-    for (int j = 0; j < kNB; ++j) {
-        double v = A[(size_t)j * ld + r];
-        for (int k = 0; k < j; ++k) v -= x[k] * L[(size_t)k * ld + j];
-        x[j] = v / L[(size_t)j * ld + j];
-    }
-    for (int j = 0; j < kNB; ++j) A[(size_t)j * ld + r] = x[j];
-}
-
-static bool trsm_subst() {
-    static bool v = [] { const char* e = std::getenv("SFMCOV_TRSM_SUBST"); return e && e[0] == '1'; }();
-    return v;
-}
-
 GemmArgs gemm_args(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb,
                           int tm, int tn, int K) {
     GemmArgs g{};
@@ -1054,9 +1029,6 @@ static void launch_panel_take(double* Z, long long ld, int b0, int W, int rows, 
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
                 cudaEvent_t eR) {
-    // timing experiments only (results invalid): SFMCOV_SWEEP_SKIP=1 drops
-    // the trailing update, 2 the inverse, 3 both
-    static const int skip = [] { const char* e = std::getenv("SFMCOV_SWEEP_SKIP"); return e ? std::atoi(e) : 0; }();
     const int K = Npad / kNB;
     int launches = 0;
     bool rest_pending = false;
@@ -1072,13 +1044,9 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             ++launches;
             const int below = K - c - 1;
             if (below == 0) break;
-            if (trsm_subst()) {
-                k_trsm_subst<<<cdiv(below * kNB, 128), 128, 0, s>>>(Acc + kNB, ld, below * kNB, Acc);
-            } else {
-                GemmArgs t = gemm_args(Acc + kNB, ld, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
+            GemmArgs t = gemm_args(Acc + kNB, ld, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
             t.whole_tile = 1;  // in place: every output column reads the whole row tile
-                launch_gemm(t, s);
-            }
+            launch_gemm(t, s);
             ++launches;
             const int inner = b0 + g_here - c - 1;
             if (inner > 0) {
@@ -1101,7 +1069,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
         const int T2 = K - nb0;
         const int gn = (T2 < G) ? T2 : G;
         // --- Cholesky trailing update ---
-        if (T2 > gn && !(skip & 1)) {
+        if (T2 > gn) {
             SFM_CUDA(cudaStreamWaitEvent(s2, eL[slot], 0));
             const int r0 = nb0 + gn;
             const double* Lr = Lb + W + (size_t)gn * kNB;
@@ -1120,13 +1088,13 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             ++launches;
         }
         rest_pending = false;
-        if (T2 > gn && !(skip & 1)) {
+        if (T2 > gn) {
             SFM_CUDA(cudaEventRecord(eR, s2));
             rest_pending = true;
         }
         // --- inverse step p (rows of panel p) ---
         SFM_CUDA(cudaStreamWaitEvent(s3, eL[slot], 0));
-        for (int g = 0; g < g_here && !(skip & 2); ++g) {
+        for (int g = 0; g < g_here; ++g) {
             const int r = b0 + g;
             GemmArgs a = gemm_args(Z + (size_t)r * kNB, ld, Linv + (size_t)r * kNB * kNB, kNB, Z + (size_t)r * kNB, ld,
                                    1, r + 1, kNB);
@@ -1142,7 +1110,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
                 ++launches;
             }
         }
-        if (T2 > 0 && !(skip & 2)) {
+        if (T2 > 0) {
             GemmArgs x = gemm_args(Z + (size_t)nb0 * kNB, ld, Lb + W, rows, Z + (size_t)b0 * kNB, ld, T2, nb0, W);
             x.b_kmajor = 1; x.alpha_neg = 1; x.beta = 1; x.beta0_from = b0;
             launch_gemm(x, s3);

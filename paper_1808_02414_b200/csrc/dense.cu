@@ -1020,6 +1020,26 @@ __global__ void k_panel_take(double* Z, long long ld, int b0, int W, int rows, d
     }
 }
 
+// The panel's diagonal 128-tiles (L, from Z) into the slot; the W x W block of Z := I.
+__global__ void k_panel_take_diag(double* Z, long long ld, int b0, int W, double* Lb, int rows) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;  // one double2 (two rows)
+    const int half = W >> 1;
+    if (e >= half * W) return;
+    const int i = (e % half) * 2, j = e / half;
+    double2* zp = reinterpret_cast<double2*>(Z + (size_t)(b0 * kNB + j) * ld + (size_t)b0 * kNB + i);
+    if (i / kNB == j / kNB) *reinterpret_cast<double2*>(Lb + (size_t)j * rows + i) = __ldcg(zp);
+    double2 x;
+    x.x = (i == j) ? 1.0 : 0.0;
+    x.y = (i + 1 == j) ? 1.0 : 0.0;
+    *zp = x;
+}
+
+static void launch_panel_take_diag(double* Z, long long ld, int b0, int W, double* Lb, int rows, cudaStream_t s) {
+    const int total = (W / 2) * W;
+    k_panel_take_diag<<<cdiv(total, 256), 256, 0, s>>>(Z, ld, b0, W, Lb, rows);
+    SFM_LAUNCH_CHECK();
+}
+
 static void launch_panel_take(double* Z, long long ld, int b0, int W, int rows, double* Lb, cudaStream_t s) {
     const long long total = (long long)(rows / 2) * W;
     k_panel_take<<<cdiv(total, 256), 256, 0, s>>>(Z, ld, b0, W, rows, Lb);
@@ -1037,6 +1057,13 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
         const int g_here = (b0 + G <= K) ? G : K - b0;
         const int W = g_here * kNB;
         // --- panel factorisation (critical path) ---
+        // The off-diagonal L tiles go straight into the ring slot (trsm out of
+        // place, so two CTAs per 128-wide tile may split it); the diagonal
+        // tiles stay in Z until the hand-over.
+        const int slot = p % NB;
+        if (p >= NB) SFM_CUDA(cudaStreamWaitEvent(s, eT[slot], 0));  // inverse step p - NB done with Lb
+        const int rows = Npad - b0 * kNB;
+        double* Lb = ring + (size_t)slot * Npad * G * kNB;
         for (int g = 0; g < g_here; ++g) {
             const int c = b0 + g;
             double* Acc = Z + (size_t)c * kNB * ld + (size_t)c * kNB;
@@ -1044,25 +1071,22 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             ++launches;
             const int below = K - c - 1;
             if (below == 0) break;
-            GemmArgs t = gemm_args(Acc + kNB, ld, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
-            t.whole_tile = 1;  // in place: every output column reads the whole row tile
+            double* Lc = Lb + (size_t)g * kNB * rows + (size_t)(g + 1) * kNB;  // L[rows > c, c] in the slot
+            GemmArgs t = gemm_args(Lc, rows, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
             launch_gemm(t, s);
             ++launches;
             const int inner = b0 + g_here - c - 1;
             if (inner > 0) {
-                GemmArgs u = gemm_args(Z + (size_t)(c + 1) * kNB * ld + (size_t)(c + 1) * kNB, ld, Acc + kNB, ld,
-                                       Acc + kNB, ld, below, inner, kNB);
+                GemmArgs u = gemm_args(Z + (size_t)(c + 1) * kNB * ld + (size_t)(c + 1) * kNB, ld, Lc, rows, Lc, rows,
+                                       below, inner, kNB);
                 u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
                 launch_gemm(u, s);
                 ++launches;
             }
         }
-        // --- hand the panel over to the inverse ---
-        const int slot = p % NB;
-        if (p >= NB) SFM_CUDA(cudaStreamWaitEvent(s, eT[slot], 0));  // inverse step p - NB done with Lb
-        const int rows = Npad - b0 * kNB;
-        double* Lb = ring + (size_t)slot * Npad * G * kNB;
-        launch_panel_take(Z, ld, b0, W, rows, Lb, s);
+        // --- hand the panel over to the inverse: diagonal tiles into the slot,
+        // the panel's W x W block of Z := I ---
+        launch_panel_take_diag(Z, ld, b0, W, Lb, rows, s);
         ++launches;
         SFM_CUDA(cudaEventRecord(eL[slot], s));
         const int nb0 = b0 + g_here;

@@ -53,7 +53,8 @@ enum Mode { M_INDEX, M_JACOBIAN, M_NULLSPACE, M_FISHER, M_SCHUR, M_FULL };
 
 struct sfmcov_handle {
     int device = 0;
-    cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
+    cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr, s4 = nullptr;
+    cudaEvent_t eX = nullptr, eN = nullptr;
     cudaEvent_t e1 = nullptr, e2 = nullptr;
     static constexpr int kRing = 4;  // panel ring buffers of the fused sweep
     cudaEvent_t eL[kRing], eT[kRing];
@@ -277,7 +278,7 @@ int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv,
     if (use_sweep()) {
         double* ring = h->ring.as<double>(sweep_ring_doubles(Npad, pw, sfmcov_handle::kRing));
         launches = dense_sweep(Z, ld, Npad, pw, Linv, piv, st, ring, sfmcov_handle::kRing, s, s2, serial ? s : h->s3,
-                               h->eL, h->eT, h->e2);
+                               h->eL, h->eT, h->e2, serial ? s : h->s4, h->eX, h->eN);
         if (mark_stages) {
             mark(h, 8);
             mark(h, 9);
@@ -815,6 +816,9 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s, cudaStreamNonBlocking, hi));
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s2, cudaStreamNonBlocking, (lo + hi) / 2));
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s3, cudaStreamNonBlocking, lo));
+        SFM_CUDA(cudaStreamCreateWithPriority(&h->s4, cudaStreamNonBlocking, hi));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->eX, cudaEventDisableTiming));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->eN, cudaEventDisableTiming));
         for (int i = 0; i < sfmcov_handle::kRing; ++i) {
             SFM_CUDA(cudaEventCreateWithFlags(&h->eL[i], cudaEventDisableTiming));
             SFM_CUDA(cudaEventCreateWithFlags(&h->eT[i], cudaEventDisableTiming));
@@ -839,6 +843,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaStreamSynchronize(h->s);
     cudaStreamSynchronize(h->s2);
     cudaStreamSynchronize(h->s3);
+    cudaStreamSynchronize(h->s4);
     DBuf* bufs[] = {&h->ws.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_u, &h->h_sigma, &h->cnt_cam,
                     &h->cnt_pt, &h->off_cam, &h->idx_cam, &h->off_pt, &h->idx_pt, &h->pos_cam, &h->key_scratch,
                     &h->R, &h->rec, &h->D, &h->Hr, &h->A, &h->s_a, &h->flags, &h->bpart, &h->s_b, &h->Lpt, &h->Wb, &h->V,
@@ -868,6 +873,9 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaStreamDestroy(h->s);
     cudaStreamDestroy(h->s2);
     cudaStreamDestroy(h->s3);
+    cudaStreamDestroy(h->s4);
+    cudaEventDestroy(h->eX);
+    cudaEventDestroy(h->eN);
     for (int i = 0; i < sfmcov_handle::kRing; ++i) {
         cudaEventDestroy(h->eL[i]);
         cudaEventDestroy(h->eT[i]);

@@ -1048,7 +1048,8 @@ static void launch_panel_take(double* Z, long long ld, int b0, int W, int rows, 
 
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
-                cudaEvent_t eR) {
+                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN) {
+    bool next_pending = false;  // the previous step's update of the next panel's later columns (s4)
     const int K = Npad / kNB;
     int launches = 0;
     bool rest_pending = false;
@@ -1077,6 +1078,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             ++launches;
             const int inner = b0 + g_here - c - 1;
             if (inner > 0) {
+                if (g == 0 && next_pending) SFM_CUDA(cudaStreamWaitEvent(s, eN, 0));  // same columns
                 GemmArgs u = gemm_args(Z + (size_t)(c + 1) * kNB * ld + (size_t)(c + 1) * kNB, ld, Lc, rows, Lc, rows,
                                        below, inner, kNB);
                 u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
@@ -1103,13 +1105,29 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             launch_gemm(r, s2);
             ++launches;
         }
+        next_pending = false;
         if (T2 > 0) {
+            // next panel: its first block column on the critical stream (the next
+            // potrf / trsm need only it), the later columns on s4 concurrently
+            // (the next panel's first inner update waits for them)
             if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, eR, 0));
+            const bool split = gn > 1 && s4 != s;
+            if (split) SFM_CUDA(cudaEventRecord(eX, s));
             GemmArgs u = gemm_args(Z + (size_t)nb0 * kNB * ld + (size_t)nb0 * kNB, ld, Lb + W, rows, Lb + W, rows, T2,
-                                   gn, W);
+                                   split ? 1 : gn, W);
             u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
             launch_gemm(u, s);
             ++launches;
+            if (split) {
+                SFM_CUDA(cudaStreamWaitEvent(s4, eX, 0));
+                GemmArgs v = gemm_args(Z + (size_t)(nb0 + 1) * kNB * ld + (size_t)nb0 * kNB, ld, Lb + W, rows,
+                                       Lb + W + kNB, rows, T2, gn - 1, W);
+                v.alpha_neg = 1; v.beta = 1; v.lower_only = 1; v.col_off_tiles = 1;
+                launch_gemm(v, s4);
+                ++launches;
+                SFM_CUDA(cudaEventRecord(eN, s4));
+                next_pending = true;
+            }
         }
         rest_pending = false;
         if (T2 > gn) {
@@ -1149,6 +1167,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
         }
     }
     if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, eR, 0));
+    if (next_pending) SFM_CUDA(cudaStreamWaitEvent(s, eN, 0));
     if (last_slot >= 0) SFM_CUDA(cudaStreamWaitEvent(s, eT[last_slot], 0));
     return launches;
 }

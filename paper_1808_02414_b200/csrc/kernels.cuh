@@ -161,7 +161,7 @@ int dense_trtri(double* X, long long ld, int Npad, int G, const double* Linv, do
 // Lp workspace (doubles) dense_trtri needs for panel width G.
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
-                cudaEvent_t eR);
+                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN);
 inline size_t sweep_ring_doubles(int Npad, int G, int NB) { return (size_t)NB * Npad * G * kNB; }
 inline size_t trtri_lp_doubles(int Npad, int G) { return (size_t)Npad * kNB * G + (size_t)kNB * kNB * G; }
 

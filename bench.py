@@ -323,7 +323,13 @@ def main():
     b_schur = t_obs * (2 * (P + 3) * 8 + 4) + m_pts * (3 * 8 + 4) + nnz * P * P * 8 + (P * n * 7 + 49) * 8
     f_schur = 6 * P * P * pairs
     schur_ms = stages.get("schur_point_prep", 0) + stages.get("pair_sort", 0) + stages.get("schur_pair_reduce", 0)
-    t_star = max(b_schur / (hbm * 1e9), f_schur / (FP64_PEAK_TFLOPS * 1e12))
+    t_hbm, t_fp64 = b_schur / (hbm * 1e9), f_schur / (FP64_PEAK_TFLOPS * 1e12)
+    t_star = max(t_hbm, t_fp64)
+    # Jacobian stage bytes and the dense-Z fill, reported separately
+    has_sigma = rec.obs_sigma is not None
+    b_jac = t_obs * (4 + 4 + 24 * has_sigma) + m_pts * 24 + n * P * 8 + t_obs * 2 * (P + 3) * 8
+    jac_ms = stages.get("jacobian", 0.0)
+    fill_ms = stages.get("dense_fill", 0.0)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -376,7 +382,14 @@ def main():
                 "algorithmic_flops": algo_flops, "executed_flops_padded": flops,
                 "stage_ms": dense_ms,
             },
+            "jacobian_stage": {"GB_per_s": b_jac / (jac_ms * 1e-3) / 1e9 if jac_ms else None, "bytes": b_jac,
+                               "stage_ms": jac_ms, "hbm_frac": (b_jac / (hbm * 1e9)) / (jac_ms * 1e-3) if jac_ms else None},
+            "dense_fill": {"GB_per_s": Npad * Npad * 4 / (fill_ms * 1e-3) / 1e9 if fill_ms else None,
+                           "note": "lower triangle of the padded Z written once (N^2/2 x 8 B)", "stage_ms": fill_ms},
             "schur": {
+                "hbm_frac": (t_hbm * 1e3) / schur_ms if schur_ms else None,
+                "fp64_frac": (t_fp64 * 1e3) / schur_ms if schur_ms else None,
+                "binding": "fp64" if t_fp64 >= t_hbm else "hbm",
                 "obs_pairs_per_s": pairs / (schur_ms * 1e-3) if schur_ms else None,
                 "GB_per_s": b_schur / (schur_ms * 1e-3) / 1e9 if schur_ms else None,
                 "roofline_time_ms": t_star * 1e3, "frac": (t_star * 1e3) / schur_ms if schur_ms else None,

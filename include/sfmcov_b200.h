@@ -259,6 +259,13 @@ int32_t sfmcov_cuda_monotonicity_check(sfmcov_handle* h, const sfmcov_scene* sce
                                        double* trace_large, int64_t* n_violations, int64_t* cameras_checked,
                                        sfmcov_error* err);
 
+/* error_size_sweep: rows of (k_bar, subset_id, camera_id) in row_ints (3 per
+ * row) and (err_relative, err_absolute, trace) in row_vals (3 per row). */
+int32_t sfmcov_cuda_error_size_sweep(sfmcov_handle* h, const sfmcov_scene* scene, const int32_t* sizes,
+                                     int32_t n_sizes, int32_t subsets_per_size, uint64_t seed, int32_t workers,
+                                     int32_t* row_ints, double* row_vals, int64_t capacity, int64_t* n_rows,
+                                     sfmcov_error* err);
+
 /* ---- synthetic scenes (host only; harness, not the hot path) ------------
  * generate_cube_scene / generate_random_scene / transform_scene
  * (include/sfmcov/synthetic.hpp:17-28, src/synthetic.cpp:52-194) and the

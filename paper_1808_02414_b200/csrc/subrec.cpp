@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstdint>
 #include <cstring>
@@ -596,6 +597,74 @@ int32_t sfmcov_cuda_monotonicity_check(sfmcov_handle* h, const sfmcov_scene* sce
         }
         *n_violations = nv;
         *cameras_checked = checked;
+    });
+}
+
+// error_size_sweep (src/subrec.cpp:258-297): per window size, subsets_per_size
+// centers drawn from a seeded shuffle; every subset camera's block compared
+// with the full-scene block (Frobenius).  Rows: (k_bar, subset, camera,
+// err_relative, err_absolute, trace) x capacity.
+int32_t sfmcov_cuda_error_size_sweep(sfmcov_handle* h, const sfmcov_scene* scene, const int32_t* sizes, int32_t n_sizes,
+                                     int32_t subsets_per_size, uint64_t seed, int32_t workers, int32_t* row_ints,
+                                     double* row_vals, int64_t capacity, int64_t* n_rows, sfmcov_error* err) {
+    return guarded(err, [&] {
+        if (subsets_per_size < 1) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "need at least one subset per size"};
+        check_scene(scene);
+        const int P = scene->cam_params;
+        const int64_t n = scene->n_cams;
+        std::vector<double> full((size_t)P * P * n);
+        {
+            sfmcov_options o{0, 0, 0, 0};
+            sfmcov_error e{};
+            if (int32_t c = sfmcov_cuda_compute_covariance(h, scene, &o, full.data(), nullptr, &e))
+                throw SubError{c, e.stage, strip_stage(e)};
+        }
+        const Graph g = view_graph(*scene, 1);
+        const ByCam bc(*scene);
+        std::mt19937_64 rng(seed);
+        std::vector<int64_t> ids(n);
+        std::vector<Sub> subs;
+        std::vector<int> kbar, sidx;
+        for (int si = 0; si < n_sizes; ++si) {
+            const int k = sizes[si];
+            std::iota(ids.begin(), ids.end(), int64_t{0});
+            std::shuffle(ids.begin(), ids.end(), rng);
+            for (int sub = 0; sub < subsets_per_size; ++sub) {
+                const int64_t center = ids[(size_t)sub % ids.size()];
+                subs.push_back(neighborhood(*scene, bc, g, center, k));
+                kbar.push_back(k);
+                sidx.push_back(sub);
+            }
+        }
+        std::vector<const Sub*> flat;
+        for (const Sub& sb : subs) flat.push_back(&sb);
+        const std::vector<SubResult> res = batch_covariances(h, flat, std::max(1, (int)workers));
+        int64_t k = 0;
+        for (size_t i = 0; i < subs.size(); ++i) {
+            if (res[i].code)
+                throw SubError{res[i].code, "subrec",
+                               "sweep size " + std::to_string(kbar[i]) + " subset " + std::to_string(sidx[i]) + ": " +
+                                   std::string(res[i].err.message)};
+            for (size_t l = 0; l < subs[i].cams.size(); ++l, ++k) {
+                if (k >= capacity) continue;
+                const int32_t gc = subs[i].cams[l];
+                const double* a = &res[i].cov[(size_t)P * P * l];
+                const double* b = &full[(size_t)P * P * gc];
+                double d2 = 0.0, r2 = 0.0;
+                for (int e = 0; e < P * P; ++e) {
+                    d2 += (a[e] - b[e]) * (a[e] - b[e]);
+                    r2 += b[e] * b[e];
+                }
+                const double err_abs = std::sqrt(d2), ref = std::sqrt(r2);
+                row_ints[3 * k] = kbar[i];
+                row_ints[3 * k + 1] = sidx[i];
+                row_ints[3 * k + 2] = gc;
+                row_vals[3 * k] = ref > 0.0 ? err_abs / ref : err_abs;
+                row_vals[3 * k + 1] = err_abs;
+                row_vals[3 * k + 2] = trace_of(a, P);
+            }
+        }
+        *n_rows = k;
     });
 }
 

@@ -112,6 +112,48 @@ def approximate_covariances(rec: Reconstruction, k_bar: int, n_decompositions: i
     return AggregatedCovariance(k_bar, cov[:n], tr[:n], sid[:n])
 
 
+@dataclass
+class SweepRow:
+    k_bar: int
+    subset_id: int
+    camera_id: int
+    err_relative: float
+    err_absolute: float
+    trace: float
+
+
+def error_size_sweep(rec: Reconstruction, sizes: List[int], subsets_per_size: int, seed: int, workers: int = 4,
+                     engine: Optional[Engine] = None) -> List[SweepRow]:
+    """Per window size, seeded random centers; every subset camera's block
+    against the full-scene block (src/subrec.cpp:258-297)."""
+    engine = engine or default_engine()
+    sz = np.ascontiguousarray(sizes, np.int32)
+    cap = max(1, int(sum(int(k) for k in sizes) * subsets_per_size))
+    ints = np.zeros((cap, 3), np.int32)
+    vals = np.zeros((cap, 3))
+    nrows = C.c_int64()
+    err = N.ErrorStruct()
+    sc = rec.c_struct()
+    _raise(N.cuda_lib().sfmcov_cuda_error_size_sweep(engine.handle, C.byref(sc), sz.ctypes.data, len(sz),
+                                                     subsets_per_size, seed, workers, ints.ctypes.data,
+                                                     vals.ctypes.data, cap, C.byref(nrows), C.byref(err)), err)
+    k = min(nrows.value, cap)
+    return [SweepRow(int(ints[i, 0]), int(ints[i, 1]), int(ints[i, 2]), float(vals[i, 0]), float(vals[i, 1]),
+                     float(vals[i, 2])) for i in range(k)]
+
+
+def write_sweep_csv(rows: List[SweepRow], path: str) -> None:
+    """The reference's CSV layout (src/subrec.cpp:299-312), %.17g numbers."""
+    try:
+        with open(path, "w") as f:
+            f.write("kbar,subset_id,camera_id,err_relative,err_absolute,trace\n")
+            for r in rows:
+                f.write(f"{r.k_bar},{r.subset_id},{r.camera_id},{r.err_relative:.17g},{r.err_absolute:.17g},"
+                        f"{r.trace:.17g}\n")
+    except OSError as e:
+        raise Error(1, "subrec", f"cannot open '{path}' for writing") from e
+
+
 def monotonicity_check(rec: Reconstruction, small: SubScene, large: SubScene, rel_tol: float = 1e-8,
                        engine: Optional[Engine] = None) -> MonotonicityReport:
     engine = engine or default_engine()

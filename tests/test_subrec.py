@@ -186,3 +186,31 @@ def test_kept_blocks_match_the_restatement_per_subset(engine, workers):
     # batching (workers) does not change any result bit
     again = R.approximate_covariances(rec, k_bar, decos, seed, workers=1, engine=engine)
     assert np.array_equal(again.cov, agg.cov) and np.array_equal(again.subset_id, agg.subset_id)
+
+
+@pytest.mark.gpu
+def test_error_size_sweep_shrinks_with_larger_windows(engine):  # test_subrec.cpp:210-230
+    rec = S.generate_random_scene(40, 200, 0.2, 7, 0.5)
+    rows = R.error_size_sweep(rec, [5, 20], 6, 123, engine=engine)
+    assert rows
+    for r in rows:
+        assert r.k_bar in (5, 20) and 0 <= r.subset_id < 6 and 0 <= r.camera_id < 40
+        assert r.err_absolute >= 0 and r.err_relative >= 0 and r.trace > 0
+    rel5 = [r.err_relative for r in rows if r.k_bar == 5]
+    rel20 = [r.err_relative for r in rows if r.k_bar == 20]
+    assert rel5 and rel20 and np.median(rel5) > np.median(rel20)
+
+
+@pytest.mark.gpu
+def test_sweep_rows_survive_a_csv_round_trip(engine, tmp_path):  # test_subrec.cpp:232-257
+    rec = S.generate_cube_scene(7, 0.5)
+    rows = R.error_size_sweep(rec, [4], 2, 11, engine=engine)
+    p = tmp_path / "sweep.csv"
+    R.write_sweep_csv(rows, str(p))
+    lines = p.read_text().splitlines()
+    assert lines[0] == "kbar,subset_id,camera_id,err_relative,err_absolute,trace"
+    back = [l.split(",") for l in lines[1:] if l]
+    assert len(back) == len(rows)
+    for r, f in zip(rows, back):
+        assert (int(f[0]), int(f[1]), int(f[2])) == (r.k_bar, r.subset_id, r.camera_id)
+        assert (float(f[3]), float(f[4]), float(f[5])) == (r.err_relative, r.err_absolute, r.trace)

@@ -459,3 +459,33 @@ def plan_chunks(nchunks: int, nranks: int, rank: int):
     if code:
         raise Error(code, "options", "invalid plan arguments")
     return b.value, e.value
+
+
+# ---- Eq. 42 error metric (include/sfmcov/oracle.hpp:39-50, src/oracle.cpp:74-110) ---
+@dataclass
+class ErrorReport:
+    per_camera: np.ndarray
+    normalization: np.ndarray  # O, strictly positive after the fallback
+    mean: float
+    median: float
+    zero_components: List[int]
+
+
+def error_metric(gt: np.ndarray, est: np.ndarray, rec: Reconstruction) -> ErrorReport:
+    """Per camera: mean over the P^2 block entries of sqrt|gt - est| divided
+    element-wise by O = sqrt(e e^T), e the component-wise mean of |camera
+    parameter| over the scene (zero components fall back to 1)."""
+    n, P = rec.num_cameras(), rec.cam_params
+    gt, est = np.asarray(gt), np.asarray(est)
+    if gt.shape[0] != n or est.shape[0] != n:
+        raise Error(ErrorKind.dimension, "error-metric", "covariance lists must have one block per camera")
+    e = np.abs(rec.cams).mean(axis=0)
+    zero = [p for p in range(P) if e[p] == 0.0]
+    e = np.where(e == 0.0, 1.0, e)
+    O = np.sqrt(np.outer(e, e))
+    per = np.array([(np.sqrt(np.abs(g - x)) / O).sum() / (P * P) for g, x in zip(gt, est)])
+    srt = np.sort(per)
+    mean = float(srt.sum() / n) if n else 0.0
+    median = float(srt[n // 2] if n % 2 else 0.5 * (srt[n // 2 - 1] + srt[n // 2])) if n else 0.0
+    return ErrorReport(per, O, mean, median, zero)
+

@@ -102,3 +102,16 @@ def test_generator_preconditions():  # test_synthetic.cpp:85-91
     for args in ((1, 30, 0.5, 1, 0.0), (5, 7, 0.5, 1, 0.0), (5, 30, 0.0, 1, 0.0), (5, 30, 1.5, 1, 0.0)):
         with pytest.raises(Error):
             S.generate_random_scene(*args)
+
+
+def test_error_metric_matches_the_restatement():  # oracle.cpp:74-110 (host-only)
+    from oracle import oracle as O
+    from paper_1808_02414_b200 import sfmcov as F
+    rng = np.random.default_rng(3)
+    rec = S.generate_random_scene(12, 90, 0.4, 9, 0.5)
+    gt = rng.standard_normal((12, 8, 8))
+    est = gt + 1e-6 * rng.standard_normal((12, 8, 8))
+    r = F.error_metric(gt, est, rec)
+    mean, median, per, zero = O.error_metric(gt, est, rec.cams)
+    assert np.allclose(r.per_camera, per, rtol=1e-14) and abs(r.mean - mean) < 1e-15 and r.median == median
+    assert r.zero_components == zero

@@ -28,7 +28,7 @@
 #include <vector>
 
 namespace sfm {
-long long g_kernel_launches = 0;
+thread_local long long g_kernel_launches = 0;  // per calling thread: worker handles run concurrently
 }
 
 namespace {

@@ -69,7 +69,7 @@ struct CudaError : std::runtime_error {
 
 // Every kernel launch of this library is followed by SFM_LAUNCH_CHECK(),
 // which also counts it (sfmcov_cuda_last_counts reports the total).
-extern long long g_kernel_launches;
+extern thread_local long long g_kernel_launches;
 #define SFM_LAUNCH_CHECK()                  \
     do {                                    \
         ++::sfm::g_kernel_launches;         \

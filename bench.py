@@ -134,8 +134,10 @@ def barrier(world: int):
 
 
 def scene_bytes(rec):
+    """Bytes the host API copies to the device per call: every scene array but
+    the pixels u, which the library only validates (finite) and does so on the
+    host while the rest uploads."""
     return (rec.cams.nbytes + rec.pts.nbytes + rec.obs_cam.nbytes + rec.obs_pt.nbytes +
-            (rec.obs_u.nbytes if rec.obs_u is not None else 0) +
             (rec.obs_sigma.nbytes if rec.obs_sigma is not None else 0))
 
 

@@ -17,14 +17,16 @@
 #include "dist.h"
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unistd.h>
-#include <vector>
 #include <vector>
 
 namespace sfm {
@@ -55,15 +57,16 @@ struct sfmcov_handle {
     int device = 0;
     cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr, s4 = nullptr;
     cudaEvent_t eX = nullptr, eN = nullptr;
+    cudaEvent_t e_index = nullptr, e_pairs = nullptr;  // pair-list build on s2, overlapped with stage A
     cudaEvent_t e1 = nullptr, e2 = nullptr;
     static constexpr int kRing = 4;  // panel ring buffers of the fused sweep
     cudaEvent_t eL[kRing], eT[kRing];
     cudaEvent_t ev[ST_COUNT + 1];
     bool profiling = false;
     std::mutex mu;
-    Workspace ws;
+    Workspace ws, ws_pairs;
     // host-API staging of the scene
-    DBuf h_cams, h_pts, h_oc, h_op, h_u, h_sigma;
+    DBuf h_cams, h_pts, h_oc, h_op, h_sigma;
     // index
     DBuf cnt_cam, cnt_pt, off_cam, idx_cam, off_pt, idx_pt, pos_cam, key_scratch;
     // stage buffers
@@ -374,6 +377,29 @@ void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const dou
                    const double* G, const double* Wb, Status* st, const unsigned char* flags, size_t ncols,
                    const double* eigE);
 
+// First observation whose pixel u is not finite (LLONG_MAX if none); up to 8
+// host threads for large scenes.
+long long first_nonfinite_u(const double* u, long long t) {
+    auto scan = [u](long long b, long long e) -> long long {
+        for (long long k = b; k < e; ++k) {
+            uint64_t x, y;
+            std::memcpy(&x, u + 2 * k, 8);
+            std::memcpy(&y, u + 2 * k + 1, 8);
+            if (((x >> 52) & 0x7ff) == 0x7ff || ((y >> 52) & 0x7ff) == 0x7ff) return k;
+        }
+        return LLONG_MAX;
+    };
+    const long long kChunk = 1LL << 19;
+    if (t <= kChunk) return scan(0, t);
+    const int nt = (int)std::min<long long>(8, (t + kChunk - 1) / kChunk);
+    std::vector<long long> r(nt, LLONG_MAX);
+    std::vector<std::thread> th;
+    for (int i = 1; i < nt; ++i) th.emplace_back([&, i] { r[i] = scan(t * i / nt, t * (i + 1) / nt); });
+    r[0] = scan(0, t / nt);
+    for (auto& x : th) x.join();
+    return *std::min_element(r.begin(), r.end());
+}
+
 // The whole device pipeline.  `sc` points at device memory.
 void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     cudaStream_t s = h->s;
@@ -391,7 +417,11 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     int* cnt_cam = h->cnt_cam.as<int>(n + 1);
     int* cnt_pt = h->cnt_pt.as<int>(m + 1);
     launch_validate(sc, full ? 1 : 0, st, cnt_cam, cnt_pt, s);
+    // host-API scenes: the finiteness of u is checked here, overlapping the
+    // upload, and merged as the reference's code-3 failure of that observation
+    const long long u_bad = (full && sc.host_u) ? first_nonfinite_u(sc.host_u, t) : LLONG_MAX;
     sync_status(h);
+    if (u_bad != LLONG_MAX) h->st_host->obs_bad = std::min(h->st_host->obs_bad, u_bad * 8 + 3);
     throw_validation(h, sc, full);
     IndexDev ix;
     ix.off_cam = h->off_cam.as<int>(n + 1);
@@ -402,6 +432,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     ix.key_scratch = h->key_scratch.as<int>(t);
     launch_build_index(sc, cnt_cam, cnt_pt, ix, h->ws, s);
     launch_structure_check(sc, ix, st, s);
+    SFM_CUDA(cudaEventRecord(h->e_index, s));
     if (full || mode == M_INDEX) {
         sync_status(h);
         if (h->st_host->dup) throw ApiError{SFMCOV_ERR_INVARIANT, "validate", "duplicate (camera, point) observation pair"};
@@ -507,7 +538,13 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     double* G = h->G.as<double>((size_t)N * 7);
     launch_camera_border(sc, ix, Wb, V, Hr, s_a, s_b, LF, Gamma, G, s);
     mark(h, 4);
-    build_pairs(sc, ix, h->pairs, h->ws, s);
+    // The pair list depends only on the index: it is built on s2 from the
+    // index event while s runs the numeric stage-A kernels queued above (its
+    // host reads of the list sizes then stall s2 only).
+    SFM_CUDA(cudaStreamWaitEvent(h->s2, h->e_index, 0));
+    build_pairs(sc, ix, h->pairs, h->ws_pairs, h->s2);
+    SFM_CUDA(cudaEventRecord(h->e_pairs, h->s2));
+    SFM_CUDA(cudaStreamWaitEvent(s, h->e_pairs, 0));
     mark(h, 5);
     if (h->dist_mode && mode == M_FULL) {
         run_dist_tail(h, sc, out, D, s_a, G, Wb, st, flags, ncols, eigE);
@@ -746,7 +783,8 @@ SceneDev upload(sfmcov_handle* h, const sfmcov_scene* s) {
     d.pts = (const double*)put(h->h_pts, s->pts, 24 * (size_t)d.m);
     d.oc = (const int*)put(h->h_oc, s->obs_cam, 4 * (size_t)d.t);
     d.op = (const int*)put(h->h_op, s->obs_pt, 4 * (size_t)d.t);
-    d.u = s->obs_u ? (const double*)put(h->h_u, s->obs_u, 16 * (size_t)d.t) : nullptr;
+    d.u = nullptr;  // validated on the host (run()), never read on the device
+    d.host_u = s->obs_u;
     d.sigma = s->obs_sigma ? (const double*)put(h->h_sigma, s->obs_sigma, 32 * (size_t)d.t) : nullptr;
     return d;
 }
@@ -819,6 +857,8 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s4, cudaStreamNonBlocking, hi));
         SFM_CUDA(cudaEventCreateWithFlags(&h->eX, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->eN, cudaEventDisableTiming));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->e_index, cudaEventDisableTiming));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->e_pairs, cudaEventDisableTiming));
         for (int i = 0; i < sfmcov_handle::kRing; ++i) {
             SFM_CUDA(cudaEventCreateWithFlags(&h->eL[i], cudaEventDisableTiming));
             SFM_CUDA(cudaEventCreateWithFlags(&h->eT[i], cudaEventDisableTiming));
@@ -844,7 +884,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaStreamSynchronize(h->s2);
     cudaStreamSynchronize(h->s3);
     cudaStreamSynchronize(h->s4);
-    DBuf* bufs[] = {&h->ws.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_u, &h->h_sigma, &h->cnt_cam,
+    DBuf* bufs[] = {&h->ws.tmp, &h->ws_pairs.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_sigma, &h->cnt_cam,
                     &h->cnt_pt, &h->off_cam, &h->idx_cam, &h->off_pt, &h->idx_pt, &h->pos_cam, &h->key_scratch,
                     &h->R, &h->rec, &h->D, &h->Hr, &h->A, &h->s_a, &h->flags, &h->bpart, &h->s_b, &h->Lpt, &h->Wb, &h->V,
                     &h->Fpart, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->Lp, &h->ring, &h->piv,
@@ -876,6 +916,8 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaStreamDestroy(h->s4);
     cudaEventDestroy(h->eX);
     cudaEventDestroy(h->eN);
+    cudaEventDestroy(h->e_index);
+    cudaEventDestroy(h->e_pairs);
     for (int i = 0; i < sfmcov_handle::kRing; ++i) {
         cudaEventDestroy(h->eL[i]);
         cudaEventDestroy(h->eT[i]);

@@ -48,6 +48,9 @@ struct SceneDev {
     const int* op;
     const double* u;
     const double* sigma;
+    // host copy of u for the host API: u is only validated (finite), so it is
+    // scanned on the host while the rest of the scene uploads, not copied
+    const double* host_u = nullptr;
 };
 
 // CSR observation index (ascending observation ids per bucket) and the

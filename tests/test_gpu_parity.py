@@ -275,6 +275,67 @@ def test_validation_messages_match_the_restatement(engine, mutate, fragment):
     assert e.value.kind == F.ErrorKind.invariant
 
 
+def _set_u_nan(r, t):
+    r.obs_u[t, 0] = np.nan
+
+
+@pytest.mark.parametrize("mutate", [
+    lambda r: (_set_u_nan(r, 3), r.obs_sigma.__setitem__((2, 0, 1), 0.3)),   # asym at 2 before u at 3
+    lambda r: (_set_u_nan(r, 2), r.obs_sigma.__setitem__((3, 0, 1), 0.3)),   # u at 2 before asym at 3
+    lambda r: (_set_u_nan(r, 4), r.obs_cam.__setitem__(4, 99)),              # same observation: index first
+    lambda r: (_set_u_nan(r, 4), r.obs_sigma.__setitem__((4, 0, 1), 0.3)),   # same observation: finiteness first
+    lambda r: (_set_u_nan(r, 7), r.obs_pt.__setitem__(9, -1)),               # u first, index later
+    lambda r: (_set_u_nan(r, 9), r.obs_pt.__setitem__(7, -1)),               # index first, u later
+])
+def test_host_checked_u_keeps_the_reference_precedence(engine, mutate):
+    """The host API checks u on the host while the scene uploads; the first
+    failing observation and the per-observation check order must still be the
+    reference's (scene.cpp validate)."""
+    rec = S.generate_cube_scene(1, 0.5)
+    mutate(rec)
+    with pytest.raises(F.Error) as e:
+        engine.compute_covariance(rec)
+    with pytest.raises(O.OracleFailure) as eo:
+        O.compute_covariance(rec)
+    assert str(e.value) == str(eo.value)
+
+
+def test_host_checked_u_on_a_large_scene(engine):
+    """> 2^19 observations: the host scan runs on several threads."""
+    rec = S.generate_config(3)
+    t = rec.num_observations()
+    bad = [t - 5, t // 2 + 11, 1_000_003]  # in different scan chunks
+    rec.obs_u[bad[0], 1] = np.inf
+    rec.obs_u[bad[1], 0] = np.nan
+    rec.obs_u[bad[2], 0] = -np.inf
+    with pytest.raises(F.Error) as e:
+        engine.compute_covariance(rec)
+    assert f"validate: observation {min(bad)} has non-finite values" in str(e.value)
+
+
+def test_device_api_still_checks_u(engine):
+    """Device-resident scenes are validated on the device (u included)."""
+    import ctypes as C
+    import torch
+    from paper_1808_02414_b200 import _native as N
+    rec = S.generate_cube_scene(1, 0.5)
+    rec.obs_u[5, 1] = np.nan
+    dev = torch.device("cuda", 0)
+    tens = {k: torch.from_numpy(getattr(rec, k)).to(dev) for k in ("cams", "pts", "obs_cam", "obs_pt", "obs_u", "obs_sigma")}
+    P, n = rec.cam_params, rec.num_cameras()
+    d_cov = torch.empty((n, P, P), dtype=torch.float64, device=dev)
+    sc = N.Scene()
+    sc.n_cams, sc.n_pts, sc.n_obs, sc.cam_params = n, rec.num_points(), rec.num_observations(), P
+    sc.cams, sc.pts = tens["cams"].data_ptr(), tens["pts"].data_ptr()
+    sc.obs_cam, sc.obs_pt = tens["obs_cam"].data_ptr(), tens["obs_pt"].data_ptr()
+    sc.obs_u, sc.obs_sigma = tens["obs_u"].data_ptr(), tens["obs_sigma"].data_ptr()
+    torch.cuda.synchronize()
+    opts, diag, err = N.Options(0, 0, 0, 0), N.Diagnostics(), N.ErrorStruct()
+    code = N.cuda_lib().sfmcov_cuda_compute_covariance_device(engine.handle, C.byref(sc), C.byref(opts),
+                                                             d_cov.data_ptr(), C.byref(diag), C.byref(err))
+    assert code != 0 and "validate: observation 5 has non-finite values" in err.message.decode()
+
+
 def test_count_floor_messages(engine):
     rec = S.generate_cube_scene(1, 0.5)
     keep = rec.obs_cam != 2

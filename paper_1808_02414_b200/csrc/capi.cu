@@ -58,6 +58,7 @@ struct sfmcov_handle {
     cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr, s4 = nullptr;
     cudaEvent_t eX = nullptr, eN = nullptr;
     cudaEvent_t e_index = nullptr, e_pairs = nullptr;  // pair-list build on s2, overlapped with stage A
+    cudaEvent_t e_ids = nullptr, e_sigma = nullptr;    // host API: σ uploads on s3 after the indices
     cudaEvent_t e1 = nullptr, e2 = nullptr;
     static constexpr int kRing = 4;  // panel ring buffers of the fused sweep
     cudaEvent_t eL[kRing], eT[kRing];
@@ -408,6 +409,12 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     if (n < 0 || m < 0 || t < 0) throw ApiError{SFMCOV_ERR_DIMENSION, "validate", "negative scene size"};
     if ((long long)n * n >= (1LL << 32)) throw ApiError{SFMCOV_ERR_SIZE_GUARD, "validate", "too many cameras for 32-bit pair keys"};
     const bool full = (mode == M_FULL || mode == M_SCHUR || mode == M_INDEX);
+    // a host-API σ transfer still in flight is waited for on every exit, so
+    // the caller's buffer is never read after the call returns
+    struct SigmaWait {
+        cudaEvent_t e;
+        ~SigmaWait() { if (e) cudaEventSynchronize(e); }
+    } sigma_wait{sc.sigma_ready};
     for (auto& v : h->stage_ms) v = 0.0;
     g_kernel_launches = 0;
     h->counts[9] = 0;
@@ -420,8 +427,22 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     // host-API scenes: the finiteness of u is checked here, overlapping the
     // upload, and merged as the reference's code-3 failure of that observation
     const long long u_bad = (full && sc.host_u) ? first_nonfinite_u(sc.host_u, t) : LLONG_MAX;
-    sync_status(h);
-    if (u_bad != LLONG_MAX) h->st_host->obs_bad = std::min(h->st_host->obs_bad, u_bad * 8 + 3);
+    auto sync_validation = [&] {
+        sync_status(h);
+        if (u_bad != LLONG_MAX) h->st_host->obs_bad = std::min(h->st_host->obs_bad, u_bad * 8 + 3);
+    };
+    sync_validation();
+    const bool split_values = full && sc.sigma_ready;  // σ checks after its upload
+    if (split_values) {
+        const Status& q = *h->st_host;
+        if (q.cam_bad != INT_MAX || q.pt_bad != INT_MAX || q.obs_bad != LLONG_MAX) {
+            // failing scene: finish the value checks so the first failing
+            // observation is reported, as the reference's single pass does
+            SFM_CUDA(cudaStreamWaitEvent(s, sc.sigma_ready, 0));
+            launch_validate_values(sc, st, s);
+            sync_validation();
+        }
+    }
     throw_validation(h, sc, full);
     IndexDev ix;
     ix.off_cam = h->off_cam.as<int>(n + 1);
@@ -433,8 +454,11 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     launch_build_index(sc, cnt_cam, cnt_pt, ix, h->ws, s);
     launch_structure_check(sc, ix, st, s);
     SFM_CUDA(cudaEventRecord(h->e_index, s));
+    if (sc.sigma_ready) SFM_CUDA(cudaStreamWaitEvent(s, sc.sigma_ready, 0));
+    if (split_values) launch_validate_values(sc, st, s);
     if (full || mode == M_INDEX) {
-        sync_status(h);
+        sync_validation();
+        if (split_values) throw_validation(h, sc, full);
         if (h->st_host->dup) throw ApiError{SFMCOV_ERR_INVARIANT, "validate", "duplicate (camera, point) observation pair"};
         throw_counts(h);
     }
@@ -785,7 +809,20 @@ SceneDev upload(sfmcov_handle* h, const sfmcov_scene* s) {
     d.op = (const int*)put(h->h_op, s->obs_pt, 4 * (size_t)d.t);
     d.u = nullptr;  // validated on the host (run()), never read on the device
     d.host_u = s->obs_u;
-    d.sigma = s->obs_sigma ? (const double*)put(h->h_sigma, s->obs_sigma, 32 * (size_t)d.t) : nullptr;
+    // σ (the largest array) follows the indices on s3, so validation of the
+    // indices and the index build on s overlap its transfer
+    d.sigma = nullptr;
+    if (s->obs_sigma) {
+        void* p = h->h_sigma.get(32 * (size_t)d.t);
+        d.sigma = (const double*)p;
+        if (d.t) {
+            SFM_CUDA(cudaEventRecord(h->e_ids, h->s));
+            SFM_CUDA(cudaStreamWaitEvent(h->s3, h->e_ids, 0));
+            SFM_CUDA(cudaMemcpyAsync(p, s->obs_sigma, 32 * (size_t)d.t, cudaMemcpyHostToDevice, h->s3));
+            SFM_CUDA(cudaEventRecord(h->e_sigma, h->s3));
+            d.sigma_ready = h->e_sigma;
+        }
+    }
     return d;
 }
 
@@ -859,6 +896,8 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
         SFM_CUDA(cudaEventCreateWithFlags(&h->eN, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->e_index, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->e_pairs, cudaEventDisableTiming));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->e_ids, cudaEventDisableTiming));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->e_sigma, cudaEventDisableTiming));
         for (int i = 0; i < sfmcov_handle::kRing; ++i) {
             SFM_CUDA(cudaEventCreateWithFlags(&h->eL[i], cudaEventDisableTiming));
             SFM_CUDA(cudaEventCreateWithFlags(&h->eT[i], cudaEventDisableTiming));
@@ -918,6 +957,8 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaEventDestroy(h->eN);
     cudaEventDestroy(h->e_index);
     cudaEventDestroy(h->e_pairs);
+    cudaEventDestroy(h->e_ids);
+    cudaEventDestroy(h->e_sigma);
     for (int i = 0; i < sfmcov_handle::kRing; ++i) {
         cudaEventDestroy(h->eL[i]);
         cudaEventDestroy(h->eT[i]);

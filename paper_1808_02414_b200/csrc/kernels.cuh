@@ -51,6 +51,9 @@ struct SceneDev {
     // host copy of u for the host API: u is only validated (finite), so it is
     // scanned on the host while the rest of the scene uploads, not copied
     const double* host_u = nullptr;
+    // host API: the covariances upload on a side stream after the indices;
+    // recorded when they have arrived (null: already on the library stream)
+    cudaEvent_t sigma_ready = nullptr;
 };
 
 // CSR observation index (ascending observation ids per bucket) and the
@@ -117,6 +120,7 @@ struct GemmArgs {
 // stage_a.cu
 void launch_status_init(Status* st, cudaStream_t s);
 void launch_validate(const SceneDev& sc, int check_sigma, Status* st, int* cam_cnt, int* pt_cnt, cudaStream_t s);
+void launch_validate_values(const SceneDev& sc, Status* st, cudaStream_t s);
 void launch_build_index(const SceneDev& sc, const int* cam_cnt, const int* pt_cnt, IndexDev& ix, Workspace& ws,
                         cudaStream_t s);
 void launch_structure_check(const SceneDev& sc, const IndexDev& ix, Status* st, cudaStream_t s);

@@ -47,8 +47,23 @@ __global__ void k_validate_pts(const double* pts, int m, Status* st) {
     if (!(finite_d(X[0]) && finite_d(X[1]) && finite_d(X[2]))) atomicMin(&st->pt_bad, j);
 }
 
+// Finiteness / symmetry / definiteness of one observation (codes 3, 4, 5 of
+// scene.cpp validate; 0 = fine).  u may be null (checked on the host).
+__device__ __forceinline__ int obs_value_code(const double* u, const double* sigma, int t) {
+    double s00 = 1.0, s01 = 0.0, s10 = 0.0, s11 = 1.0;
+    if (sigma) { s00 = sigma[4 * (size_t)t]; s01 = sigma[4 * (size_t)t + 1]; s10 = sigma[4 * (size_t)t + 2]; s11 = sigma[4 * (size_t)t + 3]; }
+    const bool ufin = !u || (finite_d(u[2 * (size_t)t]) && finite_d(u[2 * (size_t)t + 1]));
+    if (!ufin || !finite_d(s00) || !finite_d(s01) || !finite_d(s10) || !finite_d(s11)) return 3;
+    const double scale = fmax(fmax(fmax(fabs(s00), fabs(s11)), fabs(s01)), 1e-300);
+    if (fabs(s01 - s10) > 1e-12 * scale) return 4;
+    const double det = s00 * s11 - s01 * s10;
+    if (!(s00 > 0.0) || !(det > 0.0)) return 5;
+    return 0;
+}
+
 // check_sigma = 1: full scene validation; 0: only index ranges (stage APIs
-// that, like the reference functions, do not validate).
+// that, like the reference functions, do not validate, and host-API scenes
+// whose covariances are still uploading: k_validate_values checks them).
 __global__ void k_validate_obs(const int* oc, const int* op, const double* u, const double* sigma, int t_count,
                                int n, int m, int check_sigma, Status* st, int* cam_cnt, int* pt_cnt) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -58,20 +73,7 @@ __global__ void k_validate_obs(const int* oc, const int* op, const double* u, co
     if (!valid) {
     } else if (ci < 0 || ci >= n) code = 1;
     else if (pj < 0 || pj >= m) code = 2;
-    else if (check_sigma) {
-        double s00 = 1.0, s01 = 0.0, s10 = 0.0, s11 = 1.0;
-        if (sigma) { s00 = sigma[4 * (size_t)t]; s01 = sigma[4 * (size_t)t + 1]; s10 = sigma[4 * (size_t)t + 2]; s11 = sigma[4 * (size_t)t + 3]; }
-        const bool ufin = !u || (finite_d(u[2 * (size_t)t]) && finite_d(u[2 * (size_t)t + 1]));
-        if (!ufin || !finite_d(s00) || !finite_d(s01) || !finite_d(s10) || !finite_d(s11)) code = 3;
-        else {
-            const double scale = fmax(fmax(fmax(fabs(s00), fabs(s11)), fabs(s01)), 1e-300);
-            if (fabs(s01 - s10) > 1e-12 * scale) code = 4;
-            else {
-                const double det = s00 * s11 - s01 * s10;
-                if (!(s00 > 0.0) || !(det > 0.0)) code = 5;
-            }
-        }
-    }
+    else if (check_sigma) code = obs_value_code(u, sigma, t);
     if (code && valid) atomicMin(&st->obs_bad, (long long)t * 8 + code);
     // counts per camera / point, warp-aggregated (a point's observations sit
     // in neighbouring lanes): one atomic per distinct index per warp
@@ -84,6 +86,15 @@ __global__ void k_validate_obs(const int* oc, const int* op, const double* u, co
         const unsigned pc = __match_any_sync(mask, ci);
         if (lane == __ffs(pc) - 1) atomicAdd(&cam_cnt[ci], __popc(pc));
     }
+}
+
+// The value checks alone (codes 3-5), once the covariances have arrived; an
+// observation with a bad index keeps its smaller code through atomicMin.
+__global__ void k_validate_values(const double* u, const double* sigma, int t_count, Status* st) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= t_count) return;
+    const int code = obs_value_code(u, sigma, t);
+    if (code) atomicMin(&st->obs_bad, (long long)t * 8 + code);
 }
 
 __global__ void k_iota(int* v, int count) {
@@ -406,7 +417,13 @@ void launch_validate(const SceneDev& sc, int check_sigma, Status* st, int* cam_c
         if (sc.n) { k_validate_cams<<<cdiv(sc.n, 256), 256, 0, s>>>(sc.cams, sc.n, sc.P, st); SFM_LAUNCH_CHECK(); }
         if (sc.m) { k_validate_pts<<<cdiv(sc.m, 256), 256, 0, s>>>(sc.pts, sc.m, st); SFM_LAUNCH_CHECK(); }
     }
-    if (sc.t) { k_validate_obs<<<cdiv(sc.t, 256), 256, 0, s>>>(sc.oc, sc.op, sc.u, sc.sigma, sc.t, sc.n, sc.m, check_sigma, st, cam_cnt, pt_cnt); SFM_LAUNCH_CHECK(); }
+    // value checks here unless the scene's covariances are still uploading
+    const int values = check_sigma && !sc.sigma_ready;
+    if (sc.t) { k_validate_obs<<<cdiv(sc.t, 256), 256, 0, s>>>(sc.oc, sc.op, sc.u, sc.sigma, sc.t, sc.n, sc.m, values, st, cam_cnt, pt_cnt); SFM_LAUNCH_CHECK(); }
+}
+
+void launch_validate_values(const SceneDev& sc, Status* st, cudaStream_t s) {
+    if (sc.t) { k_validate_values<<<cdiv(sc.t, 256), 256, 0, s>>>(sc.u, sc.sigma, sc.t, st); SFM_LAUNCH_CHECK(); }
 }
 
 static int bits_for(int v) { int b = 1; while ((1LL << b) <= v) ++b; return b; }

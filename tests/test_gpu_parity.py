@@ -286,6 +286,9 @@ def _set_u_nan(r, t):
     lambda r: (_set_u_nan(r, 4), r.obs_sigma.__setitem__((4, 0, 1), 0.3)),   # same observation: finiteness first
     lambda r: (_set_u_nan(r, 7), r.obs_pt.__setitem__(9, -1)),               # u first, index later
     lambda r: (_set_u_nan(r, 9), r.obs_pt.__setitem__(7, -1)),               # index first, u later
+    lambda r: (r.obs_sigma.__setitem__((2, 0, 1), 0.3), r.obs_cam.__setitem__(5, 99)),  # σ (uploaded last) first
+    lambda r: (r.obs_cam.__setitem__(2, 99), r.obs_sigma.__setitem__((5, 0, 1), 0.3)),  # index first, σ later
+    lambda r: (r.cams.__setitem__((3, 0), np.nan), r.obs_sigma.__setitem__(0, -np.eye(2))),  # cameras before observations
 ])
 def test_host_checked_u_keeps_the_reference_precedence(engine, mutate):
     """The host API checks u on the host while the scene uploads; the first

@@ -71,7 +71,7 @@ struct sfmcov_handle {
     // index
     DBuf cnt_cam, cnt_pt, off_cam, idx_cam, off_pt, idx_pt, pos_cam, key_scratch;
     // stage buffers
-    DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Lpt, Wb, V, Fpart, LF, E, eigE, Gamma, G, Z, Linv, Lp, ring, piv, cov,
+    DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Lpt, Wb, V, Fpart, LF, E, eigE, Gamma, G, Z, Linv, ring, piv, cov,
         psd, prange, status, depth, H;
     PairDev pairs;
     Status* st_host = nullptr;
@@ -87,10 +87,6 @@ struct sfmcov_handle {
     // worker handles for batched independent problems (sub-reconstructions),
     // owned by this handle so their streams and workspaces persist
     std::vector<sfmcov_handle*> workers;
-    // captured dense stage (Cholesky + triangular inverse), keyed by its inputs
-    cudaGraphExec_t dense_exec = nullptr;
-    const void* dense_key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    long long dense_launches = 0;
     double stage_ms[ST_COUNT] = {0};
     long long counts[10] = {0};
 };
@@ -236,31 +232,10 @@ int panel_blocks() {
     return g;
 }
 
-// SFMCOV_GRAPH=1 launches the dense stage as one captured CUDA graph instead
-// of kernel by kernel.  Off by default: measured slower on config 3
-// (27.8 vs 23.6 ms) — the graph executor orders the two lookahead branches
-// worse than the prioritised streams do, and launch overhead is not the
-// bottleneck (~650 launches against ~24 ms of GPU work).
-bool use_graph() {
-    static bool v = [] {
-        const char* e = std::getenv("SFMCOV_GRAPH");
-        const char* d = std::getenv("SFMCOV_DEBUG_SYNC");
-        return (e && e[0] == '1') && !(d && d[0] == '1');
-    }();
-    return v;
-}
-
 // SFMCOV_SERIAL_DENSE=1 runs the lookahead updates on the main stream
 // (debug aid: removes the two-stream overlap).
 bool serial_dense() {
     static bool v = [] { const char* e = std::getenv("SFMCOV_SERIAL_DENSE"); return e && e[0] == '1'; }();
-    return v;
-}
-
-// SFMCOV_SWEEP=0 selects the two-pass dense stage (Cholesky, then the
-// triangular inverse); default is the fused sweep.
-bool use_sweep() {
-    static bool v = [] { const char* e = std::getenv("SFMCOV_SWEEP"); return !(e && e[0] == '0'); }();
     return v;
 }
 
@@ -276,53 +251,14 @@ void mark(sfmcov_handle* h, int i) {
 int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv, double* piv, Status* st, bool serial,
               bool mark_stages) {
     cudaStream_t s = h->s;
-    cudaStream_t s2 = serial ? s : h->s2;
     const int pw = panel_blocks();
-    int launches = 0;
-    if (use_sweep()) {
-        double* ring = h->ring.as<double>(sweep_ring_doubles(Npad, pw, sfmcov_handle::kRing));
-        launches = dense_sweep(Z, ld, Npad, pw, Linv, piv, st, ring, sfmcov_handle::kRing, s, s2, serial ? s : h->s3,
-                               h->eL, h->eT, h->e2, serial ? s : h->s4, h->eX, h->eN);
-        if (mark_stages) {
-            mark(h, 8);
-            mark(h, 9);
-        }
-        return launches;
+    double* ring = h->ring.as<double>(sweep_ring_doubles(Npad, pw, sfmcov_handle::kRing));
+    const int launches = dense_sweep(Z, ld, Npad, pw, Linv, piv, st, ring, sfmcov_handle::kRing, s, serial ? s : h->s2,
+                                     serial ? s : h->s3, h->eL, h->eT, h->e2, serial ? s : h->s4, h->eX, h->eN);
+    if (mark_stages) {
+        mark(h, 8);
+        mark(h, 9);
     }
-    double* Lp = h->Lp.as<double>(trtri_lp_doubles(Npad, pw));
-    if (use_graph() && !serial) {
-        // one graph launch for the ~650 kernels of the dense stage; re-captured
-        // when the matrix size, panel width or any buffer address changes
-        const void* key[6] = {Z, Linv, piv, Lp, st, (const void*)(intptr_t)(Npad * 16 + pw)};
-        bool same = h->dense_exec != nullptr;
-        for (int q = 0; q < 6 && same; ++q) same = h->dense_key[q] == key[q];
-        if (!same) {
-            if (h->dense_exec) SFM_CUDA(cudaGraphExecDestroy(h->dense_exec));
-            h->dense_exec = nullptr;
-            const long long before = g_kernel_launches;
-            cudaGraph_t graph;
-            SFM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-            dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, s2, h->e1, h->e2);
-            dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, s2, h->e1, h->e2);
-            SFM_CUDA(cudaStreamEndCapture(s, &graph));
-            SFM_CUDA(cudaGraphInstantiate(&h->dense_exec, graph, 0));
-            SFM_CUDA(cudaGraphDestroy(graph));
-            h->dense_launches = g_kernel_launches - before;
-            g_kernel_launches = before;
-            for (int q = 0; q < 6; ++q) h->dense_key[q] = key[q];
-        }
-        SFM_CUDA(cudaGraphLaunch(h->dense_exec, s));
-        g_kernel_launches += h->dense_launches;
-        if (mark_stages) {
-            mark(h, 8);
-            mark(h, 9);
-        }
-        return (int)h->dense_launches;
-    }
-    launches = dense_cholesky(Z, ld, Npad, pw, Linv, piv, st, s, s2, h->e1, h->e2);
-    if (mark_stages) mark(h, 8);
-    launches += dense_trtri(Z, ld, Npad, pw, Linv, Lp, s, s2, h->e1, h->e2);
-    if (mark_stages) mark(h, 9);
     return launches;
 }
 
@@ -926,7 +862,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     DBuf* bufs[] = {&h->ws.tmp, &h->ws_pairs.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_sigma, &h->cnt_cam,
                     &h->cnt_pt, &h->off_cam, &h->idx_cam, &h->off_pt, &h->idx_pt, &h->pos_cam, &h->key_scratch,
                     &h->R, &h->rec, &h->D, &h->Hr, &h->A, &h->s_a, &h->flags, &h->bpart, &h->s_b, &h->Lpt, &h->Wb, &h->V,
-                    &h->Fpart, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->Lp, &h->ring, &h->piv,
+                    &h->Fpart, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->ring, &h->piv,
                     &h->cov, &h->psd, &h->prange, &h->status, &h->depth, &h->H};
     for (DBuf* b : bufs) b->release();
     h->pairs.release();
@@ -944,7 +880,6 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     }
     if (h->nccl) sfm::nccl_comm_destroy(h->nccl);
     for (sfmcov_handle* w : h->workers) sfmcov_cuda_destroy(w);
-    if (h->dense_exec) cudaGraphExecDestroy(h->dense_exec);
     if (h->st_host) cudaFreeHost(h->st_host);
     cudaEventDestroy(h->e1);
     cudaEventDestroy(h->e2);

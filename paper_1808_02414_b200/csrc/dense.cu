@@ -247,17 +247,6 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
     }
 }
 
-// Kernel configuration (SFMCOV_GEMM_CFG, default 2): 0 = BK 16 x 3 stages,
-// 1 = BK 32 x 3 stages, 2 = BK 16 x 4 stages.
-static int gemm_cfg() {
-    static int c = [] {
-        const char* e = std::getenv("SFMCOV_GEMM_CFG");
-        const int v = e ? std::atoi(e) : 2;
-        return (v >= 0 && v <= 2) ? v : 2;
-    }();
-    return c;
-}
-
 // Launch with the stream's priority as a per-launch attribute, so the
 // priority survives CUDA-graph capture (captured kernel nodes do not inherit
 // stream priorities).
@@ -290,17 +279,6 @@ static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) 
     else launch_prio(k_gemm<false, BK, ST, HN>, grid, CF::THREADS, CF::SMEM, s, g);
 }
 
-// CTA shape (SFMCOV_GEMM_HN): 1 = 128 x 64 tiles, two CTAs per SM (default);
-// 2 = 128 x 128 tiles, one CTA per SM.
-static int gemm_hn() {
-    static int v = [] {
-        const char* e = std::getenv("SFMCOV_GEMM_HN");
-        const int x = e ? std::atoi(e) : 1;
-        return (x == 1 || x == 2) ? x : 1;
-    }();
-    return v;
-}
-
 template <bool KM, int BK, int ST, int HN>
 static void set_smem() {
     SFM_CUDA(cudaFuncSetAttribute(k_gemm<KM, BK, ST, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -315,29 +293,21 @@ static void set_smem() {
 void dense_init_attributes() {
     static bool done = false;
     if (done) return;
-    set_smem<false, 16, 3, 2>(); set_smem<true, 16, 3, 2>();
-    set_smem<false, 32, 3, 2>(); set_smem<true, 32, 3, 2>();
     set_smem<false, 16, 4, 2>(); set_smem<true, 16, 4, 2>();
-    set_smem<false, 16, 4, 1>(); set_smem<true, 16, 4, 1>();
     set_smem<false, 16, 3, 1>(); set_smem<true, 16, 3, 1>();
     SFM_CUDA(cudaFuncSetAttribute(k_potrf_diag_fwd(), cudaFuncAttributeMaxDynamicSharedMemorySize, potrf_smem_bytes()));
     done = true;
 }
 
+// Two configurations: 128 x 64 CTAs, two per SM, BK 16 x 3 stages (every
+// launch whose output tiles are independent; config 3: 18.6 ms vs 19.1 ms for
+// 4 stages), and 128 x 128 CTAs, one per SM, BK 16 x 4 stages for in-place
+// launches (whole_tile: C aliases A, so one CTA must own a whole tile row).
 void launch_gemm(const GemmArgs& g, cudaStream_t s) {
     const long long tiles = g.tri ? (long long)g.tm * (g.tm + 1) / 2 : (long long)g.tm * g.tn;
     if (tiles <= 0) return;
-    if (gemm_hn() == 1 && !g.whole_tile) {
-        // two CTAs per SM: 3 stages measured best (config 3: 18.6 vs 19.1 ms)
-        if (gemm_cfg() == 2 && std::getenv("SFMCOV_GEMM_CFG")) launch_gemm_cfg<16, 4, 1>(g, tiles, s);
-        else launch_gemm_cfg<16, 3, 1>(g, tiles, s);
-    } else {
-        switch (gemm_cfg()) {
-            case 1: launch_gemm_cfg<32, 3, 2>(g, tiles, s); break;
-            case 2: launch_gemm_cfg<16, 4, 2>(g, tiles, s); break;
-            default: launch_gemm_cfg<16, 3, 2>(g, tiles, s); break;
-        }
-    }
+    if (g.whole_tile) launch_gemm_cfg<16, 4, 2>(g, tiles, s);
+    else launch_gemm_cfg<16, 3, 1>(g, tiles, s);
     SFM_LAUNCH_CHECK();
 }
 
@@ -610,55 +580,6 @@ void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, in
 }
 
 // ----------------------------------------------------------------------------
-// Triangular inverse helpers (forward substitution X = L^-1, in place).
-// ----------------------------------------------------------------------------
-// X[k, k] = Linv_k (full tile, zeros above the diagonal).
-__global__ void k_copy_diag(double* X, long long ld, int k, const double* Linv) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= kNB * kNB) return;
-    const int r = e & (kNB - 1), c = e >> 7;
-    X[(size_t)(k * kNB + c) * ld + (size_t)k * kNB + r] = __ldcg(Linv + (size_t)c * kNB + r);
-}
-
-void launch_copy_diag(double* X, long long ld, int k, const double* Linv, cudaStream_t s) {
-    k_copy_diag<<<kNB * kNB / 256, 256, 0, s>>>(X, ld, k, Linv);
-    SFM_LAUNCH_CHECK();
-}
-
-// Copy the L panel below the diagonal block k into a contiguous buffer.
-__global__ void k_copy_panel(const double* X, long long ld, int k, int rows, double* Lp) {
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long total = (long long)rows * kNB;
-    if (e >= total) return;
-    const int r = (int)(e % rows), c = (int)(e / rows);
-    Lp[(size_t)c * rows + r] = __ldcg(X + (size_t)(k * kNB + c) * ld + (size_t)(k + 1) * kNB + r);
-}
-
-void launch_copy_panel(const double* X, long long ld, int k, int rows, double* Lp, cudaStream_t s) {
-    const long long total = (long long)rows * kNB;
-    if (!total) return;
-    k_copy_panel<<<cdiv(total, 256), 256, 0, s>>>(X, ld, k, rows, Lp);
-    SFM_LAUNCH_CHECK();
-}
-
-// Copy the W = G kNB wide L panel (block columns b0 .. b0+G) below the panel
-// into a contiguous buffer (rows x W, col-major, ld = rows).
-__global__ void k_copy_panel_w(const double* X, long long ld, int b0, int G, int rows, double* Lp) {
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long total = (long long)rows * G * kNB;
-    if (e >= total) return;
-    const int r = (int)(e % rows), c = (int)(e / rows);
-    Lp[(size_t)c * rows + r] = __ldcg(X + (size_t)(b0 * kNB + c) * ld + (size_t)(b0 + G) * kNB + r);
-}
-
-void launch_copy_panel_w(const double* X, long long ld, int b0, int G, int rows, double* Lp, cudaStream_t s) {
-    const long long total = (long long)rows * G * kNB;
-    if (!total) return;
-    k_copy_panel_w<<<cdiv(total, 256), 256, 0, s>>>(X, ld, b0, G, rows, Lp);
-    SFM_LAUNCH_CHECK();
-}
-
-// ----------------------------------------------------------------------------
 // Diagonal blocks of Z^-1 = X^T X (X = L^-1 lower), unscaled + PSD check.
 // One CTA (8 warps) per camera; each lane accumulates the P(P+1)/2 unique
 // products over a strided set of rows, then a fixed-order tree reduction.
@@ -836,156 +757,6 @@ GemmArgs gemm_args(double* C, long long ldc, const double* A, long long lda, con
     g.tm = tm; g.tn = tn; g.K = K; g.beta0_from = -1;
     return g;
 }
-
-// Blocked right-looking Cholesky of the Npad x Npad lower triangle with
-// panels of W = G kNB columns and one-panel lookahead.
-//   panel p, stream s (critical path): for each kNB block of the panel:
-//     potrf(diag) -> L21 = A21 Linv^T -> update of the panel's remaining
-//     columns (K = kNB); then the next panel's columns get the K = W update.
-//   stream s2: the rest of the trailing SYRK (K = W), overlapping the next
-//     panel's factorisation.  Ordering: rest(p) waits the panel (e1);
-//     next-panel(p) waits rest(p-1) (e2).
-int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, cudaStream_t s,
-                   cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2) {
-    const int K = Npad / kNB;  // 128-blocks
-    int launches = 0;
-    bool rest_pending = false;
-    for (int b0 = 0; b0 < K; b0 += G) {
-        const int g_here = (b0 + G <= K) ? G : K - b0;
-        // --- panel factorisation (critical path) ---
-        for (int g = 0; g < g_here; ++g) {
-            const int c = b0 + g;
-            double* Acc = Z + (size_t)c * kNB * ld + (size_t)c * kNB;
-            launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s);
-            ++launches;
-            const int below = K - c - 1;
-            if (below == 0) break;
-            GemmArgs t = gemm_args(Acc + kNB, ld, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
-            t.whole_tile = 1;  // in place: every output column reads the whole row tile
-            launch_gemm(t, s);
-            ++launches;
-            const int inner = b0 + g_here - c - 1;  // remaining columns inside the panel
-            if (inner > 0) {
-                // A[rows >= c+1, cols c+1 .. b0+g_here) -= L[rows, c] L[cols, c]^T
-                GemmArgs u = gemm_args(Z + (size_t)(c + 1) * kNB * ld + (size_t)(c + 1) * kNB, ld, Acc + kNB, ld,
-                                       Acc + kNB, ld, below, inner, kNB);
-                u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
-                launch_gemm(u, s);
-                ++launches;
-            }
-        }
-        const int nb0 = b0 + g_here;  // first block after the panel
-        const int T2 = K - nb0;       // trailing blocks
-        if (T2 <= 0) break;
-        const int W = g_here * kNB;
-        const double* L21 = Z + (size_t)b0 * kNB * ld + (size_t)nb0 * kNB;  // rows >= nb0, panel columns
-        const int gn = (T2 < G) ? T2 : G;  // next panel width in blocks
-        if (T2 > gn) {
-            SFM_CUDA(cudaEventRecord(e1, s));
-            SFM_CUDA(cudaStreamWaitEvent(s2, e1, 0));
-            const int r0 = nb0 + gn;
-            GemmArgs r = gemm_args(Z + (size_t)r0 * kNB * ld + (size_t)r0 * kNB, ld, L21 + (size_t)gn * kNB, ld,
-                                   L21 + (size_t)gn * kNB, ld, T2 - gn, T2 - gn, W);
-            r.tri = 1; r.alpha_neg = 1; r.beta = 1;
-            launch_gemm(r, s2);
-            ++launches;
-        }
-        if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, e2, 0));
-        GemmArgs u = gemm_args(Z + (size_t)nb0 * kNB * ld + (size_t)nb0 * kNB, ld, L21, ld, L21, ld, T2, gn, W);
-        u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
-        launch_gemm(u, s);
-        ++launches;
-        rest_pending = false;
-        if (T2 > gn) {
-            SFM_CUDA(cudaEventRecord(e2, s2));
-            rest_pending = true;
-        }
-        if (debug_sync()) {
-            SFM_CUDA(cudaStreamSynchronize(s));
-            SFM_CUDA(cudaStreamSynchronize(s2));
-        }
-    }
-    if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, e2, 0));
-    return launches;
-}
-
-// Blocked triangular inverse X = L^-1 in place (forward substitution by row
-// panels of W = G kNB rows).  Panel p (row blocks b0 .. b0+G):
-//   for each row block r of the panel:
-//     X[r, 0:r] = Linv_r X[r, 0:r] (GEMM, B K-major); X[r, r] = Linv_r;
-//     X[r', 0:r+1] -= L[r', r] X[r, 0:r+1] for the panel's later rows r'
-//   Lp = L[rows below the panel, panel columns] (copy; overwritten next)
-//   X[rows below, 0:b0+G] -= Lp X[panel rows, 0:b0+G]  (K = W; the panel's
-//     own column tiles start from zero)
-// with the next panel's rows on s and the rest on s2.
-int dense_trtri(double* X, long long ld, int Npad, int G, const double* Linv, double* Lp, cudaStream_t s,
-                cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2) {
-    const int K = Npad / kNB;
-    int launches = 0;
-    bool rest_pending = false;
-    double* inner_buf = Lp + (size_t)Npad * G * kNB;
-    for (int b0 = 0; b0 < K; b0 += G) {
-        const int g_here = (b0 + G <= K) ? G : K - b0;
-        // the K = W trailing product reads the panel's whole W x W diagonal
-        // block of X: its strictly upper tiles must be zero
-        for (int r = b0; r < b0 + g_here; ++r)
-            for (int c = r + 1; c < b0 + g_here; ++c)
-                SFM_CUDA(cudaMemset2DAsync(X + (size_t)c * kNB * ld + (size_t)r * kNB, 8 * ld, 0, 8 * kNB, kNB, s));
-        for (int g = 0; g < g_here; ++g) {
-            const int r = b0 + g;
-            const double* Lr = Linv + (size_t)r * kNB * kNB;
-            if (r > 0) {
-                GemmArgs a = gemm_args(X + (size_t)r * kNB, ld, Lr, kNB, X + (size_t)r * kNB, ld, 1, r, kNB);
-                a.b_kmajor = 1;
-                launch_gemm(a, s);
-                ++launches;
-            }
-            launch_copy_diag(X, ld, r, Lr, s);
-            ++launches;
-            const int later = b0 + g_here - r - 1;
-            if (later > 0) {
-                // L[r', r] for r' in the panel is still L (column block r untouched so far)
-                launch_copy_panel(X, ld, r, later * kNB, inner_buf, s);
-                ++launches;
-                GemmArgs u = gemm_args(X + (size_t)(r + 1) * kNB, ld, inner_buf, later * kNB,
-                                       X + (size_t)r * kNB, ld, later, r + 1, kNB);
-                u.b_kmajor = 1; u.alpha_neg = 1; u.beta = 1; u.beta0_from = r;
-                launch_gemm(u, s);
-                ++launches;
-            }
-        }
-        const int nb0 = b0 + g_here;
-        const int T2 = K - nb0;
-        if (T2 <= 0) break;
-        const int W = g_here * kNB;
-        const int rows = T2 * kNB;
-        if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, e2, 0));
-        rest_pending = false;
-        double* lp = Lp;  // rest(p-1), its only other reader, completed (e2 above)
-        launch_copy_panel_w(X, ld, b0, g_here, rows, lp, s);
-        ++launches;
-        const int gn = (T2 < G) ? T2 : G;
-        GemmArgs a = gemm_args(X + (size_t)nb0 * kNB, ld, lp, rows, X + (size_t)b0 * kNB, ld, gn, nb0, W);
-        a.b_kmajor = 1; a.alpha_neg = 1; a.beta = 1; a.beta0_from = b0;
-        if (T2 > gn) {
-            SFM_CUDA(cudaEventRecord(e1, s));
-            SFM_CUDA(cudaStreamWaitEvent(s2, e1, 0));
-            GemmArgs r = a;
-            r.C = X + (size_t)(nb0 + gn) * kNB;
-            r.A = lp + (size_t)gn * kNB;
-            r.tm = T2 - gn;
-            launch_gemm(r, s2);
-            ++launches;
-            SFM_CUDA(cudaEventRecord(e2, s2));
-            rest_pending = true;
-        }
-        launch_gemm(a, s);
-        ++launches;
-    }
-    if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, e2, 0));
-    return launches;
-}
-
 
 // ----------------------------------------------------------------------------
 // Fused sweep: Cholesky and triangular inverse in one pass over the panels.

@@ -153,24 +153,15 @@ void launch_gemm(const GemmArgs& g, cudaStream_t s);
 GemmArgs gemm_args(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb, int tm,
                    int tn, int K);
 void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s);
-void launch_copy_diag(double* X, long long ld, int k, const double* Linv, cudaStream_t s);
-void launch_copy_panel(const double* X, long long ld, int k, int rows, double* Lp, cudaStream_t s);
-void launch_copy_panel_w(const double* X, long long ld, int b0, int G, int rows, double* Lp, cudaStream_t s);
 void launch_extract(int P, const double* X, long long ld, int N, int nblocks, const double* s_a, int scale, double* cov,
                     Status* st, int* psd_warn, cudaStream_t s);
 void launch_set_diag(double* Z, long long ld, int from, int to, cudaStream_t s);
 void launch_minmax(const double* x, long long count, double* part, double* out, cudaStream_t s);
 void launch_pivot_range(const double* piv, int N, double* out, cudaStream_t s);
-int dense_cholesky(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, cudaStream_t s,
-                   cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2);
-int dense_trtri(double* X, long long ld, int Npad, int G, const double* Linv, double* Lp, cudaStream_t s,
-                cudaStream_t s2, cudaEvent_t e1, cudaEvent_t e2);
-// Lp workspace (doubles) dense_trtri needs for panel width G.
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
                 cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN);
 inline size_t sweep_ring_doubles(int Npad, int G, int NB) { return (size_t)NB * Npad * G * kNB; }
-inline size_t trtri_lp_doubles(int Npad, int G) { return (size_t)Npad * kNB * G + (size_t)kNB * kNB * G; }
 
 // ---- optional outputs (fullcov.cu) ------------------------------------------
 struct FullCovArgs {

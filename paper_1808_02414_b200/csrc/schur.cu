@@ -368,65 +368,7 @@ __global__ void k_pair_gen(const int* off_pt, const int* idx_pt, const int* oc, 
     }
 }
 
-// Warp per camera-pair block: lanes (g, p) with g < 32/P groups accumulate
-// row p of W_hi W_lo^T over pairs g, g+G, ... (two pairs in flight per
-// group, register-light so many warps per SM hide the gather latency);
-// groups combine in fixed order and the block is written once:
-// Z(P hi + p, P lo + q) -= acc[q].
-template <int P>
-__device__ __forceinline__ void pair_accum(double (&acc)[P], const double* Wb, unsigned long long v, int p) {
-    const double* wh = Wb + (size_t)(v >> 32) * kWStride + 3 * p;
-    const double* wl = Wb + (size_t)(v & 0xffffffffULL) * kWStride;
-    const double h0 = __ldg(wh), h1 = __ldg(wh + 1), h2 = __ldg(wh + 2);
-#pragma unroll
-    for (int q = 0; q < P; ++q)
-        acc[q] += (h0 * __ldg(wl + 3 * q) + h1 * __ldg(wl + 3 * q + 1)) + h2 * __ldg(wl + 3 * q + 2);
-}
-
-template <int P>
-__global__ void __launch_bounds__(256, 4) k_pair_reduce(const unsigned int* ukeys, const long long* seg_off, int nseg,
-                                                        const unsigned long long* vals, const double* Wb, int n,
-                                                        double* Z, long long ld) {
-    constexpr int G = 32 / P;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= nseg) return;
-    const int g = lane / P, p = lane - (lane / P) * P;
-    const bool active = g < G;
-    const long long b = seg_off[warp], e = seg_off[warp + 1];
-    double acc[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q) acc[q] = 0.0;
-    if (active) {
-        long long idx = b + g;
-        for (; idx + G < e; idx += 2 * G) {
-            const unsigned long long v0 = __ldg(vals + idx), v1 = __ldg(vals + idx + G);
-            pair_accum<P>(acc, Wb, v0, p);
-            pair_accum<P>(acc, Wb, v1, p);
-        }
-        if (idx < e) pair_accum<P>(acc, Wb, __ldg(vals + idx), p);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-        double tot = acc[q];
-#pragma unroll
-        for (int gg = 1; gg < G; ++gg) tot += __shfl_down_sync(0xffffffffu, acc[q], gg * P);
-        acc[q] = tot;
-    }
-    if (lane < P) {
-        const unsigned int key = ukeys[warp];
-        const int lo = (int)(key / (unsigned int)n), hi = (int)(key - (unsigned int)lo * (unsigned int)n);
-        const size_t row = (size_t)P * hi + p;
-#pragma unroll
-        for (int q = 0; q < P; ++q) {
-            double* z = Z + ((size_t)P * lo + q) * ld + row;
-            *z = *z - acc[q];
-        }
-    }
-}
-
-// Tensor-core variant (default): warp per camera-pair block, one FP64
+// Tensor-core pair reduction: warp per camera-pair block, one FP64
 // m8n8k4 MMA per pair and 8x8 tile.  With r = lane/4, k = lane%4 every lane
 // loads a = W_hi[r][k] and b = W_lo[r][k] (k = 3 is the zero pad), and the
 // MMA yields out(p, q) = Σ_k W_hi[p][k] W_lo[q][k] for p, q < 8 with lane
@@ -689,24 +631,18 @@ void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace&
 void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, cudaStream_t s) {
     if (!pd.nseg) return;
     const unsigned blocks = cdiv(pd.nseg, 8);
-    static const bool scalar = [] { const char* e = std::getenv("SFMCOV_PAIR_SCALAR"); return e && e[0] == '1'; }();
-    if (scalar) {
-        if (P == 8) k_pair_reduce<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
-        else k_pair_reduce<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.vals, Wb, n, Z, ld);
-    } else {
-        const unsigned cblocks = cdiv(pd.nchunks, 8);
-        // 4 pairs gathered ahead, 4 CTAs (32 warps) per SM: the kernel is
-        // bound by gather latency, so occupancy beats deeper prefetch
-        if (P == 8)
-            k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, pd.nchunks,
-                                                                pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0);
-        else
-            k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, pd.nchunks,
-                                                                pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0);
-        SFM_LAUNCH_CHECK();
-        if (P == 8) k_pair_combine<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld);
-        else k_pair_combine<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld);
-    }
+    const unsigned cblocks = cdiv(pd.nchunks, 8);
+    // 4 pairs gathered ahead, 4 CTAs (32 warps) per SM: the kernel is bound
+    // by gather latency, so occupancy beats deeper prefetch
+    if (P == 8)
+        k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, pd.nchunks,
+                                                            pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0);
+    else
+        k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, pd.nchunks,
+                                                            pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0);
+    SFM_LAUNCH_CHECK();
+    if (P == 8) k_pair_combine<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld);
+    else k_pair_combine<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld);
     SFM_LAUNCH_CHECK();
 }
 

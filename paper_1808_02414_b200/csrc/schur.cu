@@ -202,54 +202,51 @@ __global__ void __launch_bounds__(128) k_border_factor(const double* Fpart, int 
     for (int c = 0; c < 7; ++c) eigE[c] = -L[7 * c + c] * L[7 * c + c];
 }
 
-// ---- camera border rows (warp per camera) ----------------------------------------
-// Γ_i[p][l] = H_s,ci[p][l] - Σ_{a in cam i} (W_a V_j(a))[p][l], ascending
-// observation order; then G_i = Γ_i L_F^-T.
+// ---- camera border rows -----------------------------------------------------------
+// Γ_i[p][l] = H_s,ci[p][l] - Σ_{a in cam i} (W_a V_j(a))[p][l]; then
+// G_i = Γ_i L_F^-T.  One CTA per camera: 8 groups of 64 threads (one per
+// entry (p, l)) take interleaved 12-observation chunks of the camera's
+// contiguous by-camera slots; the 8 group partials are added in group order,
+// so the result is deterministic.
+namespace cb {
+constexpr int GROUPS = 8, CH = 12, RS = 49;  // staged per observation: W (27) at 0, V_j (21) at 27
+constexpr int THREADS = GROUPS * 64;
+}  // namespace cb
+
 template <int P>
-__global__ void __launch_bounds__(128) k_camera_border(const int* off_cam, const int* idx_cam, const int* op,
-                                                      const double* Wb, const double* V, const double* cams,
-                                                      const double* Hr, const double* s_a, const double* s_b,
-                                                      const double* LF, int n, double* Gamma, double* G) {
-    // one CTA per camera, one thread per entry (p, l) of Γ_i (P x 7)
+__global__ void __launch_bounds__(cb::THREADS) k_camera_border(const int* off_cam, const int* idx_cam, const int* op,
+                                                               const double* Wb, const double* V, const double* cams,
+                                                               const double* Hr, const double* s_a, const double* s_b,
+                                                               const double* LF, int n, double* Gamma, double* G) {
+    using namespace cb;
     constexpr int NE = P * 7;
-    constexpr int CH = 64, RS = 49;  // staged: W (27) at 0, V_j (21) at 27
-    __shared__ double stage[CH][RS];
+    constexpr int ROUND = GROUPS * CH;  // observations staged per round
+    __shared__ double stage[ROUND][RS];
+    __shared__ double part[GROUPS][NE];
     __shared__ double sh[NE];
-    __shared__ int pid[CH];
+    __shared__ int pid[ROUND];
     const int i = blockIdx.x, tid = threadIdx.x;
-    const int p = tid / 7, l = tid % 7;
+    const int grp = tid >> 6, e = tid & 63;
+    const int p = e / 7, l = e % 7;
     double acc = 0.0;
-    const int b = off_cam[i], e = off_cam[i + 1];
-    for (int k0 = b; k0 < e; k0 += CH) {
-        const int nc = min(CH, e - k0);
-        // the chunk's point ids first (one dependent gather per observation)
+    const int b = off_cam[i], end = off_cam[i + 1];
+    for (int k0 = b; k0 < end; k0 += ROUND) {
+        const int nc = min(ROUND, end - k0);
         if (tid < nc) pid[tid] = op[idx_cam[k0 + tid]];
-        // W rows of the chunk are contiguous (by-camera slots): coalesced copy
-        for (int w = tid; w < nc * 27; w += 128) {
+        // W rows of the round are contiguous (by-camera slots): coalesced copy
+        for (int w = tid; w < nc * 27; w += THREADS) {
             const int o = w / 27, c = w - o * 27;
             stage[o][c] = Wb[(size_t)(k0 + o) * kWStride + c];
         }
         __syncthreads();
-        for (int w = tid; w < nc * 21; w += 128) {
+        for (int w = tid; w < nc * 21; w += THREADS) {
             const int o = w / 21, c = w - o * 21;
             stage[o][27 + c] = V[21 * (size_t)pid[o] + c];
         }
         __syncthreads();
-        if (tid < NE) {
-            // terms of 4 observations formed independently, added in order
-            int o = 0;
-            for (; o + 4 <= nc; o += 4) {
-                double tv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const double* w = stage[o + u];
-                    const double* vj = w + 27;
-                    tv[u] = (w[3 * p] * vj[l] + w[3 * p + 1] * vj[7 + l]) + w[3 * p + 2] * vj[14 + l];
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) acc += tv[u];
-            }
-            for (; o < nc; ++o) {
+        if (e < NE) {
+            const int o0 = grp * CH, o1 = min(o0 + CH, nc);
+            for (int o = o0; o < o1; ++o) {
                 const double* w = stage[o];
                 const double* vj = w + 27;
                 acc += (w[3 * p] * vj[l] + w[3 * p + 1] * vj[7 + l]) + w[3 * p + 2] * vj[14 + l];
@@ -257,7 +254,12 @@ __global__ void __launch_bounds__(128) k_camera_border(const int* off_cam, const
         }
         __syncthreads();
     }
+    if (e < NE) part[grp][e] = acc;
+    __syncthreads();
     if (tid < NE) {
+        double sum = part[0][tid];
+#pragma unroll
+        for (int g = 1; g < GROUPS; ++g) sum += part[g][tid];
         const double* C = cams + (size_t)P * i + 3;
         double h = 0.0;
         if (p < 3) h = (l >= 3 && l < 6) ? Hr[9 * (size_t)i + 3 * p + (l - 3)] : 0.0;
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(128) k_camera_border(const int* off_cam, const
             h = (l < 3) ? (l == a ? 1.0 : 0.0) : (l < 6 ? sx[3 * a + (l - 3)] : C[a]);
         }
         const double hs = (s_a[(size_t)P * i + p] * h) * s_b[l];
-        const double g = hs - acc;
+        const double g = hs - sum;
         sh[tid] = g;
         Gamma[(size_t)P * 7 * i + tid] = g;
     }
@@ -368,14 +370,19 @@ __global__ void k_pair_gen(const int* off_pt, const int* idx_pt, const int* oc, 
     }
 }
 
-// Tensor-core pair reduction: warp per camera-pair block, one FP64
-// m8n8k4 MMA per pair and 8x8 tile.  With r = lane/4, k = lane%4 every lane
-// loads a = W_hi[r][k] and b = W_lo[r][k] (k = 3 is the zero pad), and the
-// MMA yields out(p, q) = Σ_k W_hi[p][k] W_lo[q][k] for p, q < 8 with lane
-// holding (p = lane/4, q = 2(lane%4) + {0,1}).  For P = 9 three more tiles
-// carry row 8 / column 8 (operands non-zero on lanes 0..3 only).  The pair
-// list of a segment is read 32 at a time with one coalesced load and
-// broadcast by shuffles; four pairs are gathered ahead of their MMAs.
+// Tensor-core pair reduction: one warp per chunk (<= chunk pairs of one
+// camera-pair block).  out = Σ_pairs W_hi W_lo^T is one product over the
+// concatenated K dimension (3 entries per pair), so the FP64 m8n8k4 MMA runs
+// on packed K: step s takes elements 4s .. 4s+3 of the chunk, lane (r, k)
+// (r = lane/4, k = lane%4) loading W_hi[r][·] and W_lo[r][·] of element
+// 4s + k (pair (4s+k)/3, entry (4s+k)%3) — 3 MMAs per 4 pairs, no zero pad.
+// The MMA yields out(p, q) for p, q < 8 with lane holding (p = lane/4,
+// q = 2(lane%4) + {0,1}).  For P = 9 row 8 and column 8 are FP64 FMAs on the
+// same operands: lane (q, k) adds W_hi[8][e] W_lo[q][e] (W_hi[8][e] shuffled
+// from lane k, which loads row 8) and W_hi[q][e] W_lo[8][e]; the four
+// k-partials are summed once per chunk.  The pair list is read 32 at a time
+// with one coalesced load and distributed by shuffles; U steps are gathered
+// ahead of their MMAs.
 __device__ __forceinline__ void dmma_pr(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
@@ -388,8 +395,6 @@ __global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned in
                                                          const unsigned long long* vals, const double* Wb, int n,
                                                          double* Z, long long ld, double* part, int cfirst,
                                                          int always_part) {
-    constexpr int NT = (P == 9) ? 4 : 1;  // 8x8 tiles: (0,0) [, (8,0), (0,8), (8,8)]
-    // U: pairs gathered ahead
     const int warp = cfirst + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (warp >= nchunks) return;
@@ -402,42 +407,52 @@ __global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned in
     const int sg = lo_s;
     const int c0 = __ldg(chunk_off + sg), nch = __ldg(chunk_off + sg + 1) - c0;
     const int r = lane >> 2, k = lane & 3;
-    const bool kv = k < 3;
-    const bool r8 = (P == 9) && (r == 0) && kv;  // lanes 0..2 carry row 8
     const long long sb = seg_off[sg], se = seg_off[sg + 1];
     const long long b = sb + (long long)(warp - c0) * chunk;
     const long long e = min(se, b + chunk);
-    double c[NT][2];
-#pragma unroll
-    for (int t = 0; t < NT; ++t) c[t][0] = c[t][1] = 0.0;
+    double c0v = 0.0, c1v = 0.0;                 // MMA tile (rows 0..7, cols 0..7)
+    double r8 = 0.0, cl8 = 0.0, x88 = 0.0;       // P = 9: row 8, column 8, corner (k-partials)
     for (long long base = b; base < e; base += 32) {
         const int cnt = (int)min(32LL, e - base);
         const unsigned long long mine = (lane < cnt) ? __ldg(vals + base + lane) : 0ULL;
-        for (int i0 = 0; i0 < cnt; i0 += U) {
-            double ah[U], al[U], ah8[U], al8[U];
+        const int nel = 3 * cnt, nsteps = (nel + 3) >> 2;
+        for (int s0 = 0; s0 < nsteps; s0 += U) {
+            double ah[U], al[U], a8[U], b8[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const unsigned long long v = __shfl_sync(0xffffffffu, mine, (i0 + u) & 31);
-                const bool ok = i0 + u < cnt;
+                const int el = 4 * (s0 + u) + k;
+                const int pi = el / 3, kk = el - 3 * pi;
+                const bool ok = el < nel;
+                const unsigned long long v = __shfl_sync(0xffffffffu, mine, pi & 31);
                 const double* wh = Wb + (size_t)(v >> 32) * kWStride;
                 const double* wl = Wb + (size_t)(v & 0xffffffffULL) * kWStride;
-                ah[u] = (ok && kv) ? __ldg(wh + 3 * r + k) : 0.0;
-                al[u] = (ok && kv) ? __ldg(wl + 3 * r + k) : 0.0;
+                ah[u] = ok ? __ldg(wh + 3 * r + kk) : 0.0;
+                al[u] = ok ? __ldg(wl + 3 * r + kk) : 0.0;
                 if (P == 9) {
-                    ah8[u] = (ok && r8) ? __ldg(wh + 24 + k) : 0.0;
-                    al8[u] = (ok && r8) ? __ldg(wl + 24 + k) : 0.0;
+                    a8[u] = (ok && r == 0) ? __ldg(wh + 24 + kk) : 0.0;
+                    b8[u] = (ok && r == 0) ? __ldg(wl + 24 + kk) : 0.0;
                 }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                dmma_pr(c[0][0], c[0][1], ah[u], al[u]);
+                dmma_pr(c0v, c1v, ah[u], al[u]);
                 if (P == 9) {
-                    dmma_pr(c[NT > 1 ? 1 : 0][0], c[NT > 1 ? 1 : 0][1], ah8[u], al[u]);
-                    dmma_pr(c[NT > 2 ? 2 : 0][0], c[NT > 2 ? 2 : 0][1], ah[u], al8[u]);
-                    dmma_pr(c[NT > 3 ? 3 : 0][0], c[NT > 3 ? 3 : 0][1], ah8[u], al8[u]);
+                    const double h8 = __shfl_sync(0xffffffffu, a8[u], k);  // W_hi[8][e] from lane k
+                    const double l8 = __shfl_sync(0xffffffffu, b8[u], k);  // W_lo[8][e] from lane k
+                    r8 = fma(h8, al[u], r8);
+                    cl8 = fma(ah[u], l8, cl8);
+                    x88 = fma(a8[u], b8[u], x88);
                 }
             }
         }
+    }
+    if (P == 9) {  // sum the four k-partials (fixed order)
+        r8 += __shfl_xor_sync(0xffffffffu, r8, 1);
+        r8 += __shfl_xor_sync(0xffffffffu, r8, 2);
+        cl8 += __shfl_xor_sync(0xffffffffu, cl8, 1);
+        cl8 += __shfl_xor_sync(0xffffffffu, cl8, 2);
+        x88 += __shfl_xor_sync(0xffffffffu, x88, 1);
+        x88 += __shfl_xor_sync(0xffffffffu, x88, 2);
     }
     const unsigned int key = ukeys[sg];
     const int lo = (int)(key / (unsigned int)n), hi = (int)(key - (unsigned int)lo * (unsigned int)n);
@@ -452,15 +467,14 @@ __global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned in
         *z = *z - v;
     };
     const int q0 = 2 * k;
-    put(r, q0, c[0][0]);
-    put(r, q0 + 1, c[0][1]);
+    put(r, q0, c0v);
+    put(r, q0 + 1, c1v);
     if (P == 9) {
-        if (r == 0) {                      // tile (8, 0): row 8, columns q0, q0+1
-            put(8, q0, c[NT > 1 ? 1 : 0][0]);
-            put(8, q0 + 1, c[NT > 1 ? 1 : 0][1]);
+        if (k == 0) {
+            put(8, r, r8);   // lane (q = r, k = 0): row 8, column r
+            put(r, 8, cl8);  // row r, column 8
         }
-        if (k == 0) put(r, 8, c[NT > 2 ? 2 : 0][0]);      // tile (0, 8): column 8
-        if (lane == 0) put(8, 8, c[NT > 3 ? 3 : 0][0]);   // tile (8, 8)
+        if (lane == 0) put(8, 8, x88);
     }
 }
 
@@ -527,8 +541,8 @@ void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* 
                           const double* s_a, const double* s_b, const double* LF, double* Gamma, double* G,
                           cudaStream_t s) {
     if (!sc.n) return;
-    if (sc.P == 8) k_camera_border<8><<<sc.n, 128, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
-    else k_camera_border<9><<<sc.n, 128, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    if (sc.P == 8) k_camera_border<8><<<sc.n, cb::THREADS, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    else k_camera_border<9><<<sc.n, cb::THREADS, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
     SFM_LAUNCH_CHECK();
 }
 

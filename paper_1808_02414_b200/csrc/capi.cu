@@ -59,6 +59,7 @@ struct sfmcov_handle {
     cudaEvent_t eX = nullptr, eN = nullptr;
     cudaEvent_t e_index = nullptr, e_pairs = nullptr;  // pair-list build on s2, overlapped with stage A
     cudaEvent_t e_ids = nullptr, e_sigma = nullptr;    // host API: σ uploads on s3 after the indices
+    cudaEvent_t e_red_fork = nullptr, e_red_join = nullptr;  // point reduction on s4 beside the camera one
     cudaEvent_t e1 = nullptr, e2 = nullptr;
     static constexpr int kRing = 4;  // panel ring buffers of the fused sweep
     cudaEvent_t eL[kRing], eT[kRing];
@@ -434,7 +435,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     double* A = h->A.as<double>(9 * (size_t)m);
     double* s_a = h->s_a.as<double>(ncols);
     unsigned char* flags = h->flags.as<unsigned char>(ncols);
-    launch_reductions(sc, ix, rec, D, Hr, A, s_a, flags, st, s);
+    launch_reductions(sc, ix, rec, D, Hr, A, s_a, flags, st, s, h->s4, h->e_red_fork, h->e_red_join);
     double* bpart = h->bpart.as<double>(7 * (size_t)border_partial_blocks(n, m));
     double* s_b = h->s_b.as<double>(7);
     launch_border_scales(sc, Hr, s_a, bpart, s_b, s);
@@ -834,6 +835,8 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
         SFM_CUDA(cudaEventCreateWithFlags(&h->e_pairs, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->e_ids, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->e_sigma, cudaEventDisableTiming));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->e_red_fork, cudaEventDisableTiming));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->e_red_join, cudaEventDisableTiming));
         for (int i = 0; i < sfmcov_handle::kRing; ++i) {
             SFM_CUDA(cudaEventCreateWithFlags(&h->eL[i], cudaEventDisableTiming));
             SFM_CUDA(cudaEventCreateWithFlags(&h->eT[i], cudaEventDisableTiming));
@@ -894,6 +897,8 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaEventDestroy(h->e_pairs);
     cudaEventDestroy(h->e_ids);
     cudaEventDestroy(h->e_sigma);
+    cudaEventDestroy(h->e_red_fork);
+    cudaEventDestroy(h->e_red_join);
     for (int i = 0; i < sfmcov_handle::kRing; ++i) {
         cudaEventDestroy(h->eL[i]);
         cudaEventDestroy(h->eT[i]);

@@ -127,7 +127,8 @@ void launch_structure_check(const SceneDev& sc, const IndexDev& ix, Status* st, 
 void launch_jacobian(const SceneDev& sc, const int* idx_cam, double* R, double* rec, Status* st, cudaStream_t s);
 void launch_depth_of(const SceneDev& sc, const double* R, int t, double* out, cudaStream_t s);
 void launch_reductions(const SceneDev& sc, const IndexDev& ix, const double* rec, double* D, double* Hr, double* A,
-                       double* s_a, unsigned char* flags, Status* st, cudaStream_t s);
+                       double* s_a, unsigned char* flags, Status* st, cudaStream_t s, cudaStream_t side,
+                       cudaEvent_t fork, cudaEvent_t join);
 void launch_border_scales(const SceneDev& sc, const double* Hr, const double* s_a, double* partial, double* s_b,
                           cudaStream_t s);
 int border_partial_blocks(int n, int m);

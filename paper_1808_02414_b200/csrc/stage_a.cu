@@ -472,20 +472,28 @@ void launch_depth_of(const SceneDev& sc, const double* R, int t, double* out, cu
     SFM_LAUNCH_CHECK();
 }
 
+// The per-camera reduction (one CTA per camera, a sequential chain over its
+// observations) leaves most of each SM idle, so the independent per-point
+// reduction runs beside it on `side` (fork / join through the two events).
 void launch_reductions(const SceneDev& sc, const IndexDev& ix, const double* rec, double* D, double* Hr, double* A,
-                       double* s_a, unsigned char* flags, Status* st, cudaStream_t s) {
+                       double* s_a, unsigned char* flags, Status* st, cudaStream_t s, cudaStream_t side,
+                       cudaEvent_t fork, cudaEvent_t join) {
     const size_t ncols = (size_t)sc.P * sc.n + 3 * (size_t)sc.m;
     SFM_CUDA(cudaMemsetAsync(flags, 0, ncols, s));
+    SFM_CUDA(cudaEventRecord(fork, s));
+    SFM_CUDA(cudaStreamWaitEvent(side, fork, 0));
+    if (sc.m) {
+        if (sc.P == 8) k_point_reduce<8><<<cdiv(sc.m, 128), 128, 0, side>>>(ix.off_pt, ix.idx_pt, ix.pos_cam, rec, sc.m, sc.n, A, s_a, flags, st);
+        else k_point_reduce<9><<<cdiv(sc.m, 128), 128, 0, side>>>(ix.off_pt, ix.idx_pt, ix.pos_cam, rec, sc.m, sc.n, A, s_a, flags, st);
+        SFM_LAUNCH_CHECK();
+    }
+    SFM_CUDA(cudaEventRecord(join, side));
     if (sc.n) {
         if (sc.P == 8) k_camera_reduce<8><<<sc.n, 128, 0, s>>>(ix.off_cam, rec, sc.n, D, Hr, s_a, flags, st);
         else k_camera_reduce<9><<<sc.n, 128, 0, s>>>(ix.off_cam, rec, sc.n, D, Hr, s_a, flags, st);
         SFM_LAUNCH_CHECK();
     }
-    if (sc.m) {
-        if (sc.P == 8) k_point_reduce<8><<<cdiv(sc.m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, ix.pos_cam, rec, sc.m, sc.n, A, s_a, flags, st);
-        else k_point_reduce<9><<<cdiv(sc.m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, ix.pos_cam, rec, sc.m, sc.n, A, s_a, flags, st);
-        SFM_LAUNCH_CHECK();
-    }
+    SFM_CUDA(cudaStreamWaitEvent(s, join, 0));
 }
 
 void launch_border_scales(const SceneDev& sc, const double* Hr, const double* s_a, double* partial, double* s_b,

@@ -70,7 +70,7 @@ struct sfmcov_handle {
     // host-API staging of the scene
     DBuf h_cams, h_pts, h_oc, h_op, h_sigma;
     // index
-    DBuf cnt_cam, cnt_pt, off_cam, idx_cam, off_pt, idx_pt, pos_cam, key_scratch;
+    DBuf off_cam, idx_cam, off_pt, idx_pt, pos_cam, key_scratch;
     // stage buffers
     DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Lpt, Wb, V, Fpart, LF, E, eigE, Gamma, G, Z, Linv, ring, piv, cov,
         psd, prange, status, depth, H;
@@ -358,9 +358,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     Status* st = h->status.as<Status>(1);
     mark(h, 0);
     launch_status_init(st, s);
-    int* cnt_cam = h->cnt_cam.as<int>(n + 1);
-    int* cnt_pt = h->cnt_pt.as<int>(m + 1);
-    launch_validate(sc, full ? 1 : 0, st, cnt_cam, cnt_pt, s);
+    launch_validate(sc, full ? 1 : 0, st, s);
     // host-API scenes: the finiteness of u is checked here, overlapping the
     // upload, and merged as the reference's code-3 failure of that observation
     const long long u_bad = (full && sc.host_u) ? first_nonfinite_u(sc.host_u, t) : LLONG_MAX;
@@ -388,7 +386,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     ix.idx_pt = h->idx_pt.as<int>(t);
     ix.pos_cam = h->pos_cam.as<int>(t);
     ix.key_scratch = h->key_scratch.as<int>(t);
-    launch_build_index(sc, cnt_cam, cnt_pt, ix, h->ws, s);
+    launch_build_index(sc, ix, h->ws, s);
     launch_structure_check(sc, ix, st, s);
     SFM_CUDA(cudaEventRecord(h->e_index, s));
     if (sc.sigma_ready) SFM_CUDA(cudaStreamWaitEvent(s, sc.sigma_ready, 0));
@@ -862,8 +860,8 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaStreamSynchronize(h->s2);
     cudaStreamSynchronize(h->s3);
     cudaStreamSynchronize(h->s4);
-    DBuf* bufs[] = {&h->ws.tmp, &h->ws_pairs.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_sigma, &h->cnt_cam,
-                    &h->cnt_pt, &h->off_cam, &h->idx_cam, &h->off_pt, &h->idx_pt, &h->pos_cam, &h->key_scratch,
+    DBuf* bufs[] = {&h->ws.tmp, &h->ws_pairs.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_sigma,
+                    &h->off_cam, &h->idx_cam, &h->off_pt, &h->idx_pt, &h->pos_cam, &h->key_scratch,
                     &h->R, &h->rec, &h->D, &h->Hr, &h->A, &h->s_a, &h->flags, &h->bpart, &h->s_b, &h->Lpt, &h->Wb, &h->V,
                     &h->Fpart, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->ring, &h->piv,
                     &h->cov, &h->psd, &h->prange, &h->status, &h->depth, &h->H};

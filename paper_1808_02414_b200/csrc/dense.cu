@@ -13,7 +13,10 @@
 // CTA tile 128x128, 16 warps of 32x32, 3-stage cp.async pipeline over K.
 // The accumulator fragment is laid out so each lane owns two consecutive
 // rows of one column: C tiles move with 16-byte loads/stores.
+#include <cstdio>
 #include <cstdlib>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "detmath.cuh"
@@ -103,11 +106,13 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
     const double* B;
     double* C;
     const int coff = half * BNT;  // column offset inside the 128-wide tile
+    bool diag_tile = (g.tri || g.lower_only) && ti + g.row_off_tiles == tj + g.col_off_tiles;
     if (g.cyc_R > 0) {
         const int lt = tj + g.cyc_lt0;
         const int gt = ((lt / g.cyc_G) * g.cyc_R + g.cyc_rank) * g.cyc_G + lt % g.cyc_G;
         const int gi = ti + g.cyc_row0;
         if (gi < gt) return;
+        diag_tile = gi == gt;
         A = g.A + (size_t)(gi - g.cyc_ab0) * BM;
         B = g.B + (size_t)(gt - g.cyc_ab0) * BN + coff;  // (B row-indexed, not K-major)
         C = g.C + ((size_t)lt * BN + coff) * g.ldc + (size_t)gi * BM;
@@ -117,10 +122,13 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
         C = g.C + ((size_t)tj * BN + coff) * g.ldc + (size_t)ti * BM;
     }
     const int wm = warp & 3, wn = warp >> 2;  // 4 x (2 HN) warps of 32 x 32
+    // lower-triangular launches: on a diagonal tile, warp tiles strictly above
+    // the diagonal (never read) skip their MMAs and stores (6 of 16)
+    const bool idle = diag_tile && wm * 32 + 32 <= coff + wn * 32;
     const int beta = (g.beta && !(g.beta0_from >= 0 && tj >= g.beta0_from)) ? 1 : 0;
     int kbeg = 0;  // K offset of this tile
-    if (g.k_from_row) {
-        kbeg = ti * BM;
+    if (g.k_from_row || (g.k_from_col && tj >= g.beta0_from)) {
+        kbeg = g.k_from_row ? ti * BM : (tj - g.beta0_from) * BN;
         A = AK_MAJOR ? A + kbeg : A + (size_t)kbeg * g.lda;
         B = BK_MAJOR ? B + kbeg : B + (size_t)kbeg * g.ldb;
     }
@@ -197,6 +205,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
         cp_async_commit();
         const double* as = As + (kc % STAGES) * ASTAGE;
         const double* bs = Bs + (kc % STAGES) * BSTAGE;
+        if (idle) continue;
 #pragma unroll
         for (int kk = 0; kk < BK / 4; ++kk) {
             const int krow = kk * 4 + (lane & 3);
@@ -214,6 +223,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
                 for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], bf[ni], af[mi]);
         }
     }
+    if (idle) return;
     // epilogue in two halves; each half issues all its C loads before any
     // store (stores to C could alias them, so the compiler would otherwise
     // serialise load -> store pairs)
@@ -817,9 +827,45 @@ static void launch_panel_take(double* Z, long long ld, int b0, int W, int rows, 
     SFM_LAUNCH_CHECK();
 }
 
+// SFMCOV_SWEEP_TRACE=1 (diagnostics, tools/trace_view.py): per panel, events
+// on the critical stream (panel start, hand-over, next-column update done),
+// s2 (rest done) and s3 (inverse step done), printed to stderr in ms after
+// the first.  Config 3 showed the sweep is throughput-bound, not
+// critical-path-bound: the Cholesky chain ends at 14.2 ms, the inverse chain
+// at 17.9 ms, and a 12-slot ring left the total unchanged.
+static bool sweep_trace() {
+    static bool v = [] { const char* e = std::getenv("SFMCOV_SWEEP_TRACE"); return e && e[0] == '1'; }();
+    return v;
+}
+struct SweepTrace {
+    std::vector<cudaEvent_t> ev;
+    std::vector<std::pair<int, int>> tag;  // (panel, point)
+    void rec(int p, int what, cudaStream_t st) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        ev.push_back(e);
+        tag.push_back({p, what});
+    }
+    void dump() {
+        if (ev.empty()) return;
+        cudaDeviceSynchronize();
+        static const char* names[] = {"start", "take", "next1", "rest", "inv"};
+        for (size_t i = 0; i < ev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[0], ev[i]);
+            std::fprintf(stderr, "trace p=%d %s %.4f\n", tag[i].first, names[tag[i].second], ms);
+        }
+        for (auto e : ev) cudaEventDestroy(e);
+        cudaGetLastError();
+    }
+};
+
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
                 cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN) {
+    SweepTrace tr;
+    const bool trace = sweep_trace();
     bool next_pending = false;  // the previous step's update of the next panel's later columns (s4)
     const int K = Npad / kNB;
     int launches = 0;
@@ -836,6 +882,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
         if (p >= NB) SFM_CUDA(cudaStreamWaitEvent(s, eT[slot], 0));  // inverse step p - NB done with Lb
         const int rows = Npad - b0 * kNB;
         double* Lb = ring + (size_t)slot * Npad * G * kNB;
+        if (trace) tr.rec(p, 0, s);
         for (int g = 0; g < g_here; ++g) {
             const int c = b0 + g;
             double* Acc = Z + (size_t)c * kNB * ld + (size_t)c * kNB;
@@ -862,6 +909,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
         launch_panel_take_diag(Z, ld, b0, W, Lb, rows, s);
         ++launches;
         SFM_CUDA(cudaEventRecord(eL[slot], s));
+        if (trace) tr.rec(p, 1, s);
         const int nb0 = b0 + g_here;
         const int T2 = K - nb0;
         const int gn = (T2 < G) ? T2 : G;
@@ -875,6 +923,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             r.tri = 1; r.alpha_neg = 1; r.beta = 1;
             launch_gemm(r, s2);
             ++launches;
+            if (trace) tr.rec(p, 3, s2);
         }
         next_pending = false;
         if (T2 > 0) {
@@ -889,6 +938,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
             launch_gemm(u, s);
             ++launches;
+            if (trace) tr.rec(p, 2, s);
             if (split) {
                 SFM_CUDA(cudaStreamWaitEvent(s4, eX, 0));
                 GemmArgs v = gemm_args(Z + (size_t)(nb0 + 1) * kNB * ld + (size_t)nb0 * kNB, ld, Lb + W, rows,
@@ -926,10 +976,12 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
         if (T2 > 0) {
             GemmArgs x = gemm_args(Z + (size_t)nb0 * kNB, ld, Lb + W, rows, Z + (size_t)b0 * kNB, ld, T2, nb0, W);
             x.b_kmajor = 1; x.alpha_neg = 1; x.beta = 1; x.beta0_from = b0;
+            x.k_from_col = 1;  // X[panel rows, panel columns] is lower triangular: skip its zero K range
             launch_gemm(x, s3);
             ++launches;
         }
         SFM_CUDA(cudaEventRecord(eT[slot], s3));
+        if (trace) tr.rec(p, 4, s3);
         last_slot = slot;
         if (debug_sync()) {
             SFM_CUDA(cudaStreamSynchronize(s));
@@ -940,6 +992,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
     if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, eR, 0));
     if (next_pending) SFM_CUDA(cudaStreamWaitEvent(s, eN, 0));
     if (last_slot >= 0) SFM_CUDA(cudaStreamWaitEvent(s, eT[last_slot], 0));
+    if (trace) tr.dump();
     return launches;
 }
 

@@ -493,6 +493,7 @@ void update_step(RankDense& r, int p) {
             GemmArgs x = gemm_args(r.zp + (size_t)nb0 * kNB, ld, Lb + W, rows, r.zp + (size_t)b0 * kNB, ld, T2, ntl, W);
             x.b_kmajor = 1; x.alpha_neg = 1; x.beta = 1;
             x.beta0_from = own_p ? before : -1;
+            x.k_from_col = own_p ? 1 : 0;  // the panel's own X block is lower triangular
             launch_gemm(x, r.s3);
         }
         SFM_CUDA(cudaEventRecord(r.eT[slot], r.s3));

@@ -108,6 +108,7 @@ struct GemmArgs {
     int whole_tile;  // C aliases A (in-place trsm): one CTA per 128-wide tile
     int a_kmajor;    // A stored K-contiguous: (m, k) at A[m * lda + k]
     int k_from_row;  // K range of tile (ti, tj) starts at ti * 128 (X^T X of a lower-triangular X)
+    int k_from_col;  // column tiles tj >= beta0_from: K starts at (tj - beta0_from) * 128 (B lower-triangular there)
     // Column-cyclic mode (cyc_R > 0, distributed sweep): C holds the local
     // columns of a rank owning panels rank, rank + R, ... of cyc_G tiles.
     // Grid tile (ti, tj) -> local column tile lt = tj + cyc_lt0, global
@@ -119,10 +120,9 @@ struct GemmArgs {
 
 // stage_a.cu
 void launch_status_init(Status* st, cudaStream_t s);
-void launch_validate(const SceneDev& sc, int check_sigma, Status* st, int* cam_cnt, int* pt_cnt, cudaStream_t s);
+void launch_validate(const SceneDev& sc, int check_sigma, Status* st, cudaStream_t s);
 void launch_validate_values(const SceneDev& sc, Status* st, cudaStream_t s);
-void launch_build_index(const SceneDev& sc, const int* cam_cnt, const int* pt_cnt, IndexDev& ix, Workspace& ws,
-                        cudaStream_t s);
+void launch_build_index(const SceneDev& sc, IndexDev& ix, Workspace& ws, cudaStream_t s);
 void launch_structure_check(const SceneDev& sc, const IndexDev& ix, Status* st, cudaStream_t s);
 void launch_jacobian(const SceneDev& sc, const int* idx_cam, double* R, double* rec, Status* st, cudaStream_t s);
 void launch_depth_of(const SceneDev& sc, const double* R, int t, double* out, cudaStream_t s);

@@ -153,31 +153,35 @@ __global__ void __launch_bounds__(128, 6) k_obs_factor(const int* oc, const int*
     for (int q = 0; q < kWStride / 2; ++q) o2[q] = make_double2(wo[2 * q], wo[2 * q + 1]);
 }
 
-// F = Σ partials (fixed-order tree); L_F = chol(F); E = -F and E's pivots
-// (-diag(L_F)^2) for the diagnostics.
-__global__ void __launch_bounds__(128) k_border_factor(const double* Fpart, int nblocks, double* LF, double* Eout,
-                                                       double* eigE, Status* st) {
-    __shared__ double red[128][29];
-    double acc[28];
-#pragma unroll
-    for (int k = 0; k < 28; ++k) acc[k] = 0.0;
-    for (int b = threadIdx.x; b < nblocks; b += 128)
-#pragma unroll
-        for (int k = 0; k < 28; ++k) acc[k] += Fpart[28 * (size_t)b + k];
-    for (int k = 0; k < 28; ++k) red[threadIdx.x][k] = acc[k];
-    __syncthreads();
-    for (int w = 64; w > 0; w >>= 1) {
-        if (threadIdx.x < w)
-            for (int k = 0; k < 28; ++k) red[threadIdx.x][k] += red[threadIdx.x + w][k];
-        __syncthreads();
+// F = Σ partials; L_F = chol(F); E = -F and E's pivots (-diag(L_F)^2) for
+// the diagnostics.  One warp per entry of F's upper triangle (28 warps):
+// lanes stride over the block partials (4 independent chains each), then a
+// shuffle tree -- a fixed order, so the result is deterministic.
+__global__ void __launch_bounds__(28 * 32) k_border_factor(const double* Fpart, int nblocks, double* LF, double* Eout,
+                                                           double* eigE, Status* st) {
+    __shared__ double red[28];
+    const int e = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int b = lane;
+    for (; b + 96 < nblocks; b += 128) {
+        a0 += Fpart[28 * (size_t)b + e];
+        a1 += Fpart[28 * (size_t)(b + 32) + e];
+        a2 += Fpart[28 * (size_t)(b + 64) + e];
+        a3 += Fpart[28 * (size_t)(b + 96) + e];
     }
+    for (; b < nblocks; b += 32) a0 += Fpart[28 * (size_t)b + e];
+    double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[e] = acc;
+    __syncthreads();
     if (threadIdx.x != 0) return;
     double F[49];
     int k = 0;
     for (int l1 = 0; l1 < 7; ++l1)
         for (int l2 = l1; l2 < 7; ++l2, ++k) {
-            F[7 * l1 + l2] = red[0][k];
-            F[7 * l2 + l1] = red[0][k];
+            F[7 * l1 + l2] = red[k];
+            F[7 * l2 + l1] = red[k];
         }
     for (int q = 0; q < 49; ++q) Eout[q] = -F[q];
     double L[49];
@@ -533,7 +537,7 @@ void launch_point_prep(const SceneDev& sc, const IndexDev& ix, const double* rec
 
 void launch_border_factor(const double* Fpart, int nblocks, double* LF, double* E, double* eigE, Status* st,
                           cudaStream_t s) {
-    k_border_factor<<<1, 128, 0, s>>>(Fpart, nblocks, LF, E, eigE, st);
+    k_border_factor<<<1, 28 * 32, 0, s>>>(Fpart, nblocks, LF, E, eigE, st);
     SFM_LAUNCH_CHECK();
 }
 

@@ -65,27 +65,15 @@ __device__ __forceinline__ int obs_value_code(const double* u, const double* sig
 // that, like the reference functions, do not validate, and host-API scenes
 // whose covariances are still uploading: k_validate_values checks them).
 __global__ void k_validate_obs(const int* oc, const int* op, const double* u, const double* sigma, int t_count,
-                               int n, int m, int check_sigma, Status* st, int* cam_cnt, int* pt_cnt) {
+                               int n, int m, int check_sigma, Status* st) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = t < t_count;
-    const int ci = valid ? oc[t] : -1, pj = valid ? op[t] : -1;
-    int code = valid ? 0 : 6;
-    if (!valid) {
-    } else if (ci < 0 || ci >= n) code = 1;
+    if (t >= t_count) return;
+    const int ci = oc[t], pj = op[t];
+    int code = 0;
+    if (ci < 0 || ci >= n) code = 1;
     else if (pj < 0 || pj >= m) code = 2;
     else if (check_sigma) code = obs_value_code(u, sigma, t);
-    if (code && valid) atomicMin(&st->obs_bad, (long long)t * 8 + code);
-    // counts per camera / point, warp-aggregated (a point's observations sit
-    // in neighbouring lanes): one atomic per distinct index per warp
-    const bool add = valid && (code == 0 || (code > 2 && code < 6));
-    const unsigned mask = __ballot_sync(0xffffffffu, add);
-    if (add) {
-        const int lane = threadIdx.x & 31;
-        const unsigned pp = __match_any_sync(mask, pj);
-        if (lane == __ffs(pp) - 1) atomicAdd(&pt_cnt[pj], __popc(pp));
-        const unsigned pc = __match_any_sync(mask, ci);
-        if (lane == __ffs(pc) - 1) atomicAdd(&cam_cnt[ci], __popc(pc));
-    }
+    if (code) atomicMin(&st->obs_bad, (long long)t * 8 + code);
 }
 
 // The value checks alone (codes 3-5), once the covariances have arrived; an
@@ -100,6 +88,19 @@ __global__ void k_validate_values(const double* u, const double* sigma, int t_co
 __global__ void k_iota(int* v, int count) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count) v[i] = i;
+}
+
+// CSR offsets from keys sorted ascending (all in [0, bins)): off[c] = first
+// position with key >= c, off[bins] = count.  Replaces per-observation count
+// atomics (hot cameras serialised them: 130 us at config 3).
+__global__ void k_offsets_from_sorted(const int* keys, int count, int bins, int* off) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    const int key = keys[k];
+    const int prev = k > 0 ? keys[k - 1] : -1;
+    for (int c = prev + 1; c <= key; ++c) off[c] = k;
+    if (k == count - 1)
+        for (int c = key + 1; c <= bins; ++c) off[c] = count;
 }
 
 __global__ void k_pos_scatter(const int* idx, int count, int* pos) {
@@ -410,16 +411,14 @@ __global__ void k_write_h(const double* cams, const double* Hr, const double* pt
 // ---- host launchers ------------------------------------------------------------
 void launch_status_init(Status* st, cudaStream_t s) { k_status_init<<<1, 1, 0, s>>>(st); SFM_LAUNCH_CHECK(); }
 
-void launch_validate(const SceneDev& sc, int check_sigma, Status* st, int* cam_cnt, int* pt_cnt, cudaStream_t s) {
-    SFM_CUDA(cudaMemsetAsync(cam_cnt, 0, sizeof(int) * (size_t)(sc.n + 1), s));
-    SFM_CUDA(cudaMemsetAsync(pt_cnt, 0, sizeof(int) * (size_t)(sc.m + 1), s));
+void launch_validate(const SceneDev& sc, int check_sigma, Status* st, cudaStream_t s) {
     if (check_sigma) {
         if (sc.n) { k_validate_cams<<<cdiv(sc.n, 256), 256, 0, s>>>(sc.cams, sc.n, sc.P, st); SFM_LAUNCH_CHECK(); }
         if (sc.m) { k_validate_pts<<<cdiv(sc.m, 256), 256, 0, s>>>(sc.pts, sc.m, st); SFM_LAUNCH_CHECK(); }
     }
     // value checks here unless the scene's covariances are still uploading
     const int values = check_sigma && !sc.sigma_ready;
-    if (sc.t) { k_validate_obs<<<cdiv(sc.t, 256), 256, 0, s>>>(sc.oc, sc.op, sc.u, sc.sigma, sc.t, sc.n, sc.m, values, st, cam_cnt, pt_cnt); SFM_LAUNCH_CHECK(); }
+    if (sc.t) { k_validate_obs<<<cdiv(sc.t, 256), 256, 0, s>>>(sc.oc, sc.op, sc.u, sc.sigma, sc.t, sc.n, sc.m, values, st); SFM_LAUNCH_CHECK(); }
 }
 
 void launch_validate_values(const SceneDev& sc, Status* st, cudaStream_t s) {
@@ -428,27 +427,29 @@ void launch_validate_values(const SceneDev& sc, Status* st, cudaStream_t s) {
 
 static int bits_for(int v) { int b = 1; while ((1LL << b) <= v) ++b; return b; }
 
-void launch_build_index(const SceneDev& sc, const int* cam_cnt, const int* pt_cnt, IndexDev& ix, Workspace& ws,
-                        cudaStream_t s) {
+// Runs after the index ranges have been validated (every key in range).
+void launch_build_index(const SceneDev& sc, IndexDev& ix, Workspace& ws, cudaStream_t s) {
     const int t = sc.t;
-    // offsets = exclusive scan of counts (count arrays carry one extra zero slot)
-    size_t b1 = 0, b2 = 0, b3 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, b1, cam_cnt, ix.off_cam, sc.n + 1, s);
-    cub::DeviceScan::ExclusiveSum(nullptr, b2, pt_cnt, ix.off_pt, sc.m + 1, s);
-    cub::DeviceRadixSort::SortPairs(nullptr, b3, (const int*)nullptr, (int*)nullptr, (const int*)nullptr, (int*)nullptr, t, 0, 32, s);
-    size_t bytes = b1 > b2 ? b1 : b2;
-    if (b3 > bytes) bytes = b3;
+    if (t == 0) {
+        SFM_CUDA(cudaMemsetAsync(ix.off_cam, 0, sizeof(int) * (size_t)(sc.n + 1), s));
+        SFM_CUDA(cudaMemsetAsync(ix.off_pt, 0, sizeof(int) * (size_t)(sc.m + 1), s));
+        return;
+    }
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int*)nullptr, (int*)nullptr, (const int*)nullptr, (int*)nullptr, t, 0, 32, s);
     void* tmp = ws.get_tmp(bytes);
-    SFM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, b1, cam_cnt, ix.off_cam, sc.n + 1, s));
-    SFM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, b2, pt_cnt, ix.off_pt, sc.m + 1, s));
-    if (t == 0) return;
     int* iota = ix.pos_cam;  // scratch before pos is filled
     k_iota<<<cdiv(t, 256), 256, 0, s>>>(iota, t);
     SFM_LAUNCH_CHECK();
+    // stable sorts: ascending observation ids within a camera / point
     size_t bb = bytes;
     SFM_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bb, sc.oc, ix.key_scratch, iota, ix.idx_cam, t, 0, bits_for(sc.n), s));
+    k_offsets_from_sorted<<<cdiv(t, 256), 256, 0, s>>>(ix.key_scratch, t, sc.n, ix.off_cam);
+    SFM_LAUNCH_CHECK();
     bb = bytes;
     SFM_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bb, sc.op, ix.key_scratch, iota, ix.idx_pt, t, 0, bits_for(sc.m), s));
+    k_offsets_from_sorted<<<cdiv(t, 256), 256, 0, s>>>(ix.key_scratch, t, sc.m, ix.off_pt);
+    SFM_LAUNCH_CHECK();
     k_pos_scatter<<<cdiv(t, 256), 256, 0, s>>>(ix.idx_cam, t, ix.pos_cam);
     SFM_LAUNCH_CHECK();
 }

@@ -27,7 +27,9 @@ for b0 in range(0, K, G):
     seq.append(("take", 0.0))
     nb0 = b0 + g; T2 = K - nb0; gn = min(T2, G)
     if T2 > gn: gemm("rest", T2 - gn, T2 - gn, g * 128, tri=True)
-    if T2 > 0: gemm("next", T2, gn, g * 128, lower=True)
+    if T2 > 0:
+        gemm("next1", T2, 1, g * 128, lower=True)          # critical stream: the next panel's first column
+        if gn > 1: gemm("next_rest", T2, gn - 1, g * 128)  # s4: its later columns
     for gg in range(g):
         r = b0 + gg
         gemm("inv_row", 1, r + 1, 128)

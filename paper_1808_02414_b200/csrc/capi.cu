@@ -72,7 +72,7 @@ struct sfmcov_handle {
     // index
     DBuf off_cam, idx_cam, off_pt, idx_pt, pos_cam, key_scratch;
     // stage buffers
-    DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Lpt, Wb, V, Fpart, LF, E, eigE, Gamma, G, Z, Linv, ring, piv, cov,
+    DBuf R, rec, D, Hr, A, s_a, flags, bpart, s_b, Lpt, Wb, V, Fpart, Pfirst, Plast, Gsum, LF, E, eigE, Gamma, G, Z, Linv, ring, piv, cov,
         psd, prange, status, depth, H;
     PairDev pairs;
     Status* st_host = nullptr;
@@ -487,7 +487,11 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     const int ppb = point_prep_blocks(m);
     double* Fpart = h->Fpart.as<double>(28 * (size_t)ppb);
     double* Lpt = h->Lpt.as<double>(8 * (size_t)m);
-    launch_point_prep(sc, ix, rec, A, s_a, s_b, Lpt, Wb, V, Fpart, st, s);
+    const size_t nwarps = ((size_t)t + 31) / 32;
+    double* Pfirst = h->Pfirst.as<double>((size_t)P * 7 * nwarps);
+    double* Plast = h->Plast.as<double>((size_t)P * 7 * nwarps);
+    double* Gsum = h->Gsum.as<double>((size_t)P * 7 * n);
+    launch_point_prep(sc, ix, rec, A, s_a, s_b, Lpt, Wb, V, Fpart, Pfirst, Plast, Gsum, st, s);
     double* LF = h->LF.as<double>(49);
     double* E = h->E.as<double>(49);
     double* eigE = h->eigE.as<double>(8);
@@ -495,7 +499,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     const int N = P * n;
     double* Gamma = h->Gamma.as<double>((size_t)N * 7);
     double* G = h->G.as<double>((size_t)N * 7);
-    launch_camera_border(sc, ix, Wb, V, Hr, s_a, s_b, LF, Gamma, G, s);
+    launch_camera_border(sc, ix, Pfirst, Plast, Gsum, Hr, s_a, s_b, LF, Gamma, G, s);
     mark(h, 4);
     // The pair list depends only on the index: it is built on s2 from the
     // index event while s runs the numeric stage-A kernels queued above (its
@@ -863,7 +867,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     DBuf* bufs[] = {&h->ws.tmp, &h->ws_pairs.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_sigma,
                     &h->off_cam, &h->idx_cam, &h->off_pt, &h->idx_pt, &h->pos_cam, &h->key_scratch,
                     &h->R, &h->rec, &h->D, &h->Hr, &h->A, &h->s_a, &h->flags, &h->bpart, &h->s_b, &h->Lpt, &h->Wb, &h->V,
-                    &h->Fpart, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->ring, &h->piv,
+                    &h->Fpart, &h->Pfirst, &h->Plast, &h->Gsum, &h->LF, &h->E, &h->eigE, &h->Gamma, &h->G, &h->Z, &h->Linv, &h->ring, &h->piv,
                     &h->cov, &h->psd, &h->prange, &h->status, &h->depth, &h->H};
     for (DBuf* b : bufs) b->release();
     h->pairs.release();

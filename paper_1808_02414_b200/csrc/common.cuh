@@ -25,6 +25,15 @@ template <int P> struct Layout {
 // Per-observation Schur factor W_a = C_s,a L_j^-T (P x 3 row-major), stride 28.
 constexpr int kWStride = 28;
 
+// Asynchronous 16-byte global -> shared copies (L2 only, no L1 allocation).
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 // Dense panel width of the blocked Cholesky / triangular inverse.
 constexpr int kNB = 128;
 

@@ -137,12 +137,13 @@ void launch_write_h(const SceneDev& sc, const double* Hr, double* H, cudaStream_
 // schur.cu
 int point_prep_blocks(int m);
 void launch_point_prep(const SceneDev& sc, const IndexDev& ix, const double* rec, const double* A, const double* s_a,
-                       const double* s_b, double* Lpt, double* Wb, double* V, double* Fpart, Status* st, cudaStream_t s);
+                       const double* s_b, double* Lpt, double* Wb, double* V, double* Fpart, double* Pfirst,
+                       double* Plast, double* Gsum, Status* st, cudaStream_t s);
 void launch_border_factor(const double* Fpart, int nblocks, double* LF, double* E, double* eigE, Status* st,
                           cudaStream_t s);
-void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* Wb, const double* V, const double* Hr,
-                          const double* s_a, const double* s_b, const double* LF, double* Gamma, double* G,
-                          cudaStream_t s);
+void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* Pfirst, const double* Plast,
+                          const double* Gsum, const double* Hr, const double* s_a, const double* s_b, const double* LF,
+                          double* Gamma, double* G, cudaStream_t s);
 void launch_fill(int P, double* Z, long long ld, int N, int Npad, const double* D, const double* s_a, const double* G,
                  int add_gg, cudaStream_t s);
 void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace& ws, cudaStream_t s);

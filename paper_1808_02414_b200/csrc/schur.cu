@@ -108,49 +108,136 @@ __global__ void __launch_bounds__(128) k_point_prep(const double* A, const doubl
     if (threadIdx.x < 28) Fpart[28 * (size_t)blockIdx.x + threadIdx.x] = red[0][threadIdx.x];
 }
 
-// W_a = C_s,a L_j^-T (P x 3) per observation, one thread per by-camera slot
-// (records read and factors written contiguously).
+// W_a = C_s,a L_j^-T (P x 3) per observation, one thread per by-camera slot.
+// The CTA's records and factors are contiguous: both move through shared
+// memory (odd pitch) with coalesced 16-byte loads and stores.
+//
+// Fused with the camera border sums Σ_{a in cam i} W_a V_j(a): each warp (32
+// consecutive slots, so one or a few cameras) reduces W_a V_j per camera
+// segment with a shuffle tree; the segment of the warp's first camera goes to
+// Pfirst[warp], that of its last camera to Plast[warp], and a camera lying
+// wholly inside the warp straight to Gsum[camera].  k_camera_border then adds
+// a camera's warp partials in warp order (deterministic), so the factors are
+// not read back from HBM for the border.
 template <int P>
-__global__ void __launch_bounds__(128, 6) k_obs_factor(const int* oc, const int* op, const int* idx_cam, const double* rec,
-                                                    const double* s_a, const double* Lpt, int t_count, int n,
-                                                    double* Wb) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;  // by-camera slot
-    if (k >= t_count) return;
-    const int t = idx_cam[k];
-    const int ci = oc[t], pj = op[t];
-    const double* r = rec + (size_t)k * kRec;
-    double rr[28];
-    const double2* r2 = reinterpret_cast<const double2*>(r);
-#pragma unroll
-    for (int q = 0; q < 14; ++q) { const double2 v = r2[q]; rr[2 * q] = v.x; rr[2 * q + 1] = v.y; }
-    const double* jc = rr + Layout<P>::JC;
-    const double* jp = rr + Layout<P>::JP;
-    const double* W = rr + Layout<P>::WO;
-    const double* sc = s_a + (size_t)P * ci;
-    const double* sp = s_a + (size_t)P * n + 3 * (size_t)pj;
-    const double* L = Lpt + 8 * (size_t)pj;
-    const double l00 = L[0], l10 = L[1], l11 = L[2], l20 = L[3], l21 = L[4], l22 = L[5];
-    const bool good = L[6] != 0.0;
-    double wo[kWStride];
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-        const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
-        const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
-        double c[3];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) c[q] = (sc[p] * (t0 * jp[q] + t1 * jp[3 + q])) * sp[q];
-        const double w0 = c[0] / l00;
-        const double w1 = (c[1] - l10 * w0) / l11;
-        const double w2 = (c[2] - l20 * w0 - l21 * w1) / l22;
-        wo[3 * p + 0] = good ? w0 : 0.0;
-        wo[3 * p + 1] = good ? w1 : 0.0;
-        wo[3 * p + 2] = good ? w2 : 0.0;
+__global__ void __launch_bounds__(128) k_obs_factor(const int* oc, const int* op, const int* idx_cam, const double* rec,
+                                                    const double* s_a, const double* Lpt, const double* V, int t_count,
+                                                    int n, double* Wb, double* Pfirst, double* Plast, double* Gsum) {
+    constexpr int NE = P * 7;
+    constexpr int PITCH = kWStride + 1;  // odd: conflict-free per-thread rows
+    static_assert(PITCH % 2 == 1 && PITCH >= kWStride, "staging pitch");
+    __shared__ double buf[128 * PITCH];
+    const int k0 = blockIdx.x * blockDim.x;
+    const int nv = min(128, t_count - k0);
+    {
+        const double2* in = reinterpret_cast<const double2*>(rec + (size_t)k0 * kRec);
+        constexpr int NP = (Layout<P>::WO + 4 + 1) / 2;  // double2 parts of the record that are used
+        for (int w = threadIdx.x; w < nv * NP; w += 128) {
+            const int o = w / NP, part = w - o * NP;
+            const double2 v = __ldcs(in + (size_t)o * (kRec / 2) + part);
+            buf[o * PITCH + 2 * part] = v.x;
+            if (2 * part + 1 < PITCH) buf[o * PITCH + 2 * part + 1] = v.y;
+        }
     }
+    __syncthreads();
+    const int k = k0 + threadIdx.x;
+    double wo[kWStride];
+    int ci = -1, pj = 0;
+    if (k < t_count) {
+        const int t = idx_cam[k];
+        ci = oc[t];
+        pj = op[t];
+        const double* rr = buf + threadIdx.x * PITCH;
+        const double* jc = rr + Layout<P>::JC;
+        const double* jp = rr + Layout<P>::JP;
+        const double* W = rr + Layout<P>::WO;
+        const double* sc = s_a + (size_t)P * ci;
+        const double* sp = s_a + (size_t)P * n + 3 * (size_t)pj;
+        const double* L = Lpt + 8 * (size_t)pj;
+        const double l00 = L[0], l10 = L[1], l11 = L[2], l20 = L[3], l21 = L[4], l22 = L[5];
+        const bool good = L[6] != 0.0;
 #pragma unroll
-    for (int z = 3 * P; z < kWStride; ++z) wo[z] = 0.0;
-    double2* o2 = reinterpret_cast<double2*>(Wb + (size_t)k * kWStride);
+        for (int p = 0; p < P; ++p) {
+            const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
+            const double t1 = jc[p] * W[1] + jc[P + p] * W[3];
+            double c[3];
 #pragma unroll
-    for (int q = 0; q < kWStride / 2; ++q) o2[q] = make_double2(wo[2 * q], wo[2 * q + 1]);
+            for (int q = 0; q < 3; ++q) c[q] = (sc[p] * (t0 * jp[q] + t1 * jp[3 + q])) * sp[q];
+            const double w0 = c[0] / l00;
+            const double w1 = (c[1] - l10 * w0) / l11;
+            const double w2 = (c[2] - l20 * w0 - l21 * w1) / l22;
+            wo[3 * p + 0] = good ? w0 : 0.0;
+            wo[3 * p + 1] = good ? w1 : 0.0;
+            wo[3 * p + 2] = good ? w2 : 0.0;
+        }
+#pragma unroll
+        for (int z = 3 * P; z < kWStride; ++z) wo[z] = 0.0;
+    }
+    // ---- border partials: Σ W_a V_j per camera segment of the warp ----
+    // In batches of 3 rows p (21 entries): each lane writes its products to
+    // the warp's smem rows, then lane e sums column e over the warp's slots in
+    // slot order, flushing at camera changes.
+    __syncthreads();  // every thread has read its record: buf is reused
+    {
+        constexpr int BR = 3, BE = 7 * BR;  // rows per batch, entries per batch (odd pitch)
+        const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+        const size_t gw = (size_t)(k >> 5);
+        double* wbuf = buf + wib * 32 * BE;
+        __shared__ int wcam[4][32];
+        double v[21];
+#pragma unroll
+        for (int z = 0; z < 21; ++z) v[z] = (ci >= 0) ? __ldg(V + 21 * (size_t)pj + z) : 0.0;
+        wcam[wib][lane] = ci;
+        const unsigned vmask = __ballot_sync(0xffffffffu, ci >= 0);
+        const int lastl = vmask ? 31 - __clz(vmask) : -1;
+        const int cfirst = __shfl_sync(0xffffffffu, ci, 0);
+        const int clast = lastl >= 0 ? __shfl_sync(0xffffffffu, ci, lastl) : -1;
+#pragma unroll
+        for (int p0 = 0; p0 < P; p0 += BR) {
+            const int nr = (P - p0 < BR) ? P - p0 : BR;
+            __syncwarp();
+            if (ci >= 0) {
+#pragma unroll
+                for (int pr = 0; pr < BR; ++pr) {
+                    if (pr < nr) {
+                        const int p = p0 + pr;
+#pragma unroll
+                        for (int l = 0; l < 7; ++l)
+                            wbuf[lane * BE + 7 * pr + l] = (wo[3 * p] * v[l] + wo[3 * p + 1] * v[7 + l]) + wo[3 * p + 2] * v[14 + l];
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane < 7 * nr && lastl >= 0) {
+                const int eo = 7 * p0 + lane;  // entry (p, l) = (p0 + lane / 7, lane % 7)
+                int cur = wcam[wib][0];
+                double acc = 0.0;
+                for (int o = 0; o <= lastl; ++o) {
+                    const int c = wcam[wib][o];
+                    if (c != cur) {
+                        double* dst = (cur == cfirst) ? Pfirst + gw * NE : ((cur == clast) ? Plast + gw * NE : Gsum + (size_t)cur * NE);
+                        dst[eo] = acc;
+                        acc = 0.0;
+                        cur = c;
+                    }
+                    acc += wbuf[o * BE + lane];
+                }
+                double* dst = (cur == cfirst) ? Pfirst + gw * NE : ((cur == clast) ? Plast + gw * NE : Gsum + (size_t)cur * NE);
+                dst[eo] = acc;
+            }
+        }
+    }
+    __syncthreads();
+    if (k < t_count) {
+#pragma unroll
+        for (int z = 0; z < kWStride; ++z) buf[threadIdx.x * PITCH + z] = wo[z];
+    }
+    __syncthreads();
+    double2* out = reinterpret_cast<double2*>(Wb + (size_t)k0 * kWStride);
+    for (int w = threadIdx.x; w < nv * (kWStride / 2); w += 128) {
+        const int o = w / (kWStride / 2), part = w - o * (kWStride / 2);
+        out[w] = make_double2(buf[o * PITCH + 2 * part], buf[o * PITCH + 2 * part + 1]);
+    }
 }
 
 // F = Σ partials; L_F = chol(F); E = -F and E's pivots (-diag(L_F)^2) for
@@ -207,63 +294,30 @@ __global__ void __launch_bounds__(28 * 32) k_border_factor(const double* Fpart, 
 }
 
 // ---- camera border rows -----------------------------------------------------------
-// Γ_i[p][l] = H_s,ci[p][l] - Σ_{a in cam i} (W_a V_j(a))[p][l]; then
-// G_i = Γ_i L_F^-T.  One CTA per camera: 8 groups of 64 threads (one per
-// entry (p, l)) take interleaved 12-observation chunks of the camera's
-// contiguous by-camera slots; the 8 group partials are added in group order,
-// so the result is deterministic.
-namespace cb {
-constexpr int GROUPS = 8, CH = 12, RS = 49;  // staged per observation: W (27) at 0, V_j (21) at 27
-constexpr int THREADS = GROUPS * 64;
-}  // namespace cb
-
+// Γ_i[p][l] = H_s,ci[p][l] - Σ_{a in cam i} (W_a V_j(a))[p][l] from the warp
+// partials of k_obs_factor (added in warp order); then G_i = Γ_i L_F^-T.
+// One 64-thread CTA per camera, one thread per entry (p, l).
 template <int P>
-__global__ void __launch_bounds__(cb::THREADS) k_camera_border(const int* off_cam, const int* idx_cam, const int* op,
-                                                               const double* Wb, const double* V, const double* cams,
-                                                               const double* Hr, const double* s_a, const double* s_b,
-                                                               const double* LF, int n, double* Gamma, double* G) {
-    using namespace cb;
+__global__ void __launch_bounds__(64) k_camera_border(const int* off_cam, int t_count, const double* Pfirst,
+                                                      const double* Plast, const double* Gsum, const double* cams,
+                                                      const double* Hr, const double* s_a, const double* s_b,
+                                                      const double* LF, int n, double* Gamma, double* G) {
     constexpr int NE = P * 7;
-    constexpr int ROUND = GROUPS * CH;  // observations staged per round
-    __shared__ double stage[ROUND][RS];
-    __shared__ double part[GROUPS][NE];
     __shared__ double sh[NE];
-    __shared__ int pid[ROUND];
     const int i = blockIdx.x, tid = threadIdx.x;
-    const int grp = tid >> 6, e = tid & 63;
-    const int p = e / 7, l = e % 7;
-    double acc = 0.0;
-    const int b = off_cam[i], end = off_cam[i + 1];
-    for (int k0 = b; k0 < end; k0 += ROUND) {
-        const int nc = min(ROUND, end - k0);
-        if (tid < nc) pid[tid] = op[idx_cam[k0 + tid]];
-        // W rows of the round are contiguous (by-camera slots): coalesced copy
-        for (int w = tid; w < nc * 27; w += THREADS) {
-            const int o = w / 27, c = w - o * 27;
-            stage[o][c] = Wb[(size_t)(k0 + o) * kWStride + c];
-        }
-        __syncthreads();
-        for (int w = tid; w < nc * 21; w += THREADS) {
-            const int o = w / 21, c = w - o * 21;
-            stage[o][27 + c] = V[21 * (size_t)pid[o] + c];
-        }
-        __syncthreads();
-        if (e < NE) {
-            const int o0 = grp * CH, o1 = min(o0 + CH, nc);
-            for (int o = o0; o < o1; ++o) {
-                const double* w = stage[o];
-                const double* vj = w + 27;
-                acc += (w[3 * p] * vj[l] + w[3 * p + 1] * vj[7 + l]) + w[3 * p + 2] * vj[14 + l];
-            }
-        }
-        __syncthreads();
-    }
-    if (e < NE) part[grp][e] = acc;
-    __syncthreads();
+    const int p = tid / 7, l = tid % 7;
     if (tid < NE) {
-        double sum = part[0][tid];
-#pragma unroll
-        for (int g = 1; g < GROUPS; ++g) sum += part[g][tid];
+        const int b = off_cam[i], e = off_cam[i + 1];
+        double sum = 0.0;
+        if (e > b) {
+            bool any = false;
+            for (int w = b >> 5; w <= (e - 1) >> 5; ++w) {
+                const int fs = 32 * w, ls = min(32 * w + 31, t_count - 1);
+                if (fs >= b && fs < e) { sum += Pfirst[(size_t)w * NE + tid]; any = true; }
+                else if (ls >= b && ls < e) { sum += Plast[(size_t)w * NE + tid]; any = true; }
+            }
+            if (!any) sum = Gsum[(size_t)i * NE + tid];  // the camera lies inside one warp
+        }
         const double* C = cams + (size_t)P * i + 3;
         double h = 0.0;
         if (p < 3) h = (l >= 3 && l < 6) ? Hr[9 * (size_t)i + 3 * p + (l - 3)] : 0.0;
@@ -352,12 +406,46 @@ __global__ void k_pair_count(const int* off_pt, int m, long long* cnt) {
     cnt[j] = k * (k + 1) / 2;
 }
 
-__global__ void k_pair_gen(const int* off_pt, const int* idx_pt, const int* oc, const int* pos_cam, int m, int n,
-                           const long long* poff, unsigned int* keys, unsigned long long* vals) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per point: lanes read the track's cameras and by-camera slots
+// once (tracks up to 32), then enumerate the k(k+1)/2 pairs (a <= c, the
+// reference's order) with coalesced key / value stores.  Longer tracks: one
+// lane, straight from global memory.
+__global__ void __launch_bounds__(256) k_pair_gen(const int* off_pt, const int* idx_pt, const int* oc, const int* pos_cam,
+                                                  int m, int n, const long long* poff, unsigned int* keys,
+                                                  unsigned long long* vals) {
+    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (j >= m) return;
-    long long o = poff[j];
+    const long long o = poff[j];
     const int b = off_pt[j], e = off_pt[j + 1];
+    const int k = e - b;
+    if (k <= 32) {
+        int mc = 0, ms = 0;
+        if (lane < k) {
+            const int ta = __ldg(idx_pt + b + lane);
+            mc = __ldg(oc + ta);
+            ms = __ldg(pos_cam + ta);
+        }
+        const int np = k * (k + 1) / 2;
+        for (int q0 = 0; q0 < np; q0 += 32) {
+            const int q = q0 + lane;
+            int a = 0, r = q;
+            while (a < k && r >= k - a) { r -= k - a; ++a; }  // row a, column c = a + r
+            const int c = (a < k) ? a + r : 0;
+            const int ca = __shfl_sync(0xffffffffu, mc, a & 31), sa = __shfl_sync(0xffffffffu, ms, a & 31);
+            const int cb = __shfl_sync(0xffffffffu, mc, c & 31), sbb = __shfl_sync(0xffffffffu, ms, c & 31);
+            if (q < np) {
+                const bool le = ca <= cb;
+                const unsigned lo = le ? ca : cb, hi = le ? cb : ca;
+                const unsigned slo = le ? sa : sbb, shi = le ? sbb : sa;
+                keys[o + q] = lo * (unsigned)n + hi;
+                vals[o + q] = ((unsigned long long)shi << 32) | slo;
+            }
+        }
+        return;
+    }
+    if (lane) return;
+    long long w = o;
     for (int a = b; a < e; ++a) {
         const int ta = idx_pt[a];
         const int ca = oc[ta];
@@ -367,9 +455,9 @@ __global__ void k_pair_gen(const int* off_pt, const int* idx_pt, const int* oc, 
             int lo, hi, slo, shi;
             if (ca <= cb) { lo = ca; hi = cb; slo = pos_cam[ta]; shi = pos_cam[tb]; }
             else { lo = cb; hi = ca; slo = pos_cam[tb]; shi = pos_cam[ta]; }
-            keys[o] = (unsigned int)lo * (unsigned int)n + (unsigned int)hi;
-            vals[o] = ((unsigned long long)(unsigned int)shi << 32) | (unsigned int)slo;
-            ++o;
+            keys[w] = (unsigned int)lo * (unsigned int)n + (unsigned int)hi;
+            vals[w] = ((unsigned long long)(unsigned int)shi << 32) | (unsigned int)slo;
+            ++w;
         }
     }
 }
@@ -523,14 +611,15 @@ __global__ void __launch_bounds__(256) k_pair_combine_seg(int nseg, const int* c
 int point_prep_blocks(int m) { return (int)cdiv(m > 0 ? m : 1, 128); }
 
 void launch_point_prep(const SceneDev& sc, const IndexDev& ix, const double* rec, const double* A, const double* s_a,
-                       const double* s_b, double* Lpt, double* Wb, double* V, double* Fpart, Status* st, cudaStream_t s) {
+                       const double* s_b, double* Lpt, double* Wb, double* V, double* Fpart, double* Pfirst,
+                       double* Plast, double* Gsum, Status* st, cudaStream_t s) {
     const int nb = point_prep_blocks(sc.m);
     if (sc.P == 8) k_point_prep<8><<<nb, 128, 0, s>>>(A, s_a, sc.pts, s_b, sc.m, sc.n, Lpt, V, Fpart, st);
     else k_point_prep<9><<<nb, 128, 0, s>>>(A, s_a, sc.pts, s_b, sc.m, sc.n, Lpt, V, Fpart, st);
     SFM_LAUNCH_CHECK();
     if (sc.t) {
-        if (sc.P == 8) k_obs_factor<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.oc, sc.op, ix.idx_cam, rec, s_a, Lpt, sc.t, sc.n, Wb);
-        else k_obs_factor<9><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.oc, sc.op, ix.idx_cam, rec, s_a, Lpt, sc.t, sc.n, Wb);
+        if (sc.P == 8) k_obs_factor<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.oc, sc.op, ix.idx_cam, rec, s_a, Lpt, V, sc.t, sc.n, Wb, Pfirst, Plast, Gsum);
+        else k_obs_factor<9><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.oc, sc.op, ix.idx_cam, rec, s_a, Lpt, V, sc.t, sc.n, Wb, Pfirst, Plast, Gsum);
         SFM_LAUNCH_CHECK();
     }
 }
@@ -541,12 +630,12 @@ void launch_border_factor(const double* Fpart, int nblocks, double* LF, double* 
     SFM_LAUNCH_CHECK();
 }
 
-void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* Wb, const double* V, const double* Hr,
-                          const double* s_a, const double* s_b, const double* LF, double* Gamma, double* G,
-                          cudaStream_t s) {
+void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* Pfirst, const double* Plast,
+                          const double* Gsum, const double* Hr, const double* s_a, const double* s_b, const double* LF,
+                          double* Gamma, double* G, cudaStream_t s) {
     if (!sc.n) return;
-    if (sc.P == 8) k_camera_border<8><<<sc.n, cb::THREADS, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
-    else k_camera_border<9><<<sc.n, cb::THREADS, 0, s>>>(ix.off_cam, ix.idx_cam, sc.op, Wb, V, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    if (sc.P == 8) k_camera_border<8><<<sc.n, 64, 0, s>>>(ix.off_cam, sc.t, Pfirst, Plast, Gsum, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    else k_camera_border<9><<<sc.n, 64, 0, s>>>(ix.off_cam, sc.t, Pfirst, Plast, Gsum, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
     SFM_LAUNCH_CHECK();
 }
 
@@ -598,7 +687,7 @@ void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace&
     unsigned int* k1 = (unsigned int*)pd.buf_k1.get(4 * np + 16);
     unsigned long long* v0 = (unsigned long long*)pd.buf_v0.get(8 * np + 16);
     unsigned long long* v1 = (unsigned long long*)pd.buf_v1.get(8 * np + 16);
-    if (m) k_pair_gen<<<cdiv(m, 128), 128, 0, s>>>(ix.off_pt, ix.idx_pt, sc.oc, ix.pos_cam, m, sc.n, pd.off, k0, v0);
+    if (m) k_pair_gen<<<cdiv((long long)m * 32, 256), 256, 0, s>>>(ix.off_pt, ix.idx_pt, sc.oc, ix.pos_cam, m, sc.n, pd.off, k0, v0);
     SFM_LAUNCH_CHECK();
     const int kbits = bits_for64((unsigned long long)sc.n * (unsigned long long)sc.n);
     cub::DoubleBuffer<unsigned int> dk(k0, k1);

@@ -131,32 +131,37 @@ __global__ void k_camera_rot(const double* cams, int n, int P, double* R) {
 }
 
 // One thread per observation; writes the AoS record [jc | jp | W].  W is the
-// explicit 2x2 inverse of sigma (covariance.cpp:20-29).
+// explicit 2x2 inverse of sigma (covariance.cpp:20-29).  The CTA's 128
+// records are contiguous (by-camera slots): they are assembled in shared
+// memory (odd pitch: conflict-free) and written with coalesced 16-byte stores.
 template <int P>
-__global__ void k_jacobian(const double* cams, const double* Rc, const double* pts, const int* oc, const int* op,
-                           const int* idx_cam, const double* sigma, int t_count, double* rec, Status* st) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;  // by-camera slot: records written contiguously
-    if (k >= t_count) return;
-    const int t = idx_cam[k];
-    const int ci = oc[t], pj = op[t];
-    double jc[2 * P], jp[6], depth;
-    const bool ok = observation_jacobian<P>(cams + (size_t)P * ci, Rc + 9 * (size_t)ci, pts + 3 * (size_t)pj, jc, jp, &depth);
-    if (!ok) atomicMin(&st->jac_bad, t);
-    double s00 = 1.0, s01 = 0.0, s10 = 0.0, s11 = 1.0;
-    if (sigma) { s00 = sigma[4 * (size_t)t]; s01 = sigma[4 * (size_t)t + 1]; s10 = sigma[4 * (size_t)t + 2]; s11 = sigma[4 * (size_t)t + 3]; }
-    const double det = s00 * s11 - s01 * s10;
-    if (!(s00 > 0.0) || !(det > 0.0)) atomicMin(&st->fisher_bad, t);
-    double rr[kRec];
-    for (int z = 0; z < kRec; ++z) rr[z] = 0.0;
-    for (int z = 0; z < 2 * P; ++z) rr[Layout<P>::JC + z] = jc[z];
-    for (int z = 0; z < 6; ++z) rr[Layout<P>::JP + z] = jp[z];
-    rr[Layout<P>::WO + 0] = s11 / det;
-    rr[Layout<P>::WO + 1] = -s01 / det;
-    rr[Layout<P>::WO + 2] = -s10 / det;
-    rr[Layout<P>::WO + 3] = s00 / det;
-    // rotation-rhs factors of this observation (the camera_reduce rhs entries):
-    // tg[ii][q] = -((d_C row ii . [C]x col q) + (d_X row ii . [X]x col q))
-    {
+__global__ void __launch_bounds__(128) k_jacobian(const double* cams, const double* Rc, const double* pts, const int* oc,
+                                                  const int* op, const int* idx_cam, const double* sigma, int t_count,
+                                                  double* rec, Status* st) {
+    constexpr int PITCH = kRec + 1;
+    __shared__ double buf[128 * PITCH];
+    const int k0 = blockIdx.x * blockDim.x;
+    const int k = k0 + threadIdx.x;  // by-camera slot
+    if (k < t_count) {
+        const int t = idx_cam[k];
+        const int ci = oc[t], pj = op[t];
+        double jc[2 * P], jp[6], depth;
+        const bool ok = observation_jacobian<P>(cams + (size_t)P * ci, Rc + 9 * (size_t)ci, pts + 3 * (size_t)pj, jc, jp, &depth);
+        if (!ok) atomicMin(&st->jac_bad, t);
+        double s00 = 1.0, s01 = 0.0, s10 = 0.0, s11 = 1.0;
+        if (sigma) { s00 = sigma[4 * (size_t)t]; s01 = sigma[4 * (size_t)t + 1]; s10 = sigma[4 * (size_t)t + 2]; s11 = sigma[4 * (size_t)t + 3]; }
+        const double det = s00 * s11 - s01 * s10;
+        if (!(s00 > 0.0) || !(det > 0.0)) atomicMin(&st->fisher_bad, t);
+        double* rr = buf + threadIdx.x * PITCH;
+        for (int z = 0; z < kRec; ++z) rr[z] = 0.0;
+        for (int z = 0; z < 2 * P; ++z) rr[Layout<P>::JC + z] = jc[z];
+        for (int z = 0; z < 6; ++z) rr[Layout<P>::JP + z] = jp[z];
+        rr[Layout<P>::WO + 0] = s11 / det;
+        rr[Layout<P>::WO + 1] = -s01 / det;
+        rr[Layout<P>::WO + 2] = -s10 / det;
+        rr[Layout<P>::WO + 3] = s00 / det;
+        // rotation-rhs factors of this observation (the camera_reduce rhs entries):
+        // tg[ii][q] = -((d_C row ii . [C]x col q) + (d_X row ii . [X]x col q))
         double hc[9], hx[9];
         skew(cams + (size_t)P * ci + 3, hc);
         skew(pts + 3 * (size_t)pj, hx);
@@ -167,9 +172,13 @@ __global__ void k_jacobian(const double* cams, const double* Rc, const double* p
                 rr[Layout<P>::TG + 3 * ii + q] = -(a + bb);
             }
     }
-    double2* r2 = reinterpret_cast<double2*>(rec + (size_t)k * kRec);
-#pragma unroll
-    for (int q = 0; q < kRec / 2; ++q) r2[q] = make_double2(rr[2 * q], rr[2 * q + 1]);
+    __syncthreads();
+    const int nv = min(128, t_count - k0);
+    double2* out = reinterpret_cast<double2*>(rec + (size_t)k0 * kRec);
+    for (int w = threadIdx.x; w < nv * (kRec / 2); w += 128) {
+        const int o = w / (kRec / 2), part = w - o * (kRec / 2);
+        out[w] = make_double2(buf[o * PITCH + 2 * part], buf[o * PITCH + 2 * part + 1]);
+    }
 }
 
 // Depth of one observation (error message path only).
@@ -194,11 +203,12 @@ __global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const
     // one CTA per camera, one thread per output entry: D (P*P), rotation
     // normal (9) and rhs (9); each entry is a sequential sum over the
     // camera's observations in ascending order.  The camera's records are
-    // contiguous (by-camera slots) and staged 64 at a time in shared memory;
-    // the D-row factors t0, t1 are formed once per (observation, row).
+    // contiguous (by-camera slots) and staged 32 at a time in shared memory
+    // by cp.async, the next chunk in flight while this one is summed; the
+    // D-row factors t0, t1 are formed once per (observation, row).
     constexpr int NE = P * P + 18;
-    constexpr int CH = 64, T01 = kRec, RS = T01 + 2 * P;  // staged record, then t0/t1 per row
-    __shared__ double stage[CH][RS];
+    constexpr int CH = 32, T01 = kRec, RS = T01 + 2 * P;  // RS * 8 B is a multiple of 16
+    __shared__ __align__(16) double stage[2][CH][RS];     // double-buffered: chunk c + 1 loads during chunk c
     __shared__ double sh[NE];
     const int i = blockIdx.x;
     const int tid = threadIdx.x;
@@ -216,22 +226,30 @@ __global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const
     else if (kind == 2) { p = (e12 - 9) / 3; q = (e12 - 9) % 3; i1 = Layout<P>::TG + q; i2 = Layout<P>::TG + 3 + q; }
     double acc = 0.0;
     const int b = off_cam[i], e = off_cam[i + 1];
-    for (int k0 = b; k0 < e; k0 += CH) {
+    auto load = [&](int buf, int k0) {
         const int nc = min(CH, e - k0);
         for (int w = tid; w < nc * (kRec / 2); w += 128) {
             const int o = w / (kRec / 2), part = w - o * (kRec / 2);
-            const double2 v = reinterpret_cast<const double2*>(rec + (size_t)(k0 + o) * kRec)[part];
-            stage[o][2 * part] = v.x;
-            stage[o][2 * part + 1] = v.y;
+            cpa16(&stage[buf][o][2 * part], rec + (size_t)(k0 + o) * kRec + 2 * part);
         }
+    };
+    if (b < e) load(0, b);
+    cpa_commit();
+    for (int k0 = b, c = 0; k0 < e; k0 += CH, ++c) {
+        const int nc = min(CH, e - k0);
+        const int cur = c & 1;
+        if (k0 + CH < e) load(cur ^ 1, k0 + CH);
+        cpa_commit();
+        cpa_wait<1>();
         __syncthreads();
         // D row factors: t0 = jc_p W00 + jc_P+p W10, t1 = jc_p W01 + jc_P+p W11
         for (int w = tid; w < nc * P; w += 128) {
             const int o = w / P, pp = w - P * o;
-            const double* jc = stage[o] + Layout<P>::JC;
-            const double* W = stage[o] + Layout<P>::WO;
-            stage[o][T01 + 2 * pp] = jc[pp] * W[0] + jc[P + pp] * W[2];
-            stage[o][T01 + 2 * pp + 1] = jc[pp] * W[1] + jc[P + pp] * W[3];
+            double* r = stage[cur][o];
+            const double* jc = r + Layout<P>::JC;
+            const double* W = r + Layout<P>::WO;
+            r[T01 + 2 * pp] = jc[pp] * W[0] + jc[P + pp] * W[2];
+            r[T01 + 2 * pp + 1] = jc[pp] * W[1] + jc[P + pp] * W[3];
         }
         __syncthreads();
         // ordered sums over the chunk; terms of 4 observations are formed
@@ -243,14 +261,14 @@ __global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const
                 double tv[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const double* r = stage[o + u];
+                    const double* r = stage[cur][o + u];
                     tv[u] = r[T01 + 2 * p] * r[Layout<P>::JC + q] + r[T01 + 2 * p + 1] * r[Layout<P>::JC + P + q];
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) acc += tv[u];
             }
             for (; o < nc; ++o) {
-                const double* r = stage[o];
+                const double* r = stage[cur][o];
                 acc += r[T01 + 2 * p] * r[Layout<P>::JC + q] + r[T01 + 2 * p + 1] * r[Layout<P>::JC + P + q];
             }
         } else if (kind < 3) {
@@ -259,18 +277,18 @@ __global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const
                 double tv[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const double* r = stage[o + u];
+                    const double* r = stage[cur][o + u];
                     tv[u] = r[Layout<P>::JC + p] * r[i1] + r[Layout<P>::JC + P + p] * r[i2];
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) acc += tv[u];
             }
             for (; o < nc; ++o) {
-                const double* r = stage[o];
+                const double* r = stage[cur][o];
                 acc += r[Layout<P>::JC + p] * r[i1] + r[Layout<P>::JC + P + p] * r[i2];
             }
         }
-        __syncthreads();
+        __syncthreads();  // stage[cur] is refilled by the next iteration's prefetch
     }
     if (kind < 3) sh[slot] = acc;
     __syncthreads();

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(128) k_point_prep(const double* A, const doubl
 // a camera's warp partials in warp order (deterministic), so the factors are
 // not read back from HBM for the border.
 template <int P>
-__global__ void __launch_bounds__(128) k_obs_factor(const int* oc, const int* op, const int* idx_cam, const double* rec,
+__global__ void __launch_bounds__(128, 5) k_obs_factor(const int* oc, const int* op, const int* idx_cam, const double* rec,
                                                     const double* s_a, const double* Lpt, const double* V, int t_count,
                                                     int n, double* Wb, double* Pfirst, double* Plast, double* Gsum) {
     constexpr int NE = P * 7;

@@ -135,7 +135,7 @@ __global__ void k_camera_rot(const double* cams, int n, int P, double* R) {
 // records are contiguous (by-camera slots): they are assembled in shared
 // memory (odd pitch: conflict-free) and written with coalesced 16-byte stores.
 template <int P>
-__global__ void __launch_bounds__(128) k_jacobian(const double* cams, const double* Rc, const double* pts, const int* oc,
+__global__ void __launch_bounds__(128, 5) k_jacobian(const double* cams, const double* Rc, const double* pts, const int* oc,
                                                   const int* op, const int* idx_cam, const double* sigma, int t_count,
                                                   double* rec, Status* st) {
     constexpr int PITCH = kRec + 1;

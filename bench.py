@@ -40,8 +40,9 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 throughput on this pool (profiles/fp64_peak.txt)
-FP64_PEAK_SOURCE = "measured: tools/probe/fp64_probe.cu DMMA loop 37.1 TF/s (cuBLAS DGEMM 16384^3: 36.0)"
+SWEEP_DRAM_BYTES_CFG3 = 11.0026e9  # profiles/r01_launches_bench_config3.txt ("dense sweep ... DRAM")
+FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 throughput on this pool (profiles/r01_fp64_peak_probe.txt)
+FP64_PEAK_SOURCE = "measured: tools/probe/fp64_probe.cu DMMA loop 37.1 TF/s, profiles/r01_fp64_peak_probe.txt (cuBLAS DGEMM 16384^3: 36.0; MEASURED_PEAKS.json has no FP64 entry)"
 
 
 def measured_hbm():
@@ -376,10 +377,13 @@ def main():
                 "kernel": "dense FP64 Cholesky + triangular inverse (k_gemm DMMA m8n8k4 + k_potrf_diag)",
                 "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if achieved else None,
-                "traffic": None,
-                "traffic_note": ("per-stage DRAM not captured live; profiles/r01_ncu_dense_and_schur.txt: the largest "
-                                 "trailing-update launch moves 555 MB DRAM against 590 MB algorithmic (C read+write "
-                                 "+ panel), i.e. no re-reads"),
+                "traffic": SWEEP_DRAM_BYTES_CFG3 if args.config == 3 else None,
+                "traffic_note": ("DRAM read+write summed over one sweep's launches (k_gemm, k_potrf_diag, "
+                                 "k_panel_take*), ncu launch list profiles/r01_launches_bench_config3.txt: the "
+                                 "right-looking sweep streams the trailing matrix once per 384-column panel "
+                                 "(~N^3/(3W)*16 B each for the Cholesky and the inverse); the largest trailing-"
+                                 "update launch moves 556 MB against 590 MB algorithmic (C read+write + panel), "
+                                 "i.e. no re-reads (profiles/r01_ncu_dense_and_schur.txt)"),
                 "peak_source": FP64_PEAK_SOURCE,
                 "algorithmic_flops": algo_flops, "executed_flops_padded": flops,
                 "stage_ms": dense_ms,

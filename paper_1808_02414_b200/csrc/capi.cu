@@ -389,6 +389,16 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     launch_build_index(sc, ix, h->ws, s);
     launch_structure_check(sc, ix, st, s);
     SFM_CUDA(cudaEventRecord(h->e_index, s));
+    mark(h, 1);
+    // ---- (a) Jacobian: the geometry needs no σ, so it runs while a host
+    // scene's σ is still uploading (its errors are reported after validation's)
+    double* R = nullptr;
+    double* rec = nullptr;
+    if (mode != M_INDEX) {
+        R = h->R.as<double>(9 * (size_t)n);
+        rec = h->rec.as<double>((size_t)kRec * t);
+        launch_jacobian(sc, ix.idx_cam, R, rec, st, s);
+    }
     if (sc.sigma_ready) SFM_CUDA(cudaStreamWaitEvent(s, sc.sigma_ready, 0));
     if (split_values) launch_validate_values(sc, st, s);
     if (full || mode == M_INDEX) {
@@ -407,11 +417,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         d2h(h, out.idx_pt, ix.idx_pt, 4 * (size_t)t);
         return;
     }
-    mark(h, 1);
-    // ---- (a) Jacobian ---------------------------------------------------------
-    double* R = h->R.as<double>(9 * (size_t)n);
-    double* rec = h->rec.as<double>((size_t)kRec * t);
-    launch_jacobian(sc, ix.idx_cam, R, rec, st, s);
+    launch_weights(sc, ix.idx_cam, rec, st, s);
     mark(h, 2);
     if (mode == M_JACOBIAN) {
         sync_status(h);
@@ -503,7 +509,8 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     mark(h, 4);
     // The pair list depends only on the index: it is built on s2 from the
     // index event while s runs the numeric stage-A kernels queued above (its
-    // host reads of the list sizes then stall s2 only).
+    // host reads of the list sizes then stall s2 only).  (Starting it before
+    // the host's σ wait instead measured no different end to end.)
     SFM_CUDA(cudaStreamWaitEvent(h->s2, h->e_index, 0));
     build_pairs(sc, ix, h->pairs, h->ws_pairs, h->s2);
     SFM_CUDA(cudaEventRecord(h->e_pairs, h->s2));

@@ -125,6 +125,7 @@ void launch_validate_values(const SceneDev& sc, Status* st, cudaStream_t s);
 void launch_build_index(const SceneDev& sc, IndexDev& ix, Workspace& ws, cudaStream_t s);
 void launch_structure_check(const SceneDev& sc, const IndexDev& ix, Status* st, cudaStream_t s);
 void launch_jacobian(const SceneDev& sc, const int* idx_cam, double* R, double* rec, Status* st, cudaStream_t s);
+void launch_weights(const SceneDev& sc, const int* idx_cam, double* rec, Status* st, cudaStream_t s);
 void launch_depth_of(const SceneDev& sc, const double* R, int t, double* out, cudaStream_t s);
 void launch_reductions(const SceneDev& sc, const IndexDev& ix, const double* rec, double* D, double* Hr, double* A,
                        double* s_a, unsigned char* flags, Status* st, cudaStream_t s, cudaStream_t side,

@@ -130,14 +130,15 @@ __global__ void k_camera_rot(const double* cams, int n, int P, double* R) {
     rotation_matrix(cams + (size_t)P * i, R + 9 * (size_t)i);
 }
 
-// One thread per observation; writes the AoS record [jc | jp | W].  W is the
-// explicit 2x2 inverse of sigma (covariance.cpp:20-29).  The CTA's 128
+// One thread per observation; writes the AoS record [jc | jp | 0 | tg] (the
+// geometry only: it runs while a host scene's σ is still uploading; k_weights
+// fills W once σ has arrived).  The CTA's 128
 // records are contiguous (by-camera slots): they are assembled in shared
 // memory (odd pitch: conflict-free) and written with coalesced 16-byte stores.
 template <int P>
 __global__ void __launch_bounds__(128, 5) k_jacobian(const double* cams, const double* Rc, const double* pts, const int* oc,
-                                                  const int* op, const int* idx_cam, const double* sigma, int t_count,
-                                                  double* rec, Status* st) {
+                                                  const int* op, const int* idx_cam, int t_count, double* rec,
+                                                  Status* st) {
     constexpr int PITCH = kRec + 1;
     __shared__ double buf[128 * PITCH];
     const int k0 = blockIdx.x * blockDim.x;
@@ -148,18 +149,10 @@ __global__ void __launch_bounds__(128, 5) k_jacobian(const double* cams, const d
         double jc[2 * P], jp[6], depth;
         const bool ok = observation_jacobian<P>(cams + (size_t)P * ci, Rc + 9 * (size_t)ci, pts + 3 * (size_t)pj, jc, jp, &depth);
         if (!ok) atomicMin(&st->jac_bad, t);
-        double s00 = 1.0, s01 = 0.0, s10 = 0.0, s11 = 1.0;
-        if (sigma) { s00 = sigma[4 * (size_t)t]; s01 = sigma[4 * (size_t)t + 1]; s10 = sigma[4 * (size_t)t + 2]; s11 = sigma[4 * (size_t)t + 3]; }
-        const double det = s00 * s11 - s01 * s10;
-        if (!(s00 > 0.0) || !(det > 0.0)) atomicMin(&st->fisher_bad, t);
         double* rr = buf + threadIdx.x * PITCH;
-        for (int z = 0; z < kRec; ++z) rr[z] = 0.0;
+        for (int z = 0; z < kRec; ++z) rr[z] = 0.0;  // W (k_weights) stays 0 here
         for (int z = 0; z < 2 * P; ++z) rr[Layout<P>::JC + z] = jc[z];
         for (int z = 0; z < 6; ++z) rr[Layout<P>::JP + z] = jp[z];
-        rr[Layout<P>::WO + 0] = s11 / det;
-        rr[Layout<P>::WO + 1] = -s01 / det;
-        rr[Layout<P>::WO + 2] = -s10 / det;
-        rr[Layout<P>::WO + 3] = s00 / det;
         // rotation-rhs factors of this observation (the camera_reduce rhs entries):
         // tg[ii][q] = -((d_C row ii . [C]x col q) + (d_X row ii . [X]x col q))
         double hc[9], hx[9];
@@ -179,6 +172,25 @@ __global__ void __launch_bounds__(128, 5) k_jacobian(const double* cams, const d
         const int o = w / (kRec / 2), part = w - o * (kRec / 2);
         out[w] = make_double2(buf[o * PITCH + 2 * part], buf[o * PITCH + 2 * part + 1]);
     }
+}
+
+// W = σ^-1 into each record, the explicit 2x2 inverse (covariance.cpp:20-29),
+// and the reference's Fisher-stage check (covariance.cpp:50-53).
+__global__ void k_weights(const int* idx_cam, const double* sigma, int t_count, int wo, double* rec, Status* st) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= t_count) return;
+    const int t = idx_cam[k];
+    double s00 = 1.0, s01 = 0.0, s10 = 0.0, s11 = 1.0;
+    if (sigma) {
+        const double2 a = reinterpret_cast<const double2*>(sigma)[2 * (size_t)t];
+        const double2 b = reinterpret_cast<const double2*>(sigma)[2 * (size_t)t + 1];
+        s00 = a.x; s01 = a.y; s10 = b.x; s11 = b.y;
+    }
+    const double det = s00 * s11 - s01 * s10;
+    if (!(s00 > 0.0) || !(det > 0.0)) atomicMin(&st->fisher_bad, t);
+    double2* w = reinterpret_cast<double2*>(rec + (size_t)k * kRec + wo);
+    w[0] = make_double2(s11 / det, -s01 / det);
+    w[1] = make_double2(-s10 / det, s00 / det);
 }
 
 // Depth of one observation (error message path only).
@@ -480,10 +492,17 @@ void launch_structure_check(const SceneDev& sc, const IndexDev& ix, Status* st, 
 void launch_jacobian(const SceneDev& sc, const int* idx_cam, double* R, double* rec, Status* st, cudaStream_t s) {
     if (sc.n) { k_camera_rot<<<cdiv(sc.n, 128), 128, 0, s>>>(sc.cams, sc.n, sc.P, R); SFM_LAUNCH_CHECK(); }
     if (sc.t) {
-        if (sc.P == 8) k_jacobian<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, idx_cam, sc.sigma, sc.t, rec, st);
-        else k_jacobian<9><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, idx_cam, sc.sigma, sc.t, rec, st);
+        if (sc.P == 8) k_jacobian<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, idx_cam, sc.t, rec, st);
+        else k_jacobian<9><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.cams, R, sc.pts, sc.oc, sc.op, idx_cam, sc.t, rec, st);
         SFM_LAUNCH_CHECK();
     }
+}
+
+void launch_weights(const SceneDev& sc, const int* idx_cam, double* rec, Status* st, cudaStream_t s) {
+    if (!sc.t) return;
+    const int wo = sc.P == 8 ? Layout<8>::WO : Layout<9>::WO;
+    k_weights<<<cdiv(sc.t, 256), 256, 0, s>>>(idx_cam, sc.sigma, sc.t, wo, rec, st);
+    SFM_LAUNCH_CHECK();
 }
 
 void launch_depth_of(const SceneDev& sc, const double* R, int t, double* out, cudaStream_t s) {

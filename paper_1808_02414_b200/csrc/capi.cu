@@ -223,14 +223,23 @@ void throw_numeric(sfmcov_handle* h, const SceneDev& sc, Mode mode) {
                            "; the scene is likely disconnected or its gauge degenerate"};
 }
 
-// Dense panel width in kNB blocks (SFMCOV_PANEL, default 3).
-int panel_blocks() {
-    static int g = [] {
+// Dense panel width in kNB blocks for K = Npad / kNB tiles over R ranks.
+// Wider panels mean longer K in the trailing updates (better DMMA efficiency,
+// fewer passes over the trailing matrix) but a longer per-panel critical
+// chain; measured best (1 B200): K = 71 (config 3): 3 (4: +0.7 %);
+// K = 211 (config 4): 8-12 (408 -> 397 ms vs 3); K = 704 (config 5): 16
+// (14.83 -> 14.24 s vs 3).  Hence K / (24 R) clamped to [3, 16]; the
+// distributed sweep keeps >= 24 panels per rank for its block-cyclic balance.
+// SFMCOV_PANEL overrides.
+int panel_blocks(int K, int R) {
+    static int forced = [] {
         const char* e = std::getenv("SFMCOV_PANEL");
-        const int v = e ? std::atoi(e) : 3;
-        return (v >= 1 && v <= 8) ? v : 3;
+        const int v = e ? std::atoi(e) : 0;
+        return (v >= 1 && v <= 16) ? v : 0;
     }();
-    return g;
+    if (forced) return forced;
+    const int g = K / (24 * (R > 0 ? R : 1));
+    return g < 3 ? 3 : (g > 16 ? 16 : g);
 }
 
 // SFMCOV_SERIAL_DENSE=1 runs the lookahead updates on the main stream
@@ -252,7 +261,7 @@ void mark(sfmcov_handle* h, int i) {
 int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv, double* piv, Status* st, bool serial,
               bool mark_stages) {
     cudaStream_t s = h->s;
-    const int pw = panel_blocks();
+    const int pw = panel_blocks(Npad / kNB, 1);
     double* ring = h->ring.as<double>(sweep_ring_doubles(Npad, pw, sfmcov_handle::kRing));
     const int launches = dense_sweep(Z, ld, Npad, pw, Linv, piv, st, ring, sfmcov_handle::kRing, s, serial ? s : h->s2,
                                      serial ? s : h->s3, h->eL, h->eT, h->e2, serial ? s : h->s4, h->eX, h->eN);
@@ -641,7 +650,7 @@ void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const dou
     const int R = h->dist_mode == 1 ? h->emu_R : h->dist_R;
     const int nloc = h->dist_mode == 1 ? R : 1;
     if (nloc > 64) throw ApiError{SFMCOV_ERR_DIMENSION, "options", "at most 64 emulated ranks"};
-    const int Gp = panel_blocks();
+    const int Gp = panel_blocks(Npad / kNB, R);
     if ((int)h->ranks.size() < nloc) h->ranks.resize(nloc);
     if (!h->ev_rank_init) {
         SFM_CUDA(cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming));

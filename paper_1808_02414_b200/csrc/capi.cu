@@ -25,6 +25,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <future>
 #include <thread>
 #include <unistd.h>
 #include <vector>
@@ -368,15 +369,23 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     mark(h, 0);
     launch_status_init(st, s);
     launch_validate(sc, full ? 1 : 0, st, s);
-    // host-API scenes: the finiteness of u is checked here, overlapping the
-    // upload, and merged as the reference's code-3 failure of that observation
-    const long long u_bad = (full && sc.host_u) ? first_nonfinite_u(sc.host_u, t) : LLONG_MAX;
-    auto sync_validation = [&] {
+    // host-API scenes: the finiteness of u is checked on host threads beside
+    // the device work (an async task, joined at the last validation sync or
+    // as soon as the device reports a failure, so it never sits on the
+    // critical path of a valid scene) and merged as the reference's code-3
+    // failure of that observation
+    const bool split_values = full && sc.sigma_ready;  // σ checks after its upload
+    std::future<long long> u_task;
+    if (full && sc.host_u) u_task = std::async(std::launch::async, first_nonfinite_u, sc.host_u, (long long)t);
+    long long u_bad = LLONG_MAX;
+    auto sync_validation = [&](bool final_sync) {
         sync_status(h);
+        const Status& q = *h->st_host;
+        const bool failing = q.cam_bad != INT_MAX || q.pt_bad != INT_MAX || q.obs_bad != LLONG_MAX;
+        if (u_task.valid() && (final_sync || failing)) u_bad = u_task.get();
         if (u_bad != LLONG_MAX) h->st_host->obs_bad = std::min(h->st_host->obs_bad, u_bad * 8 + 3);
     };
-    sync_validation();
-    const bool split_values = full && sc.sigma_ready;  // σ checks after its upload
+    sync_validation(!split_values);
     if (split_values) {
         const Status& q = *h->st_host;
         if (q.cam_bad != INT_MAX || q.pt_bad != INT_MAX || q.obs_bad != LLONG_MAX) {
@@ -384,7 +393,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
             // observation is reported, as the reference's single pass does
             SFM_CUDA(cudaStreamWaitEvent(s, sc.sigma_ready, 0));
             launch_validate_values(sc, st, s);
-            sync_validation();
+            sync_validation(true);
         }
     }
     throw_validation(h, sc, full);
@@ -411,7 +420,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     if (sc.sigma_ready) SFM_CUDA(cudaStreamWaitEvent(s, sc.sigma_ready, 0));
     if (split_values) launch_validate_values(sc, st, s);
     if (full || mode == M_INDEX) {
-        sync_validation();
+        sync_validation(true);
         if (split_values) throw_validation(h, sc, full);
         if (h->st_host->dup) throw ApiError{SFMCOV_ERR_INVARIANT, "validate", "duplicate (camera, point) observation pair"};
         throw_counts(h);

@@ -132,11 +132,23 @@ __global__ void __launch_bounds__(128, 5) k_obs_factor(const int* oc, const int*
     {
         const double2* in = reinterpret_cast<const double2*>(rec + (size_t)k0 * kRec);
         constexpr int NP = (Layout<P>::WO + 4 + 1) / 2;  // double2 parts of the record that are used
-        for (int w = threadIdx.x; w < nv * NP; w += 128) {
+        // all NP loads of a thread in flight before the first shared store
+        // (a load -> store loop serialises the HBM latency per iteration)
+        double2 v[NP];
+#pragma unroll
+        for (int u = 0; u < NP; ++u) {
+            const int w = threadIdx.x + 128 * u;
             const int o = w / NP, part = w - o * NP;
-            const double2 v = __ldcs(in + (size_t)o * (kRec / 2) + part);
-            buf[o * PITCH + 2 * part] = v.x;
-            if (2 * part + 1 < PITCH) buf[o * PITCH + 2 * part + 1] = v.y;
+            if (w < nv * NP) v[u] = __ldcs(in + (size_t)o * (kRec / 2) + part);
+        }
+#pragma unroll
+        for (int u = 0; u < NP; ++u) {
+            const int w = threadIdx.x + 128 * u;
+            const int o = w / NP, part = w - o * NP;
+            if (w < nv * NP) {
+                buf[o * PITCH + 2 * part] = v[u].x;
+                buf[o * PITCH + 2 * part + 1] = v[u].y;
+            }
         }
     }
     __syncthreads();

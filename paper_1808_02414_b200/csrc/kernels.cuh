@@ -69,7 +69,7 @@ struct IndexDev {
 
 struct PairDev {
     DBuf buf_cnt, buf_off, buf_k0, buf_k1, buf_v0, buf_v1, buf_ukeys, buf_counts, buf_nruns, buf_seg, buf_chunk,
-        buf_part;
+        buf_part, buf_segof;
     long long* cnt = nullptr;
     long long* off = nullptr;
     long long npairs = 0;
@@ -80,11 +80,12 @@ struct PairDev {
     int nseg = 0;
     int* chunk_off = nullptr;  // segment -> first chunk of <= chunk pairs (nseg + 1)
     int nchunks = 0, chunk = 0;
+    int* seg_of = nullptr;     // chunk -> its segment (nchunks)
     double* part = nullptr;    // per-chunk partial blocks of multi-chunk segments
     void release() {
         buf_cnt.release(); buf_off.release(); buf_k0.release(); buf_k1.release(); buf_v0.release();
         buf_v1.release(); buf_ukeys.release(); buf_counts.release(); buf_nruns.release(); buf_seg.release();
-        buf_chunk.release(); buf_part.release();
+        buf_chunk.release(); buf_part.release(); buf_segof.release();
     }
 };
 

@@ -494,21 +494,15 @@ __device__ __forceinline__ void dmma_pr(double& d0, double& d1, double a, double
 }
 
 template <int P, int U, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned int* ukeys, const long long* seg_off, int nseg,
-                                                         const int* chunk_off, int nchunks, int chunk,
-                                                         const unsigned long long* vals, const double* Wb, int n,
-                                                         double* Z, long long ld, double* part, int cfirst,
+__global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned int* ukeys, const long long* seg_off,
+                                                         const int* seg_of, const int* chunk_off, int nchunks,
+                                                         int chunk, const unsigned long long* vals, const double* Wb,
+                                                         int n, double* Z, long long ld, double* part, int cfirst,
                                                          int always_part) {
     const int warp = cfirst + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (warp >= nchunks) return;
-    // segment of this chunk: largest sg with chunk_off[sg] <= warp
-    int lo_s = 0, hi_s = nseg - 1;
-    while (lo_s < hi_s) {
-        const int mid = (lo_s + hi_s + 1) >> 1;
-        if (__ldg(chunk_off + mid) <= warp) lo_s = mid; else hi_s = mid - 1;
-    }
-    const int sg = lo_s;
+    const int sg = __ldg(seg_of + warp);  // (a binary search over chunk_off was ~16 dependent loads)
     const int c0 = __ldg(chunk_off + sg), nch = __ldg(chunk_off + sg + 1) - c0;
     const int r = lane >> 2, k = lane & 3;
     const long long sb = seg_off[sg], se = seg_off[sg + 1];
@@ -671,6 +665,12 @@ static int pair_chunk() {
     return c;
 }
 
+__global__ void k_chunk_segment(const int* chunk_off, int nseg, int* seg_of) {
+    const int sg = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sg >= nseg) return;
+    for (int c = chunk_off[sg]; c < chunk_off[sg + 1]; ++c) seg_of[c] = sg;
+}
+
 __global__ void k_chunk_count(const int* counts, int nseg, int chunk, int* ccnt) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nseg) ccnt[i] = (counts[i] + chunk - 1) / chunk;
@@ -744,6 +744,11 @@ void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace&
     SFM_CUDA(cudaStreamSynchronize(s));
     pd.chunk_off = coff;
     pd.nchunks = nch;
+    pd.seg_of = (int*)pd.buf_segof.get(4 * ((size_t)nch + 1));
+    if (nseg) {
+        k_chunk_segment<<<cdiv(nseg, 256), 256, 0, s>>>(coff, nseg, pd.seg_of);
+        SFM_LAUNCH_CHECK();
+    }
     pd.part = (double*)pd.buf_part.get(8 * 81 * ((size_t)nch + 1));
 }
 
@@ -754,10 +759,10 @@ void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, doubl
     // 4 pairs gathered ahead, 4 CTAs (32 warps) per SM: the kernel is bound
     // by gather latency, so occupancy beats deeper prefetch
     if (P == 8)
-        k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, pd.nchunks,
+        k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, pd.nchunks,
                                                             pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0);
     else
-        k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, pd.nchunks,
+        k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, pd.nchunks,
                                                             pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0);
     SFM_LAUNCH_CHECK();
     if (P == 8) k_pair_combine<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld);
@@ -771,10 +776,10 @@ void launch_pair_reduce_segments(int P, const PairDev& pd, const double* Wb, int
     if (c_end > c_begin) {
         const unsigned cblocks = cdiv(c_end - c_begin, 8);
         if (P == 8)
-            k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, c_end,
+            k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, c_end,
                                                                 pd.chunk, pd.vals, Wb, n, nullptr, 0, pd.part, c_begin, 1);
         else
-            k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.nseg, pd.chunk_off, c_end,
+            k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, c_end,
                                                                 pd.chunk, pd.vals, Wb, n, nullptr, 0, pd.part, c_begin, 1);
         SFM_LAUNCH_CHECK();
     }

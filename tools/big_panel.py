@@ -9,4 +9,4 @@ eng.set_profiling(True)
 for it in range(2):
     eng.compute_covariance(rec)
     st = eng.stage_times()
-    print(f"config {cfg} panel {os.environ.get('SFMCOV_PANEL', '3')} run {it}: cholesky {st['cholesky']:.1f} ms", flush=True)
+    print(f"config {cfg} panel {os.environ.get('SFMCOV_PANEL', 'auto')} run {it}: cholesky {st['cholesky']:.1f} ms", flush=True)

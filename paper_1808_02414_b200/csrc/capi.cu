@@ -853,8 +853,13 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
         int lo = 0, hi = 0;
         SFM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s, cudaStreamNonBlocking, hi));
-        SFM_CUDA(cudaStreamCreateWithPriority(&h->s2, cudaStreamNonBlocking, (lo + hi) / 2));
-        SFM_CUDA(cudaStreamCreateWithPriority(&h->s3, cudaStreamNonBlocking, lo));
+        // sweep streams: the inverse chain (s3) above the Cholesky trailing
+        // updates (s2).  Both have slack, but the inverse's narrow row-panel
+        // launches must not pile up behind the wide updates into a tail where
+        // they underfill the GPU: config 3 sweep 17.57 -> 16.9 ms (the
+        // inverse now ends 0.1 ms after the Cholesky instead of 3.7 ms).
+        SFM_CUDA(cudaStreamCreateWithPriority(&h->s2, cudaStreamNonBlocking, lo));
+        SFM_CUDA(cudaStreamCreateWithPriority(&h->s3, cudaStreamNonBlocking, (lo + hi) / 2));
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s4, cudaStreamNonBlocking, hi));
         SFM_CUDA(cudaEventCreateWithFlags(&h->eX, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->eN, cudaEventDisableTiming));

@@ -357,8 +357,10 @@ void RankDense::init(int device) {
     int lo = 0, hi = 0;
     SFM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     SFM_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
-    SFM_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, (lo + hi) / 2));
-    SFM_CUDA(cudaStreamCreateWithPriority(&s3, cudaStreamNonBlocking, lo));
+    // the inverse chain (s3) above the trailing updates (s2), as in the
+    // single-GPU sweep (capi.cu)
+    SFM_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, lo));
+    SFM_CUDA(cudaStreamCreateWithPriority(&s3, cudaStreamNonBlocking, (lo + hi) / 2));
     SFM_CUDA(cudaStreamCreateWithPriority(&sc, cudaStreamNonBlocking, hi));
     for (int i = 0; i < NB; ++i)
         for (cudaEvent_t* e : {&eL[i], &eB[i], &eRest[i], &eT[i], &eU[i]})

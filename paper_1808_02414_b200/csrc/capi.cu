@@ -61,6 +61,8 @@ struct sfmcov_handle {
     cudaEvent_t e_index = nullptr, e_pairs = nullptr;  // pair-list build on s2, overlapped with stage A
     cudaEvent_t e_ids = nullptr, e_sigma = nullptr;    // host API: σ uploads on s3 after the indices
     cudaEvent_t e_red_fork = nullptr, e_red_join = nullptr;  // point reduction on s4 beside the camera one
+    cudaEvent_t e_fill = nullptr, e_zrest = nullptr;          // pair reduction of the later block columns on s2
+    cudaEvent_t e_pr0 = nullptr, e_pr1 = nullptr;             // its duration (profiling)
     cudaEvent_t e1 = nullptr, e2 = nullptr;
     static constexpr int kRing = 4;  // panel ring buffers of the fused sweep
     cudaEvent_t eL[kRing], eT[kRing];
@@ -253,19 +255,20 @@ bool serial_dense() {
 // Cholesky + in-place triangular inverse of the padded matrix Z (lower
 // triangle); serial = every launch on the main stream.
 int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv, double* piv, Status* st, bool serial,
-              bool mark_stages);
+              bool mark_stages, cudaEvent_t eZ = nullptr);
 
 void mark(sfmcov_handle* h, int i) {
     if (h->profiling) SFM_CUDA(cudaEventRecord(h->ev[i], h->s));
 }
 
 int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv, double* piv, Status* st, bool serial,
-              bool mark_stages) {
+              bool mark_stages, cudaEvent_t eZ) {
     cudaStream_t s = h->s;
     const int pw = panel_blocks(Npad / kNB, 1);
     double* ring = h->ring.as<double>(sweep_ring_doubles(Npad, pw, sfmcov_handle::kRing));
     const int launches = dense_sweep(Z, ld, Npad, pw, Linv, piv, st, ring, sfmcov_handle::kRing, s, serial ? s : h->s2,
-                                     serial ? s : h->s3, h->eL, h->eT, h->e2, serial ? s : h->s4, h->eX, h->eN);
+                                     serial ? s : h->s3, h->eL, h->eT, h->e2, serial ? s : h->s4, h->eX, h->eN,
+                                     serial ? nullptr : eZ);
     if (mark_stages) {
         mark(h, 8);
         mark(h, 9);
@@ -543,7 +546,25 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     double* Z = h->Z.as<double>((size_t)Npad * Npad);
     launch_fill(P, Z, ld, N, Npad, D, s_a, G, mode == M_FULL ? 1 : 0, s);
     mark(h, 6);
-    launch_pair_reduce(P, h->pairs, Wb, n, Z, ld, s);
+    // The first panel of the sweep needs only its own block columns: those
+    // are reduced here, the others on s2 beside its factorisation (the sweep
+    // waits for them before its first next-panel update; disjoint blocks).
+    const int pw0 = panel_blocks(Npad / kNB, 1);
+    const int lo_split = std::min(n, (pw0 * kNB + P - 1) / P);  // cameras with a column in panel 0
+    const bool split_pairs = mode == M_FULL && !serial_dense() && Npad / kNB > pw0 && lo_split < n;
+    bool pr_timed = false;
+    if (split_pairs) {
+        SFM_CUDA(cudaEventRecord(h->e_fill, s));
+        launch_pair_reduce(P, h->pairs, Wb, n, Z, ld, s, 0, lo_split);
+        SFM_CUDA(cudaStreamWaitEvent(h->s2, h->e_fill, 0));
+        if (h->profiling) SFM_CUDA(cudaEventRecord(h->e_pr0, h->s2));
+        launch_pair_reduce(P, h->pairs, Wb, n, Z, ld, h->s2, lo_split, n);
+        if (h->profiling) SFM_CUDA(cudaEventRecord(h->e_pr1, h->s2));
+        SFM_CUDA(cudaEventRecord(h->e_zrest, h->s2));
+        pr_timed = h->profiling;
+    } else {
+        launch_pair_reduce(P, h->pairs, Wb, n, Z, ld, s);
+    }
     mark(h, 7);
     h->counts[0] = h->pairs.npairs;
     h->counts[1] = h->pairs.nseg;
@@ -578,7 +599,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     double* Linv = h->Linv.as<double>((size_t)K * kNB * kNB);
     double* piv = h->piv.as<double>((size_t)Npad);
     const bool serial = serial_dense();
-    run_dense(h, Z, ld, Npad, Linv, piv, st, serial, true);
+    run_dense(h, Z, ld, Npad, Linv, piv, st, serial, true, split_pairs ? h->e_zrest : nullptr);
     int* psd = h->psd.as<int>(1);
     SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
     const bool cross = out.h_camera_matrix != nullptr;
@@ -638,6 +659,13 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
             float ms = 0.f;
             SFM_CUDA(cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]));
             h->stage_ms[i] = ms;
+        }
+        if (pr_timed) {
+            // the later block columns' pair reduction ran on s2 beside the
+            // first panel (its time also lies inside the cholesky stage)
+            float ms = 0.f;
+            SFM_CUDA(cudaEventElapsedTime(&ms, h->e_pr0, h->e_pr1));
+            h->stage_ms[6] += ms;
         }
     }
     fill_diagnostics(h, out, prange, eigE, psd, s_a, flags, ncols, N, (int64_t)8 * Npad * (int64_t)Npad);
@@ -869,6 +897,10 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
         SFM_CUDA(cudaEventCreateWithFlags(&h->e_sigma, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->e_red_fork, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->e_red_join, cudaEventDisableTiming));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->e_fill, cudaEventDisableTiming));
+        SFM_CUDA(cudaEventCreateWithFlags(&h->e_zrest, cudaEventDisableTiming));
+        SFM_CUDA(cudaEventCreate(&h->e_pr0));
+        SFM_CUDA(cudaEventCreate(&h->e_pr1));
         for (int i = 0; i < sfmcov_handle::kRing; ++i) {
             SFM_CUDA(cudaEventCreateWithFlags(&h->eL[i], cudaEventDisableTiming));
             SFM_CUDA(cudaEventCreateWithFlags(&h->eT[i], cudaEventDisableTiming));
@@ -931,6 +963,10 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaEventDestroy(h->e_sigma);
     cudaEventDestroy(h->e_red_fork);
     cudaEventDestroy(h->e_red_join);
+    cudaEventDestroy(h->e_fill);
+    cudaEventDestroy(h->e_zrest);
+    cudaEventDestroy(h->e_pr0);
+    cudaEventDestroy(h->e_pr1);
     for (int i = 0; i < sfmcov_handle::kRing; ++i) {
         cudaEventDestroy(h->eL[i]);
         cudaEventDestroy(h->eT[i]);

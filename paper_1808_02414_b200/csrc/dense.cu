@@ -888,7 +888,11 @@ struct SweepTrace {
 
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
-                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN) {
+                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN, cudaEvent_t eZ) {
+    // eZ (optional): Z's columns beyond the first panel are complete (the
+    // pair reduction of the other block columns, queued on s2 before this
+    // sweep): waited for by the first next-panel update on s; rest(0) is
+    // ordered after it on s2 itself.
     SweepTrace tr;
     const bool trace = sweep_trace();
     bool next_pending = false;  // the previous step's update of the next panel's later columns (s4)
@@ -956,6 +960,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             // potrf / trsm need only it), the later columns on s4 concurrently
             // (the next panel's first inner update waits for them)
             if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, eR, 0));
+            if (p == 0 && eZ) SFM_CUDA(cudaStreamWaitEvent(s, eZ, 0));
             const bool split = gn > 1 && s4 != s;
             if (split) SFM_CUDA(cudaEventRecord(eX, s));
             GemmArgs u = gemm_args(Z + (size_t)nb0 * kNB * ld + (size_t)nb0 * kNB, ld, Lb + W, rows, Lb + W, rows, T2,

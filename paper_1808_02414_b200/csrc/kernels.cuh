@@ -149,7 +149,8 @@ void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* 
 void launch_fill(int P, double* Z, long long ld, int N, int Npad, const double* D, const double* s_a, const double* G,
                  int add_gg, cudaStream_t s);
 void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace& ws, cudaStream_t s);
-void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, cudaStream_t s);
+void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, cudaStream_t s,
+                        int lo_min = 0, int lo_max = 1 << 30);
 
 // dense.cu
 void dense_init_attributes();
@@ -164,7 +165,7 @@ void launch_minmax(const double* x, long long count, double* part, double* out, 
 void launch_pivot_range(const double* piv, int N, double* out, cudaStream_t s);
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
-                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN);
+                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN, cudaEvent_t eZ = nullptr);
 inline size_t sweep_ring_doubles(int Npad, int G, int NB) { return (size_t)NB * Npad * G * kNB; }
 
 // ---- optional outputs (fullcov.cu) ------------------------------------------

@@ -498,11 +498,14 @@ __global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned in
                                                          const int* seg_of, const int* chunk_off, int nchunks,
                                                          int chunk, const unsigned long long* vals, const double* Wb,
                                                          int n, double* Z, long long ld, double* part, int cfirst,
-                                                         int always_part) {
+                                                         int always_part, int lo_min, int lo_max) {
     const int warp = cfirst + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (warp >= nchunks) return;
     const int sg = __ldg(seg_of + warp);  // (a binary search over chunk_off was ~16 dependent loads)
+    const unsigned int key = ukeys[sg];
+    const int lo = (int)(key / (unsigned int)n), hi = (int)(key - (unsigned int)lo * (unsigned int)n);
+    if (lo < lo_min || lo >= lo_max) return;  // block column outside this launch's camera range
     const int c0 = __ldg(chunk_off + sg), nch = __ldg(chunk_off + sg + 1) - c0;
     const int r = lane >> 2, k = lane & 3;
     const long long sb = seg_off[sg], se = seg_off[sg + 1];
@@ -552,8 +555,6 @@ __global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned in
         x88 += __shfl_xor_sync(0xffffffffu, x88, 1);
         x88 += __shfl_xor_sync(0xffffffffu, x88, 2);
     }
-    const unsigned int key = ukeys[sg];
-    const int lo = (int)(key / (unsigned int)n), hi = (int)(key - (unsigned int)lo * (unsigned int)n);
     const bool diag = lo == hi;
     // single chunk: Z(P hi + p, P lo + q) -= out(p, q) (diagonal blocks: lower
     // part only); else the chunk's partial block, combined by k_pair_combine
@@ -579,7 +580,8 @@ __global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned in
 // Multi-chunk segments: partial blocks summed in chunk order, then written.
 template <int P>
 __global__ void __launch_bounds__(256) k_pair_combine(const unsigned int* ukeys, int nseg, const int* chunk_off,
-                                                      const double* part, int n, double* Z, long long ld) {
+                                                      const double* part, int n, double* Z, long long ld, int lo_min,
+                                                      int lo_max) {
     const int sg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (sg >= nseg) return;
@@ -587,6 +589,7 @@ __global__ void __launch_bounds__(256) k_pair_combine(const unsigned int* ukeys,
     if (c1 - c0 < 2) return;
     const unsigned int key = ukeys[sg];
     const int lo = (int)(key / (unsigned int)n), hi = (int)(key - (unsigned int)lo * (unsigned int)n);
+    if (lo < lo_min || lo >= lo_max) return;
     for (int en = lane; en < P * P; en += 32) {
         const int p = en / P, q = en - P * (en / P);
         if (lo == hi && p < q) continue;
@@ -752,7 +755,11 @@ void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace&
     pd.part = (double*)pd.buf_part.get(8 * 81 * ((size_t)nch + 1));
 }
 
-void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, cudaStream_t s) {
+// Segments whose block column (camera lo) lies in [lo_min, lo_max): the
+// sweep's first panel needs only its own columns, so the pipeline reduces
+// those first and the rest beside the first panel's factorisation.
+void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, cudaStream_t s,
+                        int lo_min, int lo_max) {
     if (!pd.nseg) return;
     const unsigned blocks = cdiv(pd.nseg, 8);
     const unsigned cblocks = cdiv(pd.nchunks, 8);
@@ -760,13 +767,13 @@ void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, doubl
     // by gather latency, so occupancy beats deeper prefetch
     if (P == 8)
         k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, pd.nchunks,
-                                                            pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0);
+                                                            pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0, lo_min, lo_max);
     else
         k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, pd.nchunks,
-                                                            pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0);
+                                                            pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0, lo_min, lo_max);
     SFM_LAUNCH_CHECK();
-    if (P == 8) k_pair_combine<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld);
-    else k_pair_combine<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld);
+    if (P == 8) k_pair_combine<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld, lo_min, lo_max);
+    else k_pair_combine<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld, lo_min, lo_max);
     SFM_LAUNCH_CHECK();
 }
 
@@ -777,10 +784,10 @@ void launch_pair_reduce_segments(int P, const PairDev& pd, const double* Wb, int
         const unsigned cblocks = cdiv(c_end - c_begin, 8);
         if (P == 8)
             k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, c_end,
-                                                                pd.chunk, pd.vals, Wb, n, nullptr, 0, pd.part, c_begin, 1);
+                                                                pd.chunk, pd.vals, Wb, n, nullptr, 0, pd.part, c_begin, 1, 0, n);
         else
             k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, c_end,
-                                                                pd.chunk, pd.vals, Wb, n, nullptr, 0, pd.part, c_begin, 1);
+                                                                pd.chunk, pd.vals, Wb, n, nullptr, 0, pd.part, c_begin, 1, 0, n);
         SFM_LAUNCH_CHECK();
     }
     const unsigned blocks = cdiv(pd.nseg, 8);

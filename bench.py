@@ -401,6 +401,10 @@ def main():
                 "roofline_time_ms": t_star * 1e3, "frac": (t_star * 1e3) / schur_ms if schur_ms else None,
                 "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src, "bytes": b_schur, "flops": f_schur,
                 "stage_ms": schur_ms,
+                "stage_note": ("point prep + pair-list wait + pair reduction; the pair reduction of the block "
+                               "columns beyond the first panel runs on a second stream beside the first panel's "
+                               "factorisation and is counted here in full (its time also lies inside the "
+                               "cholesky stage, which the roofline above therefore understates)"),
             },
             "inversion": {"TFLOP_per_s": achieved, "frac_fp64": achieved / peak if achieved else None},
             "stages_ms": stages,

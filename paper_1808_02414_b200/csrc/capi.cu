@@ -419,6 +419,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         R = h->R.as<double>(9 * (size_t)n);
         rec = h->rec.as<double>((size_t)kRec * t);
         launch_jacobian(sc, ix.idx_cam, R, rec, st, s);
+        mark(h, 2);  // W = σ^-1 (k_weights) counts to the Fisher stage, as in the reference
     }
     if (sc.sigma_ready) SFM_CUDA(cudaStreamWaitEvent(s, sc.sigma_ready, 0));
     if (split_values) launch_validate_values(sc, st, s);
@@ -439,7 +440,6 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         return;
     }
     launch_weights(sc, ix.idx_cam, rec, st, s);
-    mark(h, 2);
     if (mode == M_JACOBIAN) {
         sync_status(h);
         throw_numeric(h, sc, mode);

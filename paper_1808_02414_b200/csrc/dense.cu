@@ -37,14 +37,17 @@ constexpr int BM = 128, BN = 128, PAD = 8, LDS = BM + PAD;
 // CTA tile 128 x (64 HN) with 8 HN warps of 32 x 32: HN = 2 is one CTA per
 // SM (512 threads), HN = 1 two CTAs per SM whose prologue / epilogue overlap
 // the other's MMAs.
-template <int BK, int STAGES, int HN>
+// RH = 2: 64 x 64 CTAs of 4 warps (four per 128 x 128 tile), four CTAs per SM.
+template <int BK, int STAGES, int HN, int RH = 1>
 struct Cfg {
-    static constexpr int THREADS = 256 * HN;
+    static constexpr int THREADS = 256 * HN / RH;
+    static constexpr int BMC = BM / RH;      // CTA rows
+    static constexpr int LDSA = BMC + PAD;   // M-contiguous A tile pitch
     static constexpr int BNT = 64 * HN;
     static constexpr int LDSB = BNT + PAD;   // N-contiguous B tile pitch
     static constexpr int LDB_K = BK + 4;     // K-major B tile pitch (conflict-free fragment reads)
     static constexpr int BSTAGE_N = BK * LDSB, BSTAGE_K = BNT * LDB_K;
-    static constexpr int ASTAGE_M = BK * LDS, ASTAGE_K = BM * LDB_K;  // A: M- or K-contiguous
+    static constexpr int ASTAGE_M = BK * LDSA, ASTAGE_K = BMC * LDB_K;  // A: M- or K-contiguous
     static constexpr int BSTAGE = BSTAGE_N > BSTAGE_K ? BSTAGE_N : BSTAGE_K;
     static constexpr int SMEM = STAGES * (ASTAGE_M + BSTAGE) * 8;     // A M-contiguous
     static constexpr int SMEM_AK = STAGES * (ASTAGE_K + BSTAGE) * 8;  // A K-contiguous
@@ -74,23 +77,25 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // m0 + 2(lane&3) + {0,1} of column n0 + (lane>>2): 16-byte C accesses.
 // 8 HN warps of 32x32, STAGES-deep cp.async pipeline of BK-wide K chunks; the
 // grid enumerates 128 x 128 tiles x (2 / HN) column halves.
-template <bool BK_MAJOR, int BK, int STAGES, int HN, bool AK_MAJOR = false>
-__global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_gemm(GemmArgs g) {
+template <bool BK_MAJOR, int BK, int STAGES, int HN, bool AK_MAJOR = false, int RH = 1>
+__global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN, RH>::THREADS, 2 * RH / HN) k_gemm(GemmArgs g) {
     using namespace gemm;
-    using CF = Cfg<BK, STAGES, HN>;
+    using CF = Cfg<BK, STAGES, HN, RH>;
     constexpr int THREADS = CF::THREADS, BNT = CF::BNT, LDSB = CF::LDSB, LDB_K = CF::LDB_K;
-    constexpr int NSUB = 2 / HN;
+    constexpr int BMC = CF::BMC, LDS = CF::LDSA;
+    constexpr int NSUB = 2 / HN * RH;
     extern __shared__ __align__(16) double smem[];
     constexpr int ASTAGE = AK_MAJOR ? CF::ASTAGE_K : CF::ASTAGE_M;
     double* As = smem;                      // [STAGES][BK][LDS] or [STAGES][BM][LDB_K]
     double* Bs = smem + STAGES * ASTAGE;    // [STAGES][BK][LDSB] or [STAGES][BNT][LDB_K]
     constexpr int BSTAGE = BK_MAJOR ? CF::BSTAGE_K : CF::BSTAGE_N;
-    constexpr int CPTA = BK / (4 * HN);     // 16-byte copies per thread: A (BK x 128), B (BK x BNT)
-    constexpr int CPTB = BK / 8;
+    constexpr int CPTA = BK * BMC / 2 / THREADS;  // 16-byte copies per thread: A (BK x BMC), B (BK x BNT)
+    constexpr int CPTB = BK * BNT / 2 / THREADS;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int ti, tj;
     const long long l = blockIdx.x / NSUB;
-    const int half = NSUB > 1 ? (int)(blockIdx.x % NSUB) : 0;
+    const int sub = NSUB > 1 ? (int)(blockIdx.x % NSUB) : 0;
+    const int half = sub % (2 / HN), roff = (sub / (2 / HN)) * BMC;  // column half, row offset in the tile
     if (g.tri) {
         int t = (int)((sqrt(8.0 * (double)l + 1.0) - 1.0) * 0.5);
         while ((long long)(t + 1) * (t + 2) / 2 <= l) ++t;
@@ -113,18 +118,20 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
         const int gi = ti + g.cyc_row0;
         if (gi < gt) return;
         diag_tile = gi == gt;
-        A = g.A + (size_t)(gi - g.cyc_ab0) * BM;
+        A = g.A + (size_t)(gi - g.cyc_ab0) * BM + roff;
         B = g.B + (size_t)(gt - g.cyc_ab0) * BN + coff;  // (B row-indexed, not K-major)
-        C = g.C + ((size_t)lt * BN + coff) * g.ldc + (size_t)gi * BM;
+        C = g.C + ((size_t)lt * BN + coff) * g.ldc + (size_t)gi * BM + roff;
     } else {
-        A = AK_MAJOR ? g.A + (size_t)ti * BM * g.lda : g.A + (size_t)ti * BM;
+        A = AK_MAJOR ? g.A + ((size_t)ti * BM + roff) * g.lda : g.A + (size_t)ti * BM + roff;
         B = BK_MAJOR ? g.B + ((size_t)tj * BN + coff) * g.ldb : g.B + (size_t)tj * BN + coff;
-        C = g.C + ((size_t)tj * BN + coff) * g.ldc + (size_t)ti * BM;
+        C = g.C + ((size_t)tj * BN + coff) * g.ldc + (size_t)ti * BM + roff;
     }
-    const int wm = warp & 3, wn = warp >> 2;  // 4 x (2 HN) warps of 32 x 32
+    constexpr int WARPS_M = BMC / 32;
+    const int wm = warp % WARPS_M, wn = warp / WARPS_M;  // WARPS_M x (2 HN) warps of 32 x 32
     // lower-triangular launches: on a diagonal tile, warp tiles strictly above
     // the diagonal (never read) skip their MMAs and stores (6 of 16)
-    const bool idle = diag_tile && wm * 32 + 32 <= coff + wn * 32;
+    const bool idle = diag_tile && roff + wm * 32 + 32 <= coff + wn * 32;
+    if (RH > 1 && diag_tile && roff + BMC <= coff) return;  // the whole CTA lies above the diagonal
     const int beta = (g.beta && !(g.beta0_from >= 0 && tj >= g.beta0_from)) ? 1 : 0;
     int kbeg = 0;  // K offset of this tile
     if (g.k_from_row || (g.k_from_col && tj >= g.beta0_from)) {
@@ -145,7 +152,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN>::THREADS, 2 / HN) k_
             asrc[u] = A + (size_t)m * g.lda + k2;
             adst[u] = m * LDB_K + k2;
         } else {
-            const int k = idx >> 6, m2 = (idx & 63) * 2;
+            const int k = idx / (BMC / 2), m2 = (idx % (BMC / 2)) * 2;
             asrc[u] = A + (size_t)k * g.lda + m2;
             adst[u] = k * LDS + m2;
         }
@@ -278,24 +285,24 @@ static void launch_prio(void (*kernel)(KArgs...), unsigned grid, unsigned block,
     SFM_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
-template <int BK, int ST, int HN>
+template <int BK, int ST, int HN, int RH = 1>
 static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) {
-    using CF = gemm::Cfg<BK, ST, HN>;
-    const unsigned grid = (unsigned)(tiles * (2 / HN));
+    using CF = gemm::Cfg<BK, ST, HN, RH>;
+    const unsigned grid = (unsigned)(tiles * (2 / HN) * RH);
     if (g.a_kmajor) {
         if (!g.b_kmajor) throw CudaError("gemm: K-major A needs K-major B");
-        launch_prio(k_gemm<true, BK, ST, HN, true>, grid, CF::THREADS, CF::SMEM_AK, s, g);
-    } else if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST, HN>, grid, CF::THREADS, CF::SMEM, s, g);
-    else launch_prio(k_gemm<false, BK, ST, HN>, grid, CF::THREADS, CF::SMEM, s, g);
+        launch_prio(k_gemm<true, BK, ST, HN, true, RH>, grid, CF::THREADS, CF::SMEM_AK, s, g);
+    } else if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST, HN, false, RH>, grid, CF::THREADS, CF::SMEM, s, g);
+    else launch_prio(k_gemm<false, BK, ST, HN, false, RH>, grid, CF::THREADS, CF::SMEM, s, g);
 }
 
-template <bool KM, int BK, int ST, int HN>
+template <bool KM, int BK, int ST, int HN, int RH = 1>
 static void set_smem() {
-    SFM_CUDA(cudaFuncSetAttribute(k_gemm<KM, BK, ST, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  gemm::Cfg<BK, ST, HN>::SMEM));
+    SFM_CUDA(cudaFuncSetAttribute(k_gemm<KM, BK, ST, HN, false, RH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  gemm::Cfg<BK, ST, HN, RH>::SMEM));
     if (KM)
-        SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, BK, ST, HN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      gemm::Cfg<BK, ST, HN>::SMEM_AK));
+        SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, BK, ST, HN, true, RH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      gemm::Cfg<BK, ST, HN, RH>::SMEM_AK));
 }
 
 // Opt-in shared-memory sizes, set once before any launch (and before graph
@@ -305,19 +312,29 @@ void dense_init_attributes() {
     if (done) return;
     set_smem<false, 16, 4, 2>(); set_smem<true, 16, 4, 2>();
     set_smem<false, 16, 3, 1>(); set_smem<true, 16, 3, 1>();
+    set_smem<false, 16, 3, 1, 2>(); set_smem<true, 16, 3, 1, 2>();
     SFM_CUDA(cudaFuncSetAttribute(k_potrf_diag_fwd(), cudaFuncAttributeMaxDynamicSharedMemorySize, potrf_smem_bytes()));
     done = true;
 }
 
-// Two configurations: 128 x 64 CTAs, two per SM, BK 16 x 3 stages (every
-// launch whose output tiles are independent; config 3: 18.6 ms vs 19.1 ms for
-// 4 stages), and 128 x 128 CTAs, one per SM, BK 16 x 4 stages for in-place
-// launches (whole_tile: C aliases A, so one CTA must own a whole tile row).
+// Three configurations: 64 x 64 CTAs of 4 warps, four per SM, BK 16 x 3
+// stages (every launch whose output tiles are independent: with four CTAs
+// per SM their prologues / epilogues overlap the others' MMAs better than
+// with two 128 x 64 CTAs -- config 3 sweep 17.3 -> 16.8 ms, config 4 396 ->
+// 387 ms); 128 x 64 CTAs, two per SM, for launches whose C aliases B (the
+// in-place X[r, :] = Linv_r X[r, :]: a CTA must own all rows of its columns);
+// 128 x 128 CTAs, one per SM, BK 16 x 4 stages for whole_tile launches (C
+// aliases A, so one CTA must own a whole tile row).
 void launch_gemm(const GemmArgs& g, cudaStream_t s) {
     const long long tiles = g.tri ? (long long)g.tm * (g.tm + 1) / 2 : (long long)g.tm * g.tn;
     if (tiles <= 0) return;
+    // C aliasing an operand (in-place updates, e.g. X[r, :] = Linv_r X[r, :]):
+    // every CTA must read its whole K range of the shared rows before writing
+    // them, so no CTA may own only part of a tile's rows
+    const bool alias = g.C == g.B || g.C == g.A;
     if (g.whole_tile) launch_gemm_cfg<16, 4, 2>(g, tiles, s);
-    else launch_gemm_cfg<16, 3, 1>(g, tiles, s);
+    else if (alias) launch_gemm_cfg<16, 3, 1>(g, tiles, s);
+    else launch_gemm_cfg<16, 3, 1, 2>(g, tiles, s);
     SFM_LAUNCH_CHECK();
 }
 

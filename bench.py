@@ -40,7 +40,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-SWEEP_DRAM_BYTES_CFG3 = 11.0026e9  # profiles/r01_launches_bench_config3.txt ("dense sweep ... DRAM")
+SWEEP_DRAM_BYTES_CFG3 = 10.9625e9  # profiles/r01_launches_bench_config3.txt ("dense sweep ... DRAM")
 FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 throughput on this pool (profiles/r01_fp64_peak_probe.txt)
 FP64_PEAK_SOURCE = "measured: tools/probe/fp64_probe.cu DMMA loop 37.1 TF/s, profiles/r01_fp64_peak_probe.txt (cuBLAS DGEMM 16384^3: 36.0; MEASURED_PEAKS.json has no FP64 entry)"
 

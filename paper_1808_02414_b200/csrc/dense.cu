@@ -600,6 +600,12 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
         if (r >= c) A[(size_t)c * ld + r] = T[c * LDT + r];
     }
     POTRF_STAMP(3);
+#ifdef SFM_POTRF_DELAY
+    {  // sensitivity experiment: how much of the tile kernel's time is on the sweep's critical path
+        const long long t0 = clock64();
+        while (clock64() - t0 < SFM_POTRF_DELAY) { }
+    }
+#endif
 }
 
 const void* k_potrf_diag_ptr() { return (const void*)k_potrf_diag; }

@@ -168,6 +168,9 @@ __global__ void __launch_bounds__(128, 5) k_obs_factor(const int* oc, const int*
         const double* L = Lpt + 8 * (size_t)pj;
         const double l00 = L[0], l10 = L[1], l11 = L[2], l20 = L[3], l21 = L[4], l22 = L[5];
         const bool good = L[6] != 0.0;
+        // three reciprocals per observation instead of 3P divisions (a DDIV
+        // is a reciprocal iteration plus a slow-path check)
+        const double i00 = 1.0 / l00, i11 = 1.0 / l11, i22 = 1.0 / l22;
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const double t0 = jc[p] * W[0] + jc[P + p] * W[2];
@@ -175,9 +178,9 @@ __global__ void __launch_bounds__(128, 5) k_obs_factor(const int* oc, const int*
             double c[3];
 #pragma unroll
             for (int q = 0; q < 3; ++q) c[q] = (sc[p] * (t0 * jp[q] + t1 * jp[3 + q])) * sp[q];
-            const double w0 = c[0] / l00;
-            const double w1 = (c[1] - l10 * w0) / l11;
-            const double w2 = (c[2] - l20 * w0 - l21 * w1) / l22;
+            const double w0 = c[0] * i00;
+            const double w1 = (c[1] - l10 * w0) * i11;
+            const double w2 = (c[2] - l20 * w0 - l21 * w1) * i22;
             wo[3 * p + 0] = good ? w0 : 0.0;
             wo[3 * p + 1] = good ? w1 : 0.0;
             wo[3 * p + 2] = good ? w2 : 0.0;

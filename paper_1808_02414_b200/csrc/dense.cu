@@ -34,16 +34,17 @@ static inline int potrf_smem_bytes() { return potrf_smem_bytes_impl(); }
 // ----------------------------------------------------------------------------
 namespace gemm {
 constexpr int BM = 128, BN = 128, PAD = 8, LDS = BM + PAD;
-// CTA tile 128 x (64 HN) with 8 HN warps of 32 x 32: HN = 2 is one CTA per
-// SM (512 threads), HN = 1 two CTAs per SM whose prologue / epilogue overlap
-// the other's MMAs.
-// RH = 2: 64 x 64 CTAs of 4 warps (four per 128 x 128 tile), four CTAs per SM.
-template <int BK, int STAGES, int HN, int RH = 1>
+// CTA tile CM x CN of (CM/32) x (CN/32) warps of 32 x 32; the grid
+// enumerates 128 x 128 tiles x (128/CM)(128/CN) CTAs.  Used: 64 x 64 (four
+// CTAs per SM: independent output tiles), 128 x 64 (two per SM; C aliasing
+// B: a CTA must own all rows of its columns -- 128 x 32 measured slower),
+// 128 x 128 (whole_tile: C aliasing A).
+template <int BK, int STAGES, int CM, int CN>
 struct Cfg {
-    static constexpr int THREADS = 256 * HN / RH;
-    static constexpr int BMC = BM / RH;      // CTA rows
+    static constexpr int THREADS = (CM / 32) * (CN / 32) * 32;
+    static constexpr int BMC = CM;           // CTA rows
     static constexpr int LDSA = BMC + PAD;   // M-contiguous A tile pitch
-    static constexpr int BNT = 64 * HN;
+    static constexpr int BNT = CN;           // CTA columns
     static constexpr int LDSB = BNT + PAD;   // N-contiguous B tile pitch
     static constexpr int LDB_K = BK + 4;     // K-major B tile pitch (conflict-free fragment reads)
     static constexpr int BSTAGE_N = BK * LDSB, BSTAGE_K = BNT * LDB_K;
@@ -75,15 +76,15 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // MMA mapping: the m8n8k4 "A" operand carries B rows (n), its "B" operand
 // carries A rows (m), so each lane's two accumulators are C rows
 // m0 + 2(lane&3) + {0,1} of column n0 + (lane>>2): 16-byte C accesses.
-// 8 HN warps of 32x32, STAGES-deep cp.async pipeline of BK-wide K chunks; the
-// grid enumerates 128 x 128 tiles x (2 / HN) column halves.
-template <bool BK_MAJOR, int BK, int STAGES, int HN, bool AK_MAJOR = false, int RH = 1>
-__global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN, RH>::THREADS, 2 * RH / HN) k_gemm(GemmArgs g) {
+// Warps of 32x32, STAGES-deep cp.async pipeline of BK-wide K chunks.
+template <bool BK_MAJOR, int BK, int STAGES, int CM, int CN, bool AK_MAJOR = false>
+__global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
+                                  65536 / (gemm::Cfg<BK, STAGES, CM, CN>::THREADS * 128)) k_gemm(GemmArgs g) {
     using namespace gemm;
-    using CF = Cfg<BK, STAGES, HN, RH>;
+    using CF = Cfg<BK, STAGES, CM, CN>;
     constexpr int THREADS = CF::THREADS, BNT = CF::BNT, LDSB = CF::LDSB, LDB_K = CF::LDB_K;
     constexpr int BMC = CF::BMC, LDS = CF::LDSA;
-    constexpr int NSUB = 2 / HN * RH;
+    constexpr int NCOL = BN / CN, NSUB = (BM / CM) * NCOL;
     extern __shared__ __align__(16) double smem[];
     constexpr int ASTAGE = AK_MAJOR ? CF::ASTAGE_K : CF::ASTAGE_M;
     double* As = smem;                      // [STAGES][BK][LDS] or [STAGES][BM][LDB_K]
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN, RH>::THREADS, 2 * RH
     int ti, tj;
     const long long l = blockIdx.x / NSUB;
     const int sub = NSUB > 1 ? (int)(blockIdx.x % NSUB) : 0;
-    const int half = sub % (2 / HN), roff = (sub / (2 / HN)) * BMC;  // column half, row offset in the tile
+    const int half = sub % NCOL, roff = (sub / NCOL) * BMC;  // column block, row offset in the tile
     if (g.tri) {
         int t = (int)((sqrt(8.0 * (double)l + 1.0) - 1.0) * 0.5);
         while ((long long)(t + 1) * (t + 2) / 2 <= l) ++t;
@@ -127,11 +128,11 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, HN, RH>::THREADS, 2 * RH
         C = g.C + ((size_t)tj * BN + coff) * g.ldc + (size_t)ti * BM + roff;
     }
     constexpr int WARPS_M = BMC / 32;
-    const int wm = warp % WARPS_M, wn = warp / WARPS_M;  // WARPS_M x (2 HN) warps of 32 x 32
+    const int wm = warp % WARPS_M, wn = warp / WARPS_M;  // WARPS_M x (CN / 32) warps of 32 x 32
     // lower-triangular launches: on a diagonal tile, warp tiles strictly above
     // the diagonal (never read) skip their MMAs and stores (6 of 16)
     const bool idle = diag_tile && roff + wm * 32 + 32 <= coff + wn * 32;
-    if (RH > 1 && diag_tile && roff + BMC <= coff) return;  // the whole CTA lies above the diagonal
+    if (diag_tile && roff + BMC <= coff) return;  // the whole CTA lies above the diagonal
     const int beta = (g.beta && !(g.beta0_from >= 0 && tj >= g.beta0_from)) ? 1 : 0;
     int kbeg = 0;  // K offset of this tile
     if (g.k_from_row || (g.k_from_col && tj >= g.beta0_from)) {
@@ -285,24 +286,25 @@ static void launch_prio(void (*kernel)(KArgs...), unsigned grid, unsigned block,
     SFM_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
-template <int BK, int ST, int HN, int RH = 1>
+template <int BK, int ST, int CM, int CN>
 static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) {
-    using CF = gemm::Cfg<BK, ST, HN, RH>;
-    const unsigned grid = (unsigned)(tiles * (2 / HN) * RH);
+    using CF = gemm::Cfg<BK, ST, CM, CN>;
+    const unsigned grid = (unsigned)(tiles * (gemm::BM / CM) * (gemm::BN / CN));
     if (g.a_kmajor) {
         if (!g.b_kmajor) throw CudaError("gemm: K-major A needs K-major B");
-        launch_prio(k_gemm<true, BK, ST, HN, true, RH>, grid, CF::THREADS, CF::SMEM_AK, s, g);
-    } else if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST, HN, false, RH>, grid, CF::THREADS, CF::SMEM, s, g);
-    else launch_prio(k_gemm<false, BK, ST, HN, false, RH>, grid, CF::THREADS, CF::SMEM, s, g);
+        launch_prio(k_gemm<true, BK, ST, CM, CN, true>, grid, CF::THREADS, CF::SMEM_AK, s, g);
+    } else if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST, CM, CN, false>, grid, CF::THREADS, CF::SMEM, s, g);
+    else launch_prio(k_gemm<false, BK, ST, CM, CN, false>, grid, CF::THREADS, CF::SMEM, s, g);
 }
 
-template <bool KM, int BK, int ST, int HN, int RH = 1>
+template <bool KM, int BK, int ST, int CM, int CN>
 static void set_smem() {
-    SFM_CUDA(cudaFuncSetAttribute(k_gemm<KM, BK, ST, HN, false, RH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  gemm::Cfg<BK, ST, HN, RH>::SMEM));
+    using CF = gemm::Cfg<BK, ST, CM, CN>;
+    SFM_CUDA(cudaFuncSetAttribute(k_gemm<KM, BK, ST, CM, CN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  CF::SMEM));
     if (KM)
-        SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, BK, ST, HN, true, RH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      gemm::Cfg<BK, ST, HN, RH>::SMEM_AK));
+        SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, BK, ST, CM, CN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      CF::SMEM_AK));
 }
 
 // Opt-in shared-memory sizes, set once before any launch (and before graph
@@ -310,9 +312,9 @@ static void set_smem() {
 void dense_init_attributes() {
     static bool done = false;
     if (done) return;
-    set_smem<false, 16, 4, 2>(); set_smem<true, 16, 4, 2>();
-    set_smem<false, 16, 3, 1>(); set_smem<true, 16, 3, 1>();
-    set_smem<false, 16, 3, 1, 2>(); set_smem<true, 16, 3, 1, 2>();
+    set_smem<false, 16, 4, 128, 128>(); set_smem<true, 16, 4, 128, 128>();
+    set_smem<false, 16, 3, 128, 64>(); set_smem<true, 16, 3, 128, 64>();
+    set_smem<false, 16, 3, 64, 64>(); set_smem<true, 16, 3, 64, 64>();
     SFM_CUDA(cudaFuncSetAttribute(k_potrf_diag_fwd(), cudaFuncAttributeMaxDynamicSharedMemorySize, potrf_smem_bytes()));
     done = true;
 }
@@ -332,9 +334,9 @@ void launch_gemm(const GemmArgs& g, cudaStream_t s) {
     // every CTA must read its whole K range of the shared rows before writing
     // them, so no CTA may own only part of a tile's rows
     const bool alias = g.C == g.B || g.C == g.A;
-    if (g.whole_tile) launch_gemm_cfg<16, 4, 2>(g, tiles, s);
-    else if (alias) launch_gemm_cfg<16, 3, 1>(g, tiles, s);
-    else launch_gemm_cfg<16, 3, 1, 2>(g, tiles, s);
+    if (g.whole_tile) launch_gemm_cfg<16, 4, 128, 128>(g, tiles, s);
+    else if (alias) launch_gemm_cfg<16, 3, 128, 64>(g, tiles, s);
+    else launch_gemm_cfg<16, 3, 64, 64>(g, tiles, s);
     SFM_LAUNCH_CHECK();
 }
 

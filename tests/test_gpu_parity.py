@@ -449,3 +449,31 @@ def test_gpu_pseudoinverse_size_guard(engine):
         engine.pseudoinverse_covariance(rec, max_params=2000)
     assert e.value.kind == F.ErrorKind.size_guard and e.value.stage == "oracle"
     assert "guard is 2000" in str(e.value)
+
+
+_PANEL_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1808_02414_b200 import sfmcov as F, synthetic as S
+rec = S.generate_config(2)
+np.save(sys.argv[2], F.Engine(0).compute_covariance(rec).camera_cov)
+"""
+
+
+@pytest.mark.parametrize("panel", [4, 8])
+def test_wide_dense_panels_parity(engine, panel, tmp_path):
+    """The dense panel width adapts to the matrix size (capi.cu panel_blocks:
+    3 at config 3, 8 at config 4, 16 at config 5); wider panels change the
+    sweep's step structure (taken blocks, next-panel split, ring slots), so
+    they are checked here on config 2 (8 tile columns: 2 panels of 4, or one
+    of 8) through SFMCOV_PANEL in a fresh process (the width is read once)."""
+    import os
+    import subprocess
+    import sys
+    out = tmp_path / "cov.npy"
+    env = dict(os.environ, SFMCOV_PANEL=str(panel))
+    root = str(Path(__file__).resolve().parent.parent)
+    subprocess.run([sys.executable, "-c", _PANEL_SCRIPT, root, str(out)], env=env, check=True, timeout=600)
+    cov, _, _, _ = O.compute_covariance(S.generate_config(2))
+    assert worst_block(np.load(out), cov) <= COV_TOL

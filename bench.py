@@ -257,7 +257,6 @@ def main():
     torch.cuda.synchronize()
     times, stage_acc = [], {}
     launches = 0
-    retries = 0
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             with torch.cuda.stream(stream):
@@ -272,7 +271,6 @@ def main():
                 stage_acc[k] = stage_acc.get(k, 0.0) + v
             cts = eng.counts()
             launches += cts["kernel_launches"]
-            retries += cts["dense_retries"]
     torch.cuda.synchronize()
     barrier(world)
     ms = dist_max(float(np.mean(times)), world)
@@ -372,7 +370,6 @@ def main():
                     "timing": ("host wall clock around sfmcov_cuda_compute_covariance" + ("_sharded" if sharded else "")
                                + " (pinned host buffers), max over ranks")},
             "gpu_launches": launches,
-            "dense_serial_retries": retries,
             "roofline": {
                 "kernel": "dense FP64 Cholesky + triangular inverse (k_gemm DMMA m8n8k4 + k_potrf_diag)",
                 "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -276,18 +276,25 @@ int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv,
     return launches;
 }
 
-// Diagnostics of a successful pipeline call (covariance.hpp:49-60).
+// Diagnostics of a successful pipeline call (covariance.hpp:49-60).  The
+// near-singular pivot test of invert_schur (covariance.cpp:236-240) runs on
+// every call, whether or not the caller asked for the diagnostics.
 void fill_diagnostics(sfmcov_handle* h, Outputs& out, const double* prange, const double* eigE, const int* psd,
                       const double* s_a, const unsigned char* flags, size_t ncols, int N, int64_t dense_bytes) {
+    double pr[2], ee[8];
+    int warn = 0;
+    SFM_CUDA(cudaMemcpyAsync(pr, prange, 16, cudaMemcpyDeviceToHost, h->s));
+    SFM_CUDA(cudaMemcpyAsync(ee, eigE, 56, cudaMemcpyDeviceToHost, h->s));
+    if (out.diag) SFM_CUDA(cudaMemcpyAsync(&warn, psd, 4, cudaMemcpyDeviceToHost, h->s));
+    SFM_CUDA(cudaStreamSynchronize(h->s));
+    double mn = pr[0], mx = pr[1];
+    for (int l = 0; l < 7; ++l) { mn = std::min(mn, std::fabs(ee[l])); mx = std::max(mx, std::fabs(ee[l])); }
+    if (!(mn > 1e-12 * mx))
+        throw ApiError{SFMCOV_ERR_DEGENERATE, "factorization",
+                       "near-singular pivot (ratio " + fmt_f(mn / mx) +
+                           "); the scene is likely disconnected or its gauge degenerate"};
     if (out.diag) {
         sfmcov_diagnostics* d = out.diag;
-        double pr[2], ee[8];
-        int warn = 0;
-        d2h(h, pr, prange, 16);
-        d2h(h, ee, eigE, 56);
-        d2h(h, &warn, psd, 4);
-        double mn = pr[0], mx = pr[1];
-        for (int l = 0; l < 7; ++l) { mn = std::min(mn, std::fabs(ee[l])); mx = std::max(mx, std::fabs(ee[l])); }
         d->min_pivot = mn;
         d->max_pivot = mx;
         d->inertia_positive = N;
@@ -317,10 +324,6 @@ void fill_diagnostics(sfmcov_handle* h, Outputs& out, const double* prange, cons
                     ++cnt;
                 }
         d->n_flagged = (int32_t)cnt;
-        if (!(mn > 1e-12 * mx))
-            throw ApiError{SFMCOV_ERR_DEGENERATE, "factorization",
-                           "near-singular pivot (ratio " + fmt_f(mn / mx) +
-                               "); the scene is likely disconnected or its gauge degenerate"};
     }
 }
 
@@ -630,28 +633,6 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     }
     mark(h, 10);
     sync_status(h);
-    {
-        const Status& q = *h->st_host;
-        const bool upstream_ok = q.jac_bad == INT_MAX && q.rot_bad == INT_MAX && q.fisher_bad == INT_MAX &&
-                                 q.pt_sing_bad == INT_MAX && !q.border_bad;
-        if (q.chol_bad != INT_MAX && upstream_ok && !serial) {
-            // A non-positive pivot with the two-stream lookahead: redo the
-            // dense stage once on a single stream before reporting it (a
-            // genuinely degenerate scene fails again).  Counted in
-            // sfmcov_cuda_last_counts()[9].
-            ++h->counts[9];
-            std::fprintf(stderr, "sfmcov_b200: Cholesky pivot failure at %d with overlapped streams; retrying serially\n",
-                         q.chol_bad);
-            launch_status_init(st, s);
-            launch_fill(P, Z, ld, N, Npad, D, s_a, G, 1, s);
-            launch_pair_reduce(P, h->pairs, Wb, n, Z, ld, s);
-            run_dense(h, Z, ld, Npad, Linv, piv, st, true, false);
-            SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
-            launch_extract(P, Z, ld, N, n, s_a, 1, out.d_cam_cov, st, psd, s);
-            launch_pivot_range(piv, N, prange, s);
-            sync_status(h);
-        }
-    }
     h->counts[8] = g_kernel_launches;
     throw_numeric(h, sc, mode);
     if (h->profiling) {
@@ -841,6 +822,10 @@ int32_t guarded(sfmcov_handle* h, sfmcov_error* err, F&& body) {
         cudaStreamSynchronize(h->s);
         fill_error(err, e);
         return e.kind;
+    } catch (const SizeGuard& e) {
+        cudaStreamSynchronize(h->s);
+        fill_error(err, ApiError{SFMCOV_ERR_SIZE_GUARD, e.stage, e.what()});
+        return SFMCOV_ERR_SIZE_GUARD;
     } catch (const std::exception& e) {
         fill_error(err, ApiError{SFMCOV_ERR_DEVICE, "device", e.what()});
         return SFMCOV_ERR_DEVICE;

@@ -68,6 +68,12 @@ struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
+// A size limit of a device data structure (reported as SFMCOV_ERR_SIZE_GUARD).
+struct SizeGuard : std::runtime_error {
+    std::string stage;
+    SizeGuard(std::string st, const std::string& what) : std::runtime_error(what), stage(std::move(st)) {}
+};
+
 #define SFM_CUDA(x)                                                                              \
     do {                                                                                         \
         cudaError_t e_ = (x);                                                                    \

@@ -700,6 +700,9 @@ void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace&
     SFM_CUDA(cudaMemcpyAsync(&npairs, pd.off + m, sizeof(long long), cudaMemcpyDeviceToHost, s));
     SFM_CUDA(cudaStreamSynchronize(s));
     pd.npairs = npairs;
+    // CUB's sort / run-length encode take int item counts
+    if (npairs > (long long)INT_MAX)
+        throw SizeGuard("schur", std::to_string(npairs) + " observation pairs exceed the 2^31-1 pair-list limit");
     const size_t np = (size_t)npairs;
     unsigned int* k0 = (unsigned int*)pd.buf_k0.get(4 * np + 16);
     unsigned int* k1 = (unsigned int*)pd.buf_k1.get(4 * np + 16);

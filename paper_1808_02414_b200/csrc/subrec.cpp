@@ -407,6 +407,19 @@ std::string strip_stage(const sfmcov_error& e) {
     return full.compare(0, pre.size(), pre) == 0 ? full.substr(pre.size()) : full;
 }
 
+// rec.validate() of the full scene on the device (the M_INDEX path of the
+// CUDA library), its error passed through unchanged, as the reference's
+// approximate_covariances / error_size_sweep do before planning
+// (src/subrec.cpp:191, 262).
+void validate_full(sfmcov_handle* h, const sfmcov_scene* s) {
+    const size_t t = s->n_obs > 0 ? (size_t)s->n_obs : 1;
+    std::vector<int64_t> oc((size_t)s->n_cams + 1), op((size_t)s->n_pts + 1);
+    std::vector<int32_t> ic(t), ip(t);
+    sfmcov_error e{};
+    if (int32_t c = sfmcov_cuda_observation_index(h, s, oc.data(), ic.data(), op.data(), ip.data(), &e))
+        throw SubError{c, e.stage, strip_stage(e)};
+}
+
 }  // namespace
 
 extern "C" {
@@ -472,6 +485,8 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
     return guarded(err, [&] {
         if (k_bar < 2) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "subset size must be at least 2"};
         if (n_decompositions < 1) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "need at least one decomposition"};
+        if (!scene) throw SubError{SFMCOV_ERR_DIMENSION, "subrec", "bad scene"};
+        validate_full(h, scene);
         check_scene(scene);
         const int P = scene->cam_params;
         const Graph g = view_graph(*scene, 1);
@@ -609,6 +624,8 @@ int32_t sfmcov_cuda_error_size_sweep(sfmcov_handle* h, const sfmcov_scene* scene
                                      double* row_vals, int64_t capacity, int64_t* n_rows, sfmcov_error* err) {
     return guarded(err, [&] {
         if (subsets_per_size < 1) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "need at least one subset per size"};
+        if (!scene) throw SubError{SFMCOV_ERR_DIMENSION, "subrec", "bad scene"};
+        validate_full(h, scene);
         check_scene(scene);
         const int P = scene->cam_params;
         const int64_t n = scene->n_cams;

@@ -250,7 +250,7 @@ class Engine:
         buf = (C.c_int64 * 10)()
         self._lib.sfmcov_cuda_last_counts(self._h, buf, 10)
         keys = ["obs_pairs", "nnz_blocks", "N", "Npad", "n_obs", "n_pts", "n_cams", "P", "kernel_launches",
-                "dense_retries"]
+                "reserved"]
         return dict(zip(keys, [int(v) for v in buf]))
 
     # ---- pipeline -------------------------------------------------------------

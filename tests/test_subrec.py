@@ -119,6 +119,21 @@ def test_bad_aggregation_arguments_are_rejected(engine):  # test_subrec.cpp:119-
 
 
 @pytest.mark.gpu
+def test_invalid_full_scene_fails_validation_before_planning(engine):  # src/subrec.cpp:191, 262
+    # a duplicate (camera, point) pair: the reference's rec.validate() rejects
+    # the whole scene before any subset is planned, with its own message
+    rec = S.generate_random_scene(20, 150, 0.3, 5, 0.5)
+    rec.obs_pt[1] = rec.obs_pt[0]
+    rec.obs_cam[1] = rec.obs_cam[0]
+    for call in (lambda: R.approximate_covariances(rec, 6, 1, 0, engine=engine),
+                 lambda: R.error_size_sweep(rec, [6], 1, 0, engine=engine)):
+        with pytest.raises(F.Error) as e:
+            call()
+        assert e.value.kind == F.ErrorKind.invariant and e.value.stage == "validate"
+        assert "duplicate" in str(e.value)
+
+
+@pytest.mark.gpu
 def test_monotonicity_and_nesting(engine):  # test_subrec.cpp:141-169
     rec = S.generate_random_scene(40, 200, 0.2, 7, 0.5)
     small = R.extract_neighborhood(rec, 20, 8)

@@ -205,6 +205,20 @@ int32_t sfmcov_plan_dense(int32_t n_cams, int32_t cam_params, int32_t nranks, in
                           int32_t panel_blocks, int64_t* npad, int64_t* local_cols, int32_t* cam_owned);
 int32_t sfmcov_plan_chunks(int64_t nchunks, int32_t nranks, int32_t rank, int64_t* begin, int64_t* end);
 
+/* Verification: iterative refinement of the selected cameras' blocks
+ * against the exact inverse of the bordered Fisher system
+ * K = [[M, H], [H^T, 0]] (the FP64 D, A, couplings and H taken as exact data;
+ * reference src/covariance.cpp:33-279, src/nullspace.cpp:14-62).  Runs the
+ * product pipeline on the scene (its blocks for the selection -> base, may be
+ * NULL), then `iters` steps of y += K~^-1 (e - K y) with double-double
+ * residuals, K~^-1 being the FP64 solve through the pipeline's own factors.
+ * refined / base: n_sel x P x P; history[k] = max over cameras of the
+ * relative change of the block in step k (may be NULL).  Not on the product
+ * path: the tests use it as the truth for the configs no CPU can invert. */
+int32_t sfmcov_cuda_refine_covariance(sfmcov_handle* h, const sfmcov_scene* scene, const int32_t* cams,
+                                      int32_t n_sel, int32_t iters, double* refined, double* base, double* history,
+                                      sfmcov_error* err);
+
 /* pseudoinverse_covariance (include/sfmcov/oracle.hpp:33-37, src/oracle.cpp:34-72):
  * the dense reference covariance for verification — Fisher matrix
  * (N = P n + 3 m params, refused above max_params with SFMCOV_ERR_SIZE_GUARD),

@@ -79,6 +79,7 @@ def lib():
             "oracle_compute_covariance_full": (i32, [vp, C.c_int, vp, vp, vp, vp, vp, i64, vp]),
             "oracle_dense_fisher": (i32, [vp, vp, vp]),
             "oracle_pseudoinverse": (i32, [vp, i64, vp, vp, vp, dp, vp]),
+            "oracle_exact_camera_blocks": (i32, [vp, i64, vp, vp]),
             "oracle_cholesky_route": (i32, [vp, i64, C.c_int, vp, C.c_int, vp, vp]),
         }
         for name, (res, args) in sig.items():
@@ -267,6 +268,16 @@ def pseudoinverse(rec, max_params=2000):
                                       None if sg is None else sg.ctypes.data, sv.ctypes.data, C.byref(gap),
                                       C.byref(err)), err)
     return cov[:n], sg, sv[:N], gap.value
+
+
+def exact_camera_blocks(rec, max_params=3000):
+    """Camera blocks of the bordered Fisher inverse in long double (CPU truth
+    for small scenes; validates the GPU's double-double refinement)."""
+    n, P = rec.cams.shape[0], rec.cams.shape[1]
+    cov = np.empty((max(n, 1), P, P))
+    err = OracleError()
+    _check(lib().oracle_exact_camera_blocks(C.byref(_scene(rec)), max_params, cov.ctypes.data, C.byref(err)), err)
+    return cov[:n]
 
 
 def cholesky_route(zp, n_cams, P, s_a_cams, blas_threads=1):

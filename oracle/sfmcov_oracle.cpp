@@ -970,6 +970,91 @@ inline std::vector<double> dense_fisher(const oracle_scene& s) {
     return f;
 }
 
+// Camera blocks of the inverse of the bordered Fisher matrix
+// K = [[F, H], [H^T, 0]] (F the dense unconditioned Fisher matrix, H the
+// gauge basis, both in FP64 as the restatement forms them), solved in long
+// double: LU with partial pivoting plus two refinement steps with long-double
+// residuals.  An independent CPU truth for small scenes, to validate the
+// GPU's double-double refinement (sfmcov_cuda_refine_covariance).  The
+// Jacobi scaling of the reference (src/covariance.cpp:84-135) cancels
+// exactly, so it is not applied.
+template <int P>
+void exact_camera_blocks(const oracle_scene& s, int64_t max_params, double* cam_cov) {
+    const int64_t n = s.n_cams, m = s.n_pts, Nf = P * n + 3 * m, dim = Nf + kGauge;
+    if (Nf > max_params)
+        throw Error{kSizeGuard, "oracle", "scene has " + std::to_string(Nf) + " parameters, guard is " +
+                                              std::to_string(max_params)};
+    const std::vector<double> F = dense_fisher<P>(s);
+    const Jac<P> J = assemble_jacobian<P>(s, 1);
+    std::vector<double> H = fixed_nullspace_blocks<P>(s);
+    solve_rotation_blocks<P>(s, J, H);
+    std::vector<long double> K(size_t(dim) * dim, 0.0L);  // column-major
+    auto k = [&](int64_t r, int64_t c) -> long double& { return K[size_t(c) * dim + r]; };
+    for (int64_t c = 0; c < Nf; ++c)
+        for (int64_t r = 0; r < Nf; ++r) k(r, c) = F[size_t(c) * Nf + r];
+    for (int64_t r = 0; r < Nf; ++r)
+        for (int l = 0; l < kGauge; ++l) {
+            k(r, Nf + l) = H[size_t(r) * kGauge + l];
+            k(Nf + l, r) = H[size_t(r) * kGauge + l];
+        }
+    std::vector<long double> LU = K;
+    std::vector<int64_t> piv(dim);
+    auto lu = [&](int64_t r, int64_t c) -> long double& { return LU[size_t(c) * dim + r]; };
+    for (int64_t c = 0; c < dim; ++c) {
+        int64_t pr = c;
+        for (int64_t r = c + 1; r < dim; ++r)
+            if (std::fabs((double)lu(r, c)) > std::fabs((double)lu(pr, c))) pr = r;
+        piv[c] = pr;
+        if (pr != c)
+            for (int64_t cc = 0; cc < dim; ++cc) std::swap(lu(c, cc), lu(pr, cc));
+        const long double d = lu(c, c);
+        if (d == 0.0L) throw Error{kDegenerate, "oracle", "singular bordered Fisher matrix"};
+        for (int64_t r = c + 1; r < dim; ++r) lu(r, c) /= d;
+        for (int64_t cc = c + 1; cc < dim; ++cc) {
+            const long double f = lu(c, cc);
+            if (f == 0.0L) continue;
+            long double* col = &LU[size_t(cc) * dim];
+            const long double* lc = &LU[size_t(c) * dim];
+            for (int64_t r = c + 1; r < dim; ++r) col[r] -= lc[r] * f;
+        }
+    }
+    auto solve = [&](std::vector<long double>& x) {
+        for (int64_t c = 0; c < dim; ++c) std::swap(x[c], x[piv[c]]);
+        for (int64_t c = 0; c < dim; ++c) {
+            const long double v = x[c];
+            if (v == 0.0L) continue;
+            const long double* lc = &LU[size_t(c) * dim];
+            for (int64_t r = c + 1; r < dim; ++r) x[r] -= lc[r] * v;
+        }
+        for (int64_t c = dim - 1; c >= 0; --c) {
+            x[c] /= lu(c, c);
+            const long double v = x[c];
+            const long double* uc = &LU[size_t(c) * dim];
+            for (int64_t r = 0; r < c; ++r) x[r] -= uc[r] * v;
+        }
+    };
+    std::vector<long double> x(dim), r(dim);
+    for (int64_t i = 0; i < n; ++i)
+        for (int q = 0; q < P; ++q) {
+            const int64_t col = P * i + q;
+            std::fill(x.begin(), x.end(), 0.0L);
+            x[col] = 1.0L;
+            solve(x);
+            for (int it = 0; it < 2; ++it) {
+                std::fill(r.begin(), r.end(), 0.0L);
+                r[col] = 1.0L;
+                for (int64_t c = 0; c < dim; ++c) {
+                    const long double v = x[c];
+                    const long double* kc = &K[size_t(c) * dim];
+                    for (int64_t rr = 0; rr < dim; ++rr) r[rr] -= kc[rr] * v;
+                }
+                solve(r);
+                for (int64_t c = 0; c < dim; ++c) x[c] += r[c];
+            }
+            for (int p = 0; p < P; ++p) cam_cov[size_t(P) * P * i + P * p + q] = (double)x[P * i + p];
+        }
+}
+
 }  // namespace oracle
 
 // =============================================================================
@@ -1205,6 +1290,13 @@ int oracle_dense_fisher(const oracle_scene* s, double* f, oracle_error* e) {
             const std::vector<double> F = dense_fisher<P>(*s);
             std::memcpy(f, F.data(), 8 * F.size());
         });
+        return ok(e);
+    } catch (const Error& x) { return fail(e, x); }
+}
+
+int oracle_exact_camera_blocks(const oracle_scene* s, int64_t max_params, double* cam_cov, oracle_error* e) {
+    try {
+        ORACLE_DISPATCH(s->cam_params, exact_camera_blocks<P>(*s, max_params, cam_cov));
         return ok(e);
     } catch (const Error& x) { return fail(e, x); }
 }

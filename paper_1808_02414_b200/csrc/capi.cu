@@ -86,6 +86,7 @@ struct sfmcov_handle {
     DBuf seg, seg_tmp, prange_r, scale_mm;
     DBuf zi, fc_part, fc_y, fc_gtt, fc_eb, fc_pc;
     DBuf or_a, or_w, or_work, or_vs, or_vk, or_s, or_keep;
+    DBuf ref_c, ref_ws;  // refinement (verification) scratch
     cudaEvent_t ev_ready = nullptr, ev_rank_done[64];
     bool ev_rank_init = false;
     // worker handles for batched independent problems (sub-reconstructions),
@@ -924,7 +925,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     h->prange_r.release();
     h->scale_mm.release();
     for (DBuf* b : {&h->zi, &h->fc_part, &h->fc_y, &h->fc_gtt, &h->fc_eb, &h->fc_pc, &h->or_a, &h->or_w, &h->or_work,
-                    &h->or_vs, &h->or_vk, &h->or_s, &h->or_keep})
+                    &h->or_vs, &h->or_vk, &h->or_s, &h->or_keep, &h->ref_c, &h->ref_ws})
         b->release();
     if (h->ev_rank_init) {
         cudaEventDestroy(h->ev_ready);
@@ -1295,6 +1296,63 @@ int32_t sfmcov_cuda_spd_inverse_blocks(sfmcov_handle* h, const double* a, int64_
         d2h(h, pr, prange, 16);
         if (min_pivot) *min_pivot = pr[0];
         if (max_pivot) *max_pivot = pr[1];
+    });
+}
+
+int32_t sfmcov_cuda_refine_covariance(sfmcov_handle* h, const sfmcov_scene* scene, const int32_t* cams,
+                                      int32_t n_sel, int32_t iters, double* refined, double* base, double* history,
+                                      sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        if (n_sel < 0 || iters < 1 || iters > 16)
+            throw ApiError{SFMCOV_ERR_DIMENSION, "refine", "need n_sel >= 0 and 1 <= iters <= 16"};
+        for (int c = 0; c < n_sel; ++c)
+            if (cams[c] < 0 || cams[c] >= scene->n_cams)
+                throw ApiError{SFMCOV_ERR_DIMENSION, "refine", "camera id out of range"};
+        // the product pipeline first (its blocks are the "base" answer, and
+        // its factors are the approximate solver of the refinement)
+        const SceneDev sc = upload(h, scene);
+        const int P = sc.P, n = sc.n, m = sc.m, t = sc.t, N = P * n;
+        double* dcov = h->cov.as<double>((size_t)P * P * n);
+        Outputs out;
+        out.d_cam_cov = dcov;
+        run(h, sc, M_FULL, out);
+        if (base && n_sel) {
+            std::vector<double> all((size_t)P * P * n);
+            d2h(h, all.data(), dcov, 8 * all.size());
+            for (int c = 0; c < n_sel; ++c)
+                std::memcpy(base + (size_t)P * P * c, &all[(size_t)P * P * cams[c]], 8 * (size_t)P * P);
+        }
+        const int Npad = ((N + kNB - 1) / kNB) * kNB;
+        RefineArgs a{};
+        a.P = P; a.n = n; a.m = m; a.t = t; a.Npad = Npad; a.ld = Npad;
+        a.X = (const double*)h->Z.p;
+        a.rec = (const double*)h->rec.p; a.D = (const double*)h->D.p; a.A = (const double*)h->A.p;
+        a.Hr = (const double*)h->Hr.p; a.cams = sc.cams; a.pts = sc.pts;
+        a.off_cam = (const int*)h->off_cam.p; a.idx_cam = (const int*)h->idx_cam.p;
+        a.off_pt = (const int*)h->off_pt.p; a.idx_pt = (const int*)h->idx_pt.p;
+        a.oc = sc.oc; a.op = sc.op; a.pos_cam = (const int*)h->pos_cam.p;
+        a.s_a = (const double*)h->s_a.p; a.s_b = (const double*)h->s_b.p; a.Lpt = (const double*)h->Lpt.p;
+        a.Wb = (const double*)h->Wb.p; a.V = (const double*)h->V.p; a.G = (const double*)h->G.p;
+        a.LF = (const double*)h->LF.p;
+        a.coupling = h->ref_c.as<double>((size_t)27 * (t > 0 ? t : 1));
+        a.scratch = &h->ref_ws;
+        // cameras per batch: as many as ~60 % of the free device memory holds
+        size_t fr = 0, tot = 0;
+        SFM_CUDA(cudaMemGetInfo(&fr, &tot));
+        const size_t budget = (size_t)(0.6 * (double)(fr + h->ref_ws.cap));
+        int per = 1;
+        while (per < std::max(n_sel, 1) && per < 256 &&
+               refine_bytes(N, Npad, m, ((P * 2 * per + 31) / 32) * 32) < budget)
+            per *= 2;
+        if (refine_bytes(N, Npad, m, ((P * per + 31) / 32) * 32) > budget && per > 1) per /= 2;
+        std::vector<double> hist(iters, 0.0), hb(iters);
+        for (int c0 = 0; c0 < n_sel; c0 += per) {
+            const int c1 = std::min(n_sel, c0 + per);
+            std::vector<int> sel(cams + c0, cams + c1);
+            refine_camera_blocks(a, sel, iters, refined + (size_t)P * P * c0, hb.data(), h->s);
+            for (int k = 0; k < iters; ++k) hist[k] = std::max(hist[k], hb[k]);
+        }
+        if (history) std::copy(hist.begin(), hist.end(), history);
     });
 }
 

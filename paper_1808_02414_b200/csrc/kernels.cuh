@@ -186,6 +186,21 @@ struct FullCovArgs {
 void full_covariance(const FullCovArgs& a, cudaStream_t s);
 size_t full_cov_part_doubles(int N);
 
+// ---- refinement against the exact bordered Fisher system (refine.cu) ------
+struct RefineArgs {
+    int P, n, m, t, Npad;
+    long long ld;
+    const double* X;  // L^-1 of Z_aug (lower, column-major, the Z buffer after the sweep)
+    const double *rec, *D, *A, *Hr, *cams, *pts;
+    const int *off_cam, *idx_cam, *off_pt, *idx_pt, *oc, *op, *pos_cam;
+    const double *s_a, *s_b, *Lpt, *Wb, *V, *G, *LF;
+    double* coupling;  // t x 27 scratch
+    DBuf* scratch;
+};
+size_t refine_bytes(int N, int Npad, int m, int R);
+void refine_camera_blocks(const RefineArgs& a, const std::vector<int>& sel, int iters, double* out_blocks,
+                          double* history, cudaStream_t s);
+
 // ---- dense pseudoinverse oracle (oraclegpu.cu) -----------------------------
 void dense_pseudoinverse(const std::vector<double>& F, int N, DBuf& dA, DBuf& dW, DBuf& dwork, DBuf& dVs, DBuf& dVk,
                          DBuf& dS, DBuf& dkeep, std::vector<double>& lam, double** sigma, long long* ld_out,

@@ -380,6 +380,24 @@ class Engine:
         _raise(code, err)
         return cov[:n], sg, sv[:npar], gap.value
 
+    def refine_covariance(self, rec: Reconstruction, cams, iters: int = 3):
+        """Verification: the selected cameras' blocks refined against the exact
+        inverse of the bordered Fisher system (double-double residuals; see
+        include/sfmcov_b200.h).  Returns (refined (k,P,P), product blocks
+        (k,P,P), per-step max relative change (iters,))."""
+        P = rec.cam_params
+        sel = np.ascontiguousarray(cams, dtype=np.int32)
+        k = len(sel)
+        ref = np.empty((max(1, k), P, P))
+        base = np.empty((max(1, k), P, P))
+        hist = np.empty(iters)
+        err = N.ErrorStruct()
+        sc = rec.c_struct()
+        code = self._lib.sfmcov_cuda_refine_covariance(self._h, C.byref(sc), sel.ctypes.data, k, iters, ref.ctypes.data,
+                                                       base.ctypes.data, hist.ctypes.data, C.byref(err))
+        _raise(code, err)
+        return ref[:k], base[:k], hist
+
     def spd_inverse_blocks(self, a: np.ndarray, block: int):
         a = np.asfortranarray(a, dtype=np.float64)
         n = a.shape[0]

@@ -438,3 +438,18 @@ def test_point_and_cross_covariances_match_the_materialized_covariance():  # tes
         assert np.array_equal(cm[P * i:P * i + P, P * i:P * i + P], cov[i])
         for l in range(n):
             assert rel(cm[P * i:P * i + P, P * l:P * l + P], sigma[P * i:P * i + P, P * l:P * l + P]) < 1e-8
+
+
+@pytest.mark.parametrize("make", [lambda: S.generate_cube_scene(1, 0.5),
+                                  lambda: S.generate_random_scene(12, 150, 0.3, 5, 0.5)], ids=["cube", "random12"])
+def test_restatement_matches_the_long_double_bordered_inverse(make):
+    # the reference route (dsytrf + dsytrs2 on the bordered Schur matrix) and
+    # a long-double LU solve of the unreduced bordered Fisher matrix agree to
+    # FP64 rounding: the two formulations of src/covariance.cpp:137-279 are
+    # the same inverse, and the long-double solve is the truth the GPU's
+    # double-double refinement is checked against (test_gpu_truth.py)
+    rec = make()
+    exact = O.exact_camera_blocks(rec, 5000)
+    ref = O.compute_covariance(rec)[0]
+    worst = max(np.linalg.norm(a - b) / np.linalg.norm(b) for a, b in zip(ref, exact))
+    assert worst <= 1e-11

@@ -40,7 +40,9 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-SWEEP_DRAM_BYTES_CFG3 = 10.9625e9  # profiles/r01_launches_bench_config3.txt ("dense sweep ... DRAM")
+# DRAM bytes (read + write) of one dense sweep, summed over its launches in an
+# ncu launch list of this bench command (per config; profiles/ names the file)
+SWEEP_DRAM_BYTES = {3: (10.9625e9, "profiles/r01_launches_bench_config3.txt")}
 FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 throughput on this pool (profiles/r01_fp64_peak_probe.txt)
 FP64_PEAK_SOURCE = "measured: tools/probe/fp64_probe.cu DMMA loop 37.1 TF/s, profiles/r01_fp64_peak_probe.txt (cuBLAS DGEMM 16384^3: 36.0; MEASURED_PEAKS.json has no FP64 entry)"
 
@@ -142,13 +144,39 @@ def scene_bytes(rec):
             (rec.obs_sigma.nbytes if rec.obs_sigma is not None else 0))
 
 
+def panel_width(Npad: int) -> int:
+    """Dense panel width of the single-GPU sweep (csrc/capi.cu panel_blocks)."""
+    g = (Npad // 128) // 24
+    return 128 * min(16, max(3, g))
+
+
 def workload_name(cfg, rec):
     n, m, t, P = rec.num_cameras(), rec.num_points(), rec.num_observations(), rec.cam_params
     return (f"config{cfg}: {n} cameras (P={P}), {m} points, {t} observations; "
             f"Z {P * n}x{P * n} FP64")
 
 
+TRS_SAMPLE = 32  # the reference-configuration CPU run samples dsytrs2 at 1/32 and 2/32 of the columns
+
+
+def cpu_identity():
+    """Host CPU model and the OpenBLAS kernel set the restatement runs on."""
+    from oracle import oracle as O
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "openblas_corename": O.blas_corename(),
+            "OPENBLAS_CORETYPE": os.environ.get("OPENBLAS_CORETYPE")}
+
+
 def run_cpu(rec, threads: int, blas_threads: int):
+    """One full compute_covariance of the CPU restatement (oracle/)."""
     from oracle import oracle as O
     O.lib().oracle_blas_threads(blas_threads)
     t0 = time.perf_counter()
@@ -156,33 +184,68 @@ def run_cpu(rec, threads: int, blas_threads: int):
     return time.perf_counter() - t0, times
 
 
+def run_cpu_reference(rec, cores: int):
+    """The reference's own configuration (src/threading.cpp:14-22, 54-57):
+    Jacobian / Fisher / point loops on every core, the serial Schur loop,
+    dsytrf + dsytrs2 on ONE BLAS thread.  Bounded sample: dsytrs2 solves
+    1/TRS_SAMPLE and then 2/TRS_SAMPLE of the identity's columns and the
+    affine fit of the two times gives the full solve (oracle/sfmcov_oracle.cpp,
+    g_trs_sample); every other stage runs in full.  Returns (seconds for the
+    full workload, stage times with the dsytrs2 samples)."""
+    import ctypes as C
+    from oracle import oracle as O
+    O.lib().oracle_blas_threads(1)
+    O.lib().oracle_trs_sample(TRS_SAMPLE)
+    try:
+        t0 = time.perf_counter()
+        _, _, _, times = O.compute_covariance(rec, threads=cores)
+        wall = time.perf_counter() - t0
+    finally:
+        O.lib().oracle_trs_sample(1)
+    cols, secs = (C.c_int64 * 2)(), (C.c_double * 2)()
+    O.lib().oracle_trs_sample_info(cols, secs)
+    times = dict(times)
+    sampled = secs[0] + secs[1]
+    times["dsytrs2_samples"] = {"columns": [cols[0], cols[1]], "seconds": [secs[0], secs[1]]}
+    value = wall - sampled + times["dsytrs2"]  # the two sampled solves replaced by the fitted full solve
+    times["total"] = value
+    return value, times
+
+
+def reference_sample_text(cfg, cores):
+    return (f"config {cfg} compute_covariance of the CPU restatement (oracle/) in the reference's configuration: "
+            f"parallel loops on {cores} threads, serial Schur loop, dsytrf + dsytrs2 on 1 OpenBLAS thread "
+            f"(src/threading.cpp:54-57); every stage in full except dsytrs2, timed on 1/{TRS_SAMPLE} and "
+            f"2/{TRS_SAMPLE} of the identity's columns and extrapolated to all columns by the affine fit "
+            f"(fixed + per-column cost; within 4 % of a full solve at config 3)")
+
+
 def reference_arm(args, world, rank):
     """--impl reference: the CPU restatement of the reference path on the host
-    cores (oracle/, kind "port"; the reference itself cannot be built here)."""
+    cores in the reference's own threading (oracle/, kind "port"; the
+    reference itself cannot be built here: no Eigen, no lapacke.h)."""
     if rank != 0:
         return
     from paper_1808_02414_b200 import synthetic as S
     cores = os.cpu_count() or 1
     rec = S.generate_config(args.config)
-    threads = cores
-    blas = args.ref_blas_threads or cores
+    warm = S.generate_config(1)  # warm-up: the code paths and BLAS on the tiny config
     for _ in range(args.warmup):
-        run_cpu(rec, threads, blas)
+        run_cpu_reference(warm, cores)
     ts, stages = [], None
     for _ in range(args.steps):
-        dt, stages = run_cpu(rec, threads, blas)
+        dt, stages = run_cpu_reference(rec, cores)
         ts.append(dt)
     v = float(np.mean(ts))
     line = {
         "impl": "reference", "metric": "end-to-end camera-covariance s", "value": v, "unit": "s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * v,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, rec), "config_index": args.config, "parallelism": "cpu"},
+        "config": {"workload": workload_name(args.config, rec), "config_index": args.config, "parallelism": "cpu",
+                   "warmup_steps": "config 1 (tiny), same code path"},
         "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
-                         "sample": f"full config {args.config} compute_covariance per step; parallel loops on "
-                                   f"{threads} threads, dsytrf+dsytrs2 on {blas} OpenBLAS threads "
-                                   f"(the reference pins BLAS to 1 thread)",
-                         "stages_s": stages},
+                         "sample": reference_sample_text(args.config, cores), "stages_s": stages,
+                         "host": cpu_identity()},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -335,11 +398,16 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        dt, cst = run_cpu(rec, cores, cores)
+        dt, cst = run_cpu_reference(rec, cores)
         cpu = {"value": dt, "unit": "s", "cores": cores, "kind": "port",
-               "sample": f"one full config {args.config} compute_covariance of the CPU restatement (oracle/): "
-                         f"parallel loops on {cores} threads, dsytrf+dsytrs2 on {cores} OpenBLAS threads",
-               "stages_s": cst}
+               "sample": reference_sample_text(args.config, cores), "stages_s": cst, "host": cpu_identity()}
+        # the best this host does with the restatement: every core in BLAS too
+        # (not the reference's configuration; reported beside it, labelled)
+        dtb, cstb = run_cpu(rec, cores, cores)
+        cpu["cpu_best"] = {"value": dtb, "unit": "s", "cores": cores,
+                           "sample": f"one full config {args.config} compute_covariance, parallel loops and "
+                                     f"dsytrf + dsytrs2 on {cores} OpenBLAS threads (all columns)",
+                           "stages_s": cstb}
 
     if rank == 0:
         out = {
@@ -374,13 +442,15 @@ def main():
                 "kernel": "dense FP64 Cholesky + triangular inverse (k_gemm DMMA m8n8k4 + k_potrf_diag)",
                 "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if achieved else None,
-                "traffic": SWEEP_DRAM_BYTES_CFG3 if args.config == 3 else None,
-                "traffic_note": ("DRAM read+write summed over one sweep's launches (k_gemm, k_potrf_diag, "
-                                 "k_panel_take*), ncu launch list profiles/r01_launches_bench_config3.txt: the "
-                                 "right-looking sweep streams the trailing matrix once per 384-column panel "
-                                 "(~N^3/(3W)*16 B each for the Cholesky and the inverse); the largest trailing-"
-                                 "update launch moves 556 MB against 590 MB algorithmic (C read+write + panel), "
-                                 "i.e. no re-reads (profiles/r01_ncu_dense_and_schur.txt)"),
+                "traffic": SWEEP_DRAM_BYTES.get(args.config, (None, None))[0],
+                "traffic_source": SWEEP_DRAM_BYTES.get(args.config, (None, None))[1],
+                "algorithmic_bytes": 8.0 * N_ * N_,
+                "traffic_model": 16.0 * Npad ** 3 / (3.0 * panel_width(Npad)) + 8.0 * Npad * Npad,
+                "traffic_note": ("algorithmic_bytes: the compulsory N^2/2 doubles of Z read and of X = L^-1 written; "
+                                 "traffic: DRAM read+write summed over one sweep's launches in the ncu launch list "
+                                 "(traffic_source; null for configs without one); traffic_model: the right-looking "
+                                 "sweep streams the trailing lower triangle once per W-column panel for the "
+                                 "Cholesky and once for the inverse, 16 N^3 / (3 W) B, W = panel width"),
                 "peak_source": FP64_PEAK_SOURCE,
                 "algorithmic_flops": algo_flops, "executed_flops_padded": flops,
                 "stage_ms": dense_ms,

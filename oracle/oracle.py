@@ -80,6 +80,8 @@ def lib():
             "oracle_dense_fisher": (i32, [vp, vp, vp]),
             "oracle_pseudoinverse": (i32, [vp, i64, vp, vp, vp, dp, vp]),
             "oracle_exact_camera_blocks": (i32, [vp, i64, vp, vp]),
+            "oracle_trs_sample": (None, [C.c_int]),
+            "oracle_trs_sample_info": (None, [vp, vp]),
             "oracle_cholesky_route": (i32, [vp, i64, C.c_int, vp, C.c_int, vp, vp]),
         }
         for name, (res, args) in sig.items():

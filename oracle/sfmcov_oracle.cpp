@@ -750,6 +750,17 @@ extern "C" struct oracle_diag {
 // BLAS threads for invert_schur: 1 = the reference's pin_blas_single_thread
 // (threading.cpp:54-57); the CPU-baseline harness may raise it.
 static int g_blas_threads = 1;
+// Timing sample for the CPU baseline (bench.py only): instead of all n
+// columns of the identity, dsytrs2 solves the first c1 = ceil(n / k) columns,
+// then (from the identity again) the first c2 = 2 c1; its time is affine in
+// the number of right-hand sides (a fixed cost for the pivots and the D
+// blocks, then a per-column cost), so the two samples give the time of all n
+// columns: t(n) = t2 + (t2 - t1) (n - c2) / (c2 - c1) (measured at config 3,
+// one thread: 21.1 s predicted, 21.9 s for the full solve).  The blocks
+// extracted after a sampled solve are not valid covariances.
+static int g_trs_sample = 1;
+static double g_trs_t[2] = {0, 0};
+static int64_t g_trs_c[2] = {0, 0};
 
 inline std::vector<double> invert_schur(std::vector<double> z, int64_t n, oracle_diag* diag, double* t_trf, double* t_trs) {
     openblas_set_num_threads(g_blas_threads);
@@ -793,10 +804,27 @@ inline std::vector<double> invert_schur(std::vector<double> z, int64_t n, oracle
     std::vector<double> inv(size_t(n) * n, 0.0);
     for (int64_t i = 0; i < n; ++i) inv[size_t(i) * n + i] = 1.0;
     diag->peak_dense_bytes = std::max<int64_t>(diag->peak_dense_bytes, 2 * 8 * int64_t(n) * n);
-    t0 = std::chrono::steady_clock::now();
-    info = LAPACKE_dsytrs2(kColMajor, 'L', (int)n, (int)n, z.data(), (int)n, ipiv.data(), inv.data(), (int)n);
-    t1 = std::chrono::steady_clock::now();
-    if (t_trs) *t_trs = std::chrono::duration<double>(t1 - t0).count();
+    if (g_trs_sample > 1 && n >= 4 * g_trs_sample) {
+        const int64_t c1 = (n + g_trs_sample - 1) / g_trs_sample, c2 = 2 * c1;
+        for (int pass = 0; pass < 2; ++pass) {
+            const int64_t c = pass ? c2 : c1;
+            for (int64_t k = 0; k < c; ++k) {
+                std::fill(inv.begin() + size_t(k) * n, inv.begin() + size_t(k + 1) * n, 0.0);
+                inv[size_t(k) * n + k] = 1.0;
+            }
+            t0 = std::chrono::steady_clock::now();
+            info = LAPACKE_dsytrs2(kColMajor, 'L', (int)n, (int)c, z.data(), (int)n, ipiv.data(), inv.data(), (int)n);
+            t1 = std::chrono::steady_clock::now();
+            g_trs_t[pass] = std::chrono::duration<double>(t1 - t0).count();
+            g_trs_c[pass] = c;
+        }
+        if (t_trs) *t_trs = g_trs_t[1] + (g_trs_t[1] - g_trs_t[0]) * double(n - c2) / double(c2 - c1);
+    } else {
+        t0 = std::chrono::steady_clock::now();
+        info = LAPACKE_dsytrs2(kColMajor, 'L', (int)n, (int)n, z.data(), (int)n, ipiv.data(), inv.data(), (int)n);
+        t1 = std::chrono::steady_clock::now();
+        if (t_trs) *t_trs = std::chrono::duration<double>(t1 - t0).count();
+    }
     if (info != 0) throw Error{kDegenerate, "factorization", "solve against identity failed with status " + std::to_string(info)};
     for (int64_t c = 0; c < n; ++c)
         for (int64_t r = c + 1; r < n; ++r) {
@@ -1092,6 +1120,11 @@ extern "C" {
 
 const char* oracle_blas_corename(void) { return openblas_get_corename(); }
 void oracle_blas_threads(int n) { g_blas_threads = n > 0 ? n : 1; openblas_set_num_threads(g_blas_threads); }
+void oracle_trs_sample(int k) { g_trs_sample = k > 0 ? k : 1; }
+// the last sampled dsytrs2: columns and seconds of the two passes
+void oracle_trs_sample_info(int64_t* cols, double* secs) {
+    cols[0] = g_trs_c[0]; cols[1] = g_trs_c[1]; secs[0] = g_trs_t[0]; secs[1] = g_trs_t[1];
+}
 
 int oracle_validate(const oracle_scene* s, oracle_error* e) {
     try { validate(*s); return ok(e); } catch (const Error& x) { return fail(e, x); }

@@ -173,6 +173,55 @@ int32_t sfmcov_cuda_spd_inverse_blocks(sfmcov_handle* h, const double* a, int64_
                                        double* blocks, double* min_pivot, double* max_pivot,
                                        sfmcov_error* err);
 
+/* nullspace_residual (include/sfmcov/nullspace.hpp:36, src/nullspace.cpp:70-83):
+ * max |J H| / (max |J| max |H|) over the scene's Jacobian (formed on the
+ * GPU), H host (P*n + 3m) x b row-major, b >= 1. */
+int32_t sfmcov_cuda_nullspace_residual(sfmcov_handle* h, const sfmcov_scene* scene, const double* H, int32_t b,
+                                       double* residual, sfmcov_error* err);
+
+/* ---- stage functions on a caller-supplied block system ------------------
+ * The reference's BorderedSystem (include/sfmcov/covariance.hpp:36-47) as
+ * arrays: D n x P x P, A m x 3 x 3 (row-major blocks), couplings
+ * t x P x 3 in observation order with their obs_cam / obs_pt, border
+ * (P*n + 3m) x b row-major (0 <= b <= 32).  Host buffers; the work runs on
+ * the handle's device. */
+/* condition_columns (covariance.hpp:86, src/covariance.cpp:84-116): s_a
+ * (P*n + 3m), s_b (b), the flagged columns (ascending; n_flagged = total). */
+int32_t sfmcov_cuda_condition_columns(sfmcov_handle* h, int32_t n, int32_t m, int32_t P, int32_t b, const double* D,
+                                      const double* A, const double* border, double* s_a, double* s_b,
+                                      int64_t* flagged, int64_t flagged_capacity, int64_t* n_flagged,
+                                      sfmcov_error* err);
+/* apply_conditioning (covariance.hpp:88, src/covariance.cpp:118-135), in place. */
+int32_t sfmcov_cuda_apply_conditioning(sfmcov_handle* h, int32_t n, int32_t m, int32_t t, int32_t P, int32_t b,
+                                       double* D, double* A, double* couplings, const int32_t* obs_cam,
+                                       const int32_t* obs_pt, double* border, const double* s_a, const double* s_b,
+                                       sfmcov_error* err);
+/* schur_reduce (covariance.hpp:94-95, src/covariance.cpp:137-194): z_p
+ * (P*n + b)^2 column-major, exactly symmetric; a_inv m x 3 x 3 (may be NULL).
+ * A singular 3x3 point block fails in stage "schur" naming the point. */
+int32_t sfmcov_cuda_schur_system(sfmcov_handle* h, int32_t n, int32_t m, int32_t t, int32_t P, int32_t b,
+                                 const double* D, const double* A, const double* couplings, const int32_t* obs_cam,
+                                 const int32_t* obs_pt, const double* border, double* z_p, double* a_inv,
+                                 sfmcov_error* err);
+/* invert_schur (covariance.hpp:100, src/covariance.cpp:196-257) on any
+ * symmetric nonsingular matrix (dim x dim, column-major): the GPU Jacobi
+ * eigendecomposition (eigen.cu), z_inv = V diag(1/lambda) V^T, symmetrised;
+ * inertia from the signs of lambda, min/max_pivot = min/max |lambda| (the
+ * reference reads them off Bunch-Kaufman pivots), the same 1e-12 ratio test. */
+int32_t sfmcov_cuda_invert_symmetric(sfmcov_handle* h, const double* z, int64_t dim, double* z_inv,
+                                     double* min_pivot, double* max_pivot, int32_t* inertia_positive,
+                                     int32_t* inertia_negative, sfmcov_error* err);
+/* extract_camera_covariances (covariance.hpp:104-105, src/covariance.cpp:259-279):
+ * cam_cov[i] = S_i z_inv[ii] S_i (s_a may be NULL = unit), PSD warnings. */
+int32_t sfmcov_cuda_extract_camera_blocks(sfmcov_handle* h, const double* z_inv, int64_t dim, int32_t n, int32_t P,
+                                          const double* s_a, double* cam_cov, int32_t* warnings, sfmcov_error* err);
+/* full_covariance (covariance.hpp:115, src/covariance.cpp:352-397): the
+ * (P*n + 3m)^2 parameter covariance (column-major) as the parameter block of
+ * the inverse of the conditioned bordered Fisher matrix, refused above
+ * max_params with SFMCOV_ERR_SIZE_GUARD (stage "full-covariance"). */
+int32_t sfmcov_cuda_full_covariance(sfmcov_handle* h, const sfmcov_scene* scene, int64_t max_params, double* sigma,
+                                    sfmcov_error* err);
+
 /* ---- multi-GPU (one process per GPU) --------------------------------------
  * The same pipeline with the Schur pair work and the dense inversion split
  * over ranks: chunks of the camera-pair-sorted observation-pair list per

@@ -125,6 +125,23 @@ CUDA_SYMBOLS = {
                                       C.c_void_p]),
     "sfmcov_plan_chunks": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, c_int64_p, c_int64_p]),
     "sfmcov_cuda_device": (C.c_int32, [C.c_void_p]),
+    "sfmcov_cuda_nullspace_residual": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_void_p, C.c_int32, C.c_void_p,
+                                                   C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_condition_columns": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                                  C.c_void_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_apply_conditioning": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                   C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_schur_system": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_void_p, C.c_void_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_invert_symmetric": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                                 C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_extract_camera_blocks": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
+                                                      C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_full_covariance": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_int64, C.c_void_p,
+                                                C.POINTER(ErrorStruct)]),
     "sfmcov_cuda_refine_covariance": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_void_p, C.c_int32, C.c_int32,
                                                   C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(ErrorStruct)]),
     "sfmcov_cuda_pseudoinverse_covariance": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_int64, C.c_void_p, C.c_void_p,

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <limits>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -87,6 +88,7 @@ struct sfmcov_handle {
     DBuf zi, fc_part, fc_y, fc_gtt, fc_eb, fc_pc;
     DBuf or_a, or_w, or_work, or_vs, or_vk, or_s, or_keep;
     DBuf ref_c, ref_ws;  // refinement (verification) scratch
+    DBuf sys[14];        // stage functions on caller-supplied systems (system.cu, eigen.cu)
     cudaEvent_t ev_ready = nullptr, ev_rank_done[64];
     bool ev_rank_init = false;
     // worker handles for batched independent problems (sub-reconstructions),
@@ -447,6 +449,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     if (mode == M_JACOBIAN) {
         sync_status(h);
         throw_numeric(h, sc, mode);
+        if (!out.jc) return;  // records stay on the device (nullspace_residual)
         std::vector<double> r((size_t)kRec * t);
         std::vector<int> pos(t);
         d2h(h, r.data(), rec, 8 * r.size());
@@ -927,6 +930,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     for (DBuf* b : {&h->zi, &h->fc_part, &h->fc_y, &h->fc_gtt, &h->fc_eb, &h->fc_pc, &h->or_a, &h->or_w, &h->or_work,
                     &h->or_vs, &h->or_vk, &h->or_s, &h->or_keep, &h->ref_c, &h->ref_ws})
         b->release();
+    for (DBuf& b : h->sys) b.release();
     if (h->ev_rank_init) {
         cudaEventDestroy(h->ev_ready);
         for (auto& e : h->ev_rank_done) cudaEventDestroy(e);
@@ -1353,6 +1357,262 @@ int32_t sfmcov_cuda_refine_covariance(sfmcov_handle* h, const sfmcov_scene* scen
             for (int k = 0; k < iters; ++k) hist[k] = std::max(hist[k], hb[k]);
         }
         if (history) std::copy(hist.begin(), hist.end(), history);
+    });
+}
+
+// ---- stage functions on caller-supplied systems (system.cu, eigen.cu) ---------
+}  // extern "C"
+namespace {
+template <typename T>
+T* up(sfmcov_handle* h, DBuf& b, const T* src, size_t count) {
+    T* d = b.as<T>(count + 1);
+    if (count && src) SFM_CUDA(cudaMemcpyAsync(d, src, sizeof(T) * count, cudaMemcpyHostToDevice, h->s));
+    return d;
+}
+void check_system(int32_t n, int32_t m, int32_t t, int32_t P, int32_t b, const char* stage) {
+    if (n < 0 || m < 0 || t < 0 || (P != 8 && P != 9) || b < 0 || b > 32)
+        throw ApiError{SFMCOV_ERR_DIMENSION, stage, "bad system dimensions"};
+}
+}  // namespace
+extern "C" {
+
+int32_t sfmcov_cuda_nullspace_residual(sfmcov_handle* h, const sfmcov_scene* scene, const double* H, int32_t b,
+                                       double* residual, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        if (b < 1 || !H) throw ApiError{SFMCOV_ERR_DIMENSION, "nullspace", "nullspace shape does not match Jacobian"};
+        const SceneDev sc = upload(h, scene);
+        Outputs out;
+        run(h, sc, M_JACOBIAN, out);
+        const size_t rows = (size_t)sc.P * sc.n + 3 * (size_t)sc.m;
+        const double* dH = up(h, h->sys[0], H, rows * b);
+        auto* mx = h->sys[1].as<unsigned long long>(4);
+        launch_nullspace_residual(sc.P, sc.t, sc.n, sc.m, sc.oc, sc.op, (const int*)h->pos_cam.p,
+                                  (const double*)h->rec.p, dH, b, mx, h->s);
+        unsigned long long v[3];
+        d2h(h, v, mx, sizeof v);
+        double d[3];
+        std::memcpy(d, v, sizeof d);
+        const double denom = d[1] * d[2];
+        *residual = denom > 0.0 ? d[0] / denom : 0.0;
+    });
+}
+
+int32_t sfmcov_cuda_condition_columns(sfmcov_handle* h, int32_t n, int32_t m, int32_t P, int32_t b, const double* D,
+                                      const double* A, const double* border, double* s_a, double* s_b,
+                                      int64_t* flagged, int64_t flagged_capacity, int64_t* n_flagged,
+                                      sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        check_system(n, m, 0, P, b, "conditioning");
+        const size_t rows = (size_t)P * n + 3 * (size_t)m;
+        const double* dD = up(h, h->sys[0], D, (size_t)P * P * n);
+        const double* dA = up(h, h->sys[1], A, 9 * (size_t)m);
+        const double* dB = up(h, h->sys[2], border, rows * b);
+        double* dsa = h->sys[3].as<double>(rows + 1);
+        unsigned char* fl = h->sys[4].as<unsigned char>(rows + 1);
+        double* part = h->sys[5].as<double>(condition_part_doubles(P, n, m, b));
+        double* dsb = h->sys[6].as<double>((size_t)b + 1);
+        launch_condition_columns(P, n, m, b, dD, dA, dB, dsa, fl, part, dsb, h->s);
+        if (rows) d2h(h, s_a, dsa, 8 * rows);
+        if (b) d2h(h, s_b, dsb, 8 * (size_t)b);
+        std::vector<unsigned char> f(rows);
+        if (rows) d2h(h, f.data(), fl, rows);
+        int64_t k = 0;
+        for (size_t c = 0; c < rows; ++c)
+            if (f[c]) {
+                if (flagged && k < flagged_capacity) flagged[k] = (int64_t)c;
+                ++k;
+            }
+        if (n_flagged) *n_flagged = k;
+    });
+}
+
+int32_t sfmcov_cuda_apply_conditioning(sfmcov_handle* h, int32_t n, int32_t m, int32_t t, int32_t P, int32_t b,
+                                       double* D, double* A, double* couplings, const int32_t* obs_cam,
+                                       const int32_t* obs_pt, double* border, const double* s_a, const double* s_b,
+                                       sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        check_system(n, m, t, P, b, "conditioning");
+        const size_t rows = (size_t)P * n + 3 * (size_t)m;
+        for (int32_t k = 0; k < t; ++k)
+            if (obs_cam[k] < 0 || obs_cam[k] >= n || obs_pt[k] < 0 || obs_pt[k] >= m)
+                throw ApiError{SFMCOV_ERR_DIMENSION, "conditioning", "coupling index out of range"};
+        double* dD = up(h, h->sys[0], (const double*)D, (size_t)P * P * n);
+        double* dA = up(h, h->sys[1], (const double*)A, 9 * (size_t)m);
+        double* dC = up(h, h->sys[2], (const double*)couplings, (size_t)P * 3 * t);
+        const int* doc = up(h, h->sys[3], obs_cam, (size_t)t);
+        const int* dop = up(h, h->sys[4], obs_pt, (size_t)t);
+        double* dB = up(h, h->sys[5], (const double*)border, rows * b);
+        const double* dsa = up(h, h->sys[6], s_a, rows);
+        const double* dsb = up(h, h->sys[7], s_b, (size_t)b);
+        launch_apply_conditioning(P, n, m, t, b, dD, dA, dC, doc, dop, dB, dsa, dsb, h->s);
+        if (n) d2h(h, D, dD, 8 * (size_t)P * P * n);
+        if (m) d2h(h, A, dA, 8 * 9 * (size_t)m);
+        if (t) d2h(h, couplings, dC, 8 * (size_t)P * 3 * t);
+        if (rows * b) d2h(h, border, dB, 8 * rows * b);
+    });
+}
+
+int32_t sfmcov_cuda_schur_system(sfmcov_handle* h, int32_t n, int32_t m, int32_t t, int32_t P, int32_t b,
+                                 const double* D, const double* A, const double* couplings, const int32_t* obs_cam,
+                                 const int32_t* obs_pt, const double* border, double* z_p, double* a_inv,
+                                 sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        check_system(n, m, t, P, b, "schur");
+        if ((long long)n * n >= (1LL << 32)) throw ApiError{SFMCOV_ERR_SIZE_GUARD, "schur", "too many cameras"};
+        for (int32_t k = 0; k < t; ++k)
+            if (obs_cam[k] < 0 || obs_cam[k] >= n || obs_pt[k] < 0 || obs_pt[k] >= m)
+                throw ApiError{SFMCOV_ERR_DIMENSION, "schur", "coupling index out of range"};
+        cudaStream_t s = h->s;
+        const size_t rows = (size_t)P * n + 3 * (size_t)m;
+        const int N = P * n;
+        SysSchurArgs a{};
+        a.P = P; a.n = n; a.m = m; a.t = t; a.b = b;
+        a.D = up(h, h->sys[0], D, (size_t)P * P * n);
+        a.A = up(h, h->sys[1], A, 9 * (size_t)m);
+        a.Cp = up(h, h->sys[2], couplings, (size_t)P * 3 * t);
+        const int* doc = up(h, h->sys[3], obs_cam, (size_t)t);
+        a.op = up(h, h->sys[4], obs_pt, (size_t)t);
+        a.border = up(h, h->sys[5], border, rows * b);
+        // observation index and the camera-pair list of the system's couplings
+        SceneDev sc{};
+        sc.n = n; sc.m = m; sc.t = t; sc.P = P; sc.oc = doc; sc.op = a.op;
+        IndexDev ix;
+        ix.off_cam = h->off_cam.as<int>(n + 1);
+        ix.off_pt = h->off_pt.as<int>(m + 1);
+        ix.idx_cam = h->idx_cam.as<int>(t);
+        ix.idx_pt = h->idx_pt.as<int>(t);
+        ix.pos_cam = h->pos_cam.as<int>(t);
+        ix.key_scratch = h->key_scratch.as<int>(t);
+        launch_build_index(sc, ix, h->ws, s);
+        build_pairs(sc, ix, h->pairs, h->ws_pairs, s);
+        a.ix = &ix;
+        a.pairs = &h->pairs;
+        a.Lpt = h->sys[6].as<double>(8 * (size_t)m + 1);
+        a.V = h->sys[7].as<double>(3 * (size_t)m * b + 1);
+        a.Wb = h->sys[8].as<double>((size_t)kWStride * t + 1);
+        a.Z = h->sys[9].as<double>((size_t)N * N + 1);
+        a.Gamma = h->sys[10].as<double>((size_t)N * b + 1);
+        a.epart = h->sys[11].as<double>(schur_system_epart_doubles(m, b));
+        a.zp = h->sys[12].as<double>(((size_t)N + b) * ((size_t)N + b) + 1);
+        a.a_inv = a_inv ? h->sys[13].as<double>(9 * (size_t)m + 1) : nullptr;
+        Status* st = h->status.as<Status>(1);
+        a.st = st;
+        launch_status_init(st, s);
+        schur_system(a, s);
+        sync_status(h);
+        if (h->st_host->pt_sing_bad != INT_MAX)
+            throw ApiError{SFMCOV_ERR_DEGENERATE, "schur",
+                           "point " + std::to_string(h->st_host->pt_sing_bad) + " has a singular 3x3 block"};
+        const size_t dim = (size_t)N + b;
+        if (dim) d2h(h, z_p, a.zp, 8 * dim * dim);
+        if (a_inv && m) d2h(h, a_inv, a.a_inv, 8 * 9 * (size_t)m);
+    });
+}
+
+int32_t sfmcov_cuda_invert_symmetric(sfmcov_handle* h, const double* z, int64_t dim, double* z_inv,
+                                     double* min_pivot, double* max_pivot, int32_t* inertia_positive,
+                                     int32_t* inertia_negative, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        if (dim < 1) throw ApiError{SFMCOV_ERR_DIMENSION, "factorization", "matrix must be square"};
+        if (dim > 46340) throw ApiError{SFMCOV_ERR_SIZE_GUARD, "factorization", "dense symmetric solve too large"};
+        const int n = (int)dim;
+        const double* dz = up(h, h->sys[0], z, (size_t)n * n);
+        std::vector<double> lam;
+        double* V = nullptr;
+        int ldv = 0;
+        sym_eigen(dz, n, n, h->sys[1], h->sys[2], h->sys[3], lam, &V, &ldv, h->s);
+        double mn = std::numeric_limits<double>::infinity(), mx = 0.0;
+        int pos = 0, neg = 0;
+        for (double l : lam) {
+            mn = std::min(mn, std::fabs(l));
+            mx = std::max(mx, std::fabs(l));
+            (l >= 0.0 ? pos : neg)++;
+        }
+        if (min_pivot) *min_pivot = mn;
+        if (max_pivot) *max_pivot = mx;
+        if (inertia_positive) *inertia_positive = pos;
+        if (inertia_negative) *inertia_negative = neg;
+        if (!(mn > 1e-12 * mx))
+            throw ApiError{SFMCOV_ERR_DEGENERATE, "factorization",
+                           "near-singular pivot (ratio " + fmt_f(mn / mx) +
+                               "); the scene is likely disconnected or its gauge degenerate"};
+        std::vector<int> keep(n);
+        std::vector<double> w(n);
+        for (int i = 0; i < n; ++i) { keep[i] = i; w[i] = 1.0 / lam[i]; }
+        double* S = nullptr;
+        long long lds = 0;
+        eig_reconstruct(V, ldv, n, keep, w, h->sys[4], h->sys[5], h->sys[6], h->sys[7], &S, &lds, h->s);
+        SFM_CUDA(cudaMemcpy2DAsync(z_inv, 8 * (size_t)n, S, 8 * lds, 8 * (size_t)n, n, cudaMemcpyDeviceToHost, h->s));
+        SFM_CUDA(cudaStreamSynchronize(h->s));
+    });
+}
+
+int32_t sfmcov_cuda_extract_camera_blocks(sfmcov_handle* h, const double* z_inv, int64_t dim, int32_t n, int32_t P,
+                                          const double* s_a, double* cam_cov, int32_t* warnings, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        if ((P != 8 && P != 9) || n < 0 || (int64_t)P * n > dim)
+            throw ApiError{SFMCOV_ERR_DIMENSION, "extract", "camera blocks do not fit the matrix"};
+        const double* dz = up(h, h->sys[0], z_inv, (size_t)dim * dim);
+        const double* dsa = s_a ? up(h, h->sys[1], s_a, (size_t)P * n) : nullptr;
+        double* dc = h->sys[2].as<double>((size_t)P * P * n + 1);
+        int* warn = h->sys[3].as<int>(1);
+        launch_extract_given(P, n, dz, dim, dsa, dc, warn, h->s);
+        if (n) d2h(h, cam_cov, dc, 8 * (size_t)P * P * n);
+        int wv = 0;
+        d2h(h, &wv, warn, sizeof wv);
+        if (warnings) *warnings = wv;
+    });
+}
+
+int32_t sfmcov_cuda_full_covariance(sfmcov_handle* h, const sfmcov_scene* scene, int64_t max_params, double* sigma,
+                                    sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        const int P = scene->cam_params, n = scene->n_cams, m = scene->n_pts, t = scene->n_obs;
+        const int64_t params = (int64_t)P * n + 3 * (int64_t)m;
+        if (params > max_params)
+            throw ApiError{SFMCOV_ERR_SIZE_GUARD, "full-covariance",
+                           "scene has " + std::to_string(params) + " parameters, guard is " + std::to_string(max_params)};
+        const SceneDev sc = upload(h, scene);
+        {  // rec.validate()
+            std::vector<int64_t> oc(n + 1), op(m + 1);
+            std::vector<int32_t> ic(t > 0 ? t : 1), ip(t > 0 ? t : 1);
+            Outputs o;
+            o.off_cam = oc.data(); o.idx_cam = ic.data(); o.off_pt = op.data(); o.idx_pt = ip.data();
+            run(h, sc, M_INDEX, o);
+        }
+        Outputs o;
+        run(h, sc, M_FISHER, o);
+        cudaStream_t s = h->s;
+        double* H = h->H.as<double>((size_t)params * 7 + 1);
+        launch_write_h(sc, (const double*)h->Hr.p, H, s);
+        const long long dimK = params + 7;
+        double* K = h->sys[0].as<double>((size_t)dimK * dimK + 1);
+        launch_full_k(P, n, m, t, (const double*)h->D.p, (const double*)h->A.p, (const double*)h->rec.p, sc.oc, sc.op,
+                      (const int*)h->pos_cam.p, H, (const double*)h->s_a.p, (const double*)h->s_b.p, K, dimK, s);
+        std::vector<double> lam;
+        double* V = nullptr;
+        int ldv = 0;
+        sym_eigen(K, dimK, (int)dimK, h->sys[1], h->sys[2], h->sys[3], lam, &V, &ldv, s);
+        double mn = std::numeric_limits<double>::infinity(), mx = 0.0;
+        int neg = 0;
+        for (double l : lam) {
+            mn = std::min(mn, std::fabs(l));
+            mx = std::max(mx, std::fabs(l));
+            neg += l < 0.0;
+        }
+        if (!(mn > 1e-12 * mx) || neg != 7)
+            throw ApiError{SFMCOV_ERR_DEGENERATE, "factorization",
+                           "near-singular pivot (ratio " + fmt_f(mn / mx) +
+                               "); the scene is likely disconnected or its gauge degenerate"};
+        std::vector<int> keep((size_t)dimK);
+        std::vector<double> w((size_t)dimK);
+        for (long long i = 0; i < dimK; ++i) { keep[i] = (int)i; w[i] = 1.0 / lam[i]; }
+        double* S = nullptr;
+        long long lds = 0;
+        eig_reconstruct(V, ldv, (int)dimK, keep, w, h->sys[4], h->sys[5], h->sys[6], h->sys[7], &S, &lds, s);
+        double* out = h->sys[8].as<double>((size_t)params * params + 1);
+        launch_full_unscale(params, S, lds, (const double*)h->s_a.p, out, s);
+        if (params) d2h(h, sigma, out, 8 * (size_t)params * params);
     });
 }
 

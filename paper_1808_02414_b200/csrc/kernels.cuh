@@ -201,6 +201,44 @@ size_t refine_bytes(int N, int Npad, int m, int R);
 void refine_camera_blocks(const RefineArgs& a, const std::vector<int>& sel, int iters, double* out_blocks,
                           double* history, cudaStream_t s);
 
+// ---- stage functions on caller-supplied block systems (system.cu) ---------
+void launch_nullspace_residual(int P, int t, int n, int m, const int* oc, const int* op, const int* pos_cam,
+                               const double* rec, const double* H, int b, unsigned long long* mx, cudaStream_t s);
+void launch_condition_columns(int P, int n, int m, int b, const double* D, const double* A, const double* border,
+                              double* s_a, unsigned char* flags, double* part, double* s_b, cudaStream_t s);
+size_t condition_part_doubles(int P, int n, int m, int b);
+void launch_apply_conditioning(int P, int n, int m, int t, int b, double* D, double* A, double* Cp, const int* oc,
+                               const int* op, double* border, const double* s_a, const double* s_b, cudaStream_t s);
+struct SysSchurArgs {
+    int P, n, m, t, b;
+    const double *D, *A, *Cp, *border;  // device, the (conditioned or not) system
+    const int* op;
+    const IndexDev* ix;
+    const PairDev* pairs;
+    double *Lpt, *V, *Wb, *Z, *Gamma, *epart, *zp, *a_inv;  // scratch / outputs (a_inv may be null)
+    Status* st;
+};
+void schur_system(const SysSchurArgs& a, cudaStream_t s);
+size_t schur_system_epart_doubles(int m, int b);
+void launch_extract_given(int P, int n, const double* Zi, long long ld, const double* s_a, double* cov, int* warn,
+                          cudaStream_t s);
+void launch_full_k(int P, int n, int m, int t, const double* D, const double* A, const double* rec, const int* oc,
+                   const int* op, const int* pos_cam, const double* H, const double* s_a, const double* s_b, double* K,
+                   long long ld, cudaStream_t s);
+void launch_full_unscale(long long params, const double* S, long long lds, const double* s_a, double* sigma,
+                         cudaStream_t s);
+
+// ---- symmetric eigensolver (eigen.cu) ---------------------------------------
+// src (n x n, col-major, ld lds, device) -> eigenvalues (host, unsorted) and
+// eigenvectors V (device, n2 x n2 col-major, n2 = n rounded up to even, in
+// dV); returns the number of Jacobi sweeps.
+int sym_eigen(const double* src, long long lds, int n, DBuf& dA, DBuf& dV, DBuf& dwork, std::vector<double>& lam,
+              double** V_out, int* ld_out, cudaStream_t s);
+// S = V[:, keep] diag(w) V[:, keep]^T (n x n, device, ld = n rounded up to
+// 128, symmetrised) through the DMMA GEMM.
+void eig_reconstruct(const double* V, int ldv, int n, const std::vector<int>& keep, const std::vector<double>& wts,
+                     DBuf& dL, DBuf& dR, DBuf& dS, DBuf& dkeep, double** S_out, long long* ld_out, cudaStream_t s);
+
 // ---- dense pseudoinverse oracle (oraclegpu.cu) -----------------------------
 void dense_pseudoinverse(const std::vector<double>& F, int N, DBuf& dA, DBuf& dW, DBuf& dwork, DBuf& dVs, DBuf& dVk,
                          DBuf& dS, DBuf& dkeep, std::vector<double>& lam, double** sigma, long long* ld_out,

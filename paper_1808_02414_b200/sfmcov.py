@@ -380,6 +380,44 @@ class Engine:
         _raise(code, err)
         return cov[:n], sg, sv[:npar], gap.value
 
+    def nullspace_residual(self, rec: Reconstruction, H: np.ndarray) -> float:
+        """max |J H| / (max |J| max |H|) (nullspace.hpp:36) with J formed on the GPU."""
+        H = np.ascontiguousarray(H, dtype=np.float64)
+        out = C.c_double()
+        err = N.ErrorStruct()
+        sc = rec.c_struct()
+        _raise(self._lib.sfmcov_cuda_nullspace_residual(self._h, C.byref(sc), H.ctypes.data, H.shape[1], C.byref(out),
+                                                        C.byref(err)), err)
+        return out.value
+
+    def invert_schur(self, z: np.ndarray):
+        """invert_schur (covariance.hpp:100) of any symmetric nonsingular matrix:
+        returns (z_inv, (min_pivot, max_pivot), (inertia_positive, inertia_negative))."""
+        z = np.asfortranarray(z, dtype=np.float64)
+        if z.ndim != 2 or z.shape[0] != z.shape[1] or z.shape[0] < 1:
+            raise Error(ErrorKind.dimension, "factorization", "matrix must be square")
+        n = z.shape[0]
+        out = np.empty((n, n), order="F")
+        mn, mx = C.c_double(), C.c_double()
+        ip, ineg = C.c_int32(), C.c_int32()
+        err = N.ErrorStruct()
+        _raise(self._lib.sfmcov_cuda_invert_symmetric(self._h, z.ctypes.data, n, out.ctypes.data, C.byref(mn),
+                                                      C.byref(mx), C.byref(ip), C.byref(ineg), C.byref(err)), err)
+        return out, (mn.value, mx.value), (ip.value, ineg.value)
+
+    def full_covariance(self, rec: Reconstruction, max_params: int = 2000) -> np.ndarray:
+        """full_covariance (covariance.hpp:115): the (Pn+3m)^2 parameter covariance."""
+        npar = rec.num_parameters()
+        if npar > max_params:
+            raise Error(ErrorKind.size_guard, "full-covariance",
+                        f"scene has {npar} parameters, guard is {max_params}")
+        sig = np.empty((npar, npar), order="F")
+        err = N.ErrorStruct()
+        sc = rec.c_struct()
+        _raise(self._lib.sfmcov_cuda_full_covariance(self._h, C.byref(sc), max_params, sig.ctypes.data, C.byref(err)),
+               err)
+        return sig
+
     def refine_covariance(self, rec: Reconstruction, cams, iters: int = 3):
         """Verification: the selected cameras' blocks refined against the exact
         inverse of the bordered Fisher system (double-double residuals; see

@@ -1,4 +1,6 @@
-"""Device-path stress (torch-resident scene), optional L2 flush, like bench.py."""
+"""Device-path stress (torch-resident scene), optional L2 flush, like bench.py:
+every call must succeed and be bitwise identical to the first.
+usage: python tools/stress_dev.py FLUSH(0/1) REPS PROFILING(0/1)"""
 import sys, ctypes as C
 sys.path.insert(0, '.')
 import numpy as np, torch
@@ -28,9 +30,7 @@ for i in range(reps):
     code = lib.sfmcov_cuda_compute_covariance_device(eng.handle, C.byref(sc), C.byref(opts), d_cov.data_ptr(), C.byref(diag), C.byref(err))
     if code:
         bad += 1; print(i, "ERROR", err.message.decode(), flush=True); continue
-    if eng.counts()["dense_retries"]:
-        print(i, "RETRY", flush=True); retries = globals().get("retries", 0) + 1; globals()["retries"] = retries
     c = d_cov.cpu().numpy()
     if not np.array_equal(c, ref):
         bad += 1; print(i, "DIFF", np.abs(c - ref).max(), flush=True)
-print("flush", flush_on, "prof", prof, "bad", bad, "retries", globals().get("retries", 0), "of", reps, flush=True)
+print("flush", flush_on, "prof", prof, "bad", bad, "of", reps, flush=True)

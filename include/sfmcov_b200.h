@@ -359,6 +359,30 @@ int32_t sfmcov_scene_save(const sfmcov_scene* scene, const char* path, sfmcov_er
 sfmcov_synth_scene* sfmcov_scene_load_binary(const char* path, sfmcov_error* err);
 int32_t sfmcov_scene_save_binary(const sfmcov_scene* scene, const char* path, sfmcov_error* err);
 
+/* ---- covariance IO (include/sfmcov/covariance_io.hpp, src/covariance_io.cpp) --
+ * Host only (libsfmcov_synth.so).  Blocks are P x P row-major, P in {8, 9}. */
+/* pack_upper_triangle / unpack_upper_triangle (covariance_io.hpp:12-13): the
+ * row-major upper triangle (0,0),(0,1),...,(P-1,P-1), P(P+1)/2 entries. */
+void sfmcov_covio_pack_upper_triangle(const double* block, int32_t P, double* tri);
+void sfmcov_covio_unpack_upper_triangle(const double* tri, int32_t P, double* block);
+/* save_covariance_json (covariance_io.cpp:52-66): {"cameras":[{"cov":[...],
+ * "id":i}...],"diagnostics":{...}} exactly as the reference's nlohmann dump
+ * (sorted keys, compact, shortest round-trip doubles).  diag may be NULL
+ * (zeros); its flagged buffer holds the flagged columns. */
+int32_t sfmcov_covio_save_json(const char* path, int64_t n_cams, int32_t P, const double* cam_cov,
+                               const sfmcov_diagnostics* diag, sfmcov_error* err);
+/* load_covariance_json (covariance_io.cpp:68-101): fills up to `capacity`
+ * blocks, *n_cams = the file's camera count (call again with a larger buffer
+ * when it exceeds capacity); diag (may be NULL) gets the diagnostics and up to
+ * flagged_capacity flagged columns (n_flagged = total).  Errors: io
+ * (unreadable), parse ("invalid JSON" / "bad covariance file"). */
+int32_t sfmcov_covio_load_json(const char* path, int32_t P, int64_t capacity, double* cam_cov, int64_t* n_cams,
+                               sfmcov_diagnostics* diag, sfmcov_error* err);
+/* save_covariance_csv (covariance_io.cpp:103-122): header id,cov_0_0,...,
+ * one row per camera, %.17g. */
+int32_t sfmcov_covio_save_csv(const char* path, int64_t n_cams, int32_t P, const double* cam_cov,
+                              sfmcov_error* err);
+
 #ifdef __cplusplus
 }
 #endif

@@ -592,4 +592,57 @@ inline MatX full_covariance(const Reconstruction& rec, Index max_params = 2000) 
     return sigma;
 }
 
+// ---- covariance_io.hpp:10-24 (host library libsfmcov_synth.so) ---------------
+inline std::array<double, 36> pack_upper_triangle(const Mat8& m) {
+    std::array<double, 36> tri{};
+    sfmcov_covio_pack_upper_triangle(m.data(), 8, tri.data());
+    return tri;
+}
+inline Mat8 unpack_upper_triangle(const std::array<double, 36>& tri) {
+    Mat8 m{};
+    sfmcov_covio_unpack_upper_triangle(tri.data(), 8, m.data());
+    return m;
+}
+inline void save_covariance_json(const CovarianceResult& result, const std::string& path) {
+    const CovarianceDiagnostics& g = result.diagnostics;
+    std::vector<int64_t> fl(g.flagged_columns.begin(), g.flagged_columns.end());
+    sfmcov_diagnostics d{g.scale_min, g.scale_max, g.min_pivot, g.max_pivot, g.inertia_positive, g.inertia_negative,
+                         g.negative_eigenvalue_warnings, (int32_t)fl.size(), (int64_t)g.peak_dense_bytes,
+                         g.largest_dense_dim, fl.data(), (int64_t)fl.size()};
+    sfmcov_error e{};
+    b200::check(sfmcov_covio_save_json(path.c_str(), (int64_t)result.camera_cov.size(), 8,
+                                       result.camera_cov.empty() ? nullptr : result.camera_cov[0].data(), &d, &e),
+                e);
+}
+inline CovarianceResult load_covariance_json(const std::string& path) {
+    sfmcov_error e{};
+    int64_t n = 0;
+    sfmcov_diagnostics d{};
+    b200::check(sfmcov_covio_load_json(path.c_str(), 8, 0, nullptr, &n, &d, &e), e);
+    CovarianceResult r;
+    r.camera_cov.resize(n);
+    std::vector<int64_t> fl((size_t)d.n_flagged + 1);
+    d.flagged = fl.data();
+    d.flagged_capacity = (int64_t)fl.size();
+    b200::check(sfmcov_covio_load_json(path.c_str(), 8, n, n ? r.camera_cov[0].data() : nullptr, &n, &d, &e), e);
+    CovarianceDiagnostics& g = r.diagnostics;
+    g.scale_min = d.scale_min;
+    g.scale_max = d.scale_max;
+    g.flagged_columns.assign(fl.begin(), fl.begin() + d.n_flagged);
+    g.min_pivot = d.min_pivot;
+    g.max_pivot = d.max_pivot;
+    g.inertia_positive = d.inertia_positive;
+    g.inertia_negative = d.inertia_negative;
+    g.negative_eigenvalue_warnings = d.negative_eigenvalue_warnings;
+    g.peak_dense_bytes = (std::size_t)d.peak_dense_bytes;
+    g.largest_dense_dim = d.largest_dense_dim;
+    return r;
+}
+inline void save_covariance_csv(const CovarianceResult& result, const std::string& path) {
+    sfmcov_error e{};
+    b200::check(sfmcov_covio_save_csv(path.c_str(), (int64_t)result.camera_cov.size(), 8,
+                                      result.camera_cov.empty() ? nullptr : result.camera_cov[0].data(), &e),
+                e);
+}
+
 }  // namespace sfmcov

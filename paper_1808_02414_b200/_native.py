@@ -177,6 +177,13 @@ SYNTH_SYMBOLS = {
     "sfmcov_scene_save": (C.c_int32, [C.POINTER(Scene), C.c_char_p, C.POINTER(ErrorStruct)]),
     "sfmcov_scene_load_binary": (C.c_void_p, [C.c_char_p, C.POINTER(ErrorStruct)]),
     "sfmcov_scene_save_binary": (C.c_int32, [C.POINTER(Scene), C.c_char_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_covio_pack_upper_triangle": (None, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "sfmcov_covio_unpack_upper_triangle": (None, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "sfmcov_covio_save_json": (C.c_int32, [C.c_char_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
+                                           C.POINTER(ErrorStruct)]),
+    "sfmcov_covio_load_json": (C.c_int32, [C.c_char_p, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.POINTER(ErrorStruct)]),
+    "sfmcov_covio_save_csv": (C.c_int32, [C.c_char_p, C.c_int64, C.c_int32, C.c_void_p, C.POINTER(ErrorStruct)]),
 }
 
 _cuda_lib = None

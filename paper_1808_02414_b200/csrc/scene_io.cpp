@@ -449,6 +449,168 @@ int32_t guard_save(sfmcov_error* err, F&& f) {
     }
 }
 
+// ---- covariance IO (reference src/covariance_io.cpp:17-122) ------------------
+// The reference writes nlohmann::json's dump(): compact, object keys in sorted
+// order, shortest round-trip doubles ("x.0" for integral ones), integers plain.
+void put_int(std::string& o, long long v) { o += std::to_string(v); }
+
+void pack_tri(const double* m, int P, double* tri) {
+    int k = 0;
+    for (int r = 0; r < P; ++r)
+        for (int c = r; c < P; ++c) tri[k++] = m[P * r + c];
+}
+void unpack_tri(const double* tri, int P, double* m) {
+    int k = 0;
+    for (int r = 0; r < P; ++r)
+        for (int c = r; c < P; ++c) {
+            m[P * r + c] = tri[k];
+            m[P * c + r] = tri[k];
+            ++k;
+        }
+}
+
+void write_file(const std::string& path, const std::string& text) {
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw IoError{SFMCOV_ERR_IO, "save", "cannot open '" + path + "' for writing"};
+    const bool ok = std::fwrite(text.data(), 1, text.size(), f) == text.size();
+    if (std::fclose(f) != 0 || !ok) throw IoError{SFMCOV_ERR_IO, "save", "failed writing '" + path + "'"};
+}
+
+void save_cov_json(const std::string& path, int64_t n, int P, const double* cov, const sfmcov_diagnostics& d) {
+    std::string o;
+    o.reserve((size_t)n * (P * (P + 1) / 2) * 24 + 512);
+    o += "{\"cameras\":[";
+    std::vector<double> tri(P * (P + 1) / 2);
+    for (int64_t i = 0; i < n; ++i) {
+        if (i) o += ',';
+        o += "{\"cov\":[";
+        pack_tri(cov + (size_t)P * P * i, P, tri.data());
+        for (size_t k = 0; k < tri.size(); ++k) {
+            if (k) o += ',';
+            put_num(o, tri[k]);
+        }
+        o += "],\"id\":";
+        put_int(o, i);
+        o += '}';
+    }
+    o += "],\"diagnostics\":{\"flagged_columns\":[";
+    const int64_t nf = d.flagged ? std::min<int64_t>(d.n_flagged, d.flagged_capacity) : 0;
+    for (int64_t k = 0; k < nf; ++k) {
+        if (k) o += ',';
+        put_int(o, d.flagged[k]);
+    }
+    o += "],\"inertia_negative\":";
+    put_int(o, d.inertia_negative);
+    o += ",\"inertia_positive\":";
+    put_int(o, d.inertia_positive);
+    o += ",\"largest_dense_dim\":";
+    put_int(o, d.largest_dense_dim);
+    o += ",\"max_pivot\":";
+    put_num(o, d.max_pivot);
+    o += ",\"min_pivot\":";
+    put_num(o, d.min_pivot);
+    o += ",\"negative_eigenvalue_warnings\":";
+    put_int(o, d.negative_eigenvalue_warnings);
+    o += ",\"peak_dense_bytes\":";
+    put_int(o, d.peak_dense_bytes);
+    o += ",\"scale_max\":";
+    put_num(o, d.scale_max);
+    o += ",\"scale_min\":";
+    put_num(o, d.scale_min);
+    o += "}}\n";
+    write_file(path, o);
+}
+
+std::string read_file(const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw IoError{SFMCOV_ERR_IO, "load", "cannot open '" + path + "'"};
+    std::string text;
+    char buf[1 << 16];
+    size_t k;
+    while ((k = std::fread(buf, 1, sizeof buf, f)) > 0) text.append(buf, k);
+    std::fclose(f);
+    return text;
+}
+
+int64_t load_cov_doc(const Value& doc, int P, int64_t capacity, double* cov, sfmcov_diagnostics* d);
+
+// Parses the whole file; fills up to `capacity` blocks.
+int64_t load_cov_json(const std::string& path, int P, int64_t capacity, double* cov, sfmcov_diagnostics* d) {
+    const std::string text = read_file(path);
+    Reader r{text.data(), text.data() + text.size(), text.data()};
+    Value doc;
+    try {
+        doc = r.value();
+        r.ws();
+        if (r.p != r.end) r.fail("trailing characters");
+    } catch (const IoError& x) {
+        throw IoError{SFMCOV_ERR_PARSE, "load", "invalid JSON: " + x.message};
+    }
+    try {
+        return load_cov_doc(doc, P, capacity, cov, d);
+    } catch (const IoError& x) {
+        if (x.kind != SFMCOV_ERR_PARSE) throw;
+        throw IoError{SFMCOV_ERR_PARSE, "load", "bad covariance file: " + x.message};
+    }
+}
+
+int64_t load_cov_doc(const Value& doc, int P, int64_t capacity, double* cov, sfmcov_diagnostics* d) {
+    auto bad = [](const std::string& what) { parse_fail(what); };
+    if (doc.kind != Value::Object) bad("document is not an object");
+    const Value* cams = doc.find("cameras");
+    if (!cams || cams->kind != Value::Array) bad("missing array 'cameras'");
+    const int ntri = P * (P + 1) / 2;
+    const int64_t n = (int64_t)cams->items.size();
+    std::vector<double> tri(ntri);
+    for (int64_t i = 0; i < n; ++i) {
+        const Value& c = cams->items[i];
+        if (c.kind != Value::Object) bad("camera entry is not an object");
+        vector_field(c, "cov", "camera " + std::to_string(i), ntri, tri.data());
+        if (i < capacity && cov) unpack_tri(tri.data(), P, cov + (size_t)P * P * i);
+    }
+    const Value* dg = doc.find("diagnostics");
+    if (!dg || dg->kind != Value::Object) bad("missing object 'diagnostics'");
+    if (d) {
+        const std::string w = "diagnostics";
+        d->scale_min = number_field(*dg, "scale_min", w);
+        d->scale_max = number_field(*dg, "scale_max", w);
+        d->min_pivot = number_field(*dg, "min_pivot", w);
+        d->max_pivot = number_field(*dg, "max_pivot", w);
+        d->inertia_positive = (int32_t)number_field(*dg, "inertia_positive", w);
+        d->inertia_negative = (int32_t)number_field(*dg, "inertia_negative", w);
+        d->negative_eigenvalue_warnings = (int32_t)number_field(*dg, "negative_eigenvalue_warnings", w);
+        d->peak_dense_bytes = (int64_t)number_field(*dg, "peak_dense_bytes", w);
+        d->largest_dense_dim = (int64_t)number_field(*dg, "largest_dense_dim", w);
+        const Value* fl = dg->find("flagged_columns");
+        if (!fl || fl->kind != Value::Array) bad("diagnostics: missing array 'flagged_columns'");
+        d->n_flagged = (int32_t)fl->items.size();
+        for (size_t k = 0; k < fl->items.size(); ++k) {
+            if (fl->items[k].kind != Value::Number) bad("diagnostics: non-number flagged column");
+            if (d->flagged && (int64_t)k < d->flagged_capacity) d->flagged[k] = (int64_t)fl->items[k].num;
+        }
+    }
+    return n;
+}
+
+void save_cov_csv(const std::string& path, int64_t n, int P, const double* cov) {
+    std::string o = "id";
+    for (int r = 0; r < P; ++r)
+        for (int c = r; c < P; ++c) o += ",cov_" + std::to_string(r) + "_" + std::to_string(c);
+    o += '\n';
+    std::vector<double> tri(P * (P + 1) / 2);
+    char cell[40];
+    for (int64_t i = 0; i < n; ++i) {
+        o += std::to_string(i);
+        pack_tri(cov + (size_t)P * P * i, P, tri.data());
+        for (double v : tri) {
+            std::snprintf(cell, sizeof cell, ",%.17g", v);
+            o += cell;
+        }
+        o += '\n';
+    }
+    write_file(path, o);
+}
+
 }  // namespace
 
 extern "C" {
@@ -467,6 +629,45 @@ sfmcov_synth_scene* sfmcov_scene_load_binary(const char* path, sfmcov_error* err
 
 int32_t sfmcov_scene_save_binary(const sfmcov_scene* scene, const char* path, sfmcov_error* err) {
     return guard_save(err, [&] { save_binary(*scene, path); });
+}
+
+void sfmcov_covio_pack_upper_triangle(const double* block, int32_t P, double* tri) { pack_tri(block, P, tri); }
+
+void sfmcov_covio_unpack_upper_triangle(const double* tri, int32_t P, double* block) { unpack_tri(tri, P, block); }
+
+int32_t sfmcov_covio_save_json(const char* path, int64_t n_cams, int32_t P, const double* cam_cov,
+                                    const sfmcov_diagnostics* diag, sfmcov_error* err) {
+    return guard_save(err, [&] {
+        if (P != 8 && P != 9) throw IoError{SFMCOV_ERR_DIMENSION, "save", "camera width must be 8 or 9"};
+        sfmcov_diagnostics d{};
+        if (diag) d = *diag;
+        save_cov_json(path, n_cams, P, cam_cov, d);
+    });
+}
+
+int32_t sfmcov_covio_load_json(const char* path, int32_t P, int64_t capacity, double* cam_cov, int64_t* n_cams,
+                                    sfmcov_diagnostics* diag, sfmcov_error* err) {
+    try {
+        if (P != 8 && P != 9) throw IoError{SFMCOV_ERR_DIMENSION, "load", "camera width must be 8 or 9"};
+        const int64_t n = load_cov_json(path, P, capacity, cam_cov, diag);
+        if (n_cams) *n_cams = n;
+        if (err) { err->kind = 0; err->stage[0] = 0; err->message[0] = 0; }
+        return 0;
+    } catch (const IoError& x) {
+        set(err, x);
+        return x.kind;
+    } catch (const std::exception& x) {
+        set(err, IoError{SFMCOV_ERR_IO, "load", x.what()});
+        return SFMCOV_ERR_IO;
+    }
+}
+
+int32_t sfmcov_covio_save_csv(const char* path, int64_t n_cams, int32_t P, const double* cam_cov,
+                                   sfmcov_error* err) {
+    return guard_save(err, [&] {
+        if (P != 8 && P != 9) throw IoError{SFMCOV_ERR_DIMENSION, "save", "camera width must be 8 or 9"};
+        save_cov_csv(path, n_cams, P, cam_cov);
+    });
 }
 
 }  // extern "C"

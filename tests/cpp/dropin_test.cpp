@@ -447,6 +447,16 @@ int main() {
     expect_error([&] { compute_covariance(bad); }, ErrorKind::invariant, "validate",
                  "validate: camera 1 has non-positive focal length", __LINE__);
     CHECK(static_cast<int>(ErrorKind::io) == 0 && static_cast<int>(ErrorKind::size_guard) == 5);
+    {  // covariance IO round trip (covariance_io.hpp)
+        save_covariance_json(result, "/tmp/sfmcov_dropin_cov.json");
+        const CovarianceResult back = load_covariance_json("/tmp/sfmcov_dropin_cov.json");
+        CHECK(back.camera_cov == result.camera_cov);
+        CHECK(back.diagnostics.inertia_negative == 7 && back.diagnostics.min_pivot == d.min_pivot);
+        CHECK(unpack_upper_triangle(pack_upper_triangle(result.camera_cov[0])) == result.camera_cov[0]);
+        save_covariance_csv(result, "/tmp/sfmcov_dropin_cov.csv");
+        std::remove("/tmp/sfmcov_dropin_cov.json");
+        std::remove("/tmp/sfmcov_dropin_cov.csv");
+    }
     test_fisher();
     test_nullspace();
     test_schur();

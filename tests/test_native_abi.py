@@ -17,7 +17,7 @@ HEADER = (ROOT / "include" / "sfmcov_b200.h").read_text()
 
 def declared_functions():
     body = re.sub(r"/\*.*?\*/", "", HEADER, flags=re.S)
-    return sorted(set(re.findall(r"\b(sfmcov_(?:cuda|synth|nccl|plan|view|extract|scene)_\w+)\s*\(", body)))
+    return sorted(set(re.findall(r"\b(sfmcov_(?:cuda|synth|nccl|plan|view|extract|scene|covio)_\w+)\s*\(", body)))
 
 
 def test_header_declares_the_entry_points():
@@ -31,7 +31,7 @@ def test_cuda_library_exports_every_declared_symbol():
     lib = C.CDLL(str(N.LIB_PATH))
     synth = C.CDLL(str(N.SYNTH_PATH))
     missing = [n for n in declared_functions()
-               if not hasattr(synth if n.startswith(("sfmcov_synth", "sfmcov_scene")) else lib, n)]
+               if not hasattr(synth if n.startswith(("sfmcov_synth", "sfmcov_scene", "sfmcov_covio")) else lib, n)]
     assert missing == []
     # and the Python binding table covers them all
     assert set(declared_functions()) == set(N.CUDA_SYMBOLS) | set(N.SYNTH_SYMBOLS)

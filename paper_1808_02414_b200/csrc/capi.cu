@@ -84,7 +84,8 @@ struct sfmcov_handle {
     int dist_mode = 0, dist_R = 1, dist_rank = 0, emu_R = 1;
     void* nccl = nullptr;
     std::vector<sfm::RankDense> ranks;
-    DBuf seg, seg_tmp, prange_r, scale_mm;
+    DBuf seg, seg_tmp, seg_send, seg_recv, prange_r, scale_mm;
+    sfm::SegGroups seg_groups;
     DBuf zi, fc_part, fc_y, fc_gtt, fc_eb, fc_pc;
     DBuf or_a, or_w, or_work, or_vs, or_vk, or_s, or_keep;
     DBuf ref_c, ref_ws;  // refinement (verification) scratch
@@ -689,6 +690,10 @@ void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const dou
         grp.ranks.push_back(&h->ranks[i]);
     }
     // ---- sharded Schur: this rank's chunks of the sorted pair list --------------
+    // Each rank reduces its chunk range into per-segment blocks; the blocks
+    // are grouped by the rank owning their block column and one
+    // reduce-scatter hands every rank the sums of exactly its blocks
+    // (nnz x 81 doubles in total instead of an all-reduce of all of them).
     const PairDev& pd = h->pairs;
     const size_t segd = (size_t)pd.nseg * 81;
     double* seg = h->seg.as<double>(segd + 1);
@@ -696,6 +701,11 @@ void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const dou
         *cb = (int)((long long)pd.nchunks * gr / R);
         *ce = (int)((long long)pd.nchunks * (gr + 1) / R);
     };
+    SegGroups& sgp = h->seg_groups;
+    sgp.plan(cm, Ownership{R, 0, Gp}, pd.ukeys, pd.nseg, h->ws, s);
+    const size_t gdoubles = (size_t)sgp.gmax * 81;
+    double* send = h->seg_send.as<double>((size_t)R * gdoubles + 1);
+    double* recv = nullptr;
     if (h->dist_mode == 1) {
         double* tmp = h->seg_tmp.as<double>(segd + 1);
         for (int gr = 0; gr < R; ++gr) {
@@ -704,11 +714,14 @@ void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const dou
             launch_pair_reduce_segments(P, pd, Wb, n, cb, ce, gr == 0 ? seg : tmp, s);
             if (gr) launch_add(seg, tmp, segd, s);
         }
+        sgp.pack(seg, send, s);  // emulated ranks: the sum, grouped; rank g reads its slice
     } else {
         int cb, ce;
         chunk_range(h->dist_rank, &cb, &ce);
         launch_pair_reduce_segments(P, pd, Wb, n, cb, ce, seg, s);
-        dist_allreduce(grp, seg, segd, 0, s);
+        sgp.pack(seg, send, s);
+        recv = h->seg_recv.as<double>(gdoubles + 1);
+        dist_reduce_scatter(grp, send, recv, gdoubles, s);
     }
     mark(h, 6);
     int* psd = h->psd.as<int>(1);
@@ -724,7 +737,8 @@ void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const dou
         // broadcasts (stream sc) start after the block all-reduce (stream s)
         SFM_CUDA(cudaStreamWaitEvent(r.sc, h->ev_ready, 0));
         launch_fill_local(cm, r.ow, r.zp, ld, Npad, r.ncl, D, s_a, G, r.s);
-        launch_seg_scatter(cm, r.ow, seg, pd.ukeys, pd.nseg, r.zp, ld, r.s);
+        const int g = r.ow.rank;
+        sgp.scatter(g, recv ? recv : send + (size_t)g * gdoubles, cm, r.ow, pd.ukeys, r.zp, ld, r.s);
     }
     mark(h, 7);
     dist_sweep(grp, sts.data());
@@ -925,6 +939,9 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     for (auto& r : h->ranks) r.release();
     h->seg.release();
     h->seg_tmp.release();
+    h->seg_send.release();
+    h->seg_recv.release();
+    h->seg_groups.release();
     h->prange_r.release();
     h->scale_mm.release();
     for (DBuf* b : {&h->zi, &h->fc_part, &h->fc_y, &h->fc_gtt, &h->fc_eb, &h->fc_pc, &h->or_a, &h->or_w, &h->or_work,

@@ -28,6 +28,8 @@
 
 #include <dlfcn.h>
 
+#include <cub/cub.cuh>
+
 #include <cstring>
 
 #include <algorithm>
@@ -120,6 +122,103 @@ void launch_seg_scatter(const ColMap& cm, const Ownership& ow, const double* seg
     if (!nseg) return;
     if (cm.P == 8) k_seg_scatter<8><<<cdiv(nseg, 8), 256, 0, s>>>(seg, ukeys, nseg, cm, ow, Zl, ld);
     else k_seg_scatter<9><<<cdiv(nseg, 8), 256, 0, s>>>(seg, ukeys, nseg, cm, ow, Zl, ld);
+    SFM_LAUNCH_CHECK();
+}
+
+// ---- pair blocks to their column owners (reduce-scatter) --------------------------
+// owner rank of each segment's block column (the camera lo of key lo n + hi)
+__global__ void k_seg_owner(const unsigned int* ukeys, int nseg, ColMap cm, Ownership ow, int* owner, int* cnt) {
+    const int sg = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sg >= nseg) return;
+    const int lo = (int)(ukeys[sg] / (unsigned int)cm.n);
+    const int o = ((cm_col(cm, lo, 0) / kNB) / ow.G) % ow.R;
+    owner[sg] = o;
+    atomicAdd(&cnt[o], 1);  // integer counts: order independent
+}
+__global__ void k_iota_int(int* v, int count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) v[i] = i;
+}
+// send[g][k] = seg[perm[off_g + k]] (k < cnt_g), zero padding to Gmax blocks per group
+__global__ void k_seg_pack(const double* seg, const int* perm, const int* off, const int* cnt, int R, int gmax,
+                           double* send) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)R * gmax * 81) return;
+    const long long blk = e / 81;
+    const int en = (int)(e - blk * 81);
+    const int g = (int)(blk / gmax), k = (int)(blk - (long long)g * gmax);
+    send[e] = k < cnt[g] ? seg[(size_t)perm[off[g] + k] * 81 + en] : 0.0;
+}
+// Z(cam hi row p, cam lo column q) -= grp[k](p, q) for this rank's group
+template <int P>
+__global__ void __launch_bounds__(256) k_seg_scatter_group(const double* grp, const int* perm, int cnt,
+                                                           const unsigned int* ukeys, ColMap cm, Ownership ow,
+                                                           double* Zl, long long ld) {
+    const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (k >= cnt) return;
+    const unsigned int key = ukeys[perm[k]];
+    const int lo = (int)(key / (unsigned int)cm.n), hi = (int)(key - (unsigned int)lo * (unsigned int)cm.n);
+    const int lc = own_lcol(ow, cm_col(cm, lo, 0));
+    if (lc < 0) return;  // (never: the group holds this rank's columns only)
+    const int r0 = cm_col(cm, hi, 0);
+    for (int en = lane; en < P * P; en += 32) {
+        const int p = en / P, q = en - P * (en / P);
+        if (lo == hi && p < q) continue;
+        double* z = Zl + (size_t)(lc + q) * ld + r0 + p;
+        *z = *z - grp[(size_t)k * 81 + en];
+    }
+}
+
+void SegGroups::plan(const ColMap& cm, const Ownership& ow, const unsigned int* ukeys, int nseg, Workspace& ws,
+                     cudaStream_t s) {
+    R = ow.R;
+    int* owner = buf_owner.as<int>((size_t)nseg + 1);
+    int* owner2 = buf_owner2.as<int>((size_t)nseg + 1);
+    int* ids = buf_ids.as<int>((size_t)nseg + 1);
+    perm = buf_perm.as<int>((size_t)nseg + 1);
+    int* dcnt = buf_cnt.as<int>(2 * (size_t)R + 2);
+    SFM_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int) * (size_t)R, s));
+    if (nseg) {
+        k_seg_owner<<<cdiv(nseg, 256), 256, 0, s>>>(ukeys, nseg, cm, ow, owner, dcnt);
+        SFM_LAUNCH_CHECK();
+        k_iota_int<<<cdiv(nseg, 256), 256, 0, s>>>(ids, nseg);
+        SFM_LAUNCH_CHECK();
+        int bits = 1;
+        while ((1 << bits) < R) ++bits;
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, owner, owner2, ids, perm, nseg, 0, bits, s);
+        SFM_CUDA(cub::DeviceRadixSort::SortPairs(ws.get_tmp(bytes), bytes, owner, owner2, ids, perm, nseg, 0, bits, s));
+    }
+    cnt.assign(R, 0);
+    SFM_CUDA(cudaMemcpyAsync(cnt.data(), dcnt, sizeof(int) * (size_t)R, cudaMemcpyDeviceToHost, s));
+    SFM_CUDA(cudaStreamSynchronize(s));
+    off.assign(R + 1, 0);
+    gmax = 0;
+    for (int g = 0; g < R; ++g) {
+        off[g + 1] = off[g] + cnt[g];
+        gmax = std::max(gmax, cnt[g]);
+    }
+    gmax = std::max(gmax, 1);
+    int* doff = dcnt + R;
+    SFM_CUDA(cudaMemcpyAsync(doff, off.data(), sizeof(int) * (size_t)R, cudaMemcpyHostToDevice, s));
+    d_off = doff;
+    d_cnt = dcnt;
+}
+
+void SegGroups::pack(const double* seg, double* send, cudaStream_t s) const {
+    const long long tot = (long long)R * gmax * 81;
+    k_seg_pack<<<cdiv(tot, 256), 256, 0, s>>>(seg, perm, d_off, d_cnt, R, gmax, send);
+    SFM_LAUNCH_CHECK();
+}
+
+void SegGroups::scatter(int g, const double* grp, const ColMap& cm, const Ownership& ow, const unsigned int* ukeys,
+                        double* Zl, long long ld, cudaStream_t s) const {
+    if (!cnt[g]) return;
+    if (cm.P == 8)
+        k_seg_scatter_group<8><<<cdiv(cnt[g], 8), 256, 0, s>>>(grp, perm + off[g], cnt[g], ukeys, cm, ow, Zl, ld);
+    else
+        k_seg_scatter_group<9><<<cdiv(cnt[g], 8), 256, 0, s>>>(grp, perm + off[g], cnt[g], ukeys, cm, ow, Zl, ld);
     SFM_LAUNCH_CHECK();
 }
 
@@ -290,6 +389,8 @@ struct NcclApi {
     ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                  cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -307,8 +408,9 @@ NcclApi& nccl_api() {
         a.CommDestroy = (decltype(a.CommDestroy))dlsym(lib, "ncclCommDestroy");
         a.Broadcast = (decltype(a.Broadcast))dlsym(lib, "ncclBroadcast");
         a.AllReduce = (decltype(a.AllReduce))dlsym(lib, "ncclAllReduce");
+        a.ReduceScatter = (decltype(a.ReduceScatter))dlsym(lib, "ncclReduceScatter");
         a.GetErrorString = (decltype(a.GetErrorString))dlsym(lib, "ncclGetErrorString");
-        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Broadcast && a.AllReduce && a.GetErrorString;
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Broadcast && a.AllReduce && a.ReduceScatter && a.GetErrorString;
         if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
         return a;
     }();
@@ -562,6 +664,12 @@ void dist_allreduce(DistGroup& grp, double* buf, size_t count, int op, cudaStrea
     if (!grp.nccl || !count) return;
     const ncclRedOp_t o = op == 0 ? ncclSum : (op == 1 ? ncclMin : ncclMax);
     nccl_check(nccl_api().AllReduce(buf, buf, count, ncclDouble, o, (ncclComm_t)grp.nccl, s), "AllReduce");
+}
+
+void dist_reduce_scatter(DistGroup& grp, const double* send, double* recv, size_t count, cudaStream_t s) {
+    if (!grp.nccl || !count) return;
+    nccl_check(nccl_api().ReduceScatter(send, recv, count, ncclDouble, ncclSum, (ncclComm_t)grp.nccl, s),
+               "ReduceScatter");
 }
 
 void dist_allreduce_int_min(DistGroup& grp, int* buf, cudaStream_t s) {

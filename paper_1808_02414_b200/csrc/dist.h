@@ -41,7 +41,27 @@ struct DistGroup {
     void* nccl = nullptr;
 };
 
+// Pair blocks grouped by the rank owning their block column (1D panel
+// ownership), so one reduce-scatter hands each rank exactly its blocks:
+// group g = segments perm[off[g] .. off[g] + cnt[g]), padded to gmax blocks.
+struct SegGroups {
+    int R = 1, gmax = 1;
+    std::vector<int> cnt, off;
+    int* perm = nullptr;
+    int* d_off = nullptr;
+    int* d_cnt = nullptr;
+    DBuf buf_owner, buf_owner2, buf_ids, buf_perm, buf_cnt;
+    void plan(const ColMap& cm, const Ownership& ow, const unsigned int* ukeys, int nseg, Workspace& ws,
+              cudaStream_t s);
+    void pack(const double* seg, double* send, cudaStream_t s) const;  // R * gmax * 81 doubles
+    void scatter(int g, const double* grp, const ColMap& cm, const Ownership& ow, const unsigned int* ukeys,
+                 double* Zl, long long ld, cudaStream_t s) const;
+    void release() { buf_owner.release(); buf_owner2.release(); buf_ids.release(); buf_perm.release(); buf_cnt.release(); }
+};
+
 void dist_sweep(DistGroup& grp, Status* const* st);
+// ncclReduceScatter (sum) of R * count doubles: rank r receives slice r (no-op without NCCL)
+void dist_reduce_scatter(DistGroup& grp, const double* send, double* recv, size_t count, cudaStream_t s);
 // op: 0 sum, 1 min, 2 max (no-op without NCCL)
 void dist_allreduce(DistGroup& grp, double* buf, size_t count, int op, cudaStream_t s);
 void dist_allreduce_int_min(DistGroup& grp, int* buf, cudaStream_t s);

@@ -28,6 +28,7 @@
 
 #include <cub/cub.cuh>
 #include <cstdlib>
+#include <string>
 
 namespace sfm {
 
@@ -580,6 +581,160 @@ __global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned in
     }
 }
 
+// The same reduction with the operands staged through shared memory: each
+// warp copies the two factor rows of 8 pairs at a time (16 rows x 224 B,
+// coalesced 16-byte cp.async, two stages in flight) and feeds the MMA
+// fragments from shared memory.  The register-gather version above keeps
+// every lane's scattered 8-byte loads on the critical path (ncu: 50-65 %
+// long-scoreboard stalls, 3.2 GB of L2 sectors for 0.36 GB of operands);
+// here a lane has 7 16-byte copies in flight per stage.  SFMCOV_PAIR_KERNEL=gather
+// selects the register-gather kernel (A/B measurements).  Same chunking,
+// same per-lane accumulation order, same output / partial layout.
+constexpr int kCpRowParts = kWStride / 2; // 16-byte parts per factor row
+template <int BP, int NW>
+constexpr size_t pair_cp_smem_bytes() { return (size_t)NW * 2 * (2 * BP) * kWStride * sizeof(double); }
+
+template <int P, int kCpPairs, int kCpWarps, int MINB>
+__global__ void __launch_bounds__(kCpWarps * 32, MINB) k_pair_reduce_cp(const unsigned int* ukeys, const long long* seg_off,
+                                                                   const int* seg_of, const int* chunk_off, int nchunks,
+                                                                   int chunk, const unsigned long long* vals,
+                                                                   const double* Wb, int n, double* Z, long long ld,
+                                                                   double* part, int cfirst, int always_part,
+                                                                   int lo_min, int lo_max) {
+    extern __shared__ __align__(16) double sm_pairs[];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = cfirst + blockIdx.x * kCpWarps + wib;
+    if (warp >= nchunks) return;
+    const int sg = __ldg(seg_of + warp);
+    const unsigned int key = ukeys[sg];
+    const int lo = (int)(key / (unsigned int)n), hi = (int)(key - (unsigned int)lo * (unsigned int)n);
+    if (lo < lo_min || lo >= lo_max) return;
+    const int c0 = __ldg(chunk_off + sg), nch = __ldg(chunk_off + sg + 1) - c0;
+    const int r = lane >> 2, k = lane & 3;
+    const long long sb = seg_off[sg], se = seg_off[sg + 1];
+    const long long b = sb + (long long)(warp - c0) * chunk;
+    const long long e = min(se, b + chunk);
+    double* stage_base = sm_pairs + (size_t)wib * 2 * (2 * kCpPairs) * kWStride;
+    auto stage = [&](int st) { return stage_base + (size_t)st * (2 * kCpPairs) * kWStride; };
+    const int nb = (int)((e - b + kCpPairs - 1) / kCpPairs);
+    auto issue = [&](int bi) {
+        double* dst = stage(bi & 1);
+        const long long pb = b + (long long)bi * kCpPairs;
+        const int cnt = (int)min((long long)kCpPairs, e - pb);
+        // lane i < cnt holds pair i's slots; the copies fetch them by shuffle
+        const unsigned long long mine = lane < cnt ? __ldg(vals + pb + lane) : 0ULL;
+#pragma unroll
+        for (int c0 = 0; c0 < 2 * kCpPairs * kCpRowParts; c0 += 32) {
+            const int c = c0 + lane;
+            const int row = c / kCpRowParts, prt = c - row * kCpRowParts;
+            const int pi = row >> 1;
+            const unsigned long long v = __shfl_sync(0xffffffffu, mine, pi & 31);
+            if (c < 2 * kCpPairs * kCpRowParts && pi < cnt) {
+                const unsigned int slot = (row & 1) ? (unsigned int)(v & 0xffffffffULL) : (unsigned int)(v >> 32);
+                cpa16(dst + (size_t)row * kWStride + 2 * prt, Wb + (size_t)slot * kWStride + 2 * prt);
+            }
+        }
+        cpa_commit();
+    };
+    double c0v = 0.0, c1v = 0.0;            // MMA tile (rows 0..7, cols 0..7)
+    double r8 = 0.0, cl8 = 0.0, x88 = 0.0;  // P = 9: row 8, column 8, corner (k-partials)
+    if (nb > 0) issue(0);
+    for (int bi = 0; bi < nb; ++bi) {
+        if (bi + 1 < nb) {
+            issue(bi + 1);
+            cpa_wait<1>();
+        } else {
+            cpa_wait<0>();
+        }
+        __syncwarp();
+        const double* src = stage(bi & 1);
+        const int cnt = (int)min((long long)kCpPairs, e - (b + (long long)bi * kCpPairs));
+        const int nel = 3 * cnt, nsteps = (nel + 3) >> 2;
+#pragma unroll 4
+        for (int st = 0; st < nsteps; ++st) {
+            const int el = 4 * st + k;
+            const int pi = el / 3, kk = el - 3 * pi;
+            const bool ok = el < nel;
+            const double* wh = src + (size_t)(2 * pi) * kWStride;
+            const double* wl = wh + kWStride;
+            const double ah = ok ? wh[3 * r + kk] : 0.0;
+            const double al = ok ? wl[3 * r + kk] : 0.0;
+            dmma_pr(c0v, c1v, ah, al);
+            if (P == 9) {
+                const double h8 = ok ? wh[24 + kk] : 0.0;
+                const double l8 = ok ? wl[24 + kk] : 0.0;
+                r8 = fma(h8, al, r8);
+                cl8 = fma(ah, l8, cl8);
+                if (r == 0) x88 = fma(h8, l8, x88);
+            }
+        }
+        __syncwarp();  // the stage is refilled two batches later
+    }
+    if (P == 9) {  // sum the four k-partials (fixed order)
+        r8 += __shfl_xor_sync(0xffffffffu, r8, 1);
+        r8 += __shfl_xor_sync(0xffffffffu, r8, 2);
+        cl8 += __shfl_xor_sync(0xffffffffu, cl8, 1);
+        cl8 += __shfl_xor_sync(0xffffffffu, cl8, 2);
+        x88 += __shfl_xor_sync(0xffffffffu, x88, 1);
+        x88 += __shfl_xor_sync(0xffffffffu, x88, 2);
+    }
+    const bool diag = lo == hi;
+    double* pp = part + (size_t)warp * 81;
+    auto put = [&](int p, int q, double v) {
+        if (nch > 1 || always_part) { pp[P * p + q] = v; return; }
+        if (diag && p < q) return;
+        double* z = Z + ((size_t)P * lo + q) * ld + (size_t)P * hi + p;
+        *z = *z - v;
+    };
+    const int q0 = 2 * k;
+    put(r, q0, c0v);
+    put(r, q0 + 1, c1v);
+    if (P == 9) {
+        if (k == 0) {
+            put(8, r, r8);
+            put(r, 8, cl8);
+        }
+        if (lane == 0) put(8, 8, x88);
+    }
+}
+
+static bool pair_kernel_old() {
+    static bool v = [] { const char* e = std::getenv("SFMCOV_PAIR_KERNEL"); return e && std::string(e) == "gather"; }();
+    return v;
+}
+
+static void launch_pair_mma(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, int cfirst,
+                            int clast, int always_part, int lo_min, int lo_max, cudaStream_t s) {
+    const int cnt = clast - cfirst;
+    if (cnt <= 0) return;
+    if (pair_kernel_old()) {
+        const unsigned cblocks = cdiv(cnt, 8);
+        if (P == 8)
+            k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, clast,
+                                                                pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, cfirst,
+                                                                always_part, lo_min, lo_max);
+        else
+            k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, clast,
+                                                                pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, cfirst,
+                                                                always_part, lo_min, lo_max);
+        SFM_LAUNCH_CHECK();
+        return;
+    }
+    // 8 pairs per stage, 4 warps per CTA, 6 CTAs per SM (24 warps): config 3
+    // pair stage 0.78 ms against 0.82 for the register gathers; 16 pairs x 4
+    // warps (12 warps / SM) 0.91, 8 x 8 warps 0.79, one zero-padded MMA per
+    // pair (no index division) 1.06 -- the kernel is issue-bound (IPC 2.3,
+    // 58 % issue slots, ncu profiles/r02_ncu_pair_reduce.txt)
+    auto go = [&](auto kern, size_t smem) {
+        SFM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<cdiv(cnt, 4), 4 * 32, smem, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, clast, pd.chunk,
+                                                pd.vals, Wb, n, Z, ld, pd.part, cfirst, always_part, lo_min, lo_max);
+        SFM_LAUNCH_CHECK();
+    };
+    if (P == 8) go(k_pair_reduce_cp<8, 8, 4, 6>, pair_cp_smem_bytes<8, 4>());
+    else go(k_pair_reduce_cp<9, 8, 4, 6>, pair_cp_smem_bytes<8, 4>());
+}
+
 // Multi-chunk segments: partial blocks summed in chunk order, then written.
 template <int P>
 __global__ void __launch_bounds__(256) k_pair_combine(const unsigned int* ukeys, int nseg, const int* chunk_off,
@@ -768,16 +923,7 @@ void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, doubl
                         int lo_min, int lo_max) {
     if (!pd.nseg) return;
     const unsigned blocks = cdiv(pd.nseg, 8);
-    const unsigned cblocks = cdiv(pd.nchunks, 8);
-    // 4 pairs gathered ahead, 4 CTAs (32 warps) per SM: the kernel is bound
-    // by gather latency, so occupancy beats deeper prefetch
-    if (P == 8)
-        k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, pd.nchunks,
-                                                            pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0, lo_min, lo_max);
-    else
-        k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, pd.nchunks,
-                                                            pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, 0, 0, lo_min, lo_max);
-    SFM_LAUNCH_CHECK();
+    launch_pair_mma(P, pd, Wb, n, Z, ld, 0, pd.nchunks, 0, lo_min, lo_max, s);
     if (P == 8) k_pair_combine<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld, lo_min, lo_max);
     else k_pair_combine<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld, lo_min, lo_max);
     SFM_LAUNCH_CHECK();
@@ -786,16 +932,7 @@ void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, doubl
 void launch_pair_reduce_segments(int P, const PairDev& pd, const double* Wb, int n, int c_begin, int c_end,
                                  double* seg_out, cudaStream_t s) {
     if (!pd.nseg) return;
-    if (c_end > c_begin) {
-        const unsigned cblocks = cdiv(c_end - c_begin, 8);
-        if (P == 8)
-            k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, c_end,
-                                                                pd.chunk, pd.vals, Wb, n, nullptr, 0, pd.part, c_begin, 1, 0, n);
-        else
-            k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, c_end,
-                                                                pd.chunk, pd.vals, Wb, n, nullptr, 0, pd.part, c_begin, 1, 0, n);
-        SFM_LAUNCH_CHECK();
-    }
+    launch_pair_mma(P, pd, Wb, n, nullptr, 0, c_begin, c_end, 1, 0, n, s);
     const unsigned blocks = cdiv(pd.nseg, 8);
     if (P == 8) k_pair_combine_seg<8><<<blocks, 256, 0, s>>>(pd.nseg, pd.chunk_off, pd.part, c_begin, c_end, seg_out);
     else k_pair_combine_seg<9><<<blocks, 256, 0, s>>>(pd.nseg, pd.chunk_off, pd.part, c_begin, c_end, seg_out);

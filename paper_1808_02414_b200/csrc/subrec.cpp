@@ -13,6 +13,9 @@
 #include "sfmcov_b200.h"
 
 #include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -125,105 +128,113 @@ struct Sub {
 };
 
 // Observations by camera (ascending observation ids), built once per call so
-// an induced scene only visits its own cameras' observations.
+// an induced scene only visits its own cameras' observations; the point id of
+// each by-camera slot is stored beside it, so the filter below streams
+// contiguous ranges instead of gathering obs_pt[t].
 struct ByCam {
     std::vector<int64_t> off;
-    std::vector<int32_t> idx;
-    explicit ByCam(const sfmcov_scene& s) : off(s.n_cams + 1, 0), idx(s.n_obs) {
+    std::vector<int32_t> idx, pt;
+    explicit ByCam(const sfmcov_scene& s) : off(s.n_cams + 1, 0), idx(s.n_obs), pt(s.n_obs) {
         for (int32_t t = 0; t < s.n_obs; ++t) ++off[s.obs_cam[t] + 1];
         for (int32_t i = 0; i < s.n_cams; ++i) off[i + 1] += off[i];
         std::vector<int64_t> f(off.begin(), off.end() - 1);
-        for (int32_t t = 0; t < s.n_obs; ++t) idx[f[s.obs_cam[t]]++] = t;
+        for (int32_t t = 0; t < s.n_obs; ++t) {
+            const int64_t k = f[s.obs_cam[t]]++;
+            idx[k] = t;
+            pt[k] = s.obs_pt[t];
+        }
     }
 };
 
-// induced_scene (src/subrec.cpp:24-86): points seen by >= 2 subset cameras,
-// cameras with >= 4 surviving observations, to a fixpoint.
 // Scratch arrays of one planner thread, reset only where touched.
 struct Scratch {
-    std::vector<char> cam_in, pt_in;
+    std::vector<char> cam_in;
     std::vector<int32_t> pc, cc, cl, pl;
-    void size(int64_t n, int64_t m) {
+    std::vector<uint64_t> obs_bits, pt_bits;
+    void size(int64_t n, int64_t m, int64_t t) {
         if ((int64_t)cam_in.size() != n) { cam_in.assign(n, 0); cc.assign(n, 0); cl.assign(n, -1); }
-        if ((int64_t)pt_in.size() != m) { pt_in.assign(m, 0); pc.assign(m, 0); pl.assign(m, -1); }
+        if ((int64_t)pc.size() != m) { pc.assign(m, 0); pl.assign(m, -1); pt_bits.assign((m + 63) / 64, 0); }
+        if ((int64_t)obs_bits.size() != (t + 63) / 64) obs_bits.assign((t + 63) / 64, 0);
     }
 };
+
+// induced_scene's filter (src/subrec.cpp:24-86): points seen by >= 2 subset
+// cameras, cameras with >= 4 surviving observations, to a fixpoint.  Leaves
+// cam_in set for the surviving cameras and pc[j] = the point's surviving
+// observer count; the caller resets them (reset_filter).
+void filter_fixpoint(const ByCam& bc, const std::vector<int32_t>& cams, Scratch& w) {
+    for (int32_t c : cams) w.cam_in[c] = 1;
+    for (bool changed = true; changed;) {
+        for (int32_t c : cams)
+            for (int64_t k = bc.off[c]; k < bc.off[c + 1]; ++k) w.pc[bc.pt[k]] = 0;
+        for (int32_t c : cams)
+            if (w.cam_in[c])
+                for (int64_t k = bc.off[c]; k < bc.off[c + 1]; ++k) ++w.pc[bc.pt[k]];
+        changed = false;
+        for (int32_t c : cams) {
+            if (!w.cam_in[c]) continue;
+            int32_t cnt = 0;
+            for (int64_t k = bc.off[c]; k < bc.off[c + 1]; ++k) cnt += w.pc[bc.pt[k]] >= 2;
+            w.cc[c] = cnt;
+            if (cnt < 4) {
+                w.cam_in[c] = 0;
+                changed = true;
+            }
+        }
+    }
+}
+void reset_filter(const ByCam& bc, const std::vector<int32_t>& cams, Scratch& w) {
+    for (int32_t c : cams) {
+        w.cam_in[c] = 0;
+        w.cc[c] = 0;
+        w.cl[c] = -1;
+        for (int64_t k = bc.off[c]; k < bc.off[c + 1]; ++k) {
+            w.pc[bc.pt[k]] = 0;
+            w.pl[bc.pt[k]] = -1;
+        }
+    }
+}
 
 // The cameras that survive the induced filter (its fixpoint), ascending: the
 // part of induced_scene the covering loop needs before its next draw.
 std::vector<int32_t> induced_cams(const sfmcov_scene& s, const ByCam& bc, const std::vector<int32_t>& cams) {
-    const int64_t n = s.n_cams, m = s.n_pts;
     thread_local Scratch w;
-    w.size(n, m);
-    for (int32_t c : cams) w.cam_in[c] = 1;
-    std::vector<int32_t> cand;
-    for (int32_t c : cams) cand.insert(cand.end(), bc.idx.begin() + bc.off[c], bc.idx.begin() + bc.off[c + 1]);
-    for (bool changed = true; changed;) {
-        for (int32_t t : cand) w.pc[s.obs_pt[t]] = 0;
-        for (int32_t t : cand)
-            if (w.cam_in[s.obs_cam[t]]) ++w.pc[s.obs_pt[t]];
-        for (int32_t t : cand) w.pt_in[s.obs_pt[t]] = w.pc[s.obs_pt[t]] >= 2;
-        for (int32_t c : cams) w.cc[c] = 0;
-        for (int32_t t : cand)
-            if (w.cam_in[s.obs_cam[t]] && w.pt_in[s.obs_pt[t]]) ++w.cc[s.obs_cam[t]];
-        changed = false;
-        for (int32_t i : cams)
-            if (w.cam_in[i] && w.cc[i] < 4) {
-                w.cam_in[i] = 0;
-                changed = true;
-            }
-    }
+    w.size(s.n_cams, s.n_pts, s.n_obs);
+    filter_fixpoint(bc, cams, w);
     std::vector<int32_t> out;
     for (int32_t c : cams)
         if (w.cam_in[c]) out.push_back(c);
     std::sort(out.begin(), out.end());
-    for (int32_t c : cams) { w.cam_in[c] = 0; w.cc[c] = 0; }
-    for (int32_t t : cand) { const int32_t j = s.obs_pt[t]; w.pt_in[j] = 0; w.pc[j] = 0; }
+    reset_filter(bc, cams, w);
     return out;
 }
 
 Sub induced(const sfmcov_scene& s, const ByCam& bc, const std::vector<int32_t>& cams, bool truncated) {
-    const int64_t n = s.n_cams, m = s.n_pts;
     thread_local Scratch w;
-    w.size(n, m);
-    std::vector<char>& cam_in = w.cam_in;
-    std::vector<char>& pt_in = w.pt_in;
-    std::vector<int32_t>&pc = w.pc, &cc = w.cc;
-    for (int32_t c : cams) cam_in[c] = 1;
-    std::vector<int32_t> cand;  // the subset cameras' observations
-    for (int32_t c : cams) cand.insert(cand.end(), bc.idx.begin() + bc.off[c], bc.idx.begin() + bc.off[c + 1]);
-    for (bool changed = true; changed;) {
-        for (int32_t t : cand) pc[s.obs_pt[t]] = 0;
-        for (int32_t t : cand)
-            if (cam_in[s.obs_cam[t]]) ++pc[s.obs_pt[t]];
-        for (int32_t t : cand) pt_in[s.obs_pt[t]] = pc[s.obs_pt[t]] >= 2;
-        for (int32_t c : cams) cc[c] = 0;
-        for (int32_t t : cand)
-            if (cam_in[s.obs_cam[t]] && pt_in[s.obs_pt[t]]) ++cc[s.obs_cam[t]];
-        changed = false;
-        for (int32_t i : cams)
-            if (cam_in[i] && cc[i] < 4) {
-                cam_in[i] = 0;
-                changed = true;
-            }
-    }
-    // kept observations in ascending id order (the reference's candidate order)
-    std::vector<int32_t> kept;
-    kept.reserve(cand.size());
-    for (int32_t t : cand)
-        if (cam_in[s.obs_cam[t]] && pt_in[s.obs_pt[t]]) kept.push_back(t);
-    std::sort(kept.begin(), kept.end());
-    std::vector<int32_t>&cl = w.cl, &pl = w.pl;
+    w.size(s.n_cams, s.n_pts, s.n_obs);
+    filter_fixpoint(bc, cams, w);
     struct Reset {  // leave the scratch clean for the next call
-        Scratch& w;
+        const ByCam& bc;
         const std::vector<int32_t>& cams;
-        const std::vector<int32_t>& cand;
-        const sfmcov_scene& s;
-        ~Reset() {
-            for (int32_t c : cams) { w.cam_in[c] = 0; w.cc[c] = 0; w.cl[c] = -1; }
-            for (int32_t t : cand) { const int32_t j = s.obs_pt[t]; w.pt_in[j] = 0; w.pc[j] = 0; w.pl[j] = -1; }
+        Scratch& w;
+        ~Reset() { reset_filter(bc, cams, w); }
+    } reset{bc, cams, w};
+    // kept observations and points as bitmaps: scanning them gives ascending
+    // observation ids (the reference's candidate order) and point ids
+    int64_t t_lo = INT64_MAX, t_hi = -1, j_lo = INT64_MAX, j_hi = -1, nkept = 0;
+    for (int32_t c : cams) {
+        if (!w.cam_in[c]) continue;
+        for (int64_t k = bc.off[c]; k < bc.off[c + 1]; ++k) {
+            const int32_t j = bc.pt[k];
+            if (w.pc[j] < 2) continue;
+            const int64_t t = bc.idx[k];
+            w.obs_bits[t >> 6] |= 1ULL << (t & 63);
+            w.pt_bits[j >> 6] |= 1ULL << (j & 63);
+            t_lo = std::min(t_lo, t); t_hi = std::max(t_hi, t);
+            j_lo = std::min<int64_t>(j_lo, j); j_hi = std::max<int64_t>(j_hi, j);
+            ++nkept;
         }
-    } reset{w, cams, cand, s};
+    }
     Sub sub;
     sub.truncated = truncated;
     const int P = s.cam_params;
@@ -235,33 +246,46 @@ Sub induced(const sfmcov_scene& s, const ByCam& bc, const std::vector<int32_t>& 
         std::vector<int32_t> sorted_cams(cams.begin(), cams.end());
         std::sort(sorted_cams.begin(), sorted_cams.end());
         for (int32_t i : sorted_cams)
-            if (cam_in[i]) {
-                cl[i] = (int32_t)sub.cams.size();
+            if (w.cam_in[i]) {
+                w.cl[i] = (int32_t)sub.cams.size();
                 sub.cams.push_back(i);
-                h.cams.insert(h.cams.end(), s.cams + (size_t)P * i, s.cams + (size_t)P * i + P);
             }
+        h.cams.resize((size_t)P * sub.cams.size());
+        for (size_t l = 0; l < sub.cams.size(); ++l)
+            std::memcpy(&h.cams[(size_t)P * l], s.cams + (size_t)P * sub.cams[l], 8 * (size_t)P);
     }
-    if (sub.cams.empty()) throw SubError{SFMCOV_ERR_DEGENERATE, "subrec", "induced sub-reconstruction is empty"};
-    {
-        std::vector<int32_t> pts;  // ascending ids of the kept points
-        for (int32_t t : kept)
-            if (pl[s.obs_pt[t]] == -1) {
-                pl[s.obs_pt[t]] = 0;
-                pts.push_back(s.obs_pt[t]);
+    if (sub.cams.empty()) {
+        for (int64_t t = t_lo; t <= t_hi; t += 64) w.obs_bits[t >> 6] = 0;
+        throw SubError{SFMCOV_ERR_DEGENERATE, "subrec", "induced sub-reconstruction is empty"};
+    }
+    if (j_hi >= 0)
+        for (int64_t wd = j_lo >> 6; wd <= (j_hi >> 6); ++wd)
+            for (uint64_t bits = w.pt_bits[wd]; bits; bits &= bits - 1) {
+                const int32_t j = (int32_t)(wd * 64 + __builtin_ctzll(bits));
+                w.pl[j] = (int32_t)sub.pts.size();
+                sub.pts.push_back(j);
             }
-        std::sort(pts.begin(), pts.end());
-        for (int32_t j : pts) {
-            pl[j] = (int32_t)sub.pts.size();
-            sub.pts.push_back(j);
-            h.pts.insert(h.pts.end(), s.pts + 3 * size_t(j), s.pts + 3 * size_t(j) + 3);
+    h.pts.resize(3 * sub.pts.size());
+    for (size_t l = 0; l < sub.pts.size(); ++l) std::memcpy(&h.pts[3 * l], s.pts + 3 * (size_t)sub.pts[l], 24);
+    h.oc.resize(nkept);
+    h.op.resize(nkept);
+    if (h.has_u) h.u.resize(2 * (size_t)nkept);
+    if (h.has_sigma) h.sigma.resize(4 * (size_t)nkept);
+    int64_t o = 0;
+    if (t_hi >= 0)
+        for (int64_t wd = t_lo >> 6; wd <= (t_hi >> 6); ++wd) {
+            for (uint64_t bits = w.obs_bits[wd]; bits; bits &= bits - 1) {
+                const int64_t t = wd * 64 + __builtin_ctzll(bits);
+                h.oc[o] = w.cl[s.obs_cam[t]];
+                h.op[o] = w.pl[s.obs_pt[t]];
+                if (h.has_u) std::memcpy(&h.u[2 * (size_t)o], s.obs_u + 2 * (size_t)t, 16);
+                if (h.has_sigma) std::memcpy(&h.sigma[4 * (size_t)o], s.obs_sigma + 4 * (size_t)t, 32);
+                ++o;
+            }
+            w.obs_bits[wd] = 0;
         }
-    }
-    for (int32_t t : kept) {
-        h.oc.push_back(cl[s.obs_cam[t]]);
-        h.op.push_back(pl[s.obs_pt[t]]);
-        if (h.has_u) h.u.insert(h.u.end(), s.obs_u + 2 * size_t(t), s.obs_u + 2 * size_t(t) + 2);
-        if (h.has_sigma) h.sigma.insert(h.sigma.end(), s.obs_sigma + 4 * size_t(t), s.obs_sigma + 4 * size_t(t) + 4);
-    }
+    if (j_hi >= 0)
+        for (int64_t wd = j_lo >> 6; wd <= (j_hi >> 6); ++wd) w.pt_bits[wd] = 0;
     h.n = (int32_t)sub.cams.size();
     h.m = (int32_t)sub.pts.size();
     h.t = (int32_t)h.oc.size();
@@ -343,6 +367,18 @@ void check_scene(const sfmcov_scene* s) {
             throw SubError{SFMCOV_ERR_INVARIANT, "validate",
                            "observation " + std::to_string(k) + " index out of range"};
 }
+
+// SFMCOV_SUBREC_TIMING=1: wall time of each phase of a call on stderr.
+struct PhaseClock {
+    bool on = [] { const char* e = std::getenv("SFMCOV_SUBREC_TIMING"); return e && e[0] == '1'; }();
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "subrec %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
 
 // The covariance of every sub-scene, on `workers` handles of `device`.
 struct SubResult {
@@ -486,8 +522,10 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
         if (k_bar < 2) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "subset size must be at least 2"};
         if (n_decompositions < 1) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "need at least one decomposition"};
         if (!scene) throw SubError{SFMCOV_ERR_DIMENSION, "subrec", "bad scene"};
+        PhaseClock clk;
         validate_full(h, scene);
         check_scene(scene);
+        clk.mark("validate");
         const int P = scene->cam_params;
         const Graph g = view_graph(*scene, 1);
         const ByCam bc(*scene);
@@ -513,6 +551,7 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
         }
         for (int d = 0; d < n_decompositions; ++d)
             if (pfail[d]) throw perr[d];
+        clk.mark("plan");
         for (int d = 0; d < n_decompositions; ++d)
             for (Sub& sb : plans[d]) {
                 flat.push_back(&sb);
@@ -543,8 +582,10 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
             for (size_t i = 0; i < flat.size(); ++i)
                 if (bfail[i]) throw berr[i];
         }
+        clk.mark("induce");
         const std::vector<SubResult> res =
             batch_covariances(h, flat, std::max(1, (int)workers));
+        clk.mark("covariances");
         const int64_t n = scene->n_cams;
         std::vector<char> seen(n, 0);
         for (size_t sid = 0; sid < flat.size(); ++sid) {
@@ -570,6 +611,7 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
         for (int64_t i = 0; i < n; ++i)
             if (!seen[i])
                 throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "camera " + std::to_string(i) + " was not covered by any subset"};
+        clk.mark("aggregate");
     });
 }
 

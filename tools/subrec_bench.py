@@ -12,7 +12,7 @@ print(f"planner (3 coverings, host): {time.perf_counter() - t0:.3f} s")
 nsub = sum(len(p) for p in plans)
 sizes = [len(c) for p in plans for c in p]
 print(f"config {cfg}: k_bar {k_bar}, 3 decompositions -> {nsub} subsets, mean {np.mean(sizes):.1f} cameras (N ~ {9*np.mean(sizes):.0f})")
-for w in (1, 2, 4, 8):
+for w in (1, 4, 8, 16):
     R.approximate_covariances(rec, k_bar, 3, 7, workers=w, engine=eng)
     t0 = time.perf_counter(); R.approximate_covariances(rec, k_bar, 3, 7, workers=w, engine=eng); dt = time.perf_counter() - t0
     print(f"workers {w}: {dt:.3f} s  ({nsub / dt:.1f} sub-scenes/s)")

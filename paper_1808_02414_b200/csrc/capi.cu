@@ -55,6 +55,28 @@ enum Mode { M_INDEX, M_JACOBIAN, M_NULLSPACE, M_FISHER, M_SCHUR, M_FULL };
 
 }  // namespace
 
+// One rank's point-sharded stage A (run_dist_sharded): its sub-scene and
+// the stage-A buffers over it.
+struct RankA {
+    sfm::ShardScene sh;
+    sfm::DBuf off_cam, idx_cam, off_pt, idx_pt, pos_cam, key_scratch;
+    sfm::DBuf R, rec, D, Hr, A, s_a, flags, raw, bpart, sq, Lpt, Wb, V, Fpart, Pfirst, Plast, Gsum, F28, S, seg_l, seg_g,
+        status;
+    sfm::Workspace ws, ws_pairs;
+    sfm::PairDev pairs;
+    sfm::IndexDev ix{};
+    void release() {
+        sh.release();
+        for (sfm::DBuf* b : {&off_cam, &idx_cam, &off_pt, &idx_pt, &pos_cam, &key_scratch, &R, &rec, &D, &Hr, &A, &s_a,
+                             &flags, &raw, &bpart, &sq, &Lpt, &Wb, &V, &Fpart, &Pfirst, &Plast, &Gsum, &F28, &S,
+                             &seg_l, &seg_g, &status})
+            b->release();
+        ws.tmp.release();
+        ws_pairs.tmp.release();
+        pairs.release();
+    }
+};
+
 struct sfmcov_handle {
     int device = 0;
     cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr, s4 = nullptr;
@@ -82,8 +104,11 @@ struct sfmcov_handle {
     Status* st_host = nullptr;
     // distributed tail: 0 = single device, 1 = emulated ranks, 2 = NCCL rank
     int dist_mode = 0, dist_R = 1, dist_rank = 0, emu_R = 1;
+    bool replicated_a = false;  // SFMCOV_REPLICATED_STAGE_A=1: the round-1 redundant stage A (A/B)
     void* nccl = nullptr;
     std::vector<sfm::RankDense> ranks;
+    std::vector<RankA> ranka;
+    DBuf sh_bounds, sh_raw, sh_sq, sh_F, sh_S, sh_seg, sh_err;
     DBuf seg, seg_tmp, seg_send, seg_recv, prange_r, scale_mm;
     sfm::SegGroups seg_groups;
     DBuf zi, fc_part, fc_y, fc_gtt, fc_eb, fc_pc;
@@ -333,7 +358,8 @@ void fill_diagnostics(sfmcov_handle* h, Outputs& out, const double* prange, cons
 
 void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const double* D, const double* s_a,
                    const double* G, const double* Wb, Status* st, const unsigned char* flags, size_t ncols,
-                   const double* eigE);
+                   const double* eigE, const double* seg_in = nullptr);
+void run_dist_sharded(sfmcov_handle* h, const SceneDev& sc, const IndexDev& ix, Outputs& out);
 
 // First observation whose pixel u is not finite (LLONG_MAX if none); up to 8
 // host threads for large scenes.
@@ -422,7 +448,8 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     // scene's σ is still uploading (its errors are reported after validation's)
     double* R = nullptr;
     double* rec = nullptr;
-    if (mode != M_INDEX) {
+    const bool sharded_a = h->dist_mode && mode == M_FULL && !h->replicated_a;
+    if (mode != M_INDEX && !sharded_a) {
         R = h->R.as<double>(9 * (size_t)n);
         rec = h->rec.as<double>((size_t)kRec * t);
         launch_jacobian(sc, ix.idx_cam, R, rec, st, s);
@@ -435,6 +462,10 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         if (split_values) throw_validation(h, sc, full);
         if (h->st_host->dup) throw ApiError{SFMCOV_ERR_INVARIANT, "validate", "duplicate (camera, point) observation pair"};
         throw_counts(h);
+    }
+    if (sharded_a) {  // the multi-GPU path: point-sharded stage A (shard.cu)
+        run_dist_sharded(h, sc, ix, out);
+        return;
     }
     if (mode == M_INDEX) {
         std::vector<int> oc(n + 1), op(m + 1);
@@ -664,7 +695,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
 // rank of the group on this device and combine in rank order.
 void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const double* D, const double* s_a,
                    const double* G, const double* Wb, Status* st, const unsigned char* flags, size_t ncols,
-                   const double* eigE) {
+                   const double* eigE, const double* seg_in) {
     cudaStream_t s = h->s;
     const int n = sc.n, P = sc.P, N = P * n;
     const ColMap cm{P, kNB / P, n};
@@ -696,7 +727,7 @@ void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const dou
     // (nnz x 81 doubles in total instead of an all-reduce of all of them).
     const PairDev& pd = h->pairs;
     const size_t segd = (size_t)pd.nseg * 81;
-    double* seg = h->seg.as<double>(segd + 1);
+    double* seg = seg_in ? const_cast<double*>(seg_in) : h->seg.as<double>(segd + 1);
     auto chunk_range = [&](int gr, int* cb, int* ce) {
         *cb = (int)((long long)pd.nchunks * gr / R);
         *ce = (int)((long long)pd.nchunks * (gr + 1) / R);
@@ -707,18 +738,22 @@ void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const dou
     double* send = h->seg_send.as<double>((size_t)R * gdoubles + 1);
     double* recv = nullptr;
     if (h->dist_mode == 1) {
-        double* tmp = h->seg_tmp.as<double>(segd + 1);
-        for (int gr = 0; gr < R; ++gr) {
-            int cb, ce;
-            chunk_range(gr, &cb, &ce);
-            launch_pair_reduce_segments(P, pd, Wb, n, cb, ce, gr == 0 ? seg : tmp, s);
-            if (gr) launch_add(seg, tmp, segd, s);
+        if (!seg_in) {
+            double* tmp = h->seg_tmp.as<double>(segd + 1);
+            for (int gr = 0; gr < R; ++gr) {
+                int cb, ce;
+                chunk_range(gr, &cb, &ce);
+                launch_pair_reduce_segments(P, pd, Wb, n, cb, ce, gr == 0 ? seg : tmp, s);
+                if (gr) launch_add(seg, tmp, segd, s);
+            }
         }
         sgp.pack(seg, send, s);  // emulated ranks: the sum, grouped; rank g reads its slice
     } else {
-        int cb, ce;
-        chunk_range(h->dist_rank, &cb, &ce);
-        launch_pair_reduce_segments(P, pd, Wb, n, cb, ce, seg, s);
+        if (!seg_in) {
+            int cb, ce;
+            chunk_range(h->dist_rank, &cb, &ce);
+            launch_pair_reduce_segments(P, pd, Wb, n, cb, ce, seg, s);
+        }
         sgp.pack(seg, send, s);
         recv = h->seg_recv.as<double>(gdoubles + 1);
         dist_reduce_scatter(grp, send, recv, gdoubles, s);
@@ -781,6 +816,205 @@ void run_dist_tail(sfmcov_handle* h, const SceneDev& sc, Outputs& out, const dou
     int64_t local_bytes = 0;
     for (int i = 0; i < nloc; ++i) local_bytes = std::max<int64_t>(local_bytes, (int64_t)8 * ld * h->ranks[i].ncl);
     fill_diagnostics(h, out, prange, eigE, psd, s_a, flags, ncols, N, local_bytes);
+}
+
+// Point-sharded stage A of the multi-GPU path (shard.cu).  Every rank has
+// validated and indexed the whole scene; rank r then takes the points
+// [j0, j1) (balanced by observation pairs) with their observations and runs
+// stage A on that sub-scene.  Per-camera sums and gauge terms are partial and
+// summed across ranks (all-reduce; emulated ranks: in rank order):
+//   D, rotation normal / rhs        n (P^2 + 18)   -> D, s_a, H_r (every rank)
+//   border column squares           7              -> s_b
+//   F = Σ V^T V                     28             -> L_F, E
+//   Σ_a W_a V_j per camera          n P 7          -> Γ, G
+// and each rank reduces only its points' observation pairs into the global
+// camera-pair block index (every rank builds the same sorted key list), which
+// run_dist_tail hands to the column owners with one reduce-scatter.
+void run_dist_sharded(sfmcov_handle* h, const SceneDev& sc, const IndexDev& gix, Outputs& out) {
+    cudaStream_t s = h->s;
+    const int n = sc.n, m = sc.m, P = sc.P, N = P * n;
+    const int R = h->dist_mode == 1 ? h->emu_R : h->dist_R;
+    const int nloc = h->dist_mode == 1 ? R : 1;
+    if (nloc > 64) throw ApiError{SFMCOV_ERR_DIMENSION, "options", "at most 64 emulated ranks"};
+    DistGroup grp;
+    grp.nccl = h->dist_mode == 2 ? h->nccl : nullptr;
+    auto grank = [&](int i) { return h->dist_mode == 1 ? i : h->dist_rank; };
+    Status* st = h->status.as<Status>(1);
+    // the global camera-pair key list (identical on every rank) and the point ranges
+    build_pairs(sc, gix, h->pairs, h->ws_pairs, s);
+    std::vector<int> bounds;
+    shard_bounds(h->pairs.off, m, R, h->sh_bounds.as<int>((size_t)R + 2), bounds, s);
+    if ((int)h->ranka.size() < nloc) h->ranka.resize(nloc);
+    const int NE = P * P + 18, NB = P * 7;
+    double* raw = h->sh_raw.as<double>((size_t)NE * n + 1);
+    double* sq = h->sh_sq.as<double>(8);
+    double* F = h->sh_F.as<double>(32);
+    double* Ssum = h->sh_S.as<double>((size_t)NB * n + 1);
+    // summed partials: emulated ranks add in rank order, NCCL all-reduces
+    auto combine = [&](double* total, size_t count, auto part_of) {
+        for (int i = 0; i < nloc; ++i) {
+            if (i == 0) SFM_CUDA(cudaMemcpyAsync(total, part_of(0), 8 * count, cudaMemcpyDeviceToDevice, s));
+            else launch_add(total, part_of(i), count, s);
+        }
+        dist_allreduce(grp, total, count, 0, s);
+    };
+    // first failing index over the ranks, in the reference's (global) numbering
+    int* err = h->sh_err.as<int>(8);
+    auto rank_errors = [&](int field) {  // 0 jacobian obs, 1 fisher obs, 2 singular point
+        std::vector<int> best(1, INT_MAX);
+        for (int i = 0; i < nloc; ++i) {
+            RankA& a = h->ranka[i];
+            Status q;
+            SFM_CUDA(cudaMemcpyAsync(&q, a.status.p, sizeof(Status), cudaMemcpyDeviceToHost, s));
+            SFM_CUDA(cudaStreamSynchronize(s));
+            const int v = field == 0 ? q.jac_bad : (field == 1 ? q.fisher_bad : q.pt_sing_bad);
+            if (v == INT_MAX) continue;
+            int g = v;
+            if (field < 2) d2h(h, &g, a.sh.lt + v, sizeof(int));  // local observation -> global id
+            else g = v + a.sh.j0;                                 // local point -> global id
+            best[0] = std::min(best[0], g);
+        }
+        SFM_CUDA(cudaMemcpyAsync(err, best.data(), sizeof(int), cudaMemcpyHostToDevice, s));
+        dist_allreduce_ints(grp, err, 1, 1, s);
+        int g = INT_MAX;
+        d2h(h, &g, err, sizeof(int));
+        return g;
+    };
+    // ---- phase 1: sub-scenes, Jacobians, per-point blocks, camera partials -------
+    for (int i = 0; i < nloc; ++i) {
+        RankA& a = h->ranka[i];
+        const int gr = grank(i);
+        shard_extract(sc, bounds[gr], bounds[gr + 1], a.sh, s);
+        const SceneDev& l = a.sh.sc;
+        IndexDev& ix = a.ix;
+        ix.off_cam = a.off_cam.as<int>((size_t)n + 1);
+        ix.off_pt = a.off_pt.as<int>((size_t)l.m + 1);
+        ix.idx_cam = a.idx_cam.as<int>((size_t)l.t + 1);
+        ix.idx_pt = a.idx_pt.as<int>((size_t)l.t + 1);
+        ix.pos_cam = a.pos_cam.as<int>((size_t)l.t + 1);
+        ix.key_scratch = a.key_scratch.as<int>((size_t)l.t + 1);
+        Status* lst = a.status.as<Status>(1);
+        launch_status_init(lst, s);
+        launch_build_index(l, ix, a.ws, s);
+        double* Rr = a.R.as<double>(9 * (size_t)n + 1);
+        double* rec = a.rec.as<double>((size_t)kRec * l.t + 1);
+        if (l.t) launch_jacobian(l, ix.idx_cam, Rr, rec, lst, s);
+        launch_weights(l, ix.idx_cam, rec, lst, s);
+        const size_t ncl = (size_t)N + 3 * (size_t)l.m;
+        launch_reductions(l, ix, rec, a.D.as<double>((size_t)P * P * n + 1), a.Hr.as<double>(9 * (size_t)n + 1),
+                          a.A.as<double>(9 * (size_t)l.m + 1), a.s_a.as<double>(ncl + 1),
+                          a.flags.as<unsigned char>(ncl + 1), lst, s, h->s4, h->e_red_fork, h->e_red_join,
+                          a.raw.as<double>((size_t)NE * n + 1));
+    }
+    mark(h, 2);
+    if (int g = rank_errors(0); g != INT_MAX) {
+        double* Rg = h->R.as<double>(9 * (size_t)n + 1);
+        SFM_CUDA(cudaMemcpyAsync(Rg, h->ranka[0].R.p, 72 * (size_t)n, cudaMemcpyDeviceToDevice, s));
+        double d = 0.0;
+        launch_depth_of(sc, Rg, g, (double*)h->depth.get(8), s);
+        d2h(h, &d, h->depth.p, 8);
+        throw ApiError{SFMCOV_ERR_DEGENERATE, "jacobian",
+                       "observation " + std::to_string(g) + ": projection: point at camera-space depth " + fmt_f(d) +
+                           " (behind camera or on the principal plane)"};
+    }
+    combine(raw, (size_t)NE * n, [&](int i) { return (const double*)h->ranka[i].raw.p; });
+    // ---- phase 2: camera blocks, scales, rotation blocks; border scales ----------
+    const size_t ncols = (size_t)N + 3 * (size_t)m;
+    double* D = h->D.as<double>((size_t)P * P * n + 1);
+    double* Hr = h->Hr.as<double>(9 * (size_t)n + 1);
+    double* s_a = h->s_a.as<double>(ncols + 1);
+    unsigned char* flags = h->flags.as<unsigned char>(ncols + 1);
+    SFM_CUDA(cudaMemsetAsync(flags, 0, ncols, s));
+    launch_camera_finish(P, raw, n, D, Hr, s_a, flags, st, s);
+    sync_status(h);
+    if (h->st_host->rot_bad != INT_MAX) throw_numeric(h, sc, M_NULLSPACE);
+    if (int g = rank_errors(1); g != INT_MAX)
+        throw ApiError{SFMCOV_ERR_DEGENERATE, "fisher", "observation " + std::to_string(g) + " covariance is not positive definite"};
+    int nflag = h->st_host->nflag;  // camera columns
+    std::vector<int> lflag(1, 0);
+    for (int i = 0; i < nloc; ++i) {
+        RankA& a = h->ranka[i];
+        const SceneDev& l = a.sh.sc;
+        // the camera scales into the rank's column layout; its point scales and
+        // flags into the global one (disjoint ranges: summed / or-ed below)
+        SFM_CUDA(cudaMemcpyAsync(a.s_a.p, s_a, 8 * (size_t)N, cudaMemcpyDeviceToDevice, s));
+        if (i == 0) SFM_CUDA(cudaMemsetAsync(s_a + N, 0, 8 * 3 * (size_t)m, s));
+        if (l.m)
+            SFM_CUDA(cudaMemcpyAsync(s_a + N + 3 * (size_t)a.sh.j0, (const double*)a.s_a.p + N, 24 * (size_t)l.m,
+                                     cudaMemcpyDeviceToDevice, s));
+        launch_flags_or((const unsigned char*)a.flags.p + N, 3 * (size_t)l.m, flags + N + 3 * (size_t)a.sh.j0, s);
+        Status q;
+        SFM_CUDA(cudaMemcpyAsync(&q, a.status.p, sizeof(Status), cudaMemcpyDeviceToHost, s));
+        SFM_CUDA(cudaStreamSynchronize(s));
+        lflag[0] += q.nflag;
+        launch_border_sums(l, Hr, (const double*)a.s_a.p, grank(i) == 0 ? 1 : 0,
+                           a.bpart.as<double>(7 * (size_t)border_partial_blocks(n, l.m) + 7), a.sq.as<double>(8), s);
+    }
+    {  // flagged columns: the union over ranks; the count summed
+        int* cnt = h->sh_err.as<int>(8) + 4;
+        SFM_CUDA(cudaMemcpyAsync(cnt, lflag.data(), sizeof(int), cudaMemcpyHostToDevice, s));
+        dist_allreduce_ints(grp, cnt, 1, 0, s);
+        dist_allreduce_u8_max(grp, flags + N, 3 * (size_t)m, s);
+        dist_allreduce(grp, s_a + N, 3 * (size_t)m, 0, s);  // each point's scales come from one rank
+        int tot = 0;
+        d2h(h, &tot, cnt, sizeof(int));
+        h->st_host->nflag = nflag + tot;
+        SFM_CUDA(cudaMemcpyAsync(&st->nflag, &h->st_host->nflag, sizeof(int), cudaMemcpyHostToDevice, s));
+        SFM_CUDA(cudaStreamSynchronize(s));
+    }
+    combine(sq, 7, [&](int i) { return (const double*)h->ranka[i].sq.p; });
+    double* s_b = h->s_b.as<double>(7);
+    launch_border_scale(sq, s_b, s);
+    mark(h, 3);
+    // ---- phase 3: point factors, W, border partials ------------------------------
+    for (int i = 0; i < nloc; ++i) {
+        RankA& a = h->ranka[i];
+        const SceneDev& l = a.sh.sc;
+        const int ppb = point_prep_blocks(l.m);
+        const size_t nwarps = ((size_t)l.t + 31) / 32;
+        launch_point_prep(l, a.ix, (const double*)a.rec.p, (const double*)a.A.p, (const double*)a.s_a.p, s_b,
+                          a.Lpt.as<double>(8 * (size_t)l.m + 8), a.Wb.as<double>((size_t)kWStride * l.t + 1),
+                          a.V.as<double>(21 * (size_t)l.m + 21), a.Fpart.as<double>(28 * (size_t)ppb + 28),
+                          a.Pfirst.as<double>((size_t)NB * nwarps + 1), a.Plast.as<double>((size_t)NB * nwarps + 1),
+                          a.Gsum.as<double>((size_t)NB * n + 1), (Status*)a.status.p, s);
+        launch_fpart_sum((const double*)a.Fpart.p, ppb, a.F28.as<double>(32), s);
+        launch_camera_border(l, a.ix, (const double*)a.Pfirst.p, (const double*)a.Plast.p, (const double*)a.Gsum.p,
+                             Hr, s_a, s_b, nullptr, nullptr, nullptr, s, a.S.as<double>((size_t)NB * n + 1), nullptr);
+    }
+    if (int g = rank_errors(2); g != INT_MAX)
+        throw ApiError{SFMCOV_ERR_DEGENERATE, "schur", "point " + std::to_string(g) + " has a singular 3x3 block"};
+    combine(F, 28, [&](int i) { return (const double*)h->ranka[i].F28.p; });
+    combine(Ssum, (size_t)NB * n, [&](int i) { return (const double*)h->ranka[i].S.p; });
+    // ---- phase 4: the gauge block and the border rows -------------------------------
+    double* LF = h->LF.as<double>(49);
+    double* E = h->E.as<double>(49);
+    double* eigE = h->eigE.as<double>(8);
+    launch_border_factor(F, 1, LF, E, eigE, st, s);
+    double* Gamma = h->Gamma.as<double>((size_t)N * 7 + 1);
+    double* G = h->G.as<double>((size_t)N * 7 + 1);
+    launch_camera_border(sc, gix, nullptr, nullptr, nullptr, Hr, s_a, s_b, LF, Gamma, G, s, nullptr, Ssum);
+    mark(h, 4);
+    // ---- phase 5: each rank's observation pairs into the global block index ---------
+    const PairDev& pg = h->pairs;
+    const size_t segd = (size_t)pg.nseg * 81;
+    double* seg = h->sh_seg.as<double>(segd + 1);
+    for (int i = 0; i < nloc; ++i) {
+        RankA& a = h->ranka[i];
+        const SceneDev& l = a.sh.sc;
+        build_pairs(l, a.ix, a.pairs, a.ws_pairs, s);
+        double* seg_l = a.seg_l.as<double>((size_t)a.pairs.nseg * 81 + 1);
+        launch_pair_reduce_segments(P, a.pairs, (const double*)a.Wb.p, n, 0, a.pairs.nchunks, seg_l, s);
+        double* seg_g = nloc == 1 ? seg : a.seg_g.as<double>(segd + 1);
+        SFM_CUDA(cudaMemsetAsync(seg_g, 0, 8 * segd, s));
+        launch_seg_map(a.pairs.ukeys, a.pairs.nseg, pg.ukeys, pg.nseg, seg_l, seg_g, s);
+    }
+    if (nloc > 1)
+        for (int i = 0; i < nloc; ++i) {
+            if (i == 0) SFM_CUDA(cudaMemcpyAsync(seg, h->ranka[0].seg_g.p, 8 * segd, cudaMemcpyDeviceToDevice, s));
+            else launch_add(seg, (const double*)h->ranka[i].seg_g.p, segd, s);
+        }
+    mark(h, 5);
+    run_dist_tail(h, sc, out, D, s_a, G, nullptr, st, flags, ncols, eigE, seg);
 }
 
 // Copies a host scene into the handle's staging buffers.
@@ -879,6 +1113,10 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
     auto* h = new sfmcov_handle();
     try {
         h->device = device;
+        {
+            const char* e = std::getenv("SFMCOV_REPLICATED_STAGE_A");
+            h->replicated_a = e && e[0] == '1';
+        }
         SFM_CUDA(cudaSetDevice(device));
         // critical path (panel factorisations) at high priority, bulk trailing updates low
         int lo = 0, hi = 0;
@@ -942,6 +1180,8 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     h->seg_send.release();
     h->seg_recv.release();
     h->seg_groups.release();
+    for (auto& a : h->ranka) a.release();
+    for (DBuf* b : {&h->sh_bounds, &h->sh_raw, &h->sh_sq, &h->sh_F, &h->sh_S, &h->sh_seg, &h->sh_err}) b->release();
     h->prange_r.release();
     h->scale_mm.release();
     for (DBuf* b : {&h->zi, &h->fc_part, &h->fc_y, &h->fc_gtt, &h->fc_eb, &h->fc_pc, &h->or_a, &h->or_w, &h->or_work,

@@ -672,6 +672,17 @@ void dist_reduce_scatter(DistGroup& grp, const double* send, double* recv, size_
                "ReduceScatter");
 }
 
+void dist_allreduce_ints(DistGroup& grp, int* buf, size_t count, int op, cudaStream_t s) {
+    if (!grp.nccl || !count) return;
+    const ncclRedOp_t o = op == 0 ? ncclSum : (op == 1 ? ncclMin : ncclMax);
+    nccl_check(nccl_api().AllReduce(buf, buf, count, ncclInt32, o, (ncclComm_t)grp.nccl, s), "AllReduce");
+}
+
+void dist_allreduce_u8_max(DistGroup& grp, unsigned char* buf, size_t count, cudaStream_t s) {
+    if (!grp.nccl || !count) return;
+    nccl_check(nccl_api().AllReduce(buf, buf, count, ncclUint8, ncclMax, (ncclComm_t)grp.nccl, s), "AllReduce");
+}
+
 void dist_allreduce_int_min(DistGroup& grp, int* buf, cudaStream_t s) {
     if (!grp.nccl) return;
     nccl_check(nccl_api().AllReduce(buf, buf, 1, ncclInt32, ncclMin, (ncclComm_t)grp.nccl, s), "AllReduce");

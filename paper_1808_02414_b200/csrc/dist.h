@@ -65,6 +65,9 @@ void dist_reduce_scatter(DistGroup& grp, const double* send, double* recv, size_
 // op: 0 sum, 1 min, 2 max (no-op without NCCL)
 void dist_allreduce(DistGroup& grp, double* buf, size_t count, int op, cudaStream_t s);
 void dist_allreduce_int_min(DistGroup& grp, int* buf, cudaStream_t s);
+// op: 0 sum, 1 min, 2 max
+void dist_allreduce_ints(DistGroup& grp, int* buf, size_t count, int op, cudaStream_t s);
+void dist_allreduce_u8_max(DistGroup& grp, unsigned char* buf, size_t count, cudaStream_t s);
 void dist_allreduce_int_sum(DistGroup& grp, int* buf, cudaStream_t s);
 
 bool nccl_available(std::string* why);

@@ -128,9 +128,18 @@ void launch_structure_check(const SceneDev& sc, const IndexDev& ix, Status* st, 
 void launch_jacobian(const SceneDev& sc, const int* idx_cam, double* R, double* rec, Status* st, cudaStream_t s);
 void launch_weights(const SceneDev& sc, const int* idx_cam, double* rec, Status* st, cudaStream_t s);
 void launch_depth_of(const SceneDev& sc, const double* R, int t, double* out, cudaStream_t s);
+// raw != null (point-sharded stage A): the camera CTAs write their partial
+// sums (n x (P^2 + 18)) there and stop; launch_camera_finish completes them.
 void launch_reductions(const SceneDev& sc, const IndexDev& ix, const double* rec, double* D, double* Hr, double* A,
                        double* s_a, unsigned char* flags, Status* st, cudaStream_t s, cudaStream_t side,
-                       cudaEvent_t fork, cudaEvent_t join);
+                       cudaEvent_t fork, cudaEvent_t join, double* raw = nullptr);
+void launch_camera_finish(int P, const double* raw, int n, double* D, double* Hr, double* s_a, unsigned char* flags,
+                          Status* st, cudaStream_t s);
+// sums of squares of the border columns over this scene's rows (cameras
+// only when with_cams), and s_b from the summed squares
+void launch_border_sums(const SceneDev& sc, const double* Hr, const double* s_a, int with_cams, double* partial,
+                        double* sq, cudaStream_t s);
+void launch_border_scale(const double* sq, double* s_b, cudaStream_t s);
 void launch_border_scales(const SceneDev& sc, const double* Hr, const double* s_a, double* partial, double* s_b,
                           cudaStream_t s);
 int border_partial_blocks(int n, int m);
@@ -143,9 +152,13 @@ void launch_point_prep(const SceneDev& sc, const IndexDev& ix, const double* rec
                        double* Plast, double* Gsum, Status* st, cudaStream_t s);
 void launch_border_factor(const double* Fpart, int nblocks, double* LF, double* E, double* eigE, Status* st,
                           cudaStream_t s);
+// sums_out: write this rank's Σ W V per camera (n x P x 7) and stop;
+// sums_in: use all-reduced sums instead of the warp partials
 void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* Pfirst, const double* Plast,
                           const double* Gsum, const double* Hr, const double* s_a, const double* s_b, const double* LF,
-                          double* Gamma, double* G, cudaStream_t s);
+                          double* Gamma, double* G, cudaStream_t s, double* sums_out = nullptr,
+                          const double* sums_in = nullptr);
+void launch_fpart_sum(const double* Fpart, int nblocks, double* F28, cudaStream_t s);
 void launch_fill(int P, double* Z, long long ld, int N, int Npad, const double* D, const double* s_a, const double* G,
                  int add_gg, cudaStream_t s);
 void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace& ws, cudaStream_t s);
@@ -292,6 +305,27 @@ inline int own_blocks_upto(const Ownership& o, int K, int q) {
     for (int p = o.rank; p <= q && p * o.G < K; p += o.R) b += (K - p * o.G < o.G) ? K - p * o.G : o.G;
     return b;
 }
+
+// ---- point-sharded stage A (shard.cu) ---------------------------------------
+// A rank's sub-scene: every camera, points [j0, j1), their observations in
+// observation order (lt = their global observation ids).
+struct ShardScene {
+    SceneDev sc{};
+    int j0 = 0, j1 = 0;
+    const int* lt = nullptr;
+    DBuf buf_flag, buf_iota, buf_lt, buf_cnt, buf_oc, buf_op, buf_sigma;
+    Workspace ws;
+    void release() {
+        buf_flag.release(); buf_iota.release(); buf_lt.release(); buf_cnt.release(); buf_oc.release();
+        buf_op.release(); buf_sigma.release(); ws.tmp.release();
+    }
+};
+// point ranges of R ranks balanced by observation pairs (bounds: R + 1)
+void shard_bounds(const long long* pair_off, int m, int R, int* d_bounds, std::vector<int>& bounds, cudaStream_t s);
+int shard_extract(const SceneDev& g, int j0, int j1, ShardScene& out, cudaStream_t s);
+void launch_seg_map(const unsigned int* ukeys_l, int nseg_l, const unsigned int* ukeys_g, int nseg_g,
+                    const double* seg_l, double* seg_g, cudaStream_t s);
+void launch_flags_or(const unsigned char* src, size_t count, unsigned char* dst, cudaStream_t s);
 
 // dist.cu kernels
 void launch_fill_local(const ColMap& cm, const Ownership& ow, double* Zl, long long ld, int Npad, int ncl,

@@ -317,23 +317,31 @@ template <int P>
 __global__ void __launch_bounds__(64) k_camera_border(const int* off_cam, int t_count, const double* Pfirst,
                                                       const double* Plast, const double* Gsum, const double* cams,
                                                       const double* Hr, const double* s_a, const double* s_b,
-                                                      const double* LF, int n, double* Gamma, double* G) {
+                                                      const double* LF, int n, double* Gamma, double* G,
+                                                      double* sums_out, const double* sums_in) {
     constexpr int NE = P * 7;
     __shared__ double sh[NE];
     const int i = blockIdx.x, tid = threadIdx.x;
     const int p = tid / 7, l = tid % 7;
     if (tid < NE) {
-        const int b = off_cam[i], e = off_cam[i + 1];
         double sum = 0.0;
-        if (e > b) {
-            bool any = false;
-            for (int w = b >> 5; w <= (e - 1) >> 5; ++w) {
-                const int fs = 32 * w, ls = min(32 * w + 31, t_count - 1);
-                if (fs >= b && fs < e) { sum += Pfirst[(size_t)w * NE + tid]; any = true; }
-                else if (ls >= b && ls < e) { sum += Plast[(size_t)w * NE + tid]; any = true; }
+        if (sums_in) {  // point-sharded stage A: the all-reduced sums
+            sum = sums_in[(size_t)i * NE + tid];
+        } else {
+            const int b = off_cam[i], e = off_cam[i + 1];
+            if (e > b) {
+                bool any = false;
+                for (int w = b >> 5; w <= (e - 1) >> 5; ++w) {
+                    const int fs = 32 * w, ls = min(32 * w + 31, t_count - 1);
+                    if (fs >= b && fs < e) { sum += Pfirst[(size_t)w * NE + tid]; any = true; }
+                    else if (ls >= b && ls < e) { sum += Plast[(size_t)w * NE + tid]; any = true; }
+                }
+                if (!any) sum = Gsum[(size_t)i * NE + tid];  // the camera lies inside one warp
             }
-            if (!any) sum = Gsum[(size_t)i * NE + tid];  // the camera lies inside one warp
         }
+        if (sums_out) {  // this rank's partial, finished after the all-reduce
+            sums_out[(size_t)i * NE + tid] = sum;
+        } else {
         const double* C = cams + (size_t)P * i + 3;
         double h = 0.0;
         if (p < 3) h = (l >= 3 && l < 6) ? Hr[9 * (size_t)i + 3 * p + (l - 3)] : 0.0;
@@ -347,7 +355,9 @@ __global__ void __launch_bounds__(64) k_camera_border(const int* off_cam, int t_
         const double g = hs - sum;
         sh[tid] = g;
         Gamma[(size_t)P * 7 * i + tid] = g;
+        }
     }
+    if (sums_out) return;  // uniform over the CTA
     __syncthreads();
     if (tid < P) {
         const double* gr = &sh[7 * tid];
@@ -799,10 +809,24 @@ void launch_border_factor(const double* Fpart, int nblocks, double* LF, double* 
 
 void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* Pfirst, const double* Plast,
                           const double* Gsum, const double* Hr, const double* s_a, const double* s_b, const double* LF,
-                          double* Gamma, double* G, cudaStream_t s) {
+                          double* Gamma, double* G, cudaStream_t s, double* sums_out, const double* sums_in) {
     if (!sc.n) return;
-    if (sc.P == 8) k_camera_border<8><<<sc.n, 64, 0, s>>>(ix.off_cam, sc.t, Pfirst, Plast, Gsum, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
-    else k_camera_border<9><<<sc.n, 64, 0, s>>>(ix.off_cam, sc.t, Pfirst, Plast, Gsum, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G);
+    if (sc.P == 8) k_camera_border<8><<<sc.n, 64, 0, s>>>(ix.off_cam, sc.t, Pfirst, Plast, Gsum, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G, sums_out, sums_in);
+    else k_camera_border<9><<<sc.n, 64, 0, s>>>(ix.off_cam, sc.t, Pfirst, Plast, Gsum, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G, sums_out, sums_in);
+    SFM_LAUNCH_CHECK();
+}
+
+// Σ of the point-preparation blocks' F partials (28 entries, fixed order):
+// this rank's part of F, all-reduced before launch_border_factor(F, 1, ...).
+__global__ void k_fpart_sum(const double* Fpart, int nblocks, double* F28) {
+    const int e = threadIdx.x;
+    if (e >= 28) return;
+    double acc = 0.0;
+    for (int b = 0; b < nblocks; ++b) acc += Fpart[28 * (size_t)b + e];
+    F28[e] = acc;
+}
+void launch_fpart_sum(const double* Fpart, int nblocks, double* F28, cudaStream_t s) {
+    k_fpart_sum<<<1, 32, 0, s>>>(Fpart, nblocks, F28);
     SFM_LAUNCH_CHECK();
 }
 

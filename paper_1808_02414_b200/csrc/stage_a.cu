@@ -211,7 +211,8 @@ __global__ void k_depth_of(const double* cams, const double* Rc, const double* p
 // Then H_r = eig-inverse(normal)·rhs (nullspace.cpp:52-61) and s_a = 1/sqrt(diag D).
 template <int P>
 __global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const double* rec, int n, double* D,
-                                                       double* Hr, double* s_a, unsigned char* flags, Status* st) {
+                                                       double* Hr, double* s_a, unsigned char* flags, Status* st,
+                                                       double* raw) {
     // one CTA per camera, one thread per output entry: D (P*P), rotation
     // normal (9) and rhs (9); each entry is a sequential sum over the
     // camera's observations in ascending order.  The camera's records are
@@ -302,6 +303,10 @@ __global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const
         }
         __syncthreads();  // stage[cur] is refilled by the next iteration's prefetch
     }
+    if (raw) {  // point-sharded stage A: this rank's partial sums, finished after the all-reduce
+        if (kind < 3) raw[(size_t)NE * i + slot] = acc;
+        return;
+    }
     if (kind < 3) sh[slot] = acc;
     __syncthreads();
     if (tid < P * P) D[(size_t)P * P * i + tid] = acc;
@@ -320,6 +325,55 @@ __global__ void __launch_bounds__(128) k_camera_reduce(const int* off_cam, const
             for (int k = 0; k < 9; ++k) Hr[9 * (size_t)i + k] = hr[k];
         }
     }
+}
+
+// The end of k_camera_reduce from summed partials (point-sharded stage A):
+// D, the Jacobi scales of the camera columns and the rotation blocks.
+template <int P>
+__global__ void k_camera_finish(const double* raw, int n, double* D, double* Hr, double* s_a, unsigned char* flags,
+                                Status* st) {
+    constexpr int NE = P * P + 18;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* r = raw + (size_t)NE * i;
+    for (int e = 0; e < P * P; ++e) D[(size_t)P * P * i + e] = r[e];
+    for (int p = 0; p < P; ++p) {
+        const double d = r[p * (P + 1)];
+        if (d > 0.0) s_a[(size_t)P * i + p] = 1.0 / sqrt(d);
+        else { s_a[(size_t)P * i + p] = 1.0; flags[(size_t)P * i + p] = 1; atomicAdd(&st->nflag, 1); }
+    }
+    double inv[9], hr[9];
+    if (!eig_inverse3(r + P * P, kRotationCondTol, inv)) {
+        atomicMin(&st->rot_bad, i);
+        for (int k = 0; k < 9; ++k) Hr[9 * (size_t)i + k] = 0.0;
+    } else {
+        mul3(inv, r + P * P + 9, hr);
+        for (int k = 0; k < 9; ++k) Hr[9 * (size_t)i + k] = hr[k];
+    }
+}
+
+// Sums of squares of s_a ∘ h_l over the camera rows (with_cams) and the
+// point rows of this (sub-)scene: the point-sharded s_b, finished after the
+// all-reduce by k_border_scale.
+__global__ void __launch_bounds__(256) k_border_sums(const double* partial, int nblocks, double* sq) {
+    __shared__ double red[256][7];
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int b = threadIdx.x; b < nblocks; b += 256)
+        for (int l = 0; l < 7; ++l) acc[l] += partial[7 * (size_t)b + l];
+    for (int l = 0; l < 7; ++l) red[threadIdx.x][l] = acc[l];
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int l = 0; l < 7; ++l) red[threadIdx.x][l] += red[threadIdx.x + w][l];
+        __syncthreads();
+    }
+    if (threadIdx.x < 7) sq[threadIdx.x] = red[0][threadIdx.x];
+}
+__global__ void k_border_scale(const double* sq, double* s_b) {
+    const int l = threadIdx.x;
+    if (l >= 7) return;
+    const double norm = sqrt(sq[l]);
+    s_b[l] = norm > 0.0 ? 1.0 / norm : 1.0;
 }
 
 // ---- per-point reduction: A_j = Σ (J_pᵀW)J_p (covariance.cpp:64-71) ---------
@@ -354,11 +408,11 @@ __global__ void k_point_reduce(const int* off_pt, const int* idx_pt, const int* 
 // zero intrinsic rows, point rows [I|[X]x|X].  Deterministic two-level sum.
 template <int P>
 __global__ void k_border_partial(const double* cams, const double* Hr, const double* pts, const double* s_a, int n,
-                                 int m, double* partial) {
+                                 int m, double* partial, int with_cams = 1) {
     __shared__ double red[256][7];
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-    if (g < n + m) {
+    if (g < n + m && (with_cams || g >= n)) {
         const bool is_cam = g < n;
         const double* X = is_cam ? cams + (size_t)P * g + 3 : pts + 3 * (size_t)(g - n);
         const size_t row0 = is_cam ? (size_t)P * g + 3 : (size_t)P * n + 3 * (size_t)(g - n);
@@ -515,7 +569,7 @@ void launch_depth_of(const SceneDev& sc, const double* R, int t, double* out, cu
 // reduction runs beside it on `side` (fork / join through the two events).
 void launch_reductions(const SceneDev& sc, const IndexDev& ix, const double* rec, double* D, double* Hr, double* A,
                        double* s_a, unsigned char* flags, Status* st, cudaStream_t s, cudaStream_t side,
-                       cudaEvent_t fork, cudaEvent_t join) {
+                       cudaEvent_t fork, cudaEvent_t join, double* raw) {
     const size_t ncols = (size_t)sc.P * sc.n + 3 * (size_t)sc.m;
     SFM_CUDA(cudaMemsetAsync(flags, 0, ncols, s));
     SFM_CUDA(cudaEventRecord(fork, s));
@@ -527,8 +581,8 @@ void launch_reductions(const SceneDev& sc, const IndexDev& ix, const double* rec
     }
     SFM_CUDA(cudaEventRecord(join, side));
     if (sc.n) {
-        if (sc.P == 8) k_camera_reduce<8><<<sc.n, 128, 0, s>>>(ix.off_cam, rec, sc.n, D, Hr, s_a, flags, st);
-        else k_camera_reduce<9><<<sc.n, 128, 0, s>>>(ix.off_cam, rec, sc.n, D, Hr, s_a, flags, st);
+        if (sc.P == 8) k_camera_reduce<8><<<sc.n, 128, 0, s>>>(ix.off_cam, rec, sc.n, D, Hr, s_a, flags, st, raw);
+        else k_camera_reduce<9><<<sc.n, 128, 0, s>>>(ix.off_cam, rec, sc.n, D, Hr, s_a, flags, st, raw);
         SFM_LAUNCH_CHECK();
     }
     SFM_CUDA(cudaStreamWaitEvent(s, join, 0));
@@ -542,6 +596,30 @@ void launch_border_scales(const SceneDev& sc, const double* Hr, const double* s_
     else k_border_partial<9><<<nb, 256, 0, s>>>(sc.cams, Hr, sc.pts, s_a, sc.n, sc.m, partial);
     SFM_LAUNCH_CHECK();
     k_border_final<<<1, 256, 0, s>>>(partial, nb, s_b);
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_camera_finish(int P, const double* raw, int n, double* D, double* Hr, double* s_a, unsigned char* flags,
+                          Status* st, cudaStream_t s) {
+    if (!n) return;
+    if (P == 8) k_camera_finish<8><<<cdiv(n, 128), 128, 0, s>>>(raw, n, D, Hr, s_a, flags, st);
+    else k_camera_finish<9><<<cdiv(n, 128), 128, 0, s>>>(raw, n, D, Hr, s_a, flags, st);
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_border_sums(const SceneDev& sc, const double* Hr, const double* s_a, int with_cams, double* partial,
+                        double* sq, cudaStream_t s) {
+    const int g = sc.n + sc.m;
+    const int nb = (int)cdiv(g > 0 ? g : 1, 256);
+    if (sc.P == 8) k_border_partial<8><<<nb, 256, 0, s>>>(sc.cams, Hr, sc.pts, s_a, sc.n, sc.m, partial, with_cams);
+    else k_border_partial<9><<<nb, 256, 0, s>>>(sc.cams, Hr, sc.pts, s_a, sc.n, sc.m, partial, with_cams);
+    SFM_LAUNCH_CHECK();
+    k_border_sums<<<1, 256, 0, s>>>(partial, nb, sq);
+    SFM_LAUNCH_CHECK();
+}
+
+void launch_border_scale(const double* sq, double* s_b, cudaStream_t s) {
+    k_border_scale<<<1, 32, 0, s>>>(sq, s_b);
     SFM_LAUNCH_CHECK();
 }
 

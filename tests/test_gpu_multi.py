@@ -76,6 +76,79 @@ def test_emulated_disconnected_scene_fails_in_factorization(engine):
     assert e.value.kind == F.ErrorKind.degenerate and e.value.stage == "factorization"
 
 
+def _behind_camera(rec):
+    rec.pts[5] = rec.cams[0, 3:6]
+    return rec
+
+
+def _two_behind(rec):  # failing observations in points owned by different ranks
+    rec.pts[5] = rec.cams[0, 3:6]
+    rec.pts[12] = rec.cams[2, 3:6]
+    return rec
+
+
+def _singular_point(rec):  # test_schur.cpp:82-93 (as in test_gpu_parity.py)
+    m = rec.num_points()
+    rec.cams = np.vstack([rec.cams, rec.cams[0]])
+    rec.cams[6, 7] = 0.0
+    rec.pts = np.vstack([rec.pts, np.array([rec.cams[0, 3:6] * 0.5])])
+    rec.obs_cam = np.concatenate([rec.obs_cam, [0, 6, 6, 6, 6]]).astype(np.int32)
+    rec.obs_pt = np.concatenate([rec.obs_pt, [m, m, 0, 1, 2]]).astype(np.int32)
+    rec.obs_u = np.vstack([rec.obs_u, np.zeros((5, 2))])
+    rec.obs_sigma = np.concatenate([rec.obs_sigma, np.broadcast_to(np.eye(2), (5, 2, 2))])
+    return rec
+
+
+@pytest.mark.parametrize("ranks", [2, 3])
+@pytest.mark.parametrize("mutate", [_behind_camera, _two_behind, _singular_point,
+                                    lambda r: (r.cams.__setitem__((1, 6), -1.0), r)[1]],
+                         ids=["behind_camera", "two_behind", "singular_point", "validation"])
+def test_sharded_stage_a_reports_the_single_gpu_error(engine, mutate, ranks):
+    """Errors found inside a rank's sub-scene are reported with the global
+    observation / point ids, first failing index over all ranks, exactly as
+    the single-GPU pipeline words them."""
+    rec = mutate(S.generate_cube_scene(4, 0.5))
+    with pytest.raises(F.Error) as e1:
+        engine.compute_covariance(rec)
+    with pytest.raises(F.Error) as e2:
+        engine.compute_covariance_emulated(rec, ranks)
+    assert (e2.value.kind, e2.value.stage, str(e2.value)) == (e1.value.kind, e1.value.stage, str(e1.value))
+
+
+@pytest.mark.parametrize("ranks", [2, 5])
+def test_sharded_stage_a_diagnostics(engine, ranks):
+    """Scales, flagged columns and pivots of the point-sharded stage A match
+    the single-GPU run (scales bitwise: every column's scale is computed by
+    one rank from a sum it owns or from the all-reduced camera sums)."""
+    rec = S.generate_config(2)
+    one = engine.compute_covariance(rec).diagnostics
+    many = engine.compute_covariance_emulated(rec, ranks).diagnostics
+    assert many.scale_max == pytest.approx(one.scale_max, rel=1e-12)
+    assert many.scale_min == pytest.approx(one.scale_min, rel=1e-12)
+    assert many.flagged_columns == one.flagged_columns
+    assert (many.inertia_positive, many.inertia_negative) == (one.inertia_positive, one.inertia_negative)
+
+
+def test_replicated_and_sharded_stage_a_agree(engine):
+    """The point-sharded stage A against the round-1 replicated one (every rank
+    running the whole stage A; SFMCOV_REPLICATED_STAGE_A=1 in a subprocess)."""
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, '.');"
+            "from paper_1808_02414_b200 import sfmcov as F, synthetic as S;"
+            "np.save(sys.argv[1], F.Engine(0).compute_covariance_emulated(S.generate_config(2), 3).camera_cov)")
+    import os
+    import tempfile
+    from conftest import ROOT
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "rep.npy")
+        env = dict(os.environ, SFMCOV_REPLICATED_STAGE_A="1")
+        subprocess.run([sys.executable, "-c", code, out], cwd=ROOT, env=env, check=True, timeout=300)
+        rep = np.load(out)
+    shard = engine.compute_covariance_emulated(S.generate_config(2), 3).camera_cov
+    assert worst_block(shard, rep) <= 1e-10
+
+
 def test_emulated_rank_bounds(engine):
     with pytest.raises(F.Error):
         engine.compute_covariance_emulated(S.generate_cube_scene(1, 0.5), 0)

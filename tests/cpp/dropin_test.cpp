@@ -450,9 +450,13 @@ int main() {
     {  // covariance IO round trip (covariance_io.hpp)
         save_covariance_json(result, "/tmp/sfmcov_dropin_cov.json");
         const CovarianceResult back = load_covariance_json("/tmp/sfmcov_dropin_cov.json");
-        CHECK(back.camera_cov == result.camera_cov);
+        // the file holds the upper triangles (blocks are symmetric to the last bit, not bitwise)
+        CHECK(back.camera_cov.size() == result.camera_cov.size());
+        for (size_t i = 0; i < back.camera_cov.size(); ++i)
+            CHECK(pack_upper_triangle(back.camera_cov[i]) == pack_upper_triangle(result.camera_cov[i]));
         CHECK(back.diagnostics.inertia_negative == 7 && back.diagnostics.min_pivot == d.min_pivot);
-        CHECK(unpack_upper_triangle(pack_upper_triangle(result.camera_cov[0])) == result.camera_cov[0]);
+        const auto tri = pack_upper_triangle(result.camera_cov[0]);
+        CHECK(pack_upper_triangle(unpack_upper_triangle(tri)) == tri);
         save_covariance_csv(result, "/tmp/sfmcov_dropin_cov.csv");
         std::remove("/tmp/sfmcov_dropin_cov.json");
         std::remove("/tmp/sfmcov_dropin_cov.csv");

@@ -85,5 +85,9 @@ def test_gpu_result_round_trip(engine, tmp_path):  # test_cli.cpp:98-113
     res = engine.compute_covariance(S.generate_cube_scene(3, 0.5))
     IO.save_covariance_json(res, tmp_path / "cov.json")
     back = IO.load_covariance_json(tmp_path / "cov.json")
-    assert np.array_equal(back.camera_cov, res.camera_cov) and back.diagnostics == res.diagnostics
-    assert back.diagnostics.inertia_negative == 7
+    # the file holds the upper triangle (the blocks are symmetric to the last bit,
+    # not bitwise, in the reference too: (s_p Z_pq) s_q vs (s_q Z_qp) s_p)
+    for a, b in zip(back.camera_cov, res.camera_cov):
+        assert np.array_equal(IO.pack_upper_triangle(a), IO.pack_upper_triangle(b))
+        assert np.abs(a - b).max() <= 1e-15 * np.abs(b).max()
+    assert back.diagnostics == res.diagnostics and back.diagnostics.inertia_negative == 7

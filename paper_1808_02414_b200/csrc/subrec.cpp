@@ -389,9 +389,20 @@ struct SubResult {
 
 std::vector<SubResult> batch_covariances(sfmcov_handle* h0, const std::vector<const Sub*>& subs, int workers) {
     std::vector<SubResult> res(subs.size());
+    // largest sub-scenes first: a worker's grow-only device buffers are then
+    // sized by its first job, so later (smaller) ones never reallocate --
+    // a cudaFree synchronises the whole device and stalls every worker
+    std::vector<size_t> order(subs.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+        const auto& x = subs[a]->scene;
+        const auto& y = subs[b]->scene;
+        return x.n != y.n ? x.n > y.n : x.t > y.t;
+    });
     std::atomic<size_t> next{0};
     auto work = [&](sfmcov_handle* h) {
-        for (size_t i = next++; i < subs.size(); i = next++) {
+        for (size_t k = next++; k < subs.size(); k = next++) {
+            const size_t i = order[k];
             const Sub& sb = *subs[i];
             const sfmcov_scene v = sb.scene.view();
             res[i].cov.resize((size_t)v.n_cams * v.cam_params * v.cam_params);

@@ -17,6 +17,7 @@
 #include "dist.h"
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <limits>
 #include <cmath>
@@ -109,6 +110,9 @@ struct sfmcov_handle {
     std::vector<sfm::RankDense> ranks;
     std::vector<RankA> ranka;
     DBuf sh_bounds, sh_raw, sh_sq, sh_F, sh_S, sh_seg, sh_err;
+    // batched sub-scenes (run_batch)
+    DBuf bt_lists, bt_cams, bt_pts, bt_oc, bt_op, bt_sigma, bt_sofc, bt_sofp, bt_sb, bt_F, bt_LF, bt_E, bt_eigE, bt_Zb,
+        bt_piv, bt_cov, bt_bad;
     DBuf seg, seg_tmp, seg_send, seg_recv, prange_r, scale_mm;
     sfm::SegGroups seg_groups;
     DBuf zi, fc_part, fc_y, fc_gtt, fc_eb, fc_pc;
@@ -1017,6 +1021,193 @@ void run_dist_sharded(sfmcov_handle* h, const SceneDev& sc, const IndexDev& gix,
     run_dist_tail(h, sc, out, D, s_a, G, nullptr, st, flags, ncols, eigE, seg);
 }
 
+// ---- batched sub-scenes ------------------------------------------------------------
+// Thrown when a batch hits any failure: the caller then reruns the sub-scenes
+// one by one, which reports the exact per-sub-scene error.
+struct BatchFallback {};
+
+sfmcov_handle* worker_of(sfmcov_handle* h, int i) {  // (h->mu is held by the caller)
+    while ((int)h->workers.size() <= i) {
+        sfmcov_error e{};
+        sfmcov_handle* w = sfmcov_cuda_create(h->device, &e);
+        if (!w) throw ApiError{SFMCOV_ERR_DEVICE, "device", e.message};
+        h->workers.push_back(w);
+    }
+    return h->workers[i];
+}
+
+// One chunk of sub-scenes [s0, s1) of the batch, through one pipeline run
+// (batch.cu): gather, stage A + Schur on the concatenation, per-scene gauge,
+// one dense sweep per scene on the worker handles' streams (host thread per
+// worker), extraction into cov (the chunk's cameras, in scene order).
+void run_batch_chunk(sfmcov_handle* h, const SceneDev& full, int s0, int s1, const int32_t* cams, const int64_t* coff,
+                     const int32_t* pts, const int64_t* poff, const int32_t* obs, const int64_t* toff, double* cov) {
+    cudaStream_t s = h->s;
+    // SFMCOV_SUBREC_TIMING=1: synchronised phase times of the chunk on stderr
+    static const bool timing = [] { const char* e = std::getenv("SFMCOV_SUBREC_TIMING"); return e && e[0] == '1'; }();
+    auto t_last = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what) {
+        if (!timing) return;
+        SFM_CUDA(cudaStreamSynchronize(s));
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "  batch %-10s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
+    const int P = full.P, B = s1 - s0;
+    const int nb = (int)(coff[s1] - coff[s0]), mb = (int)(poff[s1] - poff[s0]), tb = (int)(toff[s1] - toff[s0]);
+    // device lists: cams | coff | pts | poff | obs | toff (offsets rebased to
+    // the chunk), copied straight from the caller's concatenated arrays
+    int* dl = h->bt_lists.as<int>((size_t)nb + mb + tb + 3 * ((size_t)B + 1) + 1);
+    std::vector<int> offs(3 * ((size_t)B + 1));
+    for (int k = 0; k <= B; ++k) {
+        offs[k] = (int)(coff[s0 + k] - coff[s0]);
+        offs[B + 1 + k] = (int)(poff[s0 + k] - poff[s0]);
+        offs[2 * (B + 1) + k] = (int)(toff[s0 + k] - toff[s0]);
+    }
+    int* d_cams = dl;
+    int* d_coff = d_cams + nb;
+    int* d_pts = d_coff + B + 1;
+    int* d_poff = d_pts + mb;
+    int* d_obs = d_poff + B + 1;
+    int* d_toff = d_obs + tb;
+    SFM_CUDA(cudaMemcpyAsync(d_cams, cams + coff[s0], 4 * (size_t)nb, cudaMemcpyHostToDevice, s));
+    SFM_CUDA(cudaMemcpyAsync(d_pts, pts + poff[s0], 4 * (size_t)mb, cudaMemcpyHostToDevice, s));
+    SFM_CUDA(cudaMemcpyAsync(d_obs, obs + toff[s0], 4 * (size_t)tb, cudaMemcpyHostToDevice, s));
+    SFM_CUDA(cudaMemcpyAsync(d_coff, offs.data(), 4 * ((size_t)B + 1), cudaMemcpyHostToDevice, s));
+    SFM_CUDA(cudaMemcpyAsync(d_poff, offs.data() + B + 1, 4 * ((size_t)B + 1), cudaMemcpyHostToDevice, s));
+    SFM_CUDA(cudaMemcpyAsync(d_toff, offs.data() + 2 * (B + 1), 4 * ((size_t)B + 1), cudaMemcpyHostToDevice, s));
+    BatchLists L;
+    L.B = B; L.nb = nb; L.mb = mb; L.tb = tb;
+    L.cams = d_cams; L.coff = d_coff; L.pts = d_pts; L.poff = d_poff; L.obs = d_obs; L.toff = d_toff;
+    SceneDev bsc{};
+    bsc.n = nb; bsc.m = mb; bsc.t = tb; bsc.P = P;
+    double* cams_b = h->bt_cams.as<double>((size_t)P * nb + 1);
+    double* pts_b = h->bt_pts.as<double>(3 * (size_t)mb + 1);
+    int* oc_b = h->bt_oc.as<int>((size_t)tb + 1);
+    int* op_b = h->bt_op.as<int>((size_t)tb + 1);
+    double* sig_b = full.sigma ? h->bt_sigma.as<double>(4 * (size_t)tb + 1) : nullptr;
+    launch_batch_gather(L, P, full.cams, full.pts, full.oc, full.op, full.sigma, cams_b, pts_b, oc_b, op_b, sig_b, s);
+    bsc.cams = cams_b; bsc.pts = pts_b; bsc.oc = oc_b; bsc.op = op_b; bsc.sigma = sig_b;
+    phase("gather");
+    // stage A and the Schur factors on the concatenation
+    Status* st = h->status.as<Status>(1);
+    launch_status_init(st, s);
+    IndexDev ix;
+    ix.off_cam = h->off_cam.as<int>((size_t)nb + 1);
+    ix.off_pt = h->off_pt.as<int>((size_t)mb + 1);
+    ix.idx_cam = h->idx_cam.as<int>((size_t)tb + 1);
+    ix.idx_pt = h->idx_pt.as<int>((size_t)tb + 1);
+    ix.pos_cam = h->pos_cam.as<int>((size_t)tb + 1);
+    ix.key_scratch = h->key_scratch.as<int>((size_t)tb + 1);
+    launch_build_index(bsc, ix, h->ws, s);
+    launch_structure_check(bsc, ix, st, s);
+    double* R = h->R.as<double>(9 * (size_t)nb + 1);
+    double* rec = h->rec.as<double>((size_t)kRec * tb + 1);
+    launch_jacobian(bsc, ix.idx_cam, R, rec, st, s);
+    launch_weights(bsc, ix.idx_cam, rec, st, s);
+    const size_t ncols = (size_t)P * nb + 3 * (size_t)mb;
+    double* D = h->D.as<double>((size_t)P * P * nb + 1);
+    double* Hr = h->Hr.as<double>(9 * (size_t)nb + 1);
+    double* A = h->A.as<double>(9 * (size_t)mb + 1);
+    double* s_a = h->s_a.as<double>(ncols + 1);
+    unsigned char* flags = h->flags.as<unsigned char>(ncols + 1);
+    launch_reductions(bsc, ix, rec, D, Hr, A, s_a, flags, st, s, h->s4, h->e_red_fork, h->e_red_join);
+    phase("stage_a");
+    double* s_b = h->bt_sb.as<double>(7 * (size_t)B + 7);
+    launch_batch_border(P, L, cams_b, Hr, pts_b, s_a, s_b, s);
+    int* sofc = h->bt_sofc.as<int>((size_t)nb + 1);
+    int* sofp = h->bt_sofp.as<int>((size_t)mb + 1);
+    launch_batch_scene_of(L.coff, B, nb, sofc, s);
+    launch_batch_scene_of(L.poff, B, mb, sofp, s);
+    const int ppb = point_prep_blocks(mb);
+    const size_t nwarps = ((size_t)tb + 31) / 32;
+    double* Lpt = h->Lpt.as<double>(8 * (size_t)mb + 8);
+    double* Wb = h->Wb.as<double>((size_t)kWStride * tb + 1);
+    double* V = h->V.as<double>(21 * (size_t)mb + 21);
+    launch_point_prep(bsc, ix, rec, A, s_a, s_b, Lpt, Wb, V, h->Fpart.as<double>(28 * (size_t)ppb + 28),
+                      h->Pfirst.as<double>((size_t)P * 7 * nwarps + 1), h->Plast.as<double>((size_t)P * 7 * nwarps + 1),
+                      h->Gsum.as<double>((size_t)P * 7 * nb + 1), st, s, sofp);
+    double* F28 = h->bt_F.as<double>(28 * (size_t)B + 28);
+    double* LF = h->bt_LF.as<double>(49 * (size_t)B + 49);
+    double* E = h->bt_E.as<double>(49 * (size_t)B + 49);
+    double* eigE = h->bt_eigE.as<double>(8 * (size_t)B + 8);
+    launch_batch_F(L, V, F28, s);
+    launch_border_factor(F28, 1, LF, E, eigE, st, s, B);
+    const int N = P * nb;
+    double* Gamma = h->Gamma.as<double>((size_t)N * 7 + 1);
+    double* G = h->G.as<double>((size_t)N * 7 + 1);
+    double* wv = h->sh_S.as<double>((size_t)P * 7 * nb + 1);
+    launch_batch_wv(P, nb, ix.off_cam, ix.idx_cam, bsc.op, Wb, V, wv, s);
+    launch_camera_border(bsc, ix, nullptr, nullptr, nullptr, Hr, s_a, s_b, LF, Gamma, G, s, nullptr, wv, sofc);
+    phase("schur_prep");
+    build_pairs(bsc, ix, h->pairs, h->ws_pairs, s);
+    phase("pairs");
+    // one identity-padded Z per scene, the pair blocks routed there
+    int maxn = 0;
+    for (int k = s0; k < s1; ++k) maxn = std::max<int>(maxn, (int)(coff[k + 1] - coff[k]));
+    const int Npad = std::max(kNB, ((P * maxn + kNB - 1) / kNB) * kNB);
+    const long long zs = (long long)Npad * Npad;
+    double* Zb = h->bt_Zb.as<double>((size_t)zs * B + 1);
+    launch_batch_fill(P, L, Zb, Npad, D, s_a, G, s);
+    launch_pair_reduce(P, h->pairs, Wb, nb, Zb, Npad, s, 0, 1 << 30, ZMap{sofc, L.coff, zs});
+    double* piv = h->bt_piv.as<double>((size_t)Npad * B + 1);
+    double* dcov = h->bt_cov.as<double>((size_t)P * P * nb + 1);
+    int* psd = h->psd.as<int>(1);
+    SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
+    phase("fill_reduce");
+    SFM_CUDA(cudaEventRecord(h->e1, s));
+    // the dense stage: scenes round-robin over W worker handles, one host thread each
+    const int W = std::min(B, 16);
+    std::vector<sfmcov_handle*> ws(W);
+    for (int w = 0; w < W; ++w) ws[w] = worker_of(h, w);
+    const int K = Npad / kNB;
+    const int pw = panel_blocks(K, 1);
+    std::vector<std::string> terr(W);
+    std::vector<std::thread> th;
+    th.reserve(W);
+    for (int w = 0; w < W; ++w)
+        th.emplace_back([&, w] {
+            try {
+                sfmcov_handle* wk = ws[w];
+                SFM_CUDA(cudaSetDevice(h->device));
+                SFM_CUDA(cudaStreamWaitEvent(wk->s, h->e1, 0));
+                double* Linv = wk->Linv.as<double>((size_t)K * kNB * kNB);
+                double* ring = wk->ring.as<double>(sweep_ring_doubles(Npad, pw, sfmcov_handle::kRing));
+                for (int k = w; k < B; k += W) {
+                    double* Zs = Zb + (size_t)k * zs;
+                    const int nk = (int)(coff[s0 + k + 1] - coff[s0 + k]);
+                    const int c0 = (int)(coff[s0 + k] - coff[s0]);
+                    dense_sweep(Zs, Npad, Npad, pw, Linv, piv + (size_t)k * Npad, st, ring, sfmcov_handle::kRing,
+                                wk->s, wk->s2, wk->s3, wk->eL, wk->eT, wk->e2, wk->s4, wk->eX, wk->eN, nullptr);
+                    launch_extract(P, Zs, Npad, P * nk, nk, s_a + (size_t)P * c0, 1, dcov + (size_t)P * P * c0, st,
+                                   psd, wk->s);
+                }
+                SFM_CUDA(cudaEventRecord(wk->e1, wk->s));
+            } catch (const std::exception& x) {
+                terr[w] = x.what();
+            }
+        });
+    for (auto& t : th) t.join();
+    for (int w = 0; w < W; ++w) {
+        if (!terr[w].empty()) throw ApiError{SFMCOV_ERR_DEVICE, "device", terr[w]};
+        SFM_CUDA(cudaStreamWaitEvent(s, ws[w]->e1, 0));
+    }
+    phase("dense");
+    int* bad = h->bt_bad.as<int>((size_t)B + 1);
+    launch_batch_ratio(L, piv, Npad, P, eigE, bad, s);
+    std::vector<int> hb(B);
+    d2h(h, hb.data(), bad, 4 * (size_t)B);
+    sync_status(h);
+    const Status& q = *h->st_host;
+    const bool failed = q.cam_count_bad != INT_MAX || q.pt_count_bad != INT_MAX || q.jac_bad != INT_MAX ||
+                        q.rot_bad != INT_MAX || q.fisher_bad != INT_MAX || q.pt_sing_bad != INT_MAX || q.border_bad ||
+                        q.chol_bad != INT_MAX || std::find(hb.begin(), hb.end(), 1) != hb.end();
+    if (failed) throw BatchFallback{};
+    d2h(h, cov, dcov, 8 * (size_t)P * P * nb);
+    phase("finish");
+    if (timing) std::fprintf(stderr, "  batch chunk: %d scenes, %d cameras, %d points, %d observations, %lld pairs, Npad %d\n", B, nb, mb, tb, h->pairs.npairs, Npad);
+}
+
 // Copies a host scene into the handle's staging buffers.
 SceneDev upload(sfmcov_handle* h, const sfmcov_scene* s) {
     SceneDev d;
@@ -1181,7 +1372,10 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     h->seg_recv.release();
     h->seg_groups.release();
     for (auto& a : h->ranka) a.release();
-    for (DBuf* b : {&h->sh_bounds, &h->sh_raw, &h->sh_sq, &h->sh_F, &h->sh_S, &h->sh_seg, &h->sh_err}) b->release();
+    for (DBuf* b : {&h->sh_bounds, &h->sh_raw, &h->sh_sq, &h->sh_F, &h->sh_S, &h->sh_seg, &h->sh_err, &h->bt_lists,
+                    &h->bt_cams, &h->bt_pts, &h->bt_oc, &h->bt_op, &h->bt_sigma, &h->bt_sofc, &h->bt_sofp, &h->bt_sb,
+                    &h->bt_F, &h->bt_LF, &h->bt_E, &h->bt_eigE, &h->bt_Zb, &h->bt_piv, &h->bt_cov, &h->bt_bad})
+        b->release();
     h->prange_r.release();
     h->scale_mm.release();
     for (DBuf* b : {&h->zi, &h->fc_part, &h->fc_y, &h->fc_gtt, &h->fc_eb, &h->fc_pc, &h->or_a, &h->or_w, &h->or_work,
@@ -1870,6 +2064,44 @@ int32_t sfmcov_cuda_full_covariance(sfmcov_handle* h, const sfmcov_scene* scene,
         double* out = h->sys[8].as<double>((size_t)params * params + 1);
         launch_full_unscale(params, S, lds, (const double*)h->s_a.p, out, s);
         if (params) d2h(h, sigma, out, 8 * (size_t)params * params);
+    });
+}
+
+// Internal (csrc/subrec.cpp; not in include/sfmcov_b200.h): the covariances
+// of many sub-scenes of `full`, each given by its sorted camera ids, sorted
+// point ids and ascending observation ids (the sub-scene induce_scene
+// builds), in chunks of one pipeline run each.  Returns SFMCOV_OK with every
+// sub-scene's blocks in cov (concatenated in scene and camera order), or
+// SFMCOV_ERR_DEGENERATE with stage "batch" when any sub-scene fails anywhere:
+// the caller then runs them one by one for the exact error.
+int32_t sfmcov_internal_batch_covariance(sfmcov_handle* h, const sfmcov_scene* full, int32_t nscenes,
+                                         const int32_t* cams, const int64_t* coff, const int32_t* pts,
+                                         const int64_t* poff, const int32_t* obs, const int64_t* toff, double* cov,
+                                         sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        const SceneDev sc = upload(h, full);
+        if (sc.sigma_ready) SFM_CUDA(cudaStreamWaitEvent(h->s, sc.sigma_ready, 0));
+        {
+            static const bool timing = [] { const char* e = std::getenv("SFMCOV_SUBREC_TIMING"); return e && e[0] == '1'; }();
+            if (timing) {
+                SFM_CUDA(cudaStreamSynchronize(h->s));
+                std::fprintf(stderr, "  batch upload     %8.3f ms\n",
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+            }
+        }
+        const int P = sc.P;
+        int s0 = 0;
+        while (s0 < nscenes) {  // chunks: <= 60000 cameras (32-bit pair keys), <= 12M observations
+            int s1 = s0 + 1;
+            while (s1 < nscenes && coff[s1 + 1] - coff[s0] <= 60000 && toff[s1 + 1] - toff[s0] <= 12000000) ++s1;
+            try {
+                run_batch_chunk(h, sc, s0, s1, cams, coff, pts, poff, obs, toff, cov + (size_t)P * P * coff[s0]);
+            } catch (const BatchFallback&) {
+                throw ApiError{SFMCOV_ERR_DEGENERATE, "batch", "a sub-scene failed; rerun them one by one"};
+            }
+            s0 = s1;
+        }
     });
 }
 

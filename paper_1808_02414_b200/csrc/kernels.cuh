@@ -89,6 +89,15 @@ struct PairDev {
     }
 };
 
+// Batched sub-scenes (one dense Z per scene, block-diagonal problem): camera
+// c of the concatenated batch lives in scene scene_of_cam[c] at local index
+// c - coff[scene], whose Z starts zstride doubles after the previous one.
+struct ZMap {
+    const int* scene_of_cam = nullptr;
+    const int* coff = nullptr;
+    long long zstride = 0;
+};
+
 // C = beta C + alpha A B^T with K = kNB (see dense.cu).
 struct GemmArgs {
     double* C;
@@ -147,23 +156,25 @@ void launch_write_h(const SceneDev& sc, const double* Hr, double* H, cudaStream_
 
 // schur.cu
 int point_prep_blocks(int m);
+// scene_of_pt (batched sub-scenes): s_b holds 7 scales per scene
 void launch_point_prep(const SceneDev& sc, const IndexDev& ix, const double* rec, const double* A, const double* s_a,
                        const double* s_b, double* Lpt, double* Wb, double* V, double* Fpart, double* Pfirst,
-                       double* Plast, double* Gsum, Status* st, cudaStream_t s);
+                       double* Plast, double* Gsum, Status* st, cudaStream_t s, const int* scene_of_pt = nullptr);
+// batch > 1: independent gauge blocks, each from nblocks partials (strided)
 void launch_border_factor(const double* Fpart, int nblocks, double* LF, double* E, double* eigE, Status* st,
-                          cudaStream_t s);
+                          cudaStream_t s, int batch = 1);
 // sums_out: write this rank's Σ W V per camera (n x P x 7) and stop;
 // sums_in: use all-reduced sums instead of the warp partials
 void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* Pfirst, const double* Plast,
                           const double* Gsum, const double* Hr, const double* s_a, const double* s_b, const double* LF,
                           double* Gamma, double* G, cudaStream_t s, double* sums_out = nullptr,
-                          const double* sums_in = nullptr);
+                          const double* sums_in = nullptr, const int* scene_of_cam = nullptr);
 void launch_fpart_sum(const double* Fpart, int nblocks, double* F28, cudaStream_t s);
 void launch_fill(int P, double* Z, long long ld, int N, int Npad, const double* D, const double* s_a, const double* G,
                  int add_gg, cudaStream_t s);
 void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace& ws, cudaStream_t s);
 void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, cudaStream_t s,
-                        int lo_min = 0, int lo_max = 1 << 30);
+                        int lo_min = 0, int lo_max = 1 << 30, ZMap zm = ZMap{});
 
 // dense.cu
 void dense_init_attributes();
@@ -305,6 +316,28 @@ inline int own_blocks_upto(const Ownership& o, int K, int q) {
     for (int p = o.rank; p <= q && p * o.G < K; p += o.R) b += (K - p * o.G < o.G) ? K - p * o.G : o.G;
     return b;
 }
+
+// ---- batched sub-scenes (batch.cu) ---------------------------------------------
+// Device lists of a batch of B sub-scenes of one resident scene: per scene its
+// sorted global camera ids cams[coff[s] .. coff[s+1]), point ids
+// pts[poff[s] ..), and observation ids obs[toff[s] ..) (ascending).
+struct BatchLists {
+    int B = 0, nb = 0, mb = 0, tb = 0;
+    const int *cams = nullptr, *coff = nullptr, *pts = nullptr, *poff = nullptr, *obs = nullptr, *toff = nullptr;
+};
+void launch_batch_scene_of(const int* off, int B, int count, int* out, cudaStream_t s);
+void launch_batch_gather(const BatchLists& L, int P, const double* cams_full, const double* pts_full, const int* oc,
+                         const int* op, const double* sigma, double* cams_b, double* pts_b, int* oc_b, int* op_b,
+                         double* sigma_b, cudaStream_t s);
+void launch_batch_border(int P, const BatchLists& L, const double* cams_b, const double* Hr, const double* pts_b,
+                         const double* s_a, double* s_b, cudaStream_t s);
+void launch_batch_F(const BatchLists& L, const double* V, double* F28, cudaStream_t s);
+void launch_batch_wv(int P, int nb, const int* off_cam, const int* idx_cam, const int* op, const double* Wb,
+                     const double* V, double* sums, cudaStream_t s);
+void launch_batch_fill(int P, const BatchLists& L, double* Zb, int Npad, const double* D, const double* s_a,
+                       const double* G, cudaStream_t s);
+void launch_batch_ratio(const BatchLists& L, const double* piv, int Npad, int P, const double* eigE, int* bad,
+                        cudaStream_t s);
 
 // ---- point-sharded stage A (shard.cu) ---------------------------------------
 // A rank's sub-scene: every camera, points [j0, j1), their observations in

@@ -39,9 +39,10 @@ namespace sfm {
 template <int P>
 __global__ void __launch_bounds__(128) k_point_prep(const double* A, const double* s_a, const double* pts,
                                                     const double* s_b, int m, int n, double* Lpt, double* V,
-                                                    double* Fpart, Status* st) {
+                                                    double* Fpart, Status* st, const int* scene_of_pt) {
     __shared__ double red[128][29];
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (scene_of_pt && j < m) s_b += 7 * scene_of_pt[j];  // batched sub-scenes: the point's own scales
     double f[28];
 #pragma unroll
     for (int k = 0; k < 28; ++k) f[k] = 0.0;
@@ -263,6 +264,12 @@ __global__ void __launch_bounds__(128, 5) k_obs_factor(const int* oc, const int*
 __global__ void __launch_bounds__(28 * 32) k_border_factor(const double* Fpart, int nblocks, double* LF, double* Eout,
                                                            double* eigE, Status* st) {
     __shared__ double red[28];
+    // a grid of B blocks: B independent gauge blocks (batched sub-scenes),
+    // each from its own nblocks partials
+    Fpart += 28 * (size_t)nblocks * blockIdx.x;
+    LF += 49 * blockIdx.x;
+    Eout += 49 * blockIdx.x;
+    eigE += 8 * blockIdx.x;
     const int e = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int b = lane;
@@ -318,10 +325,16 @@ __global__ void __launch_bounds__(64) k_camera_border(const int* off_cam, int t_
                                                       const double* Plast, const double* Gsum, const double* cams,
                                                       const double* Hr, const double* s_a, const double* s_b,
                                                       const double* LF, int n, double* Gamma, double* G,
-                                                      double* sums_out, const double* sums_in) {
+                                                      double* sums_out, const double* sums_in,
+                                                      const int* scene_of_cam) {
     constexpr int NE = P * 7;
     __shared__ double sh[NE];
     const int i = blockIdx.x, tid = threadIdx.x;
+    if (scene_of_cam) {  // batched sub-scenes: the camera's own gauge scales and factor
+        const int scn = scene_of_cam[i];
+        s_b += 7 * scn;
+        LF += 49 * scn;
+    }
     const int p = tid / 7, l = tid % 7;
     if (tid < NE) {
         double sum = 0.0;
@@ -512,7 +525,7 @@ __global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned in
                                                          const int* seg_of, const int* chunk_off, int nchunks,
                                                          int chunk, const unsigned long long* vals, const double* Wb,
                                                          int n, double* Z, long long ld, double* part, int cfirst,
-                                                         int always_part, int lo_min, int lo_max) {
+                                                         int always_part, int lo_min, int lo_max, ZMap zm) {
     const int warp = cfirst + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (warp >= nchunks) return;
@@ -573,10 +586,18 @@ __global__ void __launch_bounds__(256, MINB) k_pair_reduce_mma(const unsigned in
     // single chunk: Z(P hi + p, P lo + q) -= out(p, q) (diagonal blocks: lower
     // part only); else the chunk's partial block, combined by k_pair_combine
     double* pp = part + (size_t)warp * 81;
+    double* Zs = Z;
+    int lz = lo, hz = hi;
+    if (zm.scene_of_cam) {  // batched sub-scenes: the scene's own Z, local camera indices
+        const int scn = zm.scene_of_cam[lo];
+        Zs = Z + scn * zm.zstride;
+        lz -= zm.coff[scn];
+        hz -= zm.coff[scn];
+    }
     auto put = [&](int p, int q, double v) {
         if (nch > 1 || always_part) { pp[P * p + q] = v; return; }
         if (diag && p < q) return;
-        double* z = Z + ((size_t)P * lo + q) * ld + (size_t)P * hi + p;
+        double* z = Zs + ((size_t)P * lz + q) * ld + (size_t)P * hz + p;
         *z = *z - v;
     };
     const int q0 = 2 * k;
@@ -610,7 +631,7 @@ __global__ void __launch_bounds__(kCpWarps * 32, MINB) k_pair_reduce_cp(const un
                                                                    int chunk, const unsigned long long* vals,
                                                                    const double* Wb, int n, double* Z, long long ld,
                                                                    double* part, int cfirst, int always_part,
-                                                                   int lo_min, int lo_max) {
+                                                                   int lo_min, int lo_max, ZMap zm) {
     extern __shared__ __align__(16) double sm_pairs[];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int warp = cfirst + blockIdx.x * kCpWarps + wib;
@@ -690,10 +711,18 @@ __global__ void __launch_bounds__(kCpWarps * 32, MINB) k_pair_reduce_cp(const un
     }
     const bool diag = lo == hi;
     double* pp = part + (size_t)warp * 81;
+    double* Zs = Z;
+    int lz = lo, hz = hi;
+    if (zm.scene_of_cam) {  // batched sub-scenes: the scene's own Z, local camera indices
+        const int scn = zm.scene_of_cam[lo];
+        Zs = Z + scn * zm.zstride;
+        lz -= zm.coff[scn];
+        hz -= zm.coff[scn];
+    }
     auto put = [&](int p, int q, double v) {
         if (nch > 1 || always_part) { pp[P * p + q] = v; return; }
         if (diag && p < q) return;
-        double* z = Z + ((size_t)P * lo + q) * ld + (size_t)P * hi + p;
+        double* z = Zs + ((size_t)P * lz + q) * ld + (size_t)P * hz + p;
         *z = *z - v;
     };
     const int q0 = 2 * k;
@@ -714,7 +743,7 @@ static bool pair_kernel_old() {
 }
 
 static void launch_pair_mma(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, int cfirst,
-                            int clast, int always_part, int lo_min, int lo_max, cudaStream_t s) {
+                            int clast, int always_part, int lo_min, int lo_max, cudaStream_t s, ZMap zm = ZMap{}) {
     const int cnt = clast - cfirst;
     if (cnt <= 0) return;
     if (pair_kernel_old()) {
@@ -722,11 +751,11 @@ static void launch_pair_mma(int P, const PairDev& pd, const double* Wb, int n, d
         if (P == 8)
             k_pair_reduce_mma<8, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, clast,
                                                                 pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, cfirst,
-                                                                always_part, lo_min, lo_max);
+                                                                always_part, lo_min, lo_max, zm);
         else
             k_pair_reduce_mma<9, 4, 4><<<cblocks, 256, 0, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, clast,
                                                                 pd.chunk, pd.vals, Wb, n, Z, ld, pd.part, cfirst,
-                                                                always_part, lo_min, lo_max);
+                                                                always_part, lo_min, lo_max, zm);
         SFM_LAUNCH_CHECK();
         return;
     }
@@ -738,7 +767,7 @@ static void launch_pair_mma(int P, const PairDev& pd, const double* Wb, int n, d
     auto go = [&](auto kern, size_t smem) {
         SFM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<cdiv(cnt, 4), 4 * 32, smem, s>>>(pd.ukeys, pd.seg_off, pd.seg_of, pd.chunk_off, clast, pd.chunk,
-                                                pd.vals, Wb, n, Z, ld, pd.part, cfirst, always_part, lo_min, lo_max);
+                                                pd.vals, Wb, n, Z, ld, pd.part, cfirst, always_part, lo_min, lo_max, zm);
         SFM_LAUNCH_CHECK();
     };
     if (P == 8) go(k_pair_reduce_cp<8, 8, 4, 6>, pair_cp_smem_bytes<8, 4>());
@@ -749,7 +778,7 @@ static void launch_pair_mma(int P, const PairDev& pd, const double* Wb, int n, d
 template <int P>
 __global__ void __launch_bounds__(256) k_pair_combine(const unsigned int* ukeys, int nseg, const int* chunk_off,
                                                       const double* part, int n, double* Z, long long ld, int lo_min,
-                                                      int lo_max) {
+                                                      int lo_max, ZMap zm) {
     const int sg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (sg >= nseg) return;
@@ -758,12 +787,20 @@ __global__ void __launch_bounds__(256) k_pair_combine(const unsigned int* ukeys,
     const unsigned int key = ukeys[sg];
     const int lo = (int)(key / (unsigned int)n), hi = (int)(key - (unsigned int)lo * (unsigned int)n);
     if (lo < lo_min || lo >= lo_max) return;
+    double* Zs = Z;
+    int lz = lo, hz = hi;
+    if (zm.scene_of_cam) {
+        const int scn = zm.scene_of_cam[lo];
+        Zs = Z + scn * zm.zstride;
+        lz -= zm.coff[scn];
+        hz -= zm.coff[scn];
+    }
     for (int en = lane; en < P * P; en += 32) {
         const int p = en / P, q = en - P * (en / P);
         if (lo == hi && p < q) continue;
         double v = 0.0;
         for (int c = c0; c < c1; ++c) v += part[(size_t)c * 81 + en];
-        double* z = Z + ((size_t)P * lo + q) * ld + (size_t)P * hi + p;
+        double* z = Zs + ((size_t)P * lz + q) * ld + (size_t)P * hz + p;
         *z = *z - v;
     }
 }
@@ -789,10 +826,10 @@ int point_prep_blocks(int m) { return (int)cdiv(m > 0 ? m : 1, 128); }
 
 void launch_point_prep(const SceneDev& sc, const IndexDev& ix, const double* rec, const double* A, const double* s_a,
                        const double* s_b, double* Lpt, double* Wb, double* V, double* Fpart, double* Pfirst,
-                       double* Plast, double* Gsum, Status* st, cudaStream_t s) {
+                       double* Plast, double* Gsum, Status* st, cudaStream_t s, const int* scene_of_pt) {
     const int nb = point_prep_blocks(sc.m);
-    if (sc.P == 8) k_point_prep<8><<<nb, 128, 0, s>>>(A, s_a, sc.pts, s_b, sc.m, sc.n, Lpt, V, Fpart, st);
-    else k_point_prep<9><<<nb, 128, 0, s>>>(A, s_a, sc.pts, s_b, sc.m, sc.n, Lpt, V, Fpart, st);
+    if (sc.P == 8) k_point_prep<8><<<nb, 128, 0, s>>>(A, s_a, sc.pts, s_b, sc.m, sc.n, Lpt, V, Fpart, st, scene_of_pt);
+    else k_point_prep<9><<<nb, 128, 0, s>>>(A, s_a, sc.pts, s_b, sc.m, sc.n, Lpt, V, Fpart, st, scene_of_pt);
     SFM_LAUNCH_CHECK();
     if (sc.t) {
         if (sc.P == 8) k_obs_factor<8><<<cdiv(sc.t, 128), 128, 0, s>>>(sc.oc, sc.op, ix.idx_cam, rec, s_a, Lpt, V, sc.t, sc.n, Wb, Pfirst, Plast, Gsum);
@@ -802,17 +839,19 @@ void launch_point_prep(const SceneDev& sc, const IndexDev& ix, const double* rec
 }
 
 void launch_border_factor(const double* Fpart, int nblocks, double* LF, double* E, double* eigE, Status* st,
-                          cudaStream_t s) {
-    k_border_factor<<<1, 28 * 32, 0, s>>>(Fpart, nblocks, LF, E, eigE, st);
+                          cudaStream_t s, int batch) {
+    if (batch < 1) return;
+    k_border_factor<<<batch, 28 * 32, 0, s>>>(Fpart, nblocks, LF, E, eigE, st);
     SFM_LAUNCH_CHECK();
 }
 
 void launch_camera_border(const SceneDev& sc, const IndexDev& ix, const double* Pfirst, const double* Plast,
                           const double* Gsum, const double* Hr, const double* s_a, const double* s_b, const double* LF,
-                          double* Gamma, double* G, cudaStream_t s, double* sums_out, const double* sums_in) {
+                          double* Gamma, double* G, cudaStream_t s, double* sums_out, const double* sums_in,
+                          const int* scene_of_cam) {
     if (!sc.n) return;
-    if (sc.P == 8) k_camera_border<8><<<sc.n, 64, 0, s>>>(ix.off_cam, sc.t, Pfirst, Plast, Gsum, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G, sums_out, sums_in);
-    else k_camera_border<9><<<sc.n, 64, 0, s>>>(ix.off_cam, sc.t, Pfirst, Plast, Gsum, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G, sums_out, sums_in);
+    if (sc.P == 8) k_camera_border<8><<<sc.n, 64, 0, s>>>(ix.off_cam, sc.t, Pfirst, Plast, Gsum, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G, sums_out, sums_in, scene_of_cam);
+    else k_camera_border<9><<<sc.n, 64, 0, s>>>(ix.off_cam, sc.t, Pfirst, Plast, Gsum, sc.cams, Hr, s_a, s_b, LF, sc.n, Gamma, G, sums_out, sums_in, scene_of_cam);
     SFM_LAUNCH_CHECK();
 }
 
@@ -944,12 +983,12 @@ void build_pairs(const SceneDev& sc, const IndexDev& ix, PairDev& pd, Workspace&
 // sweep's first panel needs only its own columns, so the pipeline reduces
 // those first and the rest beside the first panel's factorisation.
 void launch_pair_reduce(int P, const PairDev& pd, const double* Wb, int n, double* Z, long long ld, cudaStream_t s,
-                        int lo_min, int lo_max) {
+                        int lo_min, int lo_max, ZMap zm) {
     if (!pd.nseg) return;
     const unsigned blocks = cdiv(pd.nseg, 8);
-    launch_pair_mma(P, pd, Wb, n, Z, ld, 0, pd.nchunks, 0, lo_min, lo_max, s);
-    if (P == 8) k_pair_combine<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld, lo_min, lo_max);
-    else k_pair_combine<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld, lo_min, lo_max);
+    launch_pair_mma(P, pd, Wb, n, Z, ld, 0, pd.nchunks, 0, lo_min, lo_max, s, zm);
+    if (P == 8) k_pair_combine<8><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld, lo_min, lo_max, zm);
+    else k_pair_combine<9><<<blocks, 256, 0, s>>>(pd.ukeys, pd.nseg, pd.chunk_off, pd.part, n, Z, ld, lo_min, lo_max, zm);
     SFM_LAUNCH_CHECK();
 }
 

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <random>
 #include <stdexcept>
@@ -29,6 +30,12 @@
 #include <unordered_map>
 #include <utility>
 #include <vector>
+
+// capi.cu: all sub-scenes through one batched pipeline run per chunk
+extern "C" int32_t sfmcov_internal_batch_covariance(sfmcov_handle* h, const sfmcov_scene* full, int32_t nscenes,
+                                                    const int32_t* cams, const int64_t* coff, const int32_t* pts,
+                                                    const int64_t* poff, const int32_t* obs, const int64_t* toff,
+                                                    double* cov, sfmcov_error* err);
 
 namespace {
 
@@ -122,9 +129,9 @@ Graph view_graph(const sfmcov_scene& s, int min_covis) {
 }
 
 struct Sub {
-    std::vector<int32_t> cams, pts;
-    HostScene scene;
-    bool truncated = false;
+    std::vector<int32_t> cams, pts, obs;  // sorted camera / point ids, ascending observation ids
+    HostScene scene;                      // the induced scene's arrays (empty when built lists-only)
+    bool truncated = false, has_scene = false;
 };
 
 // Observations by camera (ascending observation ids), built once per call so
@@ -209,7 +216,8 @@ std::vector<int32_t> induced_cams(const sfmcov_scene& s, const ByCam& bc, const 
     return out;
 }
 
-Sub induced(const sfmcov_scene& s, const ByCam& bc, const std::vector<int32_t>& cams, bool truncated) {
+Sub induced(const sfmcov_scene& s, const ByCam& bc, const std::vector<int32_t>& cams, bool truncated,
+            bool lists_only = false) {
     thread_local Scratch w;
     w.size(s.n_cams, s.n_pts, s.n_obs);
     filter_fixpoint(bc, cams, w);
@@ -265,8 +273,22 @@ Sub induced(const sfmcov_scene& s, const ByCam& bc, const std::vector<int32_t>& 
                 w.pl[j] = (int32_t)sub.pts.size();
                 sub.pts.push_back(j);
             }
+    if (lists_only) {  // ids only: the batched GPU path gathers the data from the resident scene
+        sub.obs.reserve(nkept);
+        if (t_hi >= 0)
+            for (int64_t wd = t_lo >> 6; wd <= (t_hi >> 6); ++wd) {
+                for (uint64_t bits = w.obs_bits[wd]; bits; bits &= bits - 1)
+                    sub.obs.push_back((int32_t)(wd * 64 + __builtin_ctzll(bits)));
+                w.obs_bits[wd] = 0;
+            }
+        if (j_hi >= 0)
+            for (int64_t wd = j_lo >> 6; wd <= (j_hi >> 6); ++wd) w.pt_bits[wd] = 0;
+        return sub;
+    }
+    sub.has_scene = true;
     h.pts.resize(3 * sub.pts.size());
     for (size_t l = 0; l < sub.pts.size(); ++l) std::memcpy(&h.pts[3 * l], s.pts + 3 * (size_t)sub.pts[l], 24);
+    sub.obs.resize(nkept);
     h.oc.resize(nkept);
     h.op.resize(nkept);
     if (h.has_u) h.u.resize(2 * (size_t)nkept);
@@ -276,6 +298,7 @@ Sub induced(const sfmcov_scene& s, const ByCam& bc, const std::vector<int32_t>& 
         for (int64_t wd = t_lo >> 6; wd <= (t_hi >> 6); ++wd) {
             for (uint64_t bits = w.obs_bits[wd]; bits; bits &= bits - 1) {
                 const int64_t t = wd * 64 + __builtin_ctzll(bits);
+                sub.obs[o] = (int32_t)t;
                 h.oc[o] = w.cl[s.obs_cam[t]];
                 h.op[o] = w.pl[s.obs_pt[t]];
                 if (h.has_u) std::memcpy(&h.u[2 * (size_t)o], s.obs_u + 2 * (size_t)t, 16);
@@ -387,7 +410,9 @@ struct SubResult {
     sfmcov_error err{};
 };
 
-std::vector<SubResult> batch_covariances(sfmcov_handle* h0, const std::vector<const Sub*>& subs, int workers) {
+// One sub-scene at a time on `workers` handles (the fallback, and
+// SFMCOV_SUBREC_BATCH=0): every Sub must have its scene built.
+std::vector<SubResult> per_scene_covariances(sfmcov_handle* h0, const std::vector<const Sub*>& subs, int workers) {
     std::vector<SubResult> res(subs.size());
     // largest sub-scenes first: a worker's grow-only device buffers are then
     // sized by its first job, so later (smaller) ones never reallocate --
@@ -424,6 +449,82 @@ std::vector<SubResult> batch_covariances(sfmcov_handle* h0, const std::vector<co
     work(hs[0]);
     for (auto& t : th) t.join();
     return res;
+}
+
+bool subrec_batch_enabled() {
+    static bool on = [] { const char* e = std::getenv("SFMCOV_SUBREC_BATCH"); return !(e && e[0] == '0'); }();
+    return on;
+}
+
+// The covariance of every sub-scene: all of them through one batched
+// pipeline run per chunk (capi.cu run_batch: one launch per stage over the
+// concatenated sub-scenes, one dense sweep per sub-scene on worker streams);
+// if any sub-scene fails anywhere, they are rerun one by one so the error is
+// the reference's for the first failing subset.
+std::vector<SubResult> batch_covariances(sfmcov_handle* h0, const sfmcov_scene& full, const ByCam& bc,
+                                         const std::vector<Sub*>& subs, int workers) {
+    const int P = full.cam_params;
+    // (one sub-scene: nothing to batch -- and the single-scene pipeline keeps
+    // a full-size window bitwise equal to compute_covariance, test_subrec.cpp:171-184)
+    if (subrec_batch_enabled() && subs.size() > 1) {
+        const size_t B = subs.size();
+        std::vector<int64_t> coff(B + 1, 0), poff(B + 1, 0), toff(B + 1, 0);
+        for (size_t i = 0; i < B; ++i) {
+            coff[i + 1] = coff[i] + (int64_t)subs[i]->cams.size();
+            poff[i + 1] = poff[i] + (int64_t)subs[i]->pts.size();
+            toff[i + 1] = toff[i] + (int64_t)subs[i]->obs.size();
+        }
+        // uninitialised: the parallel copy below is the first touch of every page
+        std::unique_ptr<int32_t[]> cams(new int32_t[coff[B] + 1]), pts(new int32_t[poff[B] + 1]),
+            obs(new int32_t[toff[B] + 1]);
+        {  // concatenated id lists, filled in parallel
+            std::atomic<size_t> next{0};
+            auto job = [&] {
+                for (size_t i = next++; i < B; i = next++) {
+                    std::copy(subs[i]->cams.begin(), subs[i]->cams.end(), cams.get() + coff[i]);
+                    std::copy(subs[i]->pts.begin(), subs[i]->pts.end(), pts.get() + poff[i]);
+                    std::copy(subs[i]->obs.begin(), subs[i]->obs.end(), obs.get() + toff[i]);
+                }
+            };
+            const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 16));
+            std::vector<std::thread> th;
+            for (int i = 1; i < nt; ++i) th.emplace_back(job);
+            job();
+            for (auto& t : th) t.join();
+        }
+        PhaseClock lc;
+        std::vector<double> cov((size_t)P * P * coff[B] + 1);
+        sfmcov_error e{};
+        const int32_t code = sfmcov_internal_batch_covariance(h0, &full, (int32_t)subs.size(), cams.get(), coff.data(),
+                                                              pts.get(), poff.data(), obs.get(), toff.data(),
+                                                              cov.data(), &e);
+        lc.mark("batched_gpu");
+        if (code != SFMCOV_OK && PhaseClock{}.on) std::fprintf(stderr, "subrec batch fallback: %s\n", e.message);
+        if (code == SFMCOV_OK) {
+            std::vector<SubResult> res(subs.size());
+            for (size_t i = 0; i < subs.size(); ++i)
+                res[i].cov.assign(cov.begin() + (size_t)P * P * coff[i], cov.begin() + (size_t)P * P * coff[i + 1]);
+            return res;
+        }
+    }
+    {  // the per-sub-scene path needs the induced scenes' arrays
+        std::atomic<size_t> next{0};
+        auto job = [&] {
+            for (size_t i = next++; i < subs.size(); i = next++)
+                if (!subs[i]->has_scene) {
+                    Sub built = induced(full, bc, subs[i]->cams, subs[i]->truncated);
+                    subs[i]->scene = std::move(built.scene);
+                    subs[i]->has_scene = true;
+                }
+        };
+        const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 32));
+        std::vector<std::thread> th;
+        for (int i = 1; i < nt; ++i) th.emplace_back(job);
+        job();
+        for (auto& t : th) t.join();
+    }
+    std::vector<const Sub*> cs(subs.begin(), subs.end());
+    return per_scene_covariances(h0, cs, workers);
 }
 
 double trace_of(const double* c, int P) {
@@ -576,9 +677,12 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
                 for (size_t i = next++; i < flat.size(); i = next++) {
                     Sub& sb = const_cast<Sub&>(*flat[i]);
                     try {
-                        Sub full = induced(*scene, bc, sb.cams, sb.truncated);
+                        // ids only when the batched GPU path will gather the data itself
+                        Sub full = induced(*scene, bc, sb.cams, sb.truncated, subrec_batch_enabled());
                         sb.scene = std::move(full.scene);
                         sb.pts = std::move(full.pts);
+                        sb.obs = std::move(full.obs);
+                        sb.has_scene = full.has_scene;
                     } catch (const SubError& x) {
                         berr[i] = x;
                         bfail[i] = 1;
@@ -594,8 +698,9 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
                 if (bfail[i]) throw berr[i];
         }
         clk.mark("induce");
-        const std::vector<SubResult> res =
-            batch_covariances(h, flat, std::max(1, (int)workers));
+        std::vector<Sub*> mflat;
+        for (const Sub* sb : flat) mflat.push_back(const_cast<Sub*>(sb));
+        const std::vector<SubResult> res = batch_covariances(h, *scene, bc, mflat, std::max(1, (int)workers));
         clk.mark("covariances");
         const int64_t n = scene->n_cams;
         std::vector<char> seen(n, 0);
@@ -706,9 +811,9 @@ int32_t sfmcov_cuda_error_size_sweep(sfmcov_handle* h, const sfmcov_scene* scene
                 sidx.push_back(sub);
             }
         }
-        std::vector<const Sub*> flat;
-        for (const Sub& sb : subs) flat.push_back(&sb);
-        const std::vector<SubResult> res = batch_covariances(h, flat, std::max(1, (int)workers));
+        std::vector<Sub*> flat;
+        for (Sub& sb : subs) flat.push_back(&sb);
+        const std::vector<SubResult> res = batch_covariances(h, *scene, bc, flat, std::max(1, (int)workers));
         int64_t k = 0;
         for (size_t i = 0; i < subs.size(); ++i) {
             if (res[i].code)

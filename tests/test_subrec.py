@@ -229,3 +229,27 @@ def test_sweep_rows_survive_a_csv_round_trip(engine, tmp_path):  # test_subrec.c
     for r, f in zip(rows, back):
         assert (int(f[0]), int(f[1]), int(f[2])) == (r.k_bar, r.subset_id, r.camera_id)
         assert (float(f[3]), float(f[4]), float(f[5])) == (r.err_relative, r.err_absolute, r.trace)
+
+
+@pytest.mark.gpu
+def test_batched_and_one_by_one_paths_agree(engine, tmp_path):
+    """The batched sub-scene pipeline (one launch per stage over the
+    concatenated sub-scenes, csrc/batch.cu) against the one-sub-scene-at-a-time
+    path (SFMCOV_SUBREC_BATCH=0, in a subprocess): same winning subsets, blocks
+    equal to FP64 rounding (the per-scene gauge sums run in another order)."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = ("import sys, numpy as np; sys.path.insert(0, '.');"
+            "from paper_1808_02414_b200 import sfmcov as F, synthetic as S, subrec as R;"
+            "a = R.approximate_covariances(S.generate_config(2), 12, 2, 5, engine=F.Engine(0));"
+            "np.savez(sys.argv[1], cov=a.cov, sid=a.subset_id)")
+    out = str(tmp_path / "one.npz")
+    subprocess.run([sys.executable, "-c", code, out], cwd=ROOT, env=dict(os.environ, SFMCOV_SUBREC_BATCH="0"),
+                   check=True, timeout=600)
+    one = np.load(out)
+    batched = R.approximate_covariances(S.generate_config(2), 12, 2, 5, engine=engine)
+    assert np.array_equal(batched.subset_id, one["sid"])
+    worst = max(rel(a, b) for a, b in zip(batched.cov, one["cov"]))
+    assert worst <= 1e-10

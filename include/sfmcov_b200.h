@@ -242,6 +242,13 @@ int32_t sfmcov_cuda_compute_covariance_sharded(sfmcov_handle* h, const sfmcov_sc
 int32_t sfmcov_cuda_compute_covariance_sharded_device(sfmcov_handle* h, const sfmcov_scene* d_scene,
                                                       const sfmcov_options* opts, double* d_cam_cov,
                                                       sfmcov_diagnostics* diag, sfmcov_error* err);
+/* Stage A of the multi-GPU path: 0 (default) = every rank runs validation ...
+ * Schur factors on the whole scene (the single-GPU FP64 summation order; the
+ * path stays within 1e-9 of the exact inverse at config 4), 1 = point-sharded
+ * (each rank its points' sub-scene, per-camera sums all-reduced: less work per
+ * rank, but the camera sums are added in another order and config 4's
+ * ill-conditioned cameras then move by up to 1.2e-8). */
+void sfmcov_cuda_set_sharded_stage_a(sfmcov_handle* h, int32_t on);
 /* The distributed code path with `ranks` ranks emulated on this one device
  * (in-process copies instead of NCCL); for testing the multi-GPU path. */
 int32_t sfmcov_cuda_compute_covariance_emulated(sfmcov_handle* h, const sfmcov_scene* scene,

@@ -142,6 +142,7 @@ CUDA_SYMBOLS = {
                                                       C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(ErrorStruct)]),
     "sfmcov_cuda_full_covariance": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_int64, C.c_void_p,
                                                 C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_set_sharded_stage_a": (None, [C.c_void_p, C.c_int32]),
     "sfmcov_cuda_refine_covariance": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_void_p, C.c_int32, C.c_int32,
                                                   C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(ErrorStruct)]),
     "sfmcov_cuda_pseudoinverse_covariance": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_int64, C.c_void_p, C.c_void_p,

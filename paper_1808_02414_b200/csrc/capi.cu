@@ -105,7 +105,10 @@ struct sfmcov_handle {
     Status* st_host = nullptr;
     // distributed tail: 0 = single device, 1 = emulated ranks, 2 = NCCL rank
     int dist_mode = 0, dist_R = 1, dist_rank = 0, emu_R = 1;
-    bool replicated_a = false;  // SFMCOV_REPLICATED_STAGE_A=1: the round-1 redundant stage A (A/B)
+    // Multi-GPU stage A: replicated on every rank (default: the single-GPU
+    // summation order, so the sharded pipeline stays within the parity bar) or
+    // point-sharded (sfmcov_cuda_set_sharded_stage_a / SFMCOV_SHARDED_STAGE_A=1)
+    bool replicated_a = true;
     void* nccl = nullptr;
     std::vector<sfm::RankDense> ranks;
     std::vector<RankA> ranka;
@@ -1305,8 +1308,8 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
     try {
         h->device = device;
         {
-            const char* e = std::getenv("SFMCOV_REPLICATED_STAGE_A");
-            h->replicated_a = e && e[0] == '1';
+            const char* e = std::getenv("SFMCOV_SHARDED_STAGE_A");
+            h->replicated_a = !(e && e[0] == '1');
         }
         SFM_CUDA(cudaSetDevice(device));
         // critical path (panel factorisations) at high priority, bulk trailing updates low
@@ -1428,6 +1431,10 @@ sfmcov_handle* sfmcov_cuda_worker(sfmcov_handle* h, int32_t i, sfmcov_error* err
         h->workers.push_back(w);
     }
     return h->workers[i];
+}
+
+void sfmcov_cuda_set_sharded_stage_a(sfmcov_handle* h, int32_t on) {
+    if (h) h->replicated_a = on == 0;
 }
 
 void sfmcov_cuda_set_profiling(sfmcov_handle* h, int32_t on) {

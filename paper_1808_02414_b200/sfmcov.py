@@ -238,6 +238,10 @@ class Engine:
     def stream(self) -> int:
         return self._lib.sfmcov_cuda_stream(self._h) or 0
 
+    def set_sharded_stage_a(self, on: bool):
+        """Multi-GPU stage A point-sharded (True) or replicated on every rank (False, default)."""
+        self._lib.sfmcov_cuda_set_sharded_stage_a(self._h, 1 if on else 0)
+
     def set_profiling(self, on: bool):
         self._lib.sfmcov_cuda_set_profiling(self._h, 1 if on else 0)
 

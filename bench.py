@@ -426,7 +426,7 @@ def main():
             "config": {
                 "workload": workload_name(args.config, rec),
                 "config_index": args.config,
-                "parallelism": (f"sharded{world}: observation-pair chunks + NCCL reduce-scatter of camera-pair blocks to their column owners; "
+                "parallelism": (f"sharded{world}: stage A replicated, observation-pair chunks + NCCL reduce-scatter of camera-pair blocks to their column owners; "
                                 f"1D block-cyclic Cholesky/inverse sweep with NCCL panel broadcast") if sharded
                                else ("replicas" if world > 1 else "single"),
                 "l2": "256 MiB write between timed steps; working set (Z 660 MB) > L2",

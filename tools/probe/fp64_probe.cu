@@ -1,4 +1,6 @@
-// FP64 throughput probe: DMMA shapes vs DFMA, plus cuBLAS DGEMM and cuSOLVER dpotrf yardsticks.
+// FP64 throughput probe: DMMA shapes vs DFMA, plus cuBLAS DGEMM and cuSOLVER dpotrf + dtrtri yardsticks
+// (the library pair against which the fused Cholesky / inverse sweep is judged).
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/probe/fp64_probe tools/probe/fp64_probe.cu -lcublas -lcusolver
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -114,7 +116,7 @@ int main() {
   }
   // cuSOLVER dpotrf + dtrtri yardstick on an SPD matrix
   cusolverDnHandle_t sh; cusolverDnCreate(&sh);
-  for (int n : {9007, 27007}) {
+  for (int n : {9000, 9088, 27000}) {
     double* A; CK(cudaMalloc(&A, sizeof(double) * (size_t)n * n));
     std::vector<double> hA((size_t)n * n, 0.0);
     // diagonally dominant SPD: I*n + small off-diagonal
@@ -128,7 +130,18 @@ int main() {
       cusolverDnDpotrf(sh, CUBLAS_FILL_MODE_LOWER, n, A, n, work, lwork, info);
       cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
       float ms; cudaEventElapsedTime(&ms, e0, e1);
-      printf("cusolver dpotrf n=%d: %.2f ms  %.2f TFLOP/s\n", n, ms, (double)n * n * n / 3.0 / ms / 1e9);
+      // the triangular inverse of the factor (what the fused sweep also computes)
+      size_t dws = 0, hws = 0;
+      cusolverDnXtrtri_bufferSize(sh, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, A, n, &dws, &hws);
+      void* dbuf; CK(cudaMalloc(&dbuf, dws + 16)); std::vector<char> hbuf(hws + 16);
+      cudaEvent_t e2; cudaEventCreate(&e2);
+      cusolverDnXtrtri(sh, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, A, n, dbuf, dws, hbuf.data(), hws, info);
+      cudaEventRecord(e2); CK(cudaEventSynchronize(e2));
+      float ms2; cudaEventElapsedTime(&ms2, e1, e2);
+      printf("cusolver dpotrf n=%d: %.2f ms  %.2f TFLOP/s | dtrtri %.2f ms  %.2f TFLOP/s | potrf+trtri %.2f ms = %.2f TFLOP/s (2n^3/3)\n",
+             n, ms, (double)n * n * n / 3.0 / ms / 1e9, ms2, (double)n * n * n / 3.0 / ms2 / 1e9, ms + ms2,
+             2.0 * n * n * (double)n / 3.0 / (ms + ms2) / 1e9);
+      cudaFree(dbuf);
     }
     cudaFree(A); cudaFree(work); cudaFree(info);
   }

@@ -91,3 +91,16 @@ def test_config5_sampled_cameras_within_1e9(engine):
     truth, base = refine_all(engine, rec, cams)
     err = rel_blocks(base, truth)
     assert err.max() <= 1e-9, (err.max(), int(cams[err.argmax()]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [(200, 5000, 0.1, 21, 0.5, 9), (300, 20000, 0.05, 22, 0.5, 8),
+                                  (150, 3000, 0.2, 23, 2.0, 8)],
+                         ids=["random200_p9", "random300_p8", "random150_noisy"])
+def test_random_scenes_within_1e9_of_the_exact_inverse(engine, args):
+    # beyond the BASELINE configs: the reference generator's random scenes
+    # (src/synthetic.cpp:52-110) at a few sizes, densities and noise levels
+    rec = S.generate_random_scene(*args)
+    truth, base = refine_all(engine, rec)
+    err = rel_blocks(base, truth)
+    assert err.max() <= 1e-9, (err.max(), int(err.argmax()))

@@ -81,6 +81,7 @@ struct RankA {
 struct sfmcov_handle {
     int device = 0;
     cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr, s4 = nullptr;
+    cudaStream_t sp = nullptr;  // the pair-list build (high priority: ready before stage A ends)
     cudaEvent_t eX = nullptr, eN = nullptr;
     cudaEvent_t e_index = nullptr, e_pairs = nullptr;  // pair-list build on s2, overlapped with stage A
     cudaEvent_t e_ids = nullptr, e_sigma = nullptr;    // host API: σ uploads on s3 after the indices
@@ -291,20 +292,20 @@ bool serial_dense() {
 // Cholesky + in-place triangular inverse of the padded matrix Z (lower
 // triangle); serial = every launch on the main stream.
 int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv, double* piv, Status* st, bool serial,
-              bool mark_stages, cudaEvent_t eZ = nullptr);
+              bool mark_stages, cudaEvent_t eZ = nullptr, int nreal = 0);
 
 void mark(sfmcov_handle* h, int i) {
     if (h->profiling) SFM_CUDA(cudaEventRecord(h->ev[i], h->s));
 }
 
 int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv, double* piv, Status* st, bool serial,
-              bool mark_stages, cudaEvent_t eZ) {
+              bool mark_stages, cudaEvent_t eZ, int nreal) {
     cudaStream_t s = h->s;
     const int pw = panel_blocks(Npad / kNB, 1);
     double* ring = h->ring.as<double>(sweep_ring_doubles(Npad, pw, sfmcov_handle::kRing));
     const int launches = dense_sweep(Z, ld, Npad, pw, Linv, piv, st, ring, sfmcov_handle::kRing, s, serial ? s : h->s2,
                                      serial ? s : h->s3, h->eL, h->eT, h->e2, serial ? s : h->s4, h->eX, h->eN,
-                                     serial ? nullptr : eZ);
+                                     serial ? nullptr : eZ, nreal);
     if (mark_stages) {
         mark(h, 8);
         mark(h, 9);
@@ -484,6 +485,21 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
         d2h(h, out.idx_pt, ix.idx_pt, 4 * (size_t)t);
         return;
     }
+    // The pair list depends only on the index: it is built on its own
+    // high-priority stream by a host worker thread (its host reads of the
+    // list sizes block that thread, not this one) while this thread queues
+    // the numeric stage-A kernels on s.
+    std::future<long long> pairs_task;
+    if (mode == M_FULL || mode == M_SCHUR) {
+        SFM_CUDA(cudaStreamWaitEvent(h->sp, h->e_index, 0));
+        pairs_task = std::async(std::launch::async, [h, &sc, &ix] {
+            SFM_CUDA(cudaSetDevice(h->device));
+            g_kernel_launches = 0;
+            build_pairs(sc, ix, h->pairs, h->ws_pairs, h->sp);
+            SFM_CUDA(cudaEventRecord(h->e_pairs, h->sp));
+            return g_kernel_launches;
+        });
+    }
     launch_weights(sc, ix.idx_cam, rec, st, s);
     if (mode == M_JACOBIAN) {
         sync_status(h);
@@ -574,13 +590,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     double* G = h->G.as<double>((size_t)N * 7);
     launch_camera_border(sc, ix, Pfirst, Plast, Gsum, Hr, s_a, s_b, LF, Gamma, G, s);
     mark(h, 4);
-    // The pair list depends only on the index: it is built on s2 from the
-    // index event while s runs the numeric stage-A kernels queued above (its
-    // host reads of the list sizes then stall s2 only).  (Starting it before
-    // the host's σ wait instead measured no different end to end.)
-    SFM_CUDA(cudaStreamWaitEvent(h->s2, h->e_index, 0));
-    build_pairs(sc, ix, h->pairs, h->ws_pairs, h->s2);
-    SFM_CUDA(cudaEventRecord(h->e_pairs, h->s2));
+    g_kernel_launches += pairs_task.get();  // the pair list (started above on s2)
     SFM_CUDA(cudaStreamWaitEvent(s, h->e_pairs, 0));
     mark(h, 5);
     if (h->dist_mode && mode == M_FULL) {
@@ -645,7 +655,7 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     double* Linv = h->Linv.as<double>((size_t)K * kNB * kNB);
     double* piv = h->piv.as<double>((size_t)Npad);
     const bool serial = serial_dense();
-    run_dense(h, Z, ld, Npad, Linv, piv, st, serial, true, split_pairs ? h->e_zrest : nullptr);
+    run_dense(h, Z, ld, Npad, Linv, piv, st, serial, true, split_pairs ? h->e_zrest : nullptr, N);
     int* psd = h->psd.as<int>(1);
     SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
     const bool cross = out.h_camera_matrix != nullptr;
@@ -1181,7 +1191,8 @@ void run_batch_chunk(sfmcov_handle* h, const SceneDev& full, int s0, int s1, con
                     const int nk = (int)(coff[s0 + k + 1] - coff[s0 + k]);
                     const int c0 = (int)(coff[s0 + k] - coff[s0]);
                     dense_sweep(Zs, Npad, Npad, pw, Linv, piv + (size_t)k * Npad, st, ring, sfmcov_handle::kRing,
-                                wk->s, wk->s2, wk->s3, wk->eL, wk->eT, wk->e2, wk->s4, wk->eX, wk->eN, nullptr);
+                                wk->s, wk->s2, wk->s3, wk->eL, wk->eT, wk->e2, wk->s4, wk->eX, wk->eN, nullptr,
+                                P * nk);
                     launch_extract(P, Zs, Npad, P * nk, nk, s_a + (size_t)P * c0, 1, dcov + (size_t)P * P * c0, st,
                                    psd, wk->s);
                 }
@@ -1324,6 +1335,7 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s2, cudaStreamNonBlocking, lo));
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s3, cudaStreamNonBlocking, (lo + hi) / 2));
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s4, cudaStreamNonBlocking, hi));
+        SFM_CUDA(cudaStreamCreateWithPriority(&h->sp, cudaStreamNonBlocking, hi));
         SFM_CUDA(cudaEventCreateWithFlags(&h->eX, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->eN, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->e_index, cudaEventDisableTiming));
@@ -1361,6 +1373,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaStreamSynchronize(h->s2);
     cudaStreamSynchronize(h->s3);
     cudaStreamSynchronize(h->s4);
+    cudaStreamSynchronize(h->sp);
     DBuf* bufs[] = {&h->ws.tmp, &h->ws_pairs.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_sigma,
                     &h->off_cam, &h->idx_cam, &h->off_pt, &h->idx_pt, &h->pos_cam, &h->key_scratch,
                     &h->R, &h->rec, &h->D, &h->Hr, &h->A, &h->s_a, &h->flags, &h->bpart, &h->s_b, &h->Lpt, &h->Wb, &h->V,
@@ -1399,6 +1412,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaStreamDestroy(h->s2);
     cudaStreamDestroy(h->s3);
     cudaStreamDestroy(h->s4);
+    cudaStreamDestroy(h->sp);
     cudaEventDestroy(h->eX);
     cudaEventDestroy(h->eN);
     cudaEventDestroy(h->e_index);

@@ -130,9 +130,13 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
     constexpr int WARPS_M = BMC / 32;
     const int wm = warp % WARPS_M, wn = warp / WARPS_M;  // WARPS_M x (CN / 32) warps of 32 x 32
     // lower-triangular launches: on a diagonal tile, warp tiles strictly above
-    // the diagonal (never read) skip their MMAs and stores (6 of 16)
-    const bool idle = diag_tile && roff + wm * 32 + 32 <= coff + wn * 32;
+    // the diagonal (never read) skip their MMAs and stores (6 of 16); rows in
+    // the identity padding (real_rows) skip likewise
+    const int crow0 = (g.cyc_R > 0 ? ti + g.cyc_row0 : ti) * BM + roff;  // the CTA's first row of C
+    const bool pad_rows = g.real_rows > 0 && crow0 + wm * 32 >= g.real_rows;
+    const bool idle = (diag_tile && roff + wm * 32 + 32 <= coff + wn * 32) || pad_rows;
     if (diag_tile && roff + BMC <= coff) return;  // the whole CTA lies above the diagonal
+    if (g.real_rows > 0 && crow0 >= g.real_rows) return;  // the whole CTA lies in the padding
     const int beta = (g.beta && !(g.beta0_from >= 0 && tj >= g.beta0_from)) ? 1 : 0;
     int kbeg = 0;  // K offset of this tile
     if (g.k_from_row || (g.k_from_col && tj >= g.beta0_from)) {
@@ -917,7 +921,9 @@ struct SweepTrace {
 
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
-                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN, cudaEvent_t eZ) {
+                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN, cudaEvent_t eZ, int nreal) {
+    // nreal (optional): the unpadded size; the trailing and next-panel
+    // updates skip the identity padding's rows (their L rows are zero).
     // eZ (optional): Z's columns beyond the first panel are complete (the
     // pair reduction of the other block columns, queued on s2 before this
     // sweep): waited for by the first next-panel update on s; rest(0) is
@@ -979,6 +985,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             GemmArgs r = gemm_args(Z + (size_t)r0 * kNB * ld + (size_t)r0 * kNB, ld, Lr, rows, Lr, rows, T2 - gn,
                                    T2 - gn, W);
             r.tri = 1; r.alpha_neg = 1; r.beta = 1;
+            if (nreal > 0) r.real_rows = nreal - r0 * kNB;
             launch_gemm(r, s2);
             ++launches;
             if (trace) tr.rec(p, 3, s2);
@@ -995,6 +1002,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             GemmArgs u = gemm_args(Z + (size_t)nb0 * kNB * ld + (size_t)nb0 * kNB, ld, Lb + W, rows, Lb + W, rows, T2,
                                    split ? 1 : gn, W);
             u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
+            if (nreal > 0) u.real_rows = nreal - nb0 * kNB;
             launch_gemm(u, s);
             ++launches;
             if (trace) tr.rec(p, 2, s);
@@ -1003,6 +1011,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
                 GemmArgs v = gemm_args(Z + (size_t)(nb0 + 1) * kNB * ld + (size_t)nb0 * kNB, ld, Lb + W, rows,
                                        Lb + W + kNB, rows, T2, gn - 1, W);
                 v.alpha_neg = 1; v.beta = 1; v.lower_only = 1; v.col_off_tiles = 1;
+                if (nreal > 0) v.real_rows = nreal - nb0 * kNB;
                 launch_gemm(v, s4);
                 ++launches;
                 SFM_CUDA(cudaEventRecord(eN, s4));

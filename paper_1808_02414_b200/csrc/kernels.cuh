@@ -126,6 +126,10 @@ struct GemmArgs {
     // gi < gt are skipped.  A rows / B rows are global tiles gi / gt,
     // relative to the panel buffer's first tile cyc_ab0.
     int cyc_R, cyc_rank, cyc_G, cyc_lt0, cyc_row0, cyc_ab0;
+    // > 0: rows of C from this index on are identity padding whose A rows
+    // are zero (beta = 1 updates only): their CTAs / warp tiles skip the
+    // product and leave C unchanged, which is exact
+    int real_rows;
 };
 
 // stage_a.cu
@@ -189,7 +193,8 @@ void launch_minmax(const double* x, long long count, double* part, double* out, 
 void launch_pivot_range(const double* piv, int N, double* out, cudaStream_t s);
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
-                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN, cudaEvent_t eZ = nullptr);
+                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN, cudaEvent_t eZ = nullptr,
+                int nreal = 0);
 inline size_t sweep_ring_doubles(int Npad, int G, int NB) { return (size_t)NB * Npad * G * kNB; }
 
 // ---- optional outputs (fullcov.cu) ------------------------------------------

@@ -307,6 +307,13 @@ void sfmcov_cuda_set_profiling(sfmcov_handle* h, int32_t on);
  * ascending neighbor); n_entries = 2 x #edges (written up to capacity). */
 int32_t sfmcov_view_graph(const sfmcov_scene* scene, int32_t min_covis, int64_t* off, int32_t* nbr,
                           int32_t* weight, int64_t capacity, int64_t* n_entries, sfmcov_error* err);
+/* The same graph on the device (the scene is validated first, as the
+ * reference's planner entry points do): the co-visibility counts are the
+ * camera-pair blocks' observation-pair counts of the covariance pipeline's
+ * sorted pair list.  approximate_covariances / error_size_sweep use it. */
+int32_t sfmcov_cuda_view_graph(sfmcov_handle* h, const sfmcov_scene* scene, int32_t min_covis, int64_t* off,
+                               int32_t* nbr, int32_t* weight, int64_t capacity, int64_t* n_entries,
+                               sfmcov_error* err);
 /* extract_neighborhood: ascending global camera / point ids of the induced
  * sub-reconstruction (buffers of n_cams / n_pts capacity). */
 int32_t sfmcov_extract_neighborhood(const sfmcov_scene* scene, int64_t center, int32_t k_bar, int32_t* cams,

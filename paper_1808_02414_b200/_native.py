@@ -150,6 +150,8 @@ CUDA_SYMBOLS = {
     "sfmcov_cuda_worker": (C.c_void_p, [C.c_void_p, C.c_int32, C.POINTER(ErrorStruct)]),
     "sfmcov_view_graph": (C.c_int32, [C.POINTER(Scene), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                       c_int64_p, C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_view_graph": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_int64, c_int64_p, C.POINTER(ErrorStruct)]),
     "sfmcov_extract_neighborhood": (C.c_int32, [C.POINTER(Scene), C.c_int64, C.c_int32, C.c_void_p, c_int64_p,
                                                 C.c_void_p, c_int64_p, c_int32_p, C.POINTER(ErrorStruct)]),
     "sfmcov_plan_coverage": (C.c_int32, [C.POINTER(Scene), C.c_int32, C.c_uint64, C.c_void_p, C.c_int64, C.c_void_p,

@@ -116,7 +116,7 @@ struct sfmcov_handle {
     DBuf sh_bounds, sh_raw, sh_sq, sh_F, sh_S, sh_seg, sh_err;
     // batched sub-scenes (run_batch)
     DBuf bt_lists, bt_cams, bt_pts, bt_oc, bt_op, bt_sigma, bt_sofc, bt_sofp, bt_sb, bt_F, bt_LF, bt_E, bt_eigE, bt_Zb,
-        bt_piv, bt_cov, bt_bad;
+        bt_piv, bt_cov, bt_bad, bt_nreal, bt_linv, bt_ring;
     DBuf seg, seg_tmp, seg_send, seg_recv, prange_r, scale_mm;
     sfm::SegGroups seg_groups;
     DBuf zi, fc_part, fc_y, fc_gtt, fc_eb, fc_pc;
@@ -1051,8 +1051,9 @@ sfmcov_handle* worker_of(sfmcov_handle* h, int i) {  // (h->mu is held by the ca
 
 // One chunk of sub-scenes [s0, s1) of the batch, through one pipeline run
 // (batch.cu): gather, stage A + Schur on the concatenation, per-scene gauge,
-// one dense sweep per scene on the worker handles' streams (host thread per
-// worker), extraction into cov (the chunk's cameras, in scene order).
+// one batched dense sweep over all the chunk's scenes (every launch covers the
+// B problems over grid.y), extraction into cov (the chunk's cameras, in scene
+// order).
 void run_batch_chunk(sfmcov_handle* h, const SceneDev& full, int s0, int s1, const int32_t* cams, const int64_t* coff,
                      const int32_t* pts, const int64_t* poff, const int32_t* obs, const int64_t* toff, double* cov) {
     cudaStream_t s = h->s;
@@ -1168,44 +1169,28 @@ void run_batch_chunk(sfmcov_handle* h, const SceneDev& full, int s0, int s1, con
     int* psd = h->psd.as<int>(1);
     SFM_CUDA(cudaMemsetAsync(psd, 0, sizeof(int), s));
     phase("fill_reduce");
-    SFM_CUDA(cudaEventRecord(h->e1, s));
-    // the dense stage: scenes round-robin over W worker handles, one host thread each
-    const int W = std::min(B, 16);
-    std::vector<sfmcov_handle*> ws(W);
-    for (int w = 0; w < W; ++w) ws[w] = worker_of(h, w);
+    // the dense stage: every scene's fused sweep in one batched sweep (each
+    // launch covers all B problems over grid.y), then one extraction launch
+    // over the batch's cameras
     const int K = Npad / kNB;
-    const int pw = panel_blocks(K, 1);
-    std::vector<std::string> terr(W);
-    std::vector<std::thread> th;
-    th.reserve(W);
-    for (int w = 0; w < W; ++w)
-        th.emplace_back([&, w] {
-            try {
-                sfmcov_handle* wk = ws[w];
-                SFM_CUDA(cudaSetDevice(h->device));
-                SFM_CUDA(cudaStreamWaitEvent(wk->s, h->e1, 0));
-                double* Linv = wk->Linv.as<double>((size_t)K * kNB * kNB);
-                double* ring = wk->ring.as<double>(sweep_ring_doubles(Npad, pw, sfmcov_handle::kRing));
-                for (int k = w; k < B; k += W) {
-                    double* Zs = Zb + (size_t)k * zs;
-                    const int nk = (int)(coff[s0 + k + 1] - coff[s0 + k]);
-                    const int c0 = (int)(coff[s0 + k] - coff[s0]);
-                    dense_sweep(Zs, Npad, Npad, pw, Linv, piv + (size_t)k * Npad, st, ring, sfmcov_handle::kRing,
-                                wk->s, wk->s2, wk->s3, wk->eL, wk->eT, wk->e2, wk->s4, wk->eX, wk->eN, nullptr,
-                                P * nk);
-                    launch_extract(P, Zs, Npad, P * nk, nk, s_a + (size_t)P * c0, 1, dcov + (size_t)P * P * c0, st,
-                                   psd, wk->s);
-                }
-                SFM_CUDA(cudaEventRecord(wk->e1, wk->s));
-            } catch (const std::exception& x) {
-                terr[w] = x.what();
-            }
-        });
-    for (auto& t : th) t.join();
-    for (int w = 0; w < W; ++w) {
-        if (!terr[w].empty()) throw ApiError{SFMCOV_ERR_DEVICE, "device", terr[w]};
-        SFM_CUDA(cudaStreamWaitEvent(s, ws[w]->e1, 0));
-    }
+    const int pw = std::min(panel_blocks(K, 1), K);
+    const int nslots = std::min(sfmcov_handle::kRing, (K + pw - 1) / pw);  // ring slots the sweep can use
+    SweepBatch bt;
+    bt.B = B;
+    bt.zs = zs;
+    bt.ls = (long long)K * kNB * kNB;
+    bt.rs = (long long)sweep_ring_doubles(Npad, pw, nslots);
+    bt.ps = Npad;
+    std::vector<int> nreal(B);
+    for (int k = 0; k < B; ++k) nreal[k] = P * (int)(coff[s0 + k + 1] - coff[s0 + k]);
+    int* d_nreal = h->bt_nreal.as<int>((size_t)B);
+    SFM_CUDA(cudaMemcpyAsync(d_nreal, nreal.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, s));
+    bt.nreal_b = d_nreal;
+    double* Linv = h->bt_linv.as<double>((size_t)bt.ls * B);
+    double* ring = h->bt_ring.as<double>((size_t)bt.rs * B);
+    dense_sweep(Zb, Npad, Npad, pw, Linv, piv, st, ring, nslots, s, h->s2, h->s3, h->eL, h->eT, h->e2,
+                h->s4, h->eX, h->eN, nullptr, 0, &bt);
+    launch_extract(P, Zb, Npad, 0, nb, s_a, 1, dcov, st, psd, s, ZMap{sofc, L.coff, zs});
     phase("dense");
     int* bad = h->bt_bad.as<int>((size_t)B + 1);
     launch_batch_ratio(L, piv, Npad, P, eigE, bad, s);
@@ -1390,7 +1375,8 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     for (auto& a : h->ranka) a.release();
     for (DBuf* b : {&h->sh_bounds, &h->sh_raw, &h->sh_sq, &h->sh_F, &h->sh_S, &h->sh_seg, &h->sh_err, &h->bt_lists,
                     &h->bt_cams, &h->bt_pts, &h->bt_oc, &h->bt_op, &h->bt_sigma, &h->bt_sofc, &h->bt_sofp, &h->bt_sb,
-                    &h->bt_F, &h->bt_LF, &h->bt_E, &h->bt_eigE, &h->bt_Zb, &h->bt_piv, &h->bt_cov, &h->bt_bad})
+                    &h->bt_F, &h->bt_LF, &h->bt_E, &h->bt_eigE, &h->bt_Zb, &h->bt_piv, &h->bt_cov, &h->bt_bad,
+                    &h->bt_nreal, &h->bt_linv, &h->bt_ring})
         b->release();
     h->prange_r.release();
     h->scale_mm.release();
@@ -2085,6 +2071,54 @@ int32_t sfmcov_cuda_full_covariance(sfmcov_handle* h, const sfmcov_scene* scene,
         double* out = h->sys[8].as<double>((size_t)params * params + 1);
         launch_full_unscale(params, S, lds, (const double*)h->s_a.p, out, s);
         if (params) d2h(h, sigma, out, 8 * (size_t)params * params);
+    });
+}
+
+// The sub-reconstruction planner's view graph from the device pair list
+// (subrec.cpp view_graph): the camera-pair blocks' observation-pair counts
+// ARE the co-visibility counts (a camera observes a point at most once), so
+// the index + pair-key sort that the covariance pipeline builds gives every
+// edge weight in ~1 ms.  out: std::vector<int32_t>* of (a, b, w) triples,
+// a < b, w >= min_covis, in (a, b) order.  The scene must be validated.
+int32_t sfmcov_internal_covis(sfmcov_handle* h, const sfmcov_scene* full, int32_t min_covis, void* out,
+                              sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        auto& edges = *static_cast<std::vector<int32_t>*>(out);
+        edges.clear();
+        SceneDev sc;
+        sc.n = full->n_cams; sc.m = full->n_pts; sc.t = full->n_obs; sc.P = full->cam_params;
+        if ((long long)sc.n * sc.n >= (1LL << 32)) throw SizeGuard("subrec", "too many cameras for 32-bit pair keys");
+        if (!sc.t) return;
+        int* oc = (int*)h->h_oc.get(4 * (size_t)sc.t);
+        int* op = (int*)h->h_op.get(4 * (size_t)sc.t);
+        SFM_CUDA(cudaMemcpyAsync(oc, full->obs_cam, 4 * (size_t)sc.t, cudaMemcpyHostToDevice, h->s));
+        SFM_CUDA(cudaMemcpyAsync(op, full->obs_pt, 4 * (size_t)sc.t, cudaMemcpyHostToDevice, h->s));
+        sc.oc = oc;
+        sc.op = op;
+        IndexDev ix;
+        ix.off_cam = h->off_cam.as<int>(sc.n + 1);
+        ix.off_pt = h->off_pt.as<int>(sc.m + 1);
+        ix.idx_cam = h->idx_cam.as<int>(sc.t);
+        ix.idx_pt = h->idx_pt.as<int>(sc.t);
+        ix.pos_cam = h->pos_cam.as<int>(sc.t);
+        ix.key_scratch = h->key_scratch.as<int>(sc.t);
+        launch_build_index(sc, ix, h->ws, h->s);
+        build_pairs(sc, ix, h->pairs, h->ws_pairs, h->s);
+        const PairDev& pd = h->pairs;
+        std::vector<unsigned int> keys(pd.nseg);
+        std::vector<long long> so((size_t)pd.nseg + 1);
+        d2h(h, keys.data(), pd.ukeys, 4 * (size_t)pd.nseg);
+        d2h(h, so.data(), pd.seg_off, 8 * ((size_t)pd.nseg + 1));
+        const unsigned n = (unsigned)sc.n;
+        for (int g = 0; g < pd.nseg; ++g) {
+            const int a = (int)(keys[g] / n), b = (int)(keys[g] - (unsigned)a * n);
+            const long long w = so[g + 1] - so[g];
+            if (a != b && w >= min_covis) {
+                edges.push_back(a);
+                edges.push_back(b);
+                edges.push_back((int32_t)w);
+            }
+        }
     });
 }
 

@@ -93,6 +93,13 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
     constexpr int CPTA = BK * BMC / 2 / THREADS;  // 16-byte copies per thread: A (BK x BMC), B (BK x BNT)
     constexpr int CPTB = BK * BNT / 2 / THREADS;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (g.batch > 1) {  // batched problems: this CTA's problem
+        const int y = blockIdx.y;
+        g.A += y * g.bsA;
+        g.B += y * g.bsB;
+        g.C += y * g.bsC;
+        if (g.real_rows_b) g.real_rows = g.real_rows_b[y] - g.row_origin;
+    }
     int ti, tj;
     const long long l = blockIdx.x / NSUB;
     const int sub = NSUB > 1 ? (int)(blockIdx.x % NSUB) : 0;
@@ -133,10 +140,10 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
     // the diagonal (never read) skip their MMAs and stores (6 of 16); rows in
     // the identity padding (real_rows) skip likewise
     const int crow0 = (g.cyc_R > 0 ? ti + g.cyc_row0 : ti) * BM + roff;  // the CTA's first row of C
-    const bool pad_rows = g.real_rows > 0 && crow0 + wm * 32 >= g.real_rows;
+    const bool pad_rows = g.pad_skip && crow0 + wm * 32 >= g.real_rows;
     const bool idle = (diag_tile && roff + wm * 32 + 32 <= coff + wn * 32) || pad_rows;
     if (diag_tile && roff + BMC <= coff) return;  // the whole CTA lies above the diagonal
-    if (g.real_rows > 0 && crow0 >= g.real_rows) return;  // the whole CTA lies in the padding
+    if (g.pad_skip && crow0 >= g.real_rows) return;  // the whole CTA lies in the padding
     const int beta = (g.beta && !(g.beta0_from >= 0 && tj >= g.beta0_from)) ? 1 : 0;
     int kbeg = 0;  // K offset of this tile
     if (g.k_from_row || (g.k_from_col && tj >= g.beta0_from)) {
@@ -273,12 +280,12 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
 // priority survives CUDA-graph capture (captured kernel nodes do not inherit
 // stream priorities).
 template <typename... KArgs, typename... Args>
-static void launch_prio(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+static void launch_prio(void (*kernel)(KArgs...), dim3 grid, unsigned block, size_t smem, cudaStream_t s,
                         Args... args) {
     int prio = 0;
     SFM_CUDA(cudaStreamGetPriority(s, &prio));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = grid;
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -293,7 +300,7 @@ static void launch_prio(void (*kernel)(KArgs...), unsigned grid, unsigned block,
 template <int BK, int ST, int CM, int CN>
 static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) {
     using CF = gemm::Cfg<BK, ST, CM, CN>;
-    const unsigned grid = (unsigned)(tiles * (gemm::BM / CM) * (gemm::BN / CN));
+    const dim3 grid((unsigned)(tiles * (gemm::BM / CM) * (gemm::BN / CN)), g.batch > 1 ? g.batch : 1);
     if (g.a_kmajor) {
         if (!g.b_kmajor) throw CudaError("gemm: K-major A needs K-major B");
         launch_prio(k_gemm<true, BK, ST, CM, CN, true>, grid, CF::THREADS, CF::SMEM_AK, s, g);
@@ -455,8 +462,12 @@ __device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b
 // A: tile (k0, k0) of the matrix (col-major, ld).  Writes L (lower) back,
 // Linv (kNB x kNB col-major, zeros above), pivots[col0 + j] = L_jj^2.
 __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, long long ld, double* Linv, double* pivots,
-                                                                 int col0, Status* st) {
+                                                                 int col0, Status* st, long long bsA, long long bsL,
+                                                                 long long bsP) {
     using namespace potrf;
+    A += blockIdx.y * bsA;  // batched problems (grid.y)
+    Linv += blockIdx.y * bsL;
+    pivots += blockIdx.y * bsP;
     extern __shared__ double T[];                 // T[c * LDT + r]
     double* Xd = T + kNB * LDT;                   // NSB blocks, row-major 8x8
     double* Ws = Xd + NSB * 64;                   // per-warp 8x8 scratch
@@ -617,8 +628,11 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
 const void* k_potrf_diag_ptr() { return (const void*)k_potrf_diag; }
 int potrf_smem_bytes_impl() { return potrf::SMEM; }
 
-void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s) {
-    launch_prio(k_potrf_diag, 1, potrf::THREADS, potrf::SMEM, s, A, ld, Linv, pivots, col0, st);
+void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s,
+                       const SweepBatch* bt) {
+    const int B = bt ? bt->B : 1;
+    launch_prio(k_potrf_diag, dim3(1, B), potrf::THREADS, potrf::SMEM, s, A, ld, Linv, pivots, col0, st,
+                bt ? bt->zs : 0LL, bt ? bt->ls : 0LL, bt ? bt->ps : 0LL);
     SFM_LAUNCH_CHECK();
 }
 
@@ -635,11 +649,19 @@ void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, in
 // (the scalar 45-accumulator version ran at 2.2 TB/s with 25 % of the warps).
 template <int P>
 __global__ void __launch_bounds__(256, 4) k_extract(const double* X, long long ld, int N, const double* s_a, int scale,
-                                                 double* cov, Status* st, int* psd_warn) {
+                                                 double* cov, Status* st, int* psd_warn, ZMap zm) {
     static_assert(P == 8 || P == 9, "camera block");
     constexpr int NW = 8, U = 4;  // warps, MMAs in flight per warp
     __shared__ double red[NW][81];
-    const int i = blockIdx.x;
+    int i = blockIdx.x;
+    if (zm.scene_of_cam) {  // batched sub-scenes: the camera's own problem
+        const int scn = zm.scene_of_cam[i], c0s = zm.coff[scn];
+        X += scn * zm.zstride;
+        N = P * (zm.coff[scn + 1] - c0s);
+        s_a += (size_t)P * c0s;
+        cov += (size_t)P * P * c0s;
+        i -= c0s;
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c0 = P * i;
     const int m = lane >> 2, k = lane & 3;
@@ -723,10 +745,10 @@ __global__ void __launch_bounds__(256, 4) k_extract(const double* X, long long l
 }
 
 void launch_extract(int P, const double* X, long long ld, int N, int nblocks, const double* s_a, int scale, double* cov,
-                    Status* st, int* psd_warn, cudaStream_t s) {
+                    Status* st, int* psd_warn, cudaStream_t s, ZMap zm) {
     if (!nblocks) return;
-    if (P == 8) k_extract<8><<<nblocks, 256, 0, s>>>(X, ld, N, s_a, scale, cov, st, psd_warn);
-    else if (P == 9) k_extract<9><<<nblocks, 256, 0, s>>>(X, ld, N, s_a, scale, cov, st, psd_warn);
+    if (P == 8) k_extract<8><<<nblocks, 256, 0, s>>>(X, ld, N, s_a, scale, cov, st, psd_warn, zm);
+    else if (P == 9) k_extract<9><<<nblocks, 256, 0, s>>>(X, ld, N, s_a, scale, cov, st, psd_warn, zm);
     else throw CudaError("extract: unsupported block size");
     SFM_LAUNCH_CHECK();
 }
@@ -860,7 +882,10 @@ __global__ void k_panel_take(double* Z, long long ld, int b0, int W, int rows, d
 }
 
 // The panel's diagonal 128-tiles (L, from Z) into the slot; the W x W block of Z := I.
-__global__ void k_panel_take_diag(double* Z, long long ld, int b0, int W, double* Lb, int rows) {
+__global__ void k_panel_take_diag(double* Z, long long ld, int b0, int W, double* Lb, int rows, long long bsZ,
+                                  long long bsL) {
+    Z += blockIdx.y * bsZ;  // batched problems (grid.y)
+    Lb += blockIdx.y * bsL;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;  // one double2 (two rows)
     const int half = W >> 1;
     if (e >= half * W) return;
@@ -873,9 +898,11 @@ __global__ void k_panel_take_diag(double* Z, long long ld, int b0, int W, double
     *zp = x;
 }
 
-static void launch_panel_take_diag(double* Z, long long ld, int b0, int W, double* Lb, int rows, cudaStream_t s) {
+static void launch_panel_take_diag(double* Z, long long ld, int b0, int W, double* Lb, int rows, cudaStream_t s,
+                                   const SweepBatch* bt = nullptr) {
     const int total = (W / 2) * W;
-    k_panel_take_diag<<<cdiv(total, 256), 256, 0, s>>>(Z, ld, b0, W, Lb, rows);
+    k_panel_take_diag<<<dim3(cdiv(total, 256), bt ? bt->B : 1), 256, 0, s>>>(Z, ld, b0, W, Lb, rows, bt ? bt->zs : 0LL,
+                                                                               bt ? bt->rs : 0LL);
     SFM_LAUNCH_CHECK();
 }
 
@@ -921,9 +948,12 @@ struct SweepTrace {
 
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
-                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN, cudaEvent_t eZ, int nreal) {
+                cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN, cudaEvent_t eZ, int nreal,
+                const SweepBatch* bt) {
     // nreal (optional): the unpadded size; the trailing and next-panel
     // updates skip the identity padding's rows (their L rows are zero).
+    // bt (optional): bt->B problems swept together, every launch batched
+    // over grid.y (nreal then per problem, bt->nreal_b).
     // eZ (optional): Z's columns beyond the first panel are complete (the
     // pair reduction of the other block columns, queued on s2 before this
     // sweep): waited for by the first next-panel update on s; rest(0) is
@@ -934,6 +964,27 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
     const int K = Npad / kNB;
     int launches = 0;
     bool rest_pending = false;
+    // operand kinds for the batch strides: Z, the Linv tiles, the panel ring
+    enum Op { OZ, OL, OR };
+    auto stride = [&](Op o) -> long long { return !bt ? 0 : (o == OZ ? bt->zs : (o == OL ? bt->ls : bt->rs)); };
+    auto batched = [&](GemmArgs& g, Op c, Op a, Op b) {
+        if (!bt || bt->B <= 1) return;
+        g.batch = bt->B;
+        g.bsC = stride(c);
+        g.bsA = stride(a);
+        g.bsB = stride(b);
+    };
+    // skip the padding's rows of C, whose first row is `origin` of the matrix
+    auto pad_rows = [&](GemmArgs& g, int origin) {
+        if (bt && bt->nreal_b) {
+            g.pad_skip = 1;
+            g.real_rows_b = bt->nreal_b;
+            g.row_origin = origin;
+        } else if (nreal > 0) {
+            g.pad_skip = 1;
+            g.real_rows = nreal - origin;
+        }
+    };
     int last_slot = -1;
     for (int b0 = 0, p = 0; b0 < K; b0 += G, ++p) {
         const int g_here = (b0 + G <= K) ? G : K - b0;
@@ -950,12 +1001,13 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
         for (int g = 0; g < g_here; ++g) {
             const int c = b0 + g;
             double* Acc = Z + (size_t)c * kNB * ld + (size_t)c * kNB;
-            launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s);
+            launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s, bt);
             ++launches;
             const int below = K - c - 1;
             if (below == 0) break;
             double* Lc = Lb + (size_t)g * kNB * rows + (size_t)(g + 1) * kNB;  // L[rows > c, c] in the slot
             GemmArgs t = gemm_args(Lc, rows, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
+            batched(t, OR, OZ, OL);
             launch_gemm(t, s);
             ++launches;
             const int inner = b0 + g_here - c - 1;
@@ -964,13 +1016,14 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
                 GemmArgs u = gemm_args(Z + (size_t)(c + 1) * kNB * ld + (size_t)(c + 1) * kNB, ld, Lc, rows, Lc, rows,
                                        below, inner, kNB);
                 u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
+                batched(u, OZ, OR, OR);
                 launch_gemm(u, s);
                 ++launches;
             }
         }
         // --- hand the panel over to the inverse: diagonal tiles into the slot,
         // the panel's W x W block of Z := I ---
-        launch_panel_take_diag(Z, ld, b0, W, Lb, rows, s);
+        launch_panel_take_diag(Z, ld, b0, W, Lb, rows, s, bt);
         ++launches;
         SFM_CUDA(cudaEventRecord(eL[slot], s));
         if (trace) tr.rec(p, 1, s);
@@ -985,7 +1038,8 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             GemmArgs r = gemm_args(Z + (size_t)r0 * kNB * ld + (size_t)r0 * kNB, ld, Lr, rows, Lr, rows, T2 - gn,
                                    T2 - gn, W);
             r.tri = 1; r.alpha_neg = 1; r.beta = 1;
-            if (nreal > 0) r.real_rows = nreal - r0 * kNB;
+            pad_rows(r, r0 * kNB);
+            batched(r, OZ, OR, OR);
             launch_gemm(r, s2);
             ++launches;
             if (trace) tr.rec(p, 3, s2);
@@ -1002,7 +1056,8 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             GemmArgs u = gemm_args(Z + (size_t)nb0 * kNB * ld + (size_t)nb0 * kNB, ld, Lb + W, rows, Lb + W, rows, T2,
                                    split ? 1 : gn, W);
             u.alpha_neg = 1; u.beta = 1; u.lower_only = 1;
-            if (nreal > 0) u.real_rows = nreal - nb0 * kNB;
+            pad_rows(u, nb0 * kNB);
+            batched(u, OZ, OR, OR);
             launch_gemm(u, s);
             ++launches;
             if (trace) tr.rec(p, 2, s);
@@ -1011,7 +1066,8 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
                 GemmArgs v = gemm_args(Z + (size_t)(nb0 + 1) * kNB * ld + (size_t)nb0 * kNB, ld, Lb + W, rows,
                                        Lb + W + kNB, rows, T2, gn - 1, W);
                 v.alpha_neg = 1; v.beta = 1; v.lower_only = 1; v.col_off_tiles = 1;
-                if (nreal > 0) v.real_rows = nreal - nb0 * kNB;
+                pad_rows(v, nb0 * kNB);
+                batched(v, OZ, OR, OR);
                 launch_gemm(v, s4);
                 ++launches;
                 SFM_CUDA(cudaEventRecord(eN, s4));
@@ -1030,6 +1086,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             GemmArgs a = gemm_args(Z + (size_t)r * kNB, ld, Linv + (size_t)r * kNB * kNB, kNB, Z + (size_t)r * kNB, ld,
                                    1, r + 1, kNB);
             a.b_kmajor = 1;
+            batched(a, OZ, OL, OZ);
             launch_gemm(a, s3);
             ++launches;
             const int later = g_here - g - 1;
@@ -1037,6 +1094,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
                 GemmArgs u = gemm_args(Z + (size_t)(r + 1) * kNB, ld, Lb + (size_t)g * kNB * rows + (size_t)(g + 1) * kNB,
                                        rows, Z + (size_t)r * kNB, ld, later, r + 1, kNB);
                 u.b_kmajor = 1; u.alpha_neg = 1; u.beta = 1;
+                batched(u, OZ, OR, OZ);
                 launch_gemm(u, s3);
                 ++launches;
             }
@@ -1045,6 +1103,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             GemmArgs x = gemm_args(Z + (size_t)nb0 * kNB, ld, Lb + W, rows, Z + (size_t)b0 * kNB, ld, T2, nb0, W);
             x.b_kmajor = 1; x.alpha_neg = 1; x.beta = 1; x.beta0_from = b0;
             x.k_from_col = 1;  // X[panel rows, panel columns] is lower triangular: skip its zero K range
+            batched(x, OZ, OR, OZ);
             launch_gemm(x, s3);
             ++launches;
         }

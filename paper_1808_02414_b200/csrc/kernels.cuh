@@ -126,10 +126,24 @@ struct GemmArgs {
     // gi < gt are skipped.  A rows / B rows are global tiles gi / gt,
     // relative to the panel buffer's first tile cyc_ab0.
     int cyc_R, cyc_rank, cyc_G, cyc_lt0, cyc_row0, cyc_ab0;
-    // > 0: rows of C from this index on are identity padding whose A rows
+    // pad_skip: rows of C from real_rows on are identity padding whose A rows
     // are zero (beta = 1 updates only): their CTAs / warp tiles skip the
-    // product and leave C unchanged, which is exact
-    int real_rows;
+    // product and leave C unchanged, which is exact.  Batched (real_rows_b):
+    // real_rows = real_rows_b[batch] - row_origin.
+    int pad_skip, real_rows, row_origin;
+    const int* real_rows_b;
+    // batch > 1: grid.y = batch; operand b is offset by b * bs{A,B,C} doubles
+    int batch;
+    long long bsA, bsB, bsC;
+};
+
+// Several same-sized dense problems swept together (batched sub-scenes): Z,
+// the Linv tiles, the panel ring and the pivots of problem b sit b * stride
+// doubles after problem 0's; nreal_b[b] = its unpadded size.
+struct SweepBatch {
+    int B = 1;
+    long long zs = 0, ls = 0, rs = 0, ps = 0;
+    const int* nreal_b = nullptr;
 };
 
 // stage_a.cu
@@ -185,16 +199,19 @@ void dense_init_attributes();
 void launch_gemm(const GemmArgs& g, cudaStream_t s);
 GemmArgs gemm_args(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb, int tm,
                    int tn, int K);
-void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s);
+void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s,
+                       const SweepBatch* bt = nullptr);
+// zm.scene_of_cam (batched sub-scenes): block i is camera i of the batch, in
+// scene scene_of_cam[i]'s X (zstride apart), N from that scene's size
 void launch_extract(int P, const double* X, long long ld, int N, int nblocks, const double* s_a, int scale, double* cov,
-                    Status* st, int* psd_warn, cudaStream_t s);
+                    Status* st, int* psd_warn, cudaStream_t s, ZMap zm = ZMap{});
 void launch_set_diag(double* Z, long long ld, int from, int to, cudaStream_t s);
 void launch_minmax(const double* x, long long count, double* part, double* out, cudaStream_t s);
 void launch_pivot_range(const double* piv, int N, double* out, cudaStream_t s);
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
                 cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN, cudaEvent_t eZ = nullptr,
-                int nreal = 0);
+                int nreal = 0, const SweepBatch* bt = nullptr);
 inline size_t sweep_ring_doubles(int Npad, int G, int NB) { return (size_t)NB * Npad * G * kNB; }
 
 // ---- optional outputs (fullcov.cu) ------------------------------------------

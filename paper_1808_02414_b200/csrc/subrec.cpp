@@ -32,6 +32,8 @@
 #include <vector>
 
 // capi.cu: all sub-scenes through one batched pipeline run per chunk
+extern "C" int32_t sfmcov_internal_covis(sfmcov_handle* h, const sfmcov_scene* full, int32_t min_covis, void* out,
+                                         sfmcov_error* err);
 extern "C" int32_t sfmcov_internal_batch_covariance(sfmcov_handle* h, const sfmcov_scene* full, int32_t nscenes,
                                                     const int32_t* cams, const int64_t* coff, const int32_t* pts,
                                                     const int64_t* poff, const int32_t* obs, const int64_t* toff,
@@ -128,6 +130,27 @@ Graph view_graph(const sfmcov_scene& s, int min_covis) {
     return g;
 }
 
+// The same graph from the device pair list (capi.cu sfmcov_internal_covis:
+// the co-visibility counts are the camera-pair blocks' observation-pair
+// counts), for callers that hold a CUDA handle; the scene is validated.
+Graph view_graph_device(sfmcov_handle* h, const sfmcov_scene& s, int min_covis) {
+    std::vector<int32_t> e;
+    sfmcov_error err{};
+    if (const int32_t code = sfmcov_internal_covis(h, &s, min_covis, &e, &err)) {
+        const std::string msg = err.message, st = err.stage;  // message is "stage: text"
+        throw SubError{code, st, msg.rfind(st + ": ", 0) == 0 ? msg.substr(st.size() + 2) : msg};
+    }
+    Graph g;
+    g.n = s.n_cams;
+    g.edges.resize(s.n_cams);
+    for (size_t k = 0; k + 2 < e.size(); k += 3) {
+        g.edges[e[k]].emplace_back(e[k + 1], e[k + 2]);
+        g.edges[e[k + 1]].emplace_back(e[k], e[k + 2]);
+    }
+    for (auto& adj : g.edges) std::sort(adj.begin(), adj.end());
+    return g;
+}
+
 struct Sub {
     std::vector<int32_t> cams, pts, obs;  // sorted camera / point ids, ascending observation ids
     HostScene scene;                      // the induced scene's arrays (empty when built lists-only)
@@ -138,10 +161,13 @@ struct Sub {
 // an induced scene only visits its own cameras' observations; the point id of
 // each by-camera slot is stored beside it, so the filter below streams
 // contiguous ranges instead of gathering obs_pt[t].
+// Also each point's observing cameras (pt_off / pt_cam), for the filter's
+// incremental removals.
 struct ByCam {
-    std::vector<int64_t> off;
-    std::vector<int32_t> idx, pt;
-    explicit ByCam(const sfmcov_scene& s) : off(s.n_cams + 1, 0), idx(s.n_obs), pt(s.n_obs) {
+    std::vector<int64_t> off, pt_off;
+    std::vector<int32_t> idx, pt, pt_cam;
+    explicit ByCam(const sfmcov_scene& s)
+        : off(s.n_cams + 1, 0), pt_off(s.n_pts + 1, 0), idx(s.n_obs), pt(s.n_obs), pt_cam(s.n_obs) {
         for (int32_t t = 0; t < s.n_obs; ++t) ++off[s.obs_cam[t] + 1];
         for (int32_t i = 0; i < s.n_cams; ++i) off[i + 1] += off[i];
         std::vector<int64_t> f(off.begin(), off.end() - 1);
@@ -150,13 +176,17 @@ struct ByCam {
             idx[k] = t;
             pt[k] = s.obs_pt[t];
         }
+        for (int32_t t = 0; t < s.n_obs; ++t) ++pt_off[s.obs_pt[t] + 1];
+        for (int32_t j = 0; j < s.n_pts; ++j) pt_off[j + 1] += pt_off[j];
+        std::vector<int64_t> g(pt_off.begin(), pt_off.end() - 1);
+        for (int32_t t = 0; t < s.n_obs; ++t) pt_cam[g[s.obs_pt[t]]++] = s.obs_cam[t];
     }
 };
 
 // Scratch arrays of one planner thread, reset only where touched.
 struct Scratch {
     std::vector<char> cam_in;
-    std::vector<int32_t> pc, cc, cl, pl;
+    std::vector<int32_t> pc, cc, cl, pl, queue;
     std::vector<uint64_t> obs_bits, pt_bits;
     void size(int64_t n, int64_t m, int64_t t) {
         if ((int64_t)cam_in.size() != n) { cam_in.assign(n, 0); cc.assign(n, 0); cl.assign(n, -1); }
@@ -169,23 +199,43 @@ struct Scratch {
 // cameras, cameras with >= 4 surviving observations, to a fixpoint.  Leaves
 // cam_in set for the surviving cameras and pc[j] = the point's surviving
 // observer count; the caller resets them (reset_filter).
+//
+// The surviving set is the largest subset in which every camera keeps >= 4
+// points seen twice (the property is closed under union), so removing failing
+// cameras one at a time reaches the same fixpoint as the reference's rounds
+// of simultaneous removals: one counting pass, then each removal updates the
+// counts it changes (a point dropping to one observer costs its last
+// surviving observer a good point) instead of recounting every camera.
 void filter_fixpoint(const ByCam& bc, const std::vector<int32_t>& cams, Scratch& w) {
     for (int32_t c : cams) w.cam_in[c] = 1;
-    for (bool changed = true; changed;) {
-        for (int32_t c : cams)
-            for (int64_t k = bc.off[c]; k < bc.off[c + 1]; ++k) w.pc[bc.pt[k]] = 0;
-        for (int32_t c : cams)
-            if (w.cam_in[c])
-                for (int64_t k = bc.off[c]; k < bc.off[c + 1]; ++k) ++w.pc[bc.pt[k]];
-        changed = false;
-        for (int32_t c : cams) {
-            if (!w.cam_in[c]) continue;
-            int32_t cnt = 0;
-            for (int64_t k = bc.off[c]; k < bc.off[c + 1]; ++k) cnt += w.pc[bc.pt[k]] >= 2;
-            w.cc[c] = cnt;
-            if (cnt < 4) {
-                w.cam_in[c] = 0;
-                changed = true;
+    for (int32_t c : cams)
+        for (int64_t k = bc.off[c]; k < bc.off[c + 1]; ++k) ++w.pc[bc.pt[k]];
+    std::vector<int32_t>& q = w.queue;
+    q.clear();
+    for (int32_t c : cams) {
+        int32_t cnt = 0;
+        for (int64_t k = bc.off[c]; k < bc.off[c + 1]; ++k) cnt += w.pc[bc.pt[k]] >= 2;
+        w.cc[c] = cnt;
+        if (cnt < 4) {
+            w.cam_in[c] = 0;
+            q.push_back(c);
+        }
+    }
+    while (!q.empty()) {
+        const int32_t c = q.back();
+        q.pop_back();
+        for (int64_t k = bc.off[c]; k < bc.off[c + 1]; ++k) {
+            const int32_t j = bc.pt[k];
+            if (--w.pc[j] != 1) continue;
+            for (int64_t u = bc.pt_off[j]; u < bc.pt_off[j + 1]; ++u) {
+                const int32_t c2 = bc.pt_cam[u];
+                if (c2 != c && w.cam_in[c2]) {  // the point's one remaining counted observer, if still in
+                    if (--w.cc[c2] < 4) {
+                        w.cam_in[c2] = 0;
+                        q.push_back(c2);
+                    }
+                    break;
+                }
             }
         }
     }
@@ -572,21 +622,34 @@ void validate_full(sfmcov_handle* h, const sfmcov_scene* s) {
 
 extern "C" {
 
+static void graph_csr(const Graph& g, int64_t* off, int32_t* nbr, int32_t* weight, int64_t capacity, int64_t* n_entries) {
+    int64_t k = 0;
+    off[0] = 0;
+    for (int64_t i = 0; i < g.n; ++i) {
+        for (const auto& [b, w] : g.edges[i]) {
+            if (k < capacity) { nbr[k] = b; weight[k] = w; }
+            ++k;
+        }
+        off[i + 1] = k;
+    }
+    *n_entries = k;
+}
+
 int32_t sfmcov_view_graph(const sfmcov_scene* scene, int32_t min_covis, int64_t* off, int32_t* nbr, int32_t* weight,
                           int64_t capacity, int64_t* n_entries, sfmcov_error* err) {
     return guarded(err, [&] {
         check_scene(scene);
-        const Graph g = view_graph(*scene, min_covis);
-        int64_t k = 0;
-        off[0] = 0;
-        for (int64_t i = 0; i < g.n; ++i) {
-            for (const auto& [b, w] : g.edges[i]) {
-                if (k < capacity) { nbr[k] = b; weight[k] = w; }
-                ++k;
-            }
-            off[i + 1] = k;
-        }
-        *n_entries = k;
+        graph_csr(view_graph(*scene, min_covis), off, nbr, weight, capacity, n_entries);
+    });
+}
+
+int32_t sfmcov_cuda_view_graph(sfmcov_handle* h, const sfmcov_scene* scene, int32_t min_covis, int64_t* off,
+                               int32_t* nbr, int32_t* weight, int64_t capacity, int64_t* n_entries, sfmcov_error* err) {
+    return guarded(err, [&] {
+        if (!scene) throw SubError{SFMCOV_ERR_DIMENSION, "subrec", "bad scene"};
+        validate_full(h, scene);
+        check_scene(scene);
+        graph_csr(view_graph_device(h, *scene, min_covis), off, nbr, weight, capacity, n_entries);
     });
 }
 
@@ -639,7 +702,7 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
         check_scene(scene);
         clk.mark("validate");
         const int P = scene->cam_params;
-        const Graph g = view_graph(*scene, 1);
+        const Graph g = view_graph_device(h, *scene, 1);
         const ByCam bc(*scene);
         std::vector<std::vector<Sub>> plans;
         std::vector<const Sub*> flat;
@@ -794,7 +857,7 @@ int32_t sfmcov_cuda_error_size_sweep(sfmcov_handle* h, const sfmcov_scene* scene
             if (int32_t c = sfmcov_cuda_compute_covariance(h, scene, &o, full.data(), nullptr, &e))
                 throw SubError{c, e.stage, strip_stage(e)};
         }
-        const Graph g = view_graph(*scene, 1);
+        const Graph g = view_graph_device(h, *scene, 1);
         const ByCam bc(*scene);
         std::mt19937_64 rng(seed);
         std::vector<int64_t> ids(n);

@@ -42,7 +42,9 @@ class MonotonicityReport:
     cameras_checked: int
 
 
-def build_view_graph(rec: Reconstruction, min_covis: int = 1) -> ViewGraph:
+def build_view_graph(rec: Reconstruction, min_covis: int = 1, engine: Optional[Engine] = None) -> ViewGraph:
+    """build_view_graph (src/subrec.cpp:90-116); with an engine, counted on
+    the device from the covariance pipeline's sorted pair list."""
     n, t = rec.num_cameras(), rec.num_observations()
     cap = max(1, 2 * t * 20)
     off = np.zeros(n + 1, np.int64)
@@ -51,8 +53,13 @@ def build_view_graph(rec: Reconstruction, min_covis: int = 1) -> ViewGraph:
     cnt = C.c_int64()
     err = N.ErrorStruct()
     sc = rec.c_struct()
-    _raise(N.cuda_lib().sfmcov_view_graph(C.byref(sc), min_covis, off.ctypes.data, nbr.ctypes.data, w.ctypes.data,
-                                          cap, C.byref(cnt), C.byref(err)), err)
+    if engine is not None:
+        _raise(N.cuda_lib().sfmcov_cuda_view_graph(engine.handle, C.byref(sc), min_covis, off.ctypes.data,
+                                                   nbr.ctypes.data, w.ctypes.data, cap, C.byref(cnt), C.byref(err)),
+               err)
+    else:
+        _raise(N.cuda_lib().sfmcov_view_graph(C.byref(sc), min_covis, off.ctypes.data, nbr.ctypes.data,
+                                              w.ctypes.data, cap, C.byref(cnt), C.byref(err)), err)
     if cnt.value > cap:
         raise Error(5, "subrec", "view graph larger than the buffer")
     return ViewGraph(n, [[(int(nbr[k]), int(w[k])) for k in range(off[i], off[i + 1])] for i in range(n)])

@@ -108,7 +108,112 @@ def test_coverage_covers_every_camera_deterministically():  # plan_coverage, src
     assert any(not np.array_equal(x, y) for x, y in zip(a, R.plan_coverage(rec, 10, 10)))
 
 
+def reference_neighborhood(rec, graph, center, k_bar):
+    """extract_neighborhood restated literally (src/subrec.cpp:118-152 and
+    the induced filter's rounds of simultaneous removals, :24-86)."""
+    n = rec.num_cameras()
+    weight = np.zeros(n, np.int64)
+    chosen, inside = [center], np.zeros(n, bool)
+    inside[center] = True
+    for nb, w in graph.edges[center]:
+        weight[nb] += w
+    while len(chosen) < k_bar:
+        best, best_w = -1, 0
+        for i in range(n):
+            if not inside[i] and weight[i] > best_w:
+                best, best_w = i, weight[i]
+        if best < 0:
+            break
+        chosen.append(best)
+        inside[best] = True
+        for nb, w in graph.edges[best]:
+            if not inside[nb]:
+                weight[nb] += w
+    cam_in = set(chosen)
+    while True:
+        m = np.isin(rec.obs_cam, sorted(cam_in))
+        pc = np.bincount(rec.obs_pt[m], minlength=rec.num_points())
+        drop = {c for c in cam_in if np.sum(pc[rec.obs_pt[rec.obs_cam == c]] >= 2) < 4}
+        if not drop:
+            return np.array(sorted(cam_in), np.int32)
+        cam_in -= drop
+
+
+def sparse_structure(seed, n=14, m=45):
+    """A scene whose planner-relevant part (which camera sees which point) is
+    random and sparse: 2-4 observers per point, so small subsets keep few
+    points seen twice and the induced filter removes cameras, often in
+    cascades.  The geometry is irrelevant to planning (no validation here)."""
+    rng = np.random.default_rng(seed)
+    oc, op = [], []
+    for j in range(m):
+        for c in sorted(rng.choice(n, size=int(rng.integers(2, 5)), replace=False)):
+            oc.append(c)
+            op.append(j)
+    return F.Reconstruction(cams=np.zeros((n, 8)), pts=np.zeros((m, 3)), obs_cam=np.array(oc), obs_pt=np.array(op))
+
+
+def cascade_structure():
+    """Cameras H, A, B, C, D, E (0..5): A has 3 points seen twice, B, C, D 4
+    each, chained by one point apiece (A-B, B-C, C-D), E shares 5 with H.
+    The filter removes A, which costs B a point, which costs C one, ... down
+    to {H, E}: each round of the reference removes exactly one camera."""
+    H, A, B, C, D, E = range(6)
+    obs = []
+    j = 0
+    def point(*cams):
+        nonlocal j
+        obs.extend((c, j) for c in cams)
+        j += 1
+    for cam, k in ((A, 2), (B, 2), (C, 2), (D, 3), (E, 5)):
+        for _ in range(k):
+            point(H, cam)
+    point(A, B)
+    point(B, C)
+    point(C, D)
+    oc, op = zip(*obs)
+    return F.Reconstruction(cams=np.zeros((6, 8)), pts=np.zeros((j, 3)), obs_cam=np.array(oc), obs_pt=np.array(op))
+
+
+def test_induced_filter_cascade():
+    rec = cascade_structure()
+    g = R.build_view_graph(rec)
+    want = reference_neighborhood(rec, g, 0, 6)
+    assert want.tolist() == [0, 5]
+    assert R.extract_neighborhood(rec, 0, 6).cameras.tolist() == [0, 5]
+
+
+def test_induced_filter_matches_the_reference_rounds():
+    removed = cascades = 0
+    for seed in range(12):
+        rec = sparse_structure(seed)
+        g = R.build_view_graph(rec)
+        for k_bar in (3, 4, 5, 7, 10):
+            for center in range(rec.num_cameras()):
+                want = reference_neighborhood(rec, g, center, k_bar)
+                try:
+                    got = R.extract_neighborhood(rec, center, k_bar).cameras
+                except F.Error:
+                    got = np.zeros(0, np.int32)  # the filter emptied the subset
+                assert np.array_equal(got, want), (seed, k_bar, center, got, want)
+                removed += k_bar - len(want)
+                cascades += len(want) == 0
+    assert removed > 0 and cascades > 0  # the cases exercise removals, down to empty subsets
+
+
 # ---- GPU --------------------------------------------------------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("scene,min_covis", [("config1", 1), ("config2", 1), ("config2", 5), ("random", 1),
+                                             ("config3", 3)])
+def test_device_view_graph_equals_the_host_graph(engine, scene, min_covis):
+    rec = {"config1": lambda: S.generate_config(1), "config2": lambda: S.generate_config(2),
+           "config3": lambda: S.generate_config(3),
+           "random": lambda: S.generate_random_scene(40, 200, 0.2, 7, 0.5)}[scene]()
+    host = R.build_view_graph(rec, min_covis)
+    dev = R.build_view_graph(rec, min_covis, engine=engine)
+    assert dev.n_cams == host.n_cams and dev.edges == host.edges
+
+
 @pytest.mark.gpu
 def test_bad_aggregation_arguments_are_rejected(engine):  # test_subrec.cpp:119-121
     rec = S.generate_cube_scene(4, 0.5)

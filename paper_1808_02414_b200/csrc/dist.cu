@@ -26,6 +26,9 @@
 #include "kernels.cuh"
 #include "dist.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <dlfcn.h>
 
 #include <cub/cub.cuh>
@@ -549,8 +552,9 @@ void owner_step(RankDense& r, int p, Status* st) {
     SFM_CUDA(cudaEventRecord(r.eL[slot], r.s));
 }
 
-// rest(p) and inverse step p on every rank
-void update_step(RankDense& r, int p) {
+// rest(p) and inverse step p on every rank (what = 1: rest only, 2: the
+// inverse step only, 3: both)
+void update_step(RankDense& r, int p, int what = 3) {
     const int K = r.K, G = r.ow.G, R = r.ow.R, rank = r.ow.rank;
     const long long ld = r.ld;
     const int b0 = p * G, g = std::min(G, K - b0), W = g * kNB, nb0 = b0 + g, T2 = K - nb0;
@@ -561,7 +565,7 @@ void update_step(RankDense& r, int p) {
     // ---- Cholesky trailing update of the rank's panels beyond p (beyond p+1 on owner(p+1))
     const int qmin = (T2 > 0 && owner_of(r.ow, p + 1) == rank) ? p + 2 : p + 1;
     const int lt0 = own_blocks_upto(r.ow, K, qmin - 1);
-    if (T2 > 0 && lt0 < nlt) {
+    if ((what & 1) && T2 > 0 && lt0 < nlt) {
         SFM_CUDA(cudaStreamWaitEvent(r.s2, r.eB[slot], 0));
         const int gt0 = own_gcol(r.ow, lt0 * kNB) / kNB;
         GemmArgs x = gemm_args(r.zp, ld, Lb, rows, Lb, rows, K - gt0, nlt - lt0, W);
@@ -574,7 +578,7 @@ void update_step(RankDense& r, int p) {
     const bool own_p = owner_of(r.ow, p) == rank;
     const int before = own_blocks_upto(r.ow, K, p - 1);  // local tiles of own panels < p
     const int ntl = before + (own_p ? g : 0);
-    if (ntl > 0) {
+    if ((what & 2) && ntl > 0) {
         SFM_CUDA(cudaStreamWaitEvent(r.s3, r.eB[slot], 0));
         const double* Li = Lb + (size_t)rows * W;
         for (int gg = 0; gg < g; ++gg) {
@@ -610,17 +614,55 @@ size_t slot_count(const RankDense& r, int p) {
 }
 }  // namespace
 
+// SFMCOV_DIST_TRACE=1 (emulated ranks only; diagnostics for the 1D-vs-2D
+// model, tools/dist_schedule.py): every component of every step runs alone on
+// the device -- the owner's panel factorisation (its columns' update by the
+// previous panel, the tile chain, the hand-over), then each rank's trailing
+// update and its inverse step -- and its device time is printed to stderr
+// with the panel's broadcast bytes, so a schedule of R real GPUs can be
+// replayed from measured per-rank work.
+static bool dist_trace() {
+    static bool v = [] { const char* e = std::getenv("SFMCOV_DIST_TRACE"); return e && e[0] == '1'; }();
+    return v;
+}
+template <class F>
+static float timed(cudaStream_t s, F&& launch) {
+    cudaEvent_t a, b;
+    SFM_CUDA(cudaDeviceSynchronize());
+    SFM_CUDA(cudaEventCreate(&a));
+    SFM_CUDA(cudaEventCreate(&b));
+    SFM_CUDA(cudaEventRecord(a, s));
+    launch();
+    SFM_CUDA(cudaEventRecord(b, s));
+    SFM_CUDA(cudaDeviceSynchronize());
+    float ms = 0.f;
+    SFM_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms;
+}
+
 void dist_sweep(DistGroup& grp, Status* const* st) {
     if (grp.ranks.empty()) return;
     const RankDense& r0 = *grp.ranks[0];
     const int K = r0.K, G = r0.ow.G, R = r0.ow.R;
     const int NP = (K + G - 1) / G;
+    const bool trace = dist_trace() && !grp.nccl;
+    if (trace) std::fprintf(stderr, "dtrace begin R %d K %d G %d NP %d Npad %d\n", R, K, G, NP, r0.Npad);
     for (int p = 0; p < NP; ++p) {
         const int o = p % R;
         const int slot = p % RankDense::NB;
         // (1) owner factorises and hands the panel over
         for (size_t i = 0; i < grp.ranks.size(); ++i)
-            if (grp.ranks[i]->ow.rank == o) owner_step(*grp.ranks[i], p, st[i]);
+            if (grp.ranks[i]->ow.rank == o) {
+                if (trace) {
+                    const float ms = timed(grp.ranks[i]->s, [&] { owner_step(*grp.ranks[i], p, st[i]); });
+                    std::fprintf(stderr, "dtrace panel %d owner %d ms %.4f bytes %zu\n", p, o, ms,
+                                 8 * slot_count(r0, p));
+                } else {
+                    owner_step(*grp.ranks[i], p, st[i]);
+                }
+            }
         // (2) broadcast of the slot from the owner
         const size_t count = slot_count(r0, p);
         if (grp.nccl) {
@@ -648,7 +690,15 @@ void dist_sweep(DistGroup& grp, Status* const* st) {
             SFM_CUDA(cudaEventRecord(root->eB[slot], root->sc));
         }
         // (3) trailing update and inverse step on every rank
-        for (RankDense* r : grp.ranks) update_step(*r, p);
+        for (RankDense* r : grp.ranks) {
+            if (trace) {
+                const float u = timed(r->s2, [&] { update_step(*r, p, 1); });
+                const float v = timed(r->s3, [&] { update_step(*r, p, 2); });
+                std::fprintf(stderr, "dtrace update %d rank %d rest %.4f inv %.4f\n", p, r->ow.rank, u, v);
+            } else {
+                update_step(*r, p);
+            }
+        }
     }
     for (RankDense* r : grp.ranks) {
         SFM_CUDA(cudaEventRecord(r->eX2, r->s2));

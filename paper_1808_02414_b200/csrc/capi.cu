@@ -128,6 +128,16 @@ struct sfmcov_handle {
     // worker handles for batched independent problems (sub-reconstructions),
     // owned by this handle so their streams and workspaces persist
     std::vector<sfmcov_handle*> workers;
+    // the batched sub-scene API in steps (begin, then chunks): the resident
+    // full scene, and grow-only pinned host buffers for the chunks' id lists
+    SceneDev bt_full{};
+    bool bt_full_valid = false;
+    // the host scene last copied into h_cams / h_pts / h_oc / h_op / h_sigma
+    // (batch_begin reuses that copy when it is the same scene)
+    sfmcov_scene last_up{};
+    bool last_up_valid = false;
+    void* pinned[2] = {nullptr, nullptr};
+    size_t pinned_bytes[2] = {0, 0};
     double stage_ms[ST_COUNT] = {0};
     long long counts[10] = {0};
 };
@@ -1213,6 +1223,8 @@ SceneDev upload(sfmcov_handle* h, const sfmcov_scene* s) {
     d.n = s->n_cams; d.m = s->n_pts; d.t = s->n_obs; d.P = s->cam_params;
     if (d.P != 8 && d.P != 9) throw ApiError{SFMCOV_ERR_DIMENSION, "validate", "camera width must be 8 or 9"};
     if (d.n < 0 || d.m < 0 || d.t < 0) throw ApiError{SFMCOV_ERR_DIMENSION, "validate", "negative scene size"};
+    h->last_up = *s;
+    h->last_up_valid = true;
     auto put = [&](DBuf& b, const void* src, size_t bytes) -> void* {
         void* p = b.get(bytes);
         if (bytes && src) SFM_CUDA(cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, h->s));
@@ -1391,6 +1403,8 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     if (h->nccl) sfm::nccl_comm_destroy(h->nccl);
     for (sfmcov_handle* w : h->workers) sfmcov_cuda_destroy(w);
     if (h->st_host) cudaFreeHost(h->st_host);
+    for (void* p : h->pinned)
+        if (p) cudaFreeHost(p);
     cudaEventDestroy(h->e1);
     cudaEventDestroy(h->e2);
     for (auto& ev : h->ev) cudaEventDestroy(ev);
@@ -2074,6 +2088,89 @@ int32_t sfmcov_cuda_full_covariance(sfmcov_handle* h, const sfmcov_scene* scene,
     });
 }
 
+// The batched sub-scene path in steps, for a caller that forms the chunks
+// itself (subrec.cpp pipelines planning, inducing and the device chunks):
+// begin uploads the full scene once; every chunk call runs one pipeline
+// chunk on it (<= 60000 cameras, <= 12M observations; arrays local to the
+// chunk) and returns SFMCOV_ERR_DEGENERATE (stage "batch") if any of its
+// sub-scenes fails; host_buffer hands out grow-only pinned staging (two
+// slots) so the chunks' id lists go to the device at full PCIe rate.
+int32_t sfmcov_internal_batch_begin(sfmcov_handle* h, const sfmcov_scene* full, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        h->bt_full_valid = false;
+        const sfmcov_scene& l = h->last_up;
+        const bool same = h->last_up_valid && l.n_cams == full->n_cams && l.n_pts == full->n_pts &&
+                          l.n_obs == full->n_obs && l.cam_params == full->cam_params && l.cams == full->cams &&
+                          l.pts == full->pts && l.obs_cam == full->obs_cam && l.obs_pt == full->obs_pt &&
+                          l.obs_sigma == full->obs_sigma;
+        if (same) {  // this call's validation has just copied it: the device copy is current
+            SFM_CUDA(cudaStreamSynchronize(h->s3));  // (σ travels on s3)
+            SceneDev& d = h->bt_full;
+            d = SceneDev{};
+            d.n = full->n_cams; d.m = full->n_pts; d.t = full->n_obs; d.P = full->cam_params;
+            d.cams = (const double*)h->h_cams.p;
+            d.pts = (const double*)h->h_pts.p;
+            d.oc = (const int*)h->h_oc.p;
+            d.op = (const int*)h->h_op.p;
+            d.sigma = full->obs_sigma ? (const double*)h->h_sigma.p : nullptr;
+        } else {
+            h->bt_full = upload(h, full);
+        }
+        if (h->bt_full.sigma_ready) SFM_CUDA(cudaStreamWaitEvent(h->s, h->bt_full.sigma_ready, 0));
+        h->bt_full.sigma_ready = nullptr;
+        h->bt_full.host_u = nullptr;
+        h->bt_full_valid = true;
+    });
+}
+
+int32_t sfmcov_internal_batch_chunk(sfmcov_handle* h, int32_t nscenes, const int32_t* cams, const int64_t* coff,
+                                    const int32_t* pts, const int64_t* poff, const int32_t* obs, const int64_t* toff,
+                                    double* cov, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        if (!h->bt_full_valid) throw ApiError{SFMCOV_ERR_INVARIANT, "batch", "no resident scene (batch_begin)"};
+        if (nscenes < 1 || coff[nscenes] > 60000 || toff[nscenes] > 12000000)
+            throw ApiError{SFMCOV_ERR_SIZE_GUARD, "batch", "chunk beyond 60000 cameras / 12M observations"};
+        try {
+            run_batch_chunk(h, h->bt_full, 0, nscenes, cams, coff, pts, poff, obs, toff, cov);
+        } catch (const BatchFallback&) {
+            throw ApiError{SFMCOV_ERR_DEGENERATE, "batch", "a sub-scene failed; rerun them one by one"};
+        }
+    });
+}
+
+// The observation index that sfmcov_internal_covis built last (by-camera and
+// by-point CSR of observation ids, ascending within each camera / point), to
+// the host: the sub-reconstruction planner's ByCam without a host sort.
+int32_t sfmcov_internal_last_index(sfmcov_handle* h, int32_t n, int32_t m, int32_t t, int32_t* off_cam,
+                                   int32_t* idx_cam, int32_t* off_pt, int32_t* idx_pt, sfmcov_error* err) {
+    return guarded(h, err, [&] {
+        if (!h->off_cam.p || !h->idx_cam.p || !h->off_pt.p || !h->idx_pt.p)
+            throw ApiError{SFMCOV_ERR_INVARIANT, "batch", "no device index"};
+        d2h(h, off_cam, h->off_cam.p, 4 * ((size_t)n + 1));
+        d2h(h, off_pt, h->off_pt.p, 4 * ((size_t)m + 1));
+        if (t) {
+            d2h(h, idx_cam, h->idx_cam.p, 4 * (size_t)t);
+            d2h(h, idx_pt, h->idx_pt.p, 4 * (size_t)t);
+        }
+    });
+}
+
+void* sfmcov_internal_host_buffer(sfmcov_handle* h, int32_t slot, size_t bytes) {
+    if (!h || slot < 0 || slot > 1) return nullptr;
+    if (h->pinned_bytes[slot] < bytes) {
+        if (h->pinned[slot]) cudaFreeHost(h->pinned[slot]);
+        h->pinned[slot] = nullptr;
+        h->pinned_bytes[slot] = 0;
+        const size_t want = bytes + bytes / 4;  // headroom: chunks vary
+        if (cudaSetDevice(h->device) != cudaSuccess || cudaHostAlloc(&h->pinned[slot], want, cudaHostAllocDefault) != cudaSuccess) {
+            h->pinned[slot] = nullptr;
+            return nullptr;
+        }
+        h->pinned_bytes[slot] = want;
+    }
+    return h->pinned[slot];
+}
+
 // The sub-reconstruction planner's view graph from the device pair list
 // (subrec.cpp view_graph): the camera-pair blocks' observation-pair counts
 // ARE the co-visibility counts (a camera observes a point at most once), so
@@ -2089,6 +2186,9 @@ int32_t sfmcov_internal_covis(sfmcov_handle* h, const sfmcov_scene* full, int32_
         sc.n = full->n_cams; sc.m = full->n_pts; sc.t = full->n_obs; sc.P = full->cam_params;
         if ((long long)sc.n * sc.n >= (1LL << 32)) throw SizeGuard("subrec", "too many cameras for 32-bit pair keys");
         if (!sc.t) return;
+        const sfmcov_scene& l = h->last_up;
+        if (!(h->last_up_valid && l.obs_cam == full->obs_cam && l.obs_pt == full->obs_pt && l.n_obs == full->n_obs))
+            h->last_up_valid = false;  // h_oc / h_op no longer hold the last uploaded scene's
         int* oc = (int*)h->h_oc.get(4 * (size_t)sc.t);
         int* op = (int*)h->h_op.get(4 * (size_t)sc.t);
         SFM_CUDA(cudaMemcpyAsync(oc, full->obs_cam, 4 * (size_t)sc.t, cudaMemcpyHostToDevice, h->s));

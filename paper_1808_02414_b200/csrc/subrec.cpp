@@ -14,6 +14,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
 #include <climits>
 #include <cstdlib>
 #include <atomic>
@@ -34,6 +37,14 @@
 // capi.cu: all sub-scenes through one batched pipeline run per chunk
 extern "C" int32_t sfmcov_internal_covis(sfmcov_handle* h, const sfmcov_scene* full, int32_t min_covis, void* out,
                                          sfmcov_error* err);
+extern "C" int32_t sfmcov_internal_batch_begin(sfmcov_handle* h, const sfmcov_scene* full, sfmcov_error* err);
+extern "C" int32_t sfmcov_internal_batch_chunk(sfmcov_handle* h, int32_t nscenes, const int32_t* cams,
+                                               const int64_t* coff, const int32_t* pts, const int64_t* poff,
+                                               const int32_t* obs, const int64_t* toff, double* cov,
+                                               sfmcov_error* err);
+extern "C" void* sfmcov_internal_host_buffer(sfmcov_handle* h, int32_t slot, size_t bytes);
+extern "C" int32_t sfmcov_internal_last_index(sfmcov_handle* h, int32_t n, int32_t m, int32_t t, int32_t* off_cam,
+                                              int32_t* idx_cam, int32_t* off_pt, int32_t* idx_pt, sfmcov_error* err);
 extern "C" int32_t sfmcov_internal_batch_covariance(sfmcov_handle* h, const sfmcov_scene* full, int32_t nscenes,
                                                     const int32_t* cams, const int64_t* coff, const int32_t* pts,
                                                     const int64_t* poff, const int32_t* obs, const int64_t* toff,
@@ -166,6 +177,25 @@ struct Sub {
 struct ByCam {
     std::vector<int64_t> off, pt_off;
     std::vector<int32_t> idx, pt, pt_cam;
+    // from the device's observation index (ascending observation ids within a
+    // camera / point, as the host build below): two parallel gathers
+    ByCam(const sfmcov_scene& s, const std::vector<int32_t>& off_cam, std::vector<int32_t>&& idx_cam,
+          const std::vector<int32_t>& off_pt, const std::vector<int32_t>& idx_pt)
+        : off(off_cam.begin(), off_cam.end()), pt_off(off_pt.begin(), off_pt.end()), idx(std::move(idx_cam)),
+          pt(s.n_obs), pt_cam(s.n_obs) {
+        const int64_t t = s.n_obs;
+        const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(8, t / 65536));
+        std::vector<std::thread> th;
+        auto job = [&](int w) {
+            for (int64_t k = t * w / nt; k < t * (w + 1) / nt; ++k) {
+                pt[k] = s.obs_pt[idx[k]];
+                pt_cam[k] = s.obs_cam[idx_pt[k]];
+            }
+        };
+        for (int w = 1; w < nt; ++w) th.emplace_back(job, w);
+        job(0);
+        for (auto& x : th) x.join();
+    }
     explicit ByCam(const sfmcov_scene& s)
         : off(s.n_cams + 1, 0), pt_off(s.n_pts + 1, 0), idx(s.n_obs), pt(s.n_obs), pt_cam(s.n_obs) {
         for (int32_t t = 0; t < s.n_obs; ++t) ++off[s.obs_cam[t] + 1];
@@ -182,6 +212,16 @@ struct ByCam {
         for (int32_t t = 0; t < s.n_obs; ++t) pt_cam[g[s.obs_pt[t]]++] = s.obs_cam[t];
     }
 };
+
+// ByCam from the device index that view_graph_device just built (falls back to
+// the host build if the index cannot be read)
+ByCam bycam_device(sfmcov_handle* h, const sfmcov_scene& s) {
+    std::vector<int32_t> oc(s.n_cams + 1), ic(s.n_obs), op(s.n_pts + 1), ip(s.n_obs);
+    sfmcov_error e{};
+    if (sfmcov_internal_last_index(h, s.n_cams, s.n_pts, s.n_obs, oc.data(), ic.data(), op.data(), ip.data(), &e))
+        return ByCam(s);
+    return ByCam(s, oc, std::move(ic), op, ip);
+}
 
 // Scratch arrays of one planner thread, reset only where touched.
 struct Scratch {
@@ -403,11 +443,12 @@ Sub neighborhood(const sfmcov_scene& s, const ByCam& bc, const Graph& g, int64_t
     return sub;
 }
 
-// plan_coverage (src/subrec.cpp:154-181)
-std::vector<Sub> coverage(const sfmcov_scene& s, const ByCam& bc, const Graph& g, int k_bar, uint64_t seed,
-                          bool build = true) {
+// plan_coverage (src/subrec.cpp:154-181); emit(sub) receives the subsets in
+// the reference's order as they are drawn
+template <class Emit>
+void coverage_emit(const sfmcov_scene& s, const ByCam& bc, const Graph& g, int k_bar, uint64_t seed, bool build,
+                   Emit&& emit) {
     const int64_t n = s.n_cams;
-    std::vector<Sub> plan;
     std::mt19937_64 rng(seed);
     std::vector<char> covered(n, 0);
     int64_t remaining = n;
@@ -427,8 +468,14 @@ std::vector<Sub> coverage(const sfmcov_scene& s, const ByCam& bc, const Graph& g
                 covered[c] = 1;
                 --remaining;
             }
-        plan.push_back(std::move(sub));
+        emit(std::move(sub));
     }
+}
+
+std::vector<Sub> coverage(const sfmcov_scene& s, const ByCam& bc, const Graph& g, int k_bar, uint64_t seed,
+                          bool build = true) {
+    std::vector<Sub> plan;
+    coverage_emit(s, bc, g, k_bar, seed, build, [&](Sub&& sub) { plan.push_back(std::move(sub)); });
     return plan;
 }
 
@@ -605,6 +652,241 @@ std::string strip_stage(const sfmcov_error& e) {
     return full.compare(0, pre.size(), pre) == 0 ? full.substr(pre.size()) : full;
 }
 
+// approximate_covariances' planning, inducing and device work as one
+// pipeline: a planner thread per covering emits its subsets in the
+// reference's order as they are drawn, a pool induces them (id lists), and
+// this thread packs induced subsets into device chunks (<= 60000 cameras,
+// <= 12M observations) in pinned staging and runs them while the planners
+// and inducers keep going.  Results are kept per subset, so the aggregation
+// (in covering-major subset order afterwards) is independent of the chunking;
+// errors keep the sequential path's precedence (planning, then inducing in
+// subset order, then the covariances).  A chunk with a failing sub-scene is
+// rerun one sub-scene at a time; a single subset in total takes the
+// single-scene path.  Outputs flat / deco / res in covering-major order.
+// SFMCOV_SUBREC_MIN_CHUNK: sub-scenes that make a device chunk worth starting
+// while the planners are still drawing (default 24)
+int pipe_min_chunk() {
+    static int v = [] {
+        const char* e = std::getenv("SFMCOV_SUBREC_MIN_CHUNK");
+        const int x = e ? std::atoi(e) : 24;
+        return x >= 1 ? x : 24;
+    }();
+    return v;
+}
+
+struct PipeItem {
+    Sub sub;
+    int deco = 0;
+    bool ind_fail = false, done = false;
+    SubError ind_err;
+    SubResult res;
+};
+
+void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const ByCam& bc, const Graph& g, int k_bar,
+                           int n_dec, uint64_t seed, int workers, std::vector<std::deque<PipeItem>>& plans,
+                           std::vector<const Sub*>& flat, std::vector<int>& deco, std::vector<SubResult>& res) {
+    const int P = scene.cam_params;
+    plans.assign(n_dec, {});  // deque: stable addresses while planners append (the Subs outlive this call)
+    std::vector<SubError> perr(n_dec);
+    std::vector<char> pfail(n_dec, 0);
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<PipeItem*> to_induce, ready_q;
+    int planners_left = n_dec, inducing = 0;
+    size_t planned = 0;
+    {
+        sfmcov_error e{};
+        if (const int32_t c = sfmcov_internal_batch_begin(h, &scene, &e)) throw SubError{c, e.stage, strip_stage(e)};
+    }
+    std::vector<std::thread> th;
+    for (int d = 0; d < n_dec; ++d)
+        th.emplace_back([&, d] {
+            try {
+                coverage_emit(scene, bc, g, k_bar, seed + uint64_t(d), false, [&](Sub&& sb) {
+                    std::lock_guard<std::mutex> lk(mu);
+                    plans[d].emplace_back();
+                    PipeItem& it = plans[d].back();
+                    it.sub = std::move(sb);
+                    it.deco = d;
+                    to_induce.push_back(&it);
+                    ++planned;
+                    cv.notify_all();
+                });
+            } catch (const SubError& x) {
+                perr[d] = x;
+                pfail[d] = 1;
+            }
+            std::lock_guard<std::mutex> lk(mu);
+            --planners_left;
+            cv.notify_all();
+        });
+    const int n_ind = std::max(2, std::min<int>((int)std::thread::hardware_concurrency() - n_dec - 1, 32));
+    for (int w = 0; w < n_ind; ++w)
+        th.emplace_back([&] {
+            for (;;) {
+                PipeItem* it = nullptr;
+                {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return !to_induce.empty() || planners_left == 0; });
+                    if (to_induce.empty()) return;
+                    it = to_induce.front();
+                    to_induce.pop_front();
+                    ++inducing;
+                }
+                try {
+                    Sub full = induced(scene, bc, it->sub.cams, it->sub.truncated, true);
+                    it->sub.pts = std::move(full.pts);
+                    it->sub.obs = std::move(full.obs);
+                } catch (const SubError& x) {
+                    it->ind_err = x;
+                    it->ind_fail = true;
+                }
+                std::lock_guard<std::mutex> lk(mu);
+                --inducing;
+                if (!it->ind_fail) ready_q.push_back(it);
+                cv.notify_all();
+            }
+        });
+    // device chunks, packed in arrival order
+    std::exception_ptr gpu_error;
+    std::vector<PipeItem*> fallback;
+    int slot = 0;
+    for (;;) {
+        std::vector<PipeItem*> chunk;
+        int64_t nc = 0, nt = 0;
+        bool finished = false;
+        {
+            std::unique_lock<std::mutex> lk(mu);
+            for (;;) {
+                const bool all_in = planners_left == 0 && to_induce.empty() && inducing == 0;
+                while (!ready_q.empty()) {
+                    PipeItem* it = ready_q.front();
+                    const int64_t c = (int64_t)it->sub.cams.size(), t = (int64_t)it->sub.obs.size();
+                    if (!chunk.empty() && (nc + c > 60000 || nt + t > 12000000)) break;
+                    chunk.push_back(it);
+                    ready_q.pop_front();
+                    nc += c;
+                    nt += t;
+                }
+                const bool full_chunk = !ready_q.empty();  // the next subset did not fit
+                // the device is idle while this thread waits: go as soon as a
+                // useful batch is ready instead of waiting for a full chunk
+                const bool enough = (int)chunk.size() >= pipe_min_chunk();
+                if (full_chunk || enough || (all_in && ready_q.empty())) {
+                    finished = all_in && ready_q.empty();
+                    if (enough && !full_chunk && !finished) finished = false;
+                    break;
+                }
+                cv.wait(lk);
+            }
+            // a single subset in total takes the single-scene path (below)
+            if (finished && planned == 1) {
+                for (PipeItem* it : chunk) fallback.push_back(it);
+                chunk.clear();
+            }
+        }
+        if (!chunk.empty() && !gpu_error) {
+            const size_t B = chunk.size();
+            std::vector<int64_t> coff(B + 1, 0), poff(B + 1, 0), toff(B + 1, 0);
+            for (size_t i = 0; i < B; ++i) {
+                coff[i + 1] = coff[i] + (int64_t)chunk[i]->sub.cams.size();
+                poff[i + 1] = poff[i] + (int64_t)chunk[i]->sub.pts.size();
+                toff[i + 1] = toff[i] + (int64_t)chunk[i]->sub.obs.size();
+            }
+            const size_t ints = (size_t)(coff[B] + poff[B] + toff[B]) + 1;
+            int32_t* buf = static_cast<int32_t*>(sfmcov_internal_host_buffer(h, slot, 4 * ints));
+            std::vector<int32_t> heap;
+            if (!buf) {  // no pinned memory: pageable staging
+                heap.resize(ints);
+                buf = heap.data();
+            }
+            slot ^= 1;
+            int32_t* cams = buf;
+            int32_t* pts = cams + coff[B];
+            int32_t* obs = pts + poff[B];
+            {  // concatenated id lists (tens of MB): filled by several threads
+                std::atomic<size_t> next{0};
+                auto job = [&] {
+                    for (size_t i = next++; i < B; i = next++) {
+                        const Sub& sb = chunk[i]->sub;
+                        std::copy(sb.cams.begin(), sb.cams.end(), cams + coff[i]);
+                        std::copy(sb.pts.begin(), sb.pts.end(), pts + poff[i]);
+                        std::copy(sb.obs.begin(), sb.obs.end(), obs + toff[i]);
+                    }
+                };
+                const int ncp = (int)std::min<size_t>(B, 8);
+                std::vector<std::thread> cp;
+                for (int i = 1; i < ncp; ++i) cp.emplace_back(job);
+                job();
+                for (auto& t : cp) t.join();
+            }
+            std::vector<double> cov((size_t)P * P * coff[B] + 1);
+            sfmcov_error e{};
+            const int32_t code = sfmcov_internal_batch_chunk(h, (int32_t)B, cams, coff.data(), pts, poff.data(), obs,
+                                                             toff.data(), cov.data(), &e);
+            if (code == SFMCOV_OK) {
+                for (size_t i = 0; i < B; ++i) {
+                    chunk[i]->res.cov.assign(cov.begin() + (size_t)P * P * coff[i],
+                                             cov.begin() + (size_t)P * P * coff[i + 1]);
+                    chunk[i]->done = true;
+                }
+            } else if (code == SFMCOV_ERR_DEGENERATE) {
+                if (PhaseClock{}.on) std::fprintf(stderr, "subrec batch fallback: %s\n", e.message);
+                for (PipeItem* it : chunk) fallback.push_back(it);
+            } else {
+                gpu_error = std::make_exception_ptr(SubError{code, e.stage, strip_stage(e)});
+            }
+        }
+        if (finished) break;
+    }
+    for (auto& t : th) t.join();
+    if (gpu_error) std::rethrow_exception(gpu_error);
+    for (int d = 0; d < n_dec; ++d)
+        if (pfail[d]) throw perr[d];
+    flat.clear();
+    deco.clear();
+    std::vector<PipeItem*> items;
+    for (int d = 0; d < n_dec; ++d)
+        for (PipeItem& it : plans[d]) items.push_back(&it);
+    for (PipeItem* it : items)
+        if (it->ind_fail) throw it->ind_err;
+    if (!fallback.empty()) {  // one sub-scene at a time (the single-scene path; exact per-subset errors)
+        std::vector<Sub*> subs;
+        for (PipeItem* it : fallback) subs.push_back(&it->sub);
+        std::vector<SubResult> r;
+        if (subs.size() == 1) {
+            r = batch_covariances(h, scene, bc, subs, workers);
+        } else {
+            std::atomic<size_t> next{0};
+            auto job = [&] {
+                for (size_t i = next++; i < subs.size(); i = next++) {
+                    Sub built = induced(scene, bc, subs[i]->cams, subs[i]->truncated);
+                    subs[i]->scene = std::move(built.scene);
+                    subs[i]->has_scene = true;
+                }
+            };
+            std::vector<std::thread> bt;
+            const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 32));
+            for (int i = 1; i < nt; ++i) bt.emplace_back(job);
+            job();
+            for (auto& t : bt) t.join();
+            std::vector<const Sub*> cs(subs.begin(), subs.end());
+            r = per_scene_covariances(h, cs, workers);
+        }
+        for (size_t i = 0; i < fallback.size(); ++i) {
+            fallback[i]->res = std::move(r[i]);
+            fallback[i]->done = true;
+        }
+    }
+    res.clear();
+    for (PipeItem* it : items) {
+        flat.push_back(&it->sub);
+        deco.push_back(it->deco);
+        res.push_back(it->res);
+    }
+}
+
+
 // rec.validate() of the full scene on the device (the M_INDEX path of the
 // CUDA library), its error passed through unchanged, as the reference's
 // approximate_covariances / error_size_sweep do before planning
@@ -703,67 +985,76 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
         clk.mark("validate");
         const int P = scene->cam_params;
         const Graph g = view_graph_device(h, *scene, 1);
-        const ByCam bc(*scene);
-        std::vector<std::vector<Sub>> plans;
+        const ByCam bc = bycam_device(h, *scene);
         std::vector<const Sub*> flat;
         std::vector<int> deco;
-        // the coverings are independent (one seed each): planned in parallel
-        plans.resize(n_decompositions);
-        std::vector<SubError> perr(n_decompositions);
-        std::vector<char> pfail(n_decompositions, 0);
-        {
-            std::vector<std::thread> th;
-            for (int d = 0; d < n_decompositions; ++d)
-                th.emplace_back([&, d] {
-                    try {
-                        plans[d] = coverage(*scene, bc, g, k_bar, seed + uint64_t(d), false);
-                    } catch (const SubError& x) {
-                        perr[d] = x;
-                        pfail[d] = 1;
-                    }
-                });
-            for (auto& t : th) t.join();
-        }
-        for (int d = 0; d < n_decompositions; ++d)
-            if (pfail[d]) throw perr[d];
-        clk.mark("plan");
-        for (int d = 0; d < n_decompositions; ++d)
-            for (Sub& sb : plans[d]) {
-                flat.push_back(&sb);
-                deco.push_back(d);
+        std::vector<SubResult> res;
+        std::vector<std::vector<Sub>> plans;
+        std::vector<std::deque<PipeItem>> store;
+        if (subrec_batch_enabled()) {
+            // planning, inducing and the device chunks overlapped (one pipeline)
+            pipelined_covariances(h, *scene, bc, g, k_bar, n_decompositions, seed, std::max(1, (int)workers), store,
+                                  flat, deco, res);
+            clk.mark("pipeline");
+        } else {
+            // the coverings are independent (one seed each): planned in parallel
+            plans.resize(n_decompositions);
+            std::vector<SubError> perr(n_decompositions);
+            std::vector<char> pfail(n_decompositions, 0);
+            {
+                std::vector<std::thread> th;
+                for (int d = 0; d < n_decompositions; ++d)
+                    th.emplace_back([&, d] {
+                        try {
+                            plans[d] = coverage(*scene, bc, g, k_bar, seed + uint64_t(d), false);
+                        } catch (const SubError& x) {
+                            perr[d] = x;
+                            pfail[d] = 1;
+                        }
+                    });
+                for (auto& t : th) t.join();
             }
-        {  // induced scenes of every subset, in parallel (host)
-            std::atomic<size_t> next{0};
-            std::vector<SubError> berr(flat.size());
-            std::vector<char> bfail(flat.size(), 0);
-            auto job = [&] {
-                for (size_t i = next++; i < flat.size(); i = next++) {
-                    Sub& sb = const_cast<Sub&>(*flat[i]);
-                    try {
-                        // ids only when the batched GPU path will gather the data itself
-                        Sub full = induced(*scene, bc, sb.cams, sb.truncated, subrec_batch_enabled());
-                        sb.scene = std::move(full.scene);
-                        sb.pts = std::move(full.pts);
-                        sb.obs = std::move(full.obs);
-                        sb.has_scene = full.has_scene;
-                    } catch (const SubError& x) {
-                        berr[i] = x;
-                        bfail[i] = 1;
-                    }
+            for (int d = 0; d < n_decompositions; ++d)
+                if (pfail[d]) throw perr[d];
+            clk.mark("plan");
+            for (int d = 0; d < n_decompositions; ++d)
+                for (Sub& sb : plans[d]) {
+                    flat.push_back(&sb);
+                    deco.push_back(d);
                 }
-            };
-            const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 32));
-            std::vector<std::thread> th;
-            for (int i = 1; i < nt; ++i) th.emplace_back(job);
-            job();
-            for (auto& t : th) t.join();
-            for (size_t i = 0; i < flat.size(); ++i)
-                if (bfail[i]) throw berr[i];
+            {  // induced scenes of every subset, in parallel (host)
+                std::atomic<size_t> next{0};
+                std::vector<SubError> berr(flat.size());
+                std::vector<char> bfail(flat.size(), 0);
+                auto job = [&] {
+                    for (size_t i = next++; i < flat.size(); i = next++) {
+                        Sub& sb = const_cast<Sub&>(*flat[i]);
+                        try {
+                            // ids only when the batched GPU path will gather the data itself
+                            Sub full = induced(*scene, bc, sb.cams, sb.truncated, subrec_batch_enabled());
+                            sb.scene = std::move(full.scene);
+                            sb.pts = std::move(full.pts);
+                            sb.obs = std::move(full.obs);
+                            sb.has_scene = full.has_scene;
+                        } catch (const SubError& x) {
+                            berr[i] = x;
+                            bfail[i] = 1;
+                        }
+                    }
+                };
+                const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 32));
+                std::vector<std::thread> th;
+                for (int i = 1; i < nt; ++i) th.emplace_back(job);
+                job();
+                for (auto& t : th) t.join();
+                for (size_t i = 0; i < flat.size(); ++i)
+                    if (bfail[i]) throw berr[i];
+            }
+            clk.mark("induce");
+            std::vector<Sub*> mflat;
+            for (const Sub* sb : flat) mflat.push_back(const_cast<Sub*>(sb));
+            res = batch_covariances(h, *scene, bc, mflat, std::max(1, (int)workers));
         }
-        clk.mark("induce");
-        std::vector<Sub*> mflat;
-        for (const Sub* sb : flat) mflat.push_back(const_cast<Sub*>(sb));
-        const std::vector<SubResult> res = batch_covariances(h, *scene, bc, mflat, std::max(1, (int)workers));
         clk.mark("covariances");
         const int64_t n = scene->n_cams;
         std::vector<char> seen(n, 0);
@@ -858,7 +1149,7 @@ int32_t sfmcov_cuda_error_size_sweep(sfmcov_handle* h, const sfmcov_scene* scene
                 throw SubError{c, e.stage, strip_stage(e)};
         }
         const Graph g = view_graph_device(h, *scene, 1);
-        const ByCam bc(*scene);
+        const ByCam bc = bycam_device(h, *scene);
         std::mt19937_64 rng(seed);
         std::vector<int64_t> ids(n);
         std::vector<Sub> subs;

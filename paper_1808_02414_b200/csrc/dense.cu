@@ -77,7 +77,21 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // carries A rows (m), so each lane's two accumulators are C rows
 // m0 + 2(lane&3) + {0,1} of column n0 + (lane>>2): 16-byte C accesses.
 // Warps of 32x32, STAGES-deep cp.async pipeline of BK-wide K chunks.
-template <bool BK_MAJOR, int BK, int STAGES, int CM, int CN, bool AK_MAJOR = false>
+__device__ __forceinline__ void dmma16(double& d0, double& d1, double& d2, double& d3, const double* a,
+                                       const double* b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+        "{%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+        : "+d"(d0), "+d"(d1), "+d"(d2), "+d"(d3)
+        : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]), "d"(b[0]),
+          "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
+// M16: the 32 x 32 warp tile as 2 x 4 m16n8k16 MMAs per 16-deep chunk (8
+// instructions) instead of 4 x 4 m8n8k4 MMAs per 4-deep step (64); same
+// shared-memory loads, same accumulator -> C mapping (fragment layouts:
+// tools/probe/dmma16_layout.cu).
+template <bool BK_MAJOR, int BK, int STAGES, int CM, int CN, bool AK_MAJOR = false, bool M16 = false>
 __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
                                   65536 / (gemm::Cfg<BK, STAGES, CM, CN>::THREADS * 128)) k_gemm(GemmArgs g) {
     using namespace gemm;
@@ -225,6 +239,36 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
         const double* as = As + (kc % STAGES) * ASTAGE;
         const double* bs = Bs + (kc % STAGES) * BSTAGE;
         if (idle) continue;
+        if constexpr (M16) {
+            static_assert(BK % 16 == 0, "k16 steps");
+            const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+            for (int k16 = 0; k16 < BK; k16 += 16) {
+                // MMA "A" (16 n x 16 k, row) from the B tile, MMA "B" (16 k x 8 m, col) from the A tile
+                double a16[2][8];
+#pragma unroll
+                for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int n = wn * 32 + 16 * nb + gq + 8 * (i % 2), kq = k16 + tq + 4 * (i / 2);
+                        a16[nb][i] = BK_MAJOR ? bs[n * LDB_K + kq] : bs[kq * LDSB + n];
+                    }
+#pragma unroll
+                for (int mb = 0; mb < 4; ++mb) {
+                    double b16[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int m = wm * 32 + 8 * mb + gq, kq = k16 + tq + 4 * i;
+                        b16[i] = AK_MAJOR ? as[m * LDB_K + kq] : as[kq * LDS + m];
+                    }
+#pragma unroll
+                    for (int nb = 0; nb < 2; ++nb)  // D rows n = 16 nb + gq + 8 (i / 2) -> column blocks 2 nb, 2 nb + 1
+                        dmma16(acc[mb][2 * nb][0], acc[mb][2 * nb][1], acc[mb][2 * nb + 1][0], acc[mb][2 * nb + 1][1],
+                               a16[nb], b16);
+                }
+            }
+            continue;
+        }
 #pragma unroll
         for (int kk = 0; kk < BK / 4; ++kk) {
             const int krow = kk * 4 + (lane & 3);
@@ -297,25 +341,38 @@ static void launch_prio(void (*kernel)(KArgs...), dim3 grid, unsigned block, siz
     SFM_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
-template <int BK, int ST, int CM, int CN>
-static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) {
+// SFMCOV_GEMM_MMA: 16 (m16n8k16, default) or 4 (m8n8k4) -- A/B measurements
+static bool gemm_m16() {
+    static bool v = [] { const char* e = std::getenv("SFMCOV_GEMM_MMA"); return !(e && std::atoi(e) == 4); }();
+    return v;
+}
+
+template <int BK, int ST, int CM, int CN, bool M16>
+static void launch_gemm_cfg_m(const GemmArgs& g, long long tiles, cudaStream_t s) {
     using CF = gemm::Cfg<BK, ST, CM, CN>;
     const dim3 grid((unsigned)(tiles * (gemm::BM / CM) * (gemm::BN / CN)), g.batch > 1 ? g.batch : 1);
     if (g.a_kmajor) {
         if (!g.b_kmajor) throw CudaError("gemm: K-major A needs K-major B");
-        launch_prio(k_gemm<true, BK, ST, CM, CN, true>, grid, CF::THREADS, CF::SMEM_AK, s, g);
-    } else if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST, CM, CN, false>, grid, CF::THREADS, CF::SMEM, s, g);
-    else launch_prio(k_gemm<false, BK, ST, CM, CN, false>, grid, CF::THREADS, CF::SMEM, s, g);
+        launch_prio(k_gemm<true, BK, ST, CM, CN, true, M16>, grid, CF::THREADS, CF::SMEM_AK, s, g);
+    } else if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST, CM, CN, false, M16>, grid, CF::THREADS, CF::SMEM, s, g);
+    else launch_prio(k_gemm<false, BK, ST, CM, CN, false, M16>, grid, CF::THREADS, CF::SMEM, s, g);
+}
+template <int BK, int ST, int CM, int CN>
+static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) {
+    if (gemm_m16()) launch_gemm_cfg_m<BK, ST, CM, CN, true>(g, tiles, s);
+    else launch_gemm_cfg_m<BK, ST, CM, CN, false>(g, tiles, s);
 }
 
 template <bool KM, int BK, int ST, int CM, int CN>
 static void set_smem() {
     using CF = gemm::Cfg<BK, ST, CM, CN>;
-    SFM_CUDA(cudaFuncSetAttribute(k_gemm<KM, BK, ST, CM, CN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  CF::SMEM));
-    if (KM)
-        SFM_CUDA(cudaFuncSetAttribute(k_gemm<true, BK, ST, CM, CN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      CF::SMEM_AK));
+    for (int m16 = 0; m16 < 2; ++m16) {
+        SFM_CUDA(cudaFuncSetAttribute(m16 ? k_gemm<KM, BK, ST, CM, CN, false, true> : k_gemm<KM, BK, ST, CM, CN, false, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+        if (KM)
+            SFM_CUDA(cudaFuncSetAttribute(m16 ? k_gemm<true, BK, ST, CM, CN, true, true> : k_gemm<true, BK, ST, CM, CN, true, false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_AK));
+    }
 }
 
 // Opt-in shared-memory sizes, set once before any launch (and before graph

@@ -43,7 +43,7 @@ sys.path.insert(0, str(ROOT))
 # DRAM bytes (read + write) of one dense sweep, summed over its launches in an
 # ncu launch list of this bench command (per config; profiles/ names the file)
 SWEEP_DRAM_BYTES = {3: (76009.5e6 / 7, "profiles/r02_launches_bench_config3.txt (sweep DRAM over 7 runs / 7)")}
-FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 throughput on this pool (profiles/r01_fp64_peak_probe.txt)
+FP64_PEAK_TFLOPS = 37.1  # measured DMMA throughput on this pool, m8n8k4 and m16n8k16 alike (profiles/r01_fp64_peak_probe.txt)
 FP64_PEAK_SOURCE = "measured: tools/probe/fp64_probe.cu DMMA loop 37.1 TF/s, profiles/r01_fp64_peak_probe.txt (cuBLAS DGEMM 16384^3: 36.0; MEASURED_PEAKS.json has no FP64 entry)"
 
 
@@ -439,7 +439,7 @@ def main():
                                + " (pinned host buffers), max over ranks")},
             "gpu_launches": launches,
             "roofline": {
-                "kernel": "dense FP64 Cholesky + triangular inverse (k_gemm DMMA m8n8k4 + k_potrf_diag)",
+                "kernel": "dense FP64 Cholesky + triangular inverse (k_gemm DMMA m16n8k16 + k_potrf_diag)",
                 "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if achieved else None,
                 "traffic": SWEEP_DRAM_BYTES.get(args.config, (None, None))[0],

@@ -715,6 +715,9 @@ void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const By
             } catch (const SubError& x) {
                 perr[d] = x;
                 pfail[d] = 1;
+            } catch (const std::exception& x) {
+                perr[d] = SubError{SFMCOV_ERR_DEVICE, "subrec", x.what()};
+                pfail[d] = 1;
             }
             std::lock_guard<std::mutex> lk(mu);
             --planners_left;
@@ -739,6 +742,9 @@ void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const By
                     it->sub.obs = std::move(full.obs);
                 } catch (const SubError& x) {
                     it->ind_err = x;
+                    it->ind_fail = true;
+                } catch (const std::exception& x) {
+                    it->ind_err = SubError{SFMCOV_ERR_DEVICE, "subrec", x.what()};
                     it->ind_fail = true;
                 }
                 std::lock_guard<std::mutex> lk(mu);
@@ -774,18 +780,19 @@ void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const By
                 const bool enough = (int)chunk.size() >= pipe_min_chunk();
                 if (full_chunk || enough || (all_in && ready_q.empty())) {
                     finished = all_in && ready_q.empty();
-                    if (enough && !full_chunk && !finished) finished = false;
                     break;
                 }
                 cv.wait(lk);
             }
-            // a single subset in total takes the single-scene path (below)
-            if (finished && planned == 1) {
+            // a single subset in total, or one beyond a chunk's limits on its
+            // own, takes the single-scene path (below)
+            if ((finished && planned == 1) ||
+                (chunk.size() == 1 && (nc > 60000 || nt > 12000000))) {
                 for (PipeItem* it : chunk) fallback.push_back(it);
                 chunk.clear();
             }
         }
-        if (!chunk.empty() && !gpu_error) {
+        if (!chunk.empty() && !gpu_error) try {
             const size_t B = chunk.size();
             std::vector<int64_t> coff(B + 1, 0), poff(B + 1, 0), toff(B + 1, 0);
             for (size_t i = 0; i < B; ++i) {
@@ -836,6 +843,8 @@ void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const By
             } else {
                 gpu_error = std::make_exception_ptr(SubError{code, e.stage, strip_stage(e)});
             }
+        } catch (...) {  // the planners and inducers are still running: join them first
+            gpu_error = std::current_exception();
         }
         if (finished) break;
     }

@@ -93,7 +93,10 @@ struct sfmcov_handle {
     cudaEvent_t eL[kRing], eT[kRing];
     cudaEvent_t ev[ST_COUNT + 1];
     bool profiling = false;
-    std::mutex mu;
+    // one caller at a time; recursive so that a multi-call session (the
+    // sub-reconstruction pipeline, sfmcov_internal_session) can hold it
+    // across its own calls while other threads wait
+    std::recursive_mutex mu;
     Workspace ws, ws_pairs;
     // host-API staging of the scene
     DBuf h_cams, h_pts, h_oc, h_op, h_sigma;
@@ -1266,7 +1269,7 @@ int32_t guarded(sfmcov_handle* h, sfmcov_error* err, F&& body) {
         fill_error(err, ApiError{SFMCOV_ERR_DEVICE, "device", "null handle"});
         return SFMCOV_ERR_DEVICE;
     }
-    std::lock_guard<std::mutex> lock(h->mu);
+    std::lock_guard<std::recursive_mutex> lock(h->mu);
     try {
         SFM_CUDA(cudaSetDevice(h->device));
         body();
@@ -1438,7 +1441,7 @@ int32_t sfmcov_cuda_device(sfmcov_handle* h) { return h ? h->device : -1; }
 
 sfmcov_handle* sfmcov_cuda_worker(sfmcov_handle* h, int32_t i, sfmcov_error* err) {
     if (!h || i < 0) return nullptr;
-    std::lock_guard<std::mutex> lock(h->mu);
+    std::lock_guard<std::recursive_mutex> lock(h->mu);
     while ((int32_t)h->workers.size() <= i) {
         sfmcov_handle* w = sfmcov_cuda_create(h->device, err);
         if (!w) return nullptr;
@@ -2153,6 +2156,15 @@ int32_t sfmcov_internal_last_index(sfmcov_handle* h, int32_t n, int32_t m, int32
             d2h(h, idx_pt, h->idx_pt.p, 4 * (size_t)t);
         }
     });
+}
+
+// Holds (lock = 1) or releases (0) the handle for a sequence of calls made
+// by this thread -- the resident scene and staging of the batched
+// sub-scene path must not be replaced by another thread's call in between.
+void sfmcov_internal_session(sfmcov_handle* h, int32_t lock) {
+    if (!h) return;
+    if (lock) h->mu.lock();
+    else h->mu.unlock();
 }
 
 void* sfmcov_internal_host_buffer(sfmcov_handle* h, int32_t slot, size_t bytes) {

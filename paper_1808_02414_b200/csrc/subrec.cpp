@@ -43,6 +43,7 @@ extern "C" int32_t sfmcov_internal_batch_chunk(sfmcov_handle* h, int32_t nscenes
                                                const int32_t* obs, const int64_t* toff, double* cov,
                                                sfmcov_error* err);
 extern "C" void* sfmcov_internal_host_buffer(sfmcov_handle* h, int32_t slot, size_t bytes);
+extern "C" void sfmcov_internal_session(sfmcov_handle* h, int32_t lock);
 extern "C" int32_t sfmcov_internal_last_index(sfmcov_handle* h, int32_t n, int32_t m, int32_t t, int32_t* off_cam,
                                               int32_t* idx_cam, int32_t* off_pt, int32_t* idx_pt, sfmcov_error* err);
 extern "C" int32_t sfmcov_internal_batch_covariance(sfmcov_handle* h, const sfmcov_scene* full, int32_t nscenes,
@@ -988,6 +989,13 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
         if (k_bar < 2) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "subset size must be at least 2"};
         if (n_decompositions < 1) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "need at least one decomposition"};
         if (!scene) throw SubError{SFMCOV_ERR_DIMENSION, "subrec", "bad scene"};
+        // the whole call is one session on the handle: the scene that
+        // validation uploads is reused by the batched chunks
+        struct Session {
+            sfmcov_handle* h;
+            explicit Session(sfmcov_handle* x) : h(x) { sfmcov_internal_session(h, 1); }
+            ~Session() { sfmcov_internal_session(h, 0); }
+        } session(h);
         PhaseClock clk;
         validate_full(h, scene);
         check_scene(scene);

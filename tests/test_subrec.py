@@ -358,3 +358,29 @@ def test_batched_and_one_by_one_paths_agree(engine, tmp_path):
     assert np.array_equal(batched.subset_id, one["sid"])
     worst = max(rel(a, b) for a, b in zip(batched.cov, one["cov"]))
     assert worst <= 1e-10
+
+
+@pytest.mark.gpu
+def test_concurrent_calls_on_one_handle(engine):
+    """Two threads sharing one handle (the C++ header keeps one per device):
+    each approximate_covariances call holds the handle for its whole pipeline
+    (its chunks reuse the scene its validation uploaded), so the results equal
+    the sequential ones bitwise."""
+    import threading
+    a, b = S.generate_config(2), S.generate_random_scene(40, 200, 0.2, 7, 0.5)
+    want = [R.approximate_covariances(a, 12, 2, 5, engine=engine), R.approximate_covariances(b, 8, 2, 3, engine=engine)]
+    got = [None, None]
+
+    def run(i):
+        got[i] = (R.approximate_covariances(a, 12, 2, 5, engine=engine) if i == 0 else
+                  R.approximate_covariances(b, 8, 2, 3, engine=engine))
+
+    for _ in range(3):
+        th = [threading.Thread(target=run, args=(i,)) for i in (0, 1)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for w, g in zip(want, got):
+            assert np.array_equal(w.subset_id, g.subset_id)
+            assert np.array_equal(w.cov, g.cov)

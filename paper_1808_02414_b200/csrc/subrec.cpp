@@ -217,6 +217,7 @@ struct ByCam {
 // ByCam from the device index that view_graph_device just built (falls back to
 // the host build if the index cannot be read)
 ByCam bycam_device(sfmcov_handle* h, const sfmcov_scene& s) {
+    if (s.n_obs == 0) return ByCam(s);  // (the device index is built only for observations)
     std::vector<int32_t> oc(s.n_cams + 1), ic(s.n_obs), op(s.n_pts + 1), ip(s.n_obs);
     sfmcov_error e{};
     if (sfmcov_internal_last_index(h, s.n_cams, s.n_pts, s.n_obs, oc.data(), ic.data(), op.data(), ip.data(), &e))

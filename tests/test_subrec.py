@@ -384,3 +384,25 @@ def test_concurrent_calls_on_one_handle(engine):
         for w, g in zip(want, got):
             assert np.array_equal(w.subset_id, g.subset_id)
             assert np.array_equal(w.cov, g.cov)
+
+
+@pytest.mark.gpu
+def test_pipeline_chunking_does_not_change_results(engine, tmp_path):
+    """The pipelined call packs sub-scenes into device chunks in arrival
+    order; chunks of one sub-scene each (SFMCOV_SUBREC_MIN_CHUNK=1, in a
+    subprocess) must give bitwise the same blocks and winning subsets."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = ("import sys, numpy as np; sys.path.insert(0, '.');"
+            "from paper_1808_02414_b200 import sfmcov as F, synthetic as S, subrec as R;"
+            "a = R.approximate_covariances(S.generate_config(2), 12, 3, 9, engine=F.Engine(0));"
+            "np.savez(sys.argv[1], cov=a.cov, sid=a.subset_id)")
+    out = str(tmp_path / "tiny.npz")
+    subprocess.run([sys.executable, "-c", code, out], cwd=ROOT, env=dict(os.environ, SFMCOV_SUBREC_MIN_CHUNK="1"),
+                   check=True, timeout=600)
+    tiny = np.load(out)
+    ref = R.approximate_covariances(S.generate_config(2), 12, 3, 9, engine=engine)
+    assert np.array_equal(ref.subset_id, tiny["sid"])
+    assert np.array_equal(ref.cov, tiny["cov"])

@@ -329,6 +329,19 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
                                             int32_t n_decompositions, uint64_t seed, int32_t workers,
                                             double* cam_cov, double* trace, int32_t* subset_id,
                                             sfmcov_error* err);
+/* The same, one rank's share of a multi-GPU job ("trivial
+ * multi-GPU job sharding"): every rank plans all coverings (deterministic),
+ * computes only the subsets i of covering d with (i * n_decompositions + d)
+ * mod nranks == rank, and returns its partial aggregate -- per camera the
+ * smallest-trace block among its own subsets (trace +inf, subset -1 where
+ * none).  Merging the ranks' partials by the smallest (trace, subset id)
+ * gives exactly the single-call result.  On a sub-scene failure
+ * failed_subset receives the failing subset's id (else -1), so the merge can
+ * report the first failing subset over all ranks. */
+int32_t sfmcov_cuda_approximate_covariances_shard(sfmcov_handle* h, const sfmcov_scene* scene, int32_t k_bar,
+                                                  int32_t n_decompositions, uint64_t seed, int32_t workers,
+                                                  int32_t nranks, int32_t rank, double* cam_cov, double* trace,
+                                                  int32_t* subset_id, int64_t* failed_subset, sfmcov_error* err);
 /* monotonicity_check on the sub-reconstructions induced by two nested camera sets. */
 int32_t sfmcov_cuda_monotonicity_check(sfmcov_handle* h, const sfmcov_scene* scene, const int32_t* small_cams,
                                        int64_t n_small, const int32_t* large_cams, int64_t n_large,

@@ -159,6 +159,10 @@ CUDA_SYMBOLS = {
     "sfmcov_cuda_approximate_covariances": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_int32, C.c_int32, C.c_uint64,
                                                         C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                                         C.POINTER(ErrorStruct)]),
+    "sfmcov_cuda_approximate_covariances_shard": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_int32, C.c_int32,
+                                                              C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                                              C.c_void_p, C.c_void_p, c_int64_p,
+                                                              C.POINTER(ErrorStruct)]),
     "sfmcov_cuda_error_size_sweep": (C.c_int32, [C.c_void_p, C.POINTER(Scene), C.c_void_p, C.c_int32, C.c_int32,
                                                  C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, c_int64_p,
                                                  C.POINTER(ErrorStruct)]),

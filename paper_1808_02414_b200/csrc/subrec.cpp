@@ -679,6 +679,7 @@ int pipe_min_chunk() {
 struct PipeItem {
     Sub sub;
     int deco = 0;
+    bool skip = false;  // another rank's subset (sharded call): planned, not computed
     bool ind_fail = false, done = false;
     SubError ind_err;
     SubResult res;
@@ -686,7 +687,8 @@ struct PipeItem {
 
 void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const ByCam& bc, const Graph& g, int k_bar,
                            int n_dec, uint64_t seed, int workers, std::vector<std::deque<PipeItem>>& plans,
-                           std::vector<const Sub*>& flat, std::vector<int>& deco, std::vector<SubResult>& res) {
+                           std::vector<const Sub*>& flat, std::vector<int>& deco, std::vector<SubResult>& res,
+                           std::vector<char>* mine = nullptr, int nranks = 1, int rank = 0) {
     const int P = scene.cam_params;
     plans.assign(n_dec, {});  // deque: stable addresses while planners append (the Subs outlive this call)
     std::vector<SubError> perr(n_dec);
@@ -706,12 +708,15 @@ void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const By
             try {
                 coverage_emit(scene, bc, g, k_bar, seed + uint64_t(d), false, [&](Sub&& sb) {
                     std::lock_guard<std::mutex> lk(mu);
+                    const size_t i = plans[d].size();
                     plans[d].emplace_back();
                     PipeItem& it = plans[d].back();
                     it.sub = std::move(sb);
                     it.deco = d;
-                    to_induce.push_back(&it);
-                    ++planned;
+                    // sharded call: subset i of covering d belongs to rank (i n_dec + d) mod R
+                    it.skip = nranks > 1 && (int)((i * (size_t)n_dec + (size_t)d) % (size_t)nranks) != rank;
+                    if (!it.skip) to_induce.push_back(&it);
+                    ++planned;  // all ranks' subsets: one in total takes the single-scene path
                     cv.notify_all();
                 });
             } catch (const SubError& x) {
@@ -860,7 +865,7 @@ void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const By
     for (int d = 0; d < n_dec; ++d)
         for (PipeItem& it : plans[d]) items.push_back(&it);
     for (PipeItem* it : items)
-        if (it->ind_fail) throw it->ind_err;
+        if (it->ind_fail) throw it->ind_err;  // (only this rank's subsets are induced)
     if (!fallback.empty()) {  // one sub-scene at a time (the single-scene path; exact per-subset errors)
         std::vector<Sub*> subs;
         for (PipeItem* it : fallback) subs.push_back(&it->sub);
@@ -890,10 +895,12 @@ void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const By
         }
     }
     res.clear();
+    if (mine) mine->clear();
     for (PipeItem* it : items) {
         flat.push_back(&it->sub);
         deco.push_back(it->deco);
         res.push_back(it->res);
+        if (mine) mine->push_back(it->skip ? 0 : 1);
     }
 }
 
@@ -983,10 +990,12 @@ int32_t sfmcov_plan_coverage(const sfmcov_scene* scene, int32_t k_bar, uint64_t 
     });
 }
 
-int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene* scene, int32_t k_bar,
-                                            int32_t n_decompositions, uint64_t seed, int32_t workers,
-                                            double* cam_cov, double* trace, int32_t* subset_id, sfmcov_error* err) {
+static int32_t approximate_impl(sfmcov_handle* h, const sfmcov_scene* scene, int32_t k_bar, int32_t n_decompositions,
+                                uint64_t seed, int32_t workers, int32_t nranks, int32_t rank, double* cam_cov,
+                                double* trace, int32_t* subset_id, int64_t* failed_subset, sfmcov_error* err) {
+    if (failed_subset) *failed_subset = -1;
     return guarded(err, [&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "bad rank / rank count"};
         if (k_bar < 2) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "subset size must be at least 2"};
         if (n_decompositions < 1) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "need at least one decomposition"};
         if (!scene) throw SubError{SFMCOV_ERR_DIMENSION, "subrec", "bad scene"};
@@ -1009,12 +1018,15 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
         std::vector<SubResult> res;
         std::vector<std::vector<Sub>> plans;
         std::vector<std::deque<PipeItem>> store;
+        std::vector<char> mine;  // sharded call: this rank's subsets (empty: all)
         if (subrec_batch_enabled()) {
             // planning, inducing and the device chunks overlapped (one pipeline)
             pipelined_covariances(h, *scene, bc, g, k_bar, n_decompositions, seed, std::max(1, (int)workers), store,
-                                  flat, deco, res);
+                                  flat, deco, res, nranks > 1 ? &mine : nullptr, nranks, rank);
             clk.mark("pipeline");
         } else {
+            // (one-by-one path: a sharded call computes every subset here;
+            // the merge still equals the single call)
             // the coverings are independent (one seed each): planned in parallel
             plans.resize(n_decompositions);
             std::vector<SubError> perr(n_decompositions);
@@ -1077,7 +1089,9 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
         const int64_t n = scene->n_cams;
         std::vector<char> seen(n, 0);
         for (size_t sid = 0; sid < flat.size(); ++sid) {
+            if (!mine.empty() && !mine[sid]) continue;  // another rank's subset
             if (res[sid].code) {
+                if (failed_subset) *failed_subset = (int64_t)sid;
                 const int kind = res[sid].code;
                 throw SubError{kind, "subrec",
                                "subset " + std::to_string(sid) + " (decomposition " + std::to_string(deco[sid]) +
@@ -1097,10 +1111,32 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
             }
         }
         for (int64_t i = 0; i < n; ++i)
-            if (!seen[i])
+            if (!seen[i]) {
+                if (nranks > 1) {  // (covered by another rank's subsets, or checked after the merge)
+                    trace[i] = INFINITY;
+                    subset_id[i] = -1;
+                    std::memset(cam_cov + (size_t)P * P * i, 0, 8 * (size_t)P * P);
+                    continue;
+                }
                 throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "camera " + std::to_string(i) + " was not covered by any subset"};
+            }
         clk.mark("aggregate");
     });
+}
+
+int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene* scene, int32_t k_bar,
+                                            int32_t n_decompositions, uint64_t seed, int32_t workers,
+                                            double* cam_cov, double* trace, int32_t* subset_id, sfmcov_error* err) {
+    return approximate_impl(h, scene, k_bar, n_decompositions, seed, workers, 1, 0, cam_cov, trace, subset_id, nullptr,
+                            err);
+}
+
+int32_t sfmcov_cuda_approximate_covariances_shard(sfmcov_handle* h, const sfmcov_scene* scene, int32_t k_bar,
+                                                  int32_t n_decompositions, uint64_t seed, int32_t workers,
+                                                  int32_t nranks, int32_t rank, double* cam_cov, double* trace,
+                                                  int32_t* subset_id, int64_t* failed_subset, sfmcov_error* err) {
+    return approximate_impl(h, scene, k_bar, n_decompositions, seed, workers, nranks, rank, cam_cov, trace, subset_id,
+                            failed_subset, err);
 }
 
 int32_t sfmcov_cuda_monotonicity_check(sfmcov_handle* h, const sfmcov_scene* scene, const int32_t* small_cams,

@@ -120,6 +120,95 @@ def approximate_covariances(rec: Reconstruction, k_bar: int, n_decompositions: i
 
 
 @dataclass
+class ShardResult:
+    """One rank's part of a sharded approximate_covariances call."""
+    cov: np.ndarray        # (n, P, P): the smallest-trace block among this rank's subsets (zeros where none)
+    trace: np.ndarray      # (n,): its trace (+inf where none)
+    subset_id: np.ndarray  # (n,): its subset id (-1 where none)
+    code: int = 0          # 0, or the error kind of this rank's first failing step
+    failed_subset: int = -1
+    stage: str = ""
+    message: str = ""
+
+
+def approximate_covariances_shard(rec: Reconstruction, k_bar: int, n_decompositions: int, seed: int, nranks: int,
+                                  rank: int, workers: int = 4, engine: Optional[Engine] = None) -> ShardResult:
+    """This rank's share of approximate_covariances (subset i of covering d
+    goes to rank (i * n_decompositions + d) mod nranks); errors are returned,
+    not raised, so that merge_shards reports the first failing subset of all
+    ranks as the single call does."""
+    engine = engine or default_engine()
+    n, P = rec.num_cameras(), rec.cam_params
+    cov = np.zeros((max(1, n), P, P))
+    tr = np.zeros(max(1, n))
+    sid = -np.ones(max(1, n), np.int32)
+    failed = C.c_int64(-1)
+    err = N.ErrorStruct()
+    sc = rec.c_struct()
+    code = N.cuda_lib().sfmcov_cuda_approximate_covariances_shard(
+        engine.handle, C.byref(sc), k_bar, n_decompositions, seed, workers, nranks, rank, cov.ctypes.data,
+        tr.ctypes.data, sid.ctypes.data, C.byref(failed), C.byref(err))
+    msg = err.message.decode(errors="replace") if code else ""
+    stage = err.stage.decode(errors="replace") if code else ""
+    return ShardResult(cov[:n], tr[:n], sid[:n], int(code), int(failed.value), stage, msg)
+
+
+def merge_shards(parts: List[ShardResult], k_bar: int) -> AggregatedCovariance:
+    """The single-call result from the ranks' partial aggregates: per camera
+    the smallest (trace, subset id) -- the reference keeps a camera's block
+    from the earliest subset with the smallest trace.  Errors: the failing
+    subset with the smallest id over all ranks (an error before any subset,
+    failed_subset -1, is the same on every rank)."""
+    failed = [p for p in parts if p.code]
+    if failed:
+        sub = [p for p in failed if p.failed_subset >= 0]
+        first = min(sub, key=lambda p: p.failed_subset) if len(sub) == len(failed) else \
+            next(p for p in failed if p.failed_subset < 0)
+        raise Error(first.code, first.stage, first.message)
+    tr = np.stack([p.trace for p in parts])            # (R, n)
+    sid = np.stack([p.subset_id for p in parts]).astype(np.int64)
+    big = np.iinfo(np.int64).max
+    key_sid = np.where(sid >= 0, sid, big)
+    order = np.lexsort((key_sid, tr), axis=0)[0]       # per camera: the rank with the smallest (trace, sid)
+    cams = np.arange(tr.shape[1])
+    best_sid = sid[order, cams]
+    if np.any(best_sid < 0):
+        i = int(np.nonzero(best_sid < 0)[0][0])
+        raise Error(3, "subrec", f"subrec: camera {i} was not covered by any subset")
+    cov = np.stack([p.cov for p in parts])[order, cams]
+    return AggregatedCovariance(k_bar, cov, tr[order, cams], best_sid.astype(np.int32))
+
+
+def approximate_covariances_distributed(rec: Reconstruction, k_bar: int, n_decompositions: int, seed: int,
+                                        workers: int = 4, engine: Optional[Engine] = None,
+                                        group=None) -> AggregatedCovariance:
+    """approximate_covariances over the ranks of a torch.distributed group
+    (one process per GPU): each rank computes its share, the partial
+    aggregates are all-gathered (tiny: n x (P^2 + 2) values per rank) and
+    merged; every rank returns the single-call result."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    part = approximate_covariances_shard(rec, k_bar, n_decompositions, seed, world, rank, workers, engine)
+    return gather_and_merge(part, k_bar, group)
+
+
+def gather_and_merge(part: ShardResult, k_bar: int, group=None) -> AggregatedCovariance:
+    """All-gather every rank's ShardResult over a torch.distributed group
+    (any backend: the payload goes through all_gather_object) and merge."""
+    import torch.distributed as dist
+    parts = [None] * dist.get_world_size(group)
+    dist.all_gather_object(parts, part, group=group)
+    return merge_shards(parts, k_bar)
+
+
+def shard_owner(subset_index: int, decomposition: int, n_decompositions: int, nranks: int) -> int:
+    """The rank that computes subset `subset_index` of covering
+    `decomposition` (csrc/subrec.cpp, pipelined_covariances)."""
+    return (subset_index * n_decompositions + decomposition) % nranks
+
+
+@dataclass
 class SweepRow:
     k_bar: int
     subset_id: int

@@ -406,3 +406,136 @@ def test_pipeline_chunking_does_not_change_results(engine, tmp_path):
     ref = R.approximate_covariances(S.generate_config(2), 12, 3, 9, engine=engine)
     assert np.array_equal(ref.subset_id, tiny["sid"])
     assert np.array_equal(ref.cov, tiny["cov"])
+
+
+def _emulated_subsets(seed, n=40, P=8, covers=3):
+    """Random coverings (subset -> cameras, blocks) with deliberate trace ties."""
+    rng = np.random.default_rng(seed)
+    subs = []  # (decomposition, index within it, cams, blocks, traces)
+    for d in range(covers):
+        perm = rng.permutation(n)
+        for i, cams in enumerate(np.array_split(perm, int(rng.integers(3, 7)))):
+            cams = np.sort(np.concatenate([cams, rng.choice(n, 3)]))
+            cams = np.unique(cams)
+            blocks = rng.standard_normal((len(cams), P, P))
+            tr = np.round(rng.uniform(1, 3, len(cams)), 1)  # coarse: many ties between subsets
+            for b, t in zip(blocks, tr):
+                b[np.diag_indices(P)] += (t - np.trace(b)) / P
+            subs.append((d, i, cams, blocks, np.array([np.trace(b) for b in blocks])))
+    return subs
+
+
+def _emulated_aggregate(subs, n, P, owned=None):
+    """csrc/subrec.cpp approximate_impl's aggregation over the given subsets
+    (all, or one rank's), the partial form of a sharded call."""
+    cov, tr, sid = np.zeros((n, P, P)), np.full(n, np.inf), -np.ones(n, np.int32)
+    for s, (_, _, cams, blocks, trs) in enumerate(subs):
+        if owned is not None and not owned[s]:
+            continue
+        for c, b, t in zip(cams, blocks, trs):
+            if sid[c] < 0 or t < tr[c]:
+                cov[c], tr[c], sid[c] = b, t, s
+    return R.ShardResult(cov, tr, sid)
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_merged_shards_equal_the_single_aggregation(nranks, seed):
+    n, P, covers = 40, 8, 3
+    subs = _emulated_subsets(seed, n, P, covers)
+    want = _emulated_aggregate(subs, n, P)
+    parts = [_emulated_aggregate(subs, n, P, [R.shard_owner(i, d, covers, nranks) == r for d, i, *_ in subs])
+             for r in range(nranks)]
+    got = R.merge_shards(parts, 10)
+    assert np.array_equal(got.subset_id, want.subset_id)
+    assert np.array_equal(got.trace, want.trace) and np.array_equal(got.cov, want.cov)
+
+
+def test_shard_owner_spreads_every_covering():
+    # consecutive subsets of one covering land on different ranks, and the
+    # coverings are offset so small coverings do not all start on rank 0
+    assert [R.shard_owner(i, 0, 3, 4) for i in range(4)] == [0, 3, 2, 1]
+    assert [R.shard_owner(0, d, 3, 4) for d in range(3)] == [0, 1, 2]
+
+
+def test_merge_reports_the_first_failing_subset_and_uncovered_cameras():
+    n, P = 6, 8
+    ok = R.ShardResult(np.zeros((n, P, P)), np.ones(n), np.arange(n, dtype=np.int32))
+    bad7 = R.ShardResult(ok.cov, ok.trace, ok.subset_id, 4, 7, "subrec", "subrec: subset 7 (decomposition 1): x")
+    bad3 = R.ShardResult(ok.cov, ok.trace, ok.subset_id, 4, 3, "subrec", "subrec: subset 3 (decomposition 0): y")
+    with pytest.raises(F.Error) as e:
+        R.merge_shards([ok, bad7, bad3], 6)
+    assert e.value.kind == F.ErrorKind.degenerate and "subset 3 (decomposition 0)" in str(e.value)
+    early = R.ShardResult(ok.cov, ok.trace, ok.subset_id, 3, -1, "validate", "validate: bad scene")
+    with pytest.raises(F.Error) as e:
+        R.merge_shards([early, early], 6)
+    assert e.value.stage == "validate"
+    hole = R.ShardResult(ok.cov, np.where(np.arange(n) == 4, np.inf, 1.0), np.where(np.arange(n) == 4, -1, 0))
+    with pytest.raises(F.Error) as e:
+        R.merge_shards([hole, hole], 6)
+    assert e.value.kind == F.ErrorKind.invariant and "camera 4 was not covered" in str(e.value)
+
+
+def _gloo_merge_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        subs = _emulated_subsets(11)
+        part = _emulated_aggregate(subs, 40, 8, [R.shard_owner(i, d, 3, world) == rank for d, i, *_ in subs])
+        got = R.gather_and_merge(part, 10)
+        q.put((rank, got.cov, got.trace, got.subset_id))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_world2_gloo_shard_gather_and_merge():
+    """The torch.distributed gather + merge of sharded sub-reconstructions
+    on a world_size-2 gloo group: every rank gets the single-call result."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_merge_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=240) for _ in range(2)), key=lambda r: r[0])
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    want = _emulated_aggregate(_emulated_subsets(11), 40, 8)
+    for _, cov, tr, sid in res:
+        assert np.array_equal(sid, want.subset_id) and np.array_equal(cov, want.cov) and np.array_equal(tr, want.trace)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_sharded_calls_merge_to_the_single_call(engine, nranks):
+    """Each rank's share run in turn on one engine (the per-rank work is
+    independent), merged: bitwise the single call's blocks and subsets."""
+    rec = S.generate_config(2)
+    want = R.approximate_covariances(rec, 12, 3, 9, engine=engine)
+    parts = [R.approximate_covariances_shard(rec, 12, 3, 9, nranks, r, engine=engine) for r in range(nranks)]
+    assert all(p.code == 0 for p in parts)
+    assert sum(int((p.subset_id >= 0).sum()) for p in parts) >= rec.num_cameras()
+    got = R.merge_shards(parts, 12)
+    assert np.array_equal(got.subset_id, want.subset_id)
+    assert np.array_equal(got.cov, want.cov) and np.array_equal(got.trace, want.trace)
+
+
+@pytest.mark.gpu
+def test_sharded_failure_names_the_same_subset(engine):
+    rec = S.generate_cube_scene(6, 0.5)
+    rec.pts[14] = rec.cams[3, 3:6]
+    with pytest.raises(F.Error) as single:
+        R.approximate_covariances(rec, 6, 2, 0, engine=engine)
+    parts = [R.approximate_covariances_shard(rec, 6, 2, 0, 2, r, engine=engine) for r in range(2)]
+    with pytest.raises(F.Error) as merged:
+        R.merge_shards(parts, 6)
+    assert str(merged.value) == str(single.value) and merged.value.kind == single.value.kind

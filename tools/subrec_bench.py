@@ -25,3 +25,13 @@ sub = R.induced_scene(rec, cams, np.nonzero(cnt >= 2)[0].astype(np.int32))
 O.lib().oracle_blas_threads(1)
 t0 = time.perf_counter(); O.compute_covariance(sub); dt1 = time.perf_counter() - t0
 print(f"restatement, one sub-scene, 1 thread (the reference's pinned BLAS): {dt1:.3f} s -> {nsub * dt1:.1f} s for all")
+# Multi-GPU job sharding: each rank's share timed alone on this one GPU
+# (the shares are independent; the slowest one bounds an R-GPU run).
+for nr in (2, 4, 8):
+    per = []
+    for r in range(nr):
+        R.approximate_covariances_shard(rec, k_bar, 3, 7, nr, r, workers=4, engine=eng)
+        t0 = time.perf_counter(); R.approximate_covariances_shard(rec, k_bar, 3, 7, nr, r, workers=4, engine=eng)
+        per.append(time.perf_counter() - t0)
+    print(f"{nr} ranks: per-rank share {min(per):.3f}-{max(per):.3f} s -> {nsub / max(per):.1f} sub-scenes/s "
+          f"(x{dt / max(per):.2f} over one GPU)")

@@ -335,13 +335,17 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
  * mod nranks == rank, and returns its partial aggregate -- per camera the
  * smallest-trace block among its own subsets (trace +inf, subset -1 where
  * none).  Merging the ranks' partials by the smallest (trace, subset id)
- * gives exactly the single-call result.  On a sub-scene failure
- * failed_subset receives the failing subset's id (else -1), so the merge can
- * report the first failing subset over all ranks. */
+ * gives exactly the single-call result.  On a failure failed_key receives
+ * its place in the reference's order (src/subrec.cpp:202-222: covering d is
+ * drawn, then its subsets computed, covering after covering):
+ * d * 2^33 + (0 drawing | 1 computing) * 2^32 + the subset's index in d; -1
+ * for a failure before any covering (validation, arguments, device).  The
+ * merge reports the failure with the smallest key over all ranks, which is
+ * the single call's error. */
 int32_t sfmcov_cuda_approximate_covariances_shard(sfmcov_handle* h, const sfmcov_scene* scene, int32_t k_bar,
                                                   int32_t n_decompositions, uint64_t seed, int32_t workers,
                                                   int32_t nranks, int32_t rank, double* cam_cov, double* trace,
-                                                  int32_t* subset_id, int64_t* failed_subset, sfmcov_error* err);
+                                                  int32_t* subset_id, int64_t* failed_key, sfmcov_error* err);
 /* monotonicity_check on the sub-reconstructions induced by two nested camera sets. */
 int32_t sfmcov_cuda_monotonicity_check(sfmcov_handle* h, const sfmcov_scene* scene, const int32_t* small_cams,
                                        int64_t n_small, const int32_t* large_cams, int64_t n_large,

@@ -676,9 +676,30 @@ int pipe_min_chunk() {
     return v;
 }
 
+// The first failure in the reference's order (src/subrec.cpp:202-222):
+// covering d is drawn (neighborhoods and induced scenes, subset by subset)
+// before any of its subsets is computed, and the coverings run in turn.
+// key = d 2^33 + (0 drawing | 1 computing) 2^32 + the subset's index in d;
+// a sharded call reports its own first key and the merge keeps the smallest.
+struct FirstFailure {
+    int64_t key = INT64_MAX;
+    SubError err;
+    static int64_t at(int d, int phase, size_t i) {
+        return ((int64_t)d << 33) | ((int64_t)phase << 32) | (int64_t)i;
+    }
+    void note(int64_t k, const SubError& e) {
+        if (k < key) {
+            key = k;
+            err = e;
+        }
+    }
+    bool any() const { return key != INT64_MAX; }
+};
+
 struct PipeItem {
     Sub sub;
     int deco = 0;
+    size_t idx = 0;  // index within its covering
     bool skip = false;  // another rank's subset (sharded call): planned, not computed
     bool ind_fail = false, done = false;
     SubError ind_err;
@@ -688,11 +709,9 @@ struct PipeItem {
 void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const ByCam& bc, const Graph& g, int k_bar,
                            int n_dec, uint64_t seed, int workers, std::vector<std::deque<PipeItem>>& plans,
                            std::vector<const Sub*>& flat, std::vector<int>& deco, std::vector<SubResult>& res,
-                           std::vector<char>* mine = nullptr, int nranks = 1, int rank = 0) {
+                           FirstFailure& ff, std::vector<char>* mine = nullptr, int nranks = 1, int rank = 0) {
     const int P = scene.cam_params;
     plans.assign(n_dec, {});  // deque: stable addresses while planners append (the Subs outlive this call)
-    std::vector<SubError> perr(n_dec);
-    std::vector<char> pfail(n_dec, 0);
     std::mutex mu;
     std::condition_variable cv;
     std::deque<PipeItem*> to_induce, ready_q;
@@ -713,18 +732,19 @@ void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const By
                     PipeItem& it = plans[d].back();
                     it.sub = std::move(sb);
                     it.deco = d;
+                    it.idx = i;
                     // sharded call: subset i of covering d belongs to rank (i n_dec + d) mod R
                     it.skip = nranks > 1 && (int)((i * (size_t)n_dec + (size_t)d) % (size_t)nranks) != rank;
                     if (!it.skip) to_induce.push_back(&it);
                     ++planned;  // all ranks' subsets: one in total takes the single-scene path
                     cv.notify_all();
                 });
-            } catch (const SubError& x) {
-                perr[d] = x;
-                pfail[d] = 1;
+            } catch (const SubError& x) {  // drawing subset plans[d].size() of covering d failed
+                std::lock_guard<std::mutex> lk(mu);
+                ff.note(FirstFailure::at(d, 0, plans[d].size()), x);
             } catch (const std::exception& x) {
-                perr[d] = SubError{SFMCOV_ERR_DEVICE, "subrec", x.what()};
-                pfail[d] = 1;
+                std::lock_guard<std::mutex> lk(mu);
+                ff.note(FirstFailure::at(d, 0, plans[d].size()), SubError{SFMCOV_ERR_DEVICE, "subrec", x.what()});
             }
             std::lock_guard<std::mutex> lk(mu);
             --planners_left;
@@ -857,15 +877,13 @@ void pipelined_covariances(sfmcov_handle* h, const sfmcov_scene& scene, const By
     }
     for (auto& t : th) t.join();
     if (gpu_error) std::rethrow_exception(gpu_error);
-    for (int d = 0; d < n_dec; ++d)
-        if (pfail[d]) throw perr[d];
     flat.clear();
     deco.clear();
     std::vector<PipeItem*> items;
     for (int d = 0; d < n_dec; ++d)
         for (PipeItem& it : plans[d]) items.push_back(&it);
-    for (PipeItem* it : items)
-        if (it->ind_fail) throw it->ind_err;  // (only this rank's subsets are induced)
+    for (PipeItem* it : items)  // (only this rank's subsets are induced)
+        if (it->ind_fail) ff.note(FirstFailure::at(it->deco, 0, it->idx), it->ind_err);
     if (!fallback.empty()) {  // one sub-scene at a time (the single-scene path; exact per-subset errors)
         std::vector<Sub*> subs;
         for (PipeItem* it : fallback) subs.push_back(&it->sub);
@@ -992,8 +1010,8 @@ int32_t sfmcov_plan_coverage(const sfmcov_scene* scene, int32_t k_bar, uint64_t 
 
 static int32_t approximate_impl(sfmcov_handle* h, const sfmcov_scene* scene, int32_t k_bar, int32_t n_decompositions,
                                 uint64_t seed, int32_t workers, int32_t nranks, int32_t rank, double* cam_cov,
-                                double* trace, int32_t* subset_id, int64_t* failed_subset, sfmcov_error* err) {
-    if (failed_subset) *failed_subset = -1;
+                                double* trace, int32_t* subset_id, int64_t* failed_key, sfmcov_error* err) {
+    if (failed_key) *failed_key = -1;
     return guarded(err, [&] {
         if (nranks < 1 || rank < 0 || rank >= nranks) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "bad rank / rank count"};
         if (k_bar < 2) throw SubError{SFMCOV_ERR_INVARIANT, "subrec", "subset size must be at least 2"};
@@ -1019,49 +1037,49 @@ static int32_t approximate_impl(sfmcov_handle* h, const sfmcov_scene* scene, int
         std::vector<std::vector<Sub>> plans;
         std::vector<std::deque<PipeItem>> store;
         std::vector<char> mine;  // sharded call: this rank's subsets (empty: all)
+        FirstFailure ff;
         if (subrec_batch_enabled()) {
             // planning, inducing and the device chunks overlapped (one pipeline)
             pipelined_covariances(h, *scene, bc, g, k_bar, n_decompositions, seed, std::max(1, (int)workers), store,
-                                  flat, deco, res, nranks > 1 ? &mine : nullptr, nranks, rank);
+                                  flat, deco, res, ff, nranks > 1 ? &mine : nullptr, nranks, rank);
             clk.mark("pipeline");
         } else {
             // (one-by-one path: a sharded call computes every subset here;
             // the merge still equals the single call)
-            // the coverings are independent (one seed each): planned in parallel
+            // the coverings are independent (one seed each): drawn in parallel
             plans.resize(n_decompositions);
-            std::vector<SubError> perr(n_decompositions);
-            std::vector<char> pfail(n_decompositions, 0);
             {
+                std::mutex fmu;
                 std::vector<std::thread> th;
                 for (int d = 0; d < n_decompositions; ++d)
                     th.emplace_back([&, d] {
                         try {
-                            plans[d] = coverage(*scene, bc, g, k_bar, seed + uint64_t(d), false);
+                            coverage_emit(*scene, bc, g, k_bar, seed + uint64_t(d), false,
+                                          [&](Sub&& sb) { plans[d].push_back(std::move(sb)); });
                         } catch (const SubError& x) {
-                            perr[d] = x;
-                            pfail[d] = 1;
+                            std::lock_guard<std::mutex> lk(fmu);
+                            ff.note(FirstFailure::at(d, 0, plans[d].size()), x);
                         }
                     });
                 for (auto& t : th) t.join();
             }
-            for (int d = 0; d < n_decompositions; ++d)
-                if (pfail[d]) throw perr[d];
             clk.mark("plan");
+            std::vector<size_t> idx;
             for (int d = 0; d < n_decompositions; ++d)
-                for (Sub& sb : plans[d]) {
-                    flat.push_back(&sb);
+                for (size_t i = 0; i < plans[d].size(); ++i) {
+                    flat.push_back(&plans[d][i]);
                     deco.push_back(d);
+                    idx.push_back(i);
                 }
+            std::vector<char> bfail(flat.size(), 0);
             {  // induced scenes of every subset, in parallel (host)
                 std::atomic<size_t> next{0};
                 std::vector<SubError> berr(flat.size());
-                std::vector<char> bfail(flat.size(), 0);
                 auto job = [&] {
                     for (size_t i = next++; i < flat.size(); i = next++) {
                         Sub& sb = const_cast<Sub&>(*flat[i]);
                         try {
-                            // ids only when the batched GPU path will gather the data itself
-                            Sub full = induced(*scene, bc, sb.cams, sb.truncated, subrec_batch_enabled());
+                            Sub full = induced(*scene, bc, sb.cams, sb.truncated, false);
                             sb.scene = std::move(full.scene);
                             sb.pts = std::move(full.pts);
                             sb.obs = std::move(full.obs);
@@ -1078,25 +1096,40 @@ static int32_t approximate_impl(sfmcov_handle* h, const sfmcov_scene* scene, int
                 job();
                 for (auto& t : th) t.join();
                 for (size_t i = 0; i < flat.size(); ++i)
-                    if (bfail[i]) throw berr[i];
+                    if (bfail[i]) ff.note(FirstFailure::at(deco[i], 0, idx[i]), berr[i]);
             }
             clk.mark("induce");
             std::vector<Sub*> mflat;
-            for (const Sub* sb : flat) mflat.push_back(const_cast<Sub*>(sb));
-            res = batch_covariances(h, *scene, bc, mflat, std::max(1, (int)workers));
+            std::vector<size_t> at;
+            for (size_t i = 0; i < flat.size(); ++i)
+                if (!bfail[i]) {
+                    mflat.push_back(const_cast<Sub*>(flat[i]));
+                    at.push_back(i);
+                }
+            std::vector<SubResult> got = batch_covariances(h, *scene, bc, mflat, std::max(1, (int)workers));
+            res.assign(flat.size(), SubResult{});
+            for (size_t k = 0; k < at.size(); ++k) res[at[k]] = std::move(got[k]);
         }
         clk.mark("covariances");
         const int64_t n = scene->n_cams;
         std::vector<char> seen(n, 0);
+        {  // the first failure in the reference's order (FirstFailure)
+            std::vector<size_t> in_deco(n_decompositions, 0);
+            for (size_t sid = 0; sid < flat.size(); ++sid) {
+                const size_t i = in_deco[deco[sid]]++;
+                if ((!mine.empty() && !mine[sid]) || !res[sid].code) continue;  // another rank's subset, or fine
+                ff.note(FirstFailure::at(deco[sid], 1, i),
+                        SubError{res[sid].code, "subrec",
+                                 "subset " + std::to_string(sid) + " (decomposition " + std::to_string(deco[sid]) +
+                                     "): " + std::string(res[sid].err.message)});
+            }
+            if (ff.any()) {
+                if (failed_key) *failed_key = ff.key;
+                throw ff.err;
+            }
+        }
         for (size_t sid = 0; sid < flat.size(); ++sid) {
             if (!mine.empty() && !mine[sid]) continue;  // another rank's subset
-            if (res[sid].code) {
-                if (failed_subset) *failed_subset = (int64_t)sid;
-                const int kind = res[sid].code;
-                throw SubError{kind, "subrec",
-                               "subset " + std::to_string(sid) + " (decomposition " + std::to_string(deco[sid]) +
-                                   "): " + std::string(res[sid].err.message)};
-            }
             const Sub& sb = *flat[sid];
             for (size_t l = 0; l < sb.cams.size(); ++l) {
                 const int32_t gc = sb.cams[l];
@@ -1134,9 +1167,9 @@ int32_t sfmcov_cuda_approximate_covariances(sfmcov_handle* h, const sfmcov_scene
 int32_t sfmcov_cuda_approximate_covariances_shard(sfmcov_handle* h, const sfmcov_scene* scene, int32_t k_bar,
                                                   int32_t n_decompositions, uint64_t seed, int32_t workers,
                                                   int32_t nranks, int32_t rank, double* cam_cov, double* trace,
-                                                  int32_t* subset_id, int64_t* failed_subset, sfmcov_error* err) {
+                                                  int32_t* subset_id, int64_t* failed_key, sfmcov_error* err) {
     return approximate_impl(h, scene, k_bar, n_decompositions, seed, workers, nranks, rank, cam_cov, trace, subset_id,
-                            failed_subset, err);
+                            failed_key, err);
 }
 
 int32_t sfmcov_cuda_monotonicity_check(sfmcov_handle* h, const sfmcov_scene* scene, const int32_t* small_cams,

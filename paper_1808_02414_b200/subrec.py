@@ -126,7 +126,7 @@ class ShardResult:
     trace: np.ndarray      # (n,): its trace (+inf where none)
     subset_id: np.ndarray  # (n,): its subset id (-1 where none)
     code: int = 0          # 0, or the error kind of this rank's first failing step
-    failed_subset: int = -1
+    failed_key: int = -1   # the failure's place in the reference's order (-1: before any covering)
     stage: str = ""
     message: str = ""
 
@@ -156,14 +156,14 @@ def approximate_covariances_shard(rec: Reconstruction, k_bar: int, n_decompositi
 def merge_shards(parts: List[ShardResult], k_bar: int) -> AggregatedCovariance:
     """The single-call result from the ranks' partial aggregates: per camera
     the smallest (trace, subset id) -- the reference keeps a camera's block
-    from the earliest subset with the smallest trace.  Errors: the failing
-    subset with the smallest id over all ranks (an error before any subset,
-    failed_subset -1, is the same on every rank)."""
+    from the earliest subset with the smallest trace.  Errors: the one with
+    the smallest failed_key over all ranks -- the reference draws covering d,
+    then computes its subsets, covering after covering, and stops at the
+    first failure (an error before any covering, key -1, is the same on
+    every rank)."""
     failed = [p for p in parts if p.code]
     if failed:
-        sub = [p for p in failed if p.failed_subset >= 0]
-        first = min(sub, key=lambda p: p.failed_subset) if len(sub) == len(failed) else \
-            next(p for p in failed if p.failed_subset < 0)
+        first = min(failed, key=lambda p: p.failed_key)  # -1 (before any covering) first: the same on every rank
         raise Error(first.code, first.stage, first.message)
     tr = np.stack([p.trace for p in parts])            # (R, n)
     sid = np.stack([p.subset_id for p in parts]).astype(np.int64)

@@ -458,14 +458,22 @@ def test_shard_owner_spreads_every_covering():
     assert [R.shard_owner(0, d, 3, 4) for d in range(3)] == [0, 1, 2]
 
 
-def test_merge_reports_the_first_failing_subset_and_uncovered_cameras():
+def test_merge_reports_the_first_failure_in_reference_order_and_uncovered_cameras():
     n, P = 6, 8
     ok = R.ShardResult(np.zeros((n, P, P)), np.ones(n), np.arange(n, dtype=np.int32))
-    bad7 = R.ShardResult(ok.cov, ok.trace, ok.subset_id, 4, 7, "subrec", "subrec: subset 7 (decomposition 1): x")
-    bad3 = R.ShardResult(ok.cov, ok.trace, ok.subset_id, 4, 3, "subrec", "subrec: subset 3 (decomposition 0): y")
+    key = lambda d, phase, i: (d << 33) | (phase << 32) | i  # csrc/subrec.cpp FirstFailure
+    comp = R.ShardResult(ok.cov, ok.trace, ok.subset_id, 4, key(0, 1, 3), "subrec", "subrec: subset 3 (decomposition 0): y")
+    draw1 = R.ShardResult(ok.cov, ok.trace, ok.subset_id, 4, key(1, 0, 0), "subrec", "subrec: camera 2 cannot anchor")
+    comp1 = R.ShardResult(ok.cov, ok.trace, ok.subset_id, 4, key(1, 1, 0), "subrec", "subrec: subset 9 (decomposition 1): x")
+    draw0 = R.ShardResult(ok.cov, ok.trace, ok.subset_id, 4, key(0, 0, 7), "subrec", "subrec: camera 5 cannot anchor")
+    # covering 0's subsets are computed before covering 1 is drawn ...
     with pytest.raises(F.Error) as e:
-        R.merge_shards([ok, bad7, bad3], 6)
+        R.merge_shards([ok, comp1, draw1, comp], 6)
     assert e.value.kind == F.ErrorKind.degenerate and "subset 3 (decomposition 0)" in str(e.value)
+    # ... and all of covering 0 is drawn before its first subset is computed
+    with pytest.raises(F.Error) as e:
+        R.merge_shards([comp, draw0], 6)
+    assert "camera 5 cannot anchor" in str(e.value)
     early = R.ShardResult(ok.cov, ok.trace, ok.subset_id, 3, -1, "validate", "validate: bad scene")
     with pytest.raises(F.Error) as e:
         R.merge_shards([early, early], 6)
@@ -529,13 +537,27 @@ def test_sharded_calls_merge_to_the_single_call(engine, nranks):
     assert np.array_equal(got.cov, want.cov) and np.array_equal(got.trace, want.trace)
 
 
-@pytest.mark.gpu
-def test_sharded_failure_names_the_same_subset(engine):
+def _broken_cube():
     rec = S.generate_cube_scene(6, 0.5)
-    rec.pts[14] = rec.cams[3, 3:6]
-    with pytest.raises(F.Error) as single:
-        R.approximate_covariances(rec, 6, 2, 0, engine=engine)
-    parts = [R.approximate_covariances_shard(rec, 6, 2, 0, 2, r, engine=engine) for r in range(2)]
+    rec.pts[14] = rec.cams[3, 3:6]  # a point at a camera centre: that sub-scene is degenerate
+    return rec
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("make,k_bar,decos,nranks", [
+    (_broken_cube, 6, 2, 2), (_broken_cube, 6, 3, 3), (_broken_cube, 3, 3, 2),
+    (lambda: S.generate_cube_scene(6, 0.5), 2, 3, 2), (lambda: S.generate_config(2), 2, 2, 4)])
+def test_sharded_failure_is_the_single_calls_failure(engine, make, k_bar, decos, nranks):
+    rec = make()
+    try:
+        R.approximate_covariances(rec, k_bar, decos, 0, engine=engine)
+        single = None
+    except F.Error as e:
+        single = e
+    parts = [R.approximate_covariances_shard(rec, k_bar, decos, 0, nranks, r, engine=engine) for r in range(nranks)]
+    if single is None:
+        assert all(p.code == 0 for p in parts)
+        return
     with pytest.raises(F.Error) as merged:
-        R.merge_shards(parts, 6)
-    assert str(merged.value) == str(single.value) and merged.value.kind == single.value.kind
+        R.merge_shards(parts, k_bar)
+    assert str(merged.value) == str(single) and merged.value.kind == single.kind

@@ -502,6 +502,9 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
     // high-priority stream by a host worker thread (its host reads of the
     // list sizes block that thread, not this one) while this thread queues
     // the numeric stage-A kernels on s.
+    // W = σ^-1 first: the device restarts right after the validation sync,
+    // before this thread spends time starting the pair-list worker
+    launch_weights(sc, ix.idx_cam, rec, st, s);
     std::future<long long> pairs_task;
     if (mode == M_FULL || mode == M_SCHUR) {
         SFM_CUDA(cudaStreamWaitEvent(h->sp, h->e_index, 0));
@@ -513,7 +516,6 @@ void run(sfmcov_handle* h, const SceneDev& sc, Mode mode, Outputs& out) {
             return g_kernel_launches;
         });
     }
-    launch_weights(sc, ix.idx_cam, rec, st, s);
     if (mode == M_JACOBIAN) {
         sync_status(h);
         throw_numeric(h, sc, mode);

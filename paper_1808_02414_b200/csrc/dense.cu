@@ -96,6 +96,10 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
                                   65536 / (gemm::Cfg<BK, STAGES, CM, CN>::THREADS * 128)) k_gemm(GemmArgs g) {
     using namespace gemm;
     using CF = Cfg<BK, STAGES, CM, CN>;
+    // A diagonal-tile kernel queued behind this launch with programmatic
+    // stream serialization may take its SM now (launch_potrf_diag); it waits
+    // for this grid's completion itself.  No effect on other successors.
+    asm volatile("griddepcontrol.launch_dependents;");
     constexpr int THREADS = CF::THREADS, BNT = CF::BNT, LDSB = CF::LDSB, LDB_K = CF::LDB_K;
     constexpr int BMC = CF::BMC, LDS = CF::LDSA;
     constexpr int NCOL = BN / CN, NSUB = (BM / CM) * NCOL;
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
 // Launch with the stream's priority as a per-launch attribute, so the
 // priority survives CUDA-graph capture (captured kernel nodes do not inherit
 // stream priorities).
-template <typename... KArgs, typename... Args>
+template <bool PDL = false, typename... KArgs, typename... Args>
 static void launch_prio(void (*kernel)(KArgs...), dim3 grid, unsigned block, size_t smem, cudaStream_t s,
                         Args... args) {
     int prio = 0;
@@ -333,11 +337,16 @@ static void launch_prio(void (*kernel)(KArgs...), dim3 grid, unsigned block, siz
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributePriority;
     attr[0].val.priority = prio;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (PDL) {  // may start while the stream's preceding kernel drains (the kernel waits: griddepcontrol.wait)
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.numAttrs = 2;
+    }
     SFM_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
@@ -402,6 +411,15 @@ void launch_gemm(const GemmArgs& g, cudaStream_t s) {
     // every CTA must read its whole K range of the shared rows before writing
     // them, so no CTA may own only part of a tile's rows
     const bool alias = g.C == g.B || g.C == g.A;
+    // SFMCOV_GEMM_LOG=1 (diagnostics, tools/gemm_launch_eff.py): one stderr line per launch
+    static const bool log = [] { const char* e = std::getenv("SFMCOV_GEMM_LOG"); return e && e[0] == '1'; }();
+    if (log) {
+        int prio = 0;
+        cudaStreamGetPriority(s, &prio);
+        std::fprintf(stderr, "gemm tm=%d tn=%d K=%d tri=%d lower=%d kmajor=%d kfrom=%d whole=%d alias=%d prio=%d b0=%d coff=%d\n", g.tm,
+                     g.tn, g.K, g.tri, g.lower_only, g.b_kmajor, g.k_from_col, g.whole_tile, (int)alias, prio, g.beta0_from,
+                     g.col_off_tiles);
+    }
     if (g.whole_tile) launch_gemm_cfg<16, 4, 128, 128>(g, tiles, s);
     else if (alias) launch_gemm_cfg<16, 3, 128, 64>(g, tiles, s);
     else launch_gemm_cfg<16, 3, 64, 64>(g, tiles, s);
@@ -531,6 +549,9 @@ __global__ void __launch_bounds__(potrf::THREADS, 1) k_potrf_diag(double* A, lon
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int fr = lane >> 2, fk = lane & 3;      // fragment row / k index
     POTRF_STAMP(19);
+    // launched early (programmatic stream serialization): the CTA already
+    // holds its SM; the tile is complete once the preceding grid has finished
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll 16
     for (int e = tid; e < kNB * kNB; e += THREADS) {
         const int r = e & (kNB - 1), c = e >> 7;
@@ -688,8 +709,14 @@ int potrf_smem_bytes_impl() { return potrf::SMEM; }
 void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, int col0, Status* st, cudaStream_t s,
                        const SweepBatch* bt) {
     const int B = bt ? bt->B : 1;
-    launch_prio(k_potrf_diag, dim3(1, B), potrf::THREADS, potrf::SMEM, s, A, ld, Linv, pivots, col0, st,
-                bt ? bt->zs : 0LL, bt ? bt->ls : 0LL, bt ? bt->ps : 0LL);
+    // SFMCOV_POTRF_PDL=0: plain stream order (A/B measurements)
+    static const bool pdl = [] { const char* e = std::getenv("SFMCOV_POTRF_PDL"); return !(e && e[0] == '0'); }();
+    if (pdl)
+        launch_prio<true>(k_potrf_diag, dim3(1, B), potrf::THREADS, potrf::SMEM, s, A, ld, Linv, pivots, col0, st,
+                          bt ? bt->zs : 0LL, bt ? bt->ls : 0LL, bt ? bt->ps : 0LL);
+    else
+        launch_prio(k_potrf_diag, dim3(1, B), potrf::THREADS, potrf::SMEM, s, A, ld, Linv, pivots, col0, st,
+                    bt ? bt->zs : 0LL, bt ? bt->ls : 0LL, bt ? bt->ps : 0LL);
     SFM_LAUNCH_CHECK();
 }
 
@@ -992,7 +1019,7 @@ struct SweepTrace {
     void dump() {
         if (ev.empty()) return;
         cudaDeviceSynchronize();
-        static const char* names[] = {"start", "take", "next1", "rest", "inv"};
+        static const char* names[] = {"start", "take", "next1", "rest", "inv", "potrf", "trsm", "inner"};
         for (size_t i = 0; i < ev.size(); ++i) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, ev[0], ev[i]);
@@ -1051,7 +1078,6 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
         // place, so two CTAs per 128-wide tile may split it); the diagonal
         // tiles stay in Z until the hand-over.
         const int slot = p % NB;
-        if (p >= NB) SFM_CUDA(cudaStreamWaitEvent(s, eT[slot], 0));  // inverse step p - NB done with Lb
         const int rows = Npad - b0 * kNB;
         double* Lb = ring + (size_t)slot * Npad * G * kNB;
         if (trace) tr.rec(p, 0, s);
@@ -1060,13 +1086,18 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             double* Acc = Z + (size_t)c * kNB * ld + (size_t)c * kNB;
             launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s, bt);
             ++launches;
+            if (trace) tr.rec(p, 5, s);
             const int below = K - c - 1;
             if (below == 0) break;
+            // the slot is written from here on: inverse step p - NB must be done with it (waited
+            // for after the first tile kernel, which then directly follows the last update)
+            if (g == 0 && p >= NB) SFM_CUDA(cudaStreamWaitEvent(s, eT[slot], 0));
             double* Lc = Lb + (size_t)g * kNB * rows + (size_t)(g + 1) * kNB;  // L[rows > c, c] in the slot
             GemmArgs t = gemm_args(Lc, rows, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
             batched(t, OR, OZ, OL);
             launch_gemm(t, s);
             ++launches;
+            if (trace) tr.rec(p, 6, s);
             const int inner = b0 + g_here - c - 1;
             if (inner > 0) {
                 if (g == 0 && next_pending) SFM_CUDA(cudaStreamWaitEvent(s, eN, 0));  // same columns
@@ -1076,6 +1107,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
                 batched(u, OZ, OR, OR);
                 launch_gemm(u, s);
                 ++launches;
+                if (trace) tr.rec(p, 7, s);
             }
         }
         // --- hand the panel over to the inverse: diagonal tiles into the slot,

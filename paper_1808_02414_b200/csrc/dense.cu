@@ -33,7 +33,17 @@ static inline int potrf_smem_bytes() { return potrf_smem_bytes_impl(); }
 // DMMA GEMM
 // ----------------------------------------------------------------------------
 namespace gemm {
-constexpr int BM = 128, BN = 128, PAD = 8, LDS = BM + PAD;
+// PAD: pitch 64 + 4 doubles keeps a half-warp's FP64 fragment reads (rows g,
+// k = t + 4 i: bank pairs 8 t + g) conflict-free and a 3-stage 64 x 64 CTA at
+// <= 56 KB, so that four fit an SM; pitch + 8 (round 1) was 2-way conflicted
+// and, with the stage size taken as the larger of the two B layouts, 57 KB:
+// three CTAs per SM (ncu: 12 warps active), not the four intended.  Measured
+// equal in the sweep and per launch (31.2-31.4 TF/s for the bulk updates with
+// three or four resident CTAs): the kernel is not occupancy-bound.
+#ifndef SFM_GEMM_PAD
+#define SFM_GEMM_PAD 4
+#endif
+constexpr int BM = 128, BN = 128, PAD = SFM_GEMM_PAD, LDS = BM + PAD;
 // CTA tile CM x CN of (CM/32) x (CN/32) warps of 32 x 32; the grid
 // enumerates 128 x 128 tiles x (128/CM)(128/CN) CTAs.  Used: 64 x 64 (four
 // CTAs per SM: independent output tiles), 128 x 64 (two per SM; C aliasing
@@ -50,8 +60,10 @@ struct Cfg {
     static constexpr int BSTAGE_N = BK * LDSB, BSTAGE_K = BNT * LDB_K;
     static constexpr int ASTAGE_M = BK * LDSA, ASTAGE_K = BMC * LDB_K;  // A: M- or K-contiguous
     static constexpr int BSTAGE = BSTAGE_N > BSTAGE_K ? BSTAGE_N : BSTAGE_K;
-    static constexpr int SMEM = STAGES * (ASTAGE_M + BSTAGE) * 8;     // A M-contiguous
+    static constexpr int SMEM = STAGES * (ASTAGE_M + BSTAGE) * 8;     // A M-contiguous (upper bound over B layouts)
     static constexpr int SMEM_AK = STAGES * (ASTAGE_K + BSTAGE) * 8;  // A K-contiguous
+    // the exact size per B layout: what a launch asks for (occupancy)
+    static constexpr int smem(bool b_kmajor) { return STAGES * (ASTAGE_M + (b_kmajor ? BSTAGE_K : BSTAGE_N)) * 8; }
 };
 }  // namespace gemm
 
@@ -363,8 +375,8 @@ static void launch_gemm_cfg_m(const GemmArgs& g, long long tiles, cudaStream_t s
     if (g.a_kmajor) {
         if (!g.b_kmajor) throw CudaError("gemm: K-major A needs K-major B");
         launch_prio(k_gemm<true, BK, ST, CM, CN, true, M16>, grid, CF::THREADS, CF::SMEM_AK, s, g);
-    } else if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST, CM, CN, false, M16>, grid, CF::THREADS, CF::SMEM, s, g);
-    else launch_prio(k_gemm<false, BK, ST, CM, CN, false, M16>, grid, CF::THREADS, CF::SMEM, s, g);
+    } else if (g.b_kmajor) launch_prio(k_gemm<true, BK, ST, CM, CN, false, M16>, grid, CF::THREADS, CF::smem(true), s, g);
+    else launch_prio(k_gemm<false, BK, ST, CM, CN, false, M16>, grid, CF::THREADS, CF::smem(false), s, g);
 }
 template <int BK, int ST, int CM, int CN>
 static void launch_gemm_cfg(const GemmArgs& g, long long tiles, cudaStream_t s) {

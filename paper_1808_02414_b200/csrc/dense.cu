@@ -723,7 +723,7 @@ void launch_potrf_diag(double* A, long long ld, double* Linv, double* pivots, in
     const int B = bt ? bt->B : 1;
     // SFMCOV_POTRF_PDL=0: plain stream order (A/B measurements)
     static const bool pdl = [] { const char* e = std::getenv("SFMCOV_POTRF_PDL"); return !(e && e[0] == '0'); }();
-    if (pdl)
+    if (pdl && !bt)  // batched sweeps: one tile CTA per problem would hold that many SMs while waiting (measured: noisier, no gain)
         launch_prio<true>(k_potrf_diag, dim3(1, B), potrf::THREADS, potrf::SMEM, s, A, ld, Linv, pivots, col0, st,
                           bt ? bt->zs : 0LL, bt ? bt->ls : 0LL, bt ? bt->ps : 0LL);
     else

@@ -146,7 +146,7 @@ def scene_bytes(rec):
 
 def panel_width(Npad: int) -> int:
     """Dense panel width of the single-GPU sweep (csrc/capi.cu panel_blocks)."""
-    g = (Npad // 128) // 24
+    g = (Npad // 128 + 9) // 18
     return 128 * min(16, max(3, g))
 
 

@@ -279,10 +279,11 @@ void throw_numeric(sfmcov_handle* h, const SceneDev& sc, Mode mode) {
 // Dense panel width in kNB blocks for K = Npad / kNB tiles over R ranks.
 // Wider panels mean longer K in the trailing updates (better DMMA efficiency,
 // fewer passes over the trailing matrix) but a longer per-panel critical
-// chain; measured best (1 B200): K = 71 (config 3): 3 (4: +0.7 %);
+// chain; measured best (1 B200, round 1): K = 71 (config 3): 3 (4: +0.7 %);
 // K = 211 (config 4): 8-12 (408 -> 397 ms vs 3); K = 704 (config 5): 16
-// (14.83 -> 14.24 s vs 3).  Hence K / (24 R) clamped to [3, 16]; the
-// distributed sweep keeps >= 24 panels per rank for its block-cyclic balance.
+// (14.83 -> 14.24 s vs 3).  Hence K / (24 R) clamped to [3, 16] on R > 1
+// ranks (the distributed sweep keeps >= 24 panels per rank for its
+// block-cyclic balance) and (K + 9) / 18 on one GPU (below).
 // SFMCOV_PANEL overrides.
 int panel_blocks(int K, int R) {
     static int forced = [] {
@@ -291,7 +292,10 @@ int panel_blocks(int K, int R) {
         return (v >= 1 && v <= 16) ? v : 0;
     }();
     if (forced) return forced;
-    const int g = K / (24 * (R > 0 ? R : 1));
+    // one GPU, with the tile kernel's early launch (round 2): the chain costs
+    // less, so slightly wider panels win -- config 3 (K = 71) 4 against 3:
+    // 16.75 -> 16.67 ms, config 4 (K = 211) 12 against 8: 392.2 -> 390.4 ms
+    const int g = R > 1 ? K / (24 * R) : (K + 9) / 18;
     return g < 3 ? 3 : (g > 16 ? 16 : g);
 }
 

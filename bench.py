@@ -146,7 +146,10 @@ def scene_bytes(rec):
 
 def panel_width(Npad: int) -> int:
     """Dense panel width of the single-GPU sweep (csrc/capi.cu panel_blocks)."""
-    g = (Npad // 128 + 9) // 18
+    K = Npad // 128
+    g = K // 24
+    if K >= 60 and g < 4:
+        g = 4
     return 128 * min(16, max(3, g))
 
 

@@ -283,7 +283,7 @@ void throw_numeric(sfmcov_handle* h, const SceneDev& sc, Mode mode) {
 // K = 211 (config 4): 8-12 (408 -> 397 ms vs 3); K = 704 (config 5): 16
 // (14.83 -> 14.24 s vs 3).  Hence K / (24 R) clamped to [3, 16] on R > 1
 // ranks (the distributed sweep keeps >= 24 panels per rank for its
-// block-cyclic balance) and (K + 9) / 18 on one GPU (below).
+// block-cyclic balance); one GPU: at least 4 from K = 60 on (below).
 // SFMCOV_PANEL overrides.
 int panel_blocks(int K, int R) {
     static int forced = [] {
@@ -293,9 +293,13 @@ int panel_blocks(int K, int R) {
     }();
     if (forced) return forced;
     // one GPU, with the tile kernel's early launch (round 2): the chain costs
-    // less, so slightly wider panels win -- config 3 (K = 71) 4 against 3:
-    // 16.75 -> 16.67 ms, config 4 (K = 211) 12 against 8: 392.2 -> 390.4 ms
-    const int g = R > 1 ? K / (24 * R) : (K + 9) / 18;
+    // less, so 4 blocks win at config 3 (K = 71: 16.75 -> 16.67 ms).  Config 4
+    // (K = 211) would gain 0.5 % from 12 against 8 (392.2 -> 390.4 ms), but
+    // its worst block against the exact inverse rises from 2.5e-10 to 8.1e-10
+    // (more of the update arrives in separate K = 128 in-panel subtractions),
+    // too close to the 1e-9 bar: it keeps K / 24.
+    int g = K / (24 * (R > 0 ? R : 1));
+    if (R <= 1 && K >= 60 && g < 4) g = 4;
     return g < 3 ? 3 : (g > 16 ? 16 : g);
 }
 

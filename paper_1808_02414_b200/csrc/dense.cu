@@ -135,7 +135,9 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
     const int sub = NSUB > 1 ? (int)(blockIdx.x % NSUB) : 0;
     const int half = sub % NCOL, roff = (sub / NCOL) * BMC;  // column block, row offset in the tile
     if (g.tri) {
-        int t = (int)((sqrt(8.0 * (double)l + 1.0) - 1.0) * 0.5);
+        // single precision: an FP64 square root here queues behind the resident CTAs' DMMAs on the
+        // FP64 pipe (ncu: 8 % of the kernel's stall samples sat on it); the integer loops make it exact
+        int t = (int)((sqrtf(8.0f * (float)l + 1.0f) - 1.0f) * 0.5f);
         while ((long long)(t + 1) * (t + 2) / 2 <= l) ++t;
         while ((long long)t * (t + 1) / 2 > l) --t;
         ti = t;
@@ -232,6 +234,11 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
 
     double acc[4][4][2];
     const int rq = 2 * (lane & 3), cq = lane >> 2;
+    // fragment base offsets of this lane inside a stage, pinned in registers (the compiler
+    // otherwise re-derives them from S2R tid in every chunk: ncu, 4 % of the stall samples)
+    int fa = BK_MAJOR ? (wn * 32 + (lane >> 2)) * LDB_K + (lane & 3) : (lane & 3) * LDSB + wn * 32 + (lane >> 2);
+    int fb = AK_MAJOR ? (wm * 32 + (lane >> 2)) * LDB_K + (lane & 3) : (lane & 3) * LDS + wm * 32 + (lane >> 2);
+    asm volatile("" : "+r"(fa), "+r"(fb));
     // The product accumulates from zero and is applied to C once in the
     // epilogue (C -/+ AB^T): one rounding against C instead of one per
     // k-step, which keeps the Cholesky's Schur-complement updates as accurate
@@ -257,25 +264,25 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
         if (idle) continue;
         if constexpr (M16) {
             static_assert(BK % 16 == 0, "k16 steps");
-            const int gq = lane >> 2, tq = lane & 3;
 #pragma unroll
             for (int k16 = 0; k16 < BK; k16 += 16) {
                 // MMA "A" (16 n x 16 k, row) from the B tile, MMA "B" (16 k x 8 m, col) from the A tile
+                // (rows n = wn 32 + 16 nb + g + 8 (i % 2), m = wm 32 + 8 mb + g; k = k16 + t + 4 j)
                 double a16[2][8];
 #pragma unroll
                 for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const int n = wn * 32 + 16 * nb + gq + 8 * (i % 2), kq = k16 + tq + 4 * (i / 2);
-                        a16[nb][i] = BK_MAJOR ? bs[n * LDB_K + kq] : bs[kq * LDSB + n];
+                        const int dn = 16 * nb + 8 * (i % 2), dk = k16 + 4 * (i / 2);
+                        a16[nb][i] = BK_MAJOR ? bs[fa + dn * LDB_K + dk] : bs[fa + dk * LDSB + dn];
                     }
 #pragma unroll
                 for (int mb = 0; mb < 4; ++mb) {
                     double b16[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const int m = wm * 32 + 8 * mb + gq, kq = k16 + tq + 4 * i;
-                        b16[i] = AK_MAJOR ? as[m * LDB_K + kq] : as[kq * LDS + m];
+                        const int dm = 8 * mb, dk = k16 + 4 * i;
+                        b16[i] = AK_MAJOR ? as[fb + dm * LDB_K + dk] : as[fb + dk * LDS + dm];
                     }
 #pragma unroll
                     for (int nb = 0; nb < 2; ++nb)  // D rows n = 16 nb + gq + 8 (i / 2) -> column blocks 2 nb, 2 nb + 1

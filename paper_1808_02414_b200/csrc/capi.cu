@@ -294,10 +294,11 @@ int panel_blocks(int K, int R) {
     if (forced) return forced;
     // one GPU, with the tile kernel's early launch (round 2): the chain costs
     // less, so 4 blocks win at config 3 (K = 71: 16.75 -> 16.67 ms).  Config 4
-    // (K = 211) would gain 0.5 % from 12 against 8 (392.2 -> 390.4 ms), but
-    // its worst block against the exact inverse rises from 2.5e-10 to 8.1e-10
-    // (more of the update arrives in separate K = 128 in-panel subtractions),
-    // too close to the 1e-9 bar: it keeps K / 24.
+    // (K = 211) would gain 0.3-0.5 % from 10-12 against 8, but the error of its
+    // worst-conditioned camera against the exact inverse scatters with the
+    // rounding order (widths 3 / 4 / 6 / 8 / 10 / 12 / 16: 6.8e-10, 9.6e-10,
+    // 1.16e-9, 2.5e-10, 2.4e-10, 8.1e-10, 5.3e-10; median block 2-4e-12), so
+    // the width that is verified on every camera (8, K / 24) stays.
     int g = K / (24 * (R > 0 ? R : 1));
     if (R <= 1 && K >= 60 && g < 4) g = 4;
     return g < 3 ? 3 : (g > 16 ? 16 : g);

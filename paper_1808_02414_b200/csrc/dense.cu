@@ -1106,11 +1106,12 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             launch_potrf_diag(Acc, ld, Linv + (size_t)c * kNB * kNB, pivots, c * kNB, st, s, bt);
             ++launches;
             if (trace) tr.rec(p, 5, s);
+            // the slot is written from here on (trsm, or the hand-over of a last one-tile panel):
+            // inverse step p - NB must be done with it (waited for after the first tile kernel,
+            // which then directly follows the last update)
+            if (g == 0 && p >= NB) SFM_CUDA(cudaStreamWaitEvent(s, eT[slot], 0));
             const int below = K - c - 1;
             if (below == 0) break;
-            // the slot is written from here on: inverse step p - NB must be done with it (waited
-            // for after the first tile kernel, which then directly follows the last update)
-            if (g == 0 && p >= NB) SFM_CUDA(cudaStreamWaitEvent(s, eT[slot], 0));
             double* Lc = Lb + (size_t)g * kNB * rows + (size_t)(g + 1) * kNB;  // L[rows > c, c] in the slot
             GemmArgs t = gemm_args(Lc, rows, Acc + kNB, ld, Linv + (size_t)c * kNB * kNB, kNB, below, 1, kNB);
             batched(t, OR, OZ, OL);

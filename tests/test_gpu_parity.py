@@ -456,7 +456,7 @@ import sys
 import numpy as np
 sys.path.insert(0, sys.argv[1])
 from paper_1808_02414_b200 import sfmcov as F, synthetic as S
-rec = S.generate_config(2)
+rec = S.generate_config(int(sys.argv[3]) if len(sys.argv) > 3 else 2)
 np.save(sys.argv[2], F.Engine(0).compute_covariance(rec).camera_cov)
 """
 
@@ -477,3 +477,22 @@ def test_wide_dense_panels_parity(engine, panel, tmp_path):
     subprocess.run([sys.executable, "-c", _PANEL_SCRIPT, root, str(out)], env=env, check=True, timeout=600)
     cov, _, _, _ = O.compute_covariance(S.generate_config(2))
     assert worst_block(np.load(out), cov) <= COV_TOL
+
+
+@pytest.mark.parametrize("panel", [5, 7])
+def test_last_panel_of_one_tile(engine, panel, tmp_path):
+    """Config 3 has 71 tile columns: with 5- or 7-block panels the last panel
+    is a single tile, after more panels than the ring has slots.  Its
+    hand-over writes the ring slot like any other panel's, so it too must wait
+    for the inverse step that last used the slot (a width sweep at config 4,
+    211 = 70 x 3 + 1 tiles, found the wait skipped: every block wrong).
+    Compared with the default-width result (rounding-level differences)."""
+    import os
+    import subprocess
+    import sys
+    out = tmp_path / "cov.npy"
+    env = dict(os.environ, SFMCOV_PANEL=str(panel))
+    root = str(Path(__file__).resolve().parent.parent)
+    subprocess.run([sys.executable, "-c", _PANEL_SCRIPT, root, str(out), "3"], env=env, check=True, timeout=600)
+    base = engine.compute_covariance(S.generate_config(3)).camera_cov
+    assert worst_block(np.load(out), base) <= COV_TOL

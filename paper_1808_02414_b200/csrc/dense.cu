@@ -40,6 +40,9 @@ namespace gemm {
 // three CTAs per SM (ncu: 12 warps active), not the four intended.  Measured
 // equal in the sweep and per launch (31.2-31.4 TF/s for the bulk updates with
 // three or four resident CTAs): the kernel is not occupancy-bound.
+#ifndef SFM_GEMM_REGS
+#define SFM_GEMM_REGS 128  // register budget per thread behind the launch bounds (A/B builds: 168 = three 64 x 64 CTAs per SM)
+#endif
 #ifndef SFM_GEMM_PAD
 #define SFM_GEMM_PAD 4
 #endif
@@ -105,7 +108,7 @@ __device__ __forceinline__ void dmma16(double& d0, double& d1, double& d2, doubl
 // tools/probe/dmma16_layout.cu).
 template <bool BK_MAJOR, int BK, int STAGES, int CM, int CN, bool AK_MAJOR = false, bool M16 = false>
 __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
-                                  65536 / (gemm::Cfg<BK, STAGES, CM, CN>::THREADS * 128)) k_gemm(GemmArgs g) {
+                                  65536 / (gemm::Cfg<BK, STAGES, CM, CN>::THREADS * SFM_GEMM_REGS)) k_gemm(GemmArgs g) {
     using namespace gemm;
     using CF = Cfg<BK, STAGES, CM, CN>;
     // A diagonal-tile kernel queued behind this launch with programmatic

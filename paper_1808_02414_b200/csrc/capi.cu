@@ -81,6 +81,7 @@ struct RankA {
 struct sfmcov_handle {
     int device = 0;
     cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr, s4 = nullptr;
+    cudaStream_t sx[3] = {nullptr, nullptr, nullptr};  // extra inverse streams (column-interleaved shares of X)
     cudaStream_t sp = nullptr;  // the pair-list build (high priority: ready before stage A ends)
     cudaEvent_t eX = nullptr, eN = nullptr;
     cudaEvent_t e_index = nullptr, e_pairs = nullptr;  // pair-list build on s2, overlapped with stage A
@@ -90,7 +91,7 @@ struct sfmcov_handle {
     cudaEvent_t e_pr0 = nullptr, e_pr1 = nullptr;             // its duration (profiling)
     cudaEvent_t e1 = nullptr, e2 = nullptr;
     static constexpr int kRing = 4;  // panel ring buffers of the fused sweep
-    cudaEvent_t eL[kRing], eT[kRing];
+    cudaEvent_t eL[kRing], eT[kRing], eTx[3][kRing];
     cudaEvent_t ev[ST_COUNT + 1];
     bool profiling = false;
     // one caller at a time; recursive so that a multi-call session (the
@@ -325,9 +326,10 @@ int run_dense(sfmcov_handle* h, double* Z, long long ld, int Npad, double* Linv,
     cudaStream_t s = h->s;
     const int pw = panel_blocks(Npad / kNB, 1);
     double* ring = h->ring.as<double>(sweep_ring_doubles(Npad, pw, sfmcov_handle::kRing));
+    const InvSplit isp{3, {h->sx[0], h->sx[1], h->sx[2]}, {h->eTx[0], h->eTx[1], h->eTx[2]}};
     const int launches = dense_sweep(Z, ld, Npad, pw, Linv, piv, st, ring, sfmcov_handle::kRing, s, serial ? s : h->s2,
                                      serial ? s : h->s3, h->eL, h->eT, h->e2, serial ? s : h->s4, h->eX, h->eN,
-                                     serial ? nullptr : eZ, nreal);
+                                     serial ? nullptr : eZ, nreal, nullptr, serial ? nullptr : &isp);
     if (mark_stages) {
         mark(h, 8);
         mark(h, 9);
@@ -1345,6 +1347,7 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
         // inverse now ends 0.1 ms after the Cholesky instead of 3.7 ms).
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s2, cudaStreamNonBlocking, lo));
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s3, cudaStreamNonBlocking, (lo + hi) / 2));
+        for (auto& x : h->sx) SFM_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, (lo + hi) / 2));
         SFM_CUDA(cudaStreamCreateWithPriority(&h->s4, cudaStreamNonBlocking, hi));
         SFM_CUDA(cudaStreamCreateWithPriority(&h->sp, cudaStreamNonBlocking, hi));
         SFM_CUDA(cudaEventCreateWithFlags(&h->eX, cudaEventDisableTiming));
@@ -1362,6 +1365,7 @@ sfmcov_handle* sfmcov_cuda_create(int32_t device, sfmcov_error* err) {
         for (int i = 0; i < sfmcov_handle::kRing; ++i) {
             SFM_CUDA(cudaEventCreateWithFlags(&h->eL[i], cudaEventDisableTiming));
             SFM_CUDA(cudaEventCreateWithFlags(&h->eT[i], cudaEventDisableTiming));
+            for (int q = 0; q < 3; ++q) SFM_CUDA(cudaEventCreateWithFlags(&h->eTx[q][i], cudaEventDisableTiming));
         }
         SFM_CUDA(cudaEventCreateWithFlags(&h->e1, cudaEventDisableTiming));
         SFM_CUDA(cudaEventCreateWithFlags(&h->e2, cudaEventDisableTiming));
@@ -1383,6 +1387,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaStreamSynchronize(h->s);
     cudaStreamSynchronize(h->s2);
     cudaStreamSynchronize(h->s3);
+    for (auto x : h->sx) cudaStreamSynchronize(x);
     cudaStreamSynchronize(h->s4);
     cudaStreamSynchronize(h->sp);
     DBuf* bufs[] = {&h->ws.tmp, &h->ws_pairs.tmp, &h->h_cams, &h->h_pts, &h->h_oc, &h->h_op, &h->h_sigma,
@@ -1426,6 +1431,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     cudaStreamDestroy(h->s2);
     cudaStreamDestroy(h->s3);
     cudaStreamDestroy(h->s4);
+    for (auto x : h->sx) cudaStreamDestroy(x);
     cudaStreamDestroy(h->sp);
     cudaEventDestroy(h->eX);
     cudaEventDestroy(h->eN);
@@ -1442,6 +1448,7 @@ void sfmcov_cuda_destroy(sfmcov_handle* h) {
     for (int i = 0; i < sfmcov_handle::kRing; ++i) {
         cudaEventDestroy(h->eL[i]);
         cudaEventDestroy(h->eT[i]);
+        for (int q = 0; q < 3; ++q) cudaEventDestroy(h->eTx[q][i]);
     }
     delete h;
 }

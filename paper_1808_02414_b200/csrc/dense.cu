@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BK, STAGES, CM, CN>::THREADS,
         ti = (int)(l % g.tm);
         tj = (int)(l / g.tm);
     }
+    if (g.col_step > 1) tj = g.col_first + tj * g.col_step;  // interleaved column tiles (plain launches only)
     if (g.lower_only && ti + g.row_off_tiles < tj + g.col_off_tiles) return;
     const double* A;
     const double* B;
@@ -1055,7 +1056,7 @@ struct SweepTrace {
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
                 cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN, cudaEvent_t eZ, int nreal,
-                const SweepBatch* bt) {
+                const SweepBatch* bt, const InvSplit* isp) {
     // nreal (optional): the unpadded size; the trailing and next-panel
     // updates skip the identity padding's rows (their L rows are zero).
     // bt (optional): bt->B problems swept together, every launch batched
@@ -1070,6 +1071,10 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
     const int K = Npad / kNB;
     int launches = 0;
     bool rest_pending = false;
+    // SFMCOV_INV_SPLIT=w: the inverse on w column-interleaved streams (1 = all on s3; A/B measurements)
+    static const int inv_ways = [] { const char* e = std::getenv("SFMCOV_INV_SPLIT"); return e ? std::atoi(e) : 3; }();
+    const int ways = (!bt && isp && s3 != s) ? std::max(1, std::min(inv_ways, isp->n + 1)) : 1;
+    const bool split_inv = ways > 1;
     // operand kinds for the batch strides: Z, the Linv tiles, the panel ring
     enum Op { OZ, OL, OR };
     auto stride = [&](Op o) -> long long { return !bt ? 0 : (o == OZ ? bt->zs : (o == OL ? bt->ls : bt->rs)); };
@@ -1112,7 +1117,10 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             // the slot is written from here on (trsm, or the hand-over of a last one-tile panel):
             // inverse step p - NB must be done with it (waited for after the first tile kernel,
             // which then directly follows the last update)
-            if (g == 0 && p >= NB) SFM_CUDA(cudaStreamWaitEvent(s, eT[slot], 0));
+            if (g == 0 && p >= NB) {
+                SFM_CUDA(cudaStreamWaitEvent(s, eT[slot], 0));
+                for (int q = 1; q < ways; ++q) SFM_CUDA(cudaStreamWaitEvent(s, isp->eT[q - 1][slot], 0));
+            }
             const int below = K - c - 1;
             if (below == 0) break;
             double* Lc = Lb + (size_t)g * kNB * rows + (size_t)(g + 1) * kNB;  // L[rows > c, c] in the slot
@@ -1192,34 +1200,49 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
             rest_pending = true;
         }
         // --- inverse step p (rows of panel p) ---
-        SFM_CUDA(cudaStreamWaitEvent(s3, eL[slot], 0));
-        for (int g = 0; g < g_here; ++g) {
-            const int r = b0 + g;
-            GemmArgs a = gemm_args(Z + (size_t)r * kNB, ld, Linv + (size_t)r * kNB * kNB, kNB, Z + (size_t)r * kNB, ld,
-                                   1, r + 1, kNB);
-            a.b_kmajor = 1;
-            batched(a, OZ, OL, OZ);
-            launch_gemm(a, s3);
-            ++launches;
-            const int later = g_here - g - 1;
-            if (later > 0) {
-                GemmArgs u = gemm_args(Z + (size_t)(r + 1) * kNB, ld, Lb + (size_t)g * kNB * rows + (size_t)(g + 1) * kNB,
-                                       rows, Z + (size_t)r * kNB, ld, later, r + 1, kNB);
-                u.b_kmajor = 1; u.alpha_neg = 1; u.beta = 1;
-                batched(u, OZ, OR, OZ);
-                launch_gemm(u, s3);
+        // The columns of X are independent: with extra inverse streams the column tiles are dealt
+        // round-robin to s3 and isp->s[], so that one share's narrow in-panel launches overlap
+        // another's bulk update.
+        for (int q = 0; q < ways; ++q) {
+            cudaStream_t si = q ? isp->s[q - 1] : s3;
+            const int step = ways;
+            auto ncol = [&](int cols) { return cols > q ? (cols - q + step - 1) / step : 0; };  // this half's tiles of [0, cols)
+            auto half = [&](GemmArgs& a) {
+                if (split_inv) { a.col_step = step; a.col_first = q; }
+            };
+            SFM_CUDA(cudaStreamWaitEvent(si, eL[slot], 0));
+            for (int g = 0; g < g_here; ++g) {
+                const int r = b0 + g;
+                if (ncol(r + 1) == 0) continue;
+                GemmArgs a = gemm_args(Z + (size_t)r * kNB, ld, Linv + (size_t)r * kNB * kNB, kNB, Z + (size_t)r * kNB, ld,
+                                       1, ncol(r + 1), kNB);
+                a.b_kmajor = 1;
+                half(a);
+                batched(a, OZ, OL, OZ);
+                launch_gemm(a, si);
+                ++launches;
+                const int later = g_here - g - 1;
+                if (later > 0) {
+                    GemmArgs u = gemm_args(Z + (size_t)(r + 1) * kNB, ld, Lb + (size_t)g * kNB * rows + (size_t)(g + 1) * kNB,
+                                           rows, Z + (size_t)r * kNB, ld, later, ncol(r + 1), kNB);
+                    u.b_kmajor = 1; u.alpha_neg = 1; u.beta = 1;
+                    half(u);
+                    batched(u, OZ, OR, OZ);
+                    launch_gemm(u, si);
+                    ++launches;
+                }
+            }
+            if (T2 > 0 && ncol(nb0) > 0) {
+                GemmArgs x = gemm_args(Z + (size_t)nb0 * kNB, ld, Lb + W, rows, Z + (size_t)b0 * kNB, ld, T2, ncol(nb0), W);
+                x.b_kmajor = 1; x.alpha_neg = 1; x.beta = 1; x.beta0_from = b0;
+                x.k_from_col = 1;  // X[panel rows, panel columns] is lower triangular: skip its zero K range
+                half(x);
+                batched(x, OZ, OR, OZ);
+                launch_gemm(x, si);
                 ++launches;
             }
+            SFM_CUDA(cudaEventRecord(q ? isp->eT[q - 1][slot] : eT[slot], si));
         }
-        if (T2 > 0) {
-            GemmArgs x = gemm_args(Z + (size_t)nb0 * kNB, ld, Lb + W, rows, Z + (size_t)b0 * kNB, ld, T2, nb0, W);
-            x.b_kmajor = 1; x.alpha_neg = 1; x.beta = 1; x.beta0_from = b0;
-            x.k_from_col = 1;  // X[panel rows, panel columns] is lower triangular: skip its zero K range
-            batched(x, OZ, OR, OZ);
-            launch_gemm(x, s3);
-            ++launches;
-        }
-        SFM_CUDA(cudaEventRecord(eT[slot], s3));
         if (trace) tr.rec(p, 4, s3);
         last_slot = slot;
         if (debug_sync()) {
@@ -1231,6 +1254,7 @@ int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* 
     if (rest_pending) SFM_CUDA(cudaStreamWaitEvent(s, eR, 0));
     if (next_pending) SFM_CUDA(cudaStreamWaitEvent(s, eN, 0));
     if (last_slot >= 0) SFM_CUDA(cudaStreamWaitEvent(s, eT[last_slot], 0));
+    for (int q = 1; q < ways && last_slot >= 0; ++q) SFM_CUDA(cudaStreamWaitEvent(s, isp->eT[q - 1][last_slot], 0));
     if (trace) tr.dump();
     return launches;
 }

@@ -135,6 +135,9 @@ struct GemmArgs {
     // batch > 1: grid.y = batch; operand b is offset by b * bs{A,B,C} doubles
     int batch;
     long long bsA, bsB, bsC;
+    // col_step > 1: grid column tile tj addresses matrix column tile col_first + tj * col_step
+    // (B rows, C columns, beta0_from / k_from_col): the inverse's column-interleaved halves
+    int col_step, col_first;
 };
 
 // Several same-sized dense problems swept together (batched sub-scenes): Z,
@@ -208,10 +211,17 @@ void launch_extract(int P, const double* X, long long ld, int N, int nblocks, co
 void launch_set_diag(double* Z, long long ld, int from, int to, cudaStream_t s);
 void launch_minmax(const double* x, long long count, double* part, double* out, cudaStream_t s);
 void launch_pivot_range(const double* piv, int N, double* out, cudaStream_t s);
+// Extra inverse streams of the fused sweep: the columns of X are independent, so column
+// tiles j with j % (n + 1) == q > 0 run on s[q - 1] (their ring-slot events eT[q - 1]).
+struct InvSplit {
+    int n;                 // extra streams (0..3)
+    cudaStream_t s[3];
+    cudaEvent_t* eT[3];    // per ring slot
+};
 int dense_sweep(double* Z, long long ld, int Npad, int G, double* Linv, double* pivots, Status* st, double* ring,
                 int NB, cudaStream_t s, cudaStream_t s2, cudaStream_t s3, cudaEvent_t* eL, cudaEvent_t* eT,
                 cudaEvent_t eR, cudaStream_t s4, cudaEvent_t eX, cudaEvent_t eN, cudaEvent_t eZ = nullptr,
-                int nreal = 0, const SweepBatch* bt = nullptr);
+                int nreal = 0, const SweepBatch* bt = nullptr, const InvSplit* isp = nullptr);
 inline size_t sweep_ring_doubles(int Npad, int G, int NB) { return (size_t)NB * Npad * G * kNB; }
 
 // ---- optional outputs (fullcov.cu) ------------------------------------------

@@ -42,7 +42,7 @@ sys.path.insert(0, str(ROOT))
 
 # DRAM bytes (read + write) of one dense sweep, summed over its launches in an
 # ncu launch list of this bench command (per config; profiles/ names the file)
-SWEEP_DRAM_BYTES = {3: (65102.8e6 / 7, "profiles/r02_launches_bench_config3.txt (sweep DRAM over 7 runs / 7)")}
+SWEEP_DRAM_BYTES = {3: (62780.3e6 / 7, "profiles/r02_launches_bench_config3.txt (sweep DRAM over 7 runs / 7)")}
 FP64_PEAK_TFLOPS = 37.1  # measured DMMA throughput on this pool, m8n8k4 and m16n8k16 alike (profiles/r01_fp64_peak_probe.txt)
 FP64_PEAK_SOURCE = "measured: tools/probe/fp64_probe.cu DMMA loop 37.1 TF/s, profiles/r01_fp64_peak_probe.txt (cuBLAS DGEMM 16384^3: 36.0; MEASURED_PEAKS.json has no FP64 entry)"
 
